@@ -1,0 +1,18 @@
+"""B200-native hot path of Cortex (arXiv 2011.01383): device linearization and
+persistent level-by-level evaluation of recursive cells, behind the C ABI of
+include/cx.h. See DESIGN.md.
+
+    import paper_2011_01383_b200 as cx
+    lin = cx.linearize(children_cuda_int32, cx.TREE)
+    h, aux, roots = cx.forward(cx.TREELSTM, 256, weights, emb, words, lin, num_roots=10)
+"""
+from .cx import (BF16, DAG, DAGRNN, F32, MVRNN, SEQUENCE, TREE, TREEFC, TREEGRU, TREELSTM,
+                 TREERNN, CELL_IDS, CxError, Linearization, check, forward, launch_info, lib,
+                 linearize, status, status_str)
+from . import cx as _cx
+
+OK = _cx.OK
+
+__all__ = ["linearize", "forward", "check", "status", "status_str", "launch_info", "lib",
+           "Linearization", "CxError", "SEQUENCE", "TREE", "DAG", "TREERNN", "TREEFC",
+           "TREELSTM", "TREEGRU", "MVRNN", "DAGRNN", "F32", "BF16", "CELL_IDS", "OK"]

@@ -1,0 +1,210 @@
+// api.cu -- the C ABI of include/cx.h: argument checks, workspace carving,
+// launch configuration. No C++ exception crosses the boundary; argument
+// errors return before any CUDA call.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/cx.h"
+#include "common.cuh"
+#include "fwd_kernels.cuh"
+#include "lin_kernels.cuh"
+
+namespace {
+
+std::mutex g_mu;  // guards the device-attribute cache and kernel attribute setup
+
+int num_sms_current() {
+  static int cached_dev = -1, cached_sms = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (dev != cached_dev) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    cached_dev = dev;
+    cached_sms = sms;
+  }
+  return cached_sms;
+}
+
+inline char *align_up(char *p, size_t a) {
+  uintptr_t v = reinterpret_cast<uintptr_t>(p);
+  return reinterpret_cast<char *>((v + a - 1) / a * a);
+}
+
+bool weights_ok(int cell, const cx_weights *w) {
+  static const int need[6] = {0, 2, 5, 7, 4, 3};
+  for (int i = 0; i < need[cell]; i++)
+    if (!w->p[i]) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t cx_linearize_workspace_bytes(int32_t n, int32_t max_children) {
+  (void)max_children;
+  return cx::lin_workspace_bytes(n < 0 ? 0 : n);
+}
+
+cx_status cx_linearize(const int32_t *children, int32_t n, int32_t max_children, cx_kind kind,
+                       void *workspace, size_t workspace_bytes, cx_linearization *out,
+                       void *stream) {
+  if (!out || n < 0 || max_children < 1 || (n > 0 && !children)) return CX_E_ARG;
+  if (kind != CX_SEQUENCE && kind != CX_TREE && kind != CX_DAG) return CX_E_ARG;
+  if (kind == CX_SEQUENCE && max_children != 1) return CX_E_ARG;
+  if (!out->header || (n > 0 && (!out->perm || !out->inv || !out->children || !out->height ||
+                                 !out->level_begin || !out->level_size || !out->roots)))
+    return CX_E_ARG;
+  if (!workspace || workspace_bytes < cx::lin_workspace_bytes(n)) return CX_E_WORKSPACE;
+  out->n = n;
+  out->max_children = max_children;
+  out->kind = kind;
+
+  char *p = align_up(static_cast<char *>(workspace), 128);
+  cx::LinArgs a;
+  a.bar = reinterpret_cast<cx::GridBar *>(p);
+  p += sizeof(cx::GridBar);
+  a.misc = reinterpret_cast<int32_t *>(p);
+  p += 32 * sizeof(int32_t);
+  a.indeg = reinterpret_cast<int32_t *>(p);
+  p += sizeof(int32_t) * (size_t)n;
+  a.hgt = reinterpret_cast<int32_t *>(p);
+  p += sizeof(int32_t) * (size_t)n;
+  a.cnt = reinterpret_cast<int32_t *>(p);
+  a.budget = (int)cx::lin_budget_entries(n);
+  a.ch = children;
+  a.n = n;
+  a.maxc = max_children;
+  a.kind = kind;
+  a.hdr = out->header;
+  a.perm = out->perm;
+  a.inv = out->inv;
+  a.chn = out->children;
+  a.hnew = out->height;
+  a.lbeg = out->level_begin;
+  a.lsize = out->level_size;
+  a.roots = out->roots;
+  int sms;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    sms = num_sms_current();
+  }
+  if (sms <= 0) return CX_E_CUDA;
+  cudaError_t e = cx::launch_linearize(a, sms, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? CX_OK : CX_E_CUDA;
+}
+
+size_t cx_forward_workspace_bytes(const cx_model *m, int32_t n) {
+  if (!m) return 0;
+  return cx::fwd_workspace_bytes(m->cell, m->hidden, n) + 256;
+}
+
+cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
+                     const int32_t *word_ids, const cx_linearization *lin, float *h_out,
+                     float *aux_out, float *root_out, void *workspace, size_t workspace_bytes,
+                     void *stream) {
+  if (!m || !w || !lin || !lin->header) return CX_E_ARG;
+  if (m->cell < CX_TREERNN || m->cell > CX_DAGRNN) return CX_E_ARG;
+  if (m->dtype != CX_F32 && m->dtype != CX_BF16) return CX_E_ARG;
+  if (m->hidden <= 0 || m->vocab <= 0) return CX_E_ARG;
+  const int n = lin->n;
+  if (n < 0) return CX_E_ARG;
+  if (n > 0 && (!emb || !word_ids || !h_out || !weights_ok(m->cell, w))) return CX_E_ARG;
+  if (m->dtype == CX_BF16) return CX_E_UNSUPPORTED;  // bf16 tensor-core path: DESIGN.md "next"
+  if (!workspace || workspace_bytes < cx_forward_workspace_bytes(m, n)) return CX_E_WORKSPACE;
+  if (n == 0) return CX_OK;
+
+  cx::FwdPlan plan;
+  int Gn = 0, Gu = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int sms = num_sms_current();
+    if (sms <= 0) return CX_E_CUDA;
+    if (!cx::fwd_plan(m->cell, m->hidden, lin->max_children, sms, &plan, &Gn, &Gu))
+      return CX_E_UNSUPPORTED;
+  }
+  const size_t N = (size_t)n, H = (size_t)m->hidden;
+  char *p = align_up(static_cast<char *>(workspace), 128);
+  cx::FwdArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.bar = reinterpret_cast<cx::GridBar *>(p);
+  p += sizeof(cx::GridBar);
+  float *buf = reinterpret_cast<float *>(p);
+  a.hdr = lin->header;
+  a.perm = lin->perm;
+  a.chn = lin->children;
+  a.lbeg = lin->level_begin;
+  a.lsize = lin->level_size;
+  a.hnew = lin->height;
+  a.roots = lin->roots;
+  a.n = n;
+  a.maxc = lin->max_children;
+  a.H = m->hidden;
+  a.V = m->vocab;
+  a.emb = emb;
+  a.words = word_ids;
+  for (int i = 0; i < 8; i++) a.w[i] = w->p[i];
+  a.h_out = h_out;
+  a.aux_out = aux_out;
+  a.root_out = root_out;
+  switch (m->cell) {
+    case CX_TREELSTM: a.cbuf = aux_out ? aux_out : buf; break;
+    case CX_TREEGRU: a.zbuf = buf; a.sbuf = buf + N * H; break;
+    case CX_DAGRNN: a.pbuf = buf; break;
+    case CX_MVRNN: a.Abuf = aux_out ? aux_out : buf; break;
+    default: break;
+  }
+  a.Gn = Gn;
+  a.Gu = Gu;
+  cudaError_t e = cx::fwd_launch(plan, a, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? CX_OK : CX_E_CUDA;
+}
+
+cx_status cx_status_sync(const cx_linearization *lin, int32_t *bad_node, void *stream) {
+  if (!lin || !lin->header) return CX_E_ARG;
+  int32_t hv[2] = {0, -1};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(hv, lin->header, sizeof hv, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return CX_E_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return CX_E_CUDA;
+  if (bad_node) *bad_node = hv[1];
+  return static_cast<cx_status>(hv[0]);
+}
+
+const char *cx_status_str(cx_status s) {
+  switch (s) {
+    case CX_OK: return "ok";
+    case CX_E_ARG: return "invalid argument";
+    case CX_E_CHILD_RANGE: return "child id out of range";
+    case CX_E_CHILD_LAYOUT: return "absent child before a present child";
+    case CX_E_KIND: return "structure violates its declared kind (two parents or duplicate child)";
+    case CX_E_CYCLE: return "cycle in the structure";
+    case CX_E_ARITY: return "binary cell applied to a node without exactly two children";
+    case CX_E_WORD_RANGE: return "word id out of range";
+    case CX_E_UNSUPPORTED: return "no kernel instantiation for this model";
+    case CX_E_WORKSPACE: return "workspace too small";
+    case CX_E_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+cx_status cx_forward_launch_info(const cx_model *m, int32_t *ctas, int32_t *threads,
+                                 int32_t *smem_bytes) {
+  if (!m) return CX_E_ARG;
+  cx::FwdPlan plan;
+  int Gn, Gu;
+  std::lock_guard<std::mutex> lk(g_mu);
+  int sms = num_sms_current();
+  if (sms <= 0) return CX_E_CUDA;
+  if (!cx::fwd_plan(m->cell, m->hidden, 2, sms, &plan, &Gn, &Gu)) return CX_E_UNSUPPORTED;
+  if (ctas) *ctas = plan.ctas;
+  if (threads) *threads = plan.threads;
+  if (smem_bytes) *smem_bytes = (int32_t)plan.smem;
+  return CX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,77 @@
+// common.cuh -- device primitives shared by the linearizer and forward kernels.
+//
+// The paper's global barrier (draft P:514-521; GRNN comparison P:1535-1545)
+// becomes a release/acquire counter barrier on B200: one red.release.gpu per
+// CTA, one thread spinning on ld.acquire.gpu. Data written by other CTAs is
+// read with ld.global.cg (L2) so no stale L1 line is ever used.
+#pragma once
+#include <cstdint>
+
+#include "../../include/cx.h"
+
+namespace cx {
+
+constexpr uint64_t kNoError = ~0ull;
+
+// 128-byte aligned synchronisation words kept in the caller's workspace.
+struct GridBar {
+  unsigned int count;   // arrivals, monotonic within one launch
+  unsigned int exit;    // blocks that left the kernel
+  unsigned int pad[30];
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add_u32(unsigned *p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Grid-wide barrier for a co-resident (cooperatively launched) grid.
+// `epoch` is a per-CTA register counting barriers passed so far.
+__device__ __forceinline__ void grid_sync(GridBar *bar, unsigned nblocks, unsigned &epoch) {
+  __syncthreads();
+  epoch += 1;
+  if (threadIdx.x == 0) {
+    const unsigned target = epoch * nblocks;
+    __threadfence();
+    red_release_add_u32(&bar->count, 1u);
+    while (ld_acquire_u32(&bar->count) < target) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Called once by every CTA at kernel end: the last CTA out resets the words
+// so the workspace is reusable without a memset (all CTAs have passed all
+// barriers by the time the exit count is complete).
+__device__ __forceinline__ void grid_exit(GridBar *bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned prev = atomicAdd(&bar->exit, 1u);
+    if (prev == nblocks - 1) {
+      bar->count = 0;
+      bar->exit = 0;
+      __threadfence();
+    }
+  }
+}
+
+// Latch a data error: lowest (code, node) wins.
+__device__ __forceinline__ void latch_error(cx_lin_header *h, int code, int node) {
+  unsigned long long key = ((unsigned long long)(unsigned)code << 32) | (unsigned)node;
+  atomicMin(reinterpret_cast<unsigned long long *>(&h->err_key), key);
+}
+
+__device__ __forceinline__ float4 ldcg4(const float *p) {
+  return __ldcg(reinterpret_cast<const float4 *>(p));
+}
+__device__ __forceinline__ int ldcg_i(const int *p) { return __ldcg(p); }
+
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+}  // namespace cx

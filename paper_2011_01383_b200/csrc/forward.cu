@@ -1,0 +1,862 @@
+// forward.cu -- the persistent forward kernel.
+//
+// What Cortex generates (Listing 2, App. A.4):
+//   for n in leaf_batch:           rnn[n] = leaf_case(n)          (specialised)
+//   for b in internal_batches:     barrier                        (batch loop carries the dependence)
+//     for n in batch:              rnn[n] = recursive_case(n, rnn[children(n)])
+// as ONE kernel launch with the weights persisted on chip.
+//
+// B200 design:
+//   * grid = Gn node groups x Gu unit groups, one 256-thread CTA per SM,
+//     cooperatively launched so a release/acquire grid barrier is legal;
+//   * CTA (gn, gu) owns hidden units [32 gu, 32 gu + 32) of every gate: the
+//     recurrent weight rows of those units stay resident in shared memory
+//     for the whole level loop (leaf-phase weights are staged first and then
+//     replaced while the CTA waits at the first barrier);
+//   * each level is split into contiguous chunks, one per node group; a
+//     chunk is processed in tiles of T <= 8 nodes: the tile's child rows are
+//     gathered (whole H-vectors, float4, L2) into shared memory -- the
+//     paper's dense per-iteration cache rnn_cache[b, n, i, k];
+//   * lane = hidden unit, the 8 warps split the contraction dimension; a
+//     product table per cell phase says which weight gate multiplies which
+//     gathered vector (children h_k, or their child-sum h~, or the leaf x);
+//   * partial sums are reduced through shared memory and the gate algebra is
+//     fused into the epilogue, which writes h (and c / z / s) of the owned
+//     units straight into the caller's INPUT-numbered h_out.
+// fp32 throughout: FMA on CUDA cores (the 1e-4 bound rules out TF32/bf16
+// tensor cores for this path; the bf16 tensor-core path is separate).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "fwd_kernels.cuh"
+
+namespace cx {
+namespace {
+
+constexpr int kWarps = kFwdThreads / 32;
+constexpr int kMaxC = 4;
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ void fma4(float &acc, const float4 &w, const float4 &v) {
+  acc = fmaf(w.x, v.x, acc);
+  acc = fmaf(w.y, v.y, acc);
+  acc = fmaf(w.z, v.z, acc);
+  acc = fmaf(w.w, v.w, acc);
+}
+__device__ __forceinline__ float4 add4(const float4 &a, const float4 &b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+// contiguous chunk of [0, M) owned by node group g of Gn
+__device__ __forceinline__ void chunk_of(int M, int Gn, int g, int &lo, int &hi) {
+  int q = M / Gn, r = M % Gn;
+  lo = g * q + min(g, r);
+  hi = lo + q + (g < r ? 1 : 0);
+}
+__device__ __forceinline__ int owner_of(int pos, int M, int Gn) {
+  int q = M / Gn, r = M % Gn, big = r * (q + 1);
+  return pos < big ? pos / (q + 1) : r + (pos - big) / q;
+}
+
+// ---------------------------------------------------------------------------
+// Per-cell shape traits, shared by host (smem sizing) and device.
+// NG: resident weight gates; NV: gathered vectors per node; NA: accumulators
+// per node; TMAX: node tile.
+// ---------------------------------------------------------------------------
+template <int CELL, int MAXC>
+struct Traits;
+template <int MAXC>
+struct Traits<CX_TREELSTM, MAXC> {
+  static constexpr int NG = 4, NV = MAXC, NA = 3 + MAXC, TMAX = 8;
+};
+template <int MAXC>
+struct Traits<CX_TREEGRU, MAXC> {
+  static constexpr int NG = 3, NV = MAXC, NA = 1 + MAXC, TMAX = 4;
+};
+template <int MAXC>
+struct Traits<CX_TREEFC, MAXC> {
+  static constexpr int NG = 2, NV = 2, NA = 1, TMAX = 8;
+};
+template <int MAXC>
+struct Traits<CX_DAGRNN, MAXC> {
+  static constexpr int NG = 1, NV = MAXC, NA = 1, TMAX = 8;
+};
+template <int MAXC>
+struct Traits<CX_TREERNN, MAXC> {
+  static constexpr int NG = 0, NV = 0, NA = 0, TMAX = 8;
+};
+
+template <int CELL, int MAXC>
+struct Layout {
+  using Tr = Traits<CELL, MAXC>;
+  // float offsets into dynamic shared memory
+  static __host__ __device__ size_t w_floats(int H) { return (size_t)Tr::NG * kUG * (H + 4); }
+  static __host__ __device__ size_t x_floats(int H) {
+    size_t xs = (size_t)Tr::TMAX * (Tr::NV > 0 ? Tr::NV : 1) * H;
+    size_t rs = (size_t)kWarps * Tr::NA * Tr::TMAX * 32;
+    return xs > rs ? xs : rs;
+  }
+  static __host__ __device__ size_t cv_floats() { return (size_t)Tr::TMAX * kMaxC * 32; }
+  static __host__ __device__ size_t bytes(int H) {
+    if (Tr::NG == 0) return 0;
+    return sizeof(float) * (w_floats(H) + x_floats(H) + cv_floats());
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Product tables: product p adds W[gate g(p)] . vec[v(p)] into acc a(p).
+// Vector index NV denotes the child sum h~ (computed on the fly).
+// ---------------------------------------------------------------------------
+struct PhLstmLeaf {  // [i; o; u] = W_iou x
+  static constexpr int G0 = 0, NG = 3, NV = 1, NA = 3, NP = 3;
+  static constexpr bool HT = false;
+  __device__ static constexpr int g(int p) { return p; }
+  __device__ static constexpr int v(int p) { return 0; }
+  __device__ static constexpr int a(int p) { return p; }
+};
+template <int MAXC>
+struct PhLstmLevel {  // [i; o; u] = U_iou h~ ; f_k = U_f h_k
+  static constexpr int G0 = 0, NG = 4, NV = MAXC, NA = 3 + MAXC, NP = 3 + MAXC;
+  static constexpr bool HT = true;
+  __device__ static constexpr int g(int p) { return p < 3 ? p : 3; }
+  __device__ static constexpr int v(int p) { return p < 3 ? MAXC : p - 3; }
+  __device__ static constexpr int a(int p) { return p; }
+};
+struct PhGruLeaf {  // z = W_z x ; g = W_h x
+  static constexpr int G0 = 0, NG = 2, NV = 1, NA = 2, NP = 2;
+  static constexpr bool HT = false;
+  __device__ static constexpr int g(int p) { return p; }
+  __device__ static constexpr int v(int p) { return 0; }
+  __device__ static constexpr int a(int p) { return p; }
+};
+template <int MAXC>
+struct PhGruA {  // z = U_z h~ ; r_k = U_r h_k   (gates 0, 1 of the resident set)
+  static constexpr int G0 = 0, NG = 2, NV = MAXC, NA = 1 + MAXC, NP = 1 + MAXC;
+  static constexpr bool HT = true;
+  __device__ static constexpr int g(int p) { return p < 1 ? 0 : 1; }
+  __device__ static constexpr int v(int p) { return p < 1 ? MAXC : p - 1; }
+  __device__ static constexpr int a(int p) { return p; }
+};
+struct PhGruB {  // U_h s   (gate 2 of the resident set; vector 0 = s)
+  static constexpr int G0 = 2, NG = 1, NV = 1, NA = 1, NP = 1;
+  static constexpr bool HT = false;
+  __device__ static constexpr int g(int p) { return 0; }
+  __device__ static constexpr int v(int p) { return 0; }
+  __device__ static constexpr int a(int p) { return 0; }
+};
+struct PhFcLevel {  // W [h_l; h_r] = W_l h_l + W_r h_r
+  static constexpr int G0 = 0, NG = 2, NV = 2, NA = 1, NP = 2;
+  static constexpr bool HT = false;
+  __device__ static constexpr int g(int p) { return p; }
+  __device__ static constexpr int v(int p) { return p; }
+  __device__ static constexpr int a(int p) { return 0; }
+};
+struct PhDagProj {  // W_x x
+  static constexpr int G0 = 0, NG = 1, NV = 1, NA = 1, NP = 1;
+  static constexpr bool HT = false;
+  __device__ static constexpr int g(int p) { return 0; }
+  __device__ static constexpr int v(int p) { return 0; }
+  __device__ static constexpr int a(int p) { return 0; }
+};
+template <int MAXC>
+struct PhDagLevel {  // U h~
+  static constexpr int G0 = 0, NG = 1, NV = MAXC, NA = 1, NP = 1;
+  static constexpr bool HT = true;
+  __device__ static constexpr int g(int p) { return 0; }
+  __device__ static constexpr int v(int p) { return MAXC; }
+  __device__ static constexpr int a(int p) { return 0; }
+};
+
+// Lane = unit (u < 32), warp w covers k in [w H/8, (w+1) H/8).
+// Ws: [gate][unit][H + 4] (row padding keeps float4 reads conflict-free);
+// X : [T][NV][H] (broadcast reads).
+template <class PH, int T>
+__device__ __forceinline__ void fma_engine(const float *__restrict__ Ws, const float *__restrict__ X,
+                                           int H, float (&acc)[PH::NA][T]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int HP = H + 4;
+#pragma unroll
+  for (int a = 0; a < PH::NA; a++)
+#pragma unroll
+    for (int t = 0; t < T; t++) acc[a][t] = 0.f;
+  const int kc = H / kWarps;
+  const int kb = warp * kc;
+  constexpr int NG_USED = PH::NG;
+  for (int k = kb; k < kb + kc; k += 4) {
+    float4 w[NG_USED];
+#pragma unroll
+    for (int g = 0; g < NG_USED; g++)
+      w[g] = *reinterpret_cast<const float4 *>(Ws + (size_t)((PH::G0 + g) * kUG + lane) * HP + k);
+#pragma unroll
+    for (int t = 0; t < T; t++) {
+      float4 v[PH::NV + 1];
+#pragma unroll
+      for (int j = 0; j < PH::NV; j++)
+        v[j] = *reinterpret_cast<const float4 *>(X + (size_t)(t * PH::NV + j) * H + k);
+      if constexpr (PH::HT) {
+        v[PH::NV] = v[0];
+#pragma unroll
+        for (int j = 1; j < PH::NV; j++) v[PH::NV] = add4(v[PH::NV], v[j]);
+      }
+#pragma unroll
+      for (int p = 0; p < PH::NP; p++) fma4(acc[PH::a(p)][t], w[PH::g(p)], v[PH::v(p)]);
+    }
+  }
+}
+
+// Cross-warp reduction of the K-split partial sums through `red` (aliases X).
+// Thread (t = tid / 32, u = lane) receives the full sums of node t, unit u.
+template <int NA, int T>
+__device__ __forceinline__ void reduce_acc(float *red, const float (&acc)[NA][T], float (&out)[NA]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();  // everyone is done reading X
+#pragma unroll
+  for (int a = 0; a < NA; a++)
+#pragma unroll
+    for (int t = 0; t < T; t++) red[((warp * NA + a) * T + t) * 32 + lane] = acc[a][t];
+  __syncthreads();
+  const int t = threadIdx.x >> 5;
+#pragma unroll
+  for (int a = 0; a < NA; a++) {
+    float s = 0.f;
+    if (t < T) {
+#pragma unroll
+      for (int w = 0; w < kWarps; w++) s += red[((w * NA + a) * T + t) * 32 + lane];
+    }
+    out[a] = s;
+  }
+}
+
+struct TileMeta {
+  int own[8];            // input id of each node of the tile
+  int cin[8][kMaxC];     // input ids of children, -1 absent
+  int nch[8];            // present children
+  int word[8];           // clamped word id (phases that read Emb)
+};
+
+struct GateSrc {
+  const float *base;
+  int r0, ld, c0;
+};
+
+// Stage rows (units unit0..unit0+31) of NG gates into Ws with cp.async.
+__device__ void load_gates(float *Ws, const GateSrc *gs, int NG, int unit0, int H) {
+  const int HP = H + 4, q = H >> 2, per_gate = kUG * q;
+  for (int idx = threadIdx.x; idx < NG * per_gate; idx += blockDim.x) {
+    int g = idx / per_gate, rem = idx - g * per_gate, u = rem / q, c = rem - u * q;
+    const float *src = gs[g].base + (size_t)(gs[g].r0 + unit0 + u) * gs[g].ld + gs[g].c0 + 4 * c;
+    cp_async16(Ws + (size_t)(g * kUG + u) * HP + 4 * c, src);
+  }
+  cp_async_commit();
+}
+
+// Tile bookkeeping: node new ids [i0, i0 + cnt).
+// mode 0: internal nodes (children); mode 1: nodes that read a word.
+__device__ void load_meta(const FwdArgs &a, TileMeta &m, int i0, int cnt, bool want_children,
+                          bool want_word, bool binary, bool latch) {
+  const int t = threadIdx.x;
+  if (t < cnt) {
+    int i = i0 + t;
+    int own = __ldg(a.perm + i);
+    m.own[t] = own;
+    if (want_word) {
+      int w = __ldg(a.words + own);
+      if (w < 0 || w >= a.V) {
+        if (latch) latch_error(a.hdr, CX_E_WORD_RANGE, own);
+        w = 0;
+      }
+      m.word[t] = w;
+    }
+    if (want_children) {
+      int nc = 0;
+      for (int k = 0; k < a.maxc; k++) {
+        int c = __ldg(a.chn + (size_t)k * a.n + i);
+        if (c < 0) break;
+        if (k < kMaxC) m.cin[t][k] = __ldg(a.perm + c);
+        nc++;
+      }
+      for (int k = nc; k < kMaxC; k++) m.cin[t][k] = -1;
+      if (binary && nc != 2) {
+        if (latch) latch_error(a.hdr, CX_E_ARITY, own);
+        if (nc < 2) m.cin[t][1] = m.cin[t][0];  // clamp for memory safety
+        nc = 2;
+      }
+      m.nch[t] = nc;
+    }
+  }
+}
+
+// X[t][j][:] = row src(t, j) (H floats) or zeros; rows of t >= cnt untouched.
+template <class SRC>
+__device__ __forceinline__ void gather_rows(float *X, int NV, int H, int cnt, SRC src) {
+  const int q = H >> 2, total = cnt * NV * q;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    int row = idx / q, c = idx - row * q;
+    int t = row / NV, j = row - t * NV;
+    const float *p = src(t, j);
+    float4 v = p ? ldcg4(p + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4 *>(X + (size_t)row * H + 4 * c) = v;
+  }
+}
+
+// Walk [lo, hi) in tiles of at most TMAX nodes; a tile of cnt nodes runs the
+// smallest instantiation T in {1, 2, 4, 8} with T >= cnt (warp-uniform branch).
+template <int TMAX, class F>
+__device__ __forceinline__ void tiles_T(int lo, int hi, F &f) {
+  for (int i0 = lo; i0 < hi; i0 += TMAX) {
+    int cnt = min(TMAX, hi - i0);
+    if constexpr (TMAX >= 8) {
+      if (cnt > 4) {
+        f.template run<8>(i0, cnt);
+        continue;
+      }
+    }
+    if (cnt > 2) f.template run<4>(i0, cnt);
+    else if (cnt == 2) f.template run<2>(i0, cnt);
+    else f.template run<1>(i0, cnt);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Cell bodies. Each provides leaf_range(), leaf weights, level weights,
+// phases per level, and the tile functors.
+// ---------------------------------------------------------------------------
+struct Ctx {
+  const FwdArgs *a;
+  float *Ws, *X, *cv;
+  TileMeta *m;
+  int gn, gu, unit0, H;
+  bool latch;  // only unit group 0 latches data errors (avoid duplicate atomics)
+};
+
+// ----- TreeLSTM (Q1: child-sum, [Tai et al.]) -------------------------------
+template <int MAXC>
+struct TreeLstm {
+  static constexpr int kPhases = 1;
+  struct Leaf {
+    Ctx c;
+    template <int T>
+    __device__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      const int H = c.H;
+      load_meta(a, *c.m, i0, cnt, false, true, false, c.latch);
+      __syncthreads();
+      gather_rows(c.X, 1, H, cnt, [&](int t, int) { return a.emb + (size_t)c.m->word[t] * H; });
+      __syncthreads();
+      float acc[3][T], s[3];
+      fma_engine<PhLstmLeaf, T>(c.Ws, c.X, H, acc);
+      reduce_acc<3, T>(c.X, acc, s);
+      const int t = threadIdx.x >> 5, unit = c.unit0 + (threadIdx.x & 31);
+      if (t < cnt) {
+        const float *b = a.w[2];
+        float ig = s[0] + __ldg(b + unit), og = s[1] + __ldg(b + H + unit),
+              ug = s[2] + __ldg(b + 2 * H + unit);
+        float cc = sigmoidf_(ig) * tanhf(ug);
+        float hh = sigmoidf_(og) * tanhf(cc);
+        size_t o = (size_t)c.m->own[t] * H + unit;
+        a.h_out[o] = hh;
+        a.cbuf[o] = cc;
+      }
+      __syncthreads();
+    }
+  };
+  struct Level {
+    Ctx c;
+    int phase;
+    template <int T>
+    __device__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      const int H = c.H;
+      const int lane = threadIdx.x & 31;
+      load_meta(a, *c.m, i0, cnt, true, false, false, c.latch);
+      __syncthreads();
+      gather_rows(c.X, MAXC, H, cnt, [&](int t, int j) {
+        int ci = c.m->cin[t][j];
+        return ci >= 0 ? a.h_out + (size_t)ci * H : (const float *)nullptr;
+      });
+      // children's memory cells for the owned units
+      for (int idx = threadIdx.x; idx < cnt * MAXC * 32; idx += blockDim.x) {
+        int t = idx / (MAXC * 32), r = idx - t * MAXC * 32, k = r >> 5, u = r & 31;
+        int ci = c.m->cin[t][k];
+        c.cv[(t * kMaxC + k) * 32 + u] = ci >= 0 ? __ldcg(a.cbuf + (size_t)ci * H + c.unit0 + u) : 0.f;
+      }
+      __syncthreads();
+      float acc[3 + MAXC][T], s[3 + MAXC];
+      fma_engine<PhLstmLevel<MAXC>, T>(c.Ws, c.X, H, acc);
+      reduce_acc<3 + MAXC, T>(c.X, acc, s);
+      const int t = threadIdx.x >> 5, unit = c.unit0 + lane;
+      if (t < cnt) {
+        const float *b = a.w[2], *bf = a.w[4];
+        float ig = s[0] + __ldg(b + unit), og = s[1] + __ldg(b + H + unit),
+              ug = s[2] + __ldg(b + 2 * H + unit), bfu = __ldg(bf + unit);
+        float cc = sigmoidf_(ig) * tanhf(ug);
+        const int nc = c.m->nch[t];
+#pragma unroll
+        for (int k = 0; k < MAXC; k++)
+          if (k < nc) cc += sigmoidf_(s[3 + k] + bfu) * c.cv[(t * kMaxC + k) * 32 + lane];
+        float hh = sigmoidf_(og) * tanhf(cc);
+        size_t o = (size_t)c.m->own[t] * H + unit;
+        a.h_out[o] = hh;
+        a.cbuf[o] = cc;
+      }
+      __syncthreads();
+    }
+  };
+  __device__ static int leaf_lo(const FwdArgs &, int first_leaf) { return first_leaf; }
+  __device__ static int leaf_gates(const FwdArgs &a, GateSrc *gs) {
+    const int H = a.H;
+    gs[0] = {a.w[0], 0, H, 0};
+    gs[1] = {a.w[0], H, H, 0};
+    gs[2] = {a.w[0], 2 * H, H, 0};
+    return 3;
+  }
+  __device__ static int level_gates(const FwdArgs &a, GateSrc *gs) {
+    const int H = a.H;
+    gs[0] = {a.w[1], 0, H, 0};
+    gs[1] = {a.w[1], H, H, 0};
+    gs[2] = {a.w[1], 2 * H, H, 0};
+    gs[3] = {a.w[3], 0, H, 0};
+    return 4;
+  }
+};
+
+// ----- TreeGRU (Q3: child-sum, reset gate per child before U_h) -------------
+template <int MAXC>
+struct TreeGru {
+  static constexpr int kPhases = 2;
+  struct Leaf {
+    Ctx c;
+    template <int T>
+    __device__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      const int H = c.H;
+      load_meta(a, *c.m, i0, cnt, false, true, false, c.latch);
+      __syncthreads();
+      gather_rows(c.X, 1, H, cnt, [&](int t, int) { return a.emb + (size_t)c.m->word[t] * H; });
+      __syncthreads();
+      float acc[2][T], s[2];
+      fma_engine<PhGruLeaf, T>(c.Ws, c.X, H, acc);
+      reduce_acc<2, T>(c.X, acc, s);
+      const int t = threadIdx.x >> 5, unit = c.unit0 + (threadIdx.x & 31);
+      if (t < cnt) {
+        float z = sigmoidf_(s[0] + __ldg(a.w[4] + unit));
+        float g = tanhf(s[1] + __ldg(a.w[6] + unit));
+        a.h_out[(size_t)c.m->own[t] * H + unit] = (1.f - z) * g;
+      }
+      __syncthreads();
+    }
+  };
+  struct Level {
+    Ctx c;
+    int phase;
+    template <int T>
+    __device__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      const int H = c.H;
+      const int lane = threadIdx.x & 31;
+      const int t = threadIdx.x >> 5, unit = c.unit0 + lane;
+      if (phase == 0) {
+        load_meta(a, *c.m, i0, cnt, true, false, false, c.latch);
+        __syncthreads();
+        gather_rows(c.X, MAXC, H, cnt, [&](int tt, int j) {
+          int ci = c.m->cin[tt][j];
+          return ci >= 0 ? a.h_out + (size_t)ci * H : (const float *)nullptr;
+        });
+        __syncthreads();
+        if (t < cnt) {  // stash h_k[unit] before the reduction overwrites X
+#pragma unroll
+          for (int k = 0; k < MAXC; k++)
+            c.cv[(t * kMaxC + k) * 32 + lane] = c.X[(size_t)(t * MAXC + k) * H + unit];
+        }
+        float acc[1 + MAXC][T], s[1 + MAXC];
+        fma_engine<PhGruA<MAXC>, T>(c.Ws, c.X, H, acc);
+        reduce_acc<1 + MAXC, T>(c.X, acc, s);
+        if (t < cnt) {
+          float z = sigmoidf_(s[0] + __ldg(a.w[4] + unit));
+          float br = __ldg(a.w[5] + unit);
+          float sum = 0.f, ht = 0.f;
+          const int nc = c.m->nch[t];
+#pragma unroll
+          for (int k = 0; k < MAXC; k++)
+            if (k < nc) {
+              float hk = c.cv[(t * kMaxC + k) * 32 + lane];
+              sum += sigmoidf_(s[1 + k] + br) * hk;
+              ht += hk;
+            }
+          size_t o = (size_t)c.m->own[t] * H + unit;
+          a.sbuf[o] = sum;
+          a.zbuf[o] = z;
+          a.h_out[o] = ht;  // stash h~ for phase B (overwritten there)
+        }
+        __syncthreads();
+      } else {
+        load_meta(a, *c.m, i0, cnt, false, false, false, false);
+        __syncthreads();
+        gather_rows(c.X, 1, H, cnt, [&](int tt, int) { return a.sbuf + (size_t)c.m->own[tt] * H; });
+        __syncthreads();
+        float acc[1][T], s[1];
+        fma_engine<PhGruB, T>(c.Ws, c.X, H, acc);
+        reduce_acc<1, T>(c.X, acc, s);
+        if (t < cnt) {
+          size_t o = (size_t)c.m->own[t] * H + unit;
+          float g = tanhf(s[0] + __ldg(a.w[6] + unit));
+          float z = __ldcg(a.zbuf + o), ht = __ldcg(a.h_out + o);
+          a.h_out[o] = z * ht + (1.f - z) * g;
+        }
+        __syncthreads();
+      }
+    }
+  };
+  __device__ static int leaf_lo(const FwdArgs &, int first_leaf) { return first_leaf; }
+  __device__ static int leaf_gates(const FwdArgs &a, GateSrc *gs) {
+    gs[0] = {a.w[0], 0, a.H, 0};
+    gs[1] = {a.w[0], a.H, a.H, 0};
+    return 2;
+  }
+  __device__ static int level_gates(const FwdArgs &a, GateSrc *gs) {
+    gs[0] = {a.w[1], 0, a.H, 0};
+    gs[1] = {a.w[2], 0, a.H, 0};
+    gs[2] = {a.w[3], 0, a.H, 0};
+    return 3;
+  }
+};
+
+// ----- TreeFC (Q2: h = tanh(W [h_l; h_r] + b), leaf = Emb) -----------------
+template <int MAXC>
+struct TreeFc {
+  static constexpr int kPhases = 1;
+  struct Leaf {  // pure gather (no weights): h = x
+    Ctx c;
+    template <int T>
+    __device__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      load_meta(a, *c.m, i0, cnt, false, true, false, c.latch);
+      __syncthreads();
+      const int t = threadIdx.x >> 5, unit = c.unit0 + (threadIdx.x & 31);
+      if (t < cnt)
+        a.h_out[(size_t)c.m->own[t] * c.H + unit] = __ldg(a.emb + (size_t)c.m->word[t] * c.H + unit);
+      __syncthreads();
+    }
+  };
+  struct Level {
+    Ctx c;
+    int phase;
+    template <int T>
+    __device__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      const int H = c.H;
+      load_meta(a, *c.m, i0, cnt, true, false, true, c.latch);
+      __syncthreads();
+      gather_rows(c.X, 2, H, cnt, [&](int t, int j) { return a.h_out + (size_t)c.m->cin[t][j] * H; });
+      __syncthreads();
+      float acc[1][T], s[1];
+      fma_engine<PhFcLevel, T>(c.Ws, c.X, H, acc);
+      reduce_acc<1, T>(c.X, acc, s);
+      const int t = threadIdx.x >> 5, unit = c.unit0 + (threadIdx.x & 31);
+      if (t < cnt) a.h_out[(size_t)c.m->own[t] * H + unit] = tanhf(s[0] + __ldg(a.w[1] + unit));
+      __syncthreads();
+    }
+  };
+  __device__ static int leaf_lo(const FwdArgs &, int first_leaf) { return first_leaf; }
+  __device__ static int leaf_gates(const FwdArgs &, GateSrc *) { return 0; }
+  __device__ static int level_gates(const FwdArgs &a, GateSrc *gs) {
+    gs[0] = {a.w[0], 0, 2 * a.H, 0};
+    gs[1] = {a.w[0], 0, 2 * a.H, a.H};
+    return 2;
+  }
+};
+
+// ----- DAG-RNN (Q8: h = tanh(W_x x + U sum_pred h + b), every node has x) --
+template <int MAXC>
+struct DagRnn {
+  static constexpr int kPhases = 1;
+  // "leaf" phase = input projection of EVERY node (GRNN-style input GEMM at the
+  // start); leaves finish here.
+  struct Leaf {
+    Ctx c;
+    template <int T>
+    __device__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      const int H = c.H;
+      load_meta(a, *c.m, i0, cnt, false, true, false, c.latch);
+      __syncthreads();
+      gather_rows(c.X, 1, H, cnt, [&](int t, int) { return a.emb + (size_t)c.m->word[t] * H; });
+      __syncthreads();
+      float acc[1][T], s[1];
+      fma_engine<PhDagProj, T>(c.Ws, c.X, H, acc);
+      reduce_acc<1, T>(c.X, acc, s);
+      const int t = threadIdx.x >> 5, unit = c.unit0 + (threadIdx.x & 31);
+      if (t < cnt) {
+        float p = s[0] + __ldg(a.w[2] + unit);
+        size_t o = (size_t)c.m->own[t] * H + unit;
+        a.pbuf[o] = p;
+        if (i0 + t >= a.hdr->first_leaf) a.h_out[o] = tanhf(p);
+      }
+      __syncthreads();
+    }
+  };
+  struct Level {
+    Ctx c;
+    int phase;
+    template <int T>
+    __device__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      const int H = c.H;
+      const int lane = threadIdx.x & 31;
+      load_meta(a, *c.m, i0, cnt, true, false, false, c.latch);
+      __syncthreads();
+      gather_rows(c.X, MAXC, H, cnt, [&](int t, int j) {
+        int ci = c.m->cin[t][j];
+        return ci >= 0 ? a.h_out + (size_t)ci * H : (const float *)nullptr;
+      });
+      for (int idx = threadIdx.x; idx < cnt * 32; idx += blockDim.x)
+        c.cv[idx] = __ldcg(a.pbuf + (size_t)c.m->own[idx >> 5] * H + c.unit0 + (idx & 31));
+      __syncthreads();
+      float acc[1][T], s[1];
+      fma_engine<PhDagLevel<MAXC>, T>(c.Ws, c.X, H, acc);
+      reduce_acc<1, T>(c.X, acc, s);
+      const int t = threadIdx.x >> 5, unit = c.unit0 + lane;
+      if (t < cnt) a.h_out[(size_t)c.m->own[t] * H + unit] = tanhf(s[0] + c.cv[t * 32 + lane]);
+      __syncthreads();
+    }
+  };
+  __device__ static int leaf_lo(const FwdArgs &, int) { return 0; }
+  __device__ static int leaf_gates(const FwdArgs &a, GateSrc *gs) {
+    gs[0] = {a.w[0], 0, a.H, 0};
+    return 1;
+  }
+  __device__ static int level_gates(const FwdArgs &a, GateSrc *gs) {
+    gs[0] = {a.w[1], 0, a.H, 0};
+    return 1;
+  }
+};
+
+// ----- TreeRNN (Listing 1: leaf Emb[words[n]], internal tanh(lh + rh)) ------
+template <int MAXC>
+struct TreeRnn {
+  static constexpr int kPhases = 1;
+  struct Leaf {
+    Ctx c;
+    template <int T>
+    __device__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      load_meta(a, *c.m, i0, cnt, false, true, false, c.latch);
+      __syncthreads();
+      const int ug = min(kUG, c.H);
+      for (int idx = threadIdx.x; idx < cnt * ug; idx += blockDim.x) {
+        int t = idx / ug, unit = c.unit0 + idx % ug;
+        a.h_out[(size_t)c.m->own[t] * c.H + unit] = __ldg(a.emb + (size_t)c.m->word[t] * c.H + unit);
+      }
+      __syncthreads();
+    }
+  };
+  struct Level {
+    Ctx c;
+    int phase;
+    template <int T>
+    __device__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      load_meta(a, *c.m, i0, cnt, true, false, true, c.latch);
+      __syncthreads();
+      const int ug = min(kUG, c.H);
+      for (int idx = threadIdx.x; idx < cnt * ug; idx += blockDim.x) {
+        int t = idx / ug, unit = c.unit0 + idx % ug;
+        float l = __ldcg(a.h_out + (size_t)c.m->cin[t][0] * c.H + unit);
+        float r = __ldcg(a.h_out + (size_t)c.m->cin[t][1] * c.H + unit);
+        a.h_out[(size_t)c.m->own[t] * c.H + unit] = tanhf(l + r);
+      }
+      __syncthreads();
+    }
+  };
+  __device__ static int leaf_lo(const FwdArgs &, int first_leaf) { return first_leaf; }
+  __device__ static int leaf_gates(const FwdArgs &, GateSrc *) { return 0; }
+  __device__ static int level_gates(const FwdArgs &, GateSrc *) { return 0; }
+};
+
+// ---------------------------------------------------------------------------
+// The persistent kernel skeleton shared by the unit-split cells.
+// ---------------------------------------------------------------------------
+template <int CELL, int MAXC, class C>
+__global__ void __launch_bounds__(kFwdThreads, 1) fwd_kernel(FwdArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  __shared__ TileMeta meta;
+  GateSrc gsrc[4];
+  using Lay = Layout<CELL, MAXC>;
+  using Tr = Traits<CELL, MAXC>;
+
+  if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
+  const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n;
+  const int gn = blockIdx.x / a.Gu, gu = blockIdx.x % a.Gu;
+  const int H = a.H;
+
+  Ctx ctx;
+  ctx.a = &a;
+  ctx.Ws = smem;
+  ctx.X = smem + Lay::w_floats(H);
+  ctx.cv = ctx.X + Lay::x_floats(H);
+  ctx.m = &meta;
+  ctx.gn = gn;
+  ctx.gu = gu;
+  ctx.unit0 = gu * min(kUG, H);
+  ctx.H = H;
+  ctx.latch = gu == 0;
+  unsigned epoch = 0;
+
+  // ---- leaf phase (specialised leaf loop nest) ------------------
+  {
+    int ng = C::leaf_gates(a, gsrc);
+    if (ng) {
+      load_gates(ctx.Ws, gsrc, ng, ctx.unit0, H);
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    int lo0 = C::leaf_lo(a, first_leaf);
+    int lo, hi;
+    chunk_of(n - lo0, a.Gn, gn, lo, hi);
+    typename C::Leaf f{ctx};
+    tiles_T<Tr::TMAX>(lo0 + lo, lo0 + hi, f);
+  }
+  __syncthreads();
+  // recurrent weights: issued now, landed while the CTA waits at the barrier
+  {
+    int ng = C::level_gates(a, gsrc);
+    if (ng) load_gates(ctx.Ws, gsrc, ng, ctx.unit0, H);
+  }
+  // ---- internal batches, one grid barrier per level (and phase) -----------
+  for (int l = 1; l < L; l++) {
+    const int base = __ldg(a.lbeg + l), M = __ldg(a.lsize + l);
+    int lo, hi;
+    chunk_of(M, a.Gn, gn, lo, hi);
+    for (int ph = 0; ph < C::kPhases; ph++) {
+      grid_sync(a.bar, gridDim.x, epoch);
+      if (l == 1 && ph == 0) {
+        cp_async_wait_all();
+        __syncthreads();
+      }
+      typename C::Level f{ctx, ph};
+      tiles_T<Tr::TMAX>(base + lo, base + hi, f);
+    }
+  }
+  cp_async_wait_all();
+
+  // ---- packed root states: each CTA copies the rows it wrote itself --------
+  if (a.root_out) {
+    const int R = a.hdr->num_roots;
+    const int ug = min(kUG, H);
+    const int lo0 = C::leaf_lo(a, first_leaf);
+    for (int r = 0; r < R; r++) {
+      int i = __ldg(a.roots + r);
+      int lvl = __ldg(a.hnew + i);
+      // leaves were written by the leaf (or projection) phase's chunking
+      int own = lvl == 0 ? owner_of(i - lo0, n - lo0, a.Gn)
+                         : owner_of(i - __ldg(a.lbeg + lvl), __ldg(a.lsize + lvl), a.Gn);
+      if (own != gn) continue;
+      int src = __ldg(a.perm + i);
+      for (int u = threadIdx.x; u < ug; u += blockDim.x)
+        a.root_out[(size_t)r * H + ctx.unit0 + u] = __ldcg(a.h_out + (size_t)src * H + ctx.unit0 + u);
+    }
+  }
+
+  // ---- the last CTA out publishes the latched status -----------------------
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned prev = atomicAdd(&a.bar->exit, 1u);
+    if (prev == gridDim.x - 1) {
+      unsigned long long key = atomicAdd(reinterpret_cast<unsigned long long *>(&a.hdr->err_key), 0ull);
+      if (key != kNoError) {
+        a.hdr->status = (int)(key >> 32);
+        a.hdr->bad_node = (int)(key & 0xffffffffu);
+      }
+      a.bar->count = 0;
+      a.bar->exit = 0;
+      __threadfence();
+    }
+  }
+}
+
+}  // namespace
+
+// MV-RNN lives in forward_mvrnn.cu
+bool mvrnn_plan(int H, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
+
+template <int CELL, int MAXC, class C>
+static bool plan_for(int H, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
+  using Lay = Layout<CELL, MAXC>;
+  int gu = H >= kUG ? H / kUG : 1;
+  if (H >= kUG && H % kUG) return false;
+  if (gu > num_sms) return false;
+  size_t smem = Lay::bytes(H);
+  if (smem > 227 * 1024) return false;
+  auto k = fwd_kernel<CELL, MAXC, C>;
+  static size_t smem_set = 0;  // callers serialise plans (api.cu mutex)
+  if (smem > smem_set) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return false;
+    smem_set = smem;
+  }
+  *Gu = gu;
+  *Gn = num_sms / gu;
+  p->ctas = *Gn * gu;
+  p->threads = kFwdThreads;
+  p->smem = smem;
+  p->kernel = (const void *)k;
+  return true;
+}
+
+bool fwd_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu) {
+  if (H <= 0 || H > 1024 || H % 4) return false;
+  const bool weighted = cell != CX_TREERNN && cell != CX_MVRNN;
+  if (weighted && (H % kUG)) return false;
+  switch (cell) {
+    case CX_TREERNN:
+      return plan_for<CX_TREERNN, 2, TreeRnn<2>>(H, num_sms, plan, Gn, Gu);
+    case CX_TREEFC:
+      return plan_for<CX_TREEFC, 2, TreeFc<2>>(H, num_sms, plan, Gn, Gu);
+    case CX_TREELSTM:
+      if (maxc <= 1) return plan_for<CX_TREELSTM, 1, TreeLstm<1>>(H, num_sms, plan, Gn, Gu);
+      if (maxc <= 2) return plan_for<CX_TREELSTM, 2, TreeLstm<2>>(H, num_sms, plan, Gn, Gu);
+      if (maxc <= 4) return plan_for<CX_TREELSTM, 4, TreeLstm<4>>(H, num_sms, plan, Gn, Gu);
+      return false;
+    case CX_TREEGRU:
+      if (maxc <= 1) return plan_for<CX_TREEGRU, 1, TreeGru<1>>(H, num_sms, plan, Gn, Gu);
+      if (maxc <= 2) return plan_for<CX_TREEGRU, 2, TreeGru<2>>(H, num_sms, plan, Gn, Gu);
+      if (maxc <= 4) return plan_for<CX_TREEGRU, 4, TreeGru<4>>(H, num_sms, plan, Gn, Gu);
+      return false;
+    case CX_DAGRNN:
+      if (maxc <= 1) return plan_for<CX_DAGRNN, 1, DagRnn<1>>(H, num_sms, plan, Gn, Gu);
+      if (maxc <= 2) return plan_for<CX_DAGRNN, 2, DagRnn<2>>(H, num_sms, plan, Gn, Gu);
+      if (maxc <= 4) return plan_for<CX_DAGRNN, 4, DagRnn<4>>(H, num_sms, plan, Gn, Gu);
+      return false;
+    case CX_MVRNN:
+      return mvrnn_plan(H, num_sms, plan, Gn, Gu);
+  }
+  return false;
+}
+
+size_t fwd_workspace_bytes(int cell, int H, int n) {
+  size_t N = (size_t)(n > 0 ? n : 1), h = (size_t)H;
+  size_t b = sizeof(GridBar);
+  switch (cell) {
+    case CX_TREELSTM: b += 4 * N * h; break;            // c (when aux_out == NULL)
+    case CX_TREEGRU: b += 2 * 4 * N * h; break;         // z, s
+    case CX_DAGRNN: b += 4 * N * h; break;              // projections
+    case CX_MVRNN: b += 4 * N * h * h; break;           // A (when aux_out == NULL)
+    default: break;
+  }
+  return b + 1024;
+}
+
+cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream) {
+  void *params[] = {&args};
+  return cudaLaunchCooperativeKernel(plan.kernel, dim3(plan.ctas), dim3(plan.threads), params,
+                                     plan.smem, stream);
+}
+
+}  // namespace cx

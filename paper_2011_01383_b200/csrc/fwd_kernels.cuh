@@ -1,0 +1,43 @@
+// fwd_kernels.cuh -- internal interface between api.cu and forward.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace cx {
+
+constexpr int kFwdThreads = 256;  // 8 warps; warps split the contraction (K) dim
+constexpr int kUG = 32;           // hidden units per CTA (lane = unit)
+
+struct FwdArgs {
+  cx_lin_header *hdr;
+  const int32_t *perm, *chn, *lbeg, *lsize, *hnew, *roots;
+  int n, maxc, H, V;
+  const float *emb;
+  const int32_t *words;
+  const float *w[8];
+  float *h_out, *aux_out, *root_out;
+  float *cbuf;  // TreeLSTM memory cells [n][H] (aux_out or workspace)
+  float *zbuf;  // TreeGRU update gates [n][H]
+  float *sbuf;  // TreeGRU sum_k r_k * h_k [n][H]
+  float *pbuf;  // DAG-RNN input projections W_x x + b [n][H]
+  float *Abuf;  // MV-RNN matrices [n][H][H] (aux_out or workspace)
+  GridBar *bar;
+  int Gn, Gu;   // node groups x unit groups = CTAs
+};
+
+struct FwdPlan {
+  int ctas, threads;
+  size_t smem;
+  const void *kernel;
+};
+
+// Returns false (CX_E_UNSUPPORTED) when no instantiation covers the model.
+bool fwd_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
+size_t fwd_workspace_bytes(int cell, int H, int n);
+cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream);
+
+}  // namespace cx

@@ -1,0 +1,41 @@
+// lin_kernels.cuh -- internal interface between api.cu and linearize.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace cx {
+
+// shared-memory budget of the single-CTA linearizer (int entries / bytes)
+constexpr int kLinSmemCnt = 8192;              // per-(level, segment) count table
+constexpr size_t kLinSmemMax = 200 * 1024;     // heights + in-degree + children copy + table
+
+struct LinArgs {
+  const int32_t *ch;  // [maxc][n] input ids
+  int n, maxc, kind;
+  cx_lin_header *hdr;
+  int32_t *perm, *inv, *chn, *hnew, *lbeg, *lsize, *roots;
+  // workspace
+  GridBar *bar;
+  int32_t *misc;   // 32 ints
+  int32_t *indeg;  // n
+  int32_t *hgt;    // n
+  int32_t *cnt;    // budget
+  int budget;
+};
+
+inline size_t lin_budget_entries(int n) { return 2 * (size_t)n + 4096; }
+
+inline size_t lin_workspace_bytes(int n) {
+  return sizeof(GridBar) + 32 * sizeof(int32_t) + sizeof(int32_t) * (2 * (size_t)n) +
+         sizeof(int32_t) * lin_budget_entries(n) + 256;
+}
+
+bool lin_use_single(int n, int maxc);
+size_t lin_single_smem_bytes(int n, int maxc);
+cudaError_t launch_linearize(const LinArgs &a, int num_sms, cudaStream_t stream);
+
+}  // namespace cx

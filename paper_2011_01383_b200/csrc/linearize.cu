@@ -1,0 +1,377 @@
+// linearize.cu -- device-side data-structure linearizer.
+//
+// PAPER.md §4.2 runs the linearizer on the host CPU: a
+// recursive traversal that appends each node to internal_batches[node.height]
+// and collects leaves separately (specialisation). App. B
+// fixes the numbering: a batch is a contiguous id range
+// (batch_begin/batch_length), parents get lower ids than children and leaves
+// the highest ids. Here the same arrays are produced on the GPU so the
+// forward kernel can start without a host round trip:
+//   a1 validate + in-degree     one pass, atomics
+//   a2 heights                  Jacobi rounds h(v) = 1 + max h(children);
+//                               round r finalises exactly the nodes of height r
+//   a3 level histogram + scan   per-(level, id-segment) counts, one scan
+//   a4 stable scatter           warp __match_any_sync ranking, ascending input
+//                               id inside a level (reading Q4)
+//   a5 remap                    children_new[k][i] = inv[children[k][perm[i]]]
+// Two instantiations: one CTA with everything in shared memory (small n: the
+// latency configs) and a cooperative multi-CTA one with the grid barrier of
+// common.cuh (b4096 and large DAGs).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "lin_kernels.cuh"
+
+namespace cx {
+
+namespace {
+
+constexpr int kLinThreads = 1024;
+constexpr int kSegMin = 256;
+
+template <bool MULTI>
+__device__ __forceinline__ int ld_dyn(const int *p) {
+  if constexpr (MULTI) return __ldcg(p);
+  else return *reinterpret_cast<const volatile int *>(p);
+}
+
+template <bool MULTI>
+__device__ __forceinline__ void lsync(GridBar *bar, unsigned &epoch) {
+  if constexpr (MULTI) grid_sync(bar, gridDim.x, epoch);
+  else __syncthreads();
+}
+
+// block-wide exclusive scan of one value per thread; returns the block total
+__device__ int block_exclusive_scan(int v, int &total, int *s_tmp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_tmp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int nw = blockDim.x >> 5;
+    int w = lane < nw ? s_tmp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    s_tmp[lane] = w;  // inclusive warp totals
+  }
+  __syncthreads();
+  total = s_tmp[(blockDim.x >> 5) - 1];
+  int excl = x - v + (warp > 0 ? s_tmp[warp - 1] : 0);
+  __syncthreads();
+  return excl;
+}
+
+template <bool MULTI>
+__global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
+  extern __shared__ int smem[];
+  __shared__ int s_tmp[33];
+  __shared__ int s_count;
+  __shared__ int s_fin;  // finished-node counter (single-CTA path)
+  const int n = a.n, maxc = a.maxc;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nthr = gridDim.x * blockDim.x;
+  unsigned epoch = 0;
+
+  // working arrays: shared memory on the single-CTA path, workspace otherwise
+  int *indeg, *hgt;
+  const int *ch;
+  if constexpr (MULTI) {
+    indeg = a.indeg;
+    hgt = a.hgt;
+    ch = a.ch;
+  } else {
+    indeg = smem;
+    hgt = smem + n;
+    int *chs = smem + 2 * n;
+    for (int i = threadIdx.x; i < maxc * n; i += blockDim.x) chs[i] = __ldg(a.ch + i);
+    ch = chs;
+  }
+
+  // ---- P0: init --------------------------------------------------------
+  for (int v = tid; v < n; v += nthr) {
+    indeg[v] = 0;
+    hgt[v] = -1;
+  }
+  int *fin_ptr = MULTI ? &a.misc[0] : &s_fin;
+  if (tid == 0) {
+    a.hdr->err_key = kNoError;
+    *fin_ptr = 0;
+  }
+  if (threadIdx.x == 0) {
+    s_count = 0;
+    s_tmp[32] = 0;
+  }
+  lsync<MULTI>(a.bar, epoch);
+
+  // ---- P1 (a1): validate, in-degree --------------------------------------
+  for (int v = tid; v < n; v += nthr) {
+    bool absent = false;
+    for (int k = 0; k < maxc; k++) {
+      int c = ch[k * n + v];
+      if (c == -1) {
+        absent = true;
+        continue;
+      }
+      if (absent) latch_error(a.hdr, CX_E_CHILD_LAYOUT, v);
+      if (c < 0 || c >= n) {
+        latch_error(a.hdr, CX_E_CHILD_RANGE, v);
+        continue;
+      }
+      atomicAdd(&indeg[c], 1);
+      for (int k2 = 0; k2 < k; k2++)
+        if (ch[k2 * n + v] == c) latch_error(a.hdr, CX_E_KIND, v);
+    }
+  }
+  lsync<MULTI>(a.bar, epoch);
+
+  // ---- P2: kind rule (in-degree <= 1 unless DAG), leaves at height 0 -----
+  {
+    int local = 0;
+    for (int v = tid; v < n; v += nthr) {
+      if (a.kind != CX_DAG && ld_dyn<MULTI>(&indeg[v]) > 1) latch_error(a.hdr, CX_E_KIND, v);
+      if (ch[v] == -1) {
+        hgt[v] = 0;
+        local++;
+      }
+    }
+    if (local) atomicAdd(&s_count, local);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_count) atomicAdd(fin_ptr, s_count);
+    if (threadIdx.x == 0) s_count = 0;
+  }
+  lsync<MULTI>(a.bar, epoch);
+  bool failed = __ldcg(reinterpret_cast<const unsigned long long *>(&a.hdr->err_key)) != kNoError;
+
+  // ---- P3 (a2): heights, one Jacobi round per level ----------------------
+  int L = 0;
+  if (!failed && n > 0) {
+    int fin_prev = ld_dyn<MULTI>(fin_ptr);
+    int r = 0;
+    while (fin_prev < n) {
+      r++;
+      int local = 0;
+      for (int v = tid; v < n; v += nthr) {
+        if (ld_dyn<MULTI>(&hgt[v]) >= 0) continue;
+        bool ok = true;
+        for (int k = 0; k < maxc; k++) {
+          int c = ch[k * n + v];
+          if (c == -1) break;
+          int hc = ld_dyn<MULTI>(&hgt[c]);
+          if (hc < 0 || hc >= r) {
+            ok = false;
+            break;
+          }
+        }
+        if (ok) {
+          hgt[v] = r;
+          local++;
+        }
+      }
+      if (local) atomicAdd(&s_count, local);
+      __syncthreads();
+      if (threadIdx.x == 0 && s_count) atomicAdd(fin_ptr, s_count);
+      __syncthreads();
+      if (threadIdx.x == 0) s_count = 0;
+      lsync<MULTI>(a.bar, epoch);
+      int fin = ld_dyn<MULTI>(fin_ptr);
+      if (fin == fin_prev) {  // no progress: a cycle (CX_E_CYCLE, lowest unfinished id)
+        for (int v = tid; v < n; v += nthr)
+          if (ld_dyn<MULTI>(&hgt[v]) < 0) latch_error(a.hdr, CX_E_CYCLE, v);
+        lsync<MULTI>(a.bar, epoch);
+        failed = true;
+        break;
+      }
+      fin_prev = fin;
+    }
+    L = r + 1;
+  }
+
+  if (!failed && n > 0) {
+    // ---- P4 (a3): per-(level, segment) counts + roots row -------------------
+    int seg = kSegMin, S = (n + seg - 1) / seg;
+    while ((long long)(L + 1) * S > a.budget) {
+      seg *= 2;
+      S = (n + seg - 1) / seg;
+    }
+    int *cnt = a.cnt;
+    if constexpr (!MULTI) {
+      if ((L + 1) * S <= kLinSmemCnt) cnt = smem + (maxc + 2) * n;
+    }
+    for (int e = tid; e < (L + 1) * S; e += nthr) cnt[e] = 0;
+    lsync<MULTI>(a.bar, epoch);
+
+    const int lane = threadIdx.x & 31;
+    const int gwarp = tid >> 5, nwarps = nthr >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int s = gwarp; s < S; s += nwarps) {
+      for (int base = s * seg; base < min(n, (s + 1) * seg); base += 32) {
+        int v = base + lane;
+        bool valid = v < n && v < (s + 1) * seg;
+        int hv = valid ? ld_dyn<MULTI>(&hgt[v]) : -1;
+        unsigned m = __match_any_sync(0xffffffffu, hv);
+        if (valid && (m & lt) == 0) cnt[hv * S + s] = ld_dyn<MULTI>(&cnt[hv * S + s]) + __popc(m);
+        unsigned rb = __ballot_sync(0xffffffffu, valid && ld_dyn<MULTI>(&indeg[v]) == 0);
+        if (lane == 0 && rb) cnt[L * S + s] = ld_dyn<MULTI>(&cnt[L * S + s]) + __popc(rb);
+        __syncwarp();
+      }
+    }
+    lsync<MULTI>(a.bar, epoch);
+
+    // ---- P5: scan (block 0): levels root-most first, then the roots row ---
+    if (blockIdx.x == 0) {
+      const int E = L * S;
+      const int per = (E + blockDim.x - 1) / blockDim.x;
+      const int e0 = threadIdx.x * per, e1 = min(E, e0 + per);
+      // entry e <-> (level L-1-e/S, segment e%S)
+      int sum = 0;
+      for (int e = e0; e < e1; e++) sum += ld_dyn<MULTI>(&cnt[(L - 1 - e / S) * S + e % S]);
+      int total;
+      int off = block_exclusive_scan(sum, total, s_tmp);
+      for (int e = e0; e < e1; e++) {
+        int idx = (L - 1 - e / S) * S + e % S;
+        int c = ld_dyn<MULTI>(&cnt[idx]);
+        cnt[idx] = off;
+        if (e % S == 0) a.lbeg[L - 1 - e / S] = off;
+        off += c;
+      }
+      // roots row
+      const int per2 = (S + blockDim.x - 1) / blockDim.x;
+      const int r0 = threadIdx.x * per2, r1 = min(S, r0 + per2);
+      int rs = 0;
+      for (int e = r0; e < r1; e++) rs += ld_dyn<MULTI>(&cnt[L * S + e]);
+      int rtotal;
+      int roff = block_exclusive_scan(rs, rtotal, s_tmp);
+      for (int e = r0; e < r1; e++) {
+        int c = ld_dyn<MULTI>(&cnt[L * S + e]);
+        cnt[L * S + e] = roff;
+        roff += c;
+      }
+      __syncthreads();
+      // level sizes and header
+      int mx = 0;
+      for (int l = threadIdx.x; l < L; l += blockDim.x) {
+        int b = ld_dyn<MULTI>(&a.lbeg[l]);
+        int e = l > 0 ? ld_dyn<MULTI>(&a.lbeg[l - 1]) : n;
+        a.lsize[l] = e - b;
+        mx = max(mx, e - b);
+      }
+      for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) atomicMax(&s_tmp[32], mx);
+      if (threadIdx.x == 0) {
+        a.hdr->num_levels = L;
+        a.hdr->num_roots = rtotal;
+      }
+      __syncthreads();
+      (void)total;
+    }
+    lsync<MULTI>(a.bar, epoch);
+
+    // ---- P6 (a4): stable scatter ------------------------------------------
+    for (int s = gwarp; s < S; s += nwarps) {
+      for (int base = s * seg; base < min(n, (s + 1) * seg); base += 32) {
+        int v = base + lane;
+        bool valid = v < n && v < (s + 1) * seg;
+        int hv = valid ? ld_dyn<MULTI>(&hgt[v]) : -1;
+        unsigned m = __match_any_sync(0xffffffffu, hv);
+        int leader = __ffs(m) - 1;
+        int b = 0;
+        if (valid && lane == leader) b = ld_dyn<MULTI>(&cnt[hv * S + s]);
+        b = __shfl_sync(0xffffffffu, b, leader);
+        int nid = b + __popc(m & lt);
+        if (valid && lane == leader) cnt[hv * S + s] = b + __popc(m);
+        bool isroot = valid && ld_dyn<MULTI>(&indeg[v]) == 0;
+        unsigned rb = __ballot_sync(0xffffffffu, isroot);
+        int rbase = 0;
+        if (lane == 0 && rb) rbase = ld_dyn<MULTI>(&cnt[L * S + s]);
+        rbase = __shfl_sync(0xffffffffu, rbase, 0);
+        if (valid) {
+          a.perm[nid] = v;
+          a.inv[v] = nid;
+          a.hnew[nid] = hv;
+          if (isroot) a.roots[rbase + __popc(rb & lt)] = nid;
+        }
+        if (lane == 0 && rb) cnt[L * S + s] = rbase + __popc(rb);
+        __syncwarp();
+      }
+    }
+    lsync<MULTI>(a.bar, epoch);
+
+    // ---- P7 (a5): remap children to new ids --------------------------------
+    for (int i = tid; i < n; i += nthr) {
+      int v = ld_dyn<MULTI>(&a.perm[i]);
+      for (int k = 0; k < maxc; k++) {
+        int c = ch[k * n + v];
+        a.chn[(long long)k * n + i] = c == -1 ? -1 : ld_dyn<MULTI>(&a.inv[c]);
+      }
+    }
+  }
+
+  // ---- finalize header (block 0 thread 0) ------------------------------
+  if (blockIdx.x == 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long key =
+          __ldcg(reinterpret_cast<const unsigned long long *>(&a.hdr->err_key));
+      a.hdr->num_nodes = n;
+      if (key != kNoError) {
+        a.hdr->status = (int)(key >> 32);
+        a.hdr->bad_node = (int)(key & 0xffffffffu);
+        a.hdr->num_levels = 0;
+      } else {
+        a.hdr->status = CX_OK;
+        a.hdr->bad_node = -1;
+        if (n == 0) {
+          a.hdr->num_levels = 0;
+          a.hdr->num_roots = 0;
+          a.hdr->num_leaves = 0;
+          a.hdr->first_leaf = 0;
+          a.hdr->max_level_size = 0;
+        } else {
+          int nl = ld_dyn<MULTI>(&a.lsize[0]);
+          a.hdr->num_leaves = nl;
+          a.hdr->first_leaf = n - nl;
+          a.hdr->max_level_size = s_tmp[32];
+        }
+      }
+    }
+  }
+  if constexpr (MULTI) grid_exit(a.bar, gridDim.x);
+}
+
+}  // namespace
+
+size_t lin_single_smem_bytes(int n, int maxc) {
+  return sizeof(int) * ((size_t)(maxc + 2) * n + kLinSmemCnt);
+}
+
+bool lin_use_single(int n, int maxc) {
+  return lin_single_smem_bytes(n, maxc) <= kLinSmemMax;
+}
+
+cudaError_t launch_linearize(const LinArgs &a, int num_sms, cudaStream_t stream) {
+  static bool attr_done = false;  // idempotent attribute set (benign race)
+  if (!attr_done) {
+    cudaFuncSetAttribute(lin_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kLinSmemMax);
+    attr_done = true;
+  }
+  if (lin_use_single(a.n, a.maxc)) {
+    size_t smem = lin_single_smem_bytes(a.n, a.maxc);
+    lin_kernel<false><<<1, kLinThreads, smem, stream>>>(a);
+    return cudaGetLastError();
+  }
+  LinArgs args = a;
+  void *params[] = {&args};
+  return cudaLaunchCooperativeKernel((const void *)lin_kernel<true>, dim3(num_sms),
+                                     dim3(kLinThreads), params, 0, stream);
+}
+
+}  // namespace cx

@@ -1,0 +1,234 @@
+"""Thin Python binding over libcx.so (include/cx.h). Argument marshalling only:
+every step of the hot path runs in the CUDA kernels behind the C ABI. torch
+supplies device memory and the current stream; nothing here computes.
+
+There is no CPU fallback: if libcx.so cannot be loaded (or built) the import
+of the binding raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from dataclasses import dataclass
+
+import torch
+
+from . import _build
+
+# --- enums mirrored from include/cx.h --------------------------------------
+SEQUENCE, TREE, DAG = 0, 1, 2
+TREERNN, TREEFC, TREELSTM, TREEGRU, MVRNN, DAGRNN = range(6)
+F32, BF16 = 0, 1
+OK, E_ARG, E_CHILD_RANGE, E_CHILD_LAYOUT, E_KIND, E_CYCLE, E_ARITY, E_WORD_RANGE, \
+    E_UNSUPPORTED, E_WORKSPACE, E_CUDA = range(11)
+
+CELL_IDS = {"treernn": TREERNN, "treefc": TREEFC, "treelstm": TREELSTM,
+            "treegru": TREEGRU, "mvrnn": MVRNN, "dagrnn": DAGRNN}
+N_WEIGHTS = {TREERNN: 0, TREEFC: 2, TREELSTM: 5, TREEGRU: 7, MVRNN: 4, DAGRNN: 3}
+HEADER_FIELDS = ("status", "bad_node", "num_nodes", "num_levels", "num_leaves", "first_leaf",
+                 "max_level_size", "num_roots")
+
+
+class CxError(RuntimeError):
+    def __init__(self, code, where, bad_node=-1):
+        self.code, self.bad_node = code, bad_node
+        super().__init__(f"{where}: {status_str(code)} (code {code}, node {bad_node})")
+
+
+class _Lin(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in (
+        "header", "perm", "inv", "children", "height", "level_begin", "level_size", "roots")] + [
+        ("n", ctypes.c_int32), ("max_children", ctypes.c_int32), ("kind", ctypes.c_int32)]
+
+
+class _Model(ctypes.Structure):
+    _fields_ = [("cell", ctypes.c_int32), ("hidden", ctypes.c_int32),
+                ("vocab", ctypes.c_int32), ("dtype", ctypes.c_int32)]
+
+
+class _Weights(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_void_p * 8)]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def lib():
+    """Load (building first if stale) the in-tree libcx.so. Raises if absent."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            path = _build.LIB
+            if _build.stale():
+                path = _build.build()
+            L = ctypes.CDLL(path)
+            P, I, S = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
+            L.cx_linearize_workspace_bytes.argtypes = [I, I]
+            L.cx_linearize_workspace_bytes.restype = S
+            L.cx_linearize.argtypes = [P, I, I, I, P, S, ctypes.POINTER(_Lin), P]
+            L.cx_linearize.restype = ctypes.c_int
+            L.cx_forward_workspace_bytes.argtypes = [ctypes.POINTER(_Model), I]
+            L.cx_forward_workspace_bytes.restype = S
+            L.cx_forward.argtypes = [ctypes.POINTER(_Model), ctypes.POINTER(_Weights), P, P,
+                                     ctypes.POINTER(_Lin), P, P, P, P, S, P]
+            L.cx_forward.restype = ctypes.c_int
+            L.cx_status_sync.argtypes = [ctypes.POINTER(_Lin), ctypes.POINTER(I), P]
+            L.cx_status_sync.restype = ctypes.c_int
+            L.cx_status_str.argtypes = [ctypes.c_int]
+            L.cx_status_str.restype = ctypes.c_char_p
+            L.cx_forward_launch_info.argtypes = [ctypes.POINTER(_Model), ctypes.POINTER(I),
+                                                 ctypes.POINTER(I), ctypes.POINTER(I)]
+            L.cx_forward_launch_info.restype = ctypes.c_int
+            _lib = L
+    return _lib
+
+
+def status_str(code: int) -> str:
+    return lib().cx_status_str(int(code)).decode()
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class _WorkspaceCache:
+    """Zero-filled workspaces, grown on demand, one per (device, role). The
+    kernels leave their synchronisation words zero, so reuse needs no memset."""
+
+    def __init__(self):
+        self._bufs = {}
+        self._lock = threading.Lock()
+
+    def get(self, device, role, nbytes):
+        key = (str(device), role)
+        with self._lock:
+            buf = self._bufs.get(key)
+            if buf is None or buf.numel() < nbytes:
+                buf = torch.zeros(max(nbytes, 1 << 12), dtype=torch.uint8, device=device)
+                self._bufs[key] = buf
+            return buf
+
+
+_ws = _WorkspaceCache()
+
+
+@dataclass
+class Linearization:
+    """Device tensors written by cx_linearize plus the C struct pointing at them."""
+    header: torch.Tensor      # int32[10] (cx_lin_header, 40 bytes)
+    perm: torch.Tensor
+    inv: torch.Tensor
+    children: torch.Tensor    # int32 [maxc, n]
+    height: torch.Tensor
+    level_begin: torch.Tensor
+    level_size: torch.Tensor
+    roots: torch.Tensor
+    n: int
+    max_children: int
+    kind: int
+    c: _Lin = None
+
+    def header_dict(self):
+        """Synchronising read of the header fields (host)."""
+        h = self.header.cpu().tolist()
+        return dict(zip(HEADER_FIELDS, h[:8]))
+
+
+def linearize(children: torch.Tensor, kind: int, stream=None, workspace=None) -> Linearization:
+    """cx_linearize on an int32 [max_children, n] CUDA tensor of input ids."""
+    if children.dim() != 2 or children.dtype != torch.int32 or not children.is_cuda:
+        raise ValueError("children must be an int32 CUDA tensor [max_children, n]")
+    children = children.contiguous()
+    maxc, n = children.shape
+    dev = children.device
+    size = max(n, 1)
+    mk = lambda *s: torch.empty(*s, dtype=torch.int32, device=dev)
+    lin = Linearization(header=torch.zeros(10, dtype=torch.int32, device=dev), perm=mk(size),
+                        inv=mk(size), children=mk(maxc, size), height=mk(size),
+                        level_begin=mk(size), level_size=mk(size), roots=mk(size), n=n,
+                        max_children=maxc, kind=kind)
+    c = _Lin()
+    for f in ("header", "perm", "inv", "children", "height", "level_begin", "level_size", "roots"):
+        setattr(c, f, getattr(lin, f).data_ptr())
+    lin.c = c
+    L = lib()
+    need = L.cx_linearize_workspace_bytes(n, maxc)
+    ws = workspace if workspace is not None else _ws.get(dev, "lin", need)
+    st = L.cx_linearize(_ptr(children), n, maxc, kind, _ptr(ws), ws.numel(), ctypes.byref(c),
+                        _stream(stream))
+    if st != OK:
+        raise CxError(st, "cx_linearize")
+    lin.children = lin.children[:, :n]
+    return lin
+
+
+def check(lin: Linearization, stream=None):
+    """cx_status_sync: synchronise and raise CxError if a data error was latched."""
+    bad = ctypes.c_int32(-1)
+    st = lib().cx_status_sync(ctypes.byref(lin.c), ctypes.byref(bad), _stream(stream))
+    if st != OK:
+        raise CxError(st, "device", bad.value)
+
+
+def status(lin: Linearization, stream=None):
+    bad = ctypes.c_int32(-1)
+    st = lib().cx_status_sync(ctypes.byref(lin.c), ctypes.byref(bad), _stream(stream))
+    return st, bad.value
+
+
+def _model(cell, hidden, vocab, dtype):
+    return _Model(cell=cell, hidden=hidden, vocab=vocab, dtype=dtype)
+
+
+def launch_info(cell, hidden, vocab=1, dtype=F32):
+    m = _model(cell, hidden, vocab, dtype)
+    a, b, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    st = lib().cx_forward_launch_info(ctypes.byref(m), ctypes.byref(a), ctypes.byref(b),
+                                      ctypes.byref(c))
+    if st != OK:
+        raise CxError(st, "cx_forward_launch_info")
+    return dict(ctas=a.value, threads=b.value, smem=c.value)
+
+
+def forward(cell: int, hidden: int, weights, emb: torch.Tensor, word_ids: torch.Tensor,
+            lin: Linearization, dtype: int = F32, want_aux: bool = False, num_roots=None,
+            h_out=None, aux_out=None, root_out=None, stream=None, workspace=None):
+    """cx_forward. Returns (h_out [n, H], aux or None, roots or None)."""
+    dev = emb.device
+    n = lin.n
+    vocab = emb.shape[0]
+    ws_list = list(weights)
+    if len(ws_list) != N_WEIGHTS[cell]:
+        raise ValueError(f"cell {cell} takes {N_WEIGHTS[cell]} weight tensors")
+    for w in ws_list:
+        if w.dtype != torch.float32 or not w.is_cuda or not w.is_contiguous():
+            raise ValueError("weights must be contiguous fp32 CUDA tensors")
+    if h_out is None:
+        h_out = torch.empty(max(n, 1), hidden, dtype=torch.float32, device=dev)[:n]
+    if want_aux and aux_out is None:
+        if cell == TREELSTM:
+            aux_out = torch.empty(n, hidden, dtype=torch.float32, device=dev)
+        elif cell == MVRNN:
+            aux_out = torch.empty(n, hidden, hidden, dtype=torch.float32, device=dev)
+    if num_roots is not None and root_out is None:
+        root_out = torch.empty(num_roots, hidden, dtype=torch.float32, device=dev)
+    m = _model(cell, hidden, vocab, dtype)
+    w = _Weights()
+    for i, t in enumerate(ws_list):
+        w.p[i] = t.data_ptr()
+    L = lib()
+    need = L.cx_forward_workspace_bytes(ctypes.byref(m), n)
+    ws = workspace if workspace is not None else _ws.get(dev, "fwd", need)
+    st = L.cx_forward(ctypes.byref(m), ctypes.byref(w), _ptr(emb), _ptr(word_ids),
+                      ctypes.byref(lin.c), _ptr(h_out), _ptr(aux_out), _ptr(root_out), _ptr(ws),
+                      ws.numel(), _stream(stream))
+    if st != OK:
+        raise CxError(st, "cx_forward")
+    return h_out, aux_out, root_out

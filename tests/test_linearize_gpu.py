@@ -1,0 +1,96 @@
+"""cx_linearize (CUDA) vs oracle.linearize: bit-exact on every output."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cx():
+    import paper_2011_01383_b200 as m
+    return m
+
+
+def _check(cx, ch, kind):
+    from gpu_helpers import assert_lin_equal, dev_i32, lin_to_numpy
+    lin = cx.linearize(dev_i32(ch), kind)
+    dev = lin_to_numpy(lin)
+    ref = oracle.linearize(ch, kind)
+    assert_lin_equal(dev, ref)
+    return dev
+
+
+def test_worked_examples(cx):
+    _check(cx, np.array([[1, -1, -1], [2, -1, -1]]), synth.TREE)
+    _check(cx, np.array([[1, 2, -1, -1, 5, -1, -1], [4, 3, -1, -1, 6, -1, -1]]), synth.TREE)
+
+
+def test_empty_and_single(cx):
+    d = _check(cx, np.zeros((2, 0), np.int32), synth.TREE)
+    assert d["num_levels"] == 0
+    d = _check(cx, np.full((2, 1), -1, np.int32), synth.TREE)
+    assert d["num_levels"] == 1 and d["first_leaf"] == 0
+
+
+def test_fuzz_1000(cx):
+    """>= 1000 random trees, forests, DAGs, chains (<= 200 nodes, ids shuffled)."""
+    count = 0
+    for seed in range(1000):
+        n = 1 + (seed * 37) % 200
+        r = seed % 4
+        if r == 0:
+            ch, kind = synth.random_dag(n, 1 + seed % 4, seed, p_edge=0.3), synth.DAG
+        elif r == 3:
+            ch, kind = synth.chains(1 + seed % 3, 1 + n // 3)[0], synth.SEQUENCE
+        else:
+            ch, kind = synth.random_forest(n, 1 + seed % 3, seed), synth.TREE
+        if seed % 2:
+            ch, _, _ = synth.shuffle_ids(ch, None, seed)
+        _check(cx, ch, kind)
+        count += 1
+    assert count == 1000
+
+
+@pytest.mark.parametrize("name", ["cfg1_treernn", "cfg2_treelstm_b10", "cfg3_treefc_b10",
+                                  "cfg5_dagrnn_b10", "cfg5_treelstm_b4096",
+                                  "cfg5_dagrnn_b4096"])
+def test_baseline_configs(cx, name):
+    w = synth.workload(name)
+    _check(cx, w["children"], w["kind"])
+
+
+def test_large_shuffled_forest(cx):
+    ch, _ = synth.sst_shaped_forest(600, 3)
+    ch, _, _ = synth.shuffle_ids(ch, None, 3)
+    _check(cx, ch, synth.TREE)
+
+
+@pytest.mark.parametrize("length,batch", [(10000, 1), (300, 40), (2500, 8)])
+def test_long_chains(cx, length, batch):
+    ch, _ = synth.chains(batch, length)
+    _check(cx, ch, synth.SEQUENCE)
+
+
+def test_error_cases_bit_exact(cx):
+    T, D, S = synth.TREE, synth.DAG, synth.SEQUENCE
+    cases = [
+        ([[1, 5, -1], [2, -1, -1]], T), ([[-7, -1]], S), ([[-1, -1, -1], [1, -1, -1]], T),
+        ([[2, 2, -1], [-1, -1, -1]], T), ([[2, 2, -1], [-1, -1, -1]], D),
+        ([[1, -1], [1, -1]], D), ([[1, 2, 1]], D), ([[-1, 2, 1]], D), ([[0]], D),
+        ([[-1, -1, 9], [1, -1, -1]], D), ([[1, 2, 1], [-1, -1, -1]], T),
+    ]
+    for ch, kind in cases:
+        _check(cx, np.array(ch, np.int32), kind)
+    # a large graph with a cycle deep inside (multi-CTA path)
+    ch, _ = synth.grid_dags(200, 10, 10)
+    ch = ch.copy()
+    ch[1, 12345] = 12399  # (123, 4, 5) -> (123, 9, 9): creates a cycle through the grid
+    _check(cx, ch, D)
+    # a large tree with two parents somewhere
+    ch2, _ = synth.sst_shaped_forest(400, 1)
+    ch2 = ch2.copy()
+    ch2[0, 9000] = 1  # node 1 (left child of root 0) gets a second parent
+    _check(cx, ch2, T)
