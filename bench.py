@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark of the Cortex hot path on B200.
+
+One step = cx_linearize + cx_forward over one batch of synthetic structures
+(the whole hot path, reading Q17 of DESIGN.md). Default workload =
+BASELINE.json configs[1]: TreeLSTM (child-sum, binary SST-shaped trees),
+batch 10 per GPU, H = 256, fp32. Multi-GPU: one process per GPU (torchrun),
+each rank evaluates its own independent batch (weak scaling, no data-path
+collective); timing is the max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
+    python bench.py --impl reference ...   # the CPU oracle on the host cores
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "TreeLSTM fwd latency µs (batch 10, H=256) and trees/s at 1/2/4/8 B200"
+UNIT = "trees/s"
+FMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4: SMs x FP32 lanes x 2 x max clock
+
+WORKLOADS = {
+    # name: (generator, cell, hidden, vocab, per-GPU batch or total batch, scaling)
+    "cfg2_treelstm_b10": ("sst", synth.TREELSTM, 256, 20000, 10, "weak"),
+    "cfg2_treelstm_b1": ("sst", synth.TREELSTM, 256, 20000, 1, "weak"),
+    "cfg3_treegru_b10": ("sst", synth.TREEGRU, 512, 20000, 10, "weak"),
+    "cfg3_treegru_b1": ("sst", synth.TREEGRU, 512, 20000, 1, "weak"),
+    "cfg3_treefc_b10": ("perfect7", synth.TREEFC, 512, 20000, 10, "weak"),
+    "cfg3_treefc_b1": ("perfect7", synth.TREEFC, 512, 20000, 1, "weak"),
+    "cfg4_mvrnn_b10": ("sst", synth.MVRNN, 64, 20000, 10, "weak"),
+    "cfg5_dagrnn_b10": ("grid", synth.DAGRNN, 256, 20000, 10, "weak"),
+    "cfg5_dagrnn_b1": ("grid", synth.DAGRNN, 256, 20000, 1, "weak"),
+    "cfg1_treernn": ("perfect3", synth.TREERNN, 8, 100, 1, "weak"),
+    # strong scaling: the batch is split across ranks
+    "cfg5_treelstm_b4096": ("sst", synth.TREELSTM, 256, 20000, 4096, "strong"),
+    "cfg5_dagrnn_b4096": ("grid", synth.DAGRNN, 256, 20000, 4096, "strong"),
+}
+
+
+# ---------------------------------------------------------------------------
+# inputs
+# ---------------------------------------------------------------------------
+def make_inputs(name, rank, world, seed=0):
+    gen, cell, H, V, batch, scaling = WORKLOADS[name]
+    total = batch * world if scaling == "weak" else batch
+    if gen == "sst":
+        ch, off = synth.sst_shaped_forest(total, seed)
+    elif gen == "perfect7":
+        ch, off = synth.perfect_forest(total, 7)
+    elif gen == "perfect3":
+        ch, off = synth.perfect_forest(total, 3)
+    else:
+        ch, off = synth.grid_dags(total)
+    kind = synth.DAG if gen == "grid" else synth.TREE
+    # this rank's contiguous block of structures, ids rebased to 0
+    per = total // world
+    g0, g1 = rank * per, (rank + 1) * per if rank < world - 1 else total
+    a, b = int(off[g0]), int(off[g1])
+    sub = ch[:, a:b].copy()
+    sub[sub >= 0] -= a
+    words = synth.word_ids(ch, V, seed, all_nodes=(cell == synth.DAGRNN))[a:b].copy()
+    emb = synth.embedding(V, H, seed)
+    ws = [w for _, w in synth.weights(cell, H, V)]
+    return dict(children=sub, kind=kind, words=words, emb=emb, weights=ws, cell=cell, H=H, V=V,
+                batch=g1 - g0, total=total, scaling=scaling, offsets=off[g0:g1 + 1] - a)
+
+
+def algorithmic_work(cell, H, n, n_leaves, n_internal, batch, maxc=2):
+    """Algorithmic flops and bytes per step."""
+    leaf_f = {synth.TREELSTM: 6 * H * H, synth.TREEGRU: 4 * H * H, synth.DAGRNN: 2 * H * H}.get(cell, 0)
+    int_f = {synth.TREERNN: H, synth.TREEFC: 4 * H * H, synth.TREELSTM: 10 * H * H,
+             synth.TREEGRU: 8 * H * H, synth.MVRNN: 4 * H ** 3 + 8 * H * H,
+             synth.DAGRNN: 2 * H * H}[cell]
+    flops = leaf_f * n_leaves + int_f * n_internal
+    if cell == synth.DAGRNN:
+        flops += 2 * H * H * n_internal  # every node has an input projection
+    emb_rows = n if cell == synth.DAGRNN else n_leaves
+    bytes_ = 4 * maxc * n + 4 * n + 4 * H * emb_rows + 4 * H * n  # children, words, Emb, h_out
+    if cell == synth.MVRNN:
+        bytes_ += 4 * H * H * n_leaves
+    return flops, bytes_
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML polling thread)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    BAD = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
+    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+             0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+             0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+             0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [v for k, v in self.NAMES.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU oracle on the host cores
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    name = args.workload
+    inp = make_inputs(name, 0, 1)
+    gen, cell, H, V, batch, scaling = WORKLOADS[name]
+    ch, off = inp["children"], inp["offsets"]
+    # bounded sample: at most `cap` structures per step (whole batch when small)
+    cap = 16 if batch > 64 else batch
+    a, b = 0, int(off[cap])
+    sub, words = ch[:, a:b], inp["words"][a:b]
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        lin = oracle.linearize(sub, inp["kind"])
+        st, _, _, _ = oracle.forward(cell, H, V, inp["weights"], inp["emb"], words, sub)
+        t1 = time.perf_counter()
+        assert lin["status"] == 0 and st == 0
+        if i >= args.warmup:
+            times.append(t1 - t0)
+    per = sum(times) / len(times)
+    value = cap / per
+    sample = f"{cap} of {batch} structures of {name} per step (oracle linearize + forward, fp64)"
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": name, "batch_per_step": cap, "hidden": H},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(name, seconds=12.0):
+    """The oracle as it stands, timed on one host core, on a bounded sample."""
+    import oracle
+    inp = make_inputs(name, 0, 1)
+    gen, cell, H, V, batch, _ = WORKLOADS[name]
+    cap = min(batch, 16)
+    b = int(inp["offsets"][cap])
+    sub, words = inp["children"][:, :b], inp["words"][:b]
+    done, t0 = 0, time.perf_counter()
+    while True:
+        lin = oracle.linearize(sub, inp["kind"])
+        oracle.forward(cell, H, V, inp["weights"], inp["emb"], words, sub)
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or (done >= 3 and el * (done + 1) / done > seconds * 1.5):
+            break
+    return {"value": done * cap / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{done} x {cap} structures of {name} in {el:.1f}s (fp64 naive recursion, 1 thread)"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2011_01383_b200 as cx
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    name = args.workload
+    inp = make_inputs(name, rank, world)
+    cell, H, V = inp["cell"], inp["H"], inp["V"]
+    ch_np = inp["children"]
+    n = ch_np.shape[1]
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a, dtype=dt)).to(dev)
+    children = t(ch_np, np.int32)
+    words = t(inp["words"], np.int32)
+    emb = t(inp["emb"], np.float32)
+    weights = [t(w, np.float32) for w in inp["weights"]]
+    R = inp["batch"]
+    stream = torch.cuda.current_stream()
+
+    # preallocated outputs (reused every step)
+    lin = cx.linearize(children, inp["kind"])
+    h, _, roots = cx.forward(cell, H, weights, emb, words, lin, num_roots=R)
+    cx.check(lin)
+    hdr = lin.header_dict()
+    L = hdr["num_levels"]
+    n_leaves = hdr["num_leaves"]
+
+    def step():
+        lin_ = cx.linearize(children, inp["kind"])
+        cx.forward(cell, H, weights, emb, words, lin_, h_out=h, root_out=roots)
+        return lin_
+
+    # L2 flush buffer (> 126 MB L2): written between timed steps, outside the events
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    for _ in range(args.warmup):
+        step()
+        flush.fill_(1.0)
+    torch.cuda.synchronize()
+
+    # timed region: K steps, per-step events (linearize | forward), flush between
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank)
+    with sampler:
+        for k in range(args.steps):
+            e0, e1, e2 = ev[k]
+            e0.record(stream)
+            lin_k = cx.linearize(children, inp["kind"])
+            e1.record(stream)
+            cx.forward(cell, H, weights, emb, words, lin_k, h_out=h, root_out=roots)
+            e2.record(stream)
+            flush.fill_(1.0)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    lin_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
+    fwd_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps)]
+    step_ms = [a + b for a, b in zip(lin_ms, fwd_ms)]
+    total_ms = sum(step_ms)
+    if world > 1:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+    trees_total = inp["batch"] * world if inp["scaling"] == "weak" else inp["total"]
+    value = trees_total / (ms_per_step / 1e3)
+
+    # ---- end to end through the public API with host buffers --------------
+    ch_host = torch.as_tensor(np.ascontiguousarray(ch_np, dtype=np.int32)).pin_memory()
+    w_host = torch.as_tensor(np.ascontiguousarray(inp["words"], dtype=np.int32)).pin_memory()
+    roots_host = torch.empty((R, H), dtype=torch.float32).pin_memory()
+    ch_dev = torch.empty_like(children)
+    w_dev = torch.empty_like(words)
+    e2e_steps = max(5, min(args.steps, 200))
+    for _ in range(3):
+        ch_dev.copy_(ch_host, non_blocking=True)
+        w_dev.copy_(w_host, non_blocking=True)
+        l2 = cx.linearize(ch_dev, inp["kind"])
+        cx.forward(cell, H, weights, emb, w_dev, l2, h_out=h, root_out=roots)
+        roots_host.copy_(roots, non_blocking=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2e_ms = []
+    for _ in range(e2e_steps):
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        ch_dev.copy_(ch_host, non_blocking=True)
+        w_dev.copy_(w_host, non_blocking=True)
+        l2 = cx.linearize(ch_dev, inp["kind"])
+        cx.forward(cell, H, weights, emb, w_dev, l2, h_out=h, root_out=roots)
+        roots_host.copy_(roots, non_blocking=True)
+        s1.record(stream)
+        s1.synchronize()  # the host reads the step's result
+        e2e_ms.append(s0.elapsed_time(s1))
+        flush.fill_(1.0)
+    torch.cuda.synchronize()
+    e2e_total = sum(e2e_ms)
+    if world > 1:
+        tt = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_total = float(tt.item())
+    e2e_value = trees_total / (e2e_total / e2e_steps / 1e3)
+    h2d = ch_host.numel() * 4 + w_host.numel() * 4
+    d2h = roots_host.numel() * 4
+
+    if rank != 0:
+        return
+    fwd_mean = sum(fwd_ms) / len(fwd_ms)
+    flops, alg_bytes = algorithmic_work(cell, H, n, n_leaves, n - n_leaves, R, ch_np.shape[0])
+    achieved = flops / (fwd_mean / 1e3) / 1e12
+    info = cx.launch_info(cell, H, V)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "forward_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(name)
+        except Exception:
+            traffic = None
+    clocks = sampler.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": inp["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": name, "cell": synth.CELL_NAMES[cell], "hidden": H, "vocab": V,
+                   "structures_per_gpu": R, "nodes_per_gpu": n, "levels": L,
+                   "parallelism": f"dp{world} (independent structures per rank)",
+                   "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+        "latency_us": statistics.median(step_ms) * 1e3,
+        "latency_p10_us": float(np.percentile(step_ms, 10)) * 1e3,
+        "latency_p90_us": float(np.percentile(step_ms, 90)) * 1e3,
+        "linearize_us": statistics.median(lin_ms) * 1e3,
+        "forward_us": statistics.median(fwd_ms) * 1e3,
+        "gpu_launches": 2 * args.steps,
+        "launch": info,
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": FMA_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": achieved / FMA_PEAK_TFLOPS, "traffic": traffic,
+                     "kernel": "fwd_kernel (cx_forward)", "flops_per_launch": flops,
+                     "alg_bytes_per_launch": alg_bytes,
+                     "note": "fp32 FMA peak = 148 SM x 128 lanes x 2 x 1.965 GHz; the step is "
+                             "critical-path (levels x barrier) bound, see DESIGN.md"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(name)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=500)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--workload", default="cfg2_treelstm_b10", choices=sorted(WORKLOADS))
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    args = p.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        print("bench.py: launch N>1 under torchrun (one process per GPU)", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

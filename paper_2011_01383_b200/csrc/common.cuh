@@ -38,7 +38,11 @@ __device__ __forceinline__ void grid_sync(GridBar *bar, unsigned nblocks, unsign
     const unsigned target = epoch * nblocks;
     __threadfence();
     red_release_add_u32(&bar->count, 1u);
+    // watchdog: a grid that is not co-resident would spin forever; trap
+    // (sticky launch error, reported as CX_E_CUDA) instead of hanging
+    unsigned long long spins = 0;
     while (ld_acquire_u32(&bar->count) < target) {
+      if (++spins > (1ull << 26)) __trap();
     }
     __threadfence();
   }

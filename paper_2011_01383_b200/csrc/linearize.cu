@@ -100,10 +100,15 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
     indeg[v] = 0;
     hgt[v] = -1;
   }
-  int *fin_ptr = MULTI ? &a.misc[0] : &s_fin;
+  // Finished-node counts. Multi-CTA: misc[3] counts leaves and round r adds
+  // into misc[r % 3]; a slot is read by every CTA right after barrier r and
+  // cleared (by CTA 0) only after barrier r + 1, so no CTA can observe another
+  // round's additions (which would desynchronise the round loop).
+  int *fin_ptr = MULTI ? &a.misc[3] : &s_fin;
   if (tid == 0) {
     a.hdr->err_key = kNoError;
     *fin_ptr = 0;
+    if constexpr (MULTI) a.misc[0] = a.misc[1] = a.misc[2] = 0;
   }
   if (threadIdx.x == 0) {
     s_count = 0;
@@ -157,6 +162,7 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
     int r = 0;
     while (fin_prev < n) {
       r++;
+      int *round_ptr = MULTI ? &a.misc[r % 3] : &s_fin;
       int local = 0;
       for (int v = tid; v < n; v += nthr) {
         if (ld_dyn<MULTI>(&hgt[v]) >= 0) continue;
@@ -177,11 +183,17 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
       }
       if (local) atomicAdd(&s_count, local);
       __syncthreads();
-      if (threadIdx.x == 0 && s_count) atomicAdd(fin_ptr, s_count);
+      if (threadIdx.x == 0 && s_count) atomicAdd(round_ptr, s_count);
       __syncthreads();
       if (threadIdx.x == 0) s_count = 0;
       lsync<MULTI>(a.bar, epoch);
-      int fin = ld_dyn<MULTI>(fin_ptr);
+      int fin;
+      if constexpr (MULTI) {
+        fin = fin_prev + ld_dyn<MULTI>(round_ptr);
+        if (tid == 0) a.misc[(r + 2) % 3] = 0;  // read by all before this barrier
+      } else {
+        fin = ld_dyn<MULTI>(fin_ptr);
+      }
       if (fin == fin_prev) {  // no progress: a cycle (CX_E_CYCLE, lowest unfinished id)
         for (int v = tid; v < n; v += nthr)
           if (ld_dyn<MULTI>(&hgt[v]) < 0) latch_error(a.hdr, CX_E_CYCLE, v);
