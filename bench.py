@@ -226,48 +226,61 @@ def run_gpu(args, rank, world, local_rank):
     R = inp["batch"]
     stream = torch.cuda.current_stream()
 
-    # preallocated outputs (reused every step)
-    lin = cx.linearize(children, inp["kind"])
-    h, _, roots = cx.forward(cell, H, weights, emb, words, lin, num_roots=R)
+    # preallocated outputs (reused every step; no allocation inside a step)
+    lin = cx.alloc_linearization(n, ch_np.shape[0], inp["kind"], dev)
+    h = torch.empty(n, H, dtype=torch.float32, device=dev)
+    roots = torch.empty(R, H, dtype=torch.float32, device=dev)
+    cx.linearize(children, inp["kind"], out=lin)
+    cx.forward(cell, H, weights, emb, words, lin, h_out=h, root_out=roots)
     cx.check(lin)
     hdr = lin.header_dict()
     L = hdr["num_levels"]
     n_leaves = hdr["num_leaves"]
 
+    def lin_call():
+        cx.linearize(children, inp["kind"], out=lin)
+
+    def fwd_call():
+        cx.forward(cell, H, weights, emb, words, lin, h_out=h, root_out=roots)
+
     def step():
-        lin_ = cx.linearize(children, inp["kind"])
-        cx.forward(cell, H, weights, emb, words, lin_, h_out=h, root_out=roots)
-        return lin_
+        lin_call()
+        fwd_call()
+
+    def capture(fn):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return g
+
+    # one step = one CUDA graph (2 kernel nodes); breakdown graphs for each call
+    g_step, g_lin, g_fwd = capture(step), capture(lin_call), capture(fwd_call)
+    stream = torch.cuda.current_stream()
 
     # L2 flush buffer (> 126 MB L2): written between timed steps, outside the events
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     for _ in range(args.warmup):
-        step()
+        g_step.replay()
         flush.fill_(1.0)
     torch.cuda.synchronize()
 
-    # timed region: K steps, per-step events (linearize | forward), flush between
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    # timed region: K graph replays, per-step events, flush between steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(local_rank)
     with sampler:
         for k in range(args.steps):
-            e0, e1, e2 = ev[k]
-            e0.record(stream)
-            lin_k = cx.linearize(children, inp["kind"])
-            e1.record(stream)
-            cx.forward(cell, H, weights, emb, words, lin_k, h_out=h, root_out=roots)
-            e2.record(stream)
+            ev[k][0].record(stream)
+            g_step.replay()
+            ev[k][1].record(stream)
             flush.fill_(1.0)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    lin_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
-    fwd_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps)]
-    step_ms = [a + b for a, b in zip(lin_ms, fwd_ms)]
+    step_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
     total_ms = sum(step_ms)
     if world > 1:
         tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -276,6 +289,33 @@ def run_gpu(args, rank, world, local_rank):
     ms_per_step = total_ms / args.steps
     trees_total = inp["batch"] * world if inp["scaling"] == "weak" else inp["total"]
     value = trees_total / (ms_per_step / 1e3)
+
+    # breakdown: linearize and forward graphs timed separately (same protocol)
+    nb = min(args.steps, 200)
+    evb = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(nb)]
+    for k in range(nb):
+        evb[k][0].record(stream)
+        g_lin.replay()
+        evb[k][1].record(stream)
+        g_fwd.replay()
+        evb[k][2].record(stream)
+        flush.fill_(1.0)
+    torch.cuda.synchronize()
+    lin_ms = [evb[k][0].elapsed_time(evb[k][1]) for k in range(nb)]
+    fwd_ms = [evb[k][1].elapsed_time(evb[k][2]) for k in range(nb)]
+
+    # eager (no graph) latency through the Python API, for reference
+    eager_ms = []
+    for k in range(min(args.steps, 100)):
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        step()
+        a1.record(stream)
+        flush.fill_(1.0)
+        eager_ms.append((a0, a1))
+    torch.cuda.synchronize()
+    eager_ms = [x.elapsed_time(y) for x, y in eager_ms]
 
     # ---- end to end through the public API with host buffers --------------
     ch_host = torch.as_tensor(np.ascontiguousarray(ch_np, dtype=np.int32)).pin_memory()
@@ -287,8 +327,8 @@ def run_gpu(args, rank, world, local_rank):
     for _ in range(3):
         ch_dev.copy_(ch_host, non_blocking=True)
         w_dev.copy_(w_host, non_blocking=True)
-        l2 = cx.linearize(ch_dev, inp["kind"])
-        cx.forward(cell, H, weights, emb, w_dev, l2, h_out=h, root_out=roots)
+        cx.linearize(ch_dev, inp["kind"], out=lin)
+        cx.forward(cell, H, weights, emb, w_dev, lin, h_out=h, root_out=roots)
         roots_host.copy_(roots, non_blocking=True)
     torch.cuda.synchronize()
     if world > 1:
@@ -300,8 +340,8 @@ def run_gpu(args, rank, world, local_rank):
         s0.record(stream)
         ch_dev.copy_(ch_host, non_blocking=True)
         w_dev.copy_(w_host, non_blocking=True)
-        l2 = cx.linearize(ch_dev, inp["kind"])
-        cx.forward(cell, H, weights, emb, w_dev, l2, h_out=h, root_out=roots)
+        cx.linearize(ch_dev, inp["kind"], out=lin)
+        cx.forward(cell, H, weights, emb, w_dev, lin, h_out=h, root_out=roots)
         roots_host.copy_(roots, non_blocking=True)
         s1.record(stream)
         s1.synchronize()  # the host reads the step's result
@@ -344,6 +384,8 @@ def run_gpu(args, rank, world, local_rank):
         "latency_p90_us": float(np.percentile(step_ms, 90)) * 1e3,
         "linearize_us": statistics.median(lin_ms) * 1e3,
         "forward_us": statistics.median(fwd_ms) * 1e3,
+        "eager_latency_us": statistics.median(eager_ms) * 1e3,
+        "timing": "CUDA graph replay of linearize+forward per step, events on the launch stream",
         "gpu_launches": 2 * args.steps,
         "launch": info,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FMA_PEAK_TFLOPS,

@@ -7,12 +7,12 @@ include/cx.h. See DESIGN.md.
     h, aux, roots = cx.forward(cx.TREELSTM, 256, weights, emb, words, lin, num_roots=10)
 """
 from .cx import (BF16, DAG, DAGRNN, F32, MVRNN, SEQUENCE, TREE, TREEFC, TREEGRU, TREELSTM,
-                 TREERNN, CELL_IDS, CxError, Linearization, check, forward, launch_info, lib,
+                 TREERNN, CELL_IDS, CxError, Linearization, alloc_linearization, check, forward, launch_info, lib,
                  linearize, status, status_str)
 from . import cx as _cx
 
 OK = _cx.OK
 
-__all__ = ["linearize", "forward", "check", "status", "status_str", "launch_info", "lib",
+__all__ = ["linearize", "alloc_linearization", "forward", "check", "status", "status_str", "launch_info", "lib",
            "Linearization", "CxError", "SEQUENCE", "TREE", "DAG", "TREERNN", "TREEFC",
            "TREELSTM", "TREEGRU", "MVRNN", "DAGRNN", "F32", "BF16", "CELL_IDS", "OK"]

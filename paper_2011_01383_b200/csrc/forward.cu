@@ -853,10 +853,21 @@ size_t fwd_workspace_bytes(int cell, int H, int n) {
   return b + 1024;
 }
 
+// Cooperative launch through cudaLaunchKernelEx so it can be captured into a
+// CUDA graph (the bench replays linearize + forward as one graph).
 cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream) {
   void *params[] = {&args};
-  return cudaLaunchCooperativeKernel(plan.kernel, dim3(plan.ctas), dim3(plan.threads), params,
-                                     plan.smem, stream);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(plan.ctas);
+  cfg.blockDim = dim3(plan.threads);
+  cfg.dynamicSmemBytes = plan.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, plan.kernel, params);
 }
 
 }  // namespace cx

@@ -382,8 +382,17 @@ cudaError_t launch_linearize(const LinArgs &a, int num_sms, cudaStream_t stream)
   }
   LinArgs args = a;
   void *params[] = {&args};
-  return cudaLaunchCooperativeKernel((const void *)lin_kernel<true>, dim3(num_sms),
-                                     dim3(kLinThreads), params, 0, stream);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_sms);
+  cfg.blockDim = dim3(kLinThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, (const void *)lin_kernel<true>, params);
 }
 
 }  // namespace cx

@@ -141,32 +141,45 @@ class Linearization:
         return dict(zip(HEADER_FIELDS, h[:8]))
 
 
-def linearize(children: torch.Tensor, kind: int, stream=None, workspace=None) -> Linearization:
-    """cx_linearize on an int32 [max_children, n] CUDA tensor of input ids."""
-    if children.dim() != 2 or children.dtype != torch.int32 or not children.is_cuda:
-        raise ValueError("children must be an int32 CUDA tensor [max_children, n]")
-    children = children.contiguous()
-    maxc, n = children.shape
-    dev = children.device
+def alloc_linearization(n: int, max_children: int, kind: int, device) -> Linearization:
+    """Allocate the output buffers of cx_linearize once (reusable via out=)."""
     size = max(n, 1)
-    mk = lambda *s: torch.empty(*s, dtype=torch.int32, device=dev)
-    lin = Linearization(header=torch.zeros(10, dtype=torch.int32, device=dev), perm=mk(size),
-                        inv=mk(size), children=mk(maxc, size), height=mk(size),
+    mk = lambda *s: torch.empty(*s, dtype=torch.int32, device=device)
+    lin = Linearization(header=torch.zeros(10, dtype=torch.int32, device=device), perm=mk(size),
+                        inv=mk(size), children=mk(max_children, size), height=mk(size),
                         level_begin=mk(size), level_size=mk(size), roots=mk(size), n=n,
-                        max_children=maxc, kind=kind)
+                        max_children=max_children, kind=kind)
     c = _Lin()
     for f in ("header", "perm", "inv", "children", "height", "level_begin", "level_size", "roots"):
         setattr(c, f, getattr(lin, f).data_ptr())
     lin.c = c
+    lin.children = lin.children[:, :n]
+    return lin
+
+
+def linearize(children: torch.Tensor, kind: int, stream=None, workspace=None,
+              out: Linearization = None) -> Linearization:
+    """cx_linearize on an int32 [max_children, n] CUDA tensor of input ids.
+    `out` (from alloc_linearization or a previous call) is reused without
+    allocating, which also makes the call CUDA-graph capturable."""
+    if children.dim() != 2 or children.dtype != torch.int32 or not children.is_cuda:
+        raise ValueError("children must be an int32 CUDA tensor [max_children, n]")
+    if not children.is_contiguous():
+        children = children.contiguous()
+    maxc, n = children.shape
+    if out is None:
+        out = alloc_linearization(n, maxc, kind, children.device)
+    elif (out.n, out.max_children) != (n, maxc):
+        raise ValueError("out was allocated for a different (n, max_children)")
+    out.kind = kind
     L = lib()
     need = L.cx_linearize_workspace_bytes(n, maxc)
-    ws = workspace if workspace is not None else _ws.get(dev, "lin", need)
-    st = L.cx_linearize(_ptr(children), n, maxc, kind, _ptr(ws), ws.numel(), ctypes.byref(c),
+    ws = workspace if workspace is not None else _ws.get(children.device, "lin", need)
+    st = L.cx_linearize(_ptr(children), n, maxc, kind, _ptr(ws), ws.numel(), ctypes.byref(out.c),
                         _stream(stream))
     if st != OK:
         raise CxError(st, "cx_linearize")
-    lin.children = lin.children[:, :n]
-    return lin
+    return out
 
 
 def check(lin: Linearization, stream=None):
