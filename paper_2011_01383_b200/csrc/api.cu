@@ -15,6 +15,8 @@
 namespace {
 
 std::mutex g_mu;  // guards the device-attribute cache and kernel attribute setup
+unsigned long long *g_trace = nullptr;  // debug only (cx_debug_set_trace)
+int g_trace_slots = 0;
 
 int num_sms_current() {
   static int cached_dev = -1, cached_sms = 0;
@@ -160,6 +162,11 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
   }
   a.Gn = Gn;
   a.Gu = Gu;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    a.trace = g_trace;
+    a.trace_slots = g_trace_slots;
+  }
   cudaError_t e = cx::fwd_launch(plan, a, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? CX_OK : CX_E_CUDA;
 }
@@ -173,6 +180,15 @@ cx_status cx_status_sync(const cx_linearization *lin, int32_t *bad_node, void *s
   if (cudaStreamSynchronize(s) != cudaSuccess) return CX_E_CUDA;
   if (bad_node) *bad_node = hv[1];
   return static_cast<cx_status>(hv[0]);
+}
+
+// Debug only (not part of include/cx.h): subsequent cx_forward launches record
+// %globaltimer per CTA into buf[cta * slots + s]; buf = NULL disables.
+cx_status cx_debug_set_trace(unsigned long long *buf, int32_t slots) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_trace = buf;
+  g_trace_slots = buf ? slots : 0;
+  return CX_OK;
 }
 
 const char *cx_status_str(cx_status s) {

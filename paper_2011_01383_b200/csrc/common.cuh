@@ -29,24 +29,40 @@ __device__ __forceinline__ void red_release_add_u32(unsigned *p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Grid-wide barrier for a co-resident (cooperatively launched) grid.
-// `epoch` is a per-CTA register counting barriers passed so far.
-__device__ __forceinline__ void grid_sync(GridBar *bar, unsigned nblocks, unsigned &epoch) {
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-wide barrier for a co-resident (cooperatively launched) grid, split in
+// two halves so a CTA can prefetch data that does not depend on the level
+// being completed while it waits. `epoch` counts barriers passed so far.
+// Arrive: bar.sync orders the CTA's writes before thread 0's red.release.gpu.
+// Wait: thread 0 polls with relaxed loads and finishes with one ld.acquire.gpu;
+// the trailing bar.sync publishes the acquire to the whole CTA. Data written
+// by other CTAs is then read with ld.global.cg (L2), never a stale L1 line.
+__device__ __forceinline__ void grid_arrive(GridBar *bar, unsigned &epoch) {
   __syncthreads();
   epoch += 1;
+  if (threadIdx.x == 0) red_release_add_u32(&bar->count, 1u);
+}
+__device__ __forceinline__ void grid_wait(GridBar *bar, unsigned nblocks, unsigned epoch) {
   if (threadIdx.x == 0) {
     const unsigned target = epoch * nblocks;
-    __threadfence();
-    red_release_add_u32(&bar->count, 1u);
     // watchdog: a grid that is not co-resident would spin forever; trap
     // (sticky launch error, reported as CX_E_CUDA) instead of hanging
     unsigned long long spins = 0;
-    while (ld_acquire_u32(&bar->count) < target) {
+    while (ld_relaxed_u32(&bar->count) < target) {
       if (++spins > (1ull << 26)) __trap();
     }
-    __threadfence();
+    (void)ld_acquire_u32(&bar->count);
   }
   __syncthreads();
+}
+__device__ __forceinline__ void grid_sync(GridBar *bar, unsigned nblocks, unsigned &epoch) {
+  grid_arrive(bar, epoch);
+  grid_wait(bar, nblocks, epoch);
 }
 
 // Called once by every CTA at kernel end: the last CTA out resets the words

@@ -245,13 +245,16 @@ struct GateSrc {
   int r0, ld, c0;
 };
 
-// Stage rows (units unit0..unit0+31) of NG gates into Ws with cp.async.
+// Stage rows (units unit0..unit0+31) of NG gates into Ws with cp.async:
+// warp w copies rows w, w+8, ..., lanes stride over the row's 16-byte chunks.
 __device__ void load_gates(float *Ws, const GateSrc *gs, int NG, int unit0, int H) {
-  const int HP = H + 4, q = H >> 2, per_gate = kUG * q;
-  for (int idx = threadIdx.x; idx < NG * per_gate; idx += blockDim.x) {
-    int g = idx / per_gate, rem = idx - g * per_gate, u = rem / q, c = rem - u * q;
-    const float *src = gs[g].base + (size_t)(gs[g].r0 + unit0 + u) * gs[g].ld + gs[g].c0 + 4 * c;
-    cp_async16(Ws + (size_t)(g * kUG + u) * HP + 4 * c, src);
+  const int HP = H + 4, q = H >> 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int row = warp; row < NG * kUG; row += kWarps) {
+    const int g = row >> 5, u = row & 31;
+    const float *src = gs[g].base + (size_t)(gs[g].r0 + unit0 + u) * gs[g].ld + gs[g].c0;
+    float *dst = Ws + (size_t)row * HP;
+    for (int c = lane; c < q; c += 32) cp_async16(dst + 4 * c, src + 4 * c);
   }
   cp_async_commit();
 }
@@ -330,9 +333,11 @@ __device__ __forceinline__ void tiles_T(int lo, int hi, F &f) {
 struct Ctx {
   const FwdArgs *a;
   float *Ws, *X, *cv;
+  const float *bias;  // shared memory [gate][32]: biases of the owned units
   TileMeta *m;
   int gn, gu, unit0, H;
   bool latch;  // only unit group 0 latches data errors (avoid duplicate atomics)
+  int tslot;   // debug trace: first trace slot of this level's first tile, -1 = off
 };
 
 // ----- TreeLSTM (Q1: child-sum, [Tai et al.]) -------------------------------
@@ -341,22 +346,27 @@ struct TreeLstm {
   static constexpr int kPhases = 1;
   struct Leaf {
     Ctx c;
+    int pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *c.m, i0, cnt, false, true, false, c.latch); }
     template <int T>
     __device__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
       const int H = c.H;
-      load_meta(a, *c.m, i0, cnt, false, true, false, c.latch);
-      __syncthreads();
+      if (i0 != pre) {
+        meta(i0, cnt);
+        __syncthreads();
+      }
       gather_rows(c.X, 1, H, cnt, [&](int t, int) { return a.emb + (size_t)c.m->word[t] * H; });
+      cp_async_wait_all();  // leaf weights (staged asynchronously at kernel start)
       __syncthreads();
       float acc[3][T], s[3];
       fma_engine<PhLstmLeaf, T>(c.Ws, c.X, H, acc);
       reduce_acc<3, T>(c.X, acc, s);
-      const int t = threadIdx.x >> 5, unit = c.unit0 + (threadIdx.x & 31);
+      const int lane = threadIdx.x & 31;
+      const int t = threadIdx.x >> 5, unit = c.unit0 + lane;
       if (t < cnt) {
-        const float *b = a.w[2];
-        float ig = s[0] + __ldg(b + unit), og = s[1] + __ldg(b + H + unit),
-              ug = s[2] + __ldg(b + 2 * H + unit);
+        float ig = s[0] + c.bias[0 * 32 + lane], og = s[1] + c.bias[1 * 32 + lane],
+              ug = s[2] + c.bias[2 * 32 + lane];
         float cc = sigmoidf_(ig) * tanhf(ug);
         float hh = sigmoidf_(og) * tanhf(cc);
         size_t o = (size_t)c.m->own[t] * H + unit;
@@ -368,14 +378,18 @@ struct TreeLstm {
   };
   struct Level {
     Ctx c;
-    int phase;
+    int phase, pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *c.m, i0, cnt, true, false, false, c.latch); }
     template <int T>
     __device__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
       const int H = c.H;
       const int lane = threadIdx.x & 31;
-      load_meta(a, *c.m, i0, cnt, true, false, false, c.latch);
-      __syncthreads();
+      if (i0 != pre) {
+        meta(i0, cnt);
+        __syncthreads();
+      }
+      if (c.tslot >= 0) trace_mark(a, c.tslot);
       gather_rows(c.X, MAXC, H, cnt, [&](int t, int j) {
         int ci = c.m->cin[t][j];
         return ci >= 0 ? a.h_out + (size_t)ci * H : (const float *)nullptr;
@@ -387,14 +401,16 @@ struct TreeLstm {
         c.cv[(t * kMaxC + k) * 32 + u] = ci >= 0 ? __ldcg(a.cbuf + (size_t)ci * H + c.unit0 + u) : 0.f;
       }
       __syncthreads();
+      if (c.tslot >= 0) trace_mark(a, c.tslot + 1);
       float acc[3 + MAXC][T], s[3 + MAXC];
       fma_engine<PhLstmLevel<MAXC>, T>(c.Ws, c.X, H, acc);
+      if (c.tslot >= 0) trace_mark(a, c.tslot + 2);
       reduce_acc<3 + MAXC, T>(c.X, acc, s);
+      if (c.tslot >= 0) trace_mark(a, c.tslot + 3);
       const int t = threadIdx.x >> 5, unit = c.unit0 + lane;
       if (t < cnt) {
-        const float *b = a.w[2], *bf = a.w[4];
-        float ig = s[0] + __ldg(b + unit), og = s[1] + __ldg(b + H + unit),
-              ug = s[2] + __ldg(b + 2 * H + unit), bfu = __ldg(bf + unit);
+        float ig = s[0] + c.bias[0 * 32 + lane], og = s[1] + c.bias[1 * 32 + lane],
+              ug = s[2] + c.bias[2 * 32 + lane], bfu = c.bias[3 * 32 + lane];
         float cc = sigmoidf_(ig) * tanhf(ug);
         const int nc = c.m->nch[t];
 #pragma unroll
@@ -406,8 +422,17 @@ struct TreeLstm {
         a.cbuf[o] = cc;
       }
       __syncthreads();
+      if (c.tslot >= 0) trace_mark(a, c.tslot + 4);
+      c.tslot = -1;
     }
   };
+  // biases [gate][unit]: b_i, b_o, b_u, b_f
+  __device__ static int biases(const FwdArgs &a, const float **b, int *off) {
+    b[0] = b[1] = b[2] = a.w[2];
+    off[0] = 0; off[1] = a.H; off[2] = 2 * a.H;
+    b[3] = a.w[4]; off[3] = 0;
+    return 4;
+  }
   __device__ static int leaf_lo(const FwdArgs &, int first_leaf) { return first_leaf; }
   __device__ static int leaf_gates(const FwdArgs &a, GateSrc *gs) {
     const int H = a.H;
@@ -432,21 +457,27 @@ struct TreeGru {
   static constexpr int kPhases = 2;
   struct Leaf {
     Ctx c;
+    int pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *c.m, i0, cnt, false, true, false, c.latch); }
     template <int T>
     __device__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
       const int H = c.H;
-      load_meta(a, *c.m, i0, cnt, false, true, false, c.latch);
-      __syncthreads();
+      if (i0 != pre) {
+        meta(i0, cnt);
+        __syncthreads();
+      }
       gather_rows(c.X, 1, H, cnt, [&](int t, int) { return a.emb + (size_t)c.m->word[t] * H; });
+      cp_async_wait_all();
       __syncthreads();
       float acc[2][T], s[2];
       fma_engine<PhGruLeaf, T>(c.Ws, c.X, H, acc);
       reduce_acc<2, T>(c.X, acc, s);
-      const int t = threadIdx.x >> 5, unit = c.unit0 + (threadIdx.x & 31);
+      const int lane = threadIdx.x & 31;
+      const int t = threadIdx.x >> 5, unit = c.unit0 + lane;
       if (t < cnt) {
-        float z = sigmoidf_(s[0] + __ldg(a.w[4] + unit));
-        float g = tanhf(s[1] + __ldg(a.w[6] + unit));
+        float z = sigmoidf_(s[0] + c.bias[0 * 32 + lane]);
+        float g = tanhf(s[1] + c.bias[2 * 32 + lane]);
         a.h_out[(size_t)c.m->own[t] * H + unit] = (1.f - z) * g;
       }
       __syncthreads();
@@ -454,16 +485,22 @@ struct TreeGru {
   };
   struct Level {
     Ctx c;
-    int phase;
+    int phase, pre;
+    __device__ void meta(int i0, int cnt) {
+      if (phase == 0) load_meta(*c.a, *c.m, i0, cnt, true, false, false, c.latch);
+      else load_meta(*c.a, *c.m, i0, cnt, false, false, false, false);
+    }
     template <int T>
     __device__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
       const int H = c.H;
       const int lane = threadIdx.x & 31;
       const int t = threadIdx.x >> 5, unit = c.unit0 + lane;
-      if (phase == 0) {
-        load_meta(a, *c.m, i0, cnt, true, false, false, c.latch);
+      if (i0 != pre) {
+        meta(i0, cnt);
         __syncthreads();
+      }
+      if (phase == 0) {
         gather_rows(c.X, MAXC, H, cnt, [&](int tt, int j) {
           int ci = c.m->cin[tt][j];
           return ci >= 0 ? a.h_out + (size_t)ci * H : (const float *)nullptr;
@@ -478,8 +515,8 @@ struct TreeGru {
         fma_engine<PhGruA<MAXC>, T>(c.Ws, c.X, H, acc);
         reduce_acc<1 + MAXC, T>(c.X, acc, s);
         if (t < cnt) {
-          float z = sigmoidf_(s[0] + __ldg(a.w[4] + unit));
-          float br = __ldg(a.w[5] + unit);
+          float z = sigmoidf_(s[0] + c.bias[0 * 32 + lane]);
+          float br = c.bias[1 * 32 + lane];
           float sum = 0.f, ht = 0.f;
           const int nc = c.m->nch[t];
 #pragma unroll
@@ -496,8 +533,6 @@ struct TreeGru {
         }
         __syncthreads();
       } else {
-        load_meta(a, *c.m, i0, cnt, false, false, false, false);
-        __syncthreads();
         gather_rows(c.X, 1, H, cnt, [&](int tt, int) { return a.sbuf + (size_t)c.m->own[tt] * H; });
         __syncthreads();
         float acc[1][T], s[1];
@@ -505,7 +540,7 @@ struct TreeGru {
         reduce_acc<1, T>(c.X, acc, s);
         if (t < cnt) {
           size_t o = (size_t)c.m->own[t] * H + unit;
-          float g = tanhf(s[0] + __ldg(a.w[6] + unit));
+          float g = tanhf(s[0] + c.bias[2 * 32 + lane]);
           float z = __ldcg(a.zbuf + o), ht = __ldcg(a.h_out + o);
           a.h_out[o] = z * ht + (1.f - z) * g;
         }
@@ -513,6 +548,11 @@ struct TreeGru {
       }
     }
   };
+  __device__ static int biases(const FwdArgs &a, const float **b, int *off) {
+    b[0] = a.w[4]; b[1] = a.w[5]; b[2] = a.w[6];
+    off[0] = off[1] = off[2] = 0;
+    return 3;
+  }
   __device__ static int leaf_lo(const FwdArgs &, int first_leaf) { return first_leaf; }
   __device__ static int leaf_gates(const FwdArgs &a, GateSrc *gs) {
     gs[0] = {a.w[0], 0, a.H, 0};
@@ -533,11 +573,15 @@ struct TreeFc {
   static constexpr int kPhases = 1;
   struct Leaf {  // pure gather (no weights): h = x
     Ctx c;
+    int pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *c.m, i0, cnt, false, true, false, c.latch); }
     template <int T>
     __device__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
-      load_meta(a, *c.m, i0, cnt, false, true, false, c.latch);
-      __syncthreads();
+      if (i0 != pre) {
+        meta(i0, cnt);
+        __syncthreads();
+      }
       const int t = threadIdx.x >> 5, unit = c.unit0 + (threadIdx.x & 31);
       if (t < cnt)
         a.h_out[(size_t)c.m->own[t] * c.H + unit] = __ldg(a.emb + (size_t)c.m->word[t] * c.H + unit);
@@ -546,23 +590,31 @@ struct TreeFc {
   };
   struct Level {
     Ctx c;
-    int phase;
+    int phase, pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *c.m, i0, cnt, true, false, true, c.latch); }
     template <int T>
     __device__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
       const int H = c.H;
-      load_meta(a, *c.m, i0, cnt, true, false, true, c.latch);
-      __syncthreads();
+      if (i0 != pre) {
+        meta(i0, cnt);
+        __syncthreads();
+      }
       gather_rows(c.X, 2, H, cnt, [&](int t, int j) { return a.h_out + (size_t)c.m->cin[t][j] * H; });
       __syncthreads();
       float acc[1][T], s[1];
       fma_engine<PhFcLevel, T>(c.Ws, c.X, H, acc);
       reduce_acc<1, T>(c.X, acc, s);
       const int t = threadIdx.x >> 5, unit = c.unit0 + (threadIdx.x & 31);
-      if (t < cnt) a.h_out[(size_t)c.m->own[t] * H + unit] = tanhf(s[0] + __ldg(a.w[1] + unit));
+      if (t < cnt) a.h_out[(size_t)c.m->own[t] * H + unit] = tanhf(s[0] + c.bias[threadIdx.x & 31]);
       __syncthreads();
     }
   };
+  __device__ static int biases(const FwdArgs &a, const float **b, int *off) {
+    b[0] = a.w[1];
+    off[0] = 0;
+    return 1;
+  }
   __device__ static int leaf_lo(const FwdArgs &, int first_leaf) { return first_leaf; }
   __device__ static int leaf_gates(const FwdArgs &, GateSrc *) { return 0; }
   __device__ static int level_gates(const FwdArgs &a, GateSrc *gs) {
@@ -580,20 +632,25 @@ struct DagRnn {
   // start); leaves finish here.
   struct Leaf {
     Ctx c;
+    int pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *c.m, i0, cnt, false, true, false, c.latch); }
     template <int T>
     __device__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
       const int H = c.H;
-      load_meta(a, *c.m, i0, cnt, false, true, false, c.latch);
-      __syncthreads();
+      if (i0 != pre) {
+        meta(i0, cnt);
+        __syncthreads();
+      }
       gather_rows(c.X, 1, H, cnt, [&](int t, int) { return a.emb + (size_t)c.m->word[t] * H; });
+      cp_async_wait_all();
       __syncthreads();
       float acc[1][T], s[1];
       fma_engine<PhDagProj, T>(c.Ws, c.X, H, acc);
       reduce_acc<1, T>(c.X, acc, s);
       const int t = threadIdx.x >> 5, unit = c.unit0 + (threadIdx.x & 31);
       if (t < cnt) {
-        float p = s[0] + __ldg(a.w[2] + unit);
+        float p = s[0] + c.bias[threadIdx.x & 31];
         size_t o = (size_t)c.m->own[t] * H + unit;
         a.pbuf[o] = p;
         if (i0 + t >= a.hdr->first_leaf) a.h_out[o] = tanhf(p);
@@ -603,14 +660,17 @@ struct DagRnn {
   };
   struct Level {
     Ctx c;
-    int phase;
+    int phase, pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *c.m, i0, cnt, true, false, false, c.latch); }
     template <int T>
     __device__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
       const int H = c.H;
       const int lane = threadIdx.x & 31;
-      load_meta(a, *c.m, i0, cnt, true, false, false, c.latch);
-      __syncthreads();
+      if (i0 != pre) {
+        meta(i0, cnt);
+        __syncthreads();
+      }
       gather_rows(c.X, MAXC, H, cnt, [&](int t, int j) {
         int ci = c.m->cin[t][j];
         return ci >= 0 ? a.h_out + (size_t)ci * H : (const float *)nullptr;
@@ -626,6 +686,11 @@ struct DagRnn {
       __syncthreads();
     }
   };
+  __device__ static int biases(const FwdArgs &a, const float **b, int *off) {
+    b[0] = a.w[2];
+    off[0] = 0;
+    return 1;
+  }
   __device__ static int leaf_lo(const FwdArgs &, int) { return 0; }
   __device__ static int leaf_gates(const FwdArgs &a, GateSrc *gs) {
     gs[0] = {a.w[0], 0, a.H, 0};
@@ -643,11 +708,15 @@ struct TreeRnn {
   static constexpr int kPhases = 1;
   struct Leaf {
     Ctx c;
+    int pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *c.m, i0, cnt, false, true, false, c.latch); }
     template <int T>
     __device__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
-      load_meta(a, *c.m, i0, cnt, false, true, false, c.latch);
-      __syncthreads();
+      if (i0 != pre) {
+        meta(i0, cnt);
+        __syncthreads();
+      }
       const int ug = min(kUG, c.H);
       for (int idx = threadIdx.x; idx < cnt * ug; idx += blockDim.x) {
         int t = idx / ug, unit = c.unit0 + idx % ug;
@@ -658,12 +727,15 @@ struct TreeRnn {
   };
   struct Level {
     Ctx c;
-    int phase;
+    int phase, pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *c.m, i0, cnt, true, false, true, c.latch); }
     template <int T>
     __device__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
-      load_meta(a, *c.m, i0, cnt, true, false, true, c.latch);
-      __syncthreads();
+      if (i0 != pre) {
+        meta(i0, cnt);
+        __syncthreads();
+      }
       const int ug = min(kUG, c.H);
       for (int idx = threadIdx.x; idx < cnt * ug; idx += blockDim.x) {
         int t = idx / ug, unit = c.unit0 + idx % ug;
@@ -674,6 +746,7 @@ struct TreeRnn {
       __syncthreads();
     }
   };
+  __device__ static int biases(const FwdArgs &, const float **, int *) { return 0; }
   __device__ static int leaf_lo(const FwdArgs &, int first_leaf) { return first_leaf; }
   __device__ static int leaf_gates(const FwdArgs &, GateSrc *) { return 0; }
   __device__ static int level_gates(const FwdArgs &, GateSrc *) { return 0; }
@@ -706,44 +779,74 @@ __global__ void __launch_bounds__(kFwdThreads, 1) fwd_kernel(FwdArgs a) {
   ctx.unit0 = gu * min(kUG, H);
   ctx.H = H;
   ctx.latch = gu == 0;
+  ctx.tslot = -1;
   unsigned epoch = 0;
+  trace_mark(a, 0);
+
+  // biases of the owned units -> shared memory (read by every epilogue)
+  __shared__ float s_bias[4 * kUG];
+  {
+    const float *bp[4];
+    int off[4];
+    int nb = C::biases(a, bp, off);
+    const int ug = min(kUG, H);
+    if (threadIdx.x < nb * kUG) {
+      int g = threadIdx.x / kUG, u = threadIdx.x % kUG;
+      s_bias[threadIdx.x] = u < ug ? __ldg(bp[g] + off[g] + ctx.unit0 + u) : 0.f;
+    }
+  }
+  ctx.bias = s_bias;
 
   // ---- leaf phase (specialised leaf loop nest) ------------------
+  // The leaf weights are staged with cp.async; the first tile's bookkeeping and
+  // Emb gather overlap the copy (each leaf tile waits for it before its FMA).
   {
     int ng = C::leaf_gates(a, gsrc);
-    if (ng) {
-      load_gates(ctx.Ws, gsrc, ng, ctx.unit0, H);
-      cp_async_wait_all();
-    }
+    if (ng) load_gates(ctx.Ws, gsrc, ng, ctx.unit0, H);
     __syncthreads();
+    trace_mark(a, 1);
     int lo0 = C::leaf_lo(a, first_leaf);
     int lo, hi;
     chunk_of(n - lo0, a.Gn, gn, lo, hi);
-    typename C::Leaf f{ctx};
+    typename C::Leaf f{ctx, -1};
     tiles_T<Tr::TMAX>(lo0 + lo, lo0 + hi, f);
+    cp_async_wait_all();
   }
   __syncthreads();
+  trace_mark(a, 2);
   // recurrent weights: issued now, landed while the CTA waits at the barrier
   {
     int ng = C::level_gates(a, gsrc);
     if (ng) load_gates(ctx.Ws, gsrc, ng, ctx.unit0, H);
   }
   // ---- internal batches, one grid barrier per level (and phase) -----------
+  // While waiting at a barrier the CTA already loads the bookkeeping of its
+  // first tile of the next level (it depends only on the linearization).
   for (int l = 1; l < L; l++) {
     const int base = __ldg(a.lbeg + l), M = __ldg(a.lsize + l);
     int lo, hi;
     chunk_of(M, a.Gn, gn, lo, hi);
     for (int ph = 0; ph < C::kPhases; ph++) {
-      grid_sync(a.bar, gridDim.x, epoch);
+      const int slot = 3 + 2 * ((l - 1) * C::kPhases + ph);
+      trace_mark(a, slot);
+      grid_arrive(a.bar, epoch);
+      typename C::Level f{ctx, ph, -1};
+      if (hi > lo) {
+        f.meta(base + lo, min(Tr::TMAX, hi - lo));
+        f.pre = base + lo;
+      }
+      grid_wait(a.bar, gridDim.x, epoch);
+      trace_mark(a, slot + 1);
       if (l == 1 && ph == 0) {
         cp_async_wait_all();
         __syncthreads();
       }
-      typename C::Level f{ctx, ph};
+      f.c.tslot = a.trace ? 64 + 5 * ((l - 1) * C::kPhases + ph) : -1;
       tiles_T<Tr::TMAX>(base + lo, base + hi, f);
     }
   }
   cp_async_wait_all();
+  trace_mark(a, a.trace_slots - 2);
 
   // ---- packed root states: each CTA copies the rows it wrote itself --------
   if (a.root_out) {
@@ -765,6 +868,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) fwd_kernel(FwdArgs a) {
 
   // ---- the last CTA out publishes the latched status -----------------------
   __syncthreads();
+  trace_mark(a, a.trace_slots - 1);
   if (threadIdx.x == 0) {
     __threadfence();
     unsigned prev = atomicAdd(&a.bar->exit, 1u);

@@ -27,7 +27,18 @@ struct FwdArgs {
   float *Abuf;  // MV-RNN matrices [n][H][H] (aux_out or workspace)
   GridBar *bar;
   int Gn, Gu;   // node groups x unit groups = CTAs
+  unsigned long long *trace;  // debug: %globaltimer per CTA and phase (cx_debug_set_trace)
+  int trace_slots;
 };
+
+// thread 0 of each CTA records %globaltimer into slot `s` (debug builds of a run only)
+__device__ __forceinline__ void trace_mark(const FwdArgs &a, int s) {
+  if (a.trace && threadIdx.x == 0 && s < a.trace_slots) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[(size_t)blockIdx.x * a.trace_slots + s] = t;
+  }
+}
 
 struct FwdPlan {
   int ctas, threads;

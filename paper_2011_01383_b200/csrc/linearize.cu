@@ -358,10 +358,248 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
   if constexpr (MULTI) grid_exit(a.bar, gridDim.x);
 }
 
+
+// ---------------------------------------------------------------------------
+// Single-CTA linearizer: every working array lives in shared memory; the only
+// global traffic is one coalesced read of `children` and fire-and-forget
+// stores of the outputs (no dependent global round trips on the latency path).
+// smem (ints): ch[maxc*n] | hgt[n] | indeg[n] | perm[n] | inv[n] | lb[n] | cnt[kLinSmemCnt]
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kLinThreads, 1) lin_single_kernel(LinArgs a) {
+  extern __shared__ int sm[];
+  __shared__ unsigned long long s_err;
+  __shared__ int s_tmp[33];
+  __shared__ int s_count, s_fin, s_round;
+  const int n = a.n, maxc = a.maxc, tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  int *ch = sm, *hgt = ch + maxc * n, *indeg = hgt + n, *perm = indeg + n, *inv = perm + n,
+      *lb = inv + n, *cnt_s = lb + n;
+
+  for (int i = tid; i < maxc * n; i += nthr) ch[i] = __ldg(a.ch + i);
+  for (int v = tid; v < n; v += nthr) {
+    indeg[v] = 0;
+    hgt[v] = -1;
+  }
+  if (tid == 0) {
+    s_err = kNoError;
+    s_fin = 0;
+    s_count = 0;
+    s_tmp[32] = 0;
+  }
+  __syncthreads();
+
+  // a1: validation + in-degree; errors latched in shared memory (lowest key)
+  auto latch = [&](int code, int v) {
+    atomicMin(&s_err, ((unsigned long long)(unsigned)code << 32) | (unsigned)v);
+  };
+  for (int v = tid; v < n; v += nthr) {
+    bool absent = false;
+    for (int k = 0; k < maxc; k++) {
+      int c = ch[k * n + v];
+      if (c == -1) {
+        absent = true;
+        continue;
+      }
+      if (absent) latch(CX_E_CHILD_LAYOUT, v);
+      if (c < 0 || c >= n) {
+        latch(CX_E_CHILD_RANGE, v);
+        continue;
+      }
+      atomicAdd(&indeg[c], 1);
+      for (int k2 = 0; k2 < k; k2++)
+        if (ch[k2 * n + v] == c) latch(CX_E_KIND, v);
+    }
+  }
+  __syncthreads();
+  {
+    int local = 0;
+    for (int v = tid; v < n; v += nthr) {
+      if (a.kind != CX_DAG && indeg[v] > 1) latch(CX_E_KIND, v);
+      if (ch[v] == -1) {
+        hgt[v] = 0;
+        local++;
+      }
+    }
+    if (local) atomicAdd(&s_fin, local);
+  }
+  __syncthreads();
+  bool failed = s_err != kNoError;
+
+  // a2: heights, one round per level (round r finalises the nodes of height r)
+  int L = 0;
+  if (!failed && n > 0) {
+    int r = 0;
+    int fin = s_fin;
+    while (fin < n) {
+      r++;
+      int local = 0;
+      for (int v = tid; v < n; v += nthr) {
+        if (hgt[v] >= 0) continue;
+        bool ok = true;
+        for (int k = 0; k < maxc; k++) {
+          int c = ch[k * n + v];
+          if (c == -1) break;
+          int hc = hgt[c];
+          if (hc < 0 || hc >= r) {
+            ok = false;
+            break;
+          }
+        }
+        if (ok) {
+          hgt[v] = r;
+          local++;
+        }
+      }
+      if (tid == 0) s_round = 0;
+      __syncthreads();
+      if (local) atomicAdd(&s_round, local);
+      __syncthreads();
+      int got = s_round;
+      __syncthreads();
+      if (got == 0) {
+        for (int v = tid; v < n; v += nthr)
+          if (hgt[v] < 0) latch(CX_E_CYCLE, v);
+        __syncthreads();
+        failed = true;
+        break;
+      }
+      fin += got;
+    }
+    L = r + 1;
+  }
+
+  if (!failed && n > 0) {
+    // a3: one id segment per warp; counts per (level, segment) + roots row
+    const int seg = 32 * ((((n + 31) / 32) + 31) / 32);
+    const int S = (n + seg - 1) / seg;
+    int *cnt = (long long)(L + 1) * S <= kLinSmemCnt ? cnt_s : a.cnt;
+    for (int e = tid; e < (L + 1) * S; e += nthr) cnt[e] = 0;
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    if (warp < S) {
+      const int s = warp, end = min(n, (s + 1) * seg);
+      for (int base = s * seg; base < end; base += 32) {
+        int v = base + lane;
+        bool valid = v < end;
+        int hv = valid ? hgt[v] : -1;
+        unsigned m = __match_any_sync(0xffffffffu, hv);
+        if (valid && (m & lt) == 0) cnt[hv * S + s] += __popc(m);
+        unsigned rb = __ballot_sync(0xffffffffu, valid && indeg[v] == 0);
+        if (lane == 0 && rb) cnt[L * S + s] += __popc(rb);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // exclusive scan over (level L-1 .. 0) x (segment), then over the roots row
+    {
+      const int E = L * S;
+      const int per = (E + nthr - 1) / nthr;
+      const int e0 = tid * per, e1 = min(E, e0 + per);
+      int sum = 0;
+      for (int e = e0; e < e1; e++) sum += cnt[(L - 1 - e / S) * S + e % S];
+      int total;
+      int off = block_exclusive_scan(sum, total, s_tmp);
+      for (int e = e0; e < e1; e++) {
+        int idx = (L - 1 - e / S) * S + e % S;
+        int c = cnt[idx];
+        cnt[idx] = off;
+        if (e % S == 0) lb[L - 1 - e / S] = off;
+        off += c;
+      }
+      const int per2 = (S + nthr - 1) / nthr;
+      const int r0 = tid * per2, r1 = min(S, r0 + per2);
+      int rs = 0;
+      for (int e = r0; e < r1; e++) rs += cnt[L * S + e];
+      int rtotal;
+      int roff = block_exclusive_scan(rs, rtotal, s_tmp);
+      for (int e = r0; e < r1; e++) {
+        int c = cnt[L * S + e];
+        cnt[L * S + e] = roff;
+        roff += c;
+      }
+      if (tid == 0) s_count = rtotal;
+    }
+    __syncthreads();
+    {
+      int mx = 0;
+      for (int l = tid; l < L; l += nthr) {
+        int b = lb[l], e = l > 0 ? lb[l - 1] : n;
+        a.lbeg[l] = b;
+        a.lsize[l] = e - b;
+        mx = max(mx, e - b);
+      }
+      for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) atomicMax(&s_tmp[32], mx);
+    }
+    // a4: stable scatter (each warp walks its segment in id order)
+    if (warp < S) {
+      const int s = warp, end = min(n, (s + 1) * seg);
+      for (int base = s * seg; base < end; base += 32) {
+        int v = base + lane;
+        bool valid = v < end;
+        int hv = valid ? hgt[v] : -1;
+        unsigned m = __match_any_sync(0xffffffffu, hv);
+        int leader = __ffs(m) - 1;
+        int b = (valid && lane == leader) ? cnt[hv * S + s] : 0;
+        b = __shfl_sync(0xffffffffu, b, leader);
+        int nid = b + __popc(m & lt);
+        bool isroot = valid && indeg[v] == 0;
+        unsigned rb = __ballot_sync(0xffffffffu, isroot);
+        int rbase = (lane == 0 && rb) ? cnt[L * S + s] : 0;
+        rbase = __shfl_sync(0xffffffffu, rbase, 0);
+        __syncwarp();
+        if (valid && lane == leader) cnt[hv * S + s] = b + __popc(m);
+        if (lane == 0 && rb) cnt[L * S + s] = rbase + __popc(rb);
+        if (valid) {
+          perm[nid] = v;
+          inv[v] = nid;
+          a.perm[nid] = v;
+          a.inv[v] = nid;
+          a.hnew[nid] = hv;
+          if (isroot) a.roots[rbase + __popc(rb & lt)] = nid;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // a5: remap children to new ids
+    for (int i = tid; i < n; i += nthr) {
+      int v = perm[i];
+      for (int k = 0; k < maxc; k++) {
+        int c = ch[k * n + v];
+        a.chn[(long long)k * n + i] = c == -1 ? -1 : inv[c];
+      }
+    }
+  }
+
+  // header (one thread; plain stores)
+  __syncthreads();
+  if (tid == 0) {
+    cx_lin_header *h = a.hdr;
+    unsigned long long key = s_err;
+    h->err_key = key;
+    h->num_nodes = n;
+    if (key != kNoError) {
+      h->status = (int)(key >> 32);
+      h->bad_node = (int)(key & 0xffffffffu);
+      h->num_levels = 0;
+    } else {
+      h->status = CX_OK;
+      h->bad_node = -1;
+      h->num_levels = n > 0 ? L : 0;
+      h->num_roots = n > 0 ? s_count : 0;
+      int nl = n > 0 ? n - lb[0] : 0;
+      h->num_leaves = nl;
+      h->first_leaf = n - nl;
+      h->max_level_size = n > 0 ? s_tmp[32] : 0;
+    }
+  }
+}
+
 }  // namespace
 
 size_t lin_single_smem_bytes(int n, int maxc) {
-  return sizeof(int) * ((size_t)(maxc + 2) * n + kLinSmemCnt);
+  return sizeof(int) * ((size_t)(maxc + 5) * n + kLinSmemCnt);
 }
 
 bool lin_use_single(int n, int maxc) {
@@ -371,13 +609,13 @@ bool lin_use_single(int n, int maxc) {
 cudaError_t launch_linearize(const LinArgs &a, int num_sms, cudaStream_t stream) {
   static bool attr_done = false;  // idempotent attribute set (benign race)
   if (!attr_done) {
-    cudaFuncSetAttribute(lin_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(lin_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kLinSmemMax);
     attr_done = true;
   }
   if (lin_use_single(a.n, a.maxc)) {
     size_t smem = lin_single_smem_bytes(a.n, a.maxc);
-    lin_kernel<false><<<1, kLinThreads, smem, stream>>>(a);
+    lin_single_kernel<<<1, kLinThreads, smem, stream>>>(a);
     return cudaGetLastError();
   }
   LinArgs args = a;
