@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -29,6 +30,16 @@ int num_sms_current() {
     cached_sms = sms;
   }
   return cached_sms;
+}
+
+// Debug/test override of the forward kernel family: CX_FORWARD_PATH=rw|smem
+// (read on every call; unset = automatic by batch size).
+int forward_path() {
+  const char *e = std::getenv("CX_FORWARD_PATH");
+  if (!e) return 0;
+  if (!std::strcmp(e, "rw")) return 1;
+  if (!std::strcmp(e, "smem")) return 2;
+  return 0;
 }
 
 inline char *align_up(char *p, size_t a) {
@@ -126,7 +137,8 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
     std::lock_guard<std::mutex> lk(g_mu);
     int sms = num_sms_current();
     if (sms <= 0) return CX_E_CUDA;
-    if (!cx::fwd_plan(m->cell, m->hidden, lin->max_children, sms, &plan, &Gn, &Gu))
+    if (!cx::fwd_plan(m->cell, m->hidden, lin->max_children, n, forward_path(), sms, &plan, &Gn,
+                      &Gu))
       return CX_E_UNSUPPORTED;
   }
   const size_t N = (size_t)n, H = (size_t)m->hidden;
@@ -216,7 +228,8 @@ cx_status cx_forward_launch_info(const cx_model *m, int32_t *ctas, int32_t *thre
   std::lock_guard<std::mutex> lk(g_mu);
   int sms = num_sms_current();
   if (sms <= 0) return CX_E_CUDA;
-  if (!cx::fwd_plan(m->cell, m->hidden, 2, sms, &plan, &Gn, &Gu)) return CX_E_UNSUPPORTED;
+  if (!cx::fwd_plan(m->cell, m->hidden, 2, 1, forward_path(), sms, &plan, &Gn, &Gu))
+    return CX_E_UNSUPPORTED;
   if (ctas) *ctas = plan.ctas;
   if (threads) *threads = plan.threads;
   if (smem_bytes) *smem_bytes = (int32_t)plan.smem;

@@ -887,8 +887,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1) fwd_kernel(FwdArgs a) {
 
 }  // namespace
 
-// MV-RNN lives in forward_mvrnn.cu
+// MV-RNN lives in forward_mvrnn.cu, the register-weight path in forward_rw.cu
 bool mvrnn_plan(int H, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
+bool rw_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
 
 template <int CELL, int MAXC, class C>
 static bool plan_for(int H, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
@@ -914,8 +915,16 @@ static bool plan_for(int H, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   return true;
 }
 
-bool fwd_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu) {
+bool fwd_plan(int cell, int H, int maxc, int n, int path, int num_sms, FwdPlan *plan, int *Gn,
+              int *Gu) {
   if (H <= 0 || H > 1024 || H % 4) return false;
+  // Register-resident weights (forward_rw.cu) for small and medium batches;
+  // the shared-memory-weight kernel below for large batches, where 32 units
+  // per CTA minimise the re-gathering of child rows across unit groups.
+  const bool rw_ok = (cell == CX_TREELSTM || cell == CX_TREEGRU || cell == CX_TREEFC ||
+                      cell == CX_DAGRNN) && (H == 64 || H == 128 || H == 256 || H == 512);
+  const bool want_rw = path == 1 || (path == 0 && n <= kRwMaxNodes);
+  if (rw_ok && want_rw && rw_plan(cell, H, maxc, num_sms, plan, Gn, Gu)) return true;
   const bool weighted = cell != CX_TREERNN && cell != CX_MVRNN;
   if (weighted && (H % kUG)) return false;
   switch (cell) {

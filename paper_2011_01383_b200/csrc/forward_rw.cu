@@ -1,0 +1,657 @@
+// forward_rw.cu -- persistent forward with REGISTER-resident weights
+// (the latency path: small and medium batches).
+//
+// Model persistence (App. C) keeps the
+// recurrent weights on chip across all levels. Here they live in registers:
+// CTA (gn, gu) owns 16 hidden units; its 512 threads split the contraction
+// dimension into 32 chunks of KC = H/32 (warp w, half-warp s -> chunk 2w+s)
+// and thread (u, chunk) holds W[g][unit0+u][chunk] for every gate g -- at
+// H = 256 that is 4 gates x 8 = 32 floats per thread for TreeLSTM. A tile of
+// T nodes therefore costs no weight traffic at all: the children's rows are
+// gathered into shared memory (the paper's rnn_cache), every
+// thread multiplies its register slice against its chunk of each row, the
+// two half-warps are combined with one shuffle and the 16 warps through
+// shared memory, and the gate algebra runs in the epilogue.
+//
+// Compared with forward.cu (32 units per CTA, weights streamed from shared
+// memory every tile) this halves the units per CTA, doubles the node groups
+// (Gn = 9 at H = 256) and removes the per-tile 128 KiB shared-memory weight
+// sweep that dominated small levels.
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "fwd_common.cuh"
+
+namespace cx {
+namespace {
+using namespace fwd;
+
+constexpr int kRUG = 16;            // hidden units per CTA
+constexpr int kRNW = 16;            // warps per CTA
+constexpr int kRThreads = 32 * kRNW;
+
+// ---------------------------------------------------------------------------
+// Product tables. Vectors 0..NV-1 are gathered rows; vector NV is h~, the sum
+// of the first NCH vectors (children). Product p adds W[g(p)] . vec[v(p)] into
+// accumulator a(p).
+// ---------------------------------------------------------------------------
+template <int NG_, int NV_, int NCH_, int NA_, int NP_>
+struct PhBase {
+  static constexpr int NG = NG_, NV = NV_, NCH = NCH_, NA = NA_, NP = NP_;
+};
+struct RLstmLeaf : PhBase<3, 1, 0, 3, 3> {  // [i; o; u] = W_iou x
+  __device__ static constexpr int g(int p) { return p; }
+  __device__ static constexpr int v(int p) { return 0; }
+  __device__ static constexpr int a(int p) { return p; }
+};
+template <int MAXC>
+struct RLstmLevel : PhBase<4, MAXC, MAXC, 3 + MAXC, 3 + MAXC> {  // U_iou h~ ; U_f h_k
+  __device__ static constexpr int g(int p) { return p < 3 ? p : 3; }
+  __device__ static constexpr int v(int p) { return p < 3 ? MAXC : p - 3; }
+  __device__ static constexpr int a(int p) { return p; }
+};
+struct RGruLeaf : PhBase<2, 1, 0, 2, 2> {  // W_z x ; W_h x
+  __device__ static constexpr int g(int p) { return p; }
+  __device__ static constexpr int v(int p) { return 0; }
+  __device__ static constexpr int a(int p) { return p; }
+};
+template <int MAXC>
+struct RGruA : PhBase<3, MAXC, MAXC, 1 + MAXC, 1 + MAXC> {  // U_z h~ ; U_r h_k
+  __device__ static constexpr int g(int p) { return p < 1 ? 0 : 1; }
+  __device__ static constexpr int v(int p) { return p < 1 ? MAXC : p - 1; }
+  __device__ static constexpr int a(int p) { return p; }
+};
+struct RGruB : PhBase<3, 1, 0, 1, 1> {  // U_h s
+  __device__ static constexpr int g(int p) { return 2; }
+  __device__ static constexpr int v(int p) { return 0; }
+  __device__ static constexpr int a(int p) { return 0; }
+};
+struct RFcLevel : PhBase<2, 2, 0, 1, 2> {  // W_l h_l + W_r h_r
+  __device__ static constexpr int g(int p) { return p; }
+  __device__ static constexpr int v(int p) { return p; }
+  __device__ static constexpr int a(int p) { return 0; }
+};
+struct RDagLeaf : PhBase<2, 1, 0, 1, 1> {  // W_x x (gate 0 of {W_x, U})
+  __device__ static constexpr int g(int p) { return 0; }
+  __device__ static constexpr int v(int p) { return 0; }
+  __device__ static constexpr int a(int p) { return 0; }
+};
+template <int MAXC>
+struct RDagLevel : PhBase<2, MAXC + 1, MAXC, 1, 2> {  // W_x x + U h~  (x = vector MAXC)
+  __device__ static constexpr int g(int p) { return p == 0 ? 1 : 0; }
+  __device__ static constexpr int v(int p) { return p == 0 ? MAXC + 1 : MAXC; }
+  __device__ static constexpr int a(int p) { return 0; }
+};
+
+// ---------------------------------------------------------------------------
+// Per-cell configuration (host + device): level/leaf gates, node tile,
+// gathered vectors, accumulators.
+// ---------------------------------------------------------------------------
+template <int CELL, int H, int MAXC>
+struct RCfg;
+template <int H, int MAXC>
+struct RCfg<CX_TREELSTM, H, MAXC> {
+  static constexpr int NG = 4, TMAX = H >= 512 ? 4 : 8, NVMAX = MAXC, NAMAX = 3 + MAXC;
+};
+template <int H, int MAXC>
+struct RCfg<CX_TREEGRU, H, MAXC> {
+  static constexpr int NG = 3, TMAX = 8, NVMAX = MAXC, NAMAX = 1 + MAXC;
+};
+template <int H, int MAXC>
+struct RCfg<CX_TREEFC, H, MAXC> {
+  static constexpr int NG = 2, TMAX = 16, NVMAX = 2, NAMAX = 1;
+};
+template <int H, int MAXC>
+struct RCfg<CX_DAGRNN, H, MAXC> {
+  static constexpr int NG = 2, TMAX = 16, NVMAX = MAXC + 1, NAMAX = 1;
+};
+
+template <int CELL, int H, int MAXC>
+struct RLayout {
+  using C = RCfg<CELL, H, MAXC>;
+  static constexpr size_t x_floats = (size_t)C::TMAX * C::NVMAX * H;
+  static constexpr size_t red_floats = (size_t)kRNW * C::NAMAX * C::TMAX * kRUG;
+  static constexpr size_t red2_floats = (size_t)C::NAMAX * C::TMAX * kRUG;
+  static constexpr size_t cv_floats = (size_t)C::TMAX * kMaxC * kRUG;
+  static constexpr size_t bytes = sizeof(float) * (x_floats + red_floats + red2_floats + cv_floats);
+};
+
+template <int H>
+struct RShape {
+  static constexpr int KC = H / (2 * kRNW);  // contraction chunk per thread
+};
+
+struct Gate {
+  const float *base;
+  int r0, ld, c0;
+};
+
+// wreg[g][j] = W_g[unit0 + u][k0 + j]   (global -> registers)
+template <int NG, int KC>
+__device__ __forceinline__ void load_wregs(float (&w)[4][KC], const Gate *gs, int ng, int row_u,
+                                           int k0) {
+#pragma unroll
+  for (int g = 0; g < NG; g++) {
+    if (g < ng) {
+      const float *src = gs[g].base + (size_t)(gs[g].r0 + row_u) * gs[g].ld + gs[g].c0 + k0;
+      if constexpr (KC % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < KC; j += 4) {
+          float4 v = __ldg(reinterpret_cast<const float4 *>(src + j));
+          w[g][j] = v.x; w[g][j + 1] = v.y; w[g][j + 2] = v.z; w[g][j + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < KC; j++) w[g][j] = __ldg(src + j);
+      }
+    }
+  }
+}
+
+struct RCtx {
+  const FwdArgs *a;
+  float *X, *red, *red2, *cv;
+  const float *bias;  // [gate][16]
+  int gn, gu, unit0;
+  bool latch;
+};
+
+// Contraction of one tile against the register-resident weights, reduced to
+// full sums: on return s[a] (threads tid < T*16: node t = tid/16, unit u =
+// tid%16) holds accumulator a of that (node, unit).
+template <class PH, int H, int T>
+__device__ __forceinline__ void contract(const RCtx &c, const float (&w)[4][RShape<H>::KC],
+                                         float (&s)[PH::NA]) {
+  constexpr int KC = RShape<H>::KC;
+  constexpr int NV = PH::NV;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int u = lane & 15, ksub = lane >> 4;
+  const int k0 = (warp * 2 + ksub) * KC;
+  float acc[PH::NA][T];
+#pragma unroll
+  for (int a = 0; a < PH::NA; a++)
+#pragma unroll
+    for (int t = 0; t < T; t++) acc[a][t] = 0.f;
+  constexpr int QB = KC < 4 ? KC : 4;  // k-block held in registers at a time
+#pragma unroll
+  for (int t = 0; t < T; t++) {
+#pragma unroll
+    for (int q = 0; q < KC; q += QB) {
+      float x[NV + 1][QB];
+#pragma unroll
+      for (int j = 0; j < NV; j++) {
+        const float *p = c.X + (size_t)(t * NV + j) * H + k0 + q;
+        if constexpr (QB == 4) {
+          float4 v = *reinterpret_cast<const float4 *>(p);
+          x[j][0] = v.x; x[j][1] = v.y; x[j][2] = v.z; x[j][3] = v.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < QB; e++) x[j][e] = p[e];
+        }
+      }
+      if constexpr (PH::NCH > 0) {
+#pragma unroll
+        for (int e = 0; e < QB; e++) {
+          float sum = x[0][e];
+#pragma unroll
+          for (int j = 1; j < PH::NCH; j++) sum += x[j][e];
+          x[NV][e] = sum;
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < PH::NP; p++)
+#pragma unroll
+        for (int e = 0; e < QB; e++)
+          acc[PH::a(p)][t] = fmaf(w[PH::g(p)][q + e], x[PH::v(p)][e], acc[PH::a(p)][t]);
+    }
+  }
+  // half-warps hold the two chunks of each unit: combine, then across warps
+#pragma unroll
+  for (int a = 0; a < PH::NA; a++)
+#pragma unroll
+    for (int t = 0; t < T; t++) acc[a][t] += __shfl_xor_sync(0xffffffffu, acc[a][t], 16);
+  if (ksub == 0) {
+#pragma unroll
+    for (int a = 0; a < PH::NA; a++)
+#pragma unroll
+      for (int t = 0; t < T; t++) c.red[((warp * PH::NA + a) * T + t) * kRUG + u] = acc[a][t];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < PH::NA * T * kRUG; idx += blockDim.x) {
+    float v = 0.f;
+#pragma unroll
+    for (int ww = 0; ww < kRNW; ww++) v += c.red[ww * PH::NA * T * kRUG + idx];
+    c.red2[idx] = v;
+  }
+  __syncthreads();
+  const int t = threadIdx.x >> 4, uu = threadIdx.x & 15;
+#pragma unroll
+  for (int a = 0; a < PH::NA; a++) s[a] = t < T ? c.red2[(a * T + t) * kRUG + uu] : 0.f;
+}
+
+// ---------------------------------------------------------------------------
+// Cells
+// ---------------------------------------------------------------------------
+template <int H, int MAXC>
+struct RTreeLstm {
+  static constexpr int kPhases = 1;
+  using M = TileMetaT<RCfg<CX_TREELSTM, H, MAXC>::TMAX>;
+  __device__ static int leaf_gates(const FwdArgs &a, Gate *g) {
+    g[0] = {a.w[0], 0, H, 0}; g[1] = {a.w[0], H, H, 0}; g[2] = {a.w[0], 2 * H, H, 0};
+    return 3;
+  }
+  __device__ static int level_gates(const FwdArgs &a, Gate *g) {
+    g[0] = {a.w[1], 0, H, 0}; g[1] = {a.w[1], H, H, 0}; g[2] = {a.w[1], 2 * H, H, 0};
+    g[3] = {a.w[3], 0, H, 0};
+    return 4;
+  }
+  __device__ static int biases(const FwdArgs &a, const float **b, int *off) {
+    b[0] = b[1] = b[2] = a.w[2]; off[0] = 0; off[1] = H; off[2] = 2 * H;
+    b[3] = a.w[4]; off[3] = 0;
+    return 4;
+  }
+  __device__ static int leaf_lo(int first_leaf) { return first_leaf; }
+  struct Leaf {
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *m, i0, cnt, false, true, false, c.latch); }
+    template <int T>
+    __device__ __forceinline__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
+      gather_rows_c<1, H>(c.X, cnt, [&](int t, int) { return a.emb + (size_t)m->word[t] * H; });
+      __syncthreads();
+      float s[3];
+      contract<RLstmLeaf, H, T>(c, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+      const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
+      if (t < cnt) {
+        float cc = sigmoidf_(s[0] + c.bias[u]) * tanhf(s[2] + c.bias[32 + u]);
+        float hh = sigmoidf_(s[1] + c.bias[16 + u]) * tanhf(cc);
+        size_t o = (size_t)m->own[t] * H + c.unit0 + u;
+        a.h_out[o] = hh;
+        a.cbuf[o] = cc;
+      }
+      __syncthreads();
+    }
+  };
+  struct Level {
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int phase, pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *m, i0, cnt, true, false, false, c.latch); }
+    template <int T>
+    __device__ __forceinline__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
+      gather_rows_c<MAXC, H>(c.X, cnt, [&](int t, int j) {
+        int ci = m->cin[t][j];
+        return ci >= 0 ? a.h_out + (size_t)ci * H : (const float *)nullptr;
+      });
+      for (int idx = threadIdx.x; idx < cnt * MAXC * kRUG; idx += blockDim.x) {
+        int t = idx / (MAXC * kRUG), r = idx - t * MAXC * kRUG, k = r >> 4, u = r & 15;
+        int ci = m->cin[t][k];
+        c.cv[(t * kMaxC + k) * kRUG + u] = ci >= 0 ? __ldcg(a.cbuf + (size_t)ci * H + c.unit0 + u) : 0.f;
+      }
+      __syncthreads();
+      float s[3 + MAXC];
+      contract<RLstmLevel<MAXC>, H, T>(c, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+      const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
+      if (t < cnt) {
+        float cc = sigmoidf_(s[0] + c.bias[u]) * tanhf(s[2] + c.bias[32 + u]);
+        const float bf = c.bias[48 + u];
+        const int nc = m->nch[t];
+#pragma unroll
+        for (int k = 0; k < MAXC; k++)
+          if (k < nc) cc += sigmoidf_(s[3 + k] + bf) * c.cv[(t * kMaxC + k) * kRUG + u];
+        float hh = sigmoidf_(s[1] + c.bias[16 + u]) * tanhf(cc);
+        size_t o = (size_t)m->own[t] * H + c.unit0 + u;
+        a.h_out[o] = hh;
+        a.cbuf[o] = cc;
+      }
+      __syncthreads();
+    }
+  };
+};
+
+template <int H, int MAXC>
+struct RTreeGru {
+  static constexpr int kPhases = 2;
+  using M = TileMetaT<RCfg<CX_TREEGRU, H, MAXC>::TMAX>;
+  __device__ static int leaf_gates(const FwdArgs &a, Gate *g) {
+    g[0] = {a.w[0], 0, H, 0}; g[1] = {a.w[0], H, H, 0};
+    return 2;
+  }
+  __device__ static int level_gates(const FwdArgs &a, Gate *g) {
+    g[0] = {a.w[1], 0, H, 0}; g[1] = {a.w[2], 0, H, 0}; g[2] = {a.w[3], 0, H, 0};
+    return 3;
+  }
+  __device__ static int biases(const FwdArgs &a, const float **b, int *off) {
+    b[0] = a.w[4]; b[1] = a.w[5]; b[2] = a.w[6]; off[0] = off[1] = off[2] = 0;
+    return 3;
+  }
+  __device__ static int leaf_lo(int first_leaf) { return first_leaf; }
+  struct Leaf {
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *m, i0, cnt, false, true, false, c.latch); }
+    template <int T>
+    __device__ __forceinline__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
+      gather_rows_c<1, H>(c.X, cnt, [&](int t, int) { return a.emb + (size_t)m->word[t] * H; });
+      __syncthreads();
+      float s[2];
+      contract<RGruLeaf, H, T>(c, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+      const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
+      if (t < cnt) {
+        float z = sigmoidf_(s[0] + c.bias[u]);
+        float g = tanhf(s[1] + c.bias[32 + u]);
+        a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = (1.f - z) * g;
+      }
+      __syncthreads();
+    }
+  };
+  struct Level {
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int phase, pre;
+    __device__ void meta(int i0, int cnt) {
+      if (phase == 0) load_meta(*c.a, *m, i0, cnt, true, false, false, c.latch);
+      else load_meta(*c.a, *m, i0, cnt, false, false, false, false);
+    }
+    template <int T>
+    __device__ __forceinline__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
+      const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
+      const auto &wr = *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w);
+      if (phase == 0) {
+        gather_rows_c<MAXC, H>(c.X, cnt, [&](int tt, int j) {
+          int ci = m->cin[tt][j];
+          return ci >= 0 ? a.h_out + (size_t)ci * H : (const float *)nullptr;
+        });
+        __syncthreads();
+        float s[1 + MAXC];
+        contract<RGruA<MAXC>, H, T>(c, wr, s);
+        if (t < cnt) {
+          const int unit = c.unit0 + u;
+          float z = sigmoidf_(s[0] + c.bias[u]);
+          float br = c.bias[16 + u];
+          float sum = 0.f, ht = 0.f;
+          const int nc = m->nch[t];
+#pragma unroll
+          for (int k = 0; k < MAXC; k++)
+            if (k < nc) {
+              float hk = c.X[(size_t)(t * MAXC + k) * H + unit];
+              sum += sigmoidf_(s[1 + k] + br) * hk;
+              ht += hk;
+            }
+          size_t o = (size_t)m->own[t] * H + unit;
+          a.sbuf[o] = sum;
+          a.zbuf[o] = z;
+          a.h_out[o] = ht;  // stash h~ for phase B (overwritten there)
+        }
+        __syncthreads();
+      } else {
+        gather_rows_c<1, H>(c.X, cnt, [&](int tt, int) { return a.sbuf + (size_t)m->own[tt] * H; });
+        __syncthreads();
+        float s[1];
+        contract<RGruB, H, T>(c, wr, s);
+        if (t < cnt) {
+          size_t o = (size_t)m->own[t] * H + c.unit0 + u;
+          float g = tanhf(s[0] + c.bias[32 + u]);
+          float z = __ldcg(a.zbuf + o), ht = __ldcg(a.h_out + o);
+          a.h_out[o] = z * ht + (1.f - z) * g;
+        }
+        __syncthreads();
+      }
+    }
+  };
+};
+
+template <int H, int MAXC>
+struct RTreeFc {
+  static constexpr int kPhases = 1;
+  using M = TileMetaT<RCfg<CX_TREEFC, H, MAXC>::TMAX>;
+  __device__ static int leaf_gates(const FwdArgs &, Gate *) { return 0; }
+  __device__ static int level_gates(const FwdArgs &a, Gate *g) {
+    g[0] = {a.w[0], 0, 2 * H, 0}; g[1] = {a.w[0], 0, 2 * H, H};
+    return 2;
+  }
+  __device__ static int biases(const FwdArgs &a, const float **b, int *off) {
+    b[0] = a.w[1]; off[0] = 0;
+    return 1;
+  }
+  __device__ static int leaf_lo(int first_leaf) { return first_leaf; }
+  struct Leaf {  // h = Emb[word] (pure gather)
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *m, i0, cnt, false, true, false, c.latch); }
+    template <int T>
+    __device__ __forceinline__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
+      for (int idx = threadIdx.x; idx < cnt * kRUG; idx += blockDim.x) {
+        int t = idx >> 4, u = idx & 15;
+        a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = __ldg(a.emb + (size_t)m->word[t] * H + c.unit0 + u);
+      }
+      __syncthreads();
+    }
+  };
+  struct Level {
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int phase, pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *m, i0, cnt, true, false, true, c.latch); }
+    template <int T>
+    __device__ __forceinline__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
+      gather_rows_c<2, H>(c.X, cnt, [&](int t, int j) { return a.h_out + (size_t)m->cin[t][j] * H; });
+      __syncthreads();
+      float s[1];
+      contract<RFcLevel, H, T>(c, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+      const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
+      if (t < cnt) a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = tanhf(s[0] + c.bias[u]);
+      __syncthreads();
+    }
+  };
+};
+
+template <int H, int MAXC>
+struct RDagRnn {
+  static constexpr int kPhases = 1;
+  using M = TileMetaT<RCfg<CX_DAGRNN, H, MAXC>::TMAX>;
+  // gates {W_x, U} resident through leaves and levels (input projections are
+  // fused into each level instead of a separate all-node GEMM)
+  __device__ static int leaf_gates(const FwdArgs &a, Gate *g) {
+    g[0] = {a.w[0], 0, H, 0}; g[1] = {a.w[1], 0, H, 0};
+    return 2;
+  }
+  __device__ static int level_gates(const FwdArgs &a, Gate *g) { return leaf_gates(a, g); }
+  __device__ static int biases(const FwdArgs &a, const float **b, int *off) {
+    b[0] = a.w[2]; off[0] = 0;
+    return 1;
+  }
+  __device__ static int leaf_lo(int first_leaf) { return first_leaf; }
+  struct Leaf {  // h = tanh(W_x x + b)
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *m, i0, cnt, false, true, false, c.latch); }
+    template <int T>
+    __device__ __forceinline__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
+      gather_rows_c<1, H>(c.X, cnt, [&](int t, int) { return a.emb + (size_t)m->word[t] * H; });
+      __syncthreads();
+      float s[1];
+      contract<RDagLeaf, H, T>(c, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+      const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
+      if (t < cnt) a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = tanhf(s[0] + c.bias[u]);
+      __syncthreads();
+    }
+  };
+  struct Level {  // h = tanh(W_x x + U h~ + b)
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int phase, pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *m, i0, cnt, true, true, false, c.latch); }
+    template <int T>
+    __device__ __forceinline__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
+      gather_rows_c<MAXC + 1, H>(c.X, cnt, [&](int t, int j) {
+        if (j == MAXC) return a.emb + (size_t)m->word[t] * H;
+        int ci = m->cin[t][j];
+        return ci >= 0 ? a.h_out + (size_t)ci * H : (const float *)nullptr;
+      });
+      __syncthreads();
+      float s[1];
+      contract<RDagLevel<MAXC>, H, T>(c, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+      const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
+      if (t < cnt) a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = tanhf(s[0] + c.bias[u]);
+      __syncthreads();
+    }
+  };
+};
+
+// ---------------------------------------------------------------------------
+// Kernel skeleton
+// ---------------------------------------------------------------------------
+template <int CELL, int H, int MAXC, class C>
+__global__ void __launch_bounds__(kRThreads, 1) rw_kernel(FwdArgs a) {
+  using Cfg = RCfg<CELL, H, MAXC>;
+  using Lay = RLayout<CELL, H, MAXC>;
+  constexpr int KC = RShape<H>::KC;
+  extern __shared__ __align__(16) float smem[];
+  __shared__ typename C::M meta;
+  __shared__ float s_bias[4 * kRUG];
+
+  if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
+  const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n;
+  const int gn = blockIdx.x / a.Gu, gu = blockIdx.x % a.Gu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int u = lane & 15, k0 = (warp * 2 + (lane >> 4)) * KC;
+
+  RCtx ctx;
+  ctx.a = &a;
+  ctx.X = smem;
+  ctx.red = smem + Lay::x_floats;
+  ctx.red2 = ctx.red + Lay::red_floats;
+  ctx.cv = ctx.red2 + Lay::red2_floats;
+  ctx.gn = gn;
+  ctx.gu = gu;
+  ctx.unit0 = gu * kRUG;
+  ctx.latch = gu == 0;
+  unsigned epoch = 0;
+  trace_mark(a, 0);
+
+  {
+    const float *bp[4];
+    int off[4];
+    int nb = C::biases(a, bp, off);
+    if (threadIdx.x < nb * kRUG) {
+      int g = threadIdx.x / kRUG, uu = threadIdx.x % kRUG;
+      s_bias[threadIdx.x] = __ldg(bp[g] + off[g] + ctx.unit0 + uu);
+    }
+  }
+  ctx.bias = s_bias;
+
+  float w[4][KC];
+  Gate gs[4];
+  // ---- leaf phase (specialised leaf loop nest) ------------------
+  {
+    int ng = C::leaf_gates(a, gs);
+    load_wregs<Cfg::NG, KC>(w, gs, ng, ctx.unit0 + u, k0);
+    __syncthreads();
+    trace_mark(a, 1);
+    const int lo0 = C::leaf_lo(first_leaf);
+    int lo, hi;
+    chunk_of(n - lo0, a.Gn, gn, lo, hi);
+    typename C::Leaf f{ctx, &meta, w, -1};
+    for_tiles<Cfg::TMAX>(lo0 + lo, lo0 + hi, f);
+  }
+  __syncthreads();
+  trace_mark(a, 2);
+  {
+    int ng = C::level_gates(a, gs);
+    load_wregs<Cfg::NG, KC>(w, gs, ng, ctx.unit0 + u, k0);
+  }
+  // ---- internal batches: one grid barrier per level (and phase) -------------
+  for (int l = 1; l < L; l++) {
+    const int base = __ldg(a.lbeg + l), M = __ldg(a.lsize + l);
+    int lo, hi;
+    chunk_of(M, a.Gn, gn, lo, hi);
+    for (int ph = 0; ph < C::kPhases; ph++) {
+      const int slot = 3 + 2 * ((l - 1) * C::kPhases + ph);
+      trace_mark(a, slot);
+      grid_arrive(a.bar, epoch);
+      typename C::Level f{ctx, &meta, w, ph, -1};
+      if (hi > lo) {
+        f.meta(base + lo, min(Cfg::TMAX, hi - lo));
+        f.pre = base + lo;
+      }
+      grid_wait(a.bar, gridDim.x, epoch);
+      trace_mark(a, slot + 1);
+      for_tiles<Cfg::TMAX>(base + lo, base + hi, f);
+    }
+  }
+  trace_mark(a, a.trace_slots - 2);
+  copy_roots(a, gn, ctx.unit0, kRUG, C::leaf_lo(first_leaf));
+  trace_mark(a, a.trace_slots - 1);
+  publish_and_exit(a);
+}
+
+template <int CELL, int H, int MAXC, class C>
+bool rplan(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
+  constexpr size_t smem = RLayout<CELL, H, MAXC>::bytes;
+  if (smem > 227 * 1024) return false;
+  auto k = rw_kernel<CELL, H, MAXC, C>;
+  static bool set = false;
+  if (!set) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return false;
+    set = true;
+  }
+  *Gu = H / kRUG;
+  *Gn = num_sms / *Gu;
+  if (*Gn < 1) return false;
+  p->ctas = *Gn * *Gu;
+  p->threads = kRThreads;
+  p->smem = smem;
+  p->kernel = (const void *)k;
+  return true;
+}
+
+template <int CELL, int H>
+bool rplan_maxc(int maxc, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
+  if constexpr (CELL == CX_TREEFC) {
+    return rplan<CELL, H, 2, RTreeFc<H, 2>>(num_sms, p, Gn, Gu);
+  } else {
+    auto pick = [&](auto mc) {
+      constexpr int MC = decltype(mc)::value;
+      if constexpr (CELL == CX_TREELSTM) return rplan<CELL, H, MC, RTreeLstm<H, MC>>(num_sms, p, Gn, Gu);
+      if constexpr (CELL == CX_TREEGRU) return rplan<CELL, H, MC, RTreeGru<H, MC>>(num_sms, p, Gn, Gu);
+      if constexpr (CELL == CX_DAGRNN) return rplan<CELL, H, MC, RDagRnn<H, MC>>(num_sms, p, Gn, Gu);
+      return false;
+    };
+    if (maxc <= 1) return pick(std::integral_constant<int, 1>{});
+    if (maxc <= 2) return pick(std::integral_constant<int, 2>{});
+    if (maxc <= 4) return pick(std::integral_constant<int, 4>{});
+    return false;
+  }
+}
+
+template <int H>
+bool rplan_cell(int cell, int maxc, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
+  switch (cell) {
+    case CX_TREELSTM: return rplan_maxc<CX_TREELSTM, H>(maxc, num_sms, p, Gn, Gu);
+    case CX_TREEGRU: return rplan_maxc<CX_TREEGRU, H>(maxc, num_sms, p, Gn, Gu);
+    case CX_TREEFC: return rplan_maxc<CX_TREEFC, H>(maxc, num_sms, p, Gn, Gu);
+    case CX_DAGRNN: return rplan_maxc<CX_DAGRNN, H>(maxc, num_sms, p, Gn, Gu);
+  }
+  return false;
+}
+
+}  // namespace
+
+bool rw_plan(int cell, int H, int maxc, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
+  switch (H) {
+    case 64: return rplan_cell<64>(cell, maxc, num_sms, p, Gn, Gu);
+    case 128: return rplan_cell<128>(cell, maxc, num_sms, p, Gn, Gu);
+    case 256: return rplan_cell<256>(cell, maxc, num_sms, p, Gn, Gu);
+    case 512: return rplan_cell<512>(cell, maxc, num_sms, p, Gn, Gu);
+  }
+  return false;
+}
+
+}  // namespace cx

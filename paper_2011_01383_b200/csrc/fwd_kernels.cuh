@@ -47,7 +47,11 @@ struct FwdPlan {
 };
 
 // Returns false (CX_E_UNSUPPORTED) when no instantiation covers the model.
-bool fwd_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
+// path: 0 = automatic (register weights when n <= kRwMaxNodes), 1 = force the
+// register-weight kernel, 2 = force the shared-memory-weight kernel.
+constexpr int kRwMaxNodes = 32768;
+bool fwd_plan(int cell, int H, int maxc, int n, int path, int num_sms, FwdPlan *plan, int *Gn,
+              int *Gu);
 size_t fwd_workspace_bytes(int cell, int H, int n);
 cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream);
 

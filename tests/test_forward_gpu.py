@@ -18,6 +18,17 @@ def cx():
     return m
 
 
+@pytest.fixture(params=["auto", "rw", "smem"])
+def path(request, monkeypatch):
+    """Run a test through each forward kernel family (CX_FORWARD_PATH is read
+    by libcx on every cx_forward call)."""
+    if request.param == "auto":
+        monkeypatch.delenv("CX_FORWARD_PATH", raising=False)
+    else:
+        monkeypatch.setenv("CX_FORWARD_PATH", request.param)
+    return request.param
+
+
 def _parity(cell, hidden, vocab, children, kind, seed=0, want_aux=False, all_words=None,
             check_roots=True):
     words = synth.word_ids(children, vocab, seed, all_nodes=(cell == T.DAGRNN))
@@ -44,11 +55,12 @@ def _parity(cell, hidden, vocab, children, kind, seed=0, want_aux=False, all_wor
 SMALL = [  # (cell, H) at sizes that still span several tiles and node groups
     (T.TREERNN, 8), (T.TREERNN, 64), (T.TREEFC, 64), (T.TREELSTM, 64), (T.TREEGRU, 64),
     (T.MVRNN, 16), (T.MVRNN, 64), (T.DAGRNN, 64), (T.TREELSTM, 32), (T.TREEGRU, 96),
+    (T.TREELSTM, 128), (T.TREEGRU, 512), (T.TREEFC, 512), (T.DAGRNN, 512), (T.TREELSTM, 512),
 ]
 
 
 @pytest.mark.parametrize("cell,H", SMALL)
-def test_small_forests(cx, cell, H):
+def test_small_forests(cx, cell, H, path):
     V = 97
     if cell == T.DAGRNN:
         ch, _ = synth.grid_dags(3, 5, 7)
@@ -60,7 +72,7 @@ def test_small_forests(cx, cell, H):
 
 
 @pytest.mark.parametrize("cell", [T.TREELSTM, T.TREEGRU, T.DAGRNN])
-def test_child_sum_general_arity(cx, cell):
+def test_child_sum_general_arity(cx, cell, path):
     """Child-sum cells on nodes with 0..4 children (random DAG / forest)."""
     H, V = 64, 50
     if cell == T.DAGRNN:
@@ -81,7 +93,7 @@ def test_sequences(cx, cell):
                                   "cfg3_treegru_b1", "cfg3_treegru_b10", "cfg3_treefc_b1",
                                   "cfg3_treefc_b10", "cfg4_mvrnn_b10", "cfg5_dagrnn_b1",
                                   "cfg5_dagrnn_b10"])
-def test_baseline_configs(cx, name):
+def test_baseline_configs(cx, name, path):
     w = synth.workload(name)
     _parity(w["cell"], w["hidden"], w["vocab"], w["children"], w["kind"], seed=w["seed"],
             want_aux=True)
@@ -115,7 +127,7 @@ def test_batch4096_sampled(cx, name):
     assert np.array_equal(rt[picks], hr[targets])
 
 
-def test_permutation_and_batch_invariance(cx):
+def test_permutation_and_batch_invariance(cx, path):
     """Relabelling permutes outputs identically; a tree alone == the tree in a
     forest (bitwise: per-node arithmetic does not depend on level size)."""
     H, V = 64, 40
