@@ -92,6 +92,27 @@ __device__ __forceinline__ float4 ldcg4(const float *p) {
 }
 __device__ __forceinline__ int ldcg_i(const int *p) { return __ldcg(p); }
 
-__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + expf(-x)); }
+// Gate nonlinearities on the MUFU pipe (ex2 + rcp): sigma(x) = 1 / (1 + e^-x),
+// tanh(x) = (e^2x - 1) / (e^2x + 1) with |x| clamped at 15 (tanh(15) rounds to
+// 1 in fp32). __expf's error is <= 2 + 1.16|x| ulp; over the clamp range the
+// result stays within ~5e-6 relative (absolute near 0), far inside the fp32
+// path's 1e-4 tolerance (Q10).
+__device__ __forceinline__ float sigmoidf_(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+__device__ __forceinline__ float tanhf_(float x) {
+  x = fminf(fmaxf(x, -15.f), 15.f);
+  float e = __expf(2.f * x);
+  return __fdividef(e - 1.f, e + 1.f);
+}
+
+// packed fp32x2 FMA (sm_100: FFMA2): d = a * b + c element-wise
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
 
 }  // namespace cx

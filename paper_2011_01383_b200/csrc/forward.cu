@@ -367,8 +367,8 @@ struct TreeLstm {
       if (t < cnt) {
         float ig = s[0] + c.bias[0 * 32 + lane], og = s[1] + c.bias[1 * 32 + lane],
               ug = s[2] + c.bias[2 * 32 + lane];
-        float cc = sigmoidf_(ig) * tanhf(ug);
-        float hh = sigmoidf_(og) * tanhf(cc);
+        float cc = sigmoidf_(ig) * tanhf_(ug);
+        float hh = sigmoidf_(og) * tanhf_(cc);
         size_t o = (size_t)c.m->own[t] * H + unit;
         a.h_out[o] = hh;
         a.cbuf[o] = cc;
@@ -411,12 +411,12 @@ struct TreeLstm {
       if (t < cnt) {
         float ig = s[0] + c.bias[0 * 32 + lane], og = s[1] + c.bias[1 * 32 + lane],
               ug = s[2] + c.bias[2 * 32 + lane], bfu = c.bias[3 * 32 + lane];
-        float cc = sigmoidf_(ig) * tanhf(ug);
+        float cc = sigmoidf_(ig) * tanhf_(ug);
         const int nc = c.m->nch[t];
 #pragma unroll
         for (int k = 0; k < MAXC; k++)
           if (k < nc) cc += sigmoidf_(s[3 + k] + bfu) * c.cv[(t * kMaxC + k) * 32 + lane];
-        float hh = sigmoidf_(og) * tanhf(cc);
+        float hh = sigmoidf_(og) * tanhf_(cc);
         size_t o = (size_t)c.m->own[t] * H + unit;
         a.h_out[o] = hh;
         a.cbuf[o] = cc;
@@ -477,7 +477,7 @@ struct TreeGru {
       const int t = threadIdx.x >> 5, unit = c.unit0 + lane;
       if (t < cnt) {
         float z = sigmoidf_(s[0] + c.bias[0 * 32 + lane]);
-        float g = tanhf(s[1] + c.bias[2 * 32 + lane]);
+        float g = tanhf_(s[1] + c.bias[2 * 32 + lane]);
         a.h_out[(size_t)c.m->own[t] * H + unit] = (1.f - z) * g;
       }
       __syncthreads();
@@ -540,7 +540,7 @@ struct TreeGru {
         reduce_acc<1, T>(c.X, acc, s);
         if (t < cnt) {
           size_t o = (size_t)c.m->own[t] * H + unit;
-          float g = tanhf(s[0] + c.bias[2 * 32 + lane]);
+          float g = tanhf_(s[0] + c.bias[2 * 32 + lane]);
           float z = __ldcg(a.zbuf + o), ht = __ldcg(a.h_out + o);
           a.h_out[o] = z * ht + (1.f - z) * g;
         }
@@ -606,7 +606,7 @@ struct TreeFc {
       fma_engine<PhFcLevel, T>(c.Ws, c.X, H, acc);
       reduce_acc<1, T>(c.X, acc, s);
       const int t = threadIdx.x >> 5, unit = c.unit0 + (threadIdx.x & 31);
-      if (t < cnt) a.h_out[(size_t)c.m->own[t] * H + unit] = tanhf(s[0] + c.bias[threadIdx.x & 31]);
+      if (t < cnt) a.h_out[(size_t)c.m->own[t] * H + unit] = tanhf_(s[0] + c.bias[threadIdx.x & 31]);
       __syncthreads();
     }
   };
@@ -653,7 +653,7 @@ struct DagRnn {
         float p = s[0] + c.bias[threadIdx.x & 31];
         size_t o = (size_t)c.m->own[t] * H + unit;
         a.pbuf[o] = p;
-        if (i0 + t >= a.hdr->first_leaf) a.h_out[o] = tanhf(p);
+        if (i0 + t >= a.hdr->first_leaf) a.h_out[o] = tanhf_(p);
       }
       __syncthreads();
     }
@@ -682,7 +682,7 @@ struct DagRnn {
       fma_engine<PhDagLevel<MAXC>, T>(c.Ws, c.X, H, acc);
       reduce_acc<1, T>(c.X, acc, s);
       const int t = threadIdx.x >> 5, unit = c.unit0 + lane;
-      if (t < cnt) a.h_out[(size_t)c.m->own[t] * H + unit] = tanhf(s[0] + c.cv[t * 32 + lane]);
+      if (t < cnt) a.h_out[(size_t)c.m->own[t] * H + unit] = tanhf_(s[0] + c.cv[t * 32 + lane]);
       __syncthreads();
     }
   };
@@ -741,7 +741,7 @@ struct TreeRnn {
         int t = idx / ug, unit = c.unit0 + idx % ug;
         float l = __ldcg(a.h_out + (size_t)c.m->cin[t][0] * c.H + unit);
         float r = __ldcg(a.h_out + (size_t)c.m->cin[t][1] * c.H + unit);
-        a.h_out[(size_t)c.m->own[t] * c.H + unit] = tanhf(l + r);
+        a.h_out[(size_t)c.m->own[t] * c.H + unit] = tanhf_(l + r);
       }
       __syncthreads();
     }

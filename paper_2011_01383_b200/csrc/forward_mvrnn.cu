@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kT, 1) mvrnn_kernel(FwdArgs a) {
         for (int k = q; k < 2 * H; k += TPO) s = fmaf(Ws[o * Lay::WP + k], pv[k], s);
 #pragma unroll
         for (int d = TPO / 2; d >= 1; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
-        if (q == 0) a.h_out[(size_t)s_own * H + o] = tanhf(s + __ldg(beta + o));
+        if (q == 0) a.h_out[(size_t)s_own * H + o] = tanhf_(s + __ldg(beta + o));
       }
       // A_n = W_M [A; B]: thread (ti, tj) computes rows ti*RT.., cols tj*RT..
       {

@@ -110,7 +110,7 @@ struct RCfg<CX_DAGRNN, H, MAXC> {
 template <int CELL, int H, int MAXC>
 struct RLayout {
   using C = RCfg<CELL, H, MAXC>;
-  static constexpr size_t x_floats = (size_t)C::TMAX * C::NVMAX * H;
+  static constexpr size_t x_floats = (size_t)C::TMAX * (C::NVMAX > 2 ? C::NVMAX : 2) * H;
   static constexpr size_t red_floats = (size_t)kRNW * C::NAMAX * C::TMAX * kRUG;
   static constexpr size_t red2_floats = (size_t)C::NAMAX * C::TMAX * kRUG;
   static constexpr size_t cv_floats = (size_t)C::TMAX * kMaxC * kRUG;
@@ -155,24 +155,27 @@ struct RCtx {
   const float *bias;  // [gate][16]
   int gn, gu, unit0;
   bool latch;
+  int tslot;  // debug trace slot base for this tile (-1 = off)
 };
 
 // Contraction of one tile against the register-resident weights, reduced to
 // full sums: on return s[a] (threads tid < T*16: node t = tid/16, unit u =
 // tid%16) holds accumulator a of that (node, unit).
 template <class PH, int H, int T>
-__device__ __forceinline__ void contract(const RCtx &c, const float (&w)[4][RShape<H>::KC],
-                                         float (&s)[PH::NA]) {
+__device__ __forceinline__ void contract(const RCtx &c, const float *X,
+                                         const float (&w)[4][RShape<H>::KC], float (&s)[PH::NA]) {
   constexpr int KC = RShape<H>::KC;
   constexpr int NV = PH::NV;
+  static_assert(KC % 2 == 0, "packed FFMA2 needs an even k chunk");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int u = lane & 15, ksub = lane >> 4;
   const int k0 = (warp * 2 + ksub) * KC;
-  float acc[PH::NA][T];
+  // even/odd k partial sums packed in float2 -> one FFMA2 per two products
+  float2 acc2[PH::NA][T];
 #pragma unroll
   for (int a = 0; a < PH::NA; a++)
 #pragma unroll
-    for (int t = 0; t < T; t++) acc[a][t] = 0.f;
+    for (int t = 0; t < T; t++) acc2[a][t] = make_float2(0.f, 0.f);
   constexpr int QB = KC < 4 ? KC : 4;  // k-block held in registers at a time
 #pragma unroll
   for (int t = 0; t < T; t++) {
@@ -181,13 +184,13 @@ __device__ __forceinline__ void contract(const RCtx &c, const float (&w)[4][RSha
       float x[NV + 1][QB];
 #pragma unroll
       for (int j = 0; j < NV; j++) {
-        const float *p = c.X + (size_t)(t * NV + j) * H + k0 + q;
+        const float *p = X + (size_t)(t * NV + j) * H + k0 + q;
         if constexpr (QB == 4) {
           float4 v = *reinterpret_cast<const float4 *>(p);
           x[j][0] = v.x; x[j][1] = v.y; x[j][2] = v.z; x[j][3] = v.w;
         } else {
-#pragma unroll
-          for (int e = 0; e < QB; e++) x[j][e] = p[e];
+          float2 v = *reinterpret_cast<const float2 *>(p);
+          x[j][0] = v.x; x[j][1] = v.y;
         }
       }
       if constexpr (PH::NCH > 0) {
@@ -202,10 +205,17 @@ __device__ __forceinline__ void contract(const RCtx &c, const float (&w)[4][RSha
 #pragma unroll
       for (int p = 0; p < PH::NP; p++)
 #pragma unroll
-        for (int e = 0; e < QB; e++)
-          acc[PH::a(p)][t] = fmaf(w[PH::g(p)][q + e], x[PH::v(p)][e], acc[PH::a(p)][t]);
+        for (int e = 0; e < QB; e += 2)
+          acc2[PH::a(p)][t] = ffma2(make_float2(w[PH::g(p)][q + e], w[PH::g(p)][q + e + 1]),
+                                    make_float2(x[PH::v(p)][e], x[PH::v(p)][e + 1]),
+                                    acc2[PH::a(p)][t]);
     }
   }
+  float acc[PH::NA][T];
+#pragma unroll
+  for (int a = 0; a < PH::NA; a++)
+#pragma unroll
+    for (int t = 0; t < T; t++) acc[a][t] = acc2[a][t].x + acc2[a][t].y;
   // half-warps hold the two chunks of each unit: combine, then across warps
 #pragma unroll
   for (int a = 0; a < PH::NA; a++)
@@ -218,6 +228,7 @@ __device__ __forceinline__ void contract(const RCtx &c, const float (&w)[4][RSha
       for (int t = 0; t < T; t++) c.red[((warp * PH::NA + a) * T + t) * kRUG + u] = acc[a][t];
   }
   __syncthreads();
+  if (c.tslot >= 0) trace_mark(*c.a, c.tslot + 2);
   for (int idx = threadIdx.x; idx < PH::NA * T * kRUG; idx += blockDim.x) {
     float v = 0.f;
 #pragma unroll
@@ -228,6 +239,7 @@ __device__ __forceinline__ void contract(const RCtx &c, const float (&w)[4][RSha
   const int t = threadIdx.x >> 4, uu = threadIdx.x & 15;
 #pragma unroll
   for (int a = 0; a < PH::NA; a++) s[a] = t < T ? c.red2[(a * T + t) * kRUG + uu] : 0.f;
+  if (c.tslot >= 0) trace_mark(*c.a, c.tslot + 3);
 }
 
 // ---------------------------------------------------------------------------
@@ -236,7 +248,7 @@ __device__ __forceinline__ void contract(const RCtx &c, const float (&w)[4][RSha
 template <int H, int MAXC>
 struct RTreeLstm {
   static constexpr int kPhases = 1;
-  using M = TileMetaT<RCfg<CX_TREELSTM, H, MAXC>::TMAX>;
+  using M = TileMetaT<2 * RCfg<CX_TREELSTM, H, MAXC>::TMAX>;
   __device__ static int leaf_gates(const FwdArgs &a, Gate *g) {
     g[0] = {a.w[0], 0, H, 0}; g[1] = {a.w[0], H, H, 0}; g[2] = {a.w[0], 2 * H, H, 0};
     return 3;
@@ -252,26 +264,33 @@ struct RTreeLstm {
     return 4;
   }
   __device__ static int leaf_lo(int first_leaf) { return first_leaf; }
+  // Leaf blocks: bookkeeping and Emb rows of a block of up to 2 TMAX leaves are
+  // loaded once (block()), then the block is contracted tile by tile (run()).
   struct Leaf {
-    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int pre;
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int b0;
     __device__ void meta(int i0, int cnt) { load_meta(*c.a, *m, i0, cnt, false, true, false, c.latch); }
+    __device__ void block(int cnt) {
+      const FwdArgs &a = *c.a;
+      gather_rows_c<1, H>(c.X, cnt, [&](int t, int) { return a.emb + (size_t)m->word[t] * H; });
+    }
     template <int T>
     __device__ __forceinline__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
-      if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
-      gather_rows_c<1, H>(c.X, cnt, [&](int t, int) { return a.emb + (size_t)m->word[t] * H; });
-      __syncthreads();
+      const int off = i0 - b0;
+      if (c.tslot >= 0) trace_mark(a, c.tslot + 1);
       float s[3];
-      contract<RLstmLeaf, H, T>(c, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+      contract<RLstmLeaf, H, T>(c, c.X + (size_t)(i0 - b0) * H, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
       const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
       if (t < cnt) {
-        float cc = sigmoidf_(s[0] + c.bias[u]) * tanhf(s[2] + c.bias[32 + u]);
-        float hh = sigmoidf_(s[1] + c.bias[16 + u]) * tanhf(cc);
-        size_t o = (size_t)m->own[t] * H + c.unit0 + u;
+        float cc = sigmoidf_(s[0] + c.bias[u]) * tanhf_(s[2] + c.bias[32 + u]);
+        float hh = sigmoidf_(s[1] + c.bias[16 + u]) * tanhf_(cc);
+        size_t o = (size_t)m->own[off + t] * H + c.unit0 + u;
         a.h_out[o] = hh;
         a.cbuf[o] = cc;
       }
       __syncthreads();
+      if (c.tslot >= 0) trace_mark(a, c.tslot + 4);
+      c.tslot = -1;
     }
   };
   struct Level {
@@ -281,6 +300,7 @@ struct RTreeLstm {
     __device__ __forceinline__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
       if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
+      if (c.tslot >= 0) trace_mark(a, c.tslot);
       gather_rows_c<MAXC, H>(c.X, cnt, [&](int t, int j) {
         int ci = m->cin[t][j];
         return ci >= 0 ? a.h_out + (size_t)ci * H : (const float *)nullptr;
@@ -291,22 +311,25 @@ struct RTreeLstm {
         c.cv[(t * kMaxC + k) * kRUG + u] = ci >= 0 ? __ldcg(a.cbuf + (size_t)ci * H + c.unit0 + u) : 0.f;
       }
       __syncthreads();
+      if (c.tslot >= 0) trace_mark(a, c.tslot + 1);
       float s[3 + MAXC];
-      contract<RLstmLevel<MAXC>, H, T>(c, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+      contract<RLstmLevel<MAXC>, H, T>(c, c.X, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
       const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
       if (t < cnt) {
-        float cc = sigmoidf_(s[0] + c.bias[u]) * tanhf(s[2] + c.bias[32 + u]);
+        float cc = sigmoidf_(s[0] + c.bias[u]) * tanhf_(s[2] + c.bias[32 + u]);
         const float bf = c.bias[48 + u];
         const int nc = m->nch[t];
 #pragma unroll
         for (int k = 0; k < MAXC; k++)
           if (k < nc) cc += sigmoidf_(s[3 + k] + bf) * c.cv[(t * kMaxC + k) * kRUG + u];
-        float hh = sigmoidf_(s[1] + c.bias[16 + u]) * tanhf(cc);
+        float hh = sigmoidf_(s[1] + c.bias[16 + u]) * tanhf_(cc);
         size_t o = (size_t)m->own[t] * H + c.unit0 + u;
         a.h_out[o] = hh;
         a.cbuf[o] = cc;
       }
       __syncthreads();
+      if (c.tslot >= 0) trace_mark(a, c.tslot + 4);
+      c.tslot = -1;
     }
   };
 };
@@ -314,7 +337,7 @@ struct RTreeLstm {
 template <int H, int MAXC>
 struct RTreeGru {
   static constexpr int kPhases = 2;
-  using M = TileMetaT<RCfg<CX_TREEGRU, H, MAXC>::TMAX>;
+  using M = TileMetaT<2 * RCfg<CX_TREEGRU, H, MAXC>::TMAX>;
   __device__ static int leaf_gates(const FwdArgs &a, Gate *g) {
     g[0] = {a.w[0], 0, H, 0}; g[1] = {a.w[0], H, H, 0};
     return 2;
@@ -329,21 +352,23 @@ struct RTreeGru {
   }
   __device__ static int leaf_lo(int first_leaf) { return first_leaf; }
   struct Leaf {
-    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int pre;
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int b0;
     __device__ void meta(int i0, int cnt) { load_meta(*c.a, *m, i0, cnt, false, true, false, c.latch); }
+    __device__ void block(int cnt) {
+      const FwdArgs &a = *c.a;
+      gather_rows_c<1, H>(c.X, cnt, [&](int t, int) { return a.emb + (size_t)m->word[t] * H; });
+    }
     template <int T>
     __device__ __forceinline__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
-      if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
-      gather_rows_c<1, H>(c.X, cnt, [&](int t, int) { return a.emb + (size_t)m->word[t] * H; });
-      __syncthreads();
+      const int off = i0 - b0;
       float s[2];
-      contract<RGruLeaf, H, T>(c, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+      contract<RGruLeaf, H, T>(c, c.X + (size_t)off * H, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
       const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
       if (t < cnt) {
         float z = sigmoidf_(s[0] + c.bias[u]);
-        float g = tanhf(s[1] + c.bias[32 + u]);
-        a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = (1.f - z) * g;
+        float g = tanhf_(s[1] + c.bias[32 + u]);
+        a.h_out[(size_t)m->own[off + t] * H + c.unit0 + u] = (1.f - z) * g;
       }
       __syncthreads();
     }
@@ -367,7 +392,7 @@ struct RTreeGru {
         });
         __syncthreads();
         float s[1 + MAXC];
-        contract<RGruA<MAXC>, H, T>(c, wr, s);
+        contract<RGruA<MAXC>, H, T>(c, c.X, wr, s);
         if (t < cnt) {
           const int unit = c.unit0 + u;
           float z = sigmoidf_(s[0] + c.bias[u]);
@@ -391,10 +416,10 @@ struct RTreeGru {
         gather_rows_c<1, H>(c.X, cnt, [&](int tt, int) { return a.sbuf + (size_t)m->own[tt] * H; });
         __syncthreads();
         float s[1];
-        contract<RGruB, H, T>(c, wr, s);
+        contract<RGruB, H, T>(c, c.X, wr, s);
         if (t < cnt) {
           size_t o = (size_t)m->own[t] * H + c.unit0 + u;
-          float g = tanhf(s[0] + c.bias[32 + u]);
+          float g = tanhf_(s[0] + c.bias[32 + u]);
           float z = __ldcg(a.zbuf + o), ht = __ldcg(a.h_out + o);
           a.h_out[o] = z * ht + (1.f - z) * g;
         }
@@ -407,7 +432,7 @@ struct RTreeGru {
 template <int H, int MAXC>
 struct RTreeFc {
   static constexpr int kPhases = 1;
-  using M = TileMetaT<RCfg<CX_TREEFC, H, MAXC>::TMAX>;
+  using M = TileMetaT<2 * RCfg<CX_TREEFC, H, MAXC>::TMAX>;
   __device__ static int leaf_gates(const FwdArgs &, Gate *) { return 0; }
   __device__ static int level_gates(const FwdArgs &a, Gate *g) {
     g[0] = {a.w[0], 0, 2 * H, 0}; g[1] = {a.w[0], 0, 2 * H, H};
@@ -418,19 +443,18 @@ struct RTreeFc {
     return 1;
   }
   __device__ static int leaf_lo(int first_leaf) { return first_leaf; }
-  struct Leaf {  // h = Emb[word] (pure gather)
-    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int pre;
+  struct Leaf {  // h = Emb[word] (pure gather, done for the whole block)
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int b0;
     __device__ void meta(int i0, int cnt) { load_meta(*c.a, *m, i0, cnt, false, true, false, c.latch); }
-    template <int T>
-    __device__ __forceinline__ void run(int i0, int cnt) {
+    __device__ void block(int cnt) {
       const FwdArgs &a = *c.a;
-      if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
       for (int idx = threadIdx.x; idx < cnt * kRUG; idx += blockDim.x) {
         int t = idx >> 4, u = idx & 15;
         a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = __ldg(a.emb + (size_t)m->word[t] * H + c.unit0 + u);
       }
-      __syncthreads();
     }
+    template <int T>
+    __device__ __forceinline__ void run(int, int) {}
   };
   struct Level {
     RCtx c; M *m; const float (*w)[RShape<H>::KC]; int phase, pre;
@@ -442,9 +466,9 @@ struct RTreeFc {
       gather_rows_c<2, H>(c.X, cnt, [&](int t, int j) { return a.h_out + (size_t)m->cin[t][j] * H; });
       __syncthreads();
       float s[1];
-      contract<RFcLevel, H, T>(c, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+      contract<RFcLevel, H, T>(c, c.X, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
       const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
-      if (t < cnt) a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = tanhf(s[0] + c.bias[u]);
+      if (t < cnt) a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = tanhf_(s[0] + c.bias[u]);
       __syncthreads();
     }
   };
@@ -453,7 +477,7 @@ struct RTreeFc {
 template <int H, int MAXC>
 struct RDagRnn {
   static constexpr int kPhases = 1;
-  using M = TileMetaT<RCfg<CX_DAGRNN, H, MAXC>::TMAX>;
+  using M = TileMetaT<2 * RCfg<CX_DAGRNN, H, MAXC>::TMAX>;
   // gates {W_x, U} resident through leaves and levels (input projections are
   // fused into each level instead of a separate all-node GEMM)
   __device__ static int leaf_gates(const FwdArgs &a, Gate *g) {
@@ -467,18 +491,20 @@ struct RDagRnn {
   }
   __device__ static int leaf_lo(int first_leaf) { return first_leaf; }
   struct Leaf {  // h = tanh(W_x x + b)
-    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int pre;
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int b0;
     __device__ void meta(int i0, int cnt) { load_meta(*c.a, *m, i0, cnt, false, true, false, c.latch); }
+    __device__ void block(int cnt) {
+      const FwdArgs &a = *c.a;
+      gather_rows_c<1, H>(c.X, cnt, [&](int t, int) { return a.emb + (size_t)m->word[t] * H; });
+    }
     template <int T>
     __device__ __forceinline__ void run(int i0, int cnt) {
       const FwdArgs &a = *c.a;
-      if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
-      gather_rows_c<1, H>(c.X, cnt, [&](int t, int) { return a.emb + (size_t)m->word[t] * H; });
-      __syncthreads();
+      const int off = i0 - b0;
       float s[1];
-      contract<RDagLeaf, H, T>(c, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+      contract<RDagLeaf, H, T>(c, c.X + (size_t)off * H, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
       const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
-      if (t < cnt) a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = tanhf(s[0] + c.bias[u]);
+      if (t < cnt) a.h_out[(size_t)m->own[off + t] * H + c.unit0 + u] = tanhf_(s[0] + c.bias[u]);
       __syncthreads();
     }
   };
@@ -496,9 +522,9 @@ struct RDagRnn {
       });
       __syncthreads();
       float s[1];
-      contract<RDagLevel<MAXC>, H, T>(c, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+      contract<RDagLevel<MAXC>, H, T>(c, c.X, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
       const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
-      if (t < cnt) a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = tanhf(s[0] + c.bias[u]);
+      if (t < cnt) a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = tanhf_(s[0] + c.bias[u]);
       __syncthreads();
     }
   };
@@ -532,6 +558,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rw_kernel(FwdArgs a) {
   ctx.gu = gu;
   ctx.unit0 = gu * kRUG;
   ctx.latch = gu == 0;
+  ctx.tslot = -1;
   unsigned epoch = 0;
   trace_mark(a, 0);
 
@@ -549,16 +576,28 @@ __global__ void __launch_bounds__(kRThreads, 1) rw_kernel(FwdArgs a) {
   float w[4][KC];
   Gate gs[4];
   // ---- leaf phase (specialised leaf loop nest) ------------------
+  // Leaves are processed in blocks of up to 2 TMAX: one bookkeeping pass and one
+  // Emb gather per block (the first block's overlap the weight loads).
   {
     int ng = C::leaf_gates(a, gs);
     load_wregs<Cfg::NG, KC>(w, gs, ng, ctx.unit0 + u, k0);
-    __syncthreads();
     trace_mark(a, 1);
     const int lo0 = C::leaf_lo(first_leaf);
     int lo, hi;
     chunk_of(n - lo0, a.Gn, gn, lo, hi);
-    typename C::Leaf f{ctx, &meta, w, -1};
-    for_tiles<Cfg::TMAX>(lo0 + lo, lo0 + hi, f);
+    typename C::Leaf f{ctx, &meta, w, 0};
+    f.c.tslot = a.trace ? 59 : -1;
+    for (int b0 = lo0 + lo; b0 < lo0 + hi; b0 += 2 * Cfg::TMAX) {
+      const int cntb = min(2 * Cfg::TMAX, lo0 + hi - b0);
+      __syncthreads();  // previous block's readers of meta / X are done
+      f.meta(b0, cntb);
+      __syncthreads();
+      if (f.c.tslot >= 0) trace_mark(a, f.c.tslot);
+      f.block(cntb);
+      __syncthreads();
+      f.b0 = b0;
+      for_tiles<Cfg::TMAX>(b0, b0 + cntb, f);
+    }
   }
   __syncthreads();
   trace_mark(a, 2);
@@ -582,6 +621,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rw_kernel(FwdArgs a) {
       }
       grid_wait(a.bar, gridDim.x, epoch);
       trace_mark(a, slot + 1);
+      f.c.tslot = a.trace ? 64 + 5 * ((l - 1) * C::kPhases + ph) : -1;
       for_tiles<Cfg::TMAX>(base + lo, base + hi, f);
     }
   }

@@ -51,6 +51,12 @@ print(f"{name}: ctas={info['ctas']} levels={nl} (us from earliest CTA entry)")
 print(f"entry        min {rel(tr[:,0].min()):7.2f} max {rel(tr[:,0].max()):7.2f}")
 print(f"leaf weights min {rel(tr[:,1].min()):7.2f} max {rel(tr[:,1].max()):7.2f}")
 print(f"leaf done    min {rel(tr[:,2].min()):7.2f} max {rel(tr[:,2].max()):7.2f}")
+lt = tr[:, 59:64]
+okl = (lt > 0).all(axis=1)
+if okl.any():
+    d = np.diff(lt[okl], axis=1).mean(axis=0) / 1000
+    m0 = (lt[okl][:, 0] - tr[okl, 1]).mean() / 1000
+    print(f"first leaf tile: meta {m0:5.2f} gather {d[0]:5.2f} fma {d[1]:5.2f} red {d[2]:5.2f} epi {d[3]:5.2f}")
 for j in range((nl - 1) * phases):
     arr, ex = tr[:, 3 + 2 * j], tr[:, 4 + 2 * j]
     b = 64 + 5 * j
