@@ -18,6 +18,7 @@ namespace {
 std::mutex g_mu;  // guards the device-attribute cache and kernel attribute setup
 unsigned long long *g_trace = nullptr;  // debug only (cx_debug_set_trace)
 int g_trace_slots = 0;
+unsigned long long *g_lin_trace = nullptr;  // debug only (cx_debug_set_lin_trace)
 
 int num_sms_current() {
   static int cached_dev = -1, cached_sms = 0;
@@ -101,6 +102,10 @@ cx_status cx_linearize(const int32_t *children, int32_t n, int32_t max_children,
   a.lbeg = out->level_begin;
   a.lsize = out->level_size;
   a.roots = out->roots;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    a.trace = g_lin_trace;
+  }
   int sms;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -201,6 +206,20 @@ cx_status cx_debug_set_trace(unsigned long long *buf, int32_t slots) {
   g_trace = buf;
   g_trace_slots = buf ? slots : 0;
   return CX_OK;
+}
+
+// Debug only: cx_linearize records %globaltimer per phase into buf[0..7].
+cx_status cx_debug_set_lin_trace(unsigned long long *buf) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_lin_trace = buf;
+  return CX_OK;
+}
+
+// Debug only: an empty kernel launch (measures launch overhead).
+cx_status cx_debug_empty(int32_t ctas, int32_t threads, int32_t coop, unsigned long long *t,
+                         void *stream) {
+  return cx::launch_empty(ctas, threads, coop, t, static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? CX_OK : CX_E_CUDA;
 }
 
 const char *cx_status_str(cx_status s) {

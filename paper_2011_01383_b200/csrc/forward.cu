@@ -905,6 +905,7 @@ static bool plan_for(int H, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return false;
     smem_set = smem;
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   }
   *Gu = gu;
   *Gn = num_sms / gu;

@@ -230,6 +230,7 @@ bool plan_h(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return false;
     set = true;
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   }
   *Gn = num_sms;
   *Gu = 1;

@@ -641,6 +641,7 @@ bool rplan(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return false;
     set = true;
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   }
   *Gu = H / kRUG;
   *Gn = num_sms / *Gu;

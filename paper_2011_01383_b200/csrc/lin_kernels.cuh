@@ -25,7 +25,17 @@ struct LinArgs {
   int32_t *hgt;    // n
   int32_t *cnt;    // budget
   int budget;
+  unsigned long long *trace;  // debug: %globaltimer per phase (CTA 0), NULL = off
 };
+
+__device__ __forceinline__ void lin_mark(const LinArgs &a, int s) {
+  if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[s] = t;
+    a.trace[8 + s] = clock64();
+  }
+}
 
 inline size_t lin_budget_entries(int n) { return 2 * (size_t)n + 4096; }
 
@@ -37,5 +47,6 @@ inline size_t lin_workspace_bytes(int n) {
 bool lin_use_single(int n, int maxc);
 size_t lin_single_smem_bytes(int n, int maxc);
 cudaError_t launch_linearize(const LinArgs &a, int num_sms, cudaStream_t stream);
+cudaError_t launch_empty(int ctas, int threads, int coop, unsigned long long *t, cudaStream_t stream);
 
 }  // namespace cx

@@ -26,7 +26,8 @@ namespace cx {
 
 namespace {
 
-constexpr int kLinThreads = 1024;
+constexpr int kLinThreads = 1024;   // multi-CTA path
+constexpr int kLinSingleThreads = 512;
 constexpr int kSegMin = 256;
 
 template <bool MULTI>
@@ -359,120 +360,160 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
 }
 
 
+__device__ __noinline__ void lin_latch(unsigned long long *err, int code, int v) {
+  atomicMin(err, ((unsigned long long)(unsigned)code << 32) | (unsigned)v);
+}
+
 // ---------------------------------------------------------------------------
 // Single-CTA linearizer: every working array lives in shared memory; the only
 // global traffic is one coalesced read of `children` and fire-and-forget
 // stores of the outputs (no dependent global round trips on the latency path).
 // smem (ints): ch[maxc*n] | hgt[n] | indeg[n] | perm[n] | inv[n] | lb[n] | cnt[kLinSmemCnt]
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kLinThreads, 1) lin_single_kernel(LinArgs a) {
+__global__ void __launch_bounds__(kLinSingleThreads, 1) lin_single_kernel(LinArgs a) {
   extern __shared__ int sm[];
   __shared__ unsigned long long s_err;
   __shared__ int s_tmp[33];
-  __shared__ int s_count, s_fin, s_round;
+  __shared__ int s_count, s_round;
   const int n = a.n, maxc = a.maxc, tid = threadIdx.x, nthr = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5;
   int *ch = sm, *hgt = ch + maxc * n, *indeg = hgt + n, *perm = indeg + n, *inv = perm + n,
-      *lb = inv + n, *cnt_s = lb + n;
+      *lb = inv + n, *ls_s = lb + n, *cnt_s = ls_s + n;
 
+  lin_mark(a, 0);
   for (int i = tid; i < maxc * n; i += nthr) ch[i] = __ldg(a.ch + i);
   for (int v = tid; v < n; v += nthr) {
     indeg[v] = 0;
     hgt[v] = -1;
+    perm[v] = -1;  // parent pointer (trees/sequences) until a4
   }
   if (tid == 0) {
     s_err = kNoError;
-    s_fin = 0;
     s_count = 0;
+    s_round = 0;
     s_tmp[32] = 0;
   }
   __syncthreads();
 
-  // a1: validation + in-degree; errors latched in shared memory (lowest key)
-  auto latch = [&](int code, int v) {
-    atomicMin(&s_err, ((unsigned long long)(unsigned)code << 32) | (unsigned)v);
-  };
+  // a1: validation + in-degree; errors latched in shared memory (lowest key).
+  // For trees and sequences the same pass records parent pointers (perm[] is
+  // free until a4) and the number of children (inv[]) for the walk-up below.
+  const bool tree_like = a.kind != CX_DAG;
+  int *parent = perm, *pending = inv;
   for (int v = tid; v < n; v += nthr) {
     bool absent = false;
+    int nc = 0;
     for (int k = 0; k < maxc; k++) {
       int c = ch[k * n + v];
       if (c == -1) {
         absent = true;
         continue;
       }
-      if (absent) latch(CX_E_CHILD_LAYOUT, v);
+      nc++;
+      if (absent) lin_latch(&s_err, CX_E_CHILD_LAYOUT, v);
       if (c < 0 || c >= n) {
-        latch(CX_E_CHILD_RANGE, v);
+        lin_latch(&s_err, CX_E_CHILD_RANGE, v);
         continue;
       }
       atomicAdd(&indeg[c], 1);
+      if (tree_like) parent[c] = v;
       for (int k2 = 0; k2 < k; k2++)
-        if (ch[k2 * n + v] == c) latch(CX_E_KIND, v);
+        if (ch[k2 * n + v] == c) lin_latch(&s_err, CX_E_KIND, v);
     }
+    if (nc == 0) hgt[v] = 0;
+    pending[v] = nc;
   }
   __syncthreads();
-  {
-    int local = 0;
-    for (int v = tid; v < n; v += nthr) {
-      if (a.kind != CX_DAG && indeg[v] > 1) latch(CX_E_KIND, v);
-      if (ch[v] == -1) {
-        hgt[v] = 0;
-        local++;
-      }
-    }
-    if (local) atomicAdd(&s_fin, local);
-  }
+  if (tree_like)
+    for (int v = tid; v < n; v += nthr)
+      if (indeg[v] > 1) lin_latch(&s_err, CX_E_KIND, v);
   __syncthreads();
+  lin_mark(a, 1);
   bool failed = s_err != kNoError;
 
-  // a2: heights, one round per level (round r finalises the nodes of height r)
+  // a2: heights. Trees/sequences: every leaf walks up its parent chain; at
+  // each parent it raises the height (atomicMax) and decrements the pending
+  // count -- only the last arriving child continues, so every node is
+  // finalised exactly once with h = 1 + max over its children, and no block
+  // barrier is needed per level. DAGs: Jacobi rounds, one __syncthreads_or
+  // each (round r finalises exactly the nodes of height r).
   int L = 0;
   if (!failed && n > 0) {
-    int r = 0;
-    int fin = s_fin;
-    while (fin < n) {
-      r++;
-      int local = 0;
+    int hmax = 0;
+    if (tree_like) {
       for (int v = tid; v < n; v += nthr) {
-        if (hgt[v] >= 0) continue;
-        bool ok = true;
-        for (int k = 0; k < maxc; k++) {
-          int c = ch[k * n + v];
-          if (c == -1) break;
-          int hc = hgt[c];
-          if (hc < 0 || hc >= r) {
-            ok = false;
-            break;
+        if (pending[v] != 0) continue;
+        int cur = v, hc = 0;
+        while (true) {
+          int p = parent[cur];
+          if (p < 0) break;
+          atomicMax(&hgt[p], hc + 1);
+          __threadfence_block();
+          if (atomicSub(&pending[p], 1) != 1) break;
+          __threadfence_block();
+          cur = p;
+          hc = atomicAdd(&hgt[p], 0);  // every child's atomicMax precedes its decrement
+        }
+        hmax = max(hmax, hc);
+      }
+      __syncthreads();
+      bool unfinished = false;
+      for (int v = tid; v < n; v += nthr)
+        if (pending[v] > 0) {  // on or above a cycle
+          lin_latch(&s_err, CX_E_CYCLE, v);
+          unfinished = true;
+        }
+      if (__syncthreads_or(unfinished)) failed = true;
+      for (int o = 16; o; o >>= 1) hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+      if (lane == 0) atomicMax(&s_round, hmax);
+      __syncthreads();
+      L = s_round + 1;
+    } else {
+      int r = 0;
+      bool progress = true;
+      while (progress) {
+        r++;
+        bool any = false;
+        for (int v = tid; v < n; v += nthr) {
+          if (hgt[v] >= 0) continue;
+          bool ok = true;
+          for (int k = 0; k < maxc; k++) {
+            int c = ch[k * n + v];
+            if (c == -1) break;
+            int hc = hgt[c];
+            if (hc < 0 || hc >= r) {
+              ok = false;
+              break;
+            }
+          }
+          if (ok) {
+            hgt[v] = r;
+            any = true;
           }
         }
-        if (ok) {
-          hgt[v] = r;
-          local++;
+        progress = __syncthreads_or(any);
+      }
+      bool unfinished = false;
+      for (int v = tid; v < n; v += nthr)
+        if (hgt[v] < 0) {
+          lin_latch(&s_err, CX_E_CYCLE, v);
+          unfinished = true;
         }
-      }
-      if (tid == 0) s_round = 0;
-      __syncthreads();
-      if (local) atomicAdd(&s_round, local);
-      __syncthreads();
-      int got = s_round;
-      __syncthreads();
-      if (got == 0) {
-        for (int v = tid; v < n; v += nthr)
-          if (hgt[v] < 0) latch(CX_E_CYCLE, v);
-        __syncthreads();
-        failed = true;
-        break;
-      }
-      fin += got;
+      if (__syncthreads_or(unfinished)) failed = true;
+      L = r;
     }
-    L = r + 1;
   }
+  lin_mark(a, 2);
 
   if (!failed && n > 0) {
-    // a3: one id segment per warp; counts per (level, segment) + roots row
-    const int seg = 32 * ((((n + 31) / 32) + 31) / 32);
-    const int S = (n + seg - 1) / seg;
-    int *cnt = (long long)(L + 1) * S <= kLinSmemCnt ? cnt_s : a.cnt;
+    // a3: per-(level, id segment) counts + roots row, always in shared memory:
+    // S segments of `seg` ids (one warp each), S shrinks when L is large.
+    const int nw = nthr >> 5;
+    int S = min(nw, max(1, kLinSmemCnt / (L + 1)));
+    S = min(S, (n + 31) / 32);
+    const int seg = 32 * ((((n + 31) / 32) + S - 1) / S);
+    S = (n + seg - 1) / seg;
+    int *cnt = cnt_s;
     for (int e = tid; e < (L + 1) * S; e += nthr) cnt[e] = 0;
     __syncthreads();
     const unsigned lt = (1u << lane) - 1u;
@@ -490,66 +531,88 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_single_kernel(LinArgs a) {
       }
     }
     __syncthreads();
-    // exclusive scan over (level L-1 .. 0) x (segment), then over the roots row
-    {
-      const int E = L * S;
-      const int per = (E + nthr - 1) / nthr;
-      const int e0 = tid * per, e1 = min(E, e0 + per);
-      int sum = 0;
-      for (int e = e0; e < e1; e++) sum += cnt[(L - 1 - e / S) * S + e % S];
-      int total;
-      int off = block_exclusive_scan(sum, total, s_tmp);
-      for (int e = e0; e < e1; e++) {
-        int idx = (L - 1 - e / S) * S + e % S;
-        int c = cnt[idx];
-        cnt[idx] = off;
-        if (e % S == 0) lb[L - 1 - e / S] = off;
-        off += c;
+    lin_mark(a, 3);
+    // exclusive scan in the order (level L-1 .. 0) x (segment 0 .. S-1): warp w
+    // takes levels w, w + nw, ...; level totals, then a warp-0 scan over them
+    for (int l = warp; l < L; l += nw) {
+      int x = lane < S ? cnt[l * S + lane] : 0;  // S <= 32 when L < kLinSmemCnt/32
+      int incl = x;
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
       }
-      const int per2 = (S + nthr - 1) / nthr;
-      const int r0 = tid * per2, r1 = min(S, r0 + per2);
-      int rs = 0;
-      for (int e = r0; e < r1; e++) rs += cnt[L * S + e];
-      int rtotal;
-      int roff = block_exclusive_scan(rs, rtotal, s_tmp);
-      for (int e = r0; e < r1; e++) {
-        int c = cnt[L * S + e];
-        cnt[L * S + e] = roff;
-        roff += c;
+      if (S <= 32) {
+        if (lane < S) cnt[l * S + lane] = incl - x;  // within-level offset
+        if (lane == 31) ls_s[l] = incl;               // level size
+      } else {
+        // wide tables (tiny L): serial per level
+        if (lane == 0) {
+          int acc = 0;
+          for (int s2 = 0; s2 < S; s2++) {
+            int c = cnt[l * S + s2];
+            cnt[l * S + s2] = acc;
+            acc += c;
+          }
+          ls_s[l] = acc;
+        }
       }
-      if (tid == 0) s_count = rtotal;
+    }
+    if (warp == nw - 1) {  // roots row
+      int acc = 0;
+      for (int b = 0; b < S; b += 32) {
+        int x = b + lane < S ? cnt[L * S + b + lane] : 0;
+        int incl = x;
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (b + lane < S) cnt[L * S + b + lane] = acc + incl - x;
+        acc += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) s_count = acc;
     }
     __syncthreads();
-    {
-      int mx = 0;
-      for (int l = tid; l < L; l += nthr) {
-        int b = lb[l], e = l > 0 ? lb[l - 1] : n;
-        a.lbeg[l] = b;
-        a.lsize[l] = e - b;
-        mx = max(mx, e - b);
+    // level begins: exclusive scan of level sizes from level L-1 down (warp 0)
+    if (warp == 0) {
+      int acc = 0, mx = 0;
+      for (int b = 0; b < L; b += 32) {
+        int l = L - 1 - (b + lane);
+        int x = l >= 0 ? ls_s[l] : 0;
+        int incl = x;
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (l >= 0) {
+          lb[l] = acc + incl - x;
+          a.lbeg[l] = acc + incl - x;
+          a.lsize[l] = x;
+          mx = max(mx, x);
+        }
+        acc += __shfl_sync(0xffffffffu, incl, 31);
       }
       for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0) atomicMax(&s_tmp[32], mx);
+      if (lane == 0) s_tmp[32] = mx;
     }
+    __syncthreads();
+    lin_mark(a, 4);
     // a4: stable scatter (each warp walks its segment in id order)
     if (warp < S) {
       const int s = warp, end = min(n, (s + 1) * seg);
+      int rbase = cnt[L * S + s];
       for (int base = s * seg; base < end; base += 32) {
         int v = base + lane;
         bool valid = v < end;
         int hv = valid ? hgt[v] : -1;
         unsigned m = __match_any_sync(0xffffffffu, hv);
         int leader = __ffs(m) - 1;
-        int b = (valid && lane == leader) ? cnt[hv * S + s] : 0;
+        int b = (valid && lane == leader) ? lb[hv] + cnt[hv * S + s] : 0;
         b = __shfl_sync(0xffffffffu, b, leader);
         int nid = b + __popc(m & lt);
         bool isroot = valid && indeg[v] == 0;
         unsigned rb = __ballot_sync(0xffffffffu, isroot);
-        int rbase = (lane == 0 && rb) ? cnt[L * S + s] : 0;
-        rbase = __shfl_sync(0xffffffffu, rbase, 0);
         __syncwarp();
-        if (valid && lane == leader) cnt[hv * S + s] = b + __popc(m);
-        if (lane == 0 && rb) cnt[L * S + s] = rbase + __popc(rb);
+        if (valid && lane == leader) cnt[hv * S + s] += __popc(m);
         if (valid) {
           perm[nid] = v;
           inv[v] = nid;
@@ -558,10 +621,12 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_single_kernel(LinArgs a) {
           a.hnew[nid] = hv;
           if (isroot) a.roots[rbase + __popc(rb & lt)] = nid;
         }
+        rbase += __popc(rb);
         __syncwarp();
       }
     }
     __syncthreads();
+    lin_mark(a, 5);
     // a5: remap children to new ids
     for (int i = tid; i < n; i += nthr) {
       int v = perm[i];
@@ -574,6 +639,7 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_single_kernel(LinArgs a) {
 
   // header (one thread; plain stores)
   __syncthreads();
+  lin_mark(a, 6);
   if (tid == 0) {
     cx_lin_header *h = a.hdr;
     unsigned long long key = s_err;
@@ -596,10 +662,33 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_single_kernel(LinArgs a) {
   }
 }
 
+__global__ void empty_kernel(unsigned long long *t) {
+  if (t && threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    *t = v;
+  }
+}
+
 }  // namespace
 
+// Debug: launch an empty kernel (ctas x threads, optional cooperative attribute)
+cudaError_t launch_empty(int ctas, int threads, int coop, unsigned long long *t, cudaStream_t stream) {
+  void *params[] = {&t};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(threads);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = coop;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, (const void *)empty_kernel, params);
+}
+
 size_t lin_single_smem_bytes(int n, int maxc) {
-  return sizeof(int) * ((size_t)(maxc + 5) * n + kLinSmemCnt);
+  return sizeof(int) * ((size_t)(maxc + 6) * n + kLinSmemCnt);
 }
 
 bool lin_use_single(int n, int maxc) {
@@ -611,11 +700,13 @@ cudaError_t launch_linearize(const LinArgs &a, int num_sms, cudaStream_t stream)
   if (!attr_done) {
     cudaFuncSetAttribute(lin_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kLinSmemMax);
+    cudaFuncSetAttribute(lin_single_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(lin_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr_done = true;
   }
   if (lin_use_single(a.n, a.maxc)) {
     size_t smem = lin_single_smem_bytes(a.n, a.maxc);
-    lin_single_kernel<<<1, kLinThreads, smem, stream>>>(a);
+    lin_single_kernel<<<1, kLinSingleThreads, smem, stream>>>(a);
     return cudaGetLastError();
   }
   LinArgs args = a;
