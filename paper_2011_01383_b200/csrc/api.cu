@@ -40,6 +40,7 @@ int forward_path() {
   if (!e) return 0;
   if (!std::strcmp(e, "rw")) return 1;
   if (!std::strcmp(e, "smem")) return 2;
+  if (!std::strcmp(e, "cluster")) return 3;
   return 0;
 }
 
@@ -162,6 +163,7 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
   a.roots = lin->roots;
   a.n = n;
   a.maxc = lin->max_children;
+  a.kind = lin->kind;
   a.H = m->hidden;
   a.V = m->vocab;
   a.emb = emb;

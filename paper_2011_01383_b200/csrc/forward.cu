@@ -890,6 +890,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) fwd_kernel(FwdArgs a) {
 // MV-RNN lives in forward_mvrnn.cu, the register-weight path in forward_rw.cu
 bool mvrnn_plan(int H, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
 bool rw_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
+bool cluster_plan(int cell, int H, int maxc, int n, int roots, FwdPlan *plan, int *Gn, int *Gu);
 
 template <int CELL, int MAXC, class C>
 static bool plan_for(int H, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
@@ -924,6 +925,7 @@ bool fwd_plan(int cell, int H, int maxc, int n, int path, int num_sms, FwdPlan *
   // per CTA minimise the re-gathering of child rows across unit groups.
   const bool rw_ok = (cell == CX_TREELSTM || cell == CX_TREEGRU || cell == CX_TREEFC ||
                       cell == CX_DAGRNN) && (H == 64 || H == 128 || H == 256 || H == 512);
+  if ((path == 0 || path == 3) && cluster_plan(cell, H, maxc, n, 0, plan, Gn, Gu)) return true;
   const bool want_rw = path == 1 || (path == 0 && n <= kRwMaxNodes);
   if (rw_ok && want_rw && rw_plan(cell, H, maxc, num_sms, plan, Gn, Gu)) return true;
   const bool weighted = cell != CX_TREERNN && cell != CX_MVRNN;
@@ -977,8 +979,15 @@ cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream) 
   cfg.dynamicSmemBytes = plan.smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  if (plan.cluster > 1) {  // independent clusters: no grid barrier, no co-residency needed
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = plan.cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelExC(&cfg, plan.kernel, params);

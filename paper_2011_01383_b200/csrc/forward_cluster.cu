@@ -1,0 +1,454 @@
+// forward_cluster.cu -- latency path: one thread-block cluster per group of
+// structures, hardware cluster barriers between levels, child state exchanged
+// through distributed shared memory (DSMEM).
+//
+// Structures of a batch are independent (property P.3),
+// so a level barrier only has to cover the CTAs that evaluate the same
+// structures. A cluster of CS = H / 16 CTAs (16 at H = 256) owns whole
+// structures (structure g -> cluster g mod #clusters) and each of its CTAs
+// owns 16 hidden units with register-resident weights (rw_engine.cuh):
+//   * every CTA keeps, in its own shared memory, its 16-unit slice of h (and of
+//     the TreeLSTM memory cell / DAG-RNN input projection) for every node;
+//   * a tile of T nodes pulls its children's full rows from the CS slices
+//     (DSMEM loads, the paper's rnn_cache of App. A.3), contracts
+//     them against the register weights and writes its own slice locally;
+//   * one barrier.cluster (release/acquire) per level -- ~0.3 us measured --
+//     replaces the ~1.1 us grid barrier, and nothing goes through L2 on the
+//     level-to-level path (h_out is written for the caller only).
+// The structure a node belongs to is found in the prologue by propagating
+// root indices top-down over the levels; for a DAG whose structures share
+// nodes, every node falls back to cluster 0 (still correct).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <type_traits>
+
+#include "rw_engine.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace cx {
+namespace {
+using namespace fwd;
+using namespace rw;
+
+constexpr int kCUnits = kRUG;  // units per CTA (16)
+
+template <int MAXC>
+struct CDagLevel : PhBase<2, MAXC, MAXC, 1, 1> {  // U h~ (gate 1 of {W_x, U})
+  __device__ static constexpr int g(int p) { return 1; }
+  __device__ static constexpr int v(int p) { return MAXC; }
+  __device__ static constexpr int a(int p) { return 0; }
+};
+
+template <int CELL, int MAXC>
+struct CCfg;
+template <int MAXC>
+struct CCfg<CX_TREELSTM, MAXC> {
+  static constexpr int TMAX = 8, NVMAX = MAXC, NAMAX = 3 + MAXC;
+};
+template <int MAXC>
+struct CCfg<CX_DAGRNN, MAXC> {
+  static constexpr int TMAX = 16, NVMAX = MAXC, NAMAX = 1;
+};
+
+template <int CELL, int H, int MAXC>
+struct CLayout {
+  using C = CCfg<CELL, MAXC>;
+  static constexpr size_t x_floats = (size_t)C::TMAX * (C::NVMAX > 2 ? C::NVMAX : 2) * H;
+  static constexpr size_t red_floats = (size_t)kRNW * C::NAMAX * C::TMAX * kRUG;
+  static constexpr size_t red2_floats = (size_t)C::NAMAX * C::TMAX * kRUG;
+  static constexpr size_t cv_floats = (size_t)C::TMAX * kMaxC * kRUG;
+  // per node: h slice + aux slice (floats) and perm, label, maxc children, list (ints)
+  static size_t bytes(int n, int maxc, int L) {
+    return sizeof(float) * (x_floats + red_floats + red2_floats + cv_floats + 2 * (size_t)kCUnits * n) +
+           sizeof(int) * ((size_t)(3 + maxc) * n + 2 * (size_t)L + 64);
+  }
+};
+
+// Max nodes the cluster path takes (per-node slices live in shared memory).
+constexpr int kClusterMaxN = 768;
+
+struct CS {  // shared-memory carve of one CTA
+  float *X, *red, *red2, *cv, *hsl, *aux;
+  int *perm, *lab, *chn, *list, *lbeg, *lsize;
+};
+
+// Pull the full H-rows of `rows` (new ids, -1 = zeros) from the CS slices into X.
+template <int H, int NV>
+__device__ __forceinline__ void pull_rows(cg::cluster_group &cl, const CS &s, int cnt,
+                                          const int (*rows)[kMaxC]) {
+  constexpr int CSZ = H / kCUnits;
+  constexpr int Q = kCUnits / 4;  // float4 per slice
+  const int total = cnt * NV * CSZ * Q;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    int q = idx % Q, r = idx / Q;
+    int peer = r % CSZ, tr = r / CSZ;
+    int j = tr % NV, t = tr / NV;
+    int v = rows[t][j];
+    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (v >= 0) {
+      const float *remote = cl.map_shared_rank(s.hsl, peer);
+      val = *reinterpret_cast<const float4 *>(remote + (size_t)v * kCUnits + 4 * q);
+    }
+    *reinterpret_cast<float4 *>(s.X + (size_t)(t * NV + j) * H + peer * kCUnits + 4 * q) = val;
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int CELL, int H, int MAXC>
+__global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
+  using Cfg = CCfg<CELL, MAXC>;
+  using Lay = CLayout<CELL, H, MAXC>;
+  constexpr int KC = RShape<H>::KC;
+  constexpr int TMAX = Cfg::TMAX;
+  extern __shared__ __align__(16) float smem[];
+  __shared__ int s_rows[2 * TMAX][kMaxC];
+  __shared__ int s_nodes[2 * TMAX];
+  __shared__ int s_word[2 * TMAX];
+  __shared__ int s_cnt, s_bad;
+  __shared__ float s_bias[4 * kCUnits];
+
+  cg::cluster_group cl = cg::this_cluster();
+  if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
+  const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n, R = a.hdr->num_roots;
+  const int maxc = a.maxc;
+  const int crank = (int)cl.block_rank();
+  const int cid = blockIdx.x / (int)cl.num_blocks(), ncl = gridDim.x / (int)cl.num_blocks();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int u = lane & 15, k0 = (warp * 2 + (lane >> 4)) * KC;
+  const int unit0 = crank * kCUnits;
+  const bool latch = crank == 0;
+  trace_mark(a, 0);
+
+  CS s;
+  s.X = smem;
+  s.red = s.X + Lay::x_floats;
+  s.red2 = s.red + Lay::red_floats;
+  s.cv = s.red2 + Lay::red2_floats;
+  s.hsl = s.cv + Lay::cv_floats;
+  s.aux = s.hsl + (size_t)kCUnits * n;
+  s.perm = reinterpret_cast<int *>(s.aux + (size_t)kCUnits * n);
+  s.lab = s.perm + n;
+  s.list = s.lab + n;
+  s.chn = s.list + n;
+  s.lbeg = s.chn + (size_t)maxc * n;
+  s.lsize = s.lbeg + L;
+
+  RCtx ctx;
+  ctx.a = &a;
+  ctx.X = s.X;
+  ctx.red = s.red;
+  ctx.red2 = s.red2;
+  ctx.cv = s.cv;
+  ctx.bias = s_bias;
+  ctx.gn = cid;
+  ctx.gu = crank;
+  ctx.unit0 = unit0;
+  ctx.latch = latch;
+  ctx.tslot = -1;
+
+  // ---- weights -> registers (first the leaf / projection gates) -----------
+  float w[4][KC];
+  Gate gs[4];
+  int ng;
+  if constexpr (CELL == CX_TREELSTM) {
+    gs[0] = {a.w[0], 0, H, 0}; gs[1] = {a.w[0], H, H, 0}; gs[2] = {a.w[0], 2 * H, H, 0};
+    ng = 3;
+  } else {
+    gs[0] = {a.w[0], 0, H, 0}; gs[1] = {a.w[1], 0, H, 0};
+    ng = 2;
+  }
+  load_wregs<4, KC>(w, gs, ng, unit0 + u, k0);
+  if constexpr (CELL == CX_TREELSTM) {
+    if (tid < 4 * kCUnits) {
+      int g = tid / kCUnits, uu = tid % kCUnits;
+      const float *b = g < 3 ? a.w[2] + g * H : a.w[4];
+      s_bias[tid] = __ldg(b + unit0 + uu);
+    }
+  } else {
+    if (tid < kCUnits) s_bias[tid] = __ldg(a.w[2] + unit0 + tid);
+  }
+
+  // ---- prologue: structure labels (root index, propagated top-down) --------
+  for (int l = tid; l < L; l += blockDim.x) {
+    s.lbeg[l] = __ldg(a.lbeg + l);
+    s.lsize[l] = __ldg(a.lsize + l);
+  }
+  for (int v = tid; v < n; v += blockDim.x) {
+    s.perm[v] = __ldg(a.perm + v);
+    s.lab[v] = INT_MAX;
+  }
+  for (int e = tid; e < maxc * n; e += blockDim.x) s.chn[e] = __ldg(a.chn + e);
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (int r = tid; r < R; r += blockDim.x) s.lab[__ldg(a.roots + r)] = r;
+  __syncthreads();
+  for (int l = L - 1; l >= 1; l--) {
+    const int b = s.lbeg[l], M = s.lsize[l];
+    for (int i = b + tid; i < b + M; i += blockDim.x) {
+      const int li = s.lab[i];
+      for (int k = 0; k < maxc; k++) {
+        int c = s.chn[k * n + i];
+        if (c < 0) break;
+        atomicMin(&s.lab[c], li);
+      }
+    }
+    __syncthreads();
+  }
+  if (a.kind == CX_DAG) {  // structures sharing a node: one cluster does everything
+    bool bad = false;
+    for (int i = tid; i < first_leaf; i += blockDim.x)
+      for (int k = 0; k < maxc; k++) {
+        int c = s.chn[k * n + i];
+        if (c < 0) break;
+        if (s.lab[c] != s.lab[i]) bad = true;
+      }
+    if (__syncthreads_or(bad))
+      for (int v = tid; v < n; v += blockDim.x) s.lab[v] = 0;
+    __syncthreads();
+  }
+  trace_mark(a, 1);
+
+  // work list of this cluster's nodes in [b, b + M) (order irrelevant: every
+  // slice is addressed by new id)
+  auto build_list = [&](int b, int M) -> int {
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    for (int i0 = b; i0 < b + M; i0 += blockDim.x) {
+      int i = i0 + tid;
+      bool mine = i < b + M && (s.lab[i] % ncl) == cid;
+      unsigned m = __ballot_sync(0xffffffffu, mine);
+      int base = 0;
+      if (lane == 0 && m) base = atomicAdd(&s_cnt, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (mine) s.list[base + __popc(m & ((1u << lane) - 1u))] = i;
+    }
+    __syncthreads();
+    return s_cnt;
+  };
+
+  // ---- leaf / projection phase ----------------------------------------------
+  {
+    // TreeLSTM: leaves. DAG-RNN: every node (input projection P = W_x x + b;
+    // leaves finish with h = tanh(P)).
+    const int b = CELL == CX_DAGRNN ? 0 : first_leaf;
+    const int cnt = build_list(b, n - b);
+    for (int b0 = 0; b0 < cnt; b0 += 2 * TMAX) {
+      const int cntb = min(2 * TMAX, cnt - b0);
+      if (tid < cntb) {
+        int v = s.list[b0 + tid];
+        int own = s.perm[v];
+        int wd = __ldg(a.words + own);
+        if (wd < 0 || wd >= a.V) {
+          if (latch) latch_error(a.hdr, CX_E_WORD_RANGE, own);
+          wd = 0;
+        }
+        s_nodes[tid] = v;
+        s_word[tid] = wd;
+      }
+      __syncthreads();
+      gather_rows_c<1, H>(s.X, cntb, [&](int t, int) { return a.emb + (size_t)s_word[t] * H; });
+      __syncthreads();
+      for (int t0 = 0; t0 < cntb; t0 += TMAX) {
+        const int cntt = min(TMAX, cntb - t0);
+        auto tile = [&](auto tt) {
+          constexpr int T = decltype(tt)::value;
+          const int t = tid >> 4;
+          if constexpr (CELL == CX_TREELSTM) {
+            float sacc[3];
+            contract<RLstmLeaf, H, T>(ctx, s.X + (size_t)t0 * H, w, sacc);
+            if (t < cntt) {
+              const int v = s_nodes[t0 + t];
+              float cc = sigmoidf_(sacc[0] + s_bias[u]) * tanhf_(sacc[2] + s_bias[32 + u]);
+              float hh = sigmoidf_(sacc[1] + s_bias[16 + u]) * tanhf_(cc);
+              s.hsl[(size_t)v * kCUnits + u] = hh;
+              s.aux[(size_t)v * kCUnits + u] = cc;
+              const size_t o = (size_t)s.perm[v] * H + unit0 + u;
+              a.h_out[o] = hh;
+              if (a.aux_out) a.aux_out[o] = cc;
+            }
+          } else {
+            float sacc[1];
+            contract<RDagLeaf, H, T>(ctx, s.X + (size_t)t0 * H, w, sacc);
+            if (t < cntt) {
+              const int v = s_nodes[t0 + t];
+              const float p = sacc[0] + s_bias[u];
+              s.aux[(size_t)v * kCUnits + u] = p;
+              if (v >= first_leaf) {
+                const float hh = tanhf_(p);
+                s.hsl[(size_t)v * kCUnits + u] = hh;
+                a.h_out[(size_t)s.perm[v] * H + unit0 + u] = hh;
+              }
+            }
+          }
+          __syncthreads();
+        };
+        if (cntt > 8) tile(std::integral_constant<int, (TMAX >= 16 ? 16 : TMAX)>{});
+        else if (cntt > 4) tile(std::integral_constant<int, 8>{});
+        else if (cntt > 2) tile(std::integral_constant<int, 4>{});
+        else if (cntt == 2) tile(std::integral_constant<int, 2>{});
+        else tile(std::integral_constant<int, 1>{});
+      }
+    }
+  }
+  // recurrent gates -> registers
+  if constexpr (CELL == CX_TREELSTM) {
+    gs[0] = {a.w[1], 0, H, 0}; gs[1] = {a.w[1], H, H, 0}; gs[2] = {a.w[1], 2 * H, H, 0};
+    gs[3] = {a.w[3], 0, H, 0};
+    load_wregs<4, KC>(w, gs, 4, unit0 + u, k0);
+  }
+  trace_mark(a, 2);
+  cl.sync();
+
+  // ---- internal levels: one cluster barrier per level -----------------------
+  for (int l = 1; l < L; l++) {
+    const int cnt = build_list(s.lbeg[l], s.lsize[l]);
+    for (int t0 = 0; t0 < cnt; t0 += TMAX) {
+      const int cntt = min(TMAX, cnt - t0);
+      if (tid < cntt) {
+        int v = s.list[t0 + tid];
+        s_nodes[tid] = v;
+        for (int k = 0; k < kMaxC; k++) s_rows[tid][k] = k < maxc ? s.chn[k * n + v] : -1;
+      }
+      __syncthreads();
+      pull_rows<H, Cfg::NVMAX>(cl, s, cntt, s_rows);
+      if constexpr (CELL == CX_TREELSTM) {
+        for (int idx = tid; idx < cntt * MAXC * kCUnits; idx += blockDim.x) {
+          int t = idx / (MAXC * kCUnits), r = idx - t * MAXC * kCUnits, k = r >> 4, uu = r & 15;
+          int c = s_rows[t][k];
+          s.cv[(t * kMaxC + k) * kCUnits + uu] = c >= 0 ? s.aux[(size_t)c * kCUnits + uu] : 0.f;
+        }
+      }
+      __syncthreads();
+      auto tile = [&](auto tt) {
+        constexpr int T = decltype(tt)::value;
+        const int t = tid >> 4;
+        if constexpr (CELL == CX_TREELSTM) {
+          float sacc[3 + MAXC];
+          contract<RLstmLevel<MAXC>, H, T>(ctx, s.X, w, sacc);
+          if (t < cntt) {
+            const int v = s_nodes[t];
+            float cc = sigmoidf_(sacc[0] + s_bias[u]) * tanhf_(sacc[2] + s_bias[32 + u]);
+            const float bf = s_bias[48 + u];
+#pragma unroll
+            for (int k = 0; k < MAXC; k++)
+              if (s_rows[t][k] >= 0) cc += sigmoidf_(sacc[3 + k] + bf) * s.cv[(t * kMaxC + k) * kCUnits + u];
+            float hh = sigmoidf_(sacc[1] + s_bias[16 + u]) * tanhf_(cc);
+            s.hsl[(size_t)v * kCUnits + u] = hh;
+            s.aux[(size_t)v * kCUnits + u] = cc;
+            const size_t o = (size_t)s.perm[v] * H + unit0 + u;
+            a.h_out[o] = hh;
+            if (a.aux_out) a.aux_out[o] = cc;
+          }
+        } else {
+          float sacc[1];
+          contract<CDagLevel<MAXC>, H, T>(ctx, s.X, w, sacc);
+          if (t < cntt) {
+            const int v = s_nodes[t];
+            const float hh = tanhf_(sacc[0] + s.aux[(size_t)v * kCUnits + u]);
+            s.hsl[(size_t)v * kCUnits + u] = hh;
+            a.h_out[(size_t)s.perm[v] * H + unit0 + u] = hh;
+          }
+        }
+        __syncthreads();
+      };
+      if (cntt > 8) tile(std::integral_constant<int, (TMAX >= 16 ? 16 : TMAX)>{});
+      else if (cntt > 4) tile(std::integral_constant<int, 8>{});
+      else if (cntt > 2) tile(std::integral_constant<int, 4>{});
+      else if (cntt == 2) tile(std::integral_constant<int, 2>{});
+      else tile(std::integral_constant<int, 1>{});
+    }
+    cl.sync();
+    trace_mark(a, 3 + l);
+  }
+
+  // ---- packed root states (this CTA's units of this cluster's roots) --------
+  if (a.root_out) {
+    for (int r = warp; r < R; r += kRNW) {
+      const int v = __ldg(a.roots + r);
+      if ((s.lab[v] % ncl) != cid) continue;
+      if (lane < kCUnits) a.root_out[(size_t)r * H + unit0 + lane] = s.hsl[(size_t)v * kCUnits + lane];
+    }
+  }
+  trace_mark(a, a.trace_slots - 1);
+  publish_and_exit(a);
+}
+
+template <int CELL, int H, int MAXC>
+bool cplan_one(int n, int maxc, int L_bound, int num_roots_hint, FwdPlan *p, int *Gn, int *Gu) {
+  constexpr int CSZ = H / kCUnits;
+  auto k = ck_kernel<CELL, H, MAXC>;
+  const size_t smem = CLayout<CELL, H, MAXC>::bytes(n, maxc, L_bound);
+  if (smem > 227 * 1024) return false;
+  static int cached_max = -1;
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+      return false;
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (CSZ > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    smem_set = 227 * 1024;
+  }
+  if (cached_max < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CSZ * 8);
+    cfg.blockDim = dim3(kRThreads);
+    cfg.dynamicSmemBytes = 227 * 1024;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CSZ;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int m = 0;
+    if (cudaOccupancyMaxActiveClusters(&m, (const void *)k, &cfg) != cudaSuccess) m = 0;
+    cudaGetLastError();
+    cached_max = m;
+  }
+  if (cached_max < 1) return false;
+  int ncl = cached_max;
+  if (num_roots_hint > 0 && num_roots_hint < ncl) ncl = num_roots_hint;
+  *Gn = ncl;
+  *Gu = CSZ;
+  p->ctas = ncl * CSZ;
+  p->threads = kRThreads;
+  p->smem = smem;
+  p->kernel = (const void *)k;
+  p->cluster = CSZ;
+  return true;
+}
+
+template <int CELL, int H>
+bool cplan_cell(int n, int maxc, int L_bound, int roots, FwdPlan *p, int *Gn, int *Gu) {
+  if (maxc <= 1) return cplan_one<CELL, H, 1>(n, maxc, L_bound, roots, p, Gn, Gu);
+  if (maxc <= 2) return cplan_one<CELL, H, 2>(n, maxc, L_bound, roots, p, Gn, Gu);
+  if (maxc <= 4) return cplan_one<CELL, H, 4>(n, maxc, L_bound, roots, p, Gn, Gu);
+  return false;
+}
+
+}  // namespace
+
+// Cluster path for small batches: TreeLSTM and DAG-RNN, H in {64, 128, 256},
+// n <= kClusterMaxN. `roots` (<= 0: unknown) caps the number of clusters.
+bool cluster_plan(int cell, int H, int maxc, int n, int roots, FwdPlan *p, int *Gn, int *Gu) {
+  if (n > kClusterMaxN || n < 1) return false;
+  const int L_bound = n;  // level arrays sized for the worst case
+  switch (cell) {
+    case CX_TREELSTM:
+      if (H == 256) return cplan_cell<CX_TREELSTM, 256>(n, maxc, L_bound, roots, p, Gn, Gu);
+      if (H == 128) return cplan_cell<CX_TREELSTM, 128>(n, maxc, L_bound, roots, p, Gn, Gu);
+      if (H == 64) return cplan_cell<CX_TREELSTM, 64>(n, maxc, L_bound, roots, p, Gn, Gu);
+      return false;
+    case CX_DAGRNN:
+      if (H == 256) return cplan_cell<CX_DAGRNN, 256>(n, maxc, L_bound, roots, p, Gn, Gu);
+      if (H == 128) return cplan_cell<CX_DAGRNN, 128>(n, maxc, L_bound, roots, p, Gn, Gu);
+      if (H == 64) return cplan_cell<CX_DAGRNN, 64>(n, maxc, L_bound, roots, p, Gn, Gu);
+      return false;
+  }
+  return false;
+}
+
+}  // namespace cx

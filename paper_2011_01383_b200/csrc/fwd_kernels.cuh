@@ -16,6 +16,7 @@ struct FwdArgs {
   cx_lin_header *hdr;
   const int32_t *perm, *chn, *lbeg, *lsize, *hnew, *roots;
   int n, maxc, H, V;
+  int kind;  // cx_kind of the linearization
   const float *emb;
   const int32_t *words;
   const float *w[8];
@@ -44,11 +45,14 @@ struct FwdPlan {
   int ctas, threads;
   size_t smem;
   const void *kernel;
+  int cluster = 1;  // > 1: thread-block clusters of this size (no cooperative launch)
 };
 
 // Returns false (CX_E_UNSUPPORTED) when no instantiation covers the model.
-// path: 0 = automatic (register weights when n <= kRwMaxNodes), 1 = force the
-// register-weight kernel, 2 = force the shared-memory-weight kernel.
+// path: 0 = automatic (cluster kernel for small batches of TreeLSTM / DAG-RNN,
+// register weights when n <= kRwMaxNodes, shared-memory weights above),
+// 1 = force the register-weight kernel, 2 = force the shared-memory-weight
+// kernel, 3 = force the cluster kernel.
 constexpr int kRwMaxNodes = 32768;
 bool fwd_plan(int cell, int H, int maxc, int n, int path, int num_sms, FwdPlan *plan, int *Gn,
               int *Gu);

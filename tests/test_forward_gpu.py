@@ -18,7 +18,7 @@ def cx():
     return m
 
 
-@pytest.fixture(params=["auto", "rw", "smem"])
+@pytest.fixture(params=["auto", "rw", "smem", "cluster"])
 def path(request, monkeypatch):
     """Run a test through each forward kernel family (CX_FORWARD_PATH is read
     by libcx on every cx_forward call)."""
