@@ -89,6 +89,11 @@ typedef struct {
   int32_t *level_begin;    /* n        first new id of level l (l < num_levels)    */
   int32_t *level_size;     /* n        nodes in level l (l < num_levels)           */
   int32_t *roots;          /* n        new ids of roots, ascending input id        */
+  int32_t *structure;      /* n        structure of each new id: index r in roots[]
+                                       of the root that owns it (trees/sequences: its
+                                       unique root; DAGs: the smallest r whose root
+                                       reaches it). Independent structures (P.3,
+                                       P:759-761) are the unit of sharding.            */
   int32_t n;               /* (host) number of nodes                               */
   int32_t max_children;    /* (host) declared maximum children per node            */
   int32_t kind;            /* (host) cx_kind                                       */

@@ -62,7 +62,7 @@ def _load():
             lib = ctypes.CDLL(_LIB_PATH)
             P = ctypes.c_void_p
             I = ctypes.c_int32
-            lib.oracle_linearize.argtypes = [P, I, I, I, ctypes.POINTER(LinHeader)] + [P] * 7
+            lib.oracle_linearize.argtypes = [P, I, I, I, ctypes.POINTER(LinHeader)] + [P] * 8
             lib.oracle_linearize.restype = ctypes.c_int
             lib.oracle_forward.argtypes = [I, I, I, P, P, P, P, I, I, P, P, ctypes.POINTER(I)]
             lib.oracle_forward.restype = ctypes.c_int
@@ -79,7 +79,8 @@ def _ptr(a):
 
 def linearize(children, kind: int) -> dict:
     """Returns dict with header fields and arrays perm, inv, children, height,
-    level_begin, level_size (trimmed to num_levels) and roots (trimmed)."""
+    level_begin, level_size (trimmed to num_levels), roots (trimmed) and
+    structure (per new id: index in roots of the owning root)."""
     lib = _load()
     ch = np.ascontiguousarray(children, dtype=np.int32)
     maxc, n = ch.shape
@@ -91,13 +92,14 @@ def linearize(children, kind: int) -> dict:
     lb = np.zeros(size, np.int32)
     ls = np.zeros(size, np.int32)
     roots = np.zeros(size, np.int32)
+    struct = np.zeros(size, np.int32)
     hdr = LinHeader()
     lib.oracle_linearize(_ptr(ch), n, maxc, kind, ctypes.byref(hdr), _ptr(perm), _ptr(inv),
-                         _ptr(chn), _ptr(hgt), _ptr(lb), _ptr(ls), _ptr(roots))
+                         _ptr(chn), _ptr(hgt), _ptr(lb), _ptr(ls), _ptr(roots), _ptr(struct))
     out = {f: getattr(hdr, f) for f, _ in LinHeader._fields_}
     L, R = hdr.num_levels, hdr.num_roots
     out.update(perm=perm[:n], inv=inv[:n], children=chn[:, :n], height=hgt[:n],
-               level_begin=lb[:L], level_size=ls[:L], roots=roots[:R])
+               level_begin=lb[:L], level_size=ls[:L], roots=roots[:R], structure=struct[:n])
     return out
 
 

@@ -119,7 +119,7 @@ static int32_t heights(const int32_t *ch, int32_t n, int32_t maxc, int32_t *heig
 int oracle_linearize(const int32_t *children, int32_t n, int32_t maxc, int32_t kind,
                      oracle_lin_header *hdr, int32_t *perm, int32_t *inv,
                      int32_t *children_new, int32_t *height_new, int32_t *level_begin,
-                     int32_t *level_size, int32_t *roots) {
+                     int32_t *level_size, int32_t *roots, int32_t *structure) {
   memset(hdr, 0, sizeof *hdr);
   hdr->bad_node = -1;
   hdr->num_nodes = n;
@@ -170,6 +170,30 @@ int oracle_linearize(const int32_t *children, int32_t n, int32_t maxc, int32_t k
   int32_t r = 0;
   for (int32_t v = 0; v < n; v++)
     if (indeg[v] == 0) roots[r++] = inv[v];
+  /* structures (P.3 P:759-761: independent structures): roots in ascending
+     index r each claim every not-yet-claimed node they reach (explicit-stack
+     DFS), so a node belongs to the smallest r whose root reaches it. */
+  {
+    int32_t *own = malloc(sizeof(int32_t) * (size_t)n);
+    int32_t *stk = malloc(sizeof(int32_t) * (size_t)n);
+    for (int32_t v = 0; v < n; v++) own[v] = -1;
+    for (int32_t q = 0; q < r; q++) {
+      int32_t sp = 0, root = perm[roots[q]];
+      if (own[root] >= 0) continue;
+      own[root] = q;
+      stk[sp++] = root;
+      while (sp > 0) {
+        int32_t v = stk[--sp];
+        for (int k = 0; k < maxc; k++) {
+          int32_t c = children[(int64_t)k * n + v];
+          if (c == -1) break;
+          if (own[c] < 0) { own[c] = q; stk[sp++] = c; }
+        }
+      }
+    }
+    for (int32_t i = 0; i < n; i++) structure[i] = own[perm[i]];
+    free(own); free(stk);
+  }
 
   hdr->status = OR_OK;
   hdr->num_levels = L;

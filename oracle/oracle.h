@@ -32,11 +32,13 @@ typedef struct {
 /* Linearize: children is SoA [maxc][n] of input ids (-1 = absent).
  * Outputs (all caller-allocated, n or maxc*n entries): perm (new -> input),
  * inv (input -> new), children_new [maxc][n] (new ids), height_new [n],
- * level_begin [n], level_size [n], roots [n]. Returns hdr->status. */
+ * level_begin [n], level_size [n], roots [n], structure [n] (per new id: the
+ * index r in roots[] of the first root, in ascending r, whose descendants
+ * include the node). Returns hdr->status. */
 int oracle_linearize(const int32_t *children, int32_t n, int32_t maxc, int32_t kind,
                      oracle_lin_header *hdr, int32_t *perm, int32_t *inv,
                      int32_t *children_new, int32_t *height_new, int32_t *level_begin,
-                     int32_t *level_size, int32_t *roots);
+                     int32_t *level_size, int32_t *roots, int32_t *structure);
 
 /* Forward: naive memoized recursion in INPUT numbering. weights[] are the
  * fp32 tensors in cx_weights order. h_out [n][H] double;

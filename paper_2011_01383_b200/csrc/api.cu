@@ -72,7 +72,8 @@ cx_status cx_linearize(const int32_t *children, int32_t n, int32_t max_children,
   if (kind != CX_SEQUENCE && kind != CX_TREE && kind != CX_DAG) return CX_E_ARG;
   if (kind == CX_SEQUENCE && max_children != 1) return CX_E_ARG;
   if (!out->header || (n > 0 && (!out->perm || !out->inv || !out->children || !out->height ||
-                                 !out->level_begin || !out->level_size || !out->roots)))
+                                 !out->level_begin || !out->level_size || !out->roots ||
+                                 !out->structure)))
     return CX_E_ARG;
   if (!workspace || workspace_bytes < cx::lin_workspace_bytes(n)) return CX_E_WORKSPACE;
   out->n = n;
@@ -103,6 +104,7 @@ cx_status cx_linearize(const int32_t *children, int32_t n, int32_t max_children,
   a.lbeg = out->level_begin;
   a.lsize = out->level_size;
   a.roots = out->roots;
+  a.sid = out->structure;
   {
     std::lock_guard<std::mutex> lk(g_mu);
     a.trace = g_lin_trace;
@@ -161,6 +163,7 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
   a.lsize = lin->level_size;
   a.hnew = lin->height;
   a.roots = lin->roots;
+  a.sid = lin->structure;
   a.n = n;
   a.maxc = lin->max_children;
   a.kind = lin->kind;

@@ -907,6 +907,7 @@ static bool plan_for(int H, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
       return false;
     smem_set = smem;
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaGetLastError();
   }
   *Gu = gu;
   *Gn = num_sms / gu;

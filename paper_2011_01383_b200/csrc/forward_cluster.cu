@@ -15,9 +15,9 @@
 //   * one barrier.cluster (release/acquire) per level -- ~0.3 us measured --
 //     replaces the ~1.1 us grid barrier, and nothing goes through L2 on the
 //     level-to-level path (h_out is written for the caller only).
-// The structure a node belongs to is found in the prologue by propagating
-// root indices top-down over the levels; for a DAG whose structures share
-// nodes, every node falls back to cluster 0 (still correct).
+// The structure of every node comes from cx_linearize (structure[]); for a
+// DAG whose structures share nodes, every node falls back to cluster 0
+// (still correct, just serial over one cluster).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -46,17 +46,18 @@ template <int CELL, int MAXC>
 struct CCfg;
 template <int MAXC>
 struct CCfg<CX_TREELSTM, MAXC> {
-  static constexpr int TMAX = 8, NVMAX = MAXC, NAMAX = 3 + MAXC;
+  static constexpr int TMAX = 8, NVMAX = MAXC, NAMAX = 3 + MAXC, LEAFB = 48;
 };
 template <int MAXC>
 struct CCfg<CX_DAGRNN, MAXC> {
-  static constexpr int TMAX = 16, NVMAX = MAXC, NAMAX = 1;
+  static constexpr int TMAX = 16, NVMAX = MAXC, NAMAX = 1, LEAFB = 32;
 };
 
 template <int CELL, int H, int MAXC>
 struct CLayout {
   using C = CCfg<CELL, MAXC>;
-  static constexpr size_t x_floats = (size_t)C::TMAX * (C::NVMAX > 2 ? C::NVMAX : 2) * H;
+  static constexpr size_t xl = (size_t)C::TMAX * C::NVMAX * H, xb = (size_t)C::LEAFB * H;
+  static constexpr size_t x_floats = xl > xb ? xl : xb;
   static constexpr size_t red_floats = (size_t)kRNW * C::NAMAX * C::TMAX * kRUG;
   static constexpr size_t red2_floats = (size_t)C::NAMAX * C::TMAX * kRUG;
   static constexpr size_t cv_floats = (size_t)C::TMAX * kMaxC * kRUG;
@@ -104,10 +105,11 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   constexpr int KC = RShape<H>::KC;
   constexpr int TMAX = Cfg::TMAX;
   extern __shared__ __align__(16) float smem[];
-  __shared__ int s_rows[2 * TMAX][kMaxC];
-  __shared__ int s_nodes[2 * TMAX];
-  __shared__ int s_word[2 * TMAX];
-  __shared__ int s_cnt, s_bad;
+  constexpr int LEAFB = Cfg::LEAFB;
+  __shared__ int s_rows[TMAX][kMaxC];
+  __shared__ int s_nodes[LEAFB];
+  __shared__ int s_word[LEAFB];
+  __shared__ int s_cnt;
   __shared__ float s_bias[4 * kCUnits];
 
   cg::cluster_group cl = cg::this_cluster();
@@ -178,25 +180,10 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   }
   for (int v = tid; v < n; v += blockDim.x) {
     s.perm[v] = __ldg(a.perm + v);
-    s.lab[v] = INT_MAX;
+    s.lab[v] = __ldg(a.sid + v);  // structure index (cx_linearize)
   }
   for (int e = tid; e < maxc * n; e += blockDim.x) s.chn[e] = __ldg(a.chn + e);
-  if (tid == 0) s_bad = 0;
   __syncthreads();
-  for (int r = tid; r < R; r += blockDim.x) s.lab[__ldg(a.roots + r)] = r;
-  __syncthreads();
-  for (int l = L - 1; l >= 1; l--) {
-    const int b = s.lbeg[l], M = s.lsize[l];
-    for (int i = b + tid; i < b + M; i += blockDim.x) {
-      const int li = s.lab[i];
-      for (int k = 0; k < maxc; k++) {
-        int c = s.chn[k * n + i];
-        if (c < 0) break;
-        atomicMin(&s.lab[c], li);
-      }
-    }
-    __syncthreads();
-  }
   if (a.kind == CX_DAG) {  // structures sharing a node: one cluster does everything
     bool bad = false;
     for (int i = tid; i < first_leaf; i += blockDim.x)
@@ -235,8 +222,8 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     // leaves finish with h = tanh(P)).
     const int b = CELL == CX_DAGRNN ? 0 : first_leaf;
     const int cnt = build_list(b, n - b);
-    for (int b0 = 0; b0 < cnt; b0 += 2 * TMAX) {
-      const int cntb = min(2 * TMAX, cnt - b0);
+    for (int b0 = 0; b0 < cnt; b0 += LEAFB) {
+      const int cntb = min(LEAFB, cnt - b0);
       if (tid < cntb) {
         int v = s.list[b0 + tid];
         int own = s.perm[v];
@@ -249,8 +236,10 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
         s_word[tid] = wd;
       }
       __syncthreads();
+      if (b0 == 0) trace_mark(a, 12);
       gather_rows_c<1, H>(s.X, cntb, [&](int t, int) { return a.emb + (size_t)s_word[t] * H; });
       __syncthreads();
+      if (b0 == 0) trace_mark(a, 13);
       for (int t0 = 0; t0 < cntb; t0 += TMAX) {
         const int cntt = min(TMAX, cntb - t0);
         auto tile = [&](auto tt) {
@@ -304,7 +293,9 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
 
   // ---- internal levels: one cluster barrier per level -----------------------
   for (int l = 1; l < L; l++) {
+    const int tb = 24 + 5 * l;  // debug trace slots of this level's first tile
     const int cnt = build_list(s.lbeg[l], s.lsize[l]);
+    if (l < 20) trace_mark(a, tb);
     for (int t0 = 0; t0 < cnt; t0 += TMAX) {
       const int cntt = min(TMAX, cnt - t0);
       if (tid < cntt) {
@@ -313,6 +304,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
         for (int k = 0; k < kMaxC; k++) s_rows[tid][k] = k < maxc ? s.chn[k * n + v] : -1;
       }
       __syncthreads();
+      if (t0 == 0 && l < 20) trace_mark(a, tb + 1);
       pull_rows<H, Cfg::NVMAX>(cl, s, cntt, s_rows);
       if constexpr (CELL == CX_TREELSTM) {
         for (int idx = tid; idx < cntt * MAXC * kCUnits; idx += blockDim.x) {
@@ -322,12 +314,14 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
         }
       }
       __syncthreads();
+      if (t0 == 0 && l < 20) trace_mark(a, tb + 2);
       auto tile = [&](auto tt) {
         constexpr int T = decltype(tt)::value;
         const int t = tid >> 4;
         if constexpr (CELL == CX_TREELSTM) {
           float sacc[3 + MAXC];
           contract<RLstmLevel<MAXC>, H, T>(ctx, s.X, w, sacc);
+          if (t0 == 0 && l < 20) trace_mark(a, tb + 3);
           if (t < cntt) {
             const int v = s_nodes[t];
             float cc = sigmoidf_(sacc[0] + s_bias[u]) * tanhf_(sacc[2] + s_bias[32 + u]);
@@ -359,6 +353,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       else if (cntt > 2) tile(std::integral_constant<int, 4>{});
       else if (cntt == 2) tile(std::integral_constant<int, 2>{});
       else tile(std::integral_constant<int, 1>{});
+      if (t0 == 0 && l < 20) trace_mark(a, tb + 4);
     }
     cl.sync();
     trace_mark(a, 3 + l);
@@ -385,17 +380,20 @@ bool cplan_one(int n, int maxc, int L_bound, int num_roots_hint, FwdPlan *p, int
   static int cached_max = -1;
   static size_t smem_set = 0;
   if (smem > smem_set) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+      cudaGetLastError();
       return false;
+    }
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (CSZ > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    smem_set = 227 * 1024;
+    cudaGetLastError();
+    smem_set = smem;
   }
   if (cached_max < 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CSZ * 8);
     cfg.blockDim = dim3(kRThreads);
-    cfg.dynamicSmemBytes = 227 * 1024;
+    cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CSZ;

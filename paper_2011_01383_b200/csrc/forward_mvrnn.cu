@@ -231,6 +231,7 @@ bool plan_h(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
       return false;
     set = true;
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaGetLastError();
   }
   *Gn = num_sms;
   *Gu = 1;

@@ -428,6 +428,7 @@ bool rplan(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
       return false;
     set = true;
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaGetLastError();
   }
   *Gu = H / kRUG;
   *Gn = num_sms / *Gu;

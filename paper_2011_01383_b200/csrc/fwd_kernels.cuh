@@ -14,7 +14,7 @@ constexpr int kUG = 32;           // hidden units per CTA (lane = unit)
 
 struct FwdArgs {
   cx_lin_header *hdr;
-  const int32_t *perm, *chn, *lbeg, *lsize, *hnew, *roots;
+  const int32_t *perm, *chn, *lbeg, *lsize, *hnew, *roots, *sid;
   int n, maxc, H, V;
   int kind;  // cx_kind of the linearization
   const float *emb;

@@ -17,7 +17,7 @@ struct LinArgs {
   const int32_t *ch;  // [maxc][n] input ids
   int n, maxc, kind;
   cx_lin_header *hdr;
-  int32_t *perm, *inv, *chn, *hnew, *lbeg, *lsize, *roots;
+  int32_t *perm, *inv, *chn, *hnew, *lbeg, *lsize, *roots, *sid;
   // workspace
   GridBar *bar;
   int32_t *misc;   // 32 ints

@@ -19,6 +19,8 @@
 // common.cuh (b4096 and large DAGs).
 #include <cuda_runtime.h>
 
+#include <climits>
+
 #include "common.cuh"
 #include "lin_kernels.cuh"
 
@@ -100,6 +102,7 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
   for (int v = tid; v < n; v += nthr) {
     indeg[v] = 0;
     hgt[v] = -1;
+    if constexpr (MULTI) a.sid[v] = INT_MAX;
   }
   // Finished-node counts. Multi-CTA: misc[3] counts leaves and round r adds
   // into misc[r % 3]; a slot is read by every CTA right after barrier r and
@@ -309,7 +312,10 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
           a.perm[nid] = v;
           a.inv[v] = nid;
           a.hnew[nid] = hv;
-          if (isroot) a.roots[rbase + __popc(rb & lt)] = nid;
+          if (isroot) {
+            a.roots[rbase + __popc(rb & lt)] = nid;
+            a.sid[nid] = rbase + __popc(rb & lt);
+          }
         }
         if (lane == 0 && rb) cnt[L * S + s] = rbase + __popc(rb);
         __syncwarp();
@@ -323,6 +329,19 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
       for (int k = 0; k < maxc; k++) {
         int c = ch[k * n + v];
         a.chn[(long long)k * n + i] = c == -1 ? -1 : ld_dyn<MULTI>(&a.inv[c]);
+      }
+    }
+    // ---- P8 (a6): structures, root index propagated top-down ---------------
+    for (int l = L - 1; l >= 1; l--) {
+      lsync<MULTI>(a.bar, epoch);
+      const int b = ld_dyn<MULTI>(&a.lbeg[l]), e = b + ld_dyn<MULTI>(&a.lsize[l]);
+      for (int i = b + tid; i < e; i += nthr) {
+        const int si = ld_dyn<MULTI>(&a.sid[i]);
+        for (int k = 0; k < maxc; k++) {
+          int c = ld_dyn<MULTI>(&a.chn[(long long)k * n + i]);
+          if (c == -1) break;
+          atomicMin(&a.sid[c], si);
+        }
       }
     }
   }
@@ -378,7 +397,7 @@ __global__ void __launch_bounds__(kLinSingleThreads, 1) lin_single_kernel(LinArg
   const int n = a.n, maxc = a.maxc, tid = threadIdx.x, nthr = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5;
   int *ch = sm, *hgt = ch + maxc * n, *indeg = hgt + n, *perm = indeg + n, *inv = perm + n,
-      *lb = inv + n, *ls_s = lb + n, *cnt_s = ls_s + n;
+      *lb = inv + n, *ls_s = lb + n, *sid = ls_s + n, *cnt_s = sid + n;
 
   lin_mark(a, 0);
   for (int i = tid; i < maxc * n; i += nthr) ch[i] = __ldg(a.ch + i);
@@ -386,6 +405,7 @@ __global__ void __launch_bounds__(kLinSingleThreads, 1) lin_single_kernel(LinArg
     indeg[v] = 0;
     hgt[v] = -1;
     perm[v] = -1;  // parent pointer (trees/sequences) until a4
+    sid[v] = INT_MAX;
   }
   if (tid == 0) {
     s_err = kNoError;
@@ -619,7 +639,10 @@ __global__ void __launch_bounds__(kLinSingleThreads, 1) lin_single_kernel(LinArg
           a.perm[nid] = v;
           a.inv[v] = nid;
           a.hnew[nid] = hv;
-          if (isroot) a.roots[rbase + __popc(rb & lt)] = nid;
+          if (isroot) {
+            a.roots[rbase + __popc(rb & lt)] = nid;
+            sid[nid] = rbase + __popc(rb & lt);
+          }
         }
         rbase += __popc(rb);
         __syncwarp();
@@ -635,6 +658,21 @@ __global__ void __launch_bounds__(kLinSingleThreads, 1) lin_single_kernel(LinArg
         a.chn[(long long)k * n + i] = c == -1 ? -1 : inv[c];
       }
     }
+    // a6: structure of every node: root index propagated top-down (minimum
+    // over the roots reaching it), one level per round
+    for (int l = L - 1; l >= 1; l--) {
+      const int b = lb[l], e = b + ls_s[l];
+      for (int i = b + tid; i < e; i += nthr) {
+        const int si = sid[i], v = perm[i];
+        for (int k = 0; k < maxc; k++) {
+          int c = ch[k * n + v];
+          if (c == -1) break;
+          atomicMin(&sid[inv[c]], si);
+        }
+      }
+      __syncthreads();
+    }
+    for (int i = tid; i < n; i += nthr) a.sid[i] = sid[i];
   }
 
   // header (one thread; plain stores)
@@ -688,7 +726,7 @@ cudaError_t launch_empty(int ctas, int threads, int coop, unsigned long long *t,
 }
 
 size_t lin_single_smem_bytes(int n, int maxc) {
-  return sizeof(int) * ((size_t)(maxc + 6) * n + kLinSmemCnt);
+  return sizeof(int) * ((size_t)(maxc + 7) * n + kLinSmemCnt);
 }
 
 bool lin_use_single(int n, int maxc) {
@@ -706,6 +744,7 @@ cudaError_t launch_linearize(const LinArgs &a, int num_sms, cudaStream_t stream)
   }
   if (lin_use_single(a.n, a.maxc)) {
     size_t smem = lin_single_smem_bytes(a.n, a.maxc);
+    cudaGetLastError();  // drop stale non-sticky errors of unrelated API calls
     lin_single_kernel<<<1, kLinSingleThreads, smem, stream>>>(a);
     return cudaGetLastError();
   }

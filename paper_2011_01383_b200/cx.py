@@ -38,7 +38,8 @@ class CxError(RuntimeError):
 
 class _Lin(ctypes.Structure):
     _fields_ = [(f, ctypes.c_void_p) for f in (
-        "header", "perm", "inv", "children", "height", "level_begin", "level_size", "roots")] + [
+        "header", "perm", "inv", "children", "height", "level_begin", "level_size", "roots",
+        "structure")] + [
         ("n", ctypes.c_int32), ("max_children", ctypes.c_int32), ("kind", ctypes.c_int32)]
 
 
@@ -130,6 +131,7 @@ class Linearization:
     level_begin: torch.Tensor
     level_size: torch.Tensor
     roots: torch.Tensor
+    structure: torch.Tensor   # int32 [n]: index in roots of the owning root
     n: int
     max_children: int
     kind: int
@@ -147,10 +149,12 @@ def alloc_linearization(n: int, max_children: int, kind: int, device) -> Lineari
     mk = lambda *s: torch.empty(*s, dtype=torch.int32, device=device)
     lin = Linearization(header=torch.zeros(10, dtype=torch.int32, device=device), perm=mk(size),
                         inv=mk(size), children=mk(max_children, size), height=mk(size),
-                        level_begin=mk(size), level_size=mk(size), roots=mk(size), n=n,
+                        level_begin=mk(size), level_size=mk(size), roots=mk(size),
+                        structure=mk(size), n=n,
                         max_children=max_children, kind=kind)
     c = _Lin()
-    for f in ("header", "perm", "inv", "children", "height", "level_begin", "level_size", "roots"):
+    for f in ("header", "perm", "inv", "children", "height", "level_begin", "level_size", "roots",
+              "structure"):
         setattr(c, f, getattr(lin, f).data_ptr())
     lin.c = c
     lin.children = lin.children[:, :n]

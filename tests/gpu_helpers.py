@@ -24,7 +24,8 @@ def lin_to_numpy(lin):
     out.update(perm=lin.perm[:n].cpu().numpy(), inv=lin.inv[:n].cpu().numpy(),
                children=lin.children.cpu().numpy(), height=lin.height[:n].cpu().numpy(),
                level_begin=lin.level_begin[:L].cpu().numpy(),
-               level_size=lin.level_size[:L].cpu().numpy(), roots=lin.roots[:R].cpu().numpy())
+               level_size=lin.level_size[:L].cpu().numpy(), roots=lin.roots[:R].cpu().numpy(),
+               structure=lin.structure[:n].cpu().numpy())
     return out
 
 
@@ -39,7 +40,8 @@ def assert_lin_equal(dev, ref):
         return
     for f in LIN_FIELDS:
         assert dev[f] == ref[f], (f, dev[f], ref[f])
-    for f in ("perm", "inv", "children", "height", "level_begin", "level_size", "roots"):
+    for f in ("perm", "inv", "children", "height", "level_begin", "level_size", "roots",
+              "structure"):
         assert np.array_equal(np.asarray(dev[f]), np.asarray(ref[f])), f
 
 

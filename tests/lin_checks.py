@@ -80,5 +80,17 @@ def check_invariants(children, lin):
                 indeg[children[k, v]] += 1
     want_roots = [inv[v] for v in range(n) if indeg[v] == 0]
     assert list(np.asarray(lin["roots"][:lin["num_roots"]])) == want_roots
+    # structures: roots own themselves; a node belongs to the smallest root
+    # index among its parents' structures (trees: exactly its parent's)
+    if "structure" in lin:
+        st = np.asarray(lin["structure"], dtype=np.int64)
+        R = lin["num_roots"]
+        assert ((st >= 0) & (st < max(R, 1))).all()
+        for r in range(R):
+            assert st[lin["roots"][r]] == r
+        for i in range(n):
+            pars = [p for p in range(n) for k in range(maxc) if chn[k, p] == i] if n <= 64 else None
+            if pars:
+                assert st[i] == min(st[p] for p in pars)
     # within-level independence: no node is a child of a node
     # in its own level -- implied by hn[child] < hn[parent] above

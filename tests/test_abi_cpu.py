@@ -47,7 +47,7 @@ def test_status_strings(cxmod):
 def _lin_struct(cx, n=4, maxc=2, null_header=False):
     c = cx._cx._Lin()
     for i, f in enumerate(("header", "perm", "inv", "children", "height", "level_begin",
-                           "level_size", "roots")):
+                           "level_size", "roots", "structure")):
         setattr(c, f, 0 if (null_header and f == "header") else 0x1000 + 64 * i)
     return c
 
