@@ -65,17 +65,15 @@ def make_inputs(name, rank, world, seed=0):
     else:
         ch, off = synth.grid_dags(total)
     kind = synth.DAG if gen == "grid" else synth.TREE
-    # this rank's contiguous block of structures, ids rebased to 0
-    per = total // world
-    g0, g1 = rank * per, (rank + 1) * per if rank < world - 1 else total
-    a, b = int(off[g0]), int(off[g1])
-    sub = ch[:, a:b].copy()
-    sub[sub >= 0] -= a
-    words = synth.word_ids(ch, V, seed, all_nodes=(cell == synth.DAGRNN))[a:b].copy()
+    # this rank's contiguous block of structures, ids rebased to 0 (shard.py)
+    from paper_2011_01383_b200 import shard
+    words_all = synth.word_ids(ch, V, seed, all_nodes=(cell == synth.DAGRNN))
+    sub, words, (g0, g1), a = shard.shard(ch, off, rank, world, words_all)
     emb = synth.embedding(V, H, seed)
     ws = [w for _, w in synth.weights(cell, H, V)]
     return dict(children=sub, kind=kind, words=words, emb=emb, weights=ws, cell=cell, H=H, V=V,
-                batch=g1 - g0, total=total, scaling=scaling, offsets=off[g0:g1 + 1] - a)
+                batch=g1 - g0, total=total, scaling=scaling, offsets=off[g0:g1 + 1] - a,
+                g0=g0, g1=g1)
 
 
 def algorithmic_work(cell, H, n, n_leaves, n_internal, batch, maxc=2):
@@ -317,6 +315,24 @@ def run_gpu(args, rank, world, local_rank):
     torch.cuda.synchronize()
     eager_ms = [x.elapsed_time(y) for x, y in eager_ms]
 
+    # optional NCCL all-gather of the packed root states (the only collective)
+    allgather_us = None
+    if world > 1 and args.allgather:
+        from paper_2011_01383_b200 import shard
+        for _ in range(3):
+            shard.all_gather_roots(roots, inp["total"])
+        torch.cuda.synchronize()
+        dist.barrier()
+        ag = []
+        for _ in range(50):
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            shard.all_gather_roots(roots, inp["total"])
+            a1.record(stream)
+            ag.append((a0, a1))
+        torch.cuda.synchronize()
+        allgather_us = statistics.median(x.elapsed_time(y) for x, y in ag) * 1e3
+
     # ---- end to end through the public API with host buffers --------------
     ch_host = torch.as_tensor(np.ascontiguousarray(ch_np, dtype=np.int32)).pin_memory()
     w_host = torch.as_tensor(np.ascontiguousarray(inp["words"], dtype=np.int32)).pin_memory()
@@ -387,6 +403,7 @@ def run_gpu(args, rank, world, local_rank):
         "eager_latency_us": statistics.median(eager_ms) * 1e3,
         "timing": "CUDA graph replay of linearize+forward per step, events on the launch stream",
         "gpu_launches": 2 * args.steps,
+        "allgather_roots_us": allgather_us,
         "launch": info,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FMA_PEAK_TFLOPS,
                      "unit": "TFLOP/s", "frac": achieved / FMA_PEAK_TFLOPS, "traffic": traffic,
@@ -411,6 +428,8 @@ def main():
     p.add_argument("--workload", default="cfg2_treelstm_b10", choices=sorted(WORKLOADS))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--allgather", action="store_true",
+                   help="N>1: also time the NCCL all-gather of root states")
     args = p.parse_args()
     args.warmup = max(args.warmup, 3)
 
