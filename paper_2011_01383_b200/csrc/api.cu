@@ -41,6 +41,7 @@ int forward_path() {
   if (!std::strcmp(e, "rw")) return 1;
   if (!std::strcmp(e, "smem")) return 2;
   if (!std::strcmp(e, "cluster")) return 3;
+  if (!std::strcmp(e, "big")) return 4;
   return 0;
 }
 
@@ -175,7 +176,8 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
   a.h_out = h_out;
   a.aux_out = aux_out;
   a.root_out = root_out;
-  switch (m->cell) {
+  if (plan.big) a.pbuf = buf;  // hs, st [n][H] + words [n] (forward_big.cu)
+  else switch (m->cell) {
     case CX_TREELSTM: a.cbuf = aux_out ? aux_out : buf; break;
     case CX_TREEGRU: a.zbuf = buf; a.sbuf = buf + N * H; break;
     case CX_DAGRNN: a.pbuf = buf; break;

@@ -28,10 +28,13 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "fwd_common.cuh"
 #include "fwd_kernels.cuh"
+#include "smem_engine.cuh"
 
 namespace cx {
 namespace {
+using namespace sme;
 
 constexpr int kWarps = kFwdThreads / 32;
 constexpr int kMaxC = 4;
@@ -109,136 +112,7 @@ struct Layout {
   }
 };
 
-// ---------------------------------------------------------------------------
-// Product tables: product p adds W[gate g(p)] . vec[v(p)] into acc a(p).
-// Vector index NV denotes the child sum h~ (computed on the fly).
-// ---------------------------------------------------------------------------
-struct PhLstmLeaf {  // [i; o; u] = W_iou x
-  static constexpr int G0 = 0, NG = 3, NV = 1, NA = 3, NP = 3;
-  static constexpr bool HT = false;
-  __device__ static constexpr int g(int p) { return p; }
-  __device__ static constexpr int v(int p) { return 0; }
-  __device__ static constexpr int a(int p) { return p; }
-};
-template <int MAXC>
-struct PhLstmLevel {  // [i; o; u] = U_iou h~ ; f_k = U_f h_k
-  static constexpr int G0 = 0, NG = 4, NV = MAXC, NA = 3 + MAXC, NP = 3 + MAXC;
-  static constexpr bool HT = true;
-  __device__ static constexpr int g(int p) { return p < 3 ? p : 3; }
-  __device__ static constexpr int v(int p) { return p < 3 ? MAXC : p - 3; }
-  __device__ static constexpr int a(int p) { return p; }
-};
-struct PhGruLeaf {  // z = W_z x ; g = W_h x
-  static constexpr int G0 = 0, NG = 2, NV = 1, NA = 2, NP = 2;
-  static constexpr bool HT = false;
-  __device__ static constexpr int g(int p) { return p; }
-  __device__ static constexpr int v(int p) { return 0; }
-  __device__ static constexpr int a(int p) { return p; }
-};
-template <int MAXC>
-struct PhGruA {  // z = U_z h~ ; r_k = U_r h_k   (gates 0, 1 of the resident set)
-  static constexpr int G0 = 0, NG = 2, NV = MAXC, NA = 1 + MAXC, NP = 1 + MAXC;
-  static constexpr bool HT = true;
-  __device__ static constexpr int g(int p) { return p < 1 ? 0 : 1; }
-  __device__ static constexpr int v(int p) { return p < 1 ? MAXC : p - 1; }
-  __device__ static constexpr int a(int p) { return p; }
-};
-struct PhGruB {  // U_h s   (gate 2 of the resident set; vector 0 = s)
-  static constexpr int G0 = 2, NG = 1, NV = 1, NA = 1, NP = 1;
-  static constexpr bool HT = false;
-  __device__ static constexpr int g(int p) { return 0; }
-  __device__ static constexpr int v(int p) { return 0; }
-  __device__ static constexpr int a(int p) { return 0; }
-};
-struct PhFcLevel {  // W [h_l; h_r] = W_l h_l + W_r h_r
-  static constexpr int G0 = 0, NG = 2, NV = 2, NA = 1, NP = 2;
-  static constexpr bool HT = false;
-  __device__ static constexpr int g(int p) { return p; }
-  __device__ static constexpr int v(int p) { return p; }
-  __device__ static constexpr int a(int p) { return 0; }
-};
-struct PhDagProj {  // W_x x
-  static constexpr int G0 = 0, NG = 1, NV = 1, NA = 1, NP = 1;
-  static constexpr bool HT = false;
-  __device__ static constexpr int g(int p) { return 0; }
-  __device__ static constexpr int v(int p) { return 0; }
-  __device__ static constexpr int a(int p) { return 0; }
-};
-template <int MAXC>
-struct PhDagLevel {  // U h~
-  static constexpr int G0 = 0, NG = 1, NV = MAXC, NA = 1, NP = 1;
-  static constexpr bool HT = true;
-  __device__ static constexpr int g(int p) { return 0; }
-  __device__ static constexpr int v(int p) { return MAXC; }
-  __device__ static constexpr int a(int p) { return 0; }
-};
-
-// Lane = unit (u < 32), warp w covers k in [w H/8, (w+1) H/8).
-// Ws: [gate][unit][H + 4] (row padding keeps float4 reads conflict-free);
-// X : [T][NV][H] (broadcast reads).
-template <class PH, int T>
-__device__ __forceinline__ void fma_engine(const float *__restrict__ Ws, const float *__restrict__ X,
-                                           int H, float (&acc)[PH::NA][T]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int HP = H + 4;
-#pragma unroll
-  for (int a = 0; a < PH::NA; a++)
-#pragma unroll
-    for (int t = 0; t < T; t++) acc[a][t] = 0.f;
-  const int kc = H / kWarps;
-  const int kb = warp * kc;
-  constexpr int NG_USED = PH::NG;
-  for (int k = kb; k < kb + kc; k += 4) {
-    float4 w[NG_USED];
-#pragma unroll
-    for (int g = 0; g < NG_USED; g++)
-      w[g] = *reinterpret_cast<const float4 *>(Ws + (size_t)((PH::G0 + g) * kUG + lane) * HP + k);
-#pragma unroll
-    for (int t = 0; t < T; t++) {
-      float4 v[PH::NV + 1];
-#pragma unroll
-      for (int j = 0; j < PH::NV; j++)
-        v[j] = *reinterpret_cast<const float4 *>(X + (size_t)(t * PH::NV + j) * H + k);
-      if constexpr (PH::HT) {
-        v[PH::NV] = v[0];
-#pragma unroll
-        for (int j = 1; j < PH::NV; j++) v[PH::NV] = add4(v[PH::NV], v[j]);
-      }
-#pragma unroll
-      for (int p = 0; p < PH::NP; p++) fma4(acc[PH::a(p)][t], w[PH::g(p)], v[PH::v(p)]);
-    }
-  }
-}
-
-// Cross-warp reduction of the K-split partial sums through `red` (aliases X).
-// Thread (t = tid / 32, u = lane) receives the full sums of node t, unit u.
-template <int NA, int T>
-__device__ __forceinline__ void reduce_acc(float *red, const float (&acc)[NA][T], float (&out)[NA]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __syncthreads();  // everyone is done reading X
-#pragma unroll
-  for (int a = 0; a < NA; a++)
-#pragma unroll
-    for (int t = 0; t < T; t++) red[((warp * NA + a) * T + t) * 32 + lane] = acc[a][t];
-  __syncthreads();
-  const int t = threadIdx.x >> 5;
-#pragma unroll
-  for (int a = 0; a < NA; a++) {
-    float s = 0.f;
-    if (t < T) {
-#pragma unroll
-      for (int w = 0; w < kWarps; w++) s += red[((w * NA + a) * T + t) * 32 + lane];
-    }
-    out[a] = s;
-  }
-}
-
-struct TileMeta {
-  int own[8];            // input id of each node of the tile
-  int cin[8][kMaxC];     // input ids of children, -1 absent
-  int nch[8];            // present children
-  int word[8];           // clamped word id (phases that read Emb)
-};
+using TileMeta = fwd::TileMetaT<8>;
 
 struct GateSrc {
   const float *base;
@@ -259,41 +133,8 @@ __device__ void load_gates(float *Ws, const GateSrc *gs, int NG, int unit0, int 
   cp_async_commit();
 }
 
-// Tile bookkeeping: node new ids [i0, i0 + cnt).
-// mode 0: internal nodes (children); mode 1: nodes that read a word.
-__device__ void load_meta(const FwdArgs &a, TileMeta &m, int i0, int cnt, bool want_children,
-                          bool want_word, bool binary, bool latch) {
-  const int t = threadIdx.x;
-  if (t < cnt) {
-    int i = i0 + t;
-    int own = __ldg(a.perm + i);
-    m.own[t] = own;
-    if (want_word) {
-      int w = __ldg(a.words + own);
-      if (w < 0 || w >= a.V) {
-        if (latch) latch_error(a.hdr, CX_E_WORD_RANGE, own);
-        w = 0;
-      }
-      m.word[t] = w;
-    }
-    if (want_children) {
-      int nc = 0;
-      for (int k = 0; k < a.maxc; k++) {
-        int c = __ldg(a.chn + (size_t)k * a.n + i);
-        if (c < 0) break;
-        if (k < kMaxC) m.cin[t][k] = __ldg(a.perm + c);
-        nc++;
-      }
-      for (int k = nc; k < kMaxC; k++) m.cin[t][k] = -1;
-      if (binary && nc != 2) {
-        if (latch) latch_error(a.hdr, CX_E_ARITY, own);
-        if (nc < 2) m.cin[t][1] = m.cin[t][0];  // clamp for memory safety
-        nc = 2;
-      }
-      m.nch[t] = nc;
-    }
-  }
-}
+using fwd::load_meta;
+using fwd::put_h;
 
 // X[t][j][:] = row src(t, j) (H floats) or zeros; rows of t >= cnt untouched.
 template <class SRC>
@@ -370,7 +211,7 @@ struct TreeLstm {
         float cc = sigmoidf_(ig) * tanhf_(ug);
         float hh = sigmoidf_(og) * tanhf_(cc);
         size_t o = (size_t)c.m->own[t] * H + unit;
-        a.h_out[o] = hh;
+        put_h(a, *c.m, t, unit, hh);
         a.cbuf[o] = cc;
       }
       __syncthreads();
@@ -418,7 +259,7 @@ struct TreeLstm {
           if (k < nc) cc += sigmoidf_(s[3 + k] + bfu) * c.cv[(t * kMaxC + k) * 32 + lane];
         float hh = sigmoidf_(og) * tanhf_(cc);
         size_t o = (size_t)c.m->own[t] * H + unit;
-        a.h_out[o] = hh;
+        put_h(a, *c.m, t, unit, hh);
         a.cbuf[o] = cc;
       }
       __syncthreads();
@@ -478,7 +319,7 @@ struct TreeGru {
       if (t < cnt) {
         float z = sigmoidf_(s[0] + c.bias[0 * 32 + lane]);
         float g = tanhf_(s[1] + c.bias[2 * 32 + lane]);
-        a.h_out[(size_t)c.m->own[t] * H + unit] = (1.f - z) * g;
+        put_h(a, *c.m, t, unit, (1.f - z) * g);
       }
       __syncthreads();
     }
@@ -542,7 +383,7 @@ struct TreeGru {
           size_t o = (size_t)c.m->own[t] * H + unit;
           float g = tanhf_(s[0] + c.bias[2 * 32 + lane]);
           float z = __ldcg(a.zbuf + o), ht = __ldcg(a.h_out + o);
-          a.h_out[o] = z * ht + (1.f - z) * g;
+          put_h(a, *c.m, t, unit, z * ht + (1.f - z) * g);
         }
         __syncthreads();
       }
@@ -584,7 +425,7 @@ struct TreeFc {
       }
       const int t = threadIdx.x >> 5, unit = c.unit0 + (threadIdx.x & 31);
       if (t < cnt)
-        a.h_out[(size_t)c.m->own[t] * c.H + unit] = __ldg(a.emb + (size_t)c.m->word[t] * c.H + unit);
+        put_h(a, *c.m, t, unit, __ldg(a.emb + (size_t)c.m->word[t] * c.H + unit));
       __syncthreads();
     }
   };
@@ -606,7 +447,7 @@ struct TreeFc {
       fma_engine<PhFcLevel, T>(c.Ws, c.X, H, acc);
       reduce_acc<1, T>(c.X, acc, s);
       const int t = threadIdx.x >> 5, unit = c.unit0 + (threadIdx.x & 31);
-      if (t < cnt) a.h_out[(size_t)c.m->own[t] * H + unit] = tanhf_(s[0] + c.bias[threadIdx.x & 31]);
+      if (t < cnt) put_h(a, *c.m, t, unit, tanhf_(s[0] + c.bias[threadIdx.x & 31]));
       __syncthreads();
     }
   };
@@ -653,7 +494,7 @@ struct DagRnn {
         float p = s[0] + c.bias[threadIdx.x & 31];
         size_t o = (size_t)c.m->own[t] * H + unit;
         a.pbuf[o] = p;
-        if (i0 + t >= a.hdr->first_leaf) a.h_out[o] = tanhf_(p);
+        if (i0 + t >= a.hdr->first_leaf) put_h(a, *c.m, t, unit, tanhf_(p));
       }
       __syncthreads();
     }
@@ -682,7 +523,7 @@ struct DagRnn {
       fma_engine<PhDagLevel<MAXC>, T>(c.Ws, c.X, H, acc);
       reduce_acc<1, T>(c.X, acc, s);
       const int t = threadIdx.x >> 5, unit = c.unit0 + lane;
-      if (t < cnt) a.h_out[(size_t)c.m->own[t] * H + unit] = tanhf_(s[0] + c.cv[t * 32 + lane]);
+      if (t < cnt) put_h(a, *c.m, t, unit, tanhf_(s[0] + c.cv[t * 32 + lane]));
       __syncthreads();
     }
   };
@@ -720,7 +561,7 @@ struct TreeRnn {
       const int ug = min(kUG, c.H);
       for (int idx = threadIdx.x; idx < cnt * ug; idx += blockDim.x) {
         int t = idx / ug, unit = c.unit0 + idx % ug;
-        a.h_out[(size_t)c.m->own[t] * c.H + unit] = __ldg(a.emb + (size_t)c.m->word[t] * c.H + unit);
+        put_h(a, *c.m, t, unit, __ldg(a.emb + (size_t)c.m->word[t] * c.H + unit));
       }
       __syncthreads();
     }
@@ -741,7 +582,7 @@ struct TreeRnn {
         int t = idx / ug, unit = c.unit0 + idx % ug;
         float l = __ldcg(a.h_out + (size_t)c.m->cin[t][0] * c.H + unit);
         float r = __ldcg(a.h_out + (size_t)c.m->cin[t][1] * c.H + unit);
-        a.h_out[(size_t)c.m->own[t] * c.H + unit] = tanhf_(l + r);
+        put_h(a, *c.m, t, unit, tanhf_(l + r));
       }
       __syncthreads();
     }
@@ -848,24 +689,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1) fwd_kernel(FwdArgs a) {
   cp_async_wait_all();
   trace_mark(a, a.trace_slots - 2);
 
-  // ---- packed root states: each CTA copies the rows it wrote itself --------
-  if (a.root_out) {
-    const int R = a.hdr->num_roots;
-    const int ug = min(kUG, H);
-    const int lo0 = C::leaf_lo(a, first_leaf);
-    for (int r = 0; r < R; r++) {
-      int i = __ldg(a.roots + r);
-      int lvl = __ldg(a.hnew + i);
-      // leaves were written by the leaf (or projection) phase's chunking
-      int own = lvl == 0 ? owner_of(i - lo0, n - lo0, a.Gn)
-                         : owner_of(i - __ldg(a.lbeg + lvl), __ldg(a.lsize + lvl), a.Gn);
-      if (own != gn) continue;
-      int src = __ldg(a.perm + i);
-      for (int u = threadIdx.x; u < ug; u += blockDim.x)
-        a.root_out[(size_t)r * H + ctx.unit0 + u] = __ldcg(a.h_out + (size_t)src * H + ctx.unit0 + u);
-    }
-  }
-
   // ---- the last CTA out publishes the latched status -----------------------
   __syncthreads();
   trace_mark(a, a.trace_slots - 1);
@@ -891,6 +714,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) fwd_kernel(FwdArgs a) {
 bool mvrnn_plan(int H, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
 bool rw_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
 bool cluster_plan(int cell, int H, int maxc, int n, int roots, FwdPlan *plan, int *Gn, int *Gu);
+bool big_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
+size_t big_workspace_bytes(int H, int n);
 
 template <int CELL, int MAXC, class C>
 static bool plan_for(int H, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
@@ -927,6 +752,8 @@ bool fwd_plan(int cell, int H, int maxc, int n, int path, int num_sms, FwdPlan *
   const bool rw_ok = (cell == CX_TREELSTM || cell == CX_TREEGRU || cell == CX_TREEFC ||
                       cell == CX_DAGRNN) && (H == 64 || H == 128 || H == 256 || H == 512);
   if ((path == 0 || path == 3) && cluster_plan(cell, H, maxc, n, 0, plan, Gn, Gu)) return true;
+  if ((path == 4 || (path == 0 && n > kRwMaxNodes)) && big_plan(cell, H, maxc, num_sms, plan, Gn, Gu))
+    return true;
   const bool want_rw = path == 1 || (path == 0 && n <= kRwMaxNodes);
   if (rw_ok && want_rw && rw_plan(cell, H, maxc, num_sms, plan, Gn, Gu)) return true;
   const bool weighted = cell != CX_TREERNN && cell != CX_MVRNN;
@@ -960,6 +787,11 @@ bool fwd_plan(int cell, int H, int maxc, int n, int path, int num_sms, FwdPlan *
 size_t fwd_workspace_bytes(int cell, int H, int n) {
   size_t N = (size_t)(n > 0 ? n : 1), h = (size_t)H;
   size_t b = sizeof(GridBar);
+  if (cell == CX_TREELSTM || cell == CX_DAGRNN) {  // large-batch path: hs, st + words
+    size_t big = big_workspace_bytes(H, (int)N);
+    size_t other = 4 * N * h;
+    return b + (big > other ? big : other) + 1024;
+  }
   switch (cell) {
     case CX_TREELSTM: b += 4 * N * h; break;            // c (when aux_out == NULL)
     case CX_TREEGRU: b += 2 * 4 * N * h; break;         // z, s

@@ -71,7 +71,7 @@ struct RTreeLstm {
         float cc = sigmoidf_(s[0] + c.bias[u]) * tanhf_(s[2] + c.bias[32 + u]);
         float hh = sigmoidf_(s[1] + c.bias[16 + u]) * tanhf_(cc);
         size_t o = (size_t)m->own[off + t] * H + c.unit0 + u;
-        a.h_out[o] = hh;
+        put_h(a, *m, off + t, c.unit0 + u, hh);
         a.cbuf[o] = cc;
       }
       __syncthreads();
@@ -110,7 +110,7 @@ struct RTreeLstm {
           if (k < nc) cc += sigmoidf_(s[3 + k] + bf) * c.cv[(t * kMaxC + k) * kRUG + u];
         float hh = sigmoidf_(s[1] + c.bias[16 + u]) * tanhf_(cc);
         size_t o = (size_t)m->own[t] * H + c.unit0 + u;
-        a.h_out[o] = hh;
+        put_h(a, *m, t, c.unit0 + u, hh);
         a.cbuf[o] = cc;
       }
       __syncthreads();
@@ -154,7 +154,7 @@ struct RTreeGru {
       if (t < cnt) {
         float z = sigmoidf_(s[0] + c.bias[u]);
         float g = tanhf_(s[1] + c.bias[32 + u]);
-        a.h_out[(size_t)m->own[off + t] * H + c.unit0 + u] = (1.f - z) * g;
+        put_h(a, *m, off + t, c.unit0 + u, (1.f - z) * g);
       }
       __syncthreads();
     }
@@ -207,7 +207,7 @@ struct RTreeGru {
           size_t o = (size_t)m->own[t] * H + c.unit0 + u;
           float g = tanhf_(s[0] + c.bias[32 + u]);
           float z = __ldcg(a.zbuf + o), ht = __ldcg(a.h_out + o);
-          a.h_out[o] = z * ht + (1.f - z) * g;
+          put_h(a, *m, t, c.unit0 + u, z * ht + (1.f - z) * g);
         }
         __syncthreads();
       }
@@ -236,7 +236,7 @@ struct RTreeFc {
       const FwdArgs &a = *c.a;
       for (int idx = threadIdx.x; idx < cnt * kRUG; idx += blockDim.x) {
         int t = idx >> 4, u = idx & 15;
-        a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = __ldg(a.emb + (size_t)m->word[t] * H + c.unit0 + u);
+        put_h(a, *m, t, c.unit0 + u, __ldg(a.emb + (size_t)m->word[t] * H + c.unit0 + u));
       }
     }
     template <int T>
@@ -254,7 +254,7 @@ struct RTreeFc {
       float s[1];
       contract<RFcLevel, H, T>(c, c.X, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
       const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
-      if (t < cnt) a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = tanhf_(s[0] + c.bias[u]);
+      if (t < cnt) put_h(a, *m, t, c.unit0 + u, tanhf_(s[0] + c.bias[u]));
       __syncthreads();
     }
   };
@@ -290,7 +290,7 @@ struct RDagRnn {
       float s[1];
       contract<RDagLeaf, H, T>(c, c.X + (size_t)off * H, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
       const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
-      if (t < cnt) a.h_out[(size_t)m->own[off + t] * H + c.unit0 + u] = tanhf_(s[0] + c.bias[u]);
+      if (t < cnt) put_h(a, *m, off + t, c.unit0 + u, tanhf_(s[0] + c.bias[u]));
       __syncthreads();
     }
   };
@@ -310,7 +310,7 @@ struct RDagRnn {
       float s[1];
       contract<RDagLevel<MAXC>, H, T>(c, c.X, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
       const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
-      if (t < cnt) a.h_out[(size_t)m->own[t] * H + c.unit0 + u] = tanhf_(s[0] + c.bias[u]);
+      if (t < cnt) put_h(a, *m, t, c.unit0 + u, tanhf_(s[0] + c.bias[u]));
       __syncthreads();
     }
   };
@@ -412,7 +412,6 @@ __global__ void __launch_bounds__(kRThreads, 1) rw_kernel(FwdArgs a) {
     }
   }
   trace_mark(a, a.trace_slots - 2);
-  copy_roots(a, gn, ctx.unit0, kRUG, C::leaf_lo(first_leaf));
   trace_mark(a, a.trace_slots - 1);
   publish_and_exit(a);
 }

@@ -46,7 +46,19 @@ struct TileMetaT {
   int cin[TM][kMaxC];   // input ids of children, -1 absent
   int nch[TM];          // present children
   int word[TM];         // clamped word id (phases that read Emb)
+  int root[TM];         // index in roots[] if the node is a root, else -1
 };
+
+// Write h (column col) of tile node t to h_out, and to root_out when the node
+// is a root (no separate pass over the roots).
+template <class M>
+__device__ __forceinline__ void put_h(const FwdArgs &a, const M &m, int t, int col, float v) {
+  a.h_out[(size_t)m.own[t] * a.H + col] = v;
+  if (a.root_out) {
+    const int r = m.root[t];
+    if (r >= 0) a.root_out[(size_t)r * a.H + col] = v;
+  }
+}
 
 // Tile bookkeeping for nodes with new ids [i0, i0 + cnt): depends only on the
 // linearization, so it can be loaded while the CTA waits at a barrier.
@@ -58,6 +70,12 @@ __device__ void load_meta(const FwdArgs &a, M &m, int i0, int cnt, bool want_chi
     int i = i0 + t;
     int own = __ldg(a.perm + i);
     m.own[t] = own;
+    if (a.root_out) {
+      const int r = __ldg(a.sid + i);
+      m.root[t] = __ldg(a.roots + r) == i ? r : -1;
+    } else {
+      m.root[t] = -1;
+    }
     if (want_word) {
       int w = __ldg(a.words + own);
       if (w < 0 || w >= a.V) {
@@ -139,24 +157,6 @@ __device__ __forceinline__ void publish_and_exit(const FwdArgs &a) {
       a.bar->exit = 0;
       __threadfence();
     }
-  }
-}
-
-// Root states: each CTA copies the units [unit0, unit0 + ug) of the rows it
-// wrote itself (leaves were written by the leaf phase's chunking of
-// [lo0, n)), so no extra grid barrier is needed.
-__device__ __forceinline__ void copy_roots(const FwdArgs &a, int gn, int unit0, int ug, int lo0) {
-  if (!a.root_out) return;
-  const int R = a.hdr->num_roots, n = a.n, H = a.H;
-  for (int r = 0; r < R; r++) {
-    int i = __ldg(a.roots + r);
-    int lvl = __ldg(a.hnew + i);
-    int own = lvl == 0 ? owner_of(i - lo0, n - lo0, a.Gn)
-                       : owner_of(i - __ldg(a.lbeg + lvl), __ldg(a.lsize + lvl), a.Gn);
-    if (own != gn) continue;
-    int src = __ldg(a.perm + i);
-    for (int u = threadIdx.x; u < ug; u += blockDim.x)
-      a.root_out[(size_t)r * H + unit0 + u] = __ldcg(a.h_out + (size_t)src * H + unit0 + u);
   }
 }
 

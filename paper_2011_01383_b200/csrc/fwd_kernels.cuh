@@ -46,13 +46,14 @@ struct FwdPlan {
   size_t smem;
   const void *kernel;
   int cluster = 1;  // > 1: thread-block clusters of this size (no cooperative launch)
+  bool big = false; // large-batch pipelined kernel: workspace holds hs, st [n][H] + words [n]
 };
 
 // Returns false (CX_E_UNSUPPORTED) when no instantiation covers the model.
 // path: 0 = automatic (cluster kernel for small batches of TreeLSTM / DAG-RNN,
 // register weights when n <= kRwMaxNodes, shared-memory weights above),
 // 1 = force the register-weight kernel, 2 = force the shared-memory-weight
-// kernel, 3 = force the cluster kernel.
+// kernel, 3 = force the cluster kernel, 4 = force the large-batch pipelined kernel.
 constexpr int kRwMaxNodes = 32768;
 bool fwd_plan(int cell, int H, int maxc, int n, int path, int num_sms, FwdPlan *plan, int *Gn,
               int *Gu);

@@ -18,7 +18,7 @@ def cx():
     return m
 
 
-@pytest.fixture(params=["auto", "rw", "smem", "cluster"])
+@pytest.fixture(params=["auto", "rw", "smem", "cluster", "big"])
 def path(request, monkeypatch):
     """Run a test through each forward kernel family (CX_FORWARD_PATH is read
     by libcx on every cx_forward call)."""
@@ -109,9 +109,14 @@ def test_baseline_configs(cx, name, path):
 
 
 @pytest.mark.parametrize("name", ["cfg5_treelstm_b4096", "cfg5_dagrnn_b4096"])
-def test_batch4096_sampled(cx, name):
+@pytest.mark.parametrize("fpath", ["auto", "smem"])
+def test_batch4096_sampled(cx, name, fpath, monkeypatch):
     """Full-size launch (the bench configuration); oracle on 64 sampled
     structures (their roots and everything below them)."""
+    if fpath == "auto":
+        monkeypatch.delenv("CX_FORWARD_PATH", raising=False)
+    else:
+        monkeypatch.setenv("CX_FORWARD_PATH", fpath)
     w = synth.workload(name)
     ch, cell, H, V = w["children"], w["cell"], w["hidden"], w["vocab"]
     words, emb = w["words"], synth.embedding(V, H, w["seed"])
