@@ -26,7 +26,7 @@ namespace {
 using namespace fwd;
 using namespace sme;
 
-constexpr int kBT = 8;  // tile (nodes)
+constexpr int kBTMax = 8;  // largest tile (nodes)
 
 __device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -40,21 +40,27 @@ __device__ __forceinline__ void cp_async_wait_group() {
 
 template <int CELL, int MAXC>
 struct BCfg;
+// T: tile (nodes, <= 8: the epilogue maps node t = tid / 32 over 256 threads);
+// S: pipeline stages (buffers in flight). DAG-RNN tiles carry little math, so
+// its pipeline is deeper to keep DRAM-latency gathers in flight; TreeLSTM is
+// bounded by shared memory (128 KiB of resident weights).
 template <int MAXC>
 struct BCfg<CX_TREELSTM, MAXC> {
   static constexpr int NG = 4, NV = MAXC, NA = 3 + MAXC, NAUX = MAXC;  // aux: children's c slices
+  static constexpr int T = 8, S = 2;
 };
 template <int MAXC>
 struct BCfg<CX_DAGRNN, MAXC> {
   static constexpr int NG = 1, NV = MAXC, NA = 1, NAUX = 1;  // aux: own projection slice
+  static constexpr int T = 8, S = 4;
 };
 
 struct BMeta {
   int cnt;
-  int node[kBT];         // new id
-  int own[kBT];          // input id (output row)
-  int ch[kBT][kMaxC];    // children new ids, -1 absent
-  int word[kBT];         // leaf / projection phases
+  int node[kBTMax];         // new id
+  int own[kBTMax];          // input id (output row)
+  int ch[kBTMax][kMaxC];    // children new ids, -1 absent
+  int word[kBTMax];         // leaf / projection phases
 };
 
 template <int CELL, int H, int MAXC>
@@ -63,19 +69,20 @@ struct BLayout {
   static constexpr size_t w = (size_t)C::NG * kUG * (H + 4);
   static constexpr size_t wl = (size_t)(CELL == CX_TREELSTM ? 3 : 1) * kUG * (H + 4);
   static constexpr size_t wmax = w > wl ? w : wl;
-  static constexpr size_t x = (size_t)kBT * (C::NV > 1 ? C::NV : 1) * H;  // one buffer
-  static constexpr size_t red = (size_t)kWarps * C::NA * kBT * 32;
-  static constexpr size_t aux = (size_t)kBT * C::NAUX * 32;              // one buffer
-  static constexpr size_t bytes = sizeof(float) * (wmax + 2 * x + red + 2 * aux);
+  static constexpr size_t x = (size_t)C::T * (C::NV > 1 ? C::NV : 1) * H;  // one stage
+  static constexpr size_t red = (size_t)kWarps * C::NA * C::T * 32;
+  static constexpr size_t aux = (size_t)C::T * C::NAUX * 32;              // one stage
+  static constexpr size_t bytes = sizeof(float) * (wmax + C::S * x + red + C::S * aux);
 };
 
 template <int CELL, int H, int MAXC>
 __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
   using Cf = BCfg<CELL, MAXC>;
   using Lay = BLayout<CELL, H, MAXC>;
-  constexpr int NV = Cf::NV, NAUX = Cf::NAUX;
+  constexpr int NV = Cf::NV, NAUX = Cf::NAUX, kBT = Cf::T, S = Cf::S;
+  static_assert(kBT <= kFwdThreads / 32, "epilogue covers tid / 32 < T");
   extern __shared__ __align__(16) float smem[];
-  __shared__ BMeta meta[2];
+  __shared__ BMeta meta[S];
   __shared__ float s_bias[4 * kUG];
 
   if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
@@ -85,9 +92,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
   const int unit0 = gu * kUG;
   const bool latch = gu == 0;
   float *Ws = smem;
-  float *Xb[2] = {Ws + Lay::wmax, Ws + Lay::wmax + Lay::x};
-  float *red = Ws + Lay::wmax + 2 * Lay::x;
-  float *Ab[2] = {red + Lay::red, red + Lay::red + Lay::aux};
+  float *const Xbase = Ws + Lay::wmax;
+  float *red = Xbase + S * Lay::x;
+  float *const Abase = red + Lay::red;
+  auto Xb = [&](int b) { return Xbase + (size_t)b * Lay::x; };
+  auto Ab = [&](int b) { return Abase + (size_t)b * Lay::aux; };
   float *hs = a.pbuf;                       // [n][H] h, new numbering (workspace)
   float *st = a.pbuf + (size_t)n * H;       // [n][H] c (LSTM) or projections (DAG)
   int *wn = reinterpret_cast<int *>(a.pbuf + 2 * (size_t)n * H);  // [n] word of new id
@@ -171,7 +180,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
   };
   auto gather = [&](const BMeta &M, int buf, bool leaf) {
     const int cnt = M.cnt;
-    float *X = Xb[buf];
+    float *X = Xb(buf);
     constexpr int q = H / 4;
     const int nvl = leaf ? 1 : NV;
     for (int idx = tid; idx < cnt * nvl * q; idx += blockDim.x) {
@@ -189,7 +198,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
       cp_async16_zfill(X + (size_t)row * H + 4 * c, src + 4 * c, valid);
     }
     if (!leaf) {
-      float *A = Ab[buf];
+      float *A = Ab(buf);
       constexpr int q8 = kUG / 4;  // float4 per 32-unit slice
       for (int idx = tid; idx < cnt * NAUX * q8; idx += blockDim.x) {
         const int r = idx / q8, c = idx - r * q8;
@@ -216,30 +225,31 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
     int r_own = 0, r_word = 0, r_ch[kMaxC];
 #pragma unroll
     for (int k = 0; k < kMaxC; k++) r_ch[k] = -1;
-    if (!prefetched) {
-      load_meta_regs(lo, min(kBT, hi - lo), r_own, r_ch, r_word, leaf);
-      store_meta(meta[0], lo, min(kBT, hi - lo), r_own, r_ch, r_word, leaf);
-      if (ntiles > 1) {
-        load_meta_regs(lo + kBT, min(kBT, hi - lo - kBT), r_own, r_ch, r_word, leaf);
-        store_meta(meta[1], lo + kBT, min(kBT, hi - lo - kBT), r_own, r_ch, r_word, leaf);
-      }
-      __syncthreads();
+    // bookkeeping of tiles 0 .. S-1 (levels: the first two were loaded while
+    // the CTA waited at the grid barrier)
+    for (int j = prefetched ? 2 : 0; j < S && j < ntiles; j++) {
+      load_meta_regs(lo + j * kBT, min(kBT, hi - lo - j * kBT), r_own, r_ch, r_word, leaf);
+      store_meta(meta[j], lo + j * kBT, min(kBT, hi - lo - j * kBT), r_own, r_ch, r_word, leaf);
     }
-    gather(meta[0], 0, leaf);
+    __syncthreads();
+    for (int j = 0; j < S - 1; j++) {
+      if (j < ntiles) gather(meta[j], j, leaf);
+      else cp_async_commit();  // empty group keeps the group count uniform
+    }
     for (int j = 0; j < ntiles; j++) {
-      const int b = j & 1;
-      if (j + 1 < ntiles) gather(meta[b ^ 1], b ^ 1, leaf);
-      // stage A: bookkeeping of tile j + 2 into registers (consumed after compute)
-      const int i2 = lo + (j + 2) * kBT;
-      const int cnt2 = j + 2 < ntiles ? min(kBT, hi - i2) : 0;
+      const int b = j % S;
+      if (j + S - 1 < ntiles) gather(meta[(j + S - 1) % S], (j + S - 1) % S, leaf);
+      else cp_async_commit();
+      // stage A: bookkeeping of tile j + S into registers (consumed after compute)
+      const int i2 = lo + (j + S) * kBT;
+      const int cnt2 = j + S < ntiles ? min(kBT, hi - i2) : 0;
       load_meta_regs(i2, cnt2, r_own, r_ch, r_word, leaf);
-      if (j + 1 < ntiles) cp_async_wait_group<1>();
-      else cp_async_wait_group<0>();
+      cp_async_wait_group<S - 1>();  // tile j's group has landed
       __syncthreads();
       // stage C: contraction + fused gates of tile j
       const BMeta &M = meta[b];
-      const float *X = Xb[b];
-      const float *A = Ab[b];
+      const float *X = Xb(b);
+      const float *A = Ab(b);
       const int t = tid >> 5, u = lane, unit = unit0 + u;
       const int cnt = M.cnt;
       if constexpr (CELL == CX_TREELSTM) {
@@ -337,6 +347,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
     hi += base;
     grid_arrive(a.bar, epoch);
     // bookkeeping of the first two tiles while the barrier completes
+    static_assert(S >= 2, "at least double buffering");
     {
       int r_own = 0, r_word = 0, r_ch[kMaxC];
 #pragma unroll
