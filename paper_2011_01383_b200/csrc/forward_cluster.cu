@@ -56,7 +56,7 @@ struct CCfg<CX_DAGRNN, MAXC> {
 template <int CELL, int H, int MAXC>
 struct CLayout {
   using C = CCfg<CELL, MAXC>;
-  static constexpr size_t xl = (size_t)C::TMAX * C::NVMAX * H, xb = (size_t)C::LEAFB * H;
+  static constexpr size_t xl = (size_t)C::TMAX * (C::NVMAX + 1) * H, xb = (size_t)C::LEAFB * H;
   static constexpr size_t x_floats = xl > xb ? xl : xb;
   static constexpr size_t red_floats = (size_t)kRNW * C::NAMAX * C::TMAX * kRUG;
   static constexpr size_t red2_floats = (size_t)C::NAMAX * C::TMAX * kRUG;
@@ -64,7 +64,7 @@ struct CLayout {
   // per node: h slice + aux slice (floats) and perm, label, maxc children, list (ints)
   static size_t bytes(int n, int maxc, int L) {
     return sizeof(float) * (x_floats + red_floats + red2_floats + cv_floats + 2 * (size_t)kCUnits * n) +
-           sizeof(int) * ((size_t)(3 + maxc) * n + 2 * (size_t)L + 64);
+           sizeof(int) * ((size_t)(3 + maxc) * n + 4 * (size_t)L + 64);
   }
 };
 
@@ -73,27 +73,35 @@ constexpr int kClusterMaxN = 768;
 
 struct CS {  // shared-memory carve of one CTA
   float *X, *red, *red2, *cv, *hsl, *aux;
-  int *perm, *lab, *chn, *list, *lbeg, *lsize;
+  int *perm, *lab, *chn, *list, *lbeg, *lsize, *coff, *ccur;  // coff/ccur: this cluster's level lists
 };
 
-// Pull the full H-rows of `rows` (new ids, -1 = zeros) from the CS slices into X.
+// Pull the full H-rows of `rows` (new ids, -1 = zeros) from the CS slices into
+// X (NV + 1 rows per node: the NV children, then their sum h~).
 template <int H, int NV>
 __device__ __forceinline__ void pull_rows(cg::cluster_group &cl, const CS &s, int cnt,
                                           const int (*rows)[kMaxC]) {
   constexpr int CSZ = H / kCUnits;
   constexpr int Q = kCUnits / 4;  // float4 per slice
-  const int total = cnt * NV * CSZ * Q;
+  const int total = cnt * CSZ * Q;
   for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    int q = idx % Q, r = idx / Q;
-    int peer = r % CSZ, tr = r / CSZ;
-    int j = tr % NV, t = tr / NV;
-    int v = rows[t][j];
-    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (v >= 0) {
-      const float *remote = cl.map_shared_rank(s.hsl, peer);
-      val = *reinterpret_cast<const float4 *>(remote + (size_t)v * kCUnits + 4 * q);
+    const int q = idx % Q, r = idx / Q;
+    const int peer = r % CSZ, t = r / CSZ;
+    const float *remote = cl.map_shared_rank(s.hsl, peer);
+    float4 v[NV];
+#pragma unroll
+    for (int j = 0; j < NV; j++) {
+      const int c = rows[t][j];
+      v[j] = c >= 0 ? *reinterpret_cast<const float4 *>(remote + (size_t)c * kCUnits + 4 * q)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    *reinterpret_cast<float4 *>(s.X + (size_t)(t * NV + j) * H + peer * kCUnits + 4 * q) = val;
+    float4 sum = v[0];
+#pragma unroll
+    for (int j = 0; j < NV; j++) {
+      *reinterpret_cast<float4 *>(s.X + (size_t)(t * (NV + 1) + j) * H + peer * kCUnits + 4 * q) = v[j];
+      if (j) { sum.x += v[j].x; sum.y += v[j].y; sum.z += v[j].z; sum.w += v[j].w; }
+    }
+    *reinterpret_cast<float4 *>(s.X + (size_t)(t * (NV + 1) + NV) * H + peer * kCUnits + 4 * q) = sum;
   }
 }
 
@@ -137,6 +145,8 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   s.chn = s.list + n;
   s.lbeg = s.chn + (size_t)maxc * n;
   s.lsize = s.lbeg + L;
+  s.coff = s.lsize + L;      // [L + 1] start of level l in this cluster's list
+  s.ccur = s.coff + L + 1;   // [L] fill cursors
 
   RCtx ctx;
   ctx.a = &a;
@@ -196,33 +206,55 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       for (int v = tid; v < n; v += blockDim.x) s.lab[v] = 0;
     __syncthreads();
   }
-  trace_mark(a, 1);
 
-  // work list of this cluster's nodes in [b, b + M) (order irrelevant: every
-  // slice is addressed by new id)
-  auto build_list = [&](int b, int M) -> int {
-    if (tid == 0) s_cnt = 0;
-    __syncthreads();
-    for (int i0 = b; i0 < b + M; i0 += blockDim.x) {
-      int i = i0 + tid;
-      bool mine = i < b + M && (s.lab[i] % ncl) == cid;
-      unsigned m = __ballot_sync(0xffffffffu, mine);
-      int base = 0;
-      if (lane == 0 && m) base = atomicAdd(&s_cnt, __popc(m));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (mine) s.list[base + __popc(m & ((1u << lane) - 1u))] = i;
+  // ---- this cluster's nodes, bucketed by level once (order inside a level is
+  // irrelevant: every slice is addressed by new id) ---------------------------
+  for (int l = tid; l < L; l += blockDim.x) s.ccur[l] = 0;
+  __syncthreads();
+  // level of new id i: ids are level-contiguous, root-most level first
+  auto level_of = [&](int i) {
+    int lo = 0, hi = L - 1;  // find l with lbeg[l] <= i < lbeg[l] + lsize[l]
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (i >= s.lbeg[mid]) hi = mid; else lo = mid + 1;
     }
-    __syncthreads();
-    return s_cnt;
+    return lo;
   };
+  for (int i = tid; i < n; i += blockDim.x)
+    if ((s.lab[i] % ncl) == cid) atomicAdd(&s.ccur[level_of(i)], 1);
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the per-level counts (level 0 first)
+    int acc = 0;
+    for (int b0 = 0; b0 < L; b0 += 32) {
+      int l = b0 + lane;
+      int x = l < L ? s.ccur[l] : 0, incl = x;
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (l < L) s.coff[l] = acc + incl - x;
+      acc += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) s.coff[L] = acc;
+  }
+  __syncthreads();
+  for (int l = tid; l < L; l += blockDim.x) s.ccur[l] = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x)
+    if ((s.lab[i] % ncl) == cid) {
+      const int l = level_of(i);
+      s.list[s.coff[l] + atomicAdd(&s.ccur[l], 1)] = i;
+    }
+  __syncthreads();
+  trace_mark(a, 1);
 
   // ---- leaf / projection phase ----------------------------------------------
   {
     // TreeLSTM: leaves. DAG-RNN: every node (input projection P = W_x x + b;
     // leaves finish with h = tanh(P)).
-    const int b = CELL == CX_DAGRNN ? 0 : first_leaf;
-    const int cnt = build_list(b, n - b);
-    for (int b0 = 0; b0 < cnt; b0 += LEAFB) {
+    // TreeLSTM: this cluster's leaves (level 0); DAG-RNN: all its nodes
+    const int lb0 = 0, cnt = CELL == CX_DAGRNN ? s.coff[L] : s.coff[1 <= L - 1 ? 1 : L];
+    for (int b0 = lb0; b0 < cnt; b0 += LEAFB) {
       const int cntb = min(LEAFB, cnt - b0);
       if (tid < cntb) {
         int v = s.list[b0 + tid];
@@ -294,12 +326,12 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   // ---- internal levels: one cluster barrier per level -----------------------
   for (int l = 1; l < L; l++) {
     const int tb = 24 + 5 * l;  // debug trace slots of this level's first tile
-    const int cnt = build_list(s.lbeg[l], s.lsize[l]);
+    const int lbase = s.coff[l], cnt = s.coff[l + 1] - lbase;
     if (l < 20) trace_mark(a, tb);
     for (int t0 = 0; t0 < cnt; t0 += TMAX) {
       const int cntt = min(TMAX, cnt - t0);
       if (tid < cntt) {
-        int v = s.list[t0 + tid];
+        int v = s.list[lbase + t0 + tid];
         s_nodes[tid] = v;
         for (int k = 0; k < kMaxC; k++) s_rows[tid][k] = k < maxc ? s.chn[k * n + v] : -1;
       }
@@ -320,7 +352,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
         const int t = tid >> 4;
         if constexpr (CELL == CX_TREELSTM) {
           float sacc[3 + MAXC];
-          contract<RLstmLevel<MAXC>, H, T>(ctx, s.X, w, sacc);
+          contract<RLstmLevel<MAXC>, H, T, true>(ctx, s.X, w, sacc);
           if (t0 == 0 && l < 20) trace_mark(a, tb + 3);
           if (t < cntt) {
             const int v = s_nodes[t];
@@ -338,7 +370,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
           }
         } else {
           float sacc[1];
-          contract<CDagLevel<MAXC>, H, T>(ctx, s.X, w, sacc);
+          contract<CDagLevel<MAXC>, H, T, true>(ctx, s.X, w, sacc);
           if (t < cntt) {
             const int v = s_nodes[t];
             const float hh = tanhf_(sacc[0] + s.aux[(size_t)v * kCUnits + u]);

@@ -150,11 +150,14 @@ struct RCtx {
 // Contraction of one tile against the register-resident weights, reduced to
 // full sums: on return s[a] (threads tid < T*16: node t = tid/16, unit u =
 // tid%16) holds accumulator a of that (node, unit).
-template <class PH, int H, int T>
+// HTS: X already holds the child sum h~ as an extra row after the NV gathered
+// rows of every node (computed once per tile instead of once per unit lane).
+template <class PH, int H, int T, bool HTS = false>
 __device__ __forceinline__ void contract(const RCtx &c, const float *X,
                                          const float (&w)[4][RShape<H>::KC], float (&s)[PH::NA]) {
   constexpr int KC = RShape<H>::KC;
   constexpr int NV = PH::NV;
+  constexpr int NVX = HTS ? NV + 1 : NV;  // rows per node in X
   static_assert(KC % 2 == 0, "packed FFMA2 needs an even k chunk");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int u = lane & 15, ksub = lane >> 4;
@@ -172,8 +175,8 @@ __device__ __forceinline__ void contract(const RCtx &c, const float *X,
     for (int q = 0; q < KC; q += QB) {
       float x[NV + 1][QB];
 #pragma unroll
-      for (int j = 0; j < NV; j++) {
-        const float *p = X + (size_t)(t * NV + j) * H + k0 + q;
+      for (int j = 0; j < NVX; j++) {
+        const float *p = X + (size_t)(t * NVX + j) * H + k0 + q;
         if constexpr (QB == 4) {
           float4 v = *reinterpret_cast<const float4 *>(p);
           x[j][0] = v.x; x[j][1] = v.y; x[j][2] = v.z; x[j][3] = v.w;
@@ -182,7 +185,7 @@ __device__ __forceinline__ void contract(const RCtx &c, const float *X,
           x[j][0] = v.x; x[j][1] = v.y;
         }
       }
-      if constexpr (PH::NCH > 0) {
+      if constexpr (PH::NCH > 0 && !HTS) {
 #pragma unroll
         for (int e = 0; e < QB; e++) {
           float sum = x[0][e];
@@ -205,29 +208,52 @@ __device__ __forceinline__ void contract(const RCtx &c, const float *X,
   for (int a = 0; a < PH::NA; a++)
 #pragma unroll
     for (int t = 0; t < T; t++) acc[a][t] = acc2[a][t].x + acc2[a][t].y;
-  // half-warps hold the two chunks of each unit: combine, then across warps
+  // half-warps hold the two chunks of each unit: combine with one shuffle, then
+  // across the 16 warps through shared memory. Partials are laid out
+  // [warp][acc][unit][node] so a lane stores its nodes with float4 stores; the
+  // two half-warps (which hold identical sums) split the accumulators.
 #pragma unroll
   for (int a = 0; a < PH::NA; a++)
 #pragma unroll
     for (int t = 0; t < T; t++) acc[a][t] += __shfl_xor_sync(0xffffffffu, acc[a][t], 16);
-  if (ksub == 0) {
 #pragma unroll
-    for (int a = 0; a < PH::NA; a++)
+  for (int a = 0; a < PH::NA; a++) {
+    if ((a & 1) != ksub) continue;
+    float *dst = c.red + ((size_t)(warp * PH::NA + a) * kRUG + u) * T;
+    if constexpr (T % 4 == 0) {
 #pragma unroll
-      for (int t = 0; t < T; t++) c.red[((warp * PH::NA + a) * T + t) * kRUG + u] = acc[a][t];
+      for (int t = 0; t < T; t += 4)
+        *reinterpret_cast<float4 *>(dst + t) = make_float4(acc[a][t], acc[a][t + 1], acc[a][t + 2], acc[a][t + 3]);
+    } else {
+#pragma unroll
+      for (int t = 0; t < T; t++) dst[t] = acc[a][t];
+    }
   }
   __syncthreads();
   if (c.tslot >= 0) trace_mark(*c.a, c.tslot + 2);
-  for (int idx = threadIdx.x; idx < PH::NA * T * kRUG; idx += blockDim.x) {
-    float v = 0.f;
+  constexpr int QW = T % 4 == 0 ? 4 : 1;  // floats per partial-sum load
+  constexpr int G = PH::NA * kRUG * T / QW;
+  constexpr int WS = PH::NA * kRUG * T;     // floats per warp's block
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    if constexpr (QW == 4) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int ww = 0; ww < kRNW; ww++) v += c.red[ww * PH::NA * T * kRUG + idx];
-    c.red2[idx] = v;
+      for (int ww = 0; ww < kRNW; ww++) {
+        const float4 x = *reinterpret_cast<const float4 *>(c.red + (size_t)ww * WS + 4 * g);
+        v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
+      }
+      *reinterpret_cast<float4 *>(c.red2 + 4 * g) = v;
+    } else {
+      float v = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < kRNW; ww++) v += c.red[(size_t)ww * WS + g];
+      c.red2[g] = v;
+    }
   }
   __syncthreads();
   const int t = threadIdx.x >> 4, uu = threadIdx.x & 15;
 #pragma unroll
-  for (int a = 0; a < PH::NA; a++) s[a] = t < T ? c.red2[(a * T + t) * kRUG + uu] : 0.f;
+  for (int a = 0; a < PH::NA; a++) s[a] = t < T ? c.red2[(a * kRUG + uu) * T + t] : 0.f;
   if (c.tslot >= 0) trace_mark(*c.a, c.tslot + 3);
 }
 
