@@ -122,6 +122,8 @@ cx_status cx_linearize(const int32_t *children, int32_t n, int32_t max_children,
 
 size_t cx_forward_workspace_bytes(const cx_model *m, int32_t n) {
   if (!m) return 0;
+  if (m->dtype == CX_BF16)
+    return sizeof(cx::GridBar) + cx::tc_workspace_bytes(m->cell, m->hidden, m->vocab, n) + 512;
   return cx::fwd_workspace_bytes(m->cell, m->hidden, n) + 256;
 }
 
@@ -136,7 +138,6 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
   const int n = lin->n;
   if (n < 0) return CX_E_ARG;
   if (n > 0 && (!emb || !word_ids || !h_out || !weights_ok(m->cell, w))) return CX_E_ARG;
-  if (m->dtype == CX_BF16) return CX_E_UNSUPPORTED;  // bf16 tensor-core path: DESIGN.md "next"
   if (!workspace || workspace_bytes < cx_forward_workspace_bytes(m, n)) return CX_E_WORKSPACE;
   if (n == 0) return CX_OK;
 
@@ -146,9 +147,11 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
     std::lock_guard<std::mutex> lk(g_mu);
     int sms = num_sms_current();
     if (sms <= 0) return CX_E_CUDA;
-    if (!cx::fwd_plan(m->cell, m->hidden, lin->max_children, n, forward_path(), sms, &plan, &Gn,
-                      &Gu))
-      return CX_E_UNSUPPORTED;
+    const bool ok = m->dtype == CX_BF16
+                        ? cx::tc_plan(m->cell, m->hidden, lin->max_children, sms, &plan, &Gn, &Gu)
+                        : cx::fwd_plan(m->cell, m->hidden, lin->max_children, n, forward_path(),
+                                       sms, &plan, &Gn, &Gu);
+    if (!ok) return CX_E_UNSUPPORTED;
   }
   const size_t N = (size_t)n, H = (size_t)m->hidden;
   char *p = align_up(static_cast<char *>(workspace), 128);
@@ -176,7 +179,17 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
   a.h_out = h_out;
   a.aux_out = aux_out;
   a.root_out = root_out;
-  if (plan.big) a.pbuf = buf;  // hs, st [n][H] + words [n] (forward_big.cu)
+  if (m->dtype == CX_BF16) {  // hb, cs, xb (forward_tc.cu)
+    char *q = reinterpret_cast<char *>(buf);
+    a.hb = reinterpret_cast<unsigned short *>(q);
+    q = align_up(q + 2 * N * H, 256);
+    if (m->cell == CX_TREELSTM) {
+      a.cs = reinterpret_cast<float *>(q);
+      q = align_up(q + 4 * N * H, 256);
+    }
+    a.xb = reinterpret_cast<unsigned short *>(q);
+    a.xmode = cx::tc_xmode(n, m->vocab);
+  } else if (plan.big) a.pbuf = buf;  // hs, st [n][H] + words [n] (forward_big.cu)
   else switch (m->cell) {
     case CX_TREELSTM: a.cbuf = aux_out ? aux_out : buf; break;
     case CX_TREEGRU: a.zbuf = buf; a.sbuf = buf + N * H; break;
@@ -254,8 +267,10 @@ cx_status cx_forward_launch_info(const cx_model *m, int32_t *ctas, int32_t *thre
   std::lock_guard<std::mutex> lk(g_mu);
   int sms = num_sms_current();
   if (sms <= 0) return CX_E_CUDA;
-  if (!cx::fwd_plan(m->cell, m->hidden, 2, 1, forward_path(), sms, &plan, &Gn, &Gu))
-    return CX_E_UNSUPPORTED;
+  const bool ok = m->dtype == CX_BF16 ? cx::tc_plan(m->cell, m->hidden, 2, sms, &plan, &Gn, &Gu)
+                                      : cx::fwd_plan(m->cell, m->hidden, 2, 1, forward_path(), sms,
+                                                     &plan, &Gn, &Gu);
+  if (!ok) return CX_E_UNSUPPORTED;
   if (ctas) *ctas = plan.ctas;
   if (threads) *threads = plan.threads;
   if (smem_bytes) *smem_bytes = (int32_t)plan.smem;

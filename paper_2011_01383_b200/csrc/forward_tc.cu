@@ -1,0 +1,590 @@
+// forward_tc.cu -- the bf16 tensor-core forward (cx_model.dtype == CX_BF16):
+// one persistent cooperative kernel per batch that walks the levels of the
+// linearization (Listing 2; one barrier per batch, App. A.4
+// P:2010-2040) and runs every level's contraction as a dense GEMM on the
+// 5th-generation tensor cores (tcgen05.mma, bf16 operands, fp32 accumulators
+// in tensor memory), with the gates fused into the epilogue and
+// the recurrent weights resident in shared memory for the whole batch (model
+// persistence).
+//
+// Work split. CTA (gn, gu) owns hidden units [gu*U, gu*U + U) of every gate
+// and the contiguous chunk gn of each level's nodes, walked in tiles of 128
+// nodes (the UMMA M dimension; rows are nodes, so a partial tile's unused rows
+// never influence the valid ones). A tile's GEMM is
+//     D[128 x N] (+)= A_slot[128 x H] * B_slot[N x H]^T      for each slot,
+// where a slot is one gathered operand: the bf16 state rows of the tile's k-th
+// children (zero rows for absent children) or the bf16 input rows x = Emb[word].
+// The child sums of child-sum cells use linearity (U h~ = sum_k U h_k), so no
+// operand is summed before the MMA.
+//   TreeLSTM  leaf:  slot x, B = W_iou slice (i,o,u rows)      -> [i o u]
+//             level: slot child k, B = [U_iou; U_f] slice     -> acc k = [i o u f]_k;
+//                    epilogue: iou = sum_k acc_k, f_k from acc_k (Q1)
+//   DAG-RNN   every level: slot x (B = W_x slice) + child slots (B = U slice), all
+//                    into one accumulator; h = tanh(acc + b)             (Q8)
+//   TreeFC    leaf:  h = Emb[word] (copy, no GEMM)
+//             level: slot left (B = W[:, :H] slice) + slot right (B = W[:, H:]) (Q2)
+//
+// Warp roles (416 threads): warps 0-3 epilogue (warp w owns TMEM lanes
+// 32w..32w+31 = tile rows), warp 4 MMA issuer (one lane; also allocates TMEM),
+// warps 5-12 producers. Producers gather one K-atom (64 bf16 = 128 bytes of
+// each of the tile's 128 rows) of one slot per pipeline stage with 16-byte
+// cp.async into the K-major 128B-swizzled layout (umma.cuh), fence the
+// generic->async proxy and arrive on the stage's "full" mbarrier; the MMA
+// lane waits, issues 4 MMAs (K = 16 each) and frees the stage with
+// tcgen05.commit. Accumulators are double-buffered in TMEM so the epilogue of
+// tile t overlaps the MMAs of tile t+1. A 4-deep ring of tile bookkeeping
+// (node ids, children, rows of x, roots) in shared memory is filled by the
+// producers and released by the epilogue.
+//
+// State (workspace, linearized numbering): hb [n][H] bf16 (the MMA operand
+// for parents), cs [n][H] fp32 (TreeLSTM memory cells), xb bf16 input rows:
+// either the whole embedding table converted once per call (indexed by word;
+// used when the batch has more x rows than half the vocabulary) or the batch's
+// own x rows in node order. h_out / aux_out / root_out are written by the
+// epilogue in the caller's numbering.
+#include <cuda_runtime.h>
+
+#include "fwd_common.cuh"
+#include "umma.cuh"
+
+namespace cx {
+namespace {
+using namespace fwd;
+using namespace umma;
+
+constexpr int kTM = 128;                    // tile rows = UMMA M
+constexpr int kMmaWarp = 4, kProd0 = 5, kProdWarps = 8;  // warps 0-3: epilogue
+constexpr int kTcThreads = 32 * (kProd0 + kProdWarps);  // 416
+constexpr int kProdThreads = 32 * kProdWarps;           // 256
+constexpr int kMetaRing = 4;
+constexpr int kStageBytes = kTM * 128;                  // one K-atom of one slot (16 KB)
+constexpr int kSmemLimit = 227 * 1024;
+constexpr int kChunksPerThread = kTM * 8 / kProdThreads;  // 16-byte chunks per stage per thread
+
+template <int J>
+struct TcMeta {
+  int i0, cnt;
+  int own[kTM];    // input id (output row), -1 past cnt
+  int xr[kTM];     // row of xb (word or node-order row), -1 = none
+  int root[kTM];   // index in roots[] or -1
+  int ch[J][kTM];  // children new ids, -1 absent
+};
+
+constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
+
+template <int CELL, int H, int MAXC>
+struct TcCfg {
+  static constexpr bool LSTM = CELL == CX_TREELSTM, DAG = CELL == CX_DAGRNN, FC = CELL == CX_TREEFC;
+  static constexpr int J = MAXC;
+  static constexpr int U = DAG ? (H >= 128 ? 128 : H) : 32;
+  static constexpr int KA = H / 64;
+  static constexpr int B0 = LSTM ? 3 * U : U;  // rows: LSTM W_iou | DAG W_x | FC W_left
+  static constexpr int B1 = LSTM ? 4 * U : U;  // rows: LSTM [U_iou; U_f] | DAG U | FC W_right
+  static constexpr int NACC = LSTM ? J : 1;    // accumulators per tile (level phase)
+  static constexpr int NLVL = LSTM ? 4 * U : U;  // N of a level-phase MMA
+  static constexpr int NLEAF = LSTM ? 3 * U : U;
+  static constexpr int BUFC = NACC * NLVL;      // TMEM columns per accumulator buffer
+  static constexpr int TCOLS = pow2_cols(2 * BUFC);
+  static constexpr bool XSLOT = LSTM || DAG;
+  static constexpr size_t bbytes0 = (size_t)B0 * KA * 128, bbytes1 = (size_t)B1 * KA * 128;
+  static constexpr size_t static_bytes = sizeof(TcMeta<J>) * kMetaRing + 4 * U * 4 + 64 * 8 + 64;
+  static constexpr int S_fit =
+      (int)((kSmemLimit - 1024 - static_bytes - bbytes0 - bbytes1) / kStageBytes);
+  static constexpr int S = S_fit > 8 ? 8 : S_fit;
+  static constexpr size_t dyn_bytes = 1024 + bbytes0 + bbytes1 + (size_t)S * kStageBytes;
+  static_assert(H % 64 == 0 && H % U == 0, "H must be a multiple of 64 and of U");
+  static_assert(BUFC * 2 <= 512, "TMEM: two accumulator buffers must fit 512 columns");
+  static_assert(NLVL <= 256 && NLEAF <= 256 && NLVL % 16 == 0, "UMMA N");
+
+  __host__ __device__ static constexpr int nslots(bool leaf) {
+    return leaf ? 1 : (LSTM ? J : DAG ? J + 1 : 2);
+  }
+  // slot s of a phase -> operand (-1 = x rows, k = child k), B matrix, accumulator
+  __device__ static void slot(bool leaf, int s, int &src, int &bm, int &acc) {
+    if (leaf) { src = -1; bm = 0; acc = 0; return; }
+    if (LSTM) { src = s; bm = 1; acc = s; return; }
+    if (DAG) { src = s == 0 ? -1 : s - 1; bm = s == 0 ? 0 : 1; acc = 0; return; }
+    src = s; bm = s; acc = 0;  // FC
+  }
+};
+
+__device__ __forceinline__ void cp16_zfill(uint32_t dst, const void *src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ uint4 f32x8_to_bf16(float4 a, float4 b) {
+  return make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y),
+                    pack_bf16(b.z, b.w));
+}
+__device__ __forceinline__ void store_bf16x32(unsigned short *dst, const float (&v)[32]) {
+  uint4 *d = reinterpret_cast<uint4 *>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; q++)
+    d[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                      pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+}
+__device__ __forceinline__ void store_f32x32(float *dst, const float (&v)[32]) {
+  float4 *d = reinterpret_cast<float4 *>(dst);
+#pragma unroll
+  for (int q = 0; q < 8; q++) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+}
+
+// Prologue: row q, K-atom ka, 16-byte chunk c of a resident B matrix (8 bf16)
+// <- the fp32 weights src[ka*64 + c*8 .. +8]
+__device__ __forceinline__ void stage_weight_chunk(unsigned char *Bm, int rows, int q, int ka, int c,
+                                                   const float *src) {
+  const float4 *s = reinterpret_cast<const float4 *>(src + ka * 64 + c * 8);
+  uint4 v = f32x8_to_bf16(__ldg(s), __ldg(s + 1));
+  *reinterpret_cast<uint4 *>(Bm + (size_t)ka * rows * 128 + sw128_off(q, c)) = v;
+}
+
+template <int CELL, int H, int MAXC>
+__global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(FwdArgs a) {
+  using C = TcCfg<CELL, H, MAXC>;
+  constexpr int J = C::J, U = C::U, KA = C::KA, S = C::S;
+  constexpr int LAG = S - 1;
+  extern __shared__ unsigned char smem_raw[];
+  __shared__ TcMeta<J> meta[kMetaRing];
+  __shared__ float s_bias[4 * U];
+  __shared__ __align__(8) uint64_t bar_full[S], bar_empty[S], bar_tfull[2], bar_tempty[2],
+      bar_mfull[kMetaRing], bar_mempty[kMetaRing];
+  __shared__ uint32_t s_tmem;
+
+  if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
+  const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n;
+  const int gn = blockIdx.x / a.Gu, gu = blockIdx.x % a.Gu;
+  const int unit0 = gu * U;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool latch = gu == 0;
+  unsigned char *sm = reinterpret_cast<unsigned char *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char *sB0 = sm, *sB1 = sm + C::bbytes0, *sStage = sB1 + C::bbytes1;
+  unsigned short *hb = a.hb;
+  float *cs = a.cs;
+  const unsigned short *xb = a.xb;
+  const int xlo = C::DAG ? 0 : first_leaf;  // node-order x rows start here
+  unsigned epoch = 0;
+
+  // ---- prologue: barriers, TMEM, biases, resident bf16 weights ---------------
+  if (tid == 0) {
+    for (int s = 0; s < S; s++) { mbar_init(&bar_full[s], kProdThreads); mbar_init(&bar_empty[s], 1); }
+    for (int b = 0; b < 2; b++) { mbar_init(&bar_tfull[b], 1); mbar_init(&bar_tempty[b], kTM); }
+    for (int m = 0; m < kMetaRing; m++) { mbar_init(&bar_mfull[m], 1); mbar_init(&bar_mempty[m], kTM); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) tmem_alloc<C::TCOLS>(&s_tmem);
+  if constexpr (C::LSTM) {
+    for (int q = tid; q < 4 * U; q += blockDim.x) {
+      const int g = q / U, u = q % U;
+      s_bias[q] = __ldg((g < 3 ? a.w[2] + g * H : a.w[4]) + unit0 + u);
+    }
+  } else {
+    for (int q = tid; q < U; q += blockDim.x) s_bias[q] = __ldg(a.w[C::DAG ? 2 : 1] + unit0 + q);
+  }
+  // weights: B0 / B1 rows -> bf16, K-major SW128
+  for (int idx = tid; idx < (C::B0 + C::B1) * KA * 8; idx += blockDim.x) {
+    int q = idx / (KA * 8);
+    const int rem = idx - q * (KA * 8), ka = rem >> 3, c = rem & 7;
+    const bool second = q >= C::B0;
+    if (second) q -= C::B0;
+    const float *src;
+    if constexpr (C::LSTM) {
+      const int g = q / U, u = q % U;
+      if (!second) src = a.w[0] + (size_t)(g * H + unit0 + u) * H;                 // W_iou
+      else src = g < 3 ? a.w[1] + (size_t)(g * H + unit0 + u) * H                  // U_iou
+                       : a.w[3] + (size_t)(unit0 + u) * H;                          // U_f
+    } else if constexpr (C::DAG) {
+      src = a.w[second ? 1 : 0] + (size_t)(unit0 + q) * H;                         // U | W_x
+    } else {
+      src = a.w[0] + (size_t)(unit0 + q) * 2 * H + (second ? H : 0);               // W [H][2H]
+    }
+    stage_weight_chunk(second ? sB1 : sB0, second ? C::B1 : C::B0, q, ka, c, src);
+  }
+  // ---- phase 0: bf16 input rows ------------------------------------------------
+  if constexpr (C::XSLOT) {
+    const size_t total_threads = (size_t)gridDim.x * blockDim.x;
+    const size_t gt = (size_t)blockIdx.x * blockDim.x + tid;
+    constexpr int q8 = H / 8;
+    unsigned short *xw = const_cast<unsigned short *>(xb);
+    if (a.xmode == 0) {  // whole table, indexed by word
+      const size_t total = (size_t)a.V * q8;
+      for (size_t idx = gt; idx < total; idx += total_threads) {
+        const float4 *s = reinterpret_cast<const float4 *>(a.emb + idx * 8);
+        *reinterpret_cast<uint4 *>(xw + idx * 8) = f32x8_to_bf16(__ldg(s), __ldg(s + 1));
+      }
+    } else {  // this batch's x rows in node order (new ids [xlo, n))
+      const size_t total = (size_t)(n - xlo) * q8;
+      for (size_t idx = gt; idx < total; idx += total_threads) {
+        const int r = (int)(idx / q8), c = (int)(idx - (size_t)r * q8);
+        const int own = __ldg(a.perm + xlo + r);
+        int w = __ldg(a.words + own);
+        if (w < 0 || w >= a.V) {
+          if (c == 0) latch_error(a.hdr, CX_E_WORD_RANGE, own);
+          w = 0;
+        }
+        const float4 *s = reinterpret_cast<const float4 *>(a.emb + (size_t)w * H + c * 8);
+        *reinterpret_cast<uint4 *>(xw + (size_t)r * H + c * 8) = f32x8_to_bf16(__ldg(s), __ldg(s + 1));
+      }
+    }
+  }
+  fence_proxy_async();  // resident weights (generic stores) -> tensor-core reads
+  fence_before();
+  grid_sync(a.bar, gridDim.x, epoch);
+  fence_after();
+  const uint32_t tmem = s_tmem;
+
+  uint32_t T0 = 0, Sg0 = 0;  // tiles / stages before this level (identical in every role)
+  for (int l = 0; l < L; l++) {
+    const bool leaf = l == 0;
+    if (l > 0) grid_sync(a.bar, gridDim.x, epoch);
+    int lo, hi;
+    chunk_of(__ldg(a.lsize + l), a.Gn, gn, lo, hi);
+    const int lb = __ldg(a.lbeg + l);
+    lo += lb;
+    hi += lb;
+    if constexpr (C::FC) {
+      if (leaf) {  // h = Emb[word]: this CTA's node chunk x unit slice
+        constexpr int q4 = U / 4;
+        for (int idx = tid; idx < (hi - lo) * q4; idx += blockDim.x) {
+          const int i = lo + idx / q4, c = idx % q4;
+          const int own = __ldg(a.perm + i);
+          int w = __ldg(a.words + own);
+          if (w < 0 || w >= a.V) {
+            if (latch && c == 0) latch_error(a.hdr, CX_E_WORD_RANGE, own);
+            w = 0;
+          }
+          const float4 v = __ldg(reinterpret_cast<const float4 *>(a.emb + (size_t)w * H + unit0) + c);
+          *reinterpret_cast<float4 *>(a.h_out + (size_t)own * H + unit0 + 4 * c) = v;
+          *reinterpret_cast<uint2 *>(hb + (size_t)i * H + unit0 + 4 * c) =
+              make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+          if (a.root_out) {
+            const int r = __ldg(a.sid + i);
+            if (__ldg(a.roots + r) == i)
+              *reinterpret_cast<float4 *>(a.root_out + (size_t)r * H + unit0 + 4 * c) = v;
+          }
+        }
+        continue;
+      }
+    }
+    const int ntiles = (hi - lo + kTM - 1) / kTM;
+    const int nsl = C::nslots(leaf);
+
+    if (warp >= kProd0) {
+      // =========================== producers ===================================
+      const int p = tid - kProd0 * 32;
+      uint32_t Sg = Sg0;
+      int pend = 0;
+      for (int t = 0; t < ntiles; t++) {
+        const uint32_t TT = T0 + t;
+        const int ms = TT % kMetaRing;
+        const int i0 = lo + t * kTM, cnt = min(kTM, hi - i0);
+        mbar_wait(&bar_mempty[ms], ((TT / kMetaRing) & 1) ^ 1);
+        TcMeta<J> &m = meta[ms];
+        if (p < kTM) {
+          const int r = p;
+          int own = -1, xr = -1, root = -1;
+          if (r < cnt) {
+            const int i = i0 + r;
+            own = __ldg(a.perm + i);
+            if (a.root_out) {
+              const int rr = __ldg(a.sid + i);
+              root = __ldg(a.roots + rr) == i ? rr : -1;
+            }
+            if (C::XSLOT && (leaf || C::DAG)) {
+              if (a.xmode == 0) {
+                int w = __ldg(a.words + own);
+                if (w < 0 || w >= a.V) {
+                  if (latch) latch_error(a.hdr, CX_E_WORD_RANGE, own);
+                  w = 0;
+                }
+                xr = w;
+              } else {
+                xr = i - xlo;
+              }
+            }
+          }
+          m.own[r] = own;
+          m.xr[r] = xr;
+          m.root[r] = root;
+          if (r == 0) { m.i0 = i0; m.cnt = cnt; }
+        } else if (!leaf) {
+          const int r = p - kTM;
+          int ch[J];
+          int nc = 0;
+          bool absent = false;
+#pragma unroll
+          for (int k = 0; k < J; k++) {
+            int c = -1;
+            if (r < cnt) c = __ldg(a.chn + (size_t)k * n + i0 + r);
+            absent = absent || c < 0;
+            ch[k] = absent ? -1 : c;
+            nc += ch[k] >= 0;
+          }
+          if (C::FC && r < cnt && nc != 2) {
+            if (latch) latch_error(a.hdr, CX_E_ARITY, __ldg(a.perm + i0 + r));
+          }
+#pragma unroll
+          for (int k = 0; k < J; k++) m.ch[k][r] = ch[k];
+        }
+        named_bar(1, kProdThreads);
+        if (p == 0) mbar_arrive(&bar_mfull[ms]);
+        for (int ka = 0; ka < KA; ka++) {
+          for (int s = 0; s < nsl; s++) {
+            int src, bm, acc;
+            C::slot(leaf, s, src, bm, acc);
+            const int st = Sg % S;
+            mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);
+            const uint32_t dst0 = smem_u32(sStage + (size_t)st * kStageBytes);
+#pragma unroll
+            for (int e = 0; e < kChunksPerThread; e++) {
+              const int q = p + kProdThreads * e, r = q >> 3, c = q & 7;
+              int row;
+              const unsigned short *base;
+              if (src < 0) { row = m.xr[r]; base = xb; }
+              else { row = m.ch[src][r]; base = hb; }
+              const bool valid = row >= 0;
+              const unsigned short *g = base + (size_t)(valid ? row : 0) * H + ka * 64 + c * 8;
+              cp16_zfill(dst0 + sw128_off(r, c), g, valid);
+            }
+            cp_async_commit();
+            Sg++;
+            pend++;
+            if (pend > LAG) {
+              cp_wait_group<LAG>();
+              fence_proxy_async();
+              mbar_arrive(&bar_full[(Sg - pend) % S]);
+              pend--;
+            }
+          }
+        }
+      }
+      cp_async_wait_all();
+      fence_proxy_async();
+      while (pend > 0) {
+        mbar_arrive(&bar_full[(Sg - pend) % S]);
+        pend--;
+      }
+    } else if (warp == kMmaWarp) {
+      // =========================== MMA issuer ==================================
+      if (lane == 0) {
+        const uint32_t idesc = idesc_bf16(kTM, leaf ? C::NLEAF : C::NLVL);
+        const int ncol = leaf ? C::NLEAF : C::NLVL;
+        uint32_t Sg = Sg0;
+        for (int t = 0; t < ntiles; t++) {
+          const uint32_t TT = T0 + t, buf = TT & 1;
+          mbar_wait(&bar_tempty[buf], ((TT >> 1) & 1) ^ 1);
+          fence_after();
+          uint32_t started = 0;
+          for (int ka = 0; ka < KA; ka++) {
+            for (int s = 0; s < nsl; s++) {
+              int src, bm, acc;
+              C::slot(leaf, s, src, bm, acc);
+              const int st = Sg % S;
+              mbar_wait(&bar_full[st], (Sg / S) & 1);
+              fence_after();
+              const uint32_t a0 = smem_u32(sStage + (size_t)st * kStageBytes);
+              const uint32_t b0 = smem_u32((bm ? sB1 : sB0) + (size_t)ka * (bm ? C::B1 : C::B0) * 128);
+              const uint32_t d = tmem + buf * C::BUFC + acc * ncol;
+#pragma unroll
+              for (int kk = 0; kk < 4; kk++) {
+                const uint32_t accum = ((started >> acc) & 1u) | (kk > 0 ? 1u : 0u);
+                mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, accum);
+              }
+              started |= 1u << acc;
+              mma_commit(&bar_empty[st]);
+              Sg++;
+            }
+          }
+          mma_commit(&bar_tfull[buf]);
+        }
+      }
+      __syncwarp();
+    } else {
+      // =========================== epilogue ====================================
+      const int r = tid;  // tile row = TMEM lane
+      for (int t = 0; t < ntiles; t++) {
+        const uint32_t TT = T0 + t, buf = TT & 1;
+        const int ms = TT % kMetaRing;
+        mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
+        mbar_wait(&bar_tfull[buf], (TT >> 1) & 1);
+        fence_after();
+        const TcMeta<J> &m = meta[ms];
+        const bool valid = r < m.cnt;
+        const int i = m.i0 + r, own = m.own[r], root = m.root[r];
+        const uint32_t tb = tmem + ((uint32_t)(warp * 32) << 16) + buf * C::BUFC;
+        if constexpr (C::LSTM) {
+          float c[32], h[32], v[32], w[32];
+          if (leaf) {
+            tmem_ld32(tb + 0, v);        // i
+            tmem_ld32(tb + 2 * U, w);    // u
+#pragma unroll
+            for (int j = 0; j < 32; j++) c[j] = sigmoidf_(v[j] + s_bias[j]) * tanhf_(w[j] + s_bias[2 * U + j]);
+            tmem_ld32(tb + U, v);        // o
+#pragma unroll
+            for (int j = 0; j < 32; j++) h[j] = sigmoidf_(v[j] + s_bias[U + j]) * tanhf_(c[j]);
+          } else {
+            constexpr int NL = C::NLVL;
+            // sum_k f_k * c_k
+#pragma unroll
+            for (int j = 0; j < 32; j++) c[j] = 0.f;
+#pragma unroll
+            for (int k = 0; k < J; k++) {
+              const int ck = valid ? m.ch[k][r] : -1;
+              if (ck >= 0) {
+                const float4 *cp = reinterpret_cast<const float4 *>(cs + (size_t)ck * H + unit0);
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                  float4 x = __ldcg(cp + q);
+                  w[4 * q] = x.x; w[4 * q + 1] = x.y; w[4 * q + 2] = x.z; w[4 * q + 3] = x.w;
+                }
+              }
+              tmem_ld32(tb + k * NL + 3 * U, v);  // f_k
+              if (ck >= 0) {
+#pragma unroll
+                for (int j = 0; j < 32; j++) c[j] += sigmoidf_(v[j] + s_bias[3 * U + j]) * w[j];
+              }
+            }
+            // i = sum_k acc_k[i], u = sum_k acc_k[u]
+            tmem_ld32(tb + 0, v);
+            tmem_ld32(tb + 2 * U, w);
+#pragma unroll
+            for (int k = 1; k < J; k++) {
+              tmem_ld32(tb + k * NL + 0, h);
+#pragma unroll
+              for (int j = 0; j < 32; j++) v[j] += h[j];
+              tmem_ld32(tb + k * NL + 2 * U, h);
+#pragma unroll
+              for (int j = 0; j < 32; j++) w[j] += h[j];
+            }
+#pragma unroll
+            for (int j = 0; j < 32; j++) c[j] += sigmoidf_(v[j] + s_bias[j]) * tanhf_(w[j] + s_bias[2 * U + j]);
+            tmem_ld32(tb + U, v);
+#pragma unroll
+            for (int k = 1; k < J; k++) {
+              tmem_ld32(tb + k * NL + U, h);
+#pragma unroll
+              for (int j = 0; j < 32; j++) v[j] += h[j];
+            }
+#pragma unroll
+            for (int j = 0; j < 32; j++) h[j] = sigmoidf_(v[j] + s_bias[U + j]) * tanhf_(c[j]);
+          }
+          if (valid) {
+            store_f32x32(a.h_out + (size_t)own * H + unit0, h);
+            store_bf16x32(hb + (size_t)i * H + unit0, h);
+            store_f32x32(cs + (size_t)i * H + unit0, c);
+            if (a.aux_out) store_f32x32(a.aux_out + (size_t)own * H + unit0, c);
+            if (root >= 0) store_f32x32(a.root_out + (size_t)root * H + unit0, h);
+          }
+        } else {  // DAG-RNN / TreeFC: h = tanh(acc + b), U / 32 column chunks
+#pragma unroll 1
+          for (int q = 0; q < U / 32; q++) {
+            float v[32];
+            tmem_ld32(tb + q * 32, v);
+#pragma unroll
+            for (int j = 0; j < 32; j++) v[j] = tanhf_(v[j] + s_bias[q * 32 + j]);
+            if (valid) {
+              store_f32x32(a.h_out + (size_t)own * H + unit0 + q * 32, v);
+              store_bf16x32(hb + (size_t)i * H + unit0 + q * 32, v);
+              if (root >= 0) store_f32x32(a.root_out + (size_t)root * H + unit0 + q * 32, v);
+            }
+          }
+        }
+        fence_before();
+        mbar_arrive(&bar_tempty[buf]);
+        mbar_arrive(&bar_mempty[ms]);
+      }
+    }
+    T0 += ntiles;
+    Sg0 += (uint32_t)ntiles * KA * nsl;
+  }
+
+  // ---- teardown -------------------------------------------------------------
+  fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    fence_after();
+    tmem_free<C::TCOLS>(tmem);
+  }
+  publish_and_exit(a);
+}
+
+template <int CELL, int H, int MAXC>
+bool tc_plan_one(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
+  using C = TcCfg<CELL, H, MAXC>;
+  static_assert(C::S >= 2, "at least two pipeline stages");
+  auto k = tc_kernel<CELL, H, MAXC>;
+  static bool set = false;
+  if (!set) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::dyn_bytes) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    set = true;
+  }
+  *Gu = H / C::U;
+  *Gn = num_sms / *Gu;
+  if (*Gn < 1) return false;
+  p->ctas = *Gn * *Gu;
+  p->threads = kTcThreads;
+  p->smem = C::dyn_bytes;
+  p->kernel = (const void *)k;
+  p->cluster = 1;
+  p->big = false;
+  return true;
+}
+
+template <int CELL, int H>
+bool tc_plan_c(int maxc, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
+  if constexpr (CELL == CX_TREEFC) {
+    return maxc == 2 && tc_plan_one<CELL, H, 2>(num_sms, p, Gn, Gu);
+  } else {
+    if (maxc == 1) return tc_plan_one<CELL, H, 1>(num_sms, p, Gn, Gu);
+    if (maxc == 2) return tc_plan_one<CELL, H, 2>(num_sms, p, Gn, Gu);
+    return false;
+  }
+}
+
+}  // namespace
+
+// bf16 tensor-core path: TreeLSTM / DAG-RNN H in {128, 256}, TreeFC H in {256, 512};
+// max_children <= 2 (TMEM holds two accumulator buffers of max_children x 4U columns).
+bool tc_plan(int cell, int H, int maxc, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
+  switch (cell) {
+    case CX_TREELSTM:
+      if (H == 256) return tc_plan_c<CX_TREELSTM, 256>(maxc, num_sms, p, Gn, Gu);
+      if (H == 128) return tc_plan_c<CX_TREELSTM, 128>(maxc, num_sms, p, Gn, Gu);
+      return false;
+    case CX_DAGRNN:
+      if (H == 256) return tc_plan_c<CX_DAGRNN, 256>(maxc, num_sms, p, Gn, Gu);
+      if (H == 128) return tc_plan_c<CX_DAGRNN, 128>(maxc, num_sms, p, Gn, Gu);
+      return false;
+    case CX_TREEFC:
+      if (H == 512) return tc_plan_c<CX_TREEFC, 512>(maxc, num_sms, p, Gn, Gu);
+      if (H == 256) return tc_plan_c<CX_TREEFC, 256>(maxc, num_sms, p, Gn, Gu);
+      return false;
+  }
+  return false;
+}
+
+// x rows in node order when the batch has at most V/2 of them, else the table
+int tc_xmode(int n, int V) { return (size_t)n * 2 <= (size_t)V ? 1 : 0; }
+
+// workspace bytes of the tensor-core path (after the GridBar): hb, cs, xb
+size_t tc_workspace_bytes(int cell, int H, int V, int n) {
+  const size_t N = (size_t)(n > 0 ? n : 1), h = (size_t)H;
+  size_t b = 2 * N * h + 256;                                   // hb
+  if (cell == CX_TREELSTM) b += 4 * N * h + 256;                // cs
+  if (cell == CX_TREELSTM || cell == CX_DAGRNN)                 // xb
+    b += 2 * (tc_xmode(n, V) ? N : (size_t)V) * h + 256;
+  return b;
+}
+
+}  // namespace cx

@@ -26,6 +26,11 @@ struct FwdArgs {
   float *sbuf;  // TreeGRU sum_k r_k * h_k [n][H]
   float *pbuf;  // DAG-RNN input projections W_x x + b [n][H]
   float *Abuf;  // MV-RNN matrices [n][H][H] (aux_out or workspace)
+  // bf16 tensor-core path (forward_tc.cu), workspace:
+  unsigned short *hb;  // [n][H] bf16 hidden states, new numbering (MMA operand)
+  float *cs;           // [n][H] fp32 TreeLSTM memory cells, new numbering
+  unsigned short *xb;  // bf16 input rows: [V][H] (xmode 0) or [n - xlo][H] node order (xmode 1)
+  int xmode;
   GridBar *bar;
   int Gn, Gu;   // node groups x unit groups = CTAs
   unsigned long long *trace;  // debug: %globaltimer per CTA and phase (cx_debug_set_trace)
@@ -58,6 +63,10 @@ constexpr int kRwMaxNodes = 32768;
 bool fwd_plan(int cell, int H, int maxc, int n, int path, int num_sms, FwdPlan *plan, int *Gn,
               int *Gu);
 size_t fwd_workspace_bytes(int cell, int H, int n);
+// bf16 tensor-core path (forward_tc.cu)
+bool tc_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
+int tc_xmode(int n, int V);
+size_t tc_workspace_bytes(int cell, int H, int V, int n);
 cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream);
 
 }  // namespace cx

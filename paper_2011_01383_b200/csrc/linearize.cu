@@ -462,7 +462,10 @@ __global__ void __launch_bounds__(kLinSingleThreads, 1) lin_single_kernel(LinArg
     int hmax = 0;
     if (tree_like) {
       for (int v = tid; v < n; v += nthr) {
-        if (pending[v] != 0) continue;
+        // start at leaves only: an immutable test (a node's pending count can
+        // reach 0 while this loop runs, when the walk of its last child passes
+        // through it; re-walking it would decrement its parent twice)
+        if (ch[v] != -1) continue;
         int cur = v, hc = 0;
         while (true) {
           int p = parent[cur];

@@ -1,0 +1,165 @@
+"""cx_forward with dtype = CX_BF16 (the tcgen05 tensor-core path, forward_tc.cu)
+vs the fp64 oracle: max per-node normwise relative error <= 2e-2
+(BASELINE.json north_star: "2e-2 for bf16 tensor-core paths"), on inputs that
+span several 128-node tiles per CTA with ragged tails, both input-row modes
+(embedding table converted once / node-order rows), sequences, general
+child-sum arity, every BASELINE.json configuration the path covers (sampled at
+batch 4096), latched errors and relabelling invariance."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_helpers import dev_f32, dev_i32, normwise_rel_err, weights_dev
+
+pytestmark = pytest.mark.gpu
+T = synth
+TOL_BF16 = 2e-2
+
+
+@pytest.fixture(scope="module")
+def cx():
+    import paper_2011_01383_b200 as m
+    return m
+
+
+def _run(cx, cell, H, V, ch, kind, words, emb, want_aux=False, num_roots=None):
+    _, wd = weights_dev(cell, H, V)
+    lin = cx.linearize(dev_i32(ch), kind)
+    h, aux, roots = cx.forward(cell, H, wd, dev_f32(emb), dev_i32(words), lin, dtype=cx.BF16,
+                               want_aux=want_aux, num_roots=num_roots)
+    return lin, h, aux, roots
+
+
+def _parity(cx, cell, H, V, ch, kind, seed=0, want_aux=True):
+    words = synth.word_ids(ch, V, seed, all_nodes=(cell == T.DAGRNN))
+    emb = synth.embedding(V, H, seed)
+    ref_lin = oracle.linearize(ch, kind)
+    R = ref_lin["num_roots"]
+    lin, h, aux, roots = _run(cx, cell, H, V, ch, kind, words, emb, want_aux, R)
+    assert cx.status(lin) == (0, -1)
+    ws_np, _ = weights_dev(cell, H, V)
+    rst, _, rh, raux = oracle.forward(cell, H, V, ws_np, emb, words, ch, want_aux=want_aux)
+    assert rst == 0
+    e = normwise_rel_err(h.cpu().numpy(), rh)
+    assert e <= TOL_BF16, f"h max normwise rel err {e:.3e}"
+    if want_aux and raux is not None and aux is not None:
+        ea = normwise_rel_err(aux.cpu().numpy(), raux)
+        assert ea <= TOL_BF16, f"aux err {ea:.3e}"
+    root_ids = ref_lin["perm"][ref_lin["roots"]]
+    assert np.array_equal(roots.cpu().numpy(), h.cpu().numpy()[root_ids])
+    return e
+
+
+@pytest.mark.parametrize("cell,H", [(T.TREELSTM, 128), (T.TREELSTM, 256)])
+@pytest.mark.parametrize("V", [97, 50000])  # table mode / node-order mode
+def test_treelstm_multitile(cx, cell, H, V):
+    # 300 SST-shaped trees: 6000 leaves -> several 128-row tiles per CTA, ragged
+    ch, _ = synth.sst_shaped_forest(300 if H == 128 else 120, 3)
+    _parity(cx, cell, H, V, ch, T.TREE, seed=3)
+
+
+@pytest.mark.parametrize("H", [128, 256])
+@pytest.mark.parametrize("V", [97, 50000])
+def test_dagrnn_multitile(cx, H, V):
+    ch, _ = synth.grid_dags(40, 9, 11)
+    _parity(cx, T.DAGRNN, H, V, ch, T.DAG, seed=4)
+
+
+@pytest.mark.parametrize("H", [256, 512])
+def test_treefc_perfect(cx, H):
+    ch, _ = synth.perfect_forest(12, 7)
+    _parity(cx, T.TREEFC, H, 20000, ch, T.TREE, seed=1)
+
+
+def test_treefc_sst_ragged(cx):
+    ch, _ = synth.sst_shaped_forest(150, 6, leaves=17)
+    _parity(cx, T.TREEFC, 256, 333, ch, T.TREE, seed=6)
+
+
+@pytest.mark.parametrize("cell", [T.TREELSTM, T.DAGRNN])
+def test_sequences(cx, cell):
+    ch, _ = synth.chains(300, 37)
+    _parity(cx, cell, 128, 64, ch, T.SEQUENCE, seed=8)
+
+
+@pytest.mark.parametrize("cell", [T.TREELSTM, T.DAGRNN])
+def test_child_sum_arity_1_and_2(cx, cell):
+    if cell == T.DAGRNN:
+        ch, kind = synth.random_dag(3000, 2, 11, p_edge=0.6), T.DAG
+    else:
+        ch, kind = synth.random_forest(4000, 2, 11), T.TREE
+    _parity(cx, cell, 128, 500, ch, kind, seed=2)
+
+
+@pytest.mark.parametrize("name", ["cfg2_treelstm_b10", "cfg2_treelstm_b1", "cfg3_treefc_b1",
+                                  "cfg3_treefc_b10", "cfg5_dagrnn_b1", "cfg5_dagrnn_b10"])
+def test_baseline_configs(cx, name):
+    w = synth.workload(name)
+    _parity(cx, w["cell"], w["hidden"], w["vocab"], w["children"], w["kind"], seed=w["seed"])
+
+
+@pytest.mark.parametrize("name", ["cfg5_treelstm_b4096", "cfg5_dagrnn_b4096"])
+def test_batch4096_sampled(cx, name):
+    """The bench launch (full batch, bf16) checked on 64 sampled structures."""
+    w = synth.workload(name)
+    ch, cell, H, V = w["children"], w["cell"], w["hidden"], w["vocab"]
+    words, emb = w["words"], synth.embedding(V, H, w["seed"])
+    lin, h, _, roots = _run(cx, cell, H, V, ch, w["kind"], words, emb, num_roots=w["batch"])
+    assert cx.status(lin) == (0, -1)
+    off = w["offsets"]
+    picks = np.sort(np.random.default_rng(1).choice(w["batch"], 64, replace=False))
+    targets = off[picks] if w["kind"] == T.TREE else off[picks + 1] - 1
+    ws_np, _ = weights_dev(cell, H, V)
+    rst, _, rh, _ = oracle.forward(cell, H, V, ws_np, emb, words, ch, targets=targets)
+    assert rst == 0
+    rows = np.concatenate([np.arange(off[g], off[g + 1]) for g in picks])
+    e = normwise_rel_err(h.cpu().numpy(), rh, rows=rows)
+    assert e <= TOL_BF16, e
+    assert np.array_equal(roots.cpu().numpy()[picks], h.cpu().numpy()[targets])
+
+
+def test_relabel_invariance(cx):
+    """Relabelling node ids permutes the outputs identically (bitwise: a row's
+    MMA and epilogue do not depend on its position in a tile)."""
+    H, V, cell = 128, 40, T.TREELSTM
+    ch, _ = synth.sst_shaped_forest(90, 7, leaves=11)
+    words = synth.word_ids(ch, V, 7)
+    emb = synth.embedding(V, H, 7)
+    _, h, _, _ = _run(cx, cell, H, V, ch, T.TREE, words, emb)
+    ch2, w2, pi = synth.shuffle_ids(ch, words, 7)
+    _, h2, _, _ = _run(cx, cell, H, V, ch2, T.TREE, w2, emb)
+    assert np.array_equal(h2.cpu().numpy()[pi], h.cpu().numpy())
+
+
+def test_errors(cx):
+    H, V = 128, 5
+    emb = np.ones((50, H), np.float32)
+    # word out of range at leaf 1 (TreeLSTM), both x-row modes (table: V < 2n; node order)
+    ch = np.array([[1, -1, -1], [2, -1, -1]], np.int32)
+    for Vx in (V, 50):
+        lin, _, _, _ = _run(cx, T.TREELSTM, H, Vx, ch, T.TREE, np.array([-1, 70, 0]), emb[:Vx])
+        assert cx.status(lin) == (7, 1)
+    # DAG-RNN reads every node's word
+    lin, _, _, _ = _run(cx, T.DAGRNN, H, V, ch, T.DAG, np.array([9, 0, 0]), emb[:V])
+    assert cx.status(lin) == (7, 0)
+    # TreeFC (binary): internal node with one child -> ARITY
+    ch = np.array([[1, 2, -1], [-1, -1, -1]], np.int32)
+    lin, _, _, _ = _run(cx, T.TREEFC, 256, V, ch, T.TREE, np.array([-1, -1, 0]),
+                        np.ones((V, 256), np.float32))
+    assert cx.status(lin) == (6, 0)
+    # no tensor-core instantiation: MV-RNN, TreeLSTM with max_children 4, H = 64
+    ch = np.array([[1, -1, -1], [2, -1, -1]], np.int32)
+    for cell, Hx, chx in ((T.MVRNN, 64, ch), (T.TREELSTM, 64, ch),
+                          (T.TREELSTM, 128, np.full((4, 3), -1, np.int32))):
+        with pytest.raises(cx.CxError):
+            _run(cx, cell, Hx, V, chx, T.TREE, np.zeros(3, np.int32),
+                 np.ones((V, Hx), np.float32))
+
+
+def test_single_nodes(cx):
+    """A batch of one-node structures: every node is a leaf and a root."""
+    ch = np.full((2, 300), -1, np.int32)
+    _parity(cx, T.TREELSTM, 128, 50, ch, T.TREE, seed=1)
+    _parity(cx, T.DAGRNN, 128, 50, ch, T.DAG, seed=1)
+    _parity(cx, T.TREEFC, 256, 50, ch, T.TREE, seed=1)

@@ -94,3 +94,25 @@ def test_error_cases_bit_exact(cx):
     ch2 = ch2.copy()
     ch2[0, 9000] = 1  # node 1 (left child of root 0) gets a second parent
     _check(cx, ch2, T)
+
+
+@pytest.mark.parametrize("batch", [15, 40, 60, 80, 100, 120])
+def test_mid_size_forests(cx, batch):
+    """Forests of 585..4680 nodes: the single-CTA linearizer with several
+    nodes per thread (a leaf-start race in its walk-up once produced wrong
+    heights here: pending counts were used to pick the start nodes while other
+    walkers decremented them)."""
+    for seed in range(3):
+        ch, _ = synth.sst_shaped_forest(batch, seed)
+        _check(cx, ch, synth.TREE)
+        ch2, _, _ = synth.shuffle_ids(ch, None, seed + 10)
+        _check(cx, ch2, synth.TREE)
+
+
+@pytest.mark.parametrize("n", [600, 1500, 3000, 4700])
+@pytest.mark.parametrize("maxc", [1, 2, 3, 4])
+def test_mid_size_random(cx, n, maxc):
+    ch = synth.random_forest(n, maxc, n + maxc)
+    _check(cx, ch, synth.TREE)
+    if 4 * n < 12000:
+        _check(cx, synth.random_dag(n, maxc, n + maxc, p_edge=0.4), synth.DAG)
