@@ -92,6 +92,15 @@ def algorithmic_work(cell, H, n, n_leaves, n_internal, batch, maxc=2):
     return flops, bytes_
 
 
+def measured_peaks():
+    """MEASURED_PEAKS.json (driver-written, per pod) or None."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------------------
 # clocks during the timed region (NVML polling thread)
 # ---------------------------------------------------------------------------
@@ -228,8 +237,9 @@ def run_gpu(args, rank, world, local_rank):
     lin = cx.alloc_linearization(n, ch_np.shape[0], inp["kind"], dev)
     h = torch.empty(n, H, dtype=torch.float32, device=dev)
     roots = torch.empty(R, H, dtype=torch.float32, device=dev)
+    dtype = cx.BF16 if args.dtype == "bf16" else cx.F32
     cx.linearize(children, inp["kind"], out=lin)
-    cx.forward(cell, H, weights, emb, words, lin, h_out=h, root_out=roots)
+    cx.forward(cell, H, weights, emb, words, lin, dtype=dtype, h_out=h, root_out=roots)
     cx.check(lin)
     hdr = lin.header_dict()
     L = hdr["num_levels"]
@@ -239,7 +249,7 @@ def run_gpu(args, rank, world, local_rank):
         cx.linearize(children, inp["kind"], out=lin)
 
     def fwd_call():
-        cx.forward(cell, H, weights, emb, words, lin, h_out=h, root_out=roots)
+        cx.forward(cell, H, weights, emb, words, lin, dtype=dtype, h_out=h, root_out=roots)
 
     def step():
         lin_call()
@@ -344,7 +354,7 @@ def run_gpu(args, rank, world, local_rank):
         ch_dev.copy_(ch_host, non_blocking=True)
         w_dev.copy_(w_host, non_blocking=True)
         cx.linearize(ch_dev, inp["kind"], out=lin)
-        cx.forward(cell, H, weights, emb, w_dev, lin, h_out=h, root_out=roots)
+        cx.forward(cell, H, weights, emb, w_dev, lin, dtype=dtype, h_out=h, root_out=roots)
         roots_host.copy_(roots, non_blocking=True)
     torch.cuda.synchronize()
     if world > 1:
@@ -357,7 +367,7 @@ def run_gpu(args, rank, world, local_rank):
         ch_dev.copy_(ch_host, non_blocking=True)
         w_dev.copy_(w_host, non_blocking=True)
         cx.linearize(ch_dev, inp["kind"], out=lin)
-        cx.forward(cell, H, weights, emb, w_dev, lin, h_out=h, root_out=roots)
+        cx.forward(cell, H, weights, emb, w_dev, lin, dtype=dtype, h_out=h, root_out=roots)
         roots_host.copy_(roots, non_blocking=True)
         s1.record(stream)
         s1.synchronize()  # the host reads the step's result
@@ -378,19 +388,38 @@ def run_gpu(args, rank, world, local_rank):
     fwd_mean = sum(fwd_ms) / len(fwd_ms)
     flops, alg_bytes = algorithmic_work(cell, H, n, n_leaves, n - n_leaves, R, ch_np.shape[0])
     achieved = flops / (fwd_mean / 1e3) / 1e12
-    info = cx.launch_info(cell, H, V)
+    info = cx.launch_info(cell, H, V, dtype)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "forward_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(name)
+            traffic = json.load(open(prof)).get(name if args.dtype == "f32" else f"{name}:bf16")
         except Exception:
             traffic = None
+    if args.dtype == "bf16":
+        peaks = measured_peaks()
+        peak, src = (peaks["bf16_tflops"], "MEASURED_PEAKS.json bf16_tflops (burst)") if peaks \
+            else (2250.0, "B200 nominal dense bf16 (MEASURED_PEAKS.json absent)")
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "kernel": "tc_kernel (cx_forward, dtype bf16)", "flops_per_launch": flops,
+                    "alg_bytes_per_launch": alg_bytes,
+                    "hbm_frac": alg_bytes / (fwd_mean / 1e3) / 1e9 /
+                                (peaks["hbm_gbs"] if peaks else 7700.0),
+                    "note": f"peak = {src}; algorithmic flops (SURVEY 8(d)), not the MMA's "
+                            "(child-sum by linearity issues 16H^2 per TreeLSTM node)"}
+    else:
+        roofline = {"bound": "alu", "achieved": achieved, "peak": FMA_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": achieved / FMA_PEAK_TFLOPS, "traffic": traffic,
+                    "kernel": "fwd_kernel (cx_forward)", "flops_per_launch": flops,
+                    "alg_bytes_per_launch": alg_bytes,
+                    "note": "fp32 FMA peak = 148 SM x 128 lanes x 2 x 1.965 GHz; the step is "
+                            "critical-path (levels x barrier) bound, see DESIGN.md"}
     clocks = sampler.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": inp["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": inp["scaling"], "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": name, "cell": synth.CELL_NAMES[cell], "hidden": H, "vocab": V,
                    "structures_per_gpu": R, "nodes_per_gpu": n, "levels": L,
                    "parallelism": f"dp{world} (independent structures per rank)",
@@ -405,12 +434,7 @@ def run_gpu(args, rank, world, local_rank):
         "gpu_launches": 2 * args.steps,
         "allgather_roots_us": allgather_us,
         "launch": info,
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": FMA_PEAK_TFLOPS,
-                     "unit": "TFLOP/s", "frac": achieved / FMA_PEAK_TFLOPS, "traffic": traffic,
-                     "kernel": "fwd_kernel (cx_forward)", "flops_per_launch": flops,
-                     "alg_bytes_per_launch": alg_bytes,
-                     "note": "fp32 FMA peak = 148 SM x 128 lanes x 2 x 1.965 GHz; the step is "
-                             "critical-path (levels x barrier) bound, see DESIGN.md"},
+        "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "clocks": clocks,
@@ -428,6 +452,8 @@ def main():
     p.add_argument("--workload", default="cfg2_treelstm_b10", choices=sorted(WORKLOADS))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--dtype", default="f32", choices=["f32", "bf16"],
+                   help="compute precision of cx_forward (bf16 = tcgen05 tensor-core path)")
     p.add_argument("--allgather", action="store_true",
                    help="N>1: also time the NCCL all-gather of root states")
     args = p.parse_args()

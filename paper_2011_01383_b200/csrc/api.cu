@@ -189,6 +189,7 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
     }
     a.xb = reinterpret_cast<unsigned short *>(q);
     a.xmode = cx::tc_xmode(n, m->vocab);
+    a.cell_has_x = m->cell == CX_TREELSTM || m->cell == CX_DAGRNN;
   } else if (plan.big) a.pbuf = buf;  // hs, st [n][H] + words [n] (forward_big.cu)
   else switch (m->cell) {
     case CX_TREELSTM: a.cbuf = aux_out ? aux_out : buf; break;
@@ -204,7 +205,8 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
     a.trace = g_trace;
     a.trace_slots = g_trace_slots;
   }
-  cudaError_t e = cx::fwd_launch(plan, a, static_cast<cudaStream_t>(stream));
+  cudaError_t e = plan.tc ? cx::tc_launch(plan, a, static_cast<cudaStream_t>(stream))
+                          : cx::fwd_launch(plan, a, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? CX_OK : CX_E_CUDA;
 }
 

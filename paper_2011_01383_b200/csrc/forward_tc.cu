@@ -42,7 +42,11 @@
 // used when the batch has more x rows than half the vocabulary) or the batch's
 // own x rows in node order. h_out / aux_out / root_out are written by the
 // epilogue in the caller's numbering.
+#include <cuda.h>  // CUtensorMap types (the encoder is fetched from the driver at run time)
 #include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
 
 #include "fwd_common.cuh"
 #include "umma.cuh"
@@ -53,21 +57,36 @@ using namespace fwd;
 using namespace umma;
 
 constexpr int kTM = 128;                    // tile rows = UMMA M
-constexpr int kMmaWarp = 4, kProd0 = 5, kProdWarps = 8;  // warps 0-3: epilogue
-constexpr int kTcThreads = 32 * (kProd0 + kProdWarps);  // 416
-constexpr int kProdThreads = 32 * kProdWarps;           // 256
+// warps 0-7: epilogue (warp w reads TMEM lane quadrant w % 4 = tile rows
+// 32(w%4)..+31, column half w / 4); warp 8: MMA issuer; warp 9: TMA gathers;
+// warps 10-11: tile bookkeeping (warp 10 + m fills the tiles t = m mod 2, so
+// two tiles' dependent index loads are in flight at once)
+constexpr int kEpiWarps = 8, kMmaWarp = 8, kTmaWarp = 9, kMeta0 = 10, kMetaWarps = 2;
+constexpr int kTcThreads = 32 * (kMeta0 + kMetaWarps);  // 384
+constexpr int kEpiThreads = 32 * kEpiWarps;             // 256
+constexpr int kMaxCluster = 8;                          // portable cluster size
+
+// 128-byte CUtensorMap (opaque; encoded on the host by cuTensorMapEncodeTiled)
+struct alignas(64) TmaDesc {
+  unsigned long long d[16];
+};
+// kernel parameter block: tensor maps of the gathered operands + the common args
+struct TcArgs {
+  TmaDesc tm_h;  // hb [n][H] bf16, box 64 x 1, 128B swizzle
+  TmaDesc tm_x;  // xb [rows][H] bf16 (x-slot cells), same box
+  FwdArgs f;
+};
 constexpr int kMetaRing = 4;
 constexpr int kStageBytes = kTM * 128;                  // one K-atom of one slot (16 KB)
 constexpr int kSmemLimit = 227 * 1024;
-constexpr int kChunksPerThread = kTM * 8 / kProdThreads;  // 16-byte chunks per stage per thread
 
 template <int J>
 struct TcMeta {
+  alignas(16) int own[kTM];    // input id (output row), -1 past cnt
+  alignas(16) int xr[kTM];     // row of xb (word or node-order row), -1 = none (zeros)
+  alignas(16) int root[kTM];   // index in roots[] or -1
+  alignas(16) int ch[J][kTM];  // children new ids, -1 absent (zeros)
   int i0, cnt;
-  int own[kTM];    // input id (output row), -1 past cnt
-  int xr[kTM];     // row of xb (word or node-order row), -1 = none
-  int root[kTM];   // index in roots[] or -1
-  int ch[J][kTM];  // children new ids, -1 absent
 };
 
 constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
@@ -86,6 +105,10 @@ struct TcCfg {
   static constexpr int BUFC = NACC * NLVL;      // TMEM columns per accumulator buffer
   static constexpr int TCOLS = pow2_cols(2 * BUFC);
   static constexpr bool XSLOT = LSTM || DAG;
+  // CTAs that own different unit slices of the same node tiles form a cluster
+  // of CL; each fetches 1/CL of every stage and multicasts it to all
+  static constexpr int GU = H / U;
+  static constexpr int CL = GU < kMaxCluster ? GU : kMaxCluster;
   static constexpr size_t bbytes0 = (size_t)B0 * KA * 128, bbytes1 = (size_t)B1 * KA * 128;
   static constexpr size_t static_bytes = sizeof(TcMeta<J>) * kMetaRing + 4 * U * 4 + 64 * 8 + 64;
   static constexpr int S_fit =
@@ -108,14 +131,6 @@ struct TcCfg {
   }
 };
 
-__device__ __forceinline__ void cp16_zfill(uint32_t dst, const void *src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-               "r"(valid ? 16 : 0) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_wait_group() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -123,18 +138,37 @@ __device__ __forceinline__ uint4 f32x8_to_bf16(float4 a, float4 b) {
   return make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y),
                     pack_bf16(b.z, b.w));
 }
-__device__ __forceinline__ void store_bf16x32(unsigned short *dst, const float (&v)[32]) {
+template <int N>
+__device__ __forceinline__ void store_f32(float *dst, const float (&v)[N]) {
+  float4 *d = reinterpret_cast<float4 *>(dst);
+#pragma unroll
+  for (int q = 0; q < N / 4; q++) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+}
+// caller outputs (never re-read by the kernel): streaming stores, so they do
+// not evict the state rows and input rows the next gathers read from L2
+template <int N>
+__device__ __forceinline__ void store_f32_stream(float *dst, const float (&v)[N]) {
+  float4 *d = reinterpret_cast<float4 *>(dst);
+#pragma unroll
+  for (int q = 0; q < N / 4; q++) __stcs(d + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+}
+template <int N>
+__device__ __forceinline__ void store_bf16(unsigned short *dst, const float (&v)[N]) {
   uint4 *d = reinterpret_cast<uint4 *>(dst);
 #pragma unroll
-  for (int q = 0; q < 4; q++)
+  for (int q = 0; q < N / 8; q++)
     d[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
                       pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
 }
-__device__ __forceinline__ void store_f32x32(float *dst, const float (&v)[32]) {
-  float4 *d = reinterpret_cast<float4 *>(dst);
-#pragma unroll
-  for (int q = 0; q < 8; q++) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+// Gate nonlinearities of the bf16 path: one MUFU op each (tanh.approx.f32,
+// relative error ~2^-11, far inside the bf16 path's 2e-2 budget; the fp32
+// path keeps the ex2/rcp forms of common.cuh).
+__device__ __forceinline__ float tanh_mufu(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
+__device__ __forceinline__ float sigm_mufu(float x) { return fmaf(0.5f, tanh_mufu(0.5f * x), 0.5f); }
 
 // Prologue: row q, K-atom ka, 16-byte chunk c of a resident B matrix (8 bf16)
 // <- the fp32 weights src[ka*64 + c*8 .. +8]
@@ -145,11 +179,22 @@ __device__ __forceinline__ void stage_weight_chunk(unsigned char *Bm, int rows, 
   *reinterpret_cast<uint4 *>(Bm + (size_t)ka * rows * 128 + sw128_off(q, c)) = v;
 }
 
+// debug timeline (cx_debug_set_trace): thread `who` of each CTA records
+// %globaltimer into slot s. Slots: 0 entry, 1 prologue done, 2+4l level l
+// start, 3+4l producers done, 4+4l MMA issue done, 5+4l epilogue done.
+__device__ __forceinline__ void tc_mark(const FwdArgs &a, int s, int who) {
+  if (a.trace && threadIdx.x == who && s < a.trace_slots) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[(size_t)blockIdx.x * a.trace_slots + s] = t;
+  }
+}
+
 template <int CELL, int H, int MAXC>
-__global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(FwdArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant__ TcArgs ta) {
+  const FwdArgs &a = ta.f;
   using C = TcCfg<CELL, H, MAXC>;
   constexpr int J = C::J, U = C::U, KA = C::KA, S = C::S;
-  constexpr int LAG = S - 1;
   extern __shared__ unsigned char smem_raw[];
   __shared__ TcMeta<J> meta[kMetaRing];
   __shared__ float s_bias[4 * U];
@@ -158,6 +203,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(FwdArgs a) {
   __shared__ uint32_t s_tmem;
 
   if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
+  tc_mark(a, 0, 0);
   const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n;
   const int gn = blockIdx.x / a.Gu, gu = blockIdx.x % a.Gu;
   const int unit0 = gu * U;
@@ -174,9 +220,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(FwdArgs a) {
 
   // ---- prologue: barriers, TMEM, biases, resident bf16 weights ---------------
   if (tid == 0) {
-    for (int s = 0; s < S; s++) { mbar_init(&bar_full[s], kProdThreads); mbar_init(&bar_empty[s], 1); }
-    for (int b = 0; b < 2; b++) { mbar_init(&bar_tfull[b], 1); mbar_init(&bar_tempty[b], kTM); }
-    for (int m = 0; m < kMetaRing; m++) { mbar_init(&bar_mfull[m], 1); mbar_init(&bar_mempty[m], kTM); }
+    for (int s = 0; s < S; s++) { mbar_init(&bar_full[s], 1); mbar_init(&bar_empty[s], C::CL); }
+    for (int b = 0; b < 2; b++) { mbar_init(&bar_tfull[b], 1); mbar_init(&bar_tempty[b], kEpiThreads); }
+    for (int m = 0; m < kMetaRing; m++) { mbar_init(&bar_mfull[m], 1); mbar_init(&bar_mempty[m], kEpiThreads); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) tmem_alloc<C::TCOLS>(&s_tmem);
@@ -236,14 +282,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(FwdArgs a) {
   }
   fence_proxy_async();  // resident weights (generic stores) -> tensor-core reads
   fence_before();
+  cluster_sync_all();   // peers' mbarriers initialised before any multicast
   grid_sync(a.bar, gridDim.x, epoch);
   fence_after();
   const uint32_t tmem = s_tmem;
+  tc_mark(a, 1, 0);
 
   uint32_t T0 = 0, Sg0 = 0;  // tiles / stages before this level (identical in every role)
   for (int l = 0; l < L; l++) {
     const bool leaf = l == 0;
     if (l > 0) grid_sync(a.bar, gridDim.x, epoch);
+    tc_mark(a, 2 + 4 * l, 0);
     int lo, hi;
     chunk_of(__ldg(a.lsize + l), a.Gn, gn, lo, hi);
     const int lb = __ldg(a.lbeg + l);
@@ -276,32 +325,47 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(FwdArgs a) {
     const int ntiles = (hi - lo + kTM - 1) / kTM;
     const int nsl = C::nslots(leaf);
 
-    if (warp >= kProd0) {
-      // =========================== producers ===================================
-      const int p = tid - kProd0 * 32;
-      uint32_t Sg = Sg0;
-      int pend = 0;
-      for (int t = 0; t < ntiles; t++) {
+    if (warp >= kMeta0) {
+      // ======================== tile bookkeeping ===============================
+      // lane handles rows lane + 32 q; two dependent rounds of index loads
+      const int mw = warp - kMeta0;
+      for (int t = mw; t < ntiles; t += kMetaWarps) {
         const uint32_t TT = T0 + t;
         const int ms = TT % kMetaRing;
         const int i0 = lo + t * kTM, cnt = min(kTM, hi - i0);
         mbar_wait(&bar_mempty[ms], ((TT / kMetaRing) & 1) ^ 1);
+        const int tslot = (l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
+        tc_mark(a, tslot + 0, warp * 32);
         TcMeta<J> &m = meta[ms];
-        if (p < kTM) {
-          const int r = p;
-          int own = -1, xr = -1, root = -1;
+        constexpr int RQ = kTM / 32;
+        int own[RQ], sv[RQ], ch[RQ][J];
+#pragma unroll
+        for (int q = 0; q < RQ; q++) {  // round 1: perm, structure, children
+          const int r = lane + 32 * q, i = i0 + r;
+          own[q] = -1;
+          sv[q] = -1;
+#pragma unroll
+          for (int k = 0; k < J; k++) ch[q][k] = -1;
           if (r < cnt) {
-            const int i = i0 + r;
-            own = __ldg(a.perm + i);
-            if (a.root_out) {
-              const int rr = __ldg(a.sid + i);
-              root = __ldg(a.roots + rr) == i ? rr : -1;
+            own[q] = __ldg(a.perm + i);
+            if (a.root_out) sv[q] = __ldg(a.sid + i);
+            if (!leaf) {
+#pragma unroll
+              for (int k = 0; k < J; k++) ch[q][k] = __ldg(a.chn + (size_t)k * n + i);
             }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < RQ; q++) {  // round 2: roots, words
+          const int r = lane + 32 * q, i = i0 + r;
+          int root = -1, xr = -1;
+          if (r < cnt) {
+            if (sv[q] >= 0) root = __ldg(a.roots + sv[q]) == i ? sv[q] : -1;
             if (C::XSLOT && (leaf || C::DAG)) {
               if (a.xmode == 0) {
-                int w = __ldg(a.words + own);
+                int w = __ldg(a.words + own[q]);
                 if (w < 0 || w >= a.V) {
-                  if (latch) latch_error(a.hdr, CX_E_WORD_RANGE, own);
+                  if (latch) latch_error(a.hdr, CX_E_WORD_RANGE, own[q]);
                   w = 0;
                 }
                 xr = w;
@@ -309,68 +373,69 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(FwdArgs a) {
                 xr = i - xlo;
               }
             }
+            if (!leaf) {
+              int nc = 0;
+              bool absent = false;
+#pragma unroll
+              for (int k = 0; k < J; k++) {
+                absent = absent || ch[q][k] < 0;
+                if (absent) ch[q][k] = -1;
+                nc += ch[q][k] >= 0;
+              }
+              if (C::FC && nc != 2 && latch) latch_error(a.hdr, CX_E_ARITY, own[q]);
+            }
           }
-          m.own[r] = own;
+          m.own[r] = own[q];
           m.xr[r] = xr;
           m.root[r] = root;
-          if (r == 0) { m.i0 = i0; m.cnt = cnt; }
-        } else if (!leaf) {
-          const int r = p - kTM;
-          int ch[J];
-          int nc = 0;
-          bool absent = false;
 #pragma unroll
-          for (int k = 0; k < J; k++) {
-            int c = -1;
-            if (r < cnt) c = __ldg(a.chn + (size_t)k * n + i0 + r);
-            absent = absent || c < 0;
-            ch[k] = absent ? -1 : c;
-            nc += ch[k] >= 0;
-          }
-          if (C::FC && r < cnt && nc != 2) {
-            if (latch) latch_error(a.hdr, CX_E_ARITY, __ldg(a.perm + i0 + r));
-          }
-#pragma unroll
-          for (int k = 0; k < J; k++) m.ch[k][r] = ch[k];
+          for (int k = 0; k < J; k++) m.ch[k][r] = ch[q][k];
         }
-        named_bar(1, kProdThreads);
-        if (p == 0) mbar_arrive(&bar_mfull[ms]);
+        if (lane == 0) { m.i0 = i0; m.cnt = cnt; }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_mfull[ms]);
+        tc_mark(a, tslot + 1, warp * 32);
+      }
+    } else if (warp == kTmaWarp) {
+      // ========================= TMA gathers ===================================
+      // per stage: one K-atom (64 bf16) of one slot for the tile's 128 rows.
+      // This CTA (cluster rank cr) fetches rows [cr*RPC, (cr+1)*RPC) with
+      // tile::gather4 (lane q: 4 rows) multicast to every CTA of the cluster;
+      // absent children / unused rows are row -1 -> zeros.
+      constexpr int CL = C::CL, RPC = kTM / CL;
+      constexpr uint16_t mask = (uint16_t)((1u << CL) - 1);
+      const int cr = gu % CL;
+      uint32_t Sg = Sg0;
+      for (int t = 0; t < ntiles; t++) {
+        const uint32_t TT = T0 + t;
+        const int ms = TT % kMetaRing;
+        mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
+        const TcMeta<J> &m = meta[ms];
         for (int ka = 0; ka < KA; ka++) {
           for (int s = 0; s < nsl; s++) {
             int src, bm, acc;
             C::slot(leaf, s, src, bm, acc);
             const int st = Sg % S;
-            mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);
-            const uint32_t dst0 = smem_u32(sStage + (size_t)st * kStageBytes);
-#pragma unroll
-            for (int e = 0; e < kChunksPerThread; e++) {
-              const int q = p + kProdThreads * e, r = q >> 3, c = q & 7;
-              int row;
-              const unsigned short *base;
-              if (src < 0) { row = m.xr[r]; base = xb; }
-              else { row = m.ch[src][r]; base = hb; }
-              const bool valid = row >= 0;
-              const unsigned short *g = base + (size_t)(valid ? row : 0) * H + ka * 64 + c * 8;
-              cp16_zfill(dst0 + sw128_off(r, c), g, valid);
+            const int kst = (int)(Sg - Sg0);
+            const int sslot = (l == 0 && kst >= 4 && kst < 12) ? 64 + 4 * (kst - 4)
+                              : (l == 1 && kst < 8) ? 96 + 4 * kst : 1 << 30;
+            mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);  // free in every CTA of the cluster
+            tc_mark(a, sslot + 0, kTmaWarp * 32);
+            if (lane == 0) mbar_arrive_expect_tx(&bar_full[st], kStageBytes);
+            if (lane < RPC / 4) {
+              const int rb = cr * RPC + 4 * lane;
+              const int4 rv = *reinterpret_cast<const int4 *>((src < 0 ? m.xr : m.ch[src]) + rb);
+              tma_gather4_mc(smem_u32(sStage + (size_t)st * kStageBytes + rb * 128),
+                             src < 0 ? (const void *)&ta.tm_x : (const void *)&ta.tm_h,
+                             &bar_full[st], ka * 64, rv.x, rv.y, rv.z, rv.w, mask);
             }
-            cp_async_commit();
+            __syncwarp();
+            tc_mark(a, sslot + 1, kTmaWarp * 32);
             Sg++;
-            pend++;
-            if (pend > LAG) {
-              cp_wait_group<LAG>();
-              fence_proxy_async();
-              mbar_arrive(&bar_full[(Sg - pend) % S]);
-              pend--;
-            }
           }
         }
       }
-      cp_async_wait_all();
-      fence_proxy_async();
-      while (pend > 0) {
-        mbar_arrive(&bar_full[(Sg - pend) % S]);
-        pend--;
-      }
+      tc_mark(a, 3 + 4 * l, kTmaWarp * 32);
     } else if (warp == kMmaWarp) {
       // =========================== MMA issuer ==================================
       if (lane == 0) {
@@ -381,13 +446,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(FwdArgs a) {
           const uint32_t TT = T0 + t, buf = TT & 1;
           mbar_wait(&bar_tempty[buf], ((TT >> 1) & 1) ^ 1);
           fence_after();
+          const int tslot = (l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
+          tc_mark(a, tslot + 2, kMmaWarp * 32);
           uint32_t started = 0;
           for (int ka = 0; ka < KA; ka++) {
             for (int s = 0; s < nsl; s++) {
               int src, bm, acc;
               C::slot(leaf, s, src, bm, acc);
               const int st = Sg % S;
+              const int kst = (int)(Sg - Sg0);
+              const int sslot = (l == 0 && kst >= 4 && kst < 12) ? 64 + 4 * (kst - 4)
+                                : (l == 1 && kst < 8) ? 96 + 4 * kst : 1 << 30;
               mbar_wait(&bar_full[st], (Sg / S) & 1);
+              tc_mark(a, sslot + 2, kMmaWarp * 32);
               fence_after();
               const uint32_t a0 = smem_u32(sStage + (size_t)st * kStageBytes);
               const uint32_t b0 = smem_u32((bm ? sB1 : sB0) + (size_t)ka * (bm ? C::B1 : C::B0) * 128);
@@ -398,108 +469,129 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(FwdArgs a) {
                 mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, accum);
               }
               started |= 1u << acc;
-              mma_commit(&bar_empty[st]);
+              mma_commit_mc(&bar_empty[st], (uint16_t)((1u << C::CL) - 1));  // frees the slot cluster-wide
+              tc_mark(a, sslot + 3, kMmaWarp * 32);
               Sg++;
             }
           }
           mma_commit(&bar_tfull[buf]);
+          tc_mark(a, tslot + 3, kMmaWarp * 32);
         }
+        tc_mark(a, 4 + 4 * l, kMmaWarp * 32);
       }
       __syncwarp();
     } else {
       // =========================== epilogue ====================================
-      const int r = tid;  // tile row = TMEM lane
+      // thread = tile row r (TMEM lane) x column half hh: units [u0, u0 + U/2)
+      constexpr int UC = U / 2;
+      const int q4 = warp & 3, hh = warp >> 2;
+      const int r = q4 * 32 + lane, u0 = hh * UC;
       for (int t = 0; t < ntiles; t++) {
         const uint32_t TT = T0 + t, buf = TT & 1;
         const int ms = TT % kMetaRing;
         mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
-        mbar_wait(&bar_tfull[buf], (TT >> 1) & 1);
-        fence_after();
         const TcMeta<J> &m = meta[ms];
         const bool valid = r < m.cnt;
         const int i = m.i0 + r, own = m.own[r], root = m.root[r];
-        const uint32_t tb = tmem + ((uint32_t)(warp * 32) << 16) + buf * C::BUFC;
+        const int tslot = (l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
+        const uint32_t tb = tmem + ((uint32_t)(q4 * 32) << 16) + buf * C::BUFC + u0;
         if constexpr (C::LSTM) {
-          float c[32], h[32], v[32], w[32];
+          static_assert(UC == 16, "TreeLSTM epilogue: 16 units per thread");
+          constexpr int NL = C::NLVL;
+          float c[16], h[16], v[16], w[16];
+          float cp[J][16];  // children's memory cells (prefetched before the MMA wait)
+          int ck[J];
+#pragma unroll
+          for (int k = 0; k < J; k++) {
+            ck[k] = (valid && !leaf) ? m.ch[k][r] : -1;
+            if (ck[k] >= 0) {
+              const float4 *src = reinterpret_cast<const float4 *>(cs + (size_t)ck[k] * H + unit0 + u0);
+#pragma unroll
+              for (int q = 0; q < 4; q++) {
+                const float4 x = __ldcg(src + q);
+                cp[k][4 * q] = x.x; cp[k][4 * q + 1] = x.y; cp[k][4 * q + 2] = x.z; cp[k][4 * q + 3] = x.w;
+              }
+            }
+          }
+          mbar_wait(&bar_tfull[buf], (TT >> 1) & 1);
+          fence_after();
+          tc_mark(a, tslot + 4, 0);
+          const float *bi = s_bias + u0, *bo = bi + U, *bu = bi + 2 * U, *bf = bi + 3 * U;
           if (leaf) {
-            tmem_ld32(tb + 0, v);        // i
-            tmem_ld32(tb + 2 * U, w);    // u
+            tmem_ld<16>(tb + 0, v);        // i
+            tmem_ld<16>(tb + 2 * U, w);    // u
 #pragma unroll
-            for (int j = 0; j < 32; j++) c[j] = sigmoidf_(v[j] + s_bias[j]) * tanhf_(w[j] + s_bias[2 * U + j]);
-            tmem_ld32(tb + U, v);        // o
+            for (int j = 0; j < 16; j++) c[j] = sigm_mufu(v[j] + bi[j]) * tanh_mufu(w[j] + bu[j]);
+            tmem_ld<16>(tb + U, v);        // o
 #pragma unroll
-            for (int j = 0; j < 32; j++) h[j] = sigmoidf_(v[j] + s_bias[U + j]) * tanhf_(c[j]);
+            for (int j = 0; j < 16; j++) h[j] = sigm_mufu(v[j] + bo[j]) * tanh_mufu(c[j]);
           } else {
-            constexpr int NL = C::NLVL;
-            // sum_k f_k * c_k
 #pragma unroll
-            for (int j = 0; j < 32; j++) c[j] = 0.f;
+            for (int j = 0; j < 16; j++) c[j] = 0.f;
 #pragma unroll
-            for (int k = 0; k < J; k++) {
-              const int ck = valid ? m.ch[k][r] : -1;
-              if (ck >= 0) {
-                const float4 *cp = reinterpret_cast<const float4 *>(cs + (size_t)ck * H + unit0);
+            for (int k = 0; k < J; k++) {  // sum_k f_k * c_k
+              tmem_ld<16>(tb + k * NL + 3 * U, v);
+              if (ck[k] >= 0) {
 #pragma unroll
-                for (int q = 0; q < 8; q++) {
-                  float4 x = __ldcg(cp + q);
-                  w[4 * q] = x.x; w[4 * q + 1] = x.y; w[4 * q + 2] = x.z; w[4 * q + 3] = x.w;
-                }
-              }
-              tmem_ld32(tb + k * NL + 3 * U, v);  // f_k
-              if (ck >= 0) {
-#pragma unroll
-                for (int j = 0; j < 32; j++) c[j] += sigmoidf_(v[j] + s_bias[3 * U + j]) * w[j];
+                for (int j = 0; j < 16; j++) c[j] = fmaf(sigm_mufu(v[j] + bf[j]), cp[k][j], c[j]);
               }
             }
-            // i = sum_k acc_k[i], u = sum_k acc_k[u]
-            tmem_ld32(tb + 0, v);
-            tmem_ld32(tb + 2 * U, w);
+            tmem_ld<16>(tb + 0, v);        // i = sum_k acc_k[i], u = sum_k acc_k[u]
+            tmem_ld<16>(tb + 2 * U, w);
 #pragma unroll
             for (int k = 1; k < J; k++) {
-              tmem_ld32(tb + k * NL + 0, h);
+              tmem_ld<16>(tb + k * NL + 0, h);
 #pragma unroll
-              for (int j = 0; j < 32; j++) v[j] += h[j];
-              tmem_ld32(tb + k * NL + 2 * U, h);
+              for (int j = 0; j < 16; j++) v[j] += h[j];
+              tmem_ld<16>(tb + k * NL + 2 * U, h);
 #pragma unroll
-              for (int j = 0; j < 32; j++) w[j] += h[j];
+              for (int j = 0; j < 16; j++) w[j] += h[j];
             }
 #pragma unroll
-            for (int j = 0; j < 32; j++) c[j] += sigmoidf_(v[j] + s_bias[j]) * tanhf_(w[j] + s_bias[2 * U + j]);
-            tmem_ld32(tb + U, v);
+            for (int j = 0; j < 16; j++) c[j] = fmaf(sigm_mufu(v[j] + bi[j]), tanh_mufu(w[j] + bu[j]), c[j]);
+            tmem_ld<16>(tb + U, v);        // o
 #pragma unroll
             for (int k = 1; k < J; k++) {
-              tmem_ld32(tb + k * NL + U, h);
+              tmem_ld<16>(tb + k * NL + U, h);
 #pragma unroll
-              for (int j = 0; j < 32; j++) v[j] += h[j];
+              for (int j = 0; j < 16; j++) v[j] += h[j];
             }
 #pragma unroll
-            for (int j = 0; j < 32; j++) h[j] = sigmoidf_(v[j] + s_bias[U + j]) * tanhf_(c[j]);
+            for (int j = 0; j < 16; j++) h[j] = sigm_mufu(v[j] + bo[j]) * tanh_mufu(c[j]);
           }
           if (valid) {
-            store_f32x32(a.h_out + (size_t)own * H + unit0, h);
-            store_bf16x32(hb + (size_t)i * H + unit0, h);
-            store_f32x32(cs + (size_t)i * H + unit0, c);
-            if (a.aux_out) store_f32x32(a.aux_out + (size_t)own * H + unit0, c);
-            if (root >= 0) store_f32x32(a.root_out + (size_t)root * H + unit0, h);
+            const size_t uo = (size_t)own * H + unit0 + u0, ui = (size_t)i * H + unit0 + u0;
+            store_f32_stream<16>(a.h_out + uo, h);
+            store_bf16<16>(hb + ui, h);
+            store_f32<16>(cs + ui, c);
+            if (a.aux_out) store_f32_stream<16>(a.aux_out + uo, c);
+            if (root >= 0) store_f32_stream<16>(a.root_out + (size_t)root * H + unit0 + u0, h);
           }
-        } else {  // DAG-RNN / TreeFC: h = tanh(acc + b), U / 32 column chunks
+        } else {  // DAG-RNN / TreeFC: h = tanh(acc + b)
+          constexpr int CW = UC < 32 ? UC : 32;
+          mbar_wait(&bar_tfull[buf], (TT >> 1) & 1);
+          fence_after();
+          tc_mark(a, tslot + 4, 0);
 #pragma unroll 1
-          for (int q = 0; q < U / 32; q++) {
-            float v[32];
-            tmem_ld32(tb + q * 32, v);
+          for (int q = 0; q < UC / CW; q++) {
+            float v[CW];
+            tmem_ld<CW>(tb + q * CW, v);
 #pragma unroll
-            for (int j = 0; j < 32; j++) v[j] = tanhf_(v[j] + s_bias[q * 32 + j]);
+            for (int j = 0; j < CW; j++) v[j] = tanh_mufu(v[j] + s_bias[u0 + q * CW + j]);
             if (valid) {
-              store_f32x32(a.h_out + (size_t)own * H + unit0 + q * 32, v);
-              store_bf16x32(hb + (size_t)i * H + unit0 + q * 32, v);
-              if (root >= 0) store_f32x32(a.root_out + (size_t)root * H + unit0 + q * 32, v);
+              const int uu = unit0 + u0 + q * CW;
+              store_f32_stream<CW>(a.h_out + (size_t)own * H + uu, v);
+              store_bf16<CW>(hb + (size_t)i * H + uu, v);
+              if (root >= 0) store_f32_stream<CW>(a.root_out + (size_t)root * H + uu, v);
             }
           }
         }
         fence_before();
         mbar_arrive(&bar_tempty[buf]);
         mbar_arrive(&bar_mempty[ms]);
+        tc_mark(a, tslot + 5, 0);
       }
+      tc_mark(a, 5 + 4 * l, 0);
     }
     T0 += ntiles;
     Sg0 += (uint32_t)ntiles * KA * nsl;
@@ -508,6 +600,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(FwdArgs a) {
   // ---- teardown -------------------------------------------------------------
   fence_before();
   __syncthreads();
+  cluster_sync_all();  // no peer still signals this CTA's barriers
   if (warp == kMmaWarp) {
     fence_after();
     tmem_free<C::TCOLS>(tmem);
@@ -529,15 +622,36 @@ bool tc_plan_one(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
     }
     set = true;
   }
-  *Gu = H / C::U;
-  *Gn = num_sms / *Gu;
+  static int max_clusters = -1;  // co-resident clusters (the grid barrier needs all)
+  if (max_clusters < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C::CL * 64);
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = C::dyn_bytes;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C::CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, (const void *)k, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      nc = 0;
+    }
+    max_clusters = nc;
+  }
+  *Gu = C::GU;
+  *Gn = min(num_sms / C::GU, max_clusters * C::CL / C::GU);
   if (*Gn < 1) return false;
   p->ctas = *Gn * *Gu;
   p->threads = kTcThreads;
   p->smem = C::dyn_bytes;
   p->kernel = (const void *)k;
-  p->cluster = 1;
+  p->cluster = C::CL;
   p->big = false;
+  p->tc = true;
   return true;
 }
 
@@ -572,6 +686,68 @@ bool tc_plan(int cell, int H, int maxc, int num_sms, FwdPlan *p, int *Gn, int *G
       return false;
   }
   return false;
+}
+
+// ---- launch: tensor maps of the gathered operands + cooperative launch --------
+namespace {
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                   const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                   const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static std::once_flag once;
+  static EncodeTiledFn fn = nullptr;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+// [rows][H] bf16 row-major, box = 64 columns x 1 row, 128-byte swizzle
+bool encode_rows(TmaDesc *d, const void *base, int H, long long rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || rows < 1) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)H, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)H * 2};
+  cuuint32_t box[2] = {64, 1}, es[2] = {1, 1};
+  return fn(reinterpret_cast<CUtensorMap *>(d), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+            const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &f, cudaStream_t stream) {
+  static_assert(sizeof(TmaDesc) == sizeof(CUtensorMap), "tensor map size");
+  TcArgs ta;
+  std::memset(&ta, 0, sizeof ta);
+  ta.f = f;
+  const long long xrows = f.xmode ? f.n : f.V;
+  if (!encode_rows(&ta.tm_h, f.hb, f.H, f.n)) return cudaErrorInvalidValue;
+  if (f.cell_has_x ? !encode_rows(&ta.tm_x, f.xb, f.H, xrows) : false) return cudaErrorInvalidValue;
+  if (!f.cell_has_x) ta.tm_x = ta.tm_h;
+  void *params[] = {&ta};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(plan.ctas);
+  cfg.blockDim = dim3(plan.threads);
+  cfg.dynamicSmemBytes = plan.smem;
+  cfg.stream = stream;
+  // thread-block clusters (no cooperative attribute: the grid was sized from
+  // cudaOccupancyMaxActiveClusters so every CTA is co-resident)
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = plan.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, plan.kernel, params);
 }
 
 // x rows in node order when the batch has at most V/2 of them, else the table

@@ -31,6 +31,7 @@ struct FwdArgs {
   float *cs;           // [n][H] fp32 TreeLSTM memory cells, new numbering
   unsigned short *xb;  // bf16 input rows: [V][H] (xmode 0) or [n - xlo][H] node order (xmode 1)
   int xmode;
+  int cell_has_x;      // the cell gathers input rows (TreeLSTM, DAG-RNN)
   GridBar *bar;
   int Gn, Gu;   // node groups x unit groups = CTAs
   unsigned long long *trace;  // debug: %globaltimer per CTA and phase (cx_debug_set_trace)
@@ -52,6 +53,7 @@ struct FwdPlan {
   const void *kernel;
   int cluster = 1;  // > 1: thread-block clusters of this size (no cooperative launch)
   bool big = false; // large-batch pipelined kernel: workspace holds hs, st [n][H] + words [n]
+  bool tc = false;  // bf16 tensor-core kernel (forward_tc.cu): launched by tc_launch
 };
 
 // Returns false (CX_E_UNSUPPORTED) when no instantiation covers the model.
@@ -67,6 +69,7 @@ size_t fwd_workspace_bytes(int cell, int H, int n);
 bool tc_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
 int tc_xmode(int n, int V);
 size_t tc_workspace_bytes(int cell, int H, int V, int n);
+cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &args, cudaStream_t stream);
 cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream);
 
 }  // namespace cx
