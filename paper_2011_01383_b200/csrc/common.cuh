@@ -81,6 +81,17 @@ __device__ __forceinline__ void grid_exit(GridBar *bar, unsigned nblocks) {
   }
 }
 
+// Programmatic dependent launch (PDL): cx_linearize lets the dependent
+// cx_forward grid start early; the forward stages its weights, then waits for
+// the linearization (and its memory) before reading it. Without a PDL edge
+// (standalone launch) the wait returns immediately.
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // Latch a data error: lowest (code, node) wins.
 __device__ __forceinline__ void latch_error(cx_lin_header *h, int code, int node) {
   unsigned long long key = ((unsigned long long)(unsigned)code << 32) | (unsigned)node;

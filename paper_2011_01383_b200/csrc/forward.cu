@@ -604,6 +604,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) fwd_kernel(FwdArgs a) {
   using Lay = Layout<CELL, MAXC>;
   using Tr = Traits<CELL, MAXC>;
 
+  griddep_wait();
   if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
   const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n;
   const int gn = blockIdx.x / a.Gu, gu = blockIdx.x % a.Gu;
@@ -811,7 +812,7 @@ cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream) 
   cfg.blockDim = dim3(plan.threads);
   cfg.dynamicSmemBytes = plan.smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   if (plan.cluster > 1) {  // independent clusters: no grid barrier, no co-residency needed
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = plan.cluster;
@@ -821,8 +822,12 @@ cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream) 
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
   }
+  // programmatic dependent launch: the kernel stages its weights while the
+  // preceding cx_linearize runs (griddepcontrol.wait before reading it)
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelExC(&cfg, plan.kernel, params);
 }
 

@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
   __shared__ BMeta meta[S];
   __shared__ float s_bias[4 * kUG];
 
+  griddep_wait();
   if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
   const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n;
   const int gn = blockIdx.x / a.Gu, gu = blockIdx.x % a.Gu;

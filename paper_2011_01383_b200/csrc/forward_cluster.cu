@@ -121,8 +121,6 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   __shared__ float s_bias[4 * kCUnits];
 
   cg::cluster_group cl = cg::this_cluster();
-  if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
-  const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n, R = a.hdr->num_roots;
   const int maxc = a.maxc;
   const int crank = (int)cl.block_rank();
   const int cid = blockIdx.x / (int)cl.num_blocks(), ncl = gridDim.x / (int)cl.num_blocks();
@@ -131,6 +129,32 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   const int unit0 = crank * kCUnits;
   const bool latch = crank == 0;
   trace_mark(a, 0);
+
+  // ---- weights -> registers (first the leaf / projection gates): inputs only,
+  // so this overlaps cx_linearize under programmatic dependent launch --------
+  float w[4][KC];
+  Gate gs[4];
+  int ng;
+  if constexpr (CELL == CX_TREELSTM) {
+    gs[0] = {a.w[0], 0, H, 0}; gs[1] = {a.w[0], H, H, 0}; gs[2] = {a.w[0], 2 * H, H, 0};
+    ng = 3;
+  } else {
+    gs[0] = {a.w[0], 0, H, 0}; gs[1] = {a.w[1], 0, H, 0};
+    ng = 2;
+  }
+  load_wregs<4, KC>(w, gs, ng, unit0 + u, k0);
+  if constexpr (CELL == CX_TREELSTM) {
+    if (tid < 4 * kCUnits) {
+      int g = tid / kCUnits, uu = tid % kCUnits;
+      const float *b = g < 3 ? a.w[2] + g * H : a.w[4];
+      s_bias[tid] = __ldg(b + unit0 + uu);
+    }
+  } else {
+    if (tid < kCUnits) s_bias[tid] = __ldg(a.w[2] + unit0 + tid);
+  }
+  griddep_wait();
+  if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
+  const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n, R = a.hdr->num_roots;
 
   CS s;
   s.X = smem;
@@ -161,27 +185,6 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   ctx.latch = latch;
   ctx.tslot = -1;
 
-  // ---- weights -> registers (first the leaf / projection gates) -----------
-  float w[4][KC];
-  Gate gs[4];
-  int ng;
-  if constexpr (CELL == CX_TREELSTM) {
-    gs[0] = {a.w[0], 0, H, 0}; gs[1] = {a.w[0], H, H, 0}; gs[2] = {a.w[0], 2 * H, H, 0};
-    ng = 3;
-  } else {
-    gs[0] = {a.w[0], 0, H, 0}; gs[1] = {a.w[1], 0, H, 0};
-    ng = 2;
-  }
-  load_wregs<4, KC>(w, gs, ng, unit0 + u, k0);
-  if constexpr (CELL == CX_TREELSTM) {
-    if (tid < 4 * kCUnits) {
-      int g = tid / kCUnits, uu = tid % kCUnits;
-      const float *b = g < 3 ? a.w[2] + g * H : a.w[4];
-      s_bias[tid] = __ldg(b + unit0 + uu);
-    }
-  } else {
-    if (tid < kCUnits) s_bias[tid] = __ldg(a.w[2] + unit0 + tid);
-  }
 
   // ---- prologue: structure labels (root index, propagated top-down) --------
   for (int l = tid; l < L; l += blockDim.x) {

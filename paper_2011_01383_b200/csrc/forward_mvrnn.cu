@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kT, 1) mvrnn_kernel(FwdArgs a) {
   float *pv = bv + H;            // p = [B a; A b] [2H]
   __shared__ int s_own, s_cin[2], s_leafw[2], s_isleaf[2];
 
+  griddep_wait();
   if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
   const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n;
   const int tid = threadIdx.x, G = gridDim.x, g = blockIdx.x;

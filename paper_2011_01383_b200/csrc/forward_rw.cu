@@ -328,8 +328,6 @@ __global__ void __launch_bounds__(kRThreads, 1) rw_kernel(FwdArgs a) {
   __shared__ typename C::M meta;
   __shared__ float s_bias[4 * kRUG];
 
-  if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
-  const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n;
   const int gn = blockIdx.x / a.Gu, gu = blockIdx.x % a.Gu;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int u = lane & 15, k0 = (warp * 2 + (lane >> 4)) * KC;
@@ -368,6 +366,12 @@ __global__ void __launch_bounds__(kRThreads, 1) rw_kernel(FwdArgs a) {
     int ng = C::leaf_gates(a, gs);
     load_wregs<Cfg::NG, KC>(w, gs, ng, ctx.unit0 + u, k0);
     trace_mark(a, 1);
+  }
+  // the linearization is read from here on (PDL: weights staged meanwhile)
+  griddep_wait();
+  if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
+  const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n;
+  {
     const int lo0 = C::leaf_lo(first_leaf);
     int lo, hi;
     chunk_of(n - lo0, a.Gn, gn, lo, hi);

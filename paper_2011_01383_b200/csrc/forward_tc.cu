@@ -202,9 +202,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
       bar_mfull[kMetaRing], bar_mempty[kMetaRing];
   __shared__ uint32_t s_tmem;
 
-  if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
   tc_mark(a, 0, 0);
-  const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n;
+  const int n = a.n;
   const int gn = blockIdx.x / a.Gu, gu = blockIdx.x % a.Gu;
   const int unit0 = gu * U;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -215,7 +214,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
   unsigned short *hb = a.hb;
   float *cs = a.cs;
   const unsigned short *xb = a.xb;
-  const int xlo = C::DAG ? 0 : first_leaf;  // node-order x rows start here
   unsigned epoch = 0;
 
   // ---- prologue: barriers, TMEM, biases, resident bf16 weights ---------------
@@ -253,8 +251,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     }
     stage_weight_chunk(second ? sB1 : sB0, second ? C::B1 : C::B0, q, ka, c, src);
   }
+  // the linearization is read from here on (PDL: the above overlapped it)
+  griddep_wait();
+  const int status0 = *reinterpret_cast<volatile int *>(&a.hdr->status);
+  const int L = status0 == CX_OK ? a.hdr->num_levels : 0, first_leaf = a.hdr->first_leaf;
+  const int xlo = C::DAG ? 0 : first_leaf;  // node-order x rows start here
   // ---- phase 0: bf16 input rows ------------------------------------------------
-  if constexpr (C::XSLOT) {
+  if (C::XSLOT && status0 == CX_OK) {
     const size_t total_threads = (size_t)gridDim.x * blockDim.x;
     const size_t gt = (size_t)blockIdx.x * blockDim.x + tid;
     constexpr int q8 = H / 8;
@@ -740,13 +743,15 @@ cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &f, cudaStream_t stream
   cfg.stream = stream;
   // thread-block clusters (no cooperative attribute: the grid was sized from
   // cudaOccupancyMaxActiveClusters so every CTA is co-resident)
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = plan.cluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap cx_linearize
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelExC(&cfg, plan.kernel, params);
 }
 

@@ -33,11 +33,12 @@ __device__ __forceinline__ void lin_mark(const LinArgs &a, int s) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[s] = t;
-    a.trace[8 + s] = clock64();
+    a.trace[16 + s] = clock64();
   }
 }
 
-inline size_t lin_budget_entries(int n) { return 2 * (size_t)n + 4096; }
+// multi-CTA path: parent pointers [n] + per-block level-count table
+inline size_t lin_budget_entries(int n) { return 2 * (size_t)n + 40960; }
 
 inline size_t lin_workspace_bytes(int n) {
   return sizeof(GridBar) + 32 * sizeof(int32_t) + sizeof(int32_t) * (2 * (size_t)n) +

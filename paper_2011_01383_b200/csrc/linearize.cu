@@ -8,14 +8,17 @@
 // the highest ids. Here the same arrays are produced on the GPU so the
 // forward kernel can start without a host round trip:
 //   a1 validate + in-degree     one pass, atomics
-//   a2 heights                  Jacobi rounds h(v) = 1 + max h(children);
-//                               round r finalises exactly the nodes of height r
-//   a3 level histogram + scan   per-(level, id-segment) counts, one scan
+//   a2 heights                  trees/sequences: leaf-to-root walk-up with
+//                               pending-child counts (last child continues);
+//                               DAGs: Jacobi rounds (round r finalises the
+//                               nodes of height r)
+//   a3 level histogram + scan   per-(level, block/segment) counts, one scan
 //   a4 stable scatter           warp __match_any_sync ranking, ascending input
 //                               id inside a level (reading Q4)
 //   a5 remap                    children_new[k][i] = inv[children[k][perm[i]]]
-// Two instantiations: one CTA with everything in shared memory (small n: the
-// latency configs) and a cooperative multi-CTA one with the grid barrier of
+//   a6 structures               root index of every node
+// Two kernels: one CTA with everything in shared memory (small n: the latency
+// configs) and a cooperative multi-CTA one with the grid barrier of
 // common.cuh (b4096 and large DAGs).
 #include <cuda_runtime.h>
 
@@ -31,18 +34,8 @@ namespace {
 constexpr int kLinThreads = 1024;   // multi-CTA path
 constexpr int kLinSingleThreads = 512;
 constexpr int kSegMin = 256;
-
-template <bool MULTI>
-__device__ __forceinline__ int ld_dyn(const int *p) {
-  if constexpr (MULTI) return __ldcg(p);
-  else return *reinterpret_cast<const volatile int *>(p);
-}
-
-template <bool MULTI>
-__device__ __forceinline__ void lsync(GridBar *bar, unsigned &epoch) {
-  if constexpr (MULTI) grid_sync(bar, gridDim.x, epoch);
-  else __syncthreads();
-}
+constexpr int kLinTabLevels = 256;  // levels handled by the block-chunked sort (lin_kernel)
+constexpr size_t kLinMultiSmem = sizeof(int) * (2 + 32) * kLinTabLevels;
 
 // block-wide exclusive scan of one value per thread; returns the block total
 __device__ int block_exclusive_scan(int v, int &total, int *s_tmp) {
@@ -72,312 +65,464 @@ __device__ int block_exclusive_scan(int v, int &total, int *s_tmp) {
   return excl;
 }
 
-template <bool MULTI>
+// ---------------------------------------------------------------------------
+// Multi-CTA linearizer (large n): one 1024-thread CTA per SM, cooperative
+// launch, release/acquire grid barrier between phases.
+//   P1  validate + in-degree; trees/sequences also record parent pointers and
+//       child counts
+//   P3  heights. Trees/sequences: every leaf walks up its parent chain with
+//       global atomics (atomicMax of the height, atomicSub of the pending
+//       child count; only the last arriving child continues): O(n) work and no
+//       barrier per level. DAGs: Jacobi rounds (round r finalises exactly the
+//       nodes of height r), one barrier each.
+//   P4-P6 stable counting sort by height, block-chunked: CTA b owns the ids
+//       [b C, (b+1) C); it counts its ids per level in shared memory (warp
+//       match aggregation), publishes a (L+1) x G table, derives its own
+//       output offsets from the table, and scatters its ids in ascending order
+//       (warp match ranks + per-warp prefix counts). Roots are the extra row L.
+//       Very deep structures (L + 1 > kLinTabLevels) use the per-segment
+//       variant below instead.
+//   P7  remap children to new ids
+//   P8  structures: trees walk up to their root; DAGs propagate the smallest
+//       root index top-down, one level per round.
 __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
-  extern __shared__ int smem[];
+  griddep_launch_dependents();
+  lin_mark(a, 7);
+  extern __shared__ int lsm[];  // [kLinTabLevels] x 2 + [32][kLinTabLevels]
   __shared__ int s_tmp[33];
-  __shared__ int s_count;
-  __shared__ int s_fin;  // finished-node counter (single-CTA path)
   const int n = a.n, maxc = a.maxc;
+  const int G = gridDim.x;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int nthr = gridDim.x * blockDim.x;
+  const int nthr = G * blockDim.x;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;  // warp in block
+  const unsigned lt = (1u << lane) - 1u;
+  const bool tree_like = a.kind != CX_DAG;
   unsigned epoch = 0;
-
-  // working arrays: shared memory on the single-CTA path, workspace otherwise
-  int *indeg, *hgt;
-  const int *ch;
-  if constexpr (MULTI) {
-    indeg = a.indeg;
-    hgt = a.hgt;
-    ch = a.ch;
-  } else {
-    indeg = smem;
-    hgt = smem + n;
-    int *chs = smem + 2 * n;
-    for (int i = threadIdx.x; i < maxc * n; i += blockDim.x) chs[i] = __ldg(a.ch + i);
-    ch = chs;
-  }
+  int *indeg = a.indeg, *hgt = a.hgt;
+  const int *ch = a.ch;
+  int *parent = a.cnt;       // [n] parent input id (trees/sequences), -1 = root
+  int *pending = a.perm;     // [n] children not yet final (free until P6)
+  int *tab = a.cnt + n;      // (L + 1) x G per-block counts
 
   // ---- P0: init --------------------------------------------------------
   for (int v = tid; v < n; v += nthr) {
     indeg[v] = 0;
     hgt[v] = -1;
-    if constexpr (MULTI) a.sid[v] = INT_MAX;
+    a.sid[v] = INT_MAX;
+    if (tree_like) parent[v] = -1;
   }
-  // Finished-node counts. Multi-CTA: misc[3] counts leaves and round r adds
-  // into misc[r % 3]; a slot is read by every CTA right after barrier r and
-  // cleared (by CTA 0) only after barrier r + 1, so no CTA can observe another
-  // round's additions (which would desynchronise the round loop).
-  int *fin_ptr = MULTI ? &a.misc[3] : &s_fin;
   if (tid == 0) {
     a.hdr->err_key = kNoError;
-    *fin_ptr = 0;
-    if constexpr (MULTI) a.misc[0] = a.misc[1] = a.misc[2] = 0;
+    a.misc[0] = a.misc[1] = a.misc[2] = a.misc[3] = a.misc[4] = a.misc[5] = 0;
   }
-  if (threadIdx.x == 0) {
-    s_count = 0;
-    s_tmp[32] = 0;
-  }
-  lsync<MULTI>(a.bar, epoch);
+  if (threadIdx.x == 0) s_tmp[32] = 0;
+  grid_sync(a.bar, G, epoch);
+  lin_mark(a, 8);
 
-  // ---- P1 (a1): validate, in-degree --------------------------------------
+  // ---- P1 (a1): validate, in-degree, parent pointers ----------------------
   for (int v = tid; v < n; v += nthr) {
     bool absent = false;
+    int nc = 0;
     for (int k = 0; k < maxc; k++) {
       int c = ch[k * n + v];
       if (c == -1) {
         absent = true;
         continue;
       }
+      nc++;
       if (absent) latch_error(a.hdr, CX_E_CHILD_LAYOUT, v);
       if (c < 0 || c >= n) {
         latch_error(a.hdr, CX_E_CHILD_RANGE, v);
         continue;
       }
       atomicAdd(&indeg[c], 1);
+      if (tree_like) parent[c] = v;
       for (int k2 = 0; k2 < k; k2++)
         if (ch[k2 * n + v] == c) latch_error(a.hdr, CX_E_KIND, v);
     }
+    if (nc == 0) hgt[v] = 0;
+    if (tree_like) pending[v] = nc;
   }
-  lsync<MULTI>(a.bar, epoch);
+  grid_sync(a.bar, G, epoch);
+  lin_mark(a, 9);
 
-  // ---- P2: kind rule (in-degree <= 1 unless DAG), leaves at height 0 -----
-  {
-    int local = 0;
-    for (int v = tid; v < n; v += nthr) {
-      if (a.kind != CX_DAG && ld_dyn<MULTI>(&indeg[v]) > 1) latch_error(a.hdr, CX_E_KIND, v);
-      if (ch[v] == -1) {
-        hgt[v] = 0;
-        local++;
-      }
-    }
-    if (local) atomicAdd(&s_count, local);
-    __syncthreads();
-    if (threadIdx.x == 0 && s_count) atomicAdd(fin_ptr, s_count);
-    if (threadIdx.x == 0) s_count = 0;
-  }
-  lsync<MULTI>(a.bar, epoch);
+  // ---- P2: kind rule (in-degree <= 1 unless DAG) -----------------------------
+  if (tree_like)
+    for (int v = tid; v < n; v += nthr)
+      if (__ldcg(&indeg[v]) > 1) latch_error(a.hdr, CX_E_KIND, v);
+  grid_sync(a.bar, G, epoch);
   bool failed = __ldcg(reinterpret_cast<const unsigned long long *>(&a.hdr->err_key)) != kNoError;
 
-  // ---- P3 (a2): heights, one Jacobi round per level ----------------------
+  // ---- P3 (a2): heights ----------------------------------------------------
   int L = 0;
   if (!failed && n > 0) {
-    int fin_prev = ld_dyn<MULTI>(fin_ptr);
-    int r = 0;
-    while (fin_prev < n) {
-      r++;
-      int *round_ptr = MULTI ? &a.misc[r % 3] : &s_fin;
-      int local = 0;
+    if (tree_like) {
+      int hmax = 0;
       for (int v = tid; v < n; v += nthr) {
-        if (ld_dyn<MULTI>(&hgt[v]) >= 0) continue;
-        bool ok = true;
-        for (int k = 0; k < maxc; k++) {
-          int c = ch[k * n + v];
-          if (c == -1) break;
-          int hc = ld_dyn<MULTI>(&hgt[c]);
-          if (hc < 0 || hc >= r) {
-            ok = false;
-            break;
+        if (ch[v] != -1) continue;  // walks start at leaves (an immutable test)
+        int cur = v, hc = 0;
+        while (true) {
+          const int p = __ldcg(&parent[cur]);
+          if (p < 0) break;
+          atomicMax(&hgt[p], hc + 1);
+          __threadfence();
+          if (atomicSub(&pending[p], 1) != 1) break;
+          __threadfence();
+          cur = p;
+          hc = atomicAdd(&hgt[p], 0);  // every child's atomicMax precedes its decrement
+        }
+        hmax = max(hmax, hc);
+      }
+      for (int o = 16; o; o >>= 1) hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+      if (lane == 0) atomicMax(&a.misc[4], hmax);
+      grid_sync(a.bar, G, epoch);
+      bool unfinished = false;  // on a cycle: some child never becomes final
+      for (int v = tid; v < n; v += nthr)
+        if (__ldcg(&pending[v]) > 0) {
+          latch_error(a.hdr, CX_E_CYCLE, v);
+          unfinished = true;
+        }
+      if (__syncthreads_or(unfinished) && threadIdx.x == 0) atomicAdd(&a.misc[3], 1);
+      grid_sync(a.bar, G, epoch);
+      failed = __ldcg(&a.misc[3]) != 0;
+      L = __ldcg(&a.misc[4]) + 1;
+    } else {
+      // finished-node counts: misc[3] = leaves; round r adds into misc[r % 3],
+      // read by every CTA right after barrier r and cleared only after r + 1
+      {
+        int local = 0;
+        for (int v = tid; v < n; v += nthr) local += ch[v] == -1;
+        for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+        if (lane == 0 && local) atomicAdd(&a.misc[3], local);
+      }
+      grid_sync(a.bar, G, epoch);
+      int fin_prev = __ldcg(&a.misc[3]);
+      int r = 0;
+      while (fin_prev < n) {
+        r++;
+        int *round_ptr = &a.misc[r % 3];
+        int local = 0;
+        for (int v = tid; v < n; v += nthr) {
+          if (__ldcg(&hgt[v]) >= 0) continue;
+          bool ok = true;
+          for (int k = 0; k < maxc; k++) {
+            int c = ch[k * n + v];
+            if (c == -1) break;
+            int hc = __ldcg(&hgt[c]);
+            if (hc < 0 || hc >= r) {
+              ok = false;
+              break;
+            }
+          }
+          if (ok) {
+            hgt[v] = r;
+            local++;
           }
         }
-        if (ok) {
-          hgt[v] = r;
-          local++;
-        }
-      }
-      if (local) atomicAdd(&s_count, local);
-      __syncthreads();
-      if (threadIdx.x == 0 && s_count) atomicAdd(round_ptr, s_count);
-      __syncthreads();
-      if (threadIdx.x == 0) s_count = 0;
-      lsync<MULTI>(a.bar, epoch);
-      int fin;
-      if constexpr (MULTI) {
-        fin = fin_prev + ld_dyn<MULTI>(round_ptr);
+        for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+        if (lane == 0 && local) atomicAdd(round_ptr, local);
+        grid_sync(a.bar, G, epoch);
+        const int fin = fin_prev + __ldcg(round_ptr);
         if (tid == 0) a.misc[(r + 2) % 3] = 0;  // read by all before this barrier
-      } else {
-        fin = ld_dyn<MULTI>(fin_ptr);
+        if (fin == fin_prev) {  // no progress: a cycle (CX_E_CYCLE, lowest unfinished id)
+          for (int v = tid; v < n; v += nthr)
+            if (__ldcg(&hgt[v]) < 0) latch_error(a.hdr, CX_E_CYCLE, v);
+          grid_sync(a.bar, G, epoch);
+          failed = true;
+          break;
+        }
+        fin_prev = fin;
       }
-      if (fin == fin_prev) {  // no progress: a cycle (CX_E_CYCLE, lowest unfinished id)
-        for (int v = tid; v < n; v += nthr)
-          if (ld_dyn<MULTI>(&hgt[v]) < 0) latch_error(a.hdr, CX_E_CYCLE, v);
-        lsync<MULTI>(a.bar, epoch);
-        failed = true;
-        break;
-      }
-      fin_prev = fin;
+      L = r + 1;
     }
-    L = r + 1;
   }
+  lin_mark(a, 10);
 
   if (!failed && n > 0) {
-    // ---- P4 (a3): per-(level, segment) counts + roots row -------------------
-    int seg = kSegMin, S = (n + seg - 1) / seg;
-    while ((long long)(L + 1) * S > a.budget) {
-      seg *= 2;
-      S = (n + seg - 1) / seg;
-    }
-    int *cnt = a.cnt;
-    if constexpr (!MULTI) {
-      if ((L + 1) * S <= kLinSmemCnt) cnt = smem + (maxc + 2) * n;
-    }
-    for (int e = tid; e < (L + 1) * S; e += nthr) cnt[e] = 0;
-    lsync<MULTI>(a.bar, epoch);
-
-    const int lane = threadIdx.x & 31;
-    const int gwarp = tid >> 5, nwarps = nthr >> 5;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int s = gwarp; s < S; s += nwarps) {
-      for (int base = s * seg; base < min(n, (s + 1) * seg); base += 32) {
-        int v = base + lane;
-        bool valid = v < n && v < (s + 1) * seg;
-        int hv = valid ? ld_dyn<MULTI>(&hgt[v]) : -1;
-        unsigned m = __match_any_sync(0xffffffffu, hv);
-        if (valid && (m & lt) == 0) cnt[hv * S + s] = ld_dyn<MULTI>(&cnt[hv * S + s]) + __popc(m);
-        unsigned rb = __ballot_sync(0xffffffffu, valid && ld_dyn<MULTI>(&indeg[v]) == 0);
-        if (lane == 0 && rb) cnt[L * S + s] = ld_dyn<MULTI>(&cnt[L * S + s]) + __popc(rb);
-        __syncwarp();
-      }
-    }
-    lsync<MULTI>(a.bar, epoch);
-
-    // ---- P5: scan (block 0): levels root-most first, then the roots row ---
-    if (blockIdx.x == 0) {
-      const int E = L * S;
-      const int per = (E + blockDim.x - 1) / blockDim.x;
-      const int e0 = threadIdx.x * per, e1 = min(E, e0 + per);
-      // entry e <-> (level L-1-e/S, segment e%S)
-      int sum = 0;
-      for (int e = e0; e < e1; e++) sum += ld_dyn<MULTI>(&cnt[(L - 1 - e / S) * S + e % S]);
-      int total;
-      int off = block_exclusive_scan(sum, total, s_tmp);
-      for (int e = e0; e < e1; e++) {
-        int idx = (L - 1 - e / S) * S + e % S;
-        int c = ld_dyn<MULTI>(&cnt[idx]);
-        cnt[idx] = off;
-        if (e % S == 0) a.lbeg[L - 1 - e / S] = off;
-        off += c;
-      }
-      // roots row
-      const int per2 = (S + blockDim.x - 1) / blockDim.x;
-      const int r0 = threadIdx.x * per2, r1 = min(S, r0 + per2);
-      int rs = 0;
-      for (int e = r0; e < r1; e++) rs += ld_dyn<MULTI>(&cnt[L * S + e]);
-      int rtotal;
-      int roff = block_exclusive_scan(rs, rtotal, s_tmp);
-      for (int e = r0; e < r1; e++) {
-        int c = ld_dyn<MULTI>(&cnt[L * S + e]);
-        cnt[L * S + e] = roff;
-        roff += c;
+    const bool chunked = L + 1 <= kLinTabLevels && (long long)(L + 1) * G <= a.budget - n;
+    if (chunked) {
+      // ---- P4 (a3): per-block level counts -> tab[l * G + b] ---------------
+      int *cnt_s = lsm;                       // [L + 1]
+      int *off_s = lsm + kLinTabLevels;       // [L + 1]
+      int *wcnt = lsm + 2 * kLinTabLevels;    // [32][L + 1]
+      const int C = (n + G - 1) / G;
+      const int v0 = blockIdx.x * C, v1 = min(n, v0 + C);
+      for (int l = threadIdx.x; l <= L; l += blockDim.x) cnt_s[l] = 0;
+      __syncthreads();
+      for (int base = v0; base < v1; base += blockDim.x) {
+        const int v = base + threadIdx.x;
+        const bool valid = v < v1;
+        const int hv = valid ? __ldcg(&hgt[v]) : -1;
+        const unsigned m = __match_any_sync(0xffffffffu, hv);
+        if (valid && (m & lt) == 0) atomicAdd(&cnt_s[hv], __popc(m));
+        const unsigned rb = __ballot_sync(0xffffffffu, valid && __ldcg(&indeg[v]) == 0);
+        if (lane == 0 && rb) atomicAdd(&cnt_s[L], __popc(rb));
       }
       __syncthreads();
-      // level sizes and header
-      int mx = 0;
-      for (int l = threadIdx.x; l < L; l += blockDim.x) {
-        int b = ld_dyn<MULTI>(&a.lbeg[l]);
-        int e = l > 0 ? ld_dyn<MULTI>(&a.lbeg[l - 1]) : n;
-        a.lsize[l] = e - b;
-        mx = max(mx, e - b);
-      }
-      for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0) atomicMax(&s_tmp[32], mx);
-      if (threadIdx.x == 0) {
-        a.hdr->num_levels = L;
-        a.hdr->num_roots = rtotal;
+      for (int l = threadIdx.x; l <= L; l += blockDim.x) tab[l * G + blockIdx.x] = cnt_s[l];
+      grid_sync(a.bar, G, epoch);
+      lin_mark(a, 11);
+
+      // ---- P5: level totals, level begins, this block's offsets --------------
+      // warp w reduces the rows l = w, w + 32, ...: total over all blocks and
+      // the prefix over blocks < b
+      for (int l = wib; l <= L; l += blockDim.x >> 5) {
+        int tot = 0, pre = 0;
+        for (int b = lane; b < G; b += 32) {
+          const int x = __ldcg(&tab[l * G + b]);
+          tot += x;
+          if (b < (int)blockIdx.x) pre += x;
+        }
+        for (int o = 16; o; o >>= 1) {
+          tot += __shfl_xor_sync(0xffffffffu, tot, o);
+          pre += __shfl_xor_sync(0xffffffffu, pre, o);
+        }
+        if (lane == 0) {
+          cnt_s[l] = tot;  // level size (row L: number of roots)
+          off_s[l] = pre;
+        }
       }
       __syncthreads();
-      (void)total;
-    }
-    lsync<MULTI>(a.bar, epoch);
+      if (wib == 0) {  // level begins: exclusive scan from level L-1 down
+        int acc = 0, mx = 0;
+        for (int b = 0; b < L; b += 32) {
+          const int l = L - 1 - (b + lane);
+          const int x = l >= 0 ? cnt_s[l] : 0;
+          int incl = x;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          if (l >= 0) {
+            off_s[l] += acc + incl - x;
+            if (blockIdx.x == 0) {
+              a.lbeg[l] = acc + incl - x;
+              a.lsize[l] = x;
+            }
+            mx = max(mx, x);
+          }
+          acc += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) s_tmp[32] = mx;
+        if (blockIdx.x == 0 && lane == 0) {
+          a.hdr->num_levels = L;
+          a.hdr->num_roots = cnt_s[L];
+        }
+      }
+      __syncthreads();
+      lin_mark(a, 12);
 
-    // ---- P6 (a4): stable scatter ------------------------------------------
-    for (int s = gwarp; s < S; s += nwarps) {
-      for (int base = s * seg; base < min(n, (s + 1) * seg); base += 32) {
-        int v = base + lane;
-        bool valid = v < n && v < (s + 1) * seg;
-        int hv = valid ? ld_dyn<MULTI>(&hgt[v]) : -1;
-        unsigned m = __match_any_sync(0xffffffffu, hv);
-        int leader = __ffs(m) - 1;
-        int b = 0;
-        if (valid && lane == leader) b = ld_dyn<MULTI>(&cnt[hv * S + s]);
-        b = __shfl_sync(0xffffffffu, b, leader);
-        int nid = b + __popc(m & lt);
-        if (valid && lane == leader) cnt[hv * S + s] = b + __popc(m);
-        bool isroot = valid && ld_dyn<MULTI>(&indeg[v]) == 0;
-        unsigned rb = __ballot_sync(0xffffffffu, isroot);
-        int rbase = 0;
-        if (lane == 0 && rb) rbase = ld_dyn<MULTI>(&cnt[L * S + s]);
-        rbase = __shfl_sync(0xffffffffu, rbase, 0);
+      // ---- P6 (a4): stable scatter of this block's ids -----------------------
+      const int nw = blockDim.x >> 5;
+      for (int base = v0; base < v1; base += blockDim.x) {
+        for (int e = threadIdx.x; e < nw * (L + 1); e += blockDim.x) wcnt[e] = 0;
+        __syncthreads();
+        const int v = base + threadIdx.x;
+        const bool valid = v < v1;
+        const int hv = valid ? __ldcg(&hgt[v]) : -1;
+        const unsigned m = __match_any_sync(0xffffffffu, hv);
+        const bool isroot = valid && __ldcg(&indeg[v]) == 0;
+        const unsigned rb = __ballot_sync(0xffffffffu, isroot);
+        if (valid && (m & lt) == 0) wcnt[wib * (L + 1) + hv] = __popc(m);
+        if (lane == 0) wcnt[wib * (L + 1) + L] = __popc(rb);
+        __syncthreads();
+        int nid = 0, rpos = 0;
+        if (valid) {
+          int pre = 0;
+          for (int w = 0; w < wib; w++) pre += wcnt[w * (L + 1) + hv];
+          nid = off_s[hv] + pre + __popc(m & lt);
+        }
+        if (isroot) {
+          int pre = 0;
+          for (int w = 0; w < wib; w++) pre += wcnt[w * (L + 1) + L];
+          rpos = off_s[L] + pre + __popc(rb & lt);
+        }
+        __syncthreads();
+        for (int l = threadIdx.x; l <= L; l += blockDim.x) {  // advance the running offsets
+          int s = 0;
+          for (int w = 0; w < nw; w++) s += wcnt[w * (L + 1) + l];
+          off_s[l] += s;
+        }
         if (valid) {
           a.perm[nid] = v;
           a.inv[v] = nid;
           a.hnew[nid] = hv;
           if (isroot) {
-            a.roots[rbase + __popc(rb & lt)] = nid;
-            a.sid[nid] = rbase + __popc(rb & lt);
+            a.roots[rpos] = nid;
+            a.sid[nid] = rpos;
           }
         }
-        if (lane == 0 && rb) cnt[L * S + s] = rbase + __popc(rb);
-        __syncwarp();
+        __syncthreads();
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(&a.misc[5], s_tmp[32]);
+    } else {
+      // ---- P4-P6, very deep structures: per-segment counts and scatter -------
+      int seg = kSegMin, S = (n + seg - 1) / seg;
+      while ((long long)(L + 1) * S > a.budget - n) {
+        seg *= 2;
+        S = (n + seg - 1) / seg;
+      }
+      int *cnt = tab;
+      for (int e = tid; e < (L + 1) * S; e += nthr) cnt[e] = 0;
+      grid_sync(a.bar, G, epoch);
+      const int gwarp = tid >> 5, nwarps = nthr >> 5;
+      for (int s = gwarp; s < S; s += nwarps) {
+        for (int base = s * seg; base < min(n, (s + 1) * seg); base += 32) {
+          int v = base + lane;
+          bool valid = v < n && v < (s + 1) * seg;
+          int hv = valid ? __ldcg(&hgt[v]) : -1;
+          unsigned m = __match_any_sync(0xffffffffu, hv);
+          if (valid && (m & lt) == 0) cnt[hv * S + s] = __ldcg(&cnt[hv * S + s]) + __popc(m);
+          unsigned rb = __ballot_sync(0xffffffffu, valid && __ldcg(&indeg[v]) == 0);
+          if (lane == 0 && rb) cnt[L * S + s] = __ldcg(&cnt[L * S + s]) + __popc(rb);
+          __syncwarp();
+        }
+      }
+      grid_sync(a.bar, G, epoch);
+      if (blockIdx.x == 0) {
+        const int E = L * S;
+        const int per = (E + blockDim.x - 1) / blockDim.x;
+        const int e0 = threadIdx.x * per, e1 = min(E, e0 + per);
+        int sum = 0;
+        for (int e = e0; e < e1; e++) sum += __ldcg(&cnt[(L - 1 - e / S) * S + e % S]);
+        int total;
+        int off = block_exclusive_scan(sum, total, s_tmp);
+        for (int e = e0; e < e1; e++) {
+          int idx = (L - 1 - e / S) * S + e % S;
+          int c = __ldcg(&cnt[idx]);
+          cnt[idx] = off;
+          if (e % S == 0) a.lbeg[L - 1 - e / S] = off;
+          off += c;
+        }
+        const int per2 = (S + blockDim.x - 1) / blockDim.x;
+        const int r0 = threadIdx.x * per2, r1 = min(S, r0 + per2);
+        int rs = 0;
+        for (int e = r0; e < r1; e++) rs += __ldcg(&cnt[L * S + e]);
+        int rtotal;
+        int roff = block_exclusive_scan(rs, rtotal, s_tmp);
+        for (int e = r0; e < r1; e++) {
+          int c = __ldcg(&cnt[L * S + e]);
+          cnt[L * S + e] = roff;
+          roff += c;
+        }
+        __syncthreads();
+        int mx = 0;
+        for (int l = threadIdx.x; l < L; l += blockDim.x) {
+          int b = __ldcg(&a.lbeg[l]);
+          int e = l > 0 ? __ldcg(&a.lbeg[l - 1]) : n;
+          a.lsize[l] = e - b;
+          mx = max(mx, e - b);
+        }
+        for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) atomicMax(&a.misc[5], mx);
+        if (threadIdx.x == 0) {
+          a.hdr->num_levels = L;
+          a.hdr->num_roots = rtotal;
+        }
+        (void)total;
+      }
+      grid_sync(a.bar, G, epoch);
+      for (int s = gwarp; s < S; s += nwarps) {
+        for (int base = s * seg; base < min(n, (s + 1) * seg); base += 32) {
+          int v = base + lane;
+          bool valid = v < n && v < (s + 1) * seg;
+          int hv = valid ? __ldcg(&hgt[v]) : -1;
+          unsigned m = __match_any_sync(0xffffffffu, hv);
+          int leader = __ffs(m) - 1;
+          int b = 0;
+          if (valid && lane == leader) b = __ldcg(&cnt[hv * S + s]);
+          b = __shfl_sync(0xffffffffu, b, leader);
+          int nid = b + __popc(m & lt);
+          if (valid && lane == leader) cnt[hv * S + s] = b + __popc(m);
+          bool isroot = valid && __ldcg(&indeg[v]) == 0;
+          unsigned rb = __ballot_sync(0xffffffffu, isroot);
+          int rbase = 0;
+          if (lane == 0 && rb) rbase = __ldcg(&cnt[L * S + s]);
+          rbase = __shfl_sync(0xffffffffu, rbase, 0);
+          if (valid) {
+            a.perm[nid] = v;
+            a.inv[v] = nid;
+            a.hnew[nid] = hv;
+            if (isroot) {
+              a.roots[rbase + __popc(rb & lt)] = nid;
+              a.sid[nid] = rbase + __popc(rb & lt);
+            }
+          }
+          if (lane == 0 && rb) cnt[L * S + s] = rbase + __popc(rb);
+          __syncwarp();
+        }
       }
     }
-    lsync<MULTI>(a.bar, epoch);
+    grid_sync(a.bar, G, epoch);
+    lin_mark(a, 13);
 
-    // ---- P7 (a5): remap children to new ids --------------------------------
+    // ---- P7 (a5): remap children to new ids ------------------------------------
     for (int i = tid; i < n; i += nthr) {
-      int v = ld_dyn<MULTI>(&a.perm[i]);
+      const int v = __ldcg(&a.perm[i]);
       for (int k = 0; k < maxc; k++) {
-        int c = ch[k * n + v];
-        a.chn[(long long)k * n + i] = c == -1 ? -1 : ld_dyn<MULTI>(&a.inv[c]);
+        const int c = ch[k * n + v];
+        a.chn[(long long)k * n + i] = c == -1 ? -1 : __ldcg(&a.inv[c]);
       }
     }
-    // ---- P8 (a6): structures, root index propagated top-down ---------------
-    for (int l = L - 1; l >= 1; l--) {
-      lsync<MULTI>(a.bar, epoch);
-      const int b = ld_dyn<MULTI>(&a.lbeg[l]), e = b + ld_dyn<MULTI>(&a.lsize[l]);
-      for (int i = b + tid; i < e; i += nthr) {
-        const int si = ld_dyn<MULTI>(&a.sid[i]);
-        for (int k = 0; k < maxc; k++) {
-          int c = ld_dyn<MULTI>(&a.chn[(long long)k * n + i]);
-          if (c == -1) break;
-          atomicMin(&a.sid[c], si);
+    lin_mark(a, 14);
+    // ---- P8 (a6): structures ------------------------------------------------------
+    if (tree_like) {  // walk up to the root; roots already hold their index
+      for (int i = tid; i < n; i += nthr) {
+        int v = __ldcg(&a.perm[i]);
+        int p = __ldcg(&parent[v]);
+        if (p < 0) continue;
+        while (p >= 0) {
+          v = p;
+          p = __ldcg(&parent[v]);
+        }
+        a.sid[i] = __ldcg(&a.sid[__ldcg(&a.inv[v])]);
+      }
+    } else {  // smallest root index reaching the node, propagated top-down
+      for (int l = L - 1; l >= 1; l--) {
+        grid_sync(a.bar, G, epoch);
+        const int b = __ldcg(&a.lbeg[l]), e = b + __ldcg(&a.lsize[l]);
+        for (int i = b + tid; i < e; i += nthr) {
+          const int si = __ldcg(&a.sid[i]);
+          for (int k = 0; k < maxc; k++) {
+            int c = __ldcg(&a.chn[(long long)k * n + i]);
+            if (c == -1) break;
+            atomicMin(&a.sid[c], si);
+          }
         }
       }
     }
   }
 
-  // ---- finalize header (block 0 thread 0) ------------------------------
-  if (blockIdx.x == 0) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long key =
-          __ldcg(reinterpret_cast<const unsigned long long *>(&a.hdr->err_key));
-      a.hdr->num_nodes = n;
-      if (key != kNoError) {
-        a.hdr->status = (int)(key >> 32);
-        a.hdr->bad_node = (int)(key & 0xffffffffu);
+  // ---- finalize header (block 0 thread 0, after every block is done) -------
+  grid_sync(a.bar, G, epoch);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    lin_mark(a, 15);
+    unsigned long long key = __ldcg(reinterpret_cast<const unsigned long long *>(&a.hdr->err_key));
+    a.hdr->num_nodes = n;
+    if (key != kNoError) {
+      a.hdr->status = (int)(key >> 32);
+      a.hdr->bad_node = (int)(key & 0xffffffffu);
+      a.hdr->num_levels = 0;
+    } else {
+      a.hdr->status = CX_OK;
+      a.hdr->bad_node = -1;
+      if (n == 0) {
         a.hdr->num_levels = 0;
+        a.hdr->num_roots = 0;
+        a.hdr->num_leaves = 0;
+        a.hdr->first_leaf = 0;
+        a.hdr->max_level_size = 0;
       } else {
-        a.hdr->status = CX_OK;
-        a.hdr->bad_node = -1;
-        if (n == 0) {
-          a.hdr->num_levels = 0;
-          a.hdr->num_roots = 0;
-          a.hdr->num_leaves = 0;
-          a.hdr->first_leaf = 0;
-          a.hdr->max_level_size = 0;
-        } else {
-          int nl = ld_dyn<MULTI>(&a.lsize[0]);
-          a.hdr->num_leaves = nl;
-          a.hdr->first_leaf = n - nl;
-          a.hdr->max_level_size = s_tmp[32];
-        }
+        int nl = __ldcg(&a.lsize[0]);
+        a.hdr->num_leaves = nl;
+        a.hdr->first_leaf = n - nl;
+        a.hdr->max_level_size = __ldcg(&a.misc[5]);
       }
     }
   }
-  if constexpr (MULTI) grid_exit(a.bar, gridDim.x);
+  grid_exit(a.bar, G);
 }
-
 
 __device__ __noinline__ void lin_latch(unsigned long long *err, int code, int v) {
   atomicMin(err, ((unsigned long long)(unsigned)code << 32) | (unsigned)v);
@@ -390,6 +535,7 @@ __device__ __noinline__ void lin_latch(unsigned long long *err, int code, int v)
 // smem (ints): ch[maxc*n] | hgt[n] | indeg[n] | perm[n] | inv[n] | lb[n] | cnt[kLinSmemCnt]
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kLinSingleThreads, 1) lin_single_kernel(LinArgs a) {
+  griddep_launch_dependents();  // the forward may stage its weights meanwhile
   extern __shared__ int sm[];
   __shared__ unsigned long long s_err;
   __shared__ int s_tmp[33];
@@ -742,7 +888,8 @@ cudaError_t launch_linearize(const LinArgs &a, int num_sms, cudaStream_t stream)
     cudaFuncSetAttribute(lin_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kLinSmemMax);
     cudaFuncSetAttribute(lin_single_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(lin_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(lin_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLinMultiSmem);
     attr_done = true;
   }
   if (lin_use_single(a.n, a.maxc)) {
@@ -756,14 +903,14 @@ cudaError_t launch_linearize(const LinArgs &a, int num_sms, cudaStream_t stream)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_sms);
   cfg.blockDim = dim3(kLinThreads);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = kLinMultiSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelExC(&cfg, (const void *)lin_kernel<true>, params);
+  return cudaLaunchKernelExC(&cfg, (const void *)lin_kernel, params);
 }
 
 }  // namespace cx

@@ -73,7 +73,7 @@ if __name__ == "__main__":
   for ctas, thr, coop in ((1, 32, 0), (1, 1024, 0), (144, 512, 0), (144, 512, 1), (148, 1024, 1)):
       us = timeit(lambda: L.cx_debug_empty(ctas, thr, coop, None, st()))
       print(f"empty kernel ctas={ctas:3d} threads={thr:4d} coop={coop}: {us:6.2f} us")
-  buf = torch.zeros(16, dtype=torch.int64, device=dev)
+  buf = torch.zeros(32, dtype=torch.int64, device=dev)
   for name, ch, kind in (("N=1", np.full((2, 1), -1, np.int32), synth.TREE),
                          ("b10", w["children"], w["kind"])):
       chd = t(ch, np.int32)
