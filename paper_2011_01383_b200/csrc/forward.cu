@@ -27,6 +27,8 @@
 // tensor cores for this path; the bf16 tensor-core path is separate).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "fwd_common.cuh"
 #include "fwd_kernels.cuh"
@@ -803,6 +805,19 @@ size_t fwd_workspace_bytes(int cell, int H, int n) {
   return b + 1024;
 }
 
+// Programmatic dependent launch of cx_forward behind cx_linearize is opt-in
+// (CX_PDL=1): measured on B200 it saves ~2 us eagerly and nothing under CUDA
+// graph replay, and an early-resident cooperative forward slowed the fp32
+// DAG-RNN b4096 step from 10.1 to 15.7 ms. The kernels are written for it
+// either way (weights staged before griddepcontrol.wait).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("CX_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // Cooperative launch through cudaLaunchKernelEx so it can be captured into a
 // CUDA graph (the bench replays linearize + forward as one graph).
 cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream) {
@@ -827,7 +842,7 @@ cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream) 
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelExC(&cfg, plan.kernel, params);
 }
 

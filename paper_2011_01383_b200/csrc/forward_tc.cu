@@ -751,7 +751,7 @@ cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &f, cudaStream_t stream
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap cx_linearize
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelExC(&cfg, plan.kernel, params);
 }
 

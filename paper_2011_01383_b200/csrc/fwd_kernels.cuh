@@ -71,5 +71,6 @@ int tc_xmode(int n, int V);
 size_t tc_workspace_bytes(int cell, int H, int V, int n);
 cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &args, cudaStream_t stream);
 cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream);
+bool pdl_enabled();
 
 }  // namespace cx
