@@ -44,6 +44,11 @@ WORKLOADS = {
     "cfg5_dagrnn_b10": ("grid", synth.DAGRNN, 256, 20000, 10, "weak"),
     "cfg5_dagrnn_b1": ("grid", synth.DAGRNN, 256, 20000, 1, "weak"),
     "cfg1_treernn": ("perfect3", synth.TREERNN, 8, 100, 1, "weak"),
+    # GRNN-comparison sequences (length 100, H = 256)
+    "f4_lstm_seq100_b10": ("chain100", synth.TREELSTM, 256, 20000, 10, "weak"),
+    "f4_lstm_seq100_b1": ("chain100", synth.TREELSTM, 256, 20000, 1, "weak"),
+    "f4_gru_seq100_b10": ("chain100", synth.TREEGRU, 256, 20000, 10, "weak"),
+    "f4_gru_seq100_b1": ("chain100", synth.TREEGRU, 256, 20000, 1, "weak"),
     # strong scaling: the batch is split across ranks
     "cfg5_treelstm_b4096": ("sst", synth.TREELSTM, 256, 20000, 4096, "strong"),
     "cfg5_dagrnn_b4096": ("grid", synth.DAGRNN, 256, 20000, 4096, "strong"),
@@ -62,9 +67,11 @@ def make_inputs(name, rank, world, seed=0):
         ch, off = synth.perfect_forest(total, 7)
     elif gen == "perfect3":
         ch, off = synth.perfect_forest(total, 3)
+    elif gen == "chain100":
+        ch, off = synth.chains(total, 100)
     else:
         ch, off = synth.grid_dags(total)
-    kind = synth.DAG if gen == "grid" else synth.TREE
+    kind = synth.DAG if gen == "grid" else synth.SEQUENCE if gen == "chain100" else synth.TREE
     # this rank's contiguous block of structures, ids rebased to 0 (shard.py)
     from paper_2011_01383_b200 import shard
     words_all = synth.word_ids(ch, V, seed, all_nodes=(cell == synth.DAGRNN))
@@ -208,6 +215,66 @@ def cpu_baseline(name, seconds=12.0):
             break
     return {"value": done * cap / el, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{done} x {cap} structures of {name} in {el:.1f}s (fp64 naive recursion, 1 thread)"}
+
+
+# ---------------------------------------------------------------------------
+# secondary: batch-4096 throughput (SURVEY §8(d) "headline trees/s = cfg5b")
+# ---------------------------------------------------------------------------
+def throughput_b4096(dtype_name, rank, world, local_rank, steps=30, warmup=5):
+    """cx_linearize + cx_forward over this rank's block of the 4096 SST trees
+    (strong scaling), CUDA-graph replayed, L2 flushed between steps, events on
+    the launch stream; trees/s = 4096 / max-over-ranks mean step time."""
+    import torch
+    import torch.distributed as dist
+    import paper_2011_01383_b200 as cx
+    name = "cfg5_treelstm_b4096"
+    dev = torch.device("cuda", local_rank)
+    inp = make_inputs(name, rank, world)
+    cell, H = inp["cell"], inp["H"]
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a, dtype=dt)).to(dev)
+    children, words = t(inp["children"], np.int32), t(inp["words"], np.int32)
+    emb = t(inp["emb"], np.float32)
+    weights = [t(w, np.float32) for w in inp["weights"]]
+    n = inp["children"].shape[1]
+    dtype = cx.BF16 if dtype_name == "bf16" else cx.F32
+    lin = cx.alloc_linearization(n, inp["children"].shape[0], inp["kind"], dev)
+    h = torch.empty(n, H, dtype=torch.float32, device=dev)
+    roots = torch.empty(inp["batch"], H, dtype=torch.float32, device=dev)
+
+    def step():
+        cx.linearize(children, inp["kind"], out=lin)
+        cx.forward(cell, H, weights, emb, words, lin, dtype=dtype, h_out=h, root_out=roots)
+
+    step()
+    cx.check(lin)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        g.replay()
+        flush.fill_(1.0)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for a0, a1 in evs:
+        a0.record(stream)
+        g.replay()
+        a1.record(stream)
+        flush.fill_(1.0)
+    torch.cuda.synchronize()
+    total = sum(a0.elapsed_time(a1) for a0, a1 in evs)
+    if world > 1:
+        tt = torch.tensor([total], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total = float(tt.item())
+    ms = total / steps
+    return {"workload": name, "dtype": dtype_name, "trees_per_s": inp["total"] / (ms / 1e3),
+            "ms_per_step": ms, "trees": inp["total"], "trees_per_gpu": inp["batch"],
+            "scaling": "strong", "timing": "graph replay of linearize+forward, max over ranks"}
 
 
 # ---------------------------------------------------------------------------
@@ -383,6 +450,10 @@ def run_gpu(args, rank, world, local_rank):
     h2d = ch_host.numel() * 4 + w_host.numel() * 4
     d2h = roots_host.numel() * 4
 
+    secondary = None
+    if args.secondary and name == "cfg2_treelstm_b10":
+        secondary = [throughput_b4096(dt, rank, world, local_rank) for dt in ("bf16", "f32")]
+
     if rank != 0:
         return
     fwd_mean = sum(fwd_ms) / len(fwd_ms)
@@ -439,6 +510,8 @@ def run_gpu(args, rank, world, local_rank):
                 "d2h_bytes_per_step": d2h},
         "clocks": clocks,
     }
+    if secondary:
+        line["throughput_b4096"] = secondary
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(name)
     print(json.dumps(line), flush=True)
@@ -452,6 +525,8 @@ def main():
     p.add_argument("--workload", default="cfg2_treelstm_b10", choices=sorted(WORKLOADS))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-secondary", dest="secondary", action="store_false",
+                   help="skip the batch-4096 throughput lines (bf16, f32) of the default run")
     p.add_argument("--dtype", default="f32", choices=["f32", "bf16"],
                    help="compute precision of cx_forward (bf16 = tcgen05 tensor-core path)")
     p.add_argument("--allgather", action="store_true",

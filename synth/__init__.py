@@ -309,6 +309,12 @@ def workload(name: str, seed: int = 0):
         "cfg5_dagrnn_b10": dict(cell=DAGRNN, hidden=256, vocab=20000, shape=("grid", 10)),
         "cfg5_dagrnn_b4096": dict(cell=DAGRNN, hidden=256, vocab=20000, shape=("grid", 4096)),
         "cfg5_treelstm_b4096": dict(cell=TREELSTM, hidden=256, vocab=20000, shape=("sst", 4096)),
+        # sequence workloads of the GRNN comparison (P:1535-1553,
+        # "sequence length 100 and hidden and input sizes 256"): chains, kind sequence
+        "f4_lstm_seq100_b1": dict(cell=TREELSTM, hidden=256, vocab=20000, shape=("chain", 1, 100)),
+        "f4_lstm_seq100_b10": dict(cell=TREELSTM, hidden=256, vocab=20000, shape=("chain", 10, 100)),
+        "f4_gru_seq100_b1": dict(cell=TREEGRU, hidden=256, vocab=20000, shape=("chain", 1, 100)),
+        "f4_gru_seq100_b10": dict(cell=TREEGRU, hidden=256, vocab=20000, shape=("chain", 10, 100)),
     }[name]
     shape = spec["shape"]
     if shape[0] == "sst":
@@ -320,6 +326,9 @@ def workload(name: str, seed: int = 0):
     elif shape[0] == "grid":
         ch, off = grid_dags(shape[1])
         kind = DAG
+    elif shape[0] == "chain":
+        ch, off = chains(shape[1], shape[2])
+        kind = SEQUENCE
     else:
         raise ValueError(shape)
     cell = spec["cell"]

@@ -101,7 +101,8 @@ def test_sequences(cx, cell):
 @pytest.mark.parametrize("name", ["cfg1_treernn", "cfg2_treelstm_b10", "cfg2_treelstm_b1",
                                   "cfg3_treegru_b1", "cfg3_treegru_b10", "cfg3_treefc_b1",
                                   "cfg3_treefc_b10", "cfg4_mvrnn_b10", "cfg5_dagrnn_b1",
-                                  "cfg5_dagrnn_b10"])
+                                  "cfg5_dagrnn_b10", "f4_lstm_seq100_b1", "f4_lstm_seq100_b10",
+                                  "f4_gru_seq100_b1", "f4_gru_seq100_b10"])
 def test_baseline_configs(cx, name, path):
     w = synth.workload(name)
     _parity(w["cell"], w["hidden"], w["vocab"], w["children"], w["kind"], seed=w["seed"],

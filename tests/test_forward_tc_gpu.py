@@ -93,7 +93,8 @@ def test_child_sum_arity_1_and_2(cx, cell):
 
 
 @pytest.mark.parametrize("name", ["cfg2_treelstm_b10", "cfg2_treelstm_b1", "cfg3_treefc_b1",
-                                  "cfg3_treefc_b10", "cfg5_dagrnn_b1", "cfg5_dagrnn_b10"])
+                                  "cfg3_treefc_b10", "cfg5_dagrnn_b1", "cfg5_dagrnn_b10",
+                                  "f4_lstm_seq100_b10"])
 def test_baseline_configs(cx, name):
     w = synth.workload(name)
     _parity(cx, w["cell"], w["hidden"], w["vocab"], w["children"], w["kind"], seed=w["seed"])
