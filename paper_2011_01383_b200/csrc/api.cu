@@ -179,17 +179,25 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
   a.h_out = h_out;
   a.aux_out = aux_out;
   a.root_out = root_out;
-  if (m->dtype == CX_BF16) {  // hb, cs, xb (forward_tc.cu)
+  if (m->dtype == CX_BF16) {  // hb, cs, xb [, hf, crow] (forward_tc.cu)
+    const size_t R = cx::tc_state_rows(m->cell, n, m->vocab);
     char *q = reinterpret_cast<char *>(buf);
     a.hb = reinterpret_cast<unsigned short *>(q);
-    q = align_up(q + 2 * N * H, 256);
+    q = align_up(q + 2 * R * H, 256);
     if (m->cell == CX_TREELSTM) {
       a.cs = reinterpret_cast<float *>(q);
-      q = align_up(q + 4 * N * H, 256);
+      q = align_up(q + 4 * R * H, 256);
     }
     a.xb = reinterpret_cast<unsigned short *>(q);
     a.xmode = cx::tc_xmode(n, m->vocab);
+    q = align_up(q + 2 * (a.xmode ? N : (size_t)m->vocab) * H, 256);
     a.cell_has_x = m->cell == CX_TREELSTM || m->cell == CX_DAGRNN;
+    a.hoist = cx::tc_hoist(m->cell, n, m->vocab) ? 1 : 0;
+    if (a.hoist) {
+      a.hf = reinterpret_cast<float *>(q);
+      q = align_up(q + 4 * (size_t)m->vocab * H, 256);
+      a.crow = reinterpret_cast<int *>(q);
+    }
   } else if (plan.big) a.pbuf = buf;  // hs, st [n][H] + words [n] (forward_big.cu)
   else switch (m->cell) {
     case CX_TREELSTM: a.cbuf = aux_out ? aux_out : buf; break;

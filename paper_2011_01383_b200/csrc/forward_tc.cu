@@ -256,6 +256,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
   const int status0 = *reinterpret_cast<volatile int *>(&a.hdr->status);
   const int L = status0 == CX_OK ? a.hdr->num_levels : 0, first_leaf = a.hdr->first_leaf;
   const int xlo = C::DAG ? 0 : first_leaf;  // node-order x rows start here
+  const bool hoist = C::LSTM && a.hoist;
+  const int sbase = hoist ? a.V : 0;  // state row of internal node i = sbase + i
   // ---- phase 0: bf16 input rows ------------------------------------------------
   if (C::XSLOT && status0 == CX_OK) {
     const size_t total_threads = (size_t)gridDim.x * blockDim.x;
@@ -267,6 +269,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
       for (size_t idx = gt; idx < total; idx += total_threads) {
         const float4 *s = reinterpret_cast<const float4 *>(a.emb + idx * 8);
         *reinterpret_cast<uint4 *>(xw + idx * 8) = f32x8_to_bf16(__ldg(s), __ldg(s + 1));
+      }
+      if (hoist) {  // state row of every node: leaves -> their word's row
+        for (size_t i = gt; i < (size_t)n; i += total_threads) {
+          int row = a.V + (int)i;
+          if ((int)i >= first_leaf) {
+            const int own = __ldg(a.perm + i);
+            int w = __ldg(a.words + own);
+            if (w < 0 || w >= a.V) {
+              latch_error(a.hdr, CX_E_WORD_RANGE, own);
+              w = 0;
+            }
+            row = w;
+          }
+          a.crow[i] = row;
+        }
       }
     } else {  // this batch's x rows in node order (new ids [xlo, n))
       const size_t total = (size_t)(n - xlo) * q8;
@@ -297,10 +314,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     if (l > 0) grid_sync(a.bar, gridDim.x, epoch);
     tc_mark(a, 2 + 4 * l, 0);
     int lo, hi;
-    chunk_of(__ldg(a.lsize + l), a.Gn, gn, lo, hi);
-    const int lb = __ldg(a.lbeg + l);
-    lo += lb;
-    hi += lb;
+    if (leaf && hoist) {  // the leaf cell once per vocabulary word (rows [0, V))
+      chunk_of(a.V, a.Gn, gn, lo, hi);
+    } else {
+      chunk_of(__ldg(a.lsize + l), a.Gn, gn, lo, hi);
+      const int lb = __ldg(a.lbeg + l);
+      lo += lb;
+      hi += lb;
+    }
     if constexpr (C::FC) {
       if (leaf) {  // h = Emb[word]: this CTA's node chunk x unit slice
         constexpr int q4 = U / 4;
@@ -349,7 +370,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
           sv[q] = -1;
 #pragma unroll
           for (int k = 0; k < J; k++) ch[q][k] = -1;
-          if (r < cnt) {
+          if (r < cnt && !(leaf && hoist)) {
             own[q] = __ldg(a.perm + i);
             if (a.root_out) sv[q] = __ldg(a.sid + i);
             if (!leaf) {
@@ -364,7 +385,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
           int root = -1, xr = -1;
           if (r < cnt) {
             if (sv[q] >= 0) root = __ldg(a.roots + sv[q]) == i ? sv[q] : -1;
-            if (C::XSLOT && (leaf || C::DAG)) {
+            if (leaf && hoist) {
+              xr = i;  // word row
+            } else if (C::XSLOT && (leaf || C::DAG)) {
               if (a.xmode == 0) {
                 int w = __ldg(a.words + own[q]);
                 if (w < 0 || w >= a.V) {
@@ -384,6 +407,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
                 absent = absent || ch[q][k] < 0;
                 if (absent) ch[q][k] = -1;
                 nc += ch[q][k] >= 0;
+                if (ch[q][k] >= 0) ch[q][k] = hoist ? __ldcg(a.crow + ch[q][k]) : ch[q][k];  // state row
               }
               if (C::FC && nc != 2 && latch) latch_error(a.hdr, CX_E_ARITY, own[q]);
             }
@@ -563,12 +587,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
             for (int j = 0; j < 16; j++) h[j] = sigm_mufu(v[j] + bo[j]) * tanh_mufu(c[j]);
           }
           if (valid) {
-            const size_t uo = (size_t)own * H + unit0 + u0, ui = (size_t)i * H + unit0 + u0;
-            store_f32_stream<16>(a.h_out + uo, h);
+            const bool wordrow = leaf && hoist;  // hoisted leaf cell: row i = word i
+            const size_t ui = (size_t)(wordrow ? i : sbase + i) * H + unit0 + u0;
             store_bf16<16>(hb + ui, h);
             store_f32<16>(cs + ui, c);
-            if (a.aux_out) store_f32_stream<16>(a.aux_out + uo, c);
-            if (root >= 0) store_f32_stream<16>(a.root_out + (size_t)root * H + unit0 + u0, h);
+            if (wordrow) {
+              store_f32<16>(a.hf + (size_t)i * H + unit0 + u0, h);
+            } else {
+              const size_t uo = (size_t)own * H + unit0 + u0;
+              store_f32_stream<16>(a.h_out + uo, h);
+              if (a.aux_out) store_f32_stream<16>(a.aux_out + uo, c);
+              if (root >= 0) store_f32_stream<16>(a.root_out + (size_t)root * H + unit0 + u0, h);
+            }
           }
         } else {  // DAG-RNN / TreeFC: h = tanh(acc + b)
           constexpr int CW = UC < 32 ? UC : 32;
@@ -598,6 +628,63 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     }
     T0 += ntiles;
     Sg0 += (uint32_t)ntiles * KA * nsl;
+  }
+
+  // ---- hoisted leaves: outputs copied from the word table -------------------
+  // (the table was complete at the level-1 barrier; every CTA copies a share)
+  if (hoist && L > 0) {
+    // a single-level batch has had no barrier since the table epilogue
+    if (L == 1) grid_sync(a.bar, gridDim.x, epoch);
+    // each warp takes 32 leaves: their indices in one coalesced round trip,
+    // then rows copied with float4 lanes, 4 leaves in flight
+    constexpr int q4 = H / 4;
+    const int nleaf = n - first_leaf;
+    const int gw = (blockIdx.x * blockDim.x + tid) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int j0 = gw * 32; j0 < nleaf; j0 += nw * 32) {
+      const int jl = j0 + lane;
+      int own = -1, w = 0, r = -1;
+      if (jl < nleaf) {
+        const int j = first_leaf + jl;
+        own = __ldg(a.perm + j);
+        w = __ldcg(a.crow + j);
+        if (a.root_out) {  // a one-node structure: its leaf is a root
+          const int q = __ldg(a.sid + j);
+          r = __ldg(a.roots + q) == j ? q : -1;
+        }
+      }
+      const int cnt = min(32, nleaf - j0);
+      for (int k0 = 0; k0 < cnt; k0 += 4) {
+        float4 hv[4][q4 / 32];
+        int ok[4], ow[4], rk[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int k = min(k0 + u, cnt - 1);
+          ok[u] = k0 + u < cnt;
+          ow[u] = __shfl_sync(0xffffffffu, own, k);
+          rk[u] = __shfl_sync(0xffffffffu, r, k);
+          const int wk = __shfl_sync(0xffffffffu, w, k);
+          const float4 *hs = reinterpret_cast<const float4 *>(a.hf + (size_t)wk * H);
+#pragma unroll
+          for (int e = 0; e < q4 / 32; e++) hv[u][e] = __ldcg(hs + lane + 32 * e);
+          if (a.aux_out && ok[u]) {
+            const float4 *cv = reinterpret_cast<const float4 *>(cs + (size_t)wk * H);
+#pragma unroll
+            for (int e = 0; e < q4 / 32; e++)
+              __stcs(reinterpret_cast<float4 *>(a.aux_out + (size_t)ow[u] * H) + lane + 32 * e,
+                     __ldcg(cv + lane + 32 * e));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          if (!ok[u]) continue;
+#pragma unroll
+          for (int e = 0; e < q4 / 32; e++) {
+            __stcs(reinterpret_cast<float4 *>(a.h_out + (size_t)ow[u] * H) + lane + 32 * e, hv[u][e]);
+            if (rk[u] >= 0) reinterpret_cast<float4 *>(a.root_out + (size_t)rk[u] * H)[lane + 32 * e] = hv[u][e];
+          }
+        }
+      }
+    }
   }
 
   // ---- teardown -------------------------------------------------------------
@@ -732,7 +819,8 @@ cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &f, cudaStream_t stream
   std::memset(&ta, 0, sizeof ta);
   ta.f = f;
   const long long xrows = f.xmode ? f.n : f.V;
-  if (!encode_rows(&ta.tm_h, f.hb, f.H, f.n)) return cudaErrorInvalidValue;
+  const long long hrows = (long long)f.n + (f.hoist ? f.V : 0);
+  if (!encode_rows(&ta.tm_h, f.hb, f.H, hrows)) return cudaErrorInvalidValue;
   if (f.cell_has_x ? !encode_rows(&ta.tm_x, f.xb, f.H, xrows) : false) return cudaErrorInvalidValue;
   if (!f.cell_has_x) ta.tm_x = ta.tm_h;
   void *params[] = {&ta};
@@ -759,12 +847,27 @@ cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &f, cudaStream_t stream
 int tc_xmode(int n, int V) { return (size_t)n * 2 <= (size_t)V ? 1 : 0; }
 
 // workspace bytes of the tensor-core path (after the GridBar): hb, cs, xb
+// Computation hoisting of the TreeLSTM leaf cell (PAPER §4.3 P:1127-1132,
+// SURVEY §8(f) f1): a leaf's (h, c) depends only on its word, so when the batch
+// has more leaves' worth of x rows than V/2 (table mode) the leaf level is
+// evaluated once per vocabulary word and parents read leaf children from that
+// table.
+bool tc_hoist(int cell, int n, int V) { return cell == CX_TREELSTM && tc_xmode(n, V) == 0; }
+
+// State rows: hoisted TreeLSTM keeps the V word rows first, node i at row V + i.
+size_t tc_state_rows(int cell, int n, int V) {
+  return (size_t)(n > 0 ? n : 1) + (tc_hoist(cell, n, V) ? (size_t)V : 0);
+}
+
+// workspace bytes of the tensor-core path (after the GridBar); tc_carve() in
+// api.cu lays the buffers out in this order
 size_t tc_workspace_bytes(int cell, int H, int V, int n) {
-  const size_t N = (size_t)(n > 0 ? n : 1), h = (size_t)H;
-  size_t b = 2 * N * h + 256;                                   // hb
-  if (cell == CX_TREELSTM) b += 4 * N * h + 256;                // cs
+  const size_t N = (size_t)(n > 0 ? n : 1), h = (size_t)H, R = tc_state_rows(cell, n, V);
+  size_t b = 2 * R * h + 256;                                   // hb
+  if (cell == CX_TREELSTM) b += 4 * R * h + 256;                // cs
   if (cell == CX_TREELSTM || cell == CX_DAGRNN)                 // xb
     b += 2 * (tc_xmode(n, V) ? N : (size_t)V) * h + 256;
+  if (tc_hoist(cell, n, V)) b += 4 * (size_t)V * h + 4 * N + 512;  // hf, crow
   return b;
 }
 

@@ -32,6 +32,9 @@ struct FwdArgs {
   unsigned short *xb;  // bf16 input rows: [V][H] (xmode 0) or [n - xlo][H] node order (xmode 1)
   int xmode;
   int cell_has_x;      // the cell gathers input rows (TreeLSTM, DAG-RNN)
+  int hoist;           // TreeLSTM leaf cell evaluated per vocabulary word (tc_hoist)
+  float *hf;           // [V][H] fp32 h of every word (hoist)
+  int *crow;           // [n] state row of node i: its word if a leaf, else V + i (hoist)
   GridBar *bar;
   int Gn, Gu;   // node groups x unit groups = CTAs
   unsigned long long *trace;  // debug: %globaltimer per CTA and phase (cx_debug_set_trace)
@@ -70,6 +73,8 @@ bool tc_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int
 int tc_xmode(int n, int V);
 size_t tc_workspace_bytes(int cell, int H, int V, int n);
 cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &args, cudaStream_t stream);
+bool tc_hoist(int cell, int n, int V);
+size_t tc_state_rows(int cell, int n, int V);
 cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream);
 bool pdl_enabled();
 
