@@ -444,8 +444,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
             C::slot(leaf, s, src, bm, acc);
             const int st = Sg % S;
             const int kst = (int)(Sg - Sg0);
-            const int sslot = (l == 0 && kst >= 4 && kst < 12) ? 64 + 4 * (kst - 4)
-                              : (l == 1 && kst < 8) ? 96 + 4 * kst : 1 << 30;
+            const int sslot = (l == 1 && kst < 16) ? 64 + 4 * kst : 1 << 30;
             mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);  // free in every CTA of the cluster
             tc_mark(a, sslot + 0, kTmaWarp * 32);
             if (lane == 0) mbar_arrive_expect_tx(&bar_full[st], kStageBytes);
@@ -482,8 +481,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
               C::slot(leaf, s, src, bm, acc);
               const int st = Sg % S;
               const int kst = (int)(Sg - Sg0);
-              const int sslot = (l == 0 && kst >= 4 && kst < 12) ? 64 + 4 * (kst - 4)
-                                : (l == 1 && kst < 8) ? 96 + 4 * kst : 1 << 30;
+              const int sslot = (l == 1 && kst < 16) ? 64 + 4 * kst : 1 << 30;
               mbar_wait(&bar_full[st], (Sg / S) & 1);
               tc_mark(a, sslot + 2, kMmaWarp * 32);
               fence_after();

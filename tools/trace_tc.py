@@ -60,11 +60,10 @@ for l in range(2):
             continue
         print(f"  level {l} tile {t_}: " + " ".join(f"{(x - ls) / 1000:7.2f}" if x else "    -  " for x in v))
 
-print("per-stage, CTA 0 (us rel. to level start): prod after empty-wait, prod issued, mma after full-wait, mma committed")
-for l, base, k0 in ((0, 64, 4), (1, 96, 0)):
-    ls = tr[0, 2 + 4 * l]
-    for k in range(8):
-        v = tr[0, base + 4 * k: base + 4 * k + 4]
-        if (v == 0).all():
-            continue
-        print(f"  level {l} stage {k0 + k:2d}: " + " ".join(f"{(x - ls) / 1000:7.2f}" if x else "    -  " for x in v))
+print("per-stage, CTA 0, level 1 (us rel. to level start): TMA after empty-wait, TMA issued, MMA after full-wait, MMA committed")
+ls = tr[0, 2 + 4 * 1]
+for k in range(16):
+    v = tr[0, 64 + 4 * k: 64 + 4 * k + 4]
+    if (v == 0).all():
+        continue
+    print(f"  stage {k:2d}: " + " ".join(f"{(x - ls) / 1000:7.2f}" if x else "    -  " for x in v))
