@@ -197,6 +197,12 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
       a.hf = reinterpret_cast<float *>(q);
       q = align_up(q + 4 * (size_t)m->vocab * H, 256);
       a.crow = reinterpret_cast<int *>(q);
+      q = align_up(q + 4 * N, 256);
+    }
+    if (m->cell == CX_TREELSTM) {
+      a.pb = reinterpret_cast<unsigned short *>(q);
+      q = align_up(q + 2 * (2 * N) * H, 256);
+      a.pslot = reinterpret_cast<int *>(q);
     }
   } else if (plan.big) a.pbuf = buf;  // hs, st [n][H] + words [n] (forward_big.cu)
   else switch (m->cell) {

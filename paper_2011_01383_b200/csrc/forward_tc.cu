@@ -72,8 +72,9 @@ struct alignas(64) TmaDesc {
 };
 // kernel parameter block: tensor maps of the gathered operands + the common args
 struct TcArgs {
-  TmaDesc tm_h;  // hb [n][H] bf16, box 64 x 1, 128B swizzle
-  TmaDesc tm_x;  // xb [rows][H] bf16 (x-slot cells), same box
+  TmaDesc tm_h;  // gather maps (DAG-RNN, TreeFC): hb state rows, box 64 x 1, 128B swizzle
+  TmaDesc tm_x;  // input rows xb: gather box 64 x 1 (DAG-RNN) | tile box 64 x 128/CL (TreeLSTM)
+  TmaDesc tm_p;  // TreeLSTM: parent-slot rows pb [J*n][H], tile box 64 x 128/CL
   FwdArgs f;
 };
 constexpr int kMetaRing = 4;
@@ -85,7 +86,8 @@ struct TcMeta {
   alignas(16) int own[kTM];    // input id (output row), -1 past cnt
   alignas(16) int xr[kTM];     // row of xb (word or node-order row), -1 = none (zeros)
   alignas(16) int root[kTM];   // index in roots[] or -1
-  alignas(16) int ch[J][kTM];  // children new ids, -1 absent (zeros)
+  alignas(16) int ch[J][kTM];  // children state rows, -1 absent (zeros)
+  alignas(16) int ps[kTM];     // TreeLSTM: parent-slot row of the node's h, -1 = root
   int i0, cnt;
 };
 
@@ -108,7 +110,7 @@ struct TcCfg {
   // CTAs that own different unit slices of the same node tiles form a cluster
   // of CL; each fetches 1/CL of every stage and multicasts it to all
   static constexpr int GU = H / U;
-  static constexpr int CL = GU < kMaxCluster ? GU : kMaxCluster;
+  static constexpr int CL = LSTM ? 1 : (GU < kMaxCluster ? GU : kMaxCluster);
   static constexpr size_t bbytes0 = (size_t)B0 * KA * 128, bbytes1 = (size_t)B1 * KA * 128;
   static constexpr size_t static_bytes = sizeof(TcMeta<J>) * kMetaRing + 4 * U * 4 + 64 * 8 + 64;
   static constexpr int S_fit =
@@ -160,6 +162,43 @@ __device__ __forceinline__ void store_bf16(unsigned short *dst, const float (&v)
     d[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
                       pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
 }
+// 256-bit global accesses (sm_100: LDG/STG.256): a thread's 16-unit fp32 row
+// piece is 2 requests instead of 4, its bf16 piece 1 instead of 2
+__device__ __forceinline__ void st256(float *p, const float *v) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]) : "memory");
+}
+__device__ __forceinline__ void st256_cs(float *p, const float *v) {  // streaming (caller outputs)
+  asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]) : "memory");
+}
+__device__ __forceinline__ void ld256(const float *p, float *v) {  // L1-allocating
+  asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+                 "=f"(v[7]) : "l"(p));
+}
+__device__ __forceinline__ void st256_bf16(unsigned short *p, const float *v) {  // 16 bf16
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+               "r"(pack_bf16(v[0], v[1])), "r"(pack_bf16(v[2], v[3])), "r"(pack_bf16(v[4], v[5])),
+               "r"(pack_bf16(v[6], v[7])), "r"(pack_bf16(v[8], v[9])), "r"(pack_bf16(v[10], v[11])),
+               "r"(pack_bf16(v[12], v[13])), "r"(pack_bf16(v[14], v[15])) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void st_row(float *p, const float (&v)[N]) {
+#pragma unroll
+  for (int q = 0; q < N / 8; q++) st256(p + 8 * q, v + 8 * q);
+}
+template <int N>
+__device__ __forceinline__ void st_row_cs(float *p, const float (&v)[N]) {
+#pragma unroll
+  for (int q = 0; q < N / 8; q++) st256_cs(p + 8 * q, v + 8 * q);
+}
+template <int N>
+__device__ __forceinline__ void st_row_bf16(unsigned short *p, const float (&v)[N]) {
+#pragma unroll
+  for (int q = 0; q < N / 16; q++) st256_bf16(p + 16 * q, v + 16 * q);
+}
+
 // Gate nonlinearities of the bf16 path: one MUFU op each (tanh.approx.f32,
 // relative error ~2^-11, far inside the bf16 path's 2e-2 budget; the fp32
 // path keeps the ex2/rcp forms of common.cuh).
@@ -300,6 +339,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
       }
     }
   }
+  if (C::LSTM && status0 == CX_OK) {  // parent-slot row of every non-root node
+    const size_t total_threads = (size_t)gridDim.x * blockDim.x;
+    const size_t gt = (size_t)blockIdx.x * blockDim.x + tid;
+    for (size_t pn = gt; pn < (size_t)first_leaf; pn += total_threads) {
+#pragma unroll
+      for (int k = 0; k < J; k++) {
+        const int c = __ldg(a.chn + (size_t)k * n + pn);
+        if (c >= 0) a.pslot[c] = k * n + (int)pn;
+      }
+    }
+    const int R = a.hdr->num_roots;  // roots are nobody's child: no conflict
+    for (size_t r = gt; r < (size_t)R; r += total_threads) a.pslot[__ldg(a.roots + r)] = -1;
+  }
   fence_proxy_async();  // resident weights (generic stores) -> tensor-core reads
   fence_before();
   cluster_sync_all();   // peers' mbarriers initialised before any multicast
@@ -308,10 +360,74 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
   const uint32_t tmem = s_tmem;
   tc_mark(a, 1, 0);
 
+  // Hoisted leaves: caller outputs (and, for parents, the bf16 h in each leaf's
+  // parent slot) copied from the word table once it is complete.
+  auto leaf_copy = [&](bool to_slots) {
+    // each warp takes 32 leaves: their indices in one coalesced round trip,
+    // then rows copied with float4 lanes, 4 leaves in flight
+    constexpr int q4 = H / 4;
+    const int nleaf = n - first_leaf;
+    const int gw = (blockIdx.x * blockDim.x + tid) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int j0 = gw * 32; j0 < nleaf; j0 += nw * 32) {
+      const int jl = j0 + lane;
+      int own = -1, w = 0, r = -1, ps = -1;
+      if (jl < nleaf) {
+        const int j = first_leaf + jl;
+        own = __ldg(a.perm + j);
+        w = __ldcg(a.crow + j);
+        if (to_slots) ps = __ldcg(a.pslot + j);
+        if (a.root_out) {  // a one-node structure: its leaf is a root
+          const int q = __ldg(a.sid + j);
+          r = __ldg(a.roots + q) == j ? q : -1;
+        }
+      }
+      const int cnt = min(32, nleaf - j0);
+      for (int k0 = 0; k0 < cnt; k0 += 4) {
+        float4 hv[4][q4 / 32];
+        int ok[4], ow[4], rk[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int k = min(k0 + u, cnt - 1);
+          ok[u] = k0 + u < cnt;
+          ow[u] = __shfl_sync(0xffffffffu, own, k);
+          rk[u] = __shfl_sync(0xffffffffu, r, k);
+          const int wk = __shfl_sync(0xffffffffu, w, k);
+          const int pk = __shfl_sync(0xffffffffu, ps, k);
+          if (to_slots && ok[u] && pk >= 0 && lane < H / 8)  // bf16 row: 16 B per lane
+            reinterpret_cast<uint4 *>(a.pb + (size_t)pk * H)[lane] =
+                __ldcg(reinterpret_cast<const uint4 *>(hb + (size_t)wk * H) + lane);
+          const float4 *hs = reinterpret_cast<const float4 *>(a.hf + (size_t)wk * H);
+#pragma unroll
+          for (int e = 0; e < q4 / 32; e++) hv[u][e] = __ldcg(hs + lane + 32 * e);
+          if (a.aux_out && ok[u]) {
+            const float4 *cv = reinterpret_cast<const float4 *>(cs + (size_t)wk * H);
+#pragma unroll
+            for (int e = 0; e < q4 / 32; e++)
+              __stcs(reinterpret_cast<float4 *>(a.aux_out + (size_t)ow[u] * H) + lane + 32 * e,
+                     __ldcg(cv + lane + 32 * e));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          if (!ok[u]) continue;
+#pragma unroll
+          for (int e = 0; e < q4 / 32; e++) {
+            __stcs(reinterpret_cast<float4 *>(a.h_out + (size_t)ow[u] * H) + lane + 32 * e, hv[u][e]);
+            if (rk[u] >= 0) reinterpret_cast<float4 *>(a.root_out + (size_t)rk[u] * H)[lane + 32 * e] = hv[u][e];
+          }
+        }
+      }
+    }
+  };
+
   uint32_t T0 = 0, Sg0 = 0;  // tiles / stages before this level (identical in every role)
   for (int l = 0; l < L; l++) {
     const bool leaf = l == 0;
     if (l > 0) grid_sync(a.bar, gridDim.x, epoch);
+    if (l == 1 && hoist) {  // the word table is complete: fill the leaves' parent slots
+      leaf_copy(true);
+      grid_sync(a.bar, gridDim.x, epoch);
+    }
     tc_mark(a, 2 + 4 * l, 0);
     int lo, hi;
     if (leaf && hoist) {  // the leaf cell once per vocabulary word (rows [0, V))
@@ -362,16 +478,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
         tc_mark(a, tslot + 0, warp * 32);
         TcMeta<J> &m = meta[ms];
         constexpr int RQ = kTM / 32;
-        int own[RQ], sv[RQ], ch[RQ][J];
+        int own[RQ], sv[RQ], psv[RQ], ch[RQ][J];
 #pragma unroll
         for (int q = 0; q < RQ; q++) {  // round 1: perm, structure, children
           const int r = lane + 32 * q, i = i0 + r;
           own[q] = -1;
           sv[q] = -1;
+          psv[q] = -1;
 #pragma unroll
           for (int k = 0; k < J; k++) ch[q][k] = -1;
           if (r < cnt && !(leaf && hoist)) {
             own[q] = __ldg(a.perm + i);
+            if (C::LSTM) psv[q] = __ldcg(a.pslot + i);
             if (a.root_out) sv[q] = __ldg(a.sid + i);
             if (!leaf) {
 #pragma unroll
@@ -415,6 +533,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
           m.own[r] = own[q];
           m.xr[r] = xr;
           m.root[r] = root;
+          m.ps[r] = psv[q];
 #pragma unroll
           for (int k = 0; k < J; k++) m.ch[k][r] = ch[q][k];
         }
@@ -424,11 +543,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
         tc_mark(a, tslot + 1, warp * 32);
       }
     } else if (warp == kTmaWarp) {
-      // ========================= TMA gathers ===================================
+      // ========================= TMA loads =====================================
       // per stage: one K-atom (64 bf16) of one slot for the tile's 128 rows.
-      // This CTA (cluster rank cr) fetches rows [cr*RPC, (cr+1)*RPC) with
-      // tile::gather4 (lane q: 4 rows) multicast to every CTA of the cluster;
-      // absent children / unused rows are row -1 -> zeros.
+      // This CTA (cluster rank cr) fetches rows [cr*RPC, (cr+1)*RPC), multicast
+      // to every CTA of the cluster: TreeLSTM with one 2D tile load (its
+      // operands are contiguous: h is stored in the parent's slot row, x rows
+      // are word- or node-ordered; rows of absent children / padding are not
+      // used by the epilogue); DAG-RNN / TreeFC with tile::gather4 (lane q: 4
+      // rows; absent children / unused rows are row -1 -> zeros).
       constexpr int CL = C::CL, RPC = kTM / CL;
       constexpr uint16_t mask = (uint16_t)((1u << CL) - 1);
       const int cr = gu % CL;
@@ -436,7 +558,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
       for (int t = 0; t < ntiles; t++) {
         const uint32_t TT = T0 + t;
         const int ms = TT % kMetaRing;
-        mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
+        const int i0 = lo + t * kTM;
+        // TreeLSTM operands are contiguous (parent-slot rows / x rows): no
+        // row indices needed, so the loads run ahead of the bookkeeping
+        if (!C::LSTM) mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
         const TcMeta<J> &m = meta[ms];
         for (int ka = 0; ka < KA; ka++) {
           for (int s = 0; s < nsl; s++) {
@@ -448,7 +573,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
             mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);  // free in every CTA of the cluster
             tc_mark(a, sslot + 0, kTmaWarp * 32);
             if (lane == 0) mbar_arrive_expect_tx(&bar_full[st], kStageBytes);
-            if (lane < RPC / 4) {
+            if (C::LSTM) {
+              if (lane == 0) {
+                // child slot k: rows k*n + i0 + ..; x: word rows (hoisted) or node-order rows
+                const int row0 = src >= 0 ? src * n + i0 : (hoist ? i0 : i0 - xlo);
+                tma_tile2d_mc(smem_u32(sStage + (size_t)st * kStageBytes + cr * RPC * 128),
+                              src >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x,
+                              &bar_full[st], ka * 64, row0 + cr * RPC, mask);
+              }
+            } else if (lane < RPC / 4) {
               const int rb = cr * RPC + 4 * lane;
               const int4 rv = *reinterpret_cast<const int4 *>((src < 0 ? m.xr : m.ch[src]) + rb);
               tma_gather4_mc(smem_u32(sStage + (size_t)st * kStageBytes + rb * 128),
@@ -530,12 +663,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
           for (int k = 0; k < J; k++) {
             ck[k] = (valid && !leaf) ? m.ch[k][r] : -1;
             if (ck[k] >= 0) {
-              const float4 *src = reinterpret_cast<const float4 *>(cs + (size_t)ck[k] * H + unit0 + u0);
-#pragma unroll
-              for (int q = 0; q < 4; q++) {
-                const float4 x = __ldcg(src + q);
-                cp[k][4 * q] = x.x; cp[k][4 * q + 1] = x.y; cp[k][4 * q + 2] = x.z; cp[k][4 * q + 3] = x.w;
-              }
+              // L1-allocating loads: a child's row slice (128 B = one line) is
+              // written once, at an earlier level, and read by nobody before,
+              // so no SM can hold a stale copy; the line's 4 (x 2 column
+              // halves) 16-byte pieces then cost one L2 request instead of 8
+              const float *src = cs + (size_t)ck[k] * H + unit0 + u0;
+              ld256(src, cp[k]);
+              ld256(src + 8, cp[k] + 8);
             }
           }
           mbar_wait(&bar_tfull[buf], (TT >> 1) & 1);
@@ -564,13 +698,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
             tmem_ld<16>(tb + 0, v);        // i = sum_k acc_k[i], u = sum_k acc_k[u]
             tmem_ld<16>(tb + 2 * U, w);
 #pragma unroll
-            for (int k = 1; k < J; k++) {
+            for (int k = 1; k < J; k++) {  // absent children's accumulators are not read
               tmem_ld<16>(tb + k * NL + 0, h);
+              if (ck[k] >= 0) {
 #pragma unroll
-              for (int j = 0; j < 16; j++) v[j] += h[j];
+                for (int j = 0; j < 16; j++) v[j] += h[j];
+              }
               tmem_ld<16>(tb + k * NL + 2 * U, h);
+              if (ck[k] >= 0) {
 #pragma unroll
-              for (int j = 0; j < 16; j++) w[j] += h[j];
+                for (int j = 0; j < 16; j++) w[j] += h[j];
+              }
             }
 #pragma unroll
             for (int j = 0; j < 16; j++) c[j] = fmaf(sigm_mufu(v[j] + bi[j]), tanh_mufu(w[j] + bu[j]), c[j]);
@@ -578,8 +716,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
 #pragma unroll
             for (int k = 1; k < J; k++) {
               tmem_ld<16>(tb + k * NL + U, h);
+              if (ck[k] >= 0) {
 #pragma unroll
-              for (int j = 0; j < 16; j++) v[j] += h[j];
+                for (int j = 0; j < 16; j++) v[j] += h[j];
+              }
             }
 #pragma unroll
             for (int j = 0; j < 16; j++) h[j] = sigm_mufu(v[j] + bo[j]) * tanh_mufu(c[j]);
@@ -587,15 +727,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
           if (valid) {
             const bool wordrow = leaf && hoist;  // hoisted leaf cell: row i = word i
             const size_t ui = (size_t)(wordrow ? i : sbase + i) * H + unit0 + u0;
-            store_bf16<16>(hb + ui, h);
-            store_f32<16>(cs + ui, c);
+            if (wordrow) st_row_bf16<16>(hb + ui, h);  // the word table (copied to slots below)
+            else if (m.ps[r] >= 0) st_row_bf16<16>(a.pb + (size_t)m.ps[r] * H + unit0 + u0, h);
+            st_row<16>(cs + ui, c);
             if (wordrow) {
-              store_f32<16>(a.hf + (size_t)i * H + unit0 + u0, h);
+              st_row<16>(a.hf + (size_t)i * H + unit0 + u0, h);
             } else {
               const size_t uo = (size_t)own * H + unit0 + u0;
-              store_f32_stream<16>(a.h_out + uo, h);
-              if (a.aux_out) store_f32_stream<16>(a.aux_out + uo, c);
-              if (root >= 0) store_f32_stream<16>(a.root_out + (size_t)root * H + unit0 + u0, h);
+              st_row_cs<16>(a.h_out + uo, h);
+              if (a.aux_out) st_row_cs<16>(a.aux_out + uo, c);
+              if (root >= 0) st_row_cs<16>(a.root_out + (size_t)root * H + unit0 + u0, h);
             }
           }
         } else {  // DAG-RNN / TreeFC: h = tanh(acc + b)
@@ -611,9 +752,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
             for (int j = 0; j < CW; j++) v[j] = tanh_mufu(v[j] + s_bias[u0 + q * CW + j]);
             if (valid) {
               const int uu = unit0 + u0 + q * CW;
-              store_f32_stream<CW>(a.h_out + (size_t)own * H + uu, v);
-              store_bf16<CW>(hb + (size_t)i * H + uu, v);
-              if (root >= 0) store_f32_stream<CW>(a.root_out + (size_t)root * H + uu, v);
+              st_row_cs<CW>(a.h_out + (size_t)own * H + uu, v);
+              st_row_bf16<CW>(hb + (size_t)i * H + uu, v);
+              if (root >= 0) st_row_cs<CW>(a.root_out + (size_t)root * H + uu, v);
             }
           }
         }
@@ -630,59 +771,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
 
   // ---- hoisted leaves: outputs copied from the word table -------------------
   // (the table was complete at the level-1 barrier; every CTA copies a share)
-  if (hoist && L > 0) {
-    // a single-level batch has had no barrier since the table epilogue
-    if (L == 1) grid_sync(a.bar, gridDim.x, epoch);
-    // each warp takes 32 leaves: their indices in one coalesced round trip,
-    // then rows copied with float4 lanes, 4 leaves in flight
-    constexpr int q4 = H / 4;
-    const int nleaf = n - first_leaf;
-    const int gw = (blockIdx.x * blockDim.x + tid) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-    for (int j0 = gw * 32; j0 < nleaf; j0 += nw * 32) {
-      const int jl = j0 + lane;
-      int own = -1, w = 0, r = -1;
-      if (jl < nleaf) {
-        const int j = first_leaf + jl;
-        own = __ldg(a.perm + j);
-        w = __ldcg(a.crow + j);
-        if (a.root_out) {  // a one-node structure: its leaf is a root
-          const int q = __ldg(a.sid + j);
-          r = __ldg(a.roots + q) == j ? q : -1;
-        }
-      }
-      const int cnt = min(32, nleaf - j0);
-      for (int k0 = 0; k0 < cnt; k0 += 4) {
-        float4 hv[4][q4 / 32];
-        int ok[4], ow[4], rk[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const int k = min(k0 + u, cnt - 1);
-          ok[u] = k0 + u < cnt;
-          ow[u] = __shfl_sync(0xffffffffu, own, k);
-          rk[u] = __shfl_sync(0xffffffffu, r, k);
-          const int wk = __shfl_sync(0xffffffffu, w, k);
-          const float4 *hs = reinterpret_cast<const float4 *>(a.hf + (size_t)wk * H);
-#pragma unroll
-          for (int e = 0; e < q4 / 32; e++) hv[u][e] = __ldcg(hs + lane + 32 * e);
-          if (a.aux_out && ok[u]) {
-            const float4 *cv = reinterpret_cast<const float4 *>(cs + (size_t)wk * H);
-#pragma unroll
-            for (int e = 0; e < q4 / 32; e++)
-              __stcs(reinterpret_cast<float4 *>(a.aux_out + (size_t)ow[u] * H) + lane + 32 * e,
-                     __ldcg(cv + lane + 32 * e));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-          if (!ok[u]) continue;
-#pragma unroll
-          for (int e = 0; e < q4 / 32; e++) {
-            __stcs(reinterpret_cast<float4 *>(a.h_out + (size_t)ow[u] * H) + lane + 32 * e, hv[u][e]);
-            if (rk[u] >= 0) reinterpret_cast<float4 *>(a.root_out + (size_t)rk[u] * H)[lane + 32 * e] = hv[u][e];
-          }
-        }
-      }
-    }
+  if (hoist && L == 1) {  // a single-level batch: no barrier since the table epilogue
+    grid_sync(a.bar, gridDim.x, epoch);
+    leaf_copy(false);
   }
 
   // ---- teardown -------------------------------------------------------------
@@ -797,13 +888,13 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// [rows][H] bf16 row-major, box = 64 columns x 1 row, 128-byte swizzle
-bool encode_rows(TmaDesc *d, const void *base, int H, long long rows) {
+// [rows][H] bf16 row-major, box = 64 columns x box_rows rows, 128-byte swizzle
+bool encode_rows(TmaDesc *d, const void *base, int H, long long rows, int box_rows = 1) {
   EncodeTiledFn fn = encode_fn();
   if (!fn || rows < 1) return false;
   cuuint64_t dims[2] = {(cuuint64_t)H, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)H * 2};
-  cuuint32_t box[2] = {64, 1}, es[2] = {1, 1};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows}, es[2] = {1, 1};
   return fn(reinterpret_cast<CUtensorMap *>(d), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
             const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -819,8 +910,15 @@ cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &f, cudaStream_t stream
   const long long xrows = f.xmode ? f.n : f.V;
   const long long hrows = (long long)f.n + (f.hoist ? f.V : 0);
   if (!encode_rows(&ta.tm_h, f.hb, f.H, hrows)) return cudaErrorInvalidValue;
-  if (f.cell_has_x ? !encode_rows(&ta.tm_x, f.xb, f.H, xrows) : false) return cudaErrorInvalidValue;
-  if (!f.cell_has_x) ta.tm_x = ta.tm_h;
+  if (f.pb) {  // TreeLSTM: contiguous operands, multicast tile loads of 128/CL rows
+    const int brows = kTM / plan.cluster;
+    if (!encode_rows(&ta.tm_p, f.pb, f.H, 2LL * f.n, brows)) return cudaErrorInvalidValue;
+    if (!encode_rows(&ta.tm_x, f.xb, f.H, xrows, brows)) return cudaErrorInvalidValue;
+  } else {
+    if (f.cell_has_x ? !encode_rows(&ta.tm_x, f.xb, f.H, xrows) : false) return cudaErrorInvalidValue;
+    if (!f.cell_has_x) ta.tm_x = ta.tm_h;
+    ta.tm_p = ta.tm_h;
+  }
   void *params[] = {&ta};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(plan.ctas);
@@ -866,6 +964,7 @@ size_t tc_workspace_bytes(int cell, int H, int V, int n) {
   if (cell == CX_TREELSTM || cell == CX_DAGRNN)                 // xb
     b += 2 * (tc_xmode(n, V) ? N : (size_t)V) * h + 256;
   if (tc_hoist(cell, n, V)) b += 4 * (size_t)V * h + 4 * N + 512;  // hf, crow
+  if (cell == CX_TREELSTM) b += 2 * (2 * N) * h + 4 * N + 512;     // pb (J <= 2), pslot
   return b;
 }
 

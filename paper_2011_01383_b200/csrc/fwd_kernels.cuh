@@ -35,6 +35,9 @@ struct FwdArgs {
   int hoist;           // TreeLSTM leaf cell evaluated per vocabulary word (tc_hoist)
   float *hf;           // [V][H] fp32 h of every word (hoist)
   int *crow;           // [n] state row of node i: its word if a leaf, else V + i (hoist)
+  unsigned short *pb;  // TreeLSTM: [J*n][H] bf16 h of node i stored in its parent's child
+                       // slot row k*n + parent (a level tile's k-th children are contiguous)
+  int *pslot;          // [n] that row for every non-root node
   GridBar *bar;
   int Gn, Gu;   // node groups x unit groups = CTAs
   unsigned long long *trace;  // debug: %globaltimer per CTA and phase (cx_debug_set_trace)

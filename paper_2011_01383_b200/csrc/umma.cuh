@@ -182,6 +182,16 @@ __device__ __forceinline__ void tma_gather4_mc(uint32_t dst, const void *tmap, u
         "h"(mask)
       : "memory");
 }
+// 2D tile load (box of the tensor map at {c0, c1}) delivered to every CTA in
+// `mask` (same smem offset / mbarrier offset in each), complete_tx on `bar`.
+__device__ __forceinline__ void tma_tile2d_mc(uint32_t dst, const void *tmap, uint64_t *bar, int c0,
+                                              int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
 // tcgen05.commit arriving on the mbarrier at this offset in every CTA of `mask`
 __device__ __forceinline__ void mma_commit_mc(uint64_t *bar, uint16_t mask) {
   asm volatile(
