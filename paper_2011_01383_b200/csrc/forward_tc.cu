@@ -360,60 +360,79 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
   const uint32_t tmem = s_tmem;
   tc_mark(a, 1, 0);
 
-  // Hoisted leaves: caller outputs (and, for parents, the bf16 h in each leaf's
-  // parent slot) copied from the word table once it is complete.
-  auto leaf_copy = [&](bool to_slots) {
-    // each warp takes 32 leaves: their indices in one coalesced round trip,
-    // then rows copied with float4 lanes, 4 leaves in flight
-    constexpr int q4 = H / 4;
+  // Hoisted leaves. slot_fill: each leaf's bf16 h copied from the word table
+  // into its parent's child-slot row (needed before level 1). out_copy: the
+  // leaves' caller outputs (h_out, aux_out, root_out) from the fp32 word table.
+  // A warp loads the indices of 32 leaves in one coalesced round trip, then
+  // copies 8 rows at a time (all loads before the stores) with 256-bit accesses.
+  auto leaf_pass = [&](bool slot_fill) {
     const int nleaf = n - first_leaf;
     const int gw = (blockIdx.x * blockDim.x + tid) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     for (int j0 = gw * 32; j0 < nleaf; j0 += nw * 32) {
       const int jl = j0 + lane;
-      int own = -1, w = 0, r = -1, ps = -1;
+      int dst = -1, w = 0, r = -1;
       if (jl < nleaf) {
         const int j = first_leaf + jl;
-        own = __ldg(a.perm + j);
         w = __ldcg(a.crow + j);
-        if (to_slots) ps = __ldcg(a.pslot + j);
-        if (a.root_out) {  // a one-node structure: its leaf is a root
-          const int q = __ldg(a.sid + j);
-          r = __ldg(a.roots + q) == j ? q : -1;
+        if (slot_fill) {
+          dst = __ldcg(a.pslot + j);
+        } else {
+          dst = __ldg(a.perm + j);
+          if (a.root_out) {  // a one-node structure: its leaf is a root
+            const int q = __ldg(a.sid + j);
+            r = __ldg(a.roots + q) == j ? q : -1;
+          }
         }
       }
       const int cnt = min(32, nleaf - j0);
-      for (int k0 = 0; k0 < cnt; k0 += 4) {
-        float4 hv[4][q4 / 32];
-        int ok[4], ow[4], rk[4];
+      if (slot_fill) {  // bf16 rows: H/16 lanes x 32 B per row, 32/(H/16) rows per pass
+        constexpr int LPR = H / 16, RPP = 32 / LPR;
+        for (int k0 = 0; k0 < cnt; k0 += 8 * RPP) {
+          float v[8][8];
+          int dk[8];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const int k = min(k0 + u, cnt - 1);
-          ok[u] = k0 + u < cnt;
-          ow[u] = __shfl_sync(0xffffffffu, own, k);
-          rk[u] = __shfl_sync(0xffffffffu, r, k);
-          const int wk = __shfl_sync(0xffffffffu, w, k);
-          const int pk = __shfl_sync(0xffffffffu, ps, k);
-          if (to_slots && ok[u] && pk >= 0 && lane < H / 8)  // bf16 row: 16 B per lane
-            reinterpret_cast<uint4 *>(a.pb + (size_t)pk * H)[lane] =
-                __ldcg(reinterpret_cast<const uint4 *>(hb + (size_t)wk * H) + lane);
-          const float4 *hs = reinterpret_cast<const float4 *>(a.hf + (size_t)wk * H);
-#pragma unroll
-          for (int e = 0; e < q4 / 32; e++) hv[u][e] = __ldcg(hs + lane + 32 * e);
-          if (a.aux_out && ok[u]) {
-            const float4 *cv = reinterpret_cast<const float4 *>(cs + (size_t)wk * H);
-#pragma unroll
-            for (int e = 0; e < q4 / 32; e++)
-              __stcs(reinterpret_cast<float4 *>(a.aux_out + (size_t)ow[u] * H) + lane + 32 * e,
-                     __ldcg(cv + lane + 32 * e));
+          for (int u = 0; u < 8; u++) {
+            const int k = k0 + u * RPP + lane / LPR;
+            const int kk = min(k, cnt - 1);
+            dk[u] = __shfl_sync(0xffffffffu, dst, kk);
+            const int wk = __shfl_sync(0xffffffffu, w, kk);
+            if (k >= cnt) dk[u] = -1;
+            ld256(reinterpret_cast<const float *>(hb + (size_t)wk * H) + 8 * (lane % LPR), v[u]);
           }
+#pragma unroll
+          for (int u = 0; u < 8; u++)
+            if (dk[u] >= 0) st256(reinterpret_cast<float *>(a.pb + (size_t)dk[u] * H) + 8 * (lane % LPR), v[u]);
         }
+      } else {  // fp32 rows: H/8 lanes x 32 B per row
+        constexpr int LPR = H / 8 > 32 ? 32 : H / 8, CPL = H / 8 / LPR, RPP = 32 / LPR;
+        for (int k0 = 0; k0 < cnt; k0 += 4 * RPP) {
+          float v[4][CPL][8];
+          int dk[4], rk[4], wk[4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          if (!ok[u]) continue;
+          for (int u = 0; u < 4; u++) {
+            const int k = k0 + u * RPP + lane / LPR;
+            const int kk = min(k, cnt - 1);
+            dk[u] = __shfl_sync(0xffffffffu, dst, kk);
+            rk[u] = __shfl_sync(0xffffffffu, r, kk);
+            wk[u] = __shfl_sync(0xffffffffu, w, kk);
+            if (k >= cnt) dk[u] = -1;
 #pragma unroll
-          for (int e = 0; e < q4 / 32; e++) {
-            __stcs(reinterpret_cast<float4 *>(a.h_out + (size_t)ow[u] * H) + lane + 32 * e, hv[u][e]);
-            if (rk[u] >= 0) reinterpret_cast<float4 *>(a.root_out + (size_t)rk[u] * H)[lane + 32 * e] = hv[u][e];
+            for (int e = 0; e < CPL; e++) ld256(a.hf + (size_t)wk[u] * H + 8 * (lane % LPR + LPR * e), v[u][e]);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            if (dk[u] < 0) continue;
+#pragma unroll
+            for (int e = 0; e < CPL; e++) {
+              const int col = 8 * (lane % LPR + LPR * e);
+              st256_cs(a.h_out + (size_t)dk[u] * H + col, v[u][e]);
+              if (rk[u] >= 0) st256(a.root_out + (size_t)rk[u] * H + col, v[u][e]);
+              if (a.aux_out) {
+                float cv[8];
+                ld256(cs + (size_t)wk[u] * H + col, cv);
+                st256_cs(a.aux_out + (size_t)dk[u] * H + col, cv);
+              }
+            }
           }
         }
       }
@@ -425,7 +444,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     const bool leaf = l == 0;
     if (l > 0) grid_sync(a.bar, gridDim.x, epoch);
     if (l == 1 && hoist) {  // the word table is complete: fill the leaves' parent slots
-      leaf_copy(true);
+      leaf_pass(true);
       grid_sync(a.bar, gridDim.x, epoch);
     }
     tc_mark(a, 2 + 4 * l, 0);
@@ -771,9 +790,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
 
   // ---- hoisted leaves: outputs copied from the word table -------------------
   // (the table was complete at the level-1 barrier; every CTA copies a share)
-  if (hoist && L == 1) {  // a single-level batch: no barrier since the table epilogue
-    grid_sync(a.bar, gridDim.x, epoch);
-    leaf_copy(false);
+  if (hoist && L > 0) {  // leaves' caller outputs (the table is complete since level 1)
+    if (L == 1) grid_sync(a.bar, gridDim.x, epoch);  // single level: no barrier yet
+    leaf_pass(false);
   }
 
   // ---- teardown -------------------------------------------------------------

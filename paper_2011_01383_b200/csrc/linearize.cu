@@ -157,34 +157,62 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
   int L = 0;
   if (!failed && n > 0) {
     if (tree_like) {
+      // every leaf walks to its root with dependent parent loads only and posts
+      // height[ancestor] = max(., distance) fire-and-forget: height = longest
+      // distance to a leaf below. Brent's check stops a walk that entered a
+      // cycle (invalid input; handled below).
       int hmax = 0;
+      bool looped = false;
       for (int v = tid; v < n; v += nthr) {
-        if (ch[v] != -1) continue;  // walks start at leaves (an immutable test)
-        int cur = v, hc = 0;
+        if (ch[v] != -1) continue;  // walks start at leaves
+        int cur = v, d = 0, tort = v, power = 1, lam = 0;
         while (true) {
           const int p = __ldcg(&parent[cur]);
           if (p < 0) break;
-          atomicMax(&hgt[p], hc + 1);
-          __threadfence();
-          if (atomicSub(&pending[p], 1) != 1) break;
-          __threadfence();
+          d++;
+          atomicMax(&hgt[p], d);  // result unused: a RED.MAX
           cur = p;
-          hc = atomicAdd(&hgt[p], 0);  // every child's atomicMax precedes its decrement
+          if (cur == tort) {
+            looped = true;
+            break;
+          }
+          if (++lam == power) {
+            tort = cur;
+            power <<= 1;
+            lam = 0;
+          }
         }
-        hmax = max(hmax, hc);
+        hmax = max(hmax, d);
       }
       for (int o = 16; o; o >>= 1) hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
       if (lane == 0) atomicMax(&a.misc[4], hmax);
+      if (__syncthreads_or(looped) && threadIdx.x == 0) atomicAdd(&a.misc[3], 1);
       grid_sync(a.bar, G, epoch);
-      bool unfinished = false;  // on a cycle: some child never becomes final
-      for (int v = tid; v < n; v += nthr)
-        if (__ldcg(&pending[v]) > 0) {
-          latch_error(a.hdr, CX_E_CYCLE, v);
-          unfinished = true;
+      // a node no walk reached (a cycle without leaves below) also means a cycle
+      bool unreached = false;
+      for (int v = tid; v < n; v += nthr) unreached = unreached || __ldcg(&hgt[v]) < 0;
+      if (__syncthreads_or(unreached) && threadIdx.x == 0) atomicAdd(&a.misc[3], 1);
+      grid_sync(a.bar, G, epoch);
+      if (__ldcg(&a.misc[3]) != 0) {
+        // error path: peel the acyclic part from the leaves with pending child
+        // counts (the last arriving child continues); what is left are the
+        // cycle nodes, the lowest of which is reported
+        for (int v = tid; v < n; v += nthr) {
+          if (ch[v] != -1) continue;
+          int cur = v;
+          while (true) {
+            const int p = __ldcg(&parent[cur]);
+            if (p < 0) break;
+            __threadfence();
+            if (atomicSub(&pending[p], 1) != 1) break;
+            cur = p;
+          }
         }
-      if (__syncthreads_or(unfinished) && threadIdx.x == 0) atomicAdd(&a.misc[3], 1);
-      grid_sync(a.bar, G, epoch);
-      failed = __ldcg(&a.misc[3]) != 0;
+        grid_sync(a.bar, G, epoch);
+        for (int v = tid; v < n; v += nthr)
+          if (__ldcg(&pending[v]) > 0) latch_error(a.hdr, CX_E_CYCLE, v);
+        failed = true;
+      }
       L = __ldcg(&a.misc[4]) + 1;
     } else {
       // finished-node counts: misc[3] = leaves; round r adds into misc[r % 3],

@@ -116,3 +116,21 @@ def test_mid_size_random(cx, n, maxc):
     _check(cx, ch, synth.TREE)
     if 4 * n < 12000:
         _check(cx, synth.random_dag(n, maxc, n + maxc, p_edge=0.4), synth.DAG)
+
+
+def test_tree_cycles_multi_cta(cx):
+    """Tree-kind inputs with a cycle at multi-CTA size (n > 4.8k): a root made
+    the child of one of its own leaves (walks from hanging leaves enter the
+    cycle) and a leafless 3-ring appended to a valid forest; status and the
+    lowest cycle node must match the oracle."""
+    ch, off = synth.sst_shaped_forest(300, 5)
+    n = ch.shape[1]
+    c1 = ch.copy()
+    r = int(off[137])                       # a root
+    leaf = next(v for v in range(int(off[137]), int(off[138])) if c1[0, v] == -1)
+    c1[0, leaf] = r                         # leaf -> root: a cycle through the tree
+    _check(cx, c1, synth.TREE)
+    c2 = np.full((2, n + 3), -1, np.int32)
+    c2[:, :n] = ch
+    c2[0, n], c2[0, n + 1], c2[0, n + 2] = n + 1, n + 2, n  # ring without leaves
+    _check(cx, c2, synth.TREE)
