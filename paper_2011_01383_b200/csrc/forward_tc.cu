@@ -271,25 +271,58 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
   } else {
     for (int q = tid; q < U; q += blockDim.x) s_bias[q] = __ldg(a.w[C::DAG ? 2 : 1] + unit0 + q);
   }
-  // weights: B0 / B1 rows -> bf16, K-major SW128
-  for (int idx = tid; idx < (C::B0 + C::B1) * KA * 8; idx += blockDim.x) {
-    int q = idx / (KA * 8);
-    const int rem = idx - q * (KA * 8), ka = rem >> 3, c = rem & 7;
-    const bool second = q >= C::B0;
-    if (second) q -= C::B0;
-    const float *src;
-    if constexpr (C::LSTM) {
-      const int g = q / U, u = q % U;
-      if (!second) src = a.w[0] + (size_t)(g * H + unit0 + u) * H;                 // W_iou
-      else src = g < 3 ? a.w[1] + (size_t)(g * H + unit0 + u) * H                  // U_iou
-                       : a.w[3] + (size_t)(unit0 + u) * H;                          // U_f
-    } else if constexpr (C::DAG) {
-      src = a.w[second ? 1 : 0] + (size_t)(unit0 + q) * H;                         // U | W_x
-    } else {
-      src = a.w[0] + (size_t)(unit0 + q) * 2 * H + (second ? H : 0);               // W [H][2H]
+  // weights: B0 / B1 rows -> bf16, K-major SW128; 8 chunks' loads in flight
+  // per thread before their conversions and stores
+  {
+    constexpr int NCH = (C::B0 + C::B1) * KA * 8;
+    auto wsrc = [&](int idx, unsigned char *&Bm, int &rows, int &q, int &ka, int &c) -> const float * {
+      q = idx / (KA * 8);
+      const int rem = idx - q * (KA * 8);
+      ka = rem >> 3;
+      c = rem & 7;
+      const bool second = q >= C::B0;
+      if (second) q -= C::B0;
+      Bm = second ? sB1 : sB0;
+      rows = second ? C::B1 : C::B0;
+      if constexpr (C::LSTM) {
+        const int g = q / U, u = q % U;
+        if (!second) return a.w[0] + (size_t)(g * H + unit0 + u) * H;                // W_iou
+        return g < 3 ? a.w[1] + (size_t)(g * H + unit0 + u) * H                      // U_iou
+                     : a.w[3] + (size_t)(unit0 + u) * H;                              // U_f
+      } else if constexpr (C::DAG) {
+        return a.w[second ? 1 : 0] + (size_t)(unit0 + q) * H;                        // U | W_x
+      } else {
+        return a.w[0] + (size_t)(unit0 + q) * 2 * H + (second ? H : 0);              // W [H][2H]
+      }
+    };
+    for (int base = 0; base < NCH; base += 8 * (int)blockDim.x) {
+      float4 lo[8], hi[8];
+#pragma unroll
+      for (int e = 0; e < 8; e++) {
+        const int idx = base + e * blockDim.x + tid;
+        if (idx < NCH) {
+          unsigned char *Bm;
+          int rows, q, ka, c;
+          const float *row = wsrc(idx, Bm, rows, q, ka, c);
+          const float4 *sp = reinterpret_cast<const float4 *>(row + ka * 64 + c * 8);
+          lo[e] = __ldg(sp);
+          hi[e] = __ldg(sp + 1);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 8; e++) {
+        const int idx = base + e * blockDim.x + tid;
+        if (idx < NCH) {
+          unsigned char *Bm;
+          int rows, q, ka, c;
+          (void)wsrc(idx, Bm, rows, q, ka, c);
+          *reinterpret_cast<uint4 *>(Bm + (size_t)ka * rows * 128 + sw128_off(q, c)) = f32x8_to_bf16(lo[e], hi[e]);
+        }
+      }
     }
-    stage_weight_chunk(second ? sB1 : sB0, second ? C::B1 : C::B0, q, ka, c, src);
   }
+
+  tc_mark(a, 60, 0);
   // the linearization is read from here on (PDL: the above overlapped it)
   griddep_wait();
   const int status0 = *reinterpret_cast<volatile int *>(&a.hdr->status);
@@ -305,9 +338,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     unsigned short *xw = const_cast<unsigned short *>(xb);
     if (a.xmode == 0) {  // whole table, indexed by word
       const size_t total = (size_t)a.V * q8;
-      for (size_t idx = gt; idx < total; idx += total_threads) {
-        const float4 *s = reinterpret_cast<const float4 *>(a.emb + idx * 8);
-        *reinterpret_cast<uint4 *>(xw + idx * 8) = f32x8_to_bf16(__ldg(s), __ldg(s + 1));
+      for (size_t b0 = gt; b0 < total; b0 += 4 * total_threads) {  // 4 chunks in flight
+        float4 lo[4], hi[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const size_t idx = b0 + e * total_threads;
+          if (idx < total) {
+            const float4 *sp = reinterpret_cast<const float4 *>(a.emb + idx * 8);
+            lo[e] = __ldg(sp);
+            hi[e] = __ldg(sp + 1);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const size_t idx = b0 + e * total_threads;
+          if (idx < total) *reinterpret_cast<uint4 *>(xw + idx * 8) = f32x8_to_bf16(lo[e], hi[e]);
+        }
       }
       if (hoist) {  // state row of every node: leaves -> their word's row
         for (size_t i = gt; i < (size_t)n; i += total_threads) {
@@ -352,6 +398,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     const int R = a.hdr->num_roots;  // roots are nobody's child: no conflict
     for (size_t r = gt; r < (size_t)R; r += total_threads) a.pslot[__ldg(a.roots + r)] = -1;
   }
+  tc_mark(a, 61, 0);
   fence_proxy_async();  // resident weights (generic stores) -> tensor-core reads
   fence_before();
   cluster_sync_all();   // peers' mbarriers initialised before any multicast

@@ -42,6 +42,7 @@ sizes = lin.level_size[:nl].cpu().numpy()
 t0 = tr[:, 0].min()
 rel = lambda x: (x - t0) / 1000.0
 print(f"{name} bf16: ctas={info['ctas']} levels={nl} (us from earliest CTA entry)")
+print(f"weights staged: min {rel(tr[:,60].min()):8.2f} max {rel(tr[:,60].max()):8.2f}; phase 0 done: max {rel(tr[:,61].max()):8.2f}")
 print(f"prologue done: min {rel(tr[:,1].min()):8.2f} max {rel(tr[:,1].max()):8.2f}")
 for l in range(nl):
     st, pr, mm, ep = (tr[:, 2 + 4 * l + k] for k in range(4))
