@@ -64,6 +64,7 @@ constexpr int kTM = 128;                    // tile rows = UMMA M
 constexpr int kEpiWarps = 8, kMmaWarp = 8, kTmaWarp = 9, kMeta0 = 10, kMetaWarps = 2;
 constexpr int kTcThreads = 32 * (kMeta0 + kMetaWarps);  // 384
 constexpr int kEpiThreads = 32 * kEpiWarps;             // 256
+constexpr int kWork = 32 * kMeta0;                      // threads of the working warps (320)
 constexpr int kMaxCluster = 8;                          // portable cluster size
 
 // 128-byte CUtensorMap (opaque; encoded on the host by cuTensorMapEncodeTiled)
@@ -209,14 +210,6 @@ __device__ __forceinline__ float tanh_mufu(float x) {
 }
 __device__ __forceinline__ float sigm_mufu(float x) { return fmaf(0.5f, tanh_mufu(0.5f * x), 0.5f); }
 
-// Prologue: row q, K-atom ka, 16-byte chunk c of a resident B matrix (8 bf16)
-// <- the fp32 weights src[ka*64 + c*8 .. +8]
-__device__ __forceinline__ void stage_weight_chunk(unsigned char *Bm, int rows, int q, int ka, int c,
-                                                   const float *src) {
-  const float4 *s = reinterpret_cast<const float4 *>(src + ka * 64 + c * 8);
-  uint4 v = f32x8_to_bf16(__ldg(s), __ldg(s + 1));
-  *reinterpret_cast<uint4 *>(Bm + (size_t)ka * rows * 128 + sw128_off(q, c)) = v;
-}
 
 // debug timeline (cx_debug_set_trace): thread `who` of each CTA records
 // %globaltimer into slot s. Slots: 0 entry, 1 prologue done, 2+4l level l
@@ -414,7 +407,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
   // copies 8 rows at a time (all loads before the stores) with 256-bit accesses.
   auto leaf_pass = [&](bool slot_fill) {
     const int nleaf = n - first_leaf;
-    const int gw = (blockIdx.x * blockDim.x + tid) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int gw = (blockIdx.x * kWork + tid) >> 5, nw = (gridDim.x * kWork) >> 5;
     for (int j0 = gw * 32; j0 < nleaf; j0 += nw * 32) {
       const int jl = j0 + lane;
       int dst = -1, w = 0, r = -1;
@@ -452,11 +445,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
         }
       } else {  // fp32 rows: H/8 lanes x 32 B per row
         constexpr int LPR = H / 8 > 32 ? 32 : H / 8, CPL = H / 8 / LPR, RPP = 32 / LPR;
-        for (int k0 = 0; k0 < cnt; k0 += 4 * RPP) {
-          float v[4][CPL][8];
-          int dk[4], rk[4], wk[4];
+        for (int k0 = 0; k0 < cnt; k0 += 8 * RPP) {
+          float v[8][CPL][8];
+          int dk[8], rk[8], wk[8];
 #pragma unroll
-          for (int u = 0; u < 4; u++) {
+          for (int u = 0; u < 8; u++) {
             const int k = k0 + u * RPP + lane / LPR;
             const int kk = min(k, cnt - 1);
             dk[u] = __shfl_sync(0xffffffffu, dst, kk);
@@ -467,7 +460,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
             for (int e = 0; e < CPL; e++) ld256(a.hf + (size_t)wk[u] * H + 8 * (lane % LPR + LPR * e), v[u][e]);
           }
 #pragma unroll
-          for (int u = 0; u < 4; u++) {
+          for (int u = 0; u < 8; u++) {
             if (dk[u] < 0) continue;
 #pragma unroll
             for (int e = 0; e < CPL; e++) {
@@ -486,17 +479,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
     }
   };
 
-  uint32_t T0 = 0, Sg0 = 0;  // tiles / stages before this level (identical in every role)
-  for (int l = 0; l < L; l++) {
-    const bool leaf = l == 0;
-    if (l > 0) grid_sync(a.bar, gridDim.x, epoch);
-    if (l == 1 && hoist) {  // the word table is complete: fill the leaves' parent slots
-      leaf_pass(true);
-      grid_sync(a.bar, gridDim.x, epoch);
-    }
-    tc_mark(a, 2 + 4 * l, 0);
-    int lo, hi;
-    if (leaf && hoist) {  // the leaf cell once per vocabulary word (rows [0, V))
+  // level ranges: identical in every role
+  auto level_range = [&](int l, int &lo, int &hi) {
+    if (l == 0 && hoist) {  // the leaf cell once per vocabulary word (rows [0, V))
       chunk_of(a.V, a.Gn, gn, lo, hi);
     } else {
       chunk_of(__ldg(a.lsize + l), a.Gn, gn, lo, hi);
@@ -504,35 +489,36 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
       lo += lb;
       hi += lb;
     }
-    if constexpr (C::FC) {
-      if (leaf) {  // h = Emb[word]: this CTA's node chunk x unit slice
-        constexpr int q4 = U / 4;
-        for (int idx = tid; idx < (hi - lo) * q4; idx += blockDim.x) {
-          const int i = lo + idx / q4, c = idx % q4;
-          const int own = __ldg(a.perm + i);
-          int w = __ldg(a.words + own);
-          if (w < 0 || w >= a.V) {
-            if (latch && c == 0) latch_error(a.hdr, CX_E_WORD_RANGE, own);
-            w = 0;
-          }
-          const float4 v = __ldg(reinterpret_cast<const float4 *>(a.emb + (size_t)w * H + unit0) + c);
-          *reinterpret_cast<float4 *>(a.h_out + (size_t)own * H + unit0 + 4 * c) = v;
-          *reinterpret_cast<uint2 *>(hb + (size_t)i * H + unit0 + 4 * c) =
-              make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
-          if (a.root_out) {
-            const int r = __ldg(a.sid + i);
-            if (__ldg(a.roots + r) == i)
-              *reinterpret_cast<float4 *>(a.root_out + (size_t)r * H + unit0 + 4 * c) = v;
-          }
-        }
-        continue;
+  };
+  // grid barrier between levels among the working warps (the bookkeeping warps
+  // do not wait): named barrier, then thread 0's release/acquire counter
+  auto level_sync = [&]() {
+    named_bar(3, kWork);
+    epoch += 1;
+    if (tid == 0) {
+      red_release_add_u32(&a.bar->count, 1u);
+      const unsigned target = epoch * gridDim.x;
+      unsigned long long spins = 0;
+      while (ld_relaxed_u32(&a.bar->count) < target) {
+        if (++spins > (1ull << 26)) __trap();
       }
+      (void)ld_acquire_u32(&a.bar->count);
     }
-    const int ntiles = (hi - lo + kTM - 1) / kTM;
-    const int nsl = C::nslots(leaf);
+    named_bar(3, kWork);
+  };
 
-    if (warp >= kMeta0) {
-      // ======================== tile bookkeeping ===============================
+  if (warp >= kMeta0) {
+    // ======================== tile bookkeeping ===============================
+    // It depends on the linearization only, so these warps run ahead of the
+    // level barriers (bounded by the 4-slot ring the epilogue releases).
+    uint32_t T0m = 0;
+    for (int l = 0; l < L; l++) {
+      const bool leaf = l == 0;
+      if (C::FC && leaf) continue;  // TreeFC leaves: a copy, no tiles
+      int lo, hi;
+      level_range(l, lo, hi);
+      const int ntiles = (hi - lo + kTM - 1) / kTM;
+      const uint32_t T0 = T0m;
       // lane handles rows lane + 32 q; two dependent rounds of index loads
       const int mw = warp - kMeta0;
       for (int t = mw; t < ntiles; t += kMetaWarps) {
@@ -608,72 +594,68 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
         if (lane == 0) mbar_arrive(&bar_mfull[ms]);
         tc_mark(a, tslot + 1, warp * 32);
       }
-    } else if (warp == kTmaWarp) {
-      // ========================= TMA loads =====================================
-      // per stage: one K-atom (64 bf16) of one slot for the tile's 128 rows.
-      // This CTA (cluster rank cr) fetches rows [cr*RPC, (cr+1)*RPC), multicast
-      // to every CTA of the cluster: TreeLSTM with one 2D tile load (its
-      // operands are contiguous: h is stored in the parent's slot row, x rows
-      // are word- or node-ordered; rows of absent children / padding are not
-      // used by the epilogue); DAG-RNN / TreeFC with tile::gather4 (lane q: 4
-      // rows; absent children / unused rows are row -1 -> zeros).
-      constexpr int CL = C::CL, RPC = kTM / CL;
-      constexpr uint16_t mask = (uint16_t)((1u << CL) - 1);
-      const int cr = gu % CL;
-      uint32_t Sg = Sg0;
-      for (int t = 0; t < ntiles; t++) {
-        const uint32_t TT = T0 + t;
-        const int ms = TT % kMetaRing;
-        const int i0 = lo + t * kTM;
-        // TreeLSTM operands are contiguous (parent-slot rows / x rows): no
-        // row indices needed, so the loads run ahead of the bookkeeping
-        if (!C::LSTM) mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
-        const TcMeta<J> &m = meta[ms];
-        for (int ka = 0; ka < KA; ka++) {
-          for (int s = 0; s < nsl; s++) {
-            int src, bm, acc;
-            C::slot(leaf, s, src, bm, acc);
-            const int st = Sg % S;
-            const int kst = (int)(Sg - Sg0);
-            const int sslot = (l == 1 && kst < 16) ? 64 + 4 * kst : 1 << 30;
-            mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);  // free in every CTA of the cluster
-            tc_mark(a, sslot + 0, kTmaWarp * 32);
-            if (lane == 0) mbar_arrive_expect_tx(&bar_full[st], kStageBytes);
-            if (C::LSTM) {
-              if (lane == 0) {
-                // child slot k: rows k*n + i0 + ..; x: word rows (hoisted) or node-order rows
-                const int row0 = src >= 0 ? src * n + i0 : (hoist ? i0 : i0 - xlo);
-                tma_tile2d_mc(smem_u32(sStage + (size_t)st * kStageBytes + cr * RPC * 128),
-                              src >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x,
-                              &bar_full[st], ka * 64, row0 + cr * RPC, mask);
-              }
-            } else if (lane < RPC / 4) {
-              const int rb = cr * RPC + 4 * lane;
-              const int4 rv = *reinterpret_cast<const int4 *>((src < 0 ? m.xr : m.ch[src]) + rb);
-              tma_gather4_mc(smem_u32(sStage + (size_t)st * kStageBytes + rb * 128),
-                             src < 0 ? (const void *)&ta.tm_x : (const void *)&ta.tm_h,
-                             &bar_full[st], ka * 64, rv.x, rv.y, rv.z, rv.w, mask);
+      T0m += ntiles;
+    }
+  } else {
+    uint32_t T0 = 0, Sg0 = 0;  // tiles / stages before this level (identical in every role)
+    for (int l = 0; l < L; l++) {
+      const bool leaf = l == 0;
+      if (l > 0) level_sync();
+      if (l == 1 && hoist) {  // the word table is complete: fill the leaves' parent slots
+        leaf_pass(true);
+        level_sync();
+      }
+      tc_mark(a, 2 + 4 * l, 0);
+      int lo, hi;
+      level_range(l, lo, hi);
+      if constexpr (C::FC) {
+        if (leaf) {  // h = Emb[word]: this CTA's node chunk x unit slice
+          constexpr int q4 = U / 4;
+          for (int idx = tid; idx < (hi - lo) * q4; idx += kWork) {
+            const int i = lo + idx / q4, c = idx % q4;
+            const int own = __ldg(a.perm + i);
+            int w = __ldg(a.words + own);
+            if (w < 0 || w >= a.V) {
+              if (latch && c == 0) latch_error(a.hdr, CX_E_WORD_RANGE, own);
+              w = 0;
             }
-            __syncwarp();
-            tc_mark(a, sslot + 1, kTmaWarp * 32);
-            Sg++;
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(a.emb + (size_t)w * H + unit0) + c);
+            *reinterpret_cast<float4 *>(a.h_out + (size_t)own * H + unit0 + 4 * c) = v;
+            *reinterpret_cast<uint2 *>(hb + (size_t)i * H + unit0 + 4 * c) =
+                make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+            if (a.root_out) {
+              const int r = __ldg(a.sid + i);
+              if (__ldg(a.roots + r) == i)
+                *reinterpret_cast<float4 *>(a.root_out + (size_t)r * H + unit0 + 4 * c) = v;
+            }
           }
+          continue;
         }
       }
-      tc_mark(a, 3 + 4 * l, kTmaWarp * 32);
-    } else if (warp == kMmaWarp) {
-      // =========================== MMA issuer ==================================
-      if (lane == 0) {
-        const uint32_t idesc = idesc_bf16(kTM, leaf ? C::NLEAF : C::NLVL);
-        const int ncol = leaf ? C::NLEAF : C::NLVL;
+      const int ntiles = (hi - lo + kTM - 1) / kTM;
+      const int nsl = C::nslots(leaf);
+
+      if (warp == kTmaWarp) {
+        // ========================= TMA loads =====================================
+        // per stage: one K-atom (64 bf16) of one slot for the tile's 128 rows.
+        // This CTA (cluster rank cr) fetches rows [cr*RPC, (cr+1)*RPC), multicast
+        // to every CTA of the cluster: TreeLSTM with one 2D tile load (its
+        // operands are contiguous: h is stored in the parent's slot row, x rows
+        // are word- or node-ordered; rows of absent children / padding are not
+        // used by the epilogue); DAG-RNN / TreeFC with tile::gather4 (lane q: 4
+        // rows; absent children / unused rows are row -1 -> zeros).
+        constexpr int CL = C::CL, RPC = kTM / CL;
+        constexpr uint16_t mask = (uint16_t)((1u << CL) - 1);
+        const int cr = gu % CL;
         uint32_t Sg = Sg0;
         for (int t = 0; t < ntiles; t++) {
-          const uint32_t TT = T0 + t, buf = TT & 1;
-          mbar_wait(&bar_tempty[buf], ((TT >> 1) & 1) ^ 1);
-          fence_after();
-          const int tslot = (l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
-          tc_mark(a, tslot + 2, kMmaWarp * 32);
-          uint32_t started = 0;
+          const uint32_t TT = T0 + t;
+          const int ms = TT % kMetaRing;
+          const int i0 = lo + t * kTM;
+          // TreeLSTM operands are contiguous (parent-slot rows / x rows): no
+          // row indices needed, so the loads run ahead of the bookkeeping
+          if (!C::LSTM) mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
+          const TcMeta<J> &m = meta[ms];
           for (int ka = 0; ka < KA; ka++) {
             for (int s = 0; s < nsl; s++) {
               int src, bm, acc;
@@ -681,167 +663,217 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
               const int st = Sg % S;
               const int kst = (int)(Sg - Sg0);
               const int sslot = (l == 1 && kst < 16) ? 64 + 4 * kst : 1 << 30;
-              mbar_wait(&bar_full[st], (Sg / S) & 1);
-              tc_mark(a, sslot + 2, kMmaWarp * 32);
-              fence_after();
-              const uint32_t a0 = smem_u32(sStage + (size_t)st * kStageBytes);
-              const uint32_t b0 = smem_u32((bm ? sB1 : sB0) + (size_t)ka * (bm ? C::B1 : C::B0) * 128);
-              const uint32_t d = tmem + buf * C::BUFC + acc * ncol;
-#pragma unroll
-              for (int kk = 0; kk < 4; kk++) {
-                const uint32_t accum = ((started >> acc) & 1u) | (kk > 0 ? 1u : 0u);
-                mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, accum);
+              mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);  // free in every CTA of the cluster
+              tc_mark(a, sslot + 0, kTmaWarp * 32);
+              if (lane == 0) mbar_arrive_expect_tx(&bar_full[st], kStageBytes);
+              if (C::LSTM) {
+                if (lane == 0) {
+                  // child slot k: rows k*n + i0 + ..; x: word rows (hoisted) or node-order rows
+                  const int row0 = src >= 0 ? src * n + i0 : (hoist ? i0 : i0 - xlo);
+                  tma_tile2d_mc(smem_u32(sStage + (size_t)st * kStageBytes + cr * RPC * 128),
+                                src >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x,
+                                &bar_full[st], ka * 64, row0 + cr * RPC, mask);
+                }
+              } else if (lane < RPC / 4) {
+                const int rb = cr * RPC + 4 * lane;
+                const int4 rv = *reinterpret_cast<const int4 *>((src < 0 ? m.xr : m.ch[src]) + rb);
+                tma_gather4_mc(smem_u32(sStage + (size_t)st * kStageBytes + rb * 128),
+                               src < 0 ? (const void *)&ta.tm_x : (const void *)&ta.tm_h,
+                               &bar_full[st], ka * 64, rv.x, rv.y, rv.z, rv.w, mask);
               }
-              started |= 1u << acc;
-              mma_commit_mc(&bar_empty[st], (uint16_t)((1u << C::CL) - 1));  // frees the slot cluster-wide
-              tc_mark(a, sslot + 3, kMmaWarp * 32);
+              __syncwarp();
+              tc_mark(a, sslot + 1, kTmaWarp * 32);
               Sg++;
             }
           }
-          mma_commit(&bar_tfull[buf]);
-          tc_mark(a, tslot + 3, kMmaWarp * 32);
         }
-        tc_mark(a, 4 + 4 * l, kMmaWarp * 32);
-      }
-      __syncwarp();
-    } else {
-      // =========================== epilogue ====================================
-      // thread = tile row r (TMEM lane) x column half hh: units [u0, u0 + U/2)
-      constexpr int UC = U / 2;
-      const int q4 = warp & 3, hh = warp >> 2;
-      const int r = q4 * 32 + lane, u0 = hh * UC;
-      for (int t = 0; t < ntiles; t++) {
-        const uint32_t TT = T0 + t, buf = TT & 1;
-        const int ms = TT % kMetaRing;
-        mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
-        const TcMeta<J> &m = meta[ms];
-        const bool valid = r < m.cnt;
-        const int i = m.i0 + r, own = m.own[r], root = m.root[r];
-        const int tslot = (l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
-        const uint32_t tb = tmem + ((uint32_t)(q4 * 32) << 16) + buf * C::BUFC + u0;
-        if constexpr (C::LSTM) {
-          static_assert(UC == 16, "TreeLSTM epilogue: 16 units per thread");
-          constexpr int NL = C::NLVL;
-          float c[16], h[16], v[16], w[16];
-          float cp[J][16];  // children's memory cells (prefetched before the MMA wait)
-          int ck[J];
-#pragma unroll
-          for (int k = 0; k < J; k++) {
-            ck[k] = (valid && !leaf) ? m.ch[k][r] : -1;
-            if (ck[k] >= 0) {
-              // L1-allocating loads: a child's row slice (128 B = one line) is
-              // written once, at an earlier level, and read by nobody before,
-              // so no SM can hold a stale copy; the line's 4 (x 2 column
-              // halves) 16-byte pieces then cost one L2 request instead of 8
-              const float *src = cs + (size_t)ck[k] * H + unit0 + u0;
-              ld256(src, cp[k]);
-              ld256(src + 8, cp[k] + 8);
+        tc_mark(a, 3 + 4 * l, kTmaWarp * 32);
+      } else if (warp == kMmaWarp) {
+        // =========================== MMA issuer ==================================
+        if (lane == 0) {
+          const uint32_t idesc = idesc_bf16(kTM, leaf ? C::NLEAF : C::NLVL);
+          const int ncol = leaf ? C::NLEAF : C::NLVL;
+          uint32_t Sg = Sg0;
+          for (int t = 0; t < ntiles; t++) {
+            const uint32_t TT = T0 + t, buf = TT & 1;
+            mbar_wait(&bar_tempty[buf], ((TT >> 1) & 1) ^ 1);
+            fence_after();
+            const int tslot = (l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
+            tc_mark(a, tslot + 2, kMmaWarp * 32);
+            uint32_t started = 0;
+            for (int ka = 0; ka < KA; ka++) {
+              for (int s = 0; s < nsl; s++) {
+                int src, bm, acc;
+                C::slot(leaf, s, src, bm, acc);
+                const int st = Sg % S;
+                const int kst = (int)(Sg - Sg0);
+                const int sslot = (l == 1 && kst < 16) ? 64 + 4 * kst : 1 << 30;
+                mbar_wait(&bar_full[st], (Sg / S) & 1);
+                tc_mark(a, sslot + 2, kMmaWarp * 32);
+                fence_after();
+                const uint32_t a0 = smem_u32(sStage + (size_t)st * kStageBytes);
+                const uint32_t b0 = smem_u32((bm ? sB1 : sB0) + (size_t)ka * (bm ? C::B1 : C::B0) * 128);
+                const uint32_t d = tmem + buf * C::BUFC + acc * ncol;
+  #pragma unroll
+                for (int kk = 0; kk < 4; kk++) {
+                  const uint32_t accum = ((started >> acc) & 1u) | (kk > 0 ? 1u : 0u);
+                  mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, accum);
+                }
+                started |= 1u << acc;
+                mma_commit_mc(&bar_empty[st], (uint16_t)((1u << C::CL) - 1));  // frees the slot cluster-wide
+                tc_mark(a, sslot + 3, kMmaWarp * 32);
+                Sg++;
+              }
             }
+            mma_commit(&bar_tfull[buf]);
+            tc_mark(a, tslot + 3, kMmaWarp * 32);
           }
-          mbar_wait(&bar_tfull[buf], (TT >> 1) & 1);
-          fence_after();
-          tc_mark(a, tslot + 4, 0);
-          const float *bi = s_bias + u0, *bo = bi + U, *bu = bi + 2 * U, *bf = bi + 3 * U;
-          if (leaf) {
-            tmem_ld<16>(tb + 0, v);        // i
-            tmem_ld<16>(tb + 2 * U, w);    // u
-#pragma unroll
-            for (int j = 0; j < 16; j++) c[j] = sigm_mufu(v[j] + bi[j]) * tanh_mufu(w[j] + bu[j]);
-            tmem_ld<16>(tb + U, v);        // o
-#pragma unroll
-            for (int j = 0; j < 16; j++) h[j] = sigm_mufu(v[j] + bo[j]) * tanh_mufu(c[j]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; j++) c[j] = 0.f;
-#pragma unroll
-            for (int k = 0; k < J; k++) {  // sum_k f_k * c_k
-              tmem_ld<16>(tb + k * NL + 3 * U, v);
+          tc_mark(a, 4 + 4 * l, kMmaWarp * 32);
+        }
+        __syncwarp();
+      } else {
+        // =========================== epilogue ====================================
+        // thread = tile row r (TMEM lane) x column half hh: units [u0, u0 + U/2)
+        constexpr int UC = U / 2;
+        const int q4 = warp & 3, hh = warp >> 2;
+        const int r = q4 * 32 + lane, u0 = hh * UC;
+        for (int t = 0; t < ntiles; t++) {
+          const uint32_t TT = T0 + t, buf = TT & 1;
+          const int ms = TT % kMetaRing;
+          mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
+          const TcMeta<J> &m = meta[ms];
+          const bool valid = r < m.cnt;
+          const int i = m.i0 + r, own = m.own[r], root = m.root[r];
+          const int tslot = (l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
+          const uint32_t tb = tmem + ((uint32_t)(q4 * 32) << 16) + buf * C::BUFC + u0;
+          if constexpr (C::LSTM) {
+            static_assert(UC == 16, "TreeLSTM epilogue: 16 units per thread");
+            constexpr int NL = C::NLVL;
+            float c[16], h[16], v[16], w[16];
+            float cp[J][16];  // children's memory cells (prefetched before the MMA wait)
+            int ck[J];
+  #pragma unroll
+            for (int k = 0; k < J; k++) {
+              ck[k] = (valid && !leaf) ? m.ch[k][r] : -1;
               if (ck[k] >= 0) {
-#pragma unroll
-                for (int j = 0; j < 16; j++) c[j] = fmaf(sigm_mufu(v[j] + bf[j]), cp[k][j], c[j]);
+                // L1-allocating loads: a child's row slice (128 B = one line) is
+                // written once, at an earlier level, and read by nobody before,
+                // so no SM can hold a stale copy; the line's 4 (x 2 column
+                // halves) 16-byte pieces then cost one L2 request instead of 8
+                const float *src = cs + (size_t)ck[k] * H + unit0 + u0;
+                ld256(src, cp[k]);
+                ld256(src + 8, cp[k] + 8);
               }
             }
-            tmem_ld<16>(tb + 0, v);        // i = sum_k acc_k[i], u = sum_k acc_k[u]
-            tmem_ld<16>(tb + 2 * U, w);
-#pragma unroll
-            for (int k = 1; k < J; k++) {  // absent children's accumulators are not read
-              tmem_ld<16>(tb + k * NL + 0, h);
-              if (ck[k] >= 0) {
-#pragma unroll
-                for (int j = 0; j < 16; j++) v[j] += h[j];
-              }
-              tmem_ld<16>(tb + k * NL + 2 * U, h);
-              if (ck[k] >= 0) {
-#pragma unroll
-                for (int j = 0; j < 16; j++) w[j] += h[j];
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < 16; j++) c[j] = fmaf(sigm_mufu(v[j] + bi[j]), tanh_mufu(w[j] + bu[j]), c[j]);
-            tmem_ld<16>(tb + U, v);        // o
-#pragma unroll
-            for (int k = 1; k < J; k++) {
-              tmem_ld<16>(tb + k * NL + U, h);
-              if (ck[k] >= 0) {
-#pragma unroll
-                for (int j = 0; j < 16; j++) v[j] += h[j];
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < 16; j++) h[j] = sigm_mufu(v[j] + bo[j]) * tanh_mufu(c[j]);
-          }
-          if (valid) {
-            const bool wordrow = leaf && hoist;  // hoisted leaf cell: row i = word i
-            const size_t ui = (size_t)(wordrow ? i : sbase + i) * H + unit0 + u0;
-            if (wordrow) st_row_bf16<16>(hb + ui, h);  // the word table (copied to slots below)
-            else if (m.ps[r] >= 0) st_row_bf16<16>(a.pb + (size_t)m.ps[r] * H + unit0 + u0, h);
-            st_row<16>(cs + ui, c);
-            if (wordrow) {
-              st_row<16>(a.hf + (size_t)i * H + unit0 + u0, h);
+            mbar_wait(&bar_tfull[buf], (TT >> 1) & 1);
+            fence_after();
+            tc_mark(a, tslot + 4, 0);
+            const float *bi = s_bias + u0, *bo = bi + U, *bu = bi + 2 * U, *bf = bi + 3 * U;
+            if (leaf) {
+              tmem_ld<16>(tb + 0, v);        // i
+              tmem_ld<16>(tb + 2 * U, w);    // u
+  #pragma unroll
+              for (int j = 0; j < 16; j++) c[j] = sigm_mufu(v[j] + bi[j]) * tanh_mufu(w[j] + bu[j]);
+              tmem_ld<16>(tb + U, v);        // o
+  #pragma unroll
+              for (int j = 0; j < 16; j++) h[j] = sigm_mufu(v[j] + bo[j]) * tanh_mufu(c[j]);
             } else {
-              const size_t uo = (size_t)own * H + unit0 + u0;
-              st_row_cs<16>(a.h_out + uo, h);
-              if (a.aux_out) st_row_cs<16>(a.aux_out + uo, c);
-              if (root >= 0) st_row_cs<16>(a.root_out + (size_t)root * H + unit0 + u0, h);
+  #pragma unroll
+              for (int j = 0; j < 16; j++) c[j] = 0.f;
+  #pragma unroll
+              for (int k = 0; k < J; k++) {  // sum_k f_k * c_k
+                tmem_ld<16>(tb + k * NL + 3 * U, v);
+                if (ck[k] >= 0) {
+  #pragma unroll
+                  for (int j = 0; j < 16; j++) c[j] = fmaf(sigm_mufu(v[j] + bf[j]), cp[k][j], c[j]);
+                }
+              }
+              tmem_ld<16>(tb + 0, v);        // i = sum_k acc_k[i], u = sum_k acc_k[u]
+              tmem_ld<16>(tb + 2 * U, w);
+  #pragma unroll
+              for (int k = 1; k < J; k++) {  // absent children's accumulators are not read
+                tmem_ld<16>(tb + k * NL + 0, h);
+                if (ck[k] >= 0) {
+  #pragma unroll
+                  for (int j = 0; j < 16; j++) v[j] += h[j];
+                }
+                tmem_ld<16>(tb + k * NL + 2 * U, h);
+                if (ck[k] >= 0) {
+  #pragma unroll
+                  for (int j = 0; j < 16; j++) w[j] += h[j];
+                }
+              }
+  #pragma unroll
+              for (int j = 0; j < 16; j++) c[j] = fmaf(sigm_mufu(v[j] + bi[j]), tanh_mufu(w[j] + bu[j]), c[j]);
+              tmem_ld<16>(tb + U, v);        // o
+  #pragma unroll
+              for (int k = 1; k < J; k++) {
+                tmem_ld<16>(tb + k * NL + U, h);
+                if (ck[k] >= 0) {
+  #pragma unroll
+                  for (int j = 0; j < 16; j++) v[j] += h[j];
+                }
+              }
+  #pragma unroll
+              for (int j = 0; j < 16; j++) h[j] = sigm_mufu(v[j] + bo[j]) * tanh_mufu(c[j]);
             }
-          }
-        } else {  // DAG-RNN / TreeFC: h = tanh(acc + b)
-          constexpr int CW = UC < 32 ? UC : 32;
-          mbar_wait(&bar_tfull[buf], (TT >> 1) & 1);
-          fence_after();
-          tc_mark(a, tslot + 4, 0);
-#pragma unroll 1
-          for (int q = 0; q < UC / CW; q++) {
-            float v[CW];
-            tmem_ld<CW>(tb + q * CW, v);
-#pragma unroll
-            for (int j = 0; j < CW; j++) v[j] = tanh_mufu(v[j] + s_bias[u0 + q * CW + j]);
             if (valid) {
-              const int uu = unit0 + u0 + q * CW;
-              st_row_cs<CW>(a.h_out + (size_t)own * H + uu, v);
-              st_row_bf16<CW>(hb + (size_t)i * H + uu, v);
-              if (root >= 0) st_row_cs<CW>(a.root_out + (size_t)root * H + uu, v);
+              const bool wordrow = leaf && hoist;  // hoisted leaf cell: row i = word i
+              const size_t ui = (size_t)(wordrow ? i : sbase + i) * H + unit0 + u0;
+              if (wordrow) st_row_bf16<16>(hb + ui, h);  // the word table (copied to slots below)
+              else if (m.ps[r] >= 0) st_row_bf16<16>(a.pb + (size_t)m.ps[r] * H + unit0 + u0, h);
+              st_row<16>(cs + ui, c);
+              if (wordrow) {
+                st_row<16>(a.hf + (size_t)i * H + unit0 + u0, h);
+              } else {
+                const size_t uo = (size_t)own * H + unit0 + u0;
+                st_row_cs<16>(a.h_out + uo, h);
+                if (a.aux_out) st_row_cs<16>(a.aux_out + uo, c);
+                if (root >= 0) st_row_cs<16>(a.root_out + (size_t)root * H + unit0 + u0, h);
+              }
+            }
+          } else {  // DAG-RNN / TreeFC: h = tanh(acc + b)
+            constexpr int CW = UC < 32 ? UC : 32;
+            mbar_wait(&bar_tfull[buf], (TT >> 1) & 1);
+            fence_after();
+            tc_mark(a, tslot + 4, 0);
+  #pragma unroll 1
+            for (int q = 0; q < UC / CW; q++) {
+              float v[CW];
+              tmem_ld<CW>(tb + q * CW, v);
+  #pragma unroll
+              for (int j = 0; j < CW; j++) v[j] = tanh_mufu(v[j] + s_bias[u0 + q * CW + j]);
+              if (valid) {
+                const int uu = unit0 + u0 + q * CW;
+                st_row_cs<CW>(a.h_out + (size_t)own * H + uu, v);
+                st_row_bf16<CW>(hb + (size_t)i * H + uu, v);
+                if (root >= 0) st_row_cs<CW>(a.root_out + (size_t)root * H + uu, v);
+              }
             }
           }
+          fence_before();
+          mbar_arrive(&bar_tempty[buf]);
+          mbar_arrive(&bar_mempty[ms]);
+          tc_mark(a, tslot + 5, 0);
         }
-        fence_before();
-        mbar_arrive(&bar_tempty[buf]);
-        mbar_arrive(&bar_mempty[ms]);
-        tc_mark(a, tslot + 5, 0);
+        tc_mark(a, 5 + 4 * l, 0);
       }
-      tc_mark(a, 5 + 4 * l, 0);
+      T0 += ntiles;
+      Sg0 += (uint32_t)ntiles * KA * nsl;
     }
-    T0 += ntiles;
-    Sg0 += (uint32_t)ntiles * KA * nsl;
+
+    if (hoist && L > 0) {  // leaves' caller outputs (the table is complete since level 1)
+      if (L == 1) level_sync();  // single level: no barrier yet
+      tc_mark(a, 62, 0);
+      leaf_pass(false);
+      tc_mark(a, 63, 0);
+    }
+
   }
+
 
   // ---- hoisted leaves: outputs copied from the word table -------------------
   // (the table was complete at the level-1 barrier; every CTA copies a share)
-  if (hoist && L > 0) {  // leaves' caller outputs (the table is complete since level 1)
-    if (L == 1) grid_sync(a.bar, gridDim.x, epoch);  // single level: no barrier yet
-    leaf_pass(false);
-  }
-
   // ---- teardown -------------------------------------------------------------
   fence_before();
   __syncthreads();
