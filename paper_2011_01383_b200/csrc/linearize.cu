@@ -571,14 +571,14 @@ __global__ void __launch_bounds__(kLinSingleThreads, 1) lin_single_kernel(LinArg
   const int n = a.n, maxc = a.maxc, tid = threadIdx.x, nthr = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5;
   int *ch = sm, *hgt = ch + maxc * n, *indeg = hgt + n, *perm = indeg + n, *inv = perm + n,
-      *lb = inv + n, *ls_s = lb + n, *sid = ls_s + n, *cnt_s = sid + n;
+      *lb = inv + n, *ls_s = lb + n, *sid = ls_s + n, *par = sid + n, *cnt_s = par + n;
 
   lin_mark(a, 0);
   for (int i = tid; i < maxc * n; i += nthr) ch[i] = __ldg(a.ch + i);
   for (int v = tid; v < n; v += nthr) {
     indeg[v] = 0;
     hgt[v] = -1;
-    perm[v] = -1;  // parent pointer (trees/sequences) until a4
+    par[v] = -1;  // parent pointer (trees/sequences)
     sid[v] = INT_MAX;
   }
   if (tid == 0) {
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(kLinSingleThreads, 1) lin_single_kernel(LinArg
   // For trees and sequences the same pass records parent pointers (perm[] is
   // free until a4) and the number of children (inv[]) for the walk-up below.
   const bool tree_like = a.kind != CX_DAG;
-  int *parent = perm, *pending = inv;
+  int *parent = par, *pending = inv;
   for (int v = tid; v < n; v += nthr) {
     bool absent = false;
     int nc = 0;
@@ -835,19 +835,34 @@ __global__ void __launch_bounds__(kLinSingleThreads, 1) lin_single_kernel(LinArg
         a.chn[(long long)k * n + i] = c == -1 ? -1 : inv[c];
       }
     }
-    // a6: structure of every node: root index propagated top-down (minimum
-    // over the roots reaching it), one level per round
-    for (int l = L - 1; l >= 1; l--) {
-      const int b = lb[l], e = b + ls_s[l];
-      for (int i = b + tid; i < e; i += nthr) {
-        const int si = sid[i], v = perm[i];
-        for (int k = 0; k < maxc; k++) {
-          int c = ch[k * n + v];
-          if (c == -1) break;
-          atomicMin(&sid[inv[c]], si);
+    // a6: structure of every node. Trees/sequences: walk up to the root (roots
+    // already hold their index); DAGs: the smallest root index reaching the
+    // node, propagated top-down one level per round.
+    if (tree_like) {
+      __syncthreads();
+      for (int i = tid; i < n; i += nthr) {
+        int v = perm[i], p = parent[v];
+        if (p < 0) continue;
+        while (p >= 0) {
+          v = p;
+          p = parent[v];
         }
+        sid[i] = sid[inv[v]];
       }
       __syncthreads();
+    } else {
+      for (int l = L - 1; l >= 1; l--) {
+        const int b = lb[l], e = b + ls_s[l];
+        for (int i = b + tid; i < e; i += nthr) {
+          const int si = sid[i], v = perm[i];
+          for (int k = 0; k < maxc; k++) {
+            int c = ch[k * n + v];
+            if (c == -1) break;
+            atomicMin(&sid[inv[c]], si);
+          }
+        }
+        __syncthreads();
+      }
     }
     for (int i = tid; i < n; i += nthr) a.sid[i] = sid[i];
   }
@@ -903,7 +918,7 @@ cudaError_t launch_empty(int ctas, int threads, int coop, unsigned long long *t,
 }
 
 size_t lin_single_smem_bytes(int n, int maxc) {
-  return sizeof(int) * ((size_t)(maxc + 7) * n + kLinSmemCnt);
+  return sizeof(int) * ((size_t)(maxc + 8) * n + kLinSmemCnt);
 }
 
 bool lin_use_single(int n, int maxc) {
