@@ -35,6 +35,7 @@ constexpr int kLinThreads = 1024;   // multi-CTA path
 constexpr int kLinSingleThreads = 512;
 constexpr int kSegMin = 256;
 constexpr int kLinTabLevels = 256;  // levels handled by the block-chunked sort (lin_kernel)
+constexpr int kJacNodes = 4, kJacMaxC = 4;  // DAG Jacobi rounds: per-thread register cache
 constexpr size_t kLinMultiSmem = sizeof(int) * (2 + 32) * kLinTabLevels;
 
 // block-wide exclusive scan of one value per thread; returns the block total
@@ -225,26 +226,61 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
       }
       grid_sync(a.bar, G, epoch);
       int fin_prev = __ldcg(&a.misc[3]);
+      // register cache: up to kJacNodes nodes per thread with <= kJacMaxC children
+      const bool cached = (long long)n <= (long long)kJacNodes * nthr && maxc <= kJacMaxC;
+      int cv[kJacNodes], cc[kJacNodes][kJacMaxC];
+      unsigned todo = 0;
+      if (cached) {
+#pragma unroll
+        for (int j = 0; j < kJacNodes; j++) {
+          const int v = tid + j * nthr;
+          cv[j] = v;
+#pragma unroll
+          for (int k = 0; k < kJacMaxC; k++) cc[j][k] = (v < n && k < maxc) ? ch[k * n + v] : -1;
+          if (v < n && __ldcg(&hgt[v]) < 0) todo |= 1u << j;
+        }
+      }
       int r = 0;
       while (fin_prev < n) {
         r++;
         int *round_ptr = &a.misc[r % 3];
         int local = 0;
-        for (int v = tid; v < n; v += nthr) {
-          if (__ldcg(&hgt[v]) >= 0) continue;
-          bool ok = true;
-          for (int k = 0; k < maxc; k++) {
-            int c = ch[k * n + v];
-            if (c == -1) break;
-            int hc = __ldcg(&hgt[c]);
-            if (hc < 0 || hc >= r) {
-              ok = false;
-              break;
+        if (cached) {
+          // this thread's unfinished nodes and their children live in registers:
+          // one round of (independent) height loads per round
+#pragma unroll
+          for (int j = 0; j < kJacNodes; j++) {
+            if (!(todo & (1u << j))) continue;
+            bool ok = true;
+#pragma unroll
+            for (int k = 0; k < kJacMaxC; k++) {
+              if (cc[j][k] < 0) break;
+              const int hc = __ldcg(&hgt[cc[j][k]]);
+              ok = ok && hc >= 0 && hc < r;
+            }
+            if (ok) {
+              hgt[cv[j]] = r;
+              todo &= ~(1u << j);
+              local++;
             }
           }
-          if (ok) {
-            hgt[v] = r;
-            local++;
+        } else {
+          for (int v = tid; v < n; v += nthr) {
+            if (__ldcg(&hgt[v]) >= 0) continue;
+            bool ok = true;
+            for (int k = 0; k < maxc; k++) {
+              int c = ch[k * n + v];
+              if (c == -1) break;
+              int hc = __ldcg(&hgt[c]);
+              if (hc < 0 || hc >= r) {
+                ok = false;
+                break;
+              }
+            }
+            if (ok) {
+              hgt[v] = r;
+              local++;
+            }
           }
         }
         for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
