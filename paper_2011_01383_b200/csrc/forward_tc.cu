@@ -58,13 +58,12 @@ using namespace umma;
 
 constexpr int kTM = 128;                    // tile rows = UMMA M
 // warps 0-7: epilogue (warp w reads TMEM lane quadrant w % 4 = tile rows
-// 32(w%4)..+31, column half w / 4); warp 8: MMA issuer; warp 9: TMA gathers;
-// warps 10-11: tile bookkeeping (warp 10 + m fills the tiles t = m mod 2, so
-// two tiles' dependent index loads are in flight at once)
-constexpr int kEpiWarps = 8, kMmaWarp = 8, kTmaWarp = 9, kMeta0 = 10, kMetaWarps = 2;
-constexpr int kTcThreads = 32 * (kMeta0 + kMetaWarps);  // 384
+// 32(w%4)..+31, column half w / 4); warp 8: MMA issuer; warps 9..: operand
+// feeding (TreeLSTM: 1 TMA warp; DAG-RNN / TreeFC: 4 cp.async warps); last 2
+// warps: tile bookkeeping (warp m of them fills the tiles t = m mod 2, so two
+// tiles' dependent index loads are in flight at once)
+constexpr int kEpiWarps = 8, kMmaWarp = 8, kFeed0 = 9, kMetaWarps = 2;
 constexpr int kEpiThreads = 32 * kEpiWarps;             // 256
-constexpr int kWork = 32 * kMeta0;                      // threads of the working warps (320)
 constexpr int kMaxCluster = 8;                          // portable cluster size
 
 // 128-byte CUtensorMap (opaque; encoded on the host by cuTensorMapEncodeTiled)
@@ -73,9 +72,8 @@ struct alignas(64) TmaDesc {
 };
 // kernel parameter block: tensor maps of the gathered operands + the common args
 struct TcArgs {
-  TmaDesc tm_h;  // gather maps (DAG-RNN, TreeFC): hb state rows, box 64 x 1, 128B swizzle
-  TmaDesc tm_x;  // input rows xb: gather box 64 x 1 (DAG-RNN) | tile box 64 x 128/CL (TreeLSTM)
-  TmaDesc tm_p;  // TreeLSTM: parent-slot rows pb [J*n][H], tile box 64 x 128/CL
+  TmaDesc tm_x;  // TreeLSTM input rows xb, tile box 64 x 128, 128B swizzle
+  TmaDesc tm_p;  // TreeLSTM parent-slot rows pb [J*n][H], same box
   FwdArgs f;
 };
 constexpr int kMetaRing = 4;
@@ -111,7 +109,14 @@ struct TcCfg {
   // CTAs that own different unit slices of the same node tiles form a cluster
   // of CL; each fetches 1/CL of every stage and multicasts it to all
   static constexpr int GU = H / U;
-  static constexpr int CL = LSTM ? 1 : (GU < kMaxCluster ? GU : kMaxCluster);
+  // one CTA per cluster: measured, cluster-multicast gathers were gated by the
+  // slowest CTA and TMA gather4 is issue-bound; TreeLSTM loads contiguous
+  // tiles, the others gather with per-CTA cp.async
+  static constexpr int CL = 1;
+  static constexpr int FEEDW = LSTM ? 1 : 4;             // feeding warps
+  static constexpr int META0 = kFeed0 + FEEDW;           // first bookkeeping warp
+  static constexpr int THREADS = 32 * (META0 + kMetaWarps);
+  static constexpr int WORK = 32 * META0;                // threads of the working warps
   static constexpr size_t bbytes0 = (size_t)B0 * KA * 128, bbytes1 = (size_t)B1 * KA * 128;
   static constexpr size_t static_bytes = sizeof(TcMeta<J>) * kMetaRing + 4 * U * 4 + 64 * 8 + 64;
   static constexpr int S_fit =
@@ -134,6 +139,10 @@ struct TcCfg {
   }
 };
 
+__device__ __forceinline__ void cp16_zfill(uint32_t dst, const void *src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0) : "memory");
+}
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -223,9 +232,11 @@ __device__ __forceinline__ void tc_mark(const FwdArgs &a, int s, int who) {
 }
 
 template <int CELL, int H, int MAXC>
-__global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant__ TcArgs ta) {
+__global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
+    tc_kernel(const __grid_constant__ TcArgs ta) {
   const FwdArgs &a = ta.f;
   using C = TcCfg<CELL, H, MAXC>;
+  constexpr int kMeta0 = C::META0, kWork = C::WORK;
   constexpr int J = C::J, U = C::U, KA = C::KA, S = C::S;
   extern __shared__ unsigned char smem_raw[];
   __shared__ TcMeta<J> meta[kMetaRing];
@@ -250,7 +261,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
 
   // ---- prologue: barriers, TMEM, biases, resident bf16 weights ---------------
   if (tid == 0) {
-    for (int s = 0; s < S; s++) { mbar_init(&bar_full[s], 1); mbar_init(&bar_empty[s], C::CL); }
+    // full: TreeLSTM 1 arrive + TMA bytes; cp.async feeding: one noinc arrival per thread
+    for (int s = 0; s < S; s++) { mbar_init(&bar_full[s], C::LSTM ? 1 : 32 * C::FEEDW); mbar_init(&bar_empty[s], C::CL); }
     for (int b = 0; b < 2; b++) { mbar_init(&bar_tfull[b], 1); mbar_init(&bar_tempty[b], kEpiThreads); }
     for (int m = 0; m < kMetaRing; m++) { mbar_init(&bar_mfull[m], 1); mbar_init(&bar_mempty[m], kEpiThreads); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -635,27 +647,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
       const int ntiles = (hi - lo + kTM - 1) / kTM;
       const int nsl = C::nslots(leaf);
 
-      if (warp == kTmaWarp) {
-        // ========================= TMA loads =====================================
-        // per stage: one K-atom (64 bf16) of one slot for the tile's 128 rows.
-        // This CTA (cluster rank cr) fetches rows [cr*RPC, (cr+1)*RPC), multicast
-        // to every CTA of the cluster: TreeLSTM with one 2D tile load (its
-        // operands are contiguous: h is stored in the parent's slot row, x rows
-        // are word- or node-ordered; rows of absent children / padding are not
-        // used by the epilogue); DAG-RNN / TreeFC with tile::gather4 (lane q: 4
-        // rows; absent children / unused rows are row -1 -> zeros).
-        constexpr int CL = C::CL, RPC = kTM / CL;
-        constexpr uint16_t mask = (uint16_t)((1u << CL) - 1);
-        const int cr = gu % CL;
+      if (C::LSTM && warp == kFeed0) {
+        // ========================= TMA tile loads ================================
+        // per stage: one K-atom (64 bf16) of one slot for the tile's 128 rows
+        // with one 2D tile load: TreeLSTM operands are contiguous (h stored in
+        // the parent's child-slot row, x rows word- or node-ordered); rows of
+        // absent children / padding rows are not read by the epilogue
         uint32_t Sg = Sg0;
         for (int t = 0; t < ntiles; t++) {
-          const uint32_t TT = T0 + t;
-          const int ms = TT % kMetaRing;
           const int i0 = lo + t * kTM;
-          // TreeLSTM operands are contiguous (parent-slot rows / x rows): no
-          // row indices needed, so the loads run ahead of the bookkeeping
-          if (!C::LSTM) mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
-          const TcMeta<J> &m = meta[ms];
           for (int ka = 0; ka < KA; ka++) {
             for (int s = 0; s < nsl; s++) {
               int src, bm, acc;
@@ -663,31 +663,58 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
               const int st = Sg % S;
               const int kst = (int)(Sg - Sg0);
               const int sslot = (l == 1 && kst < 16) ? 64 + 4 * kst : 1 << 30;
-              mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);  // free in every CTA of the cluster
-              tc_mark(a, sslot + 0, kTmaWarp * 32);
-              if (lane == 0) mbar_arrive_expect_tx(&bar_full[st], kStageBytes);
-              if (C::LSTM) {
-                if (lane == 0) {
-                  // child slot k: rows k*n + i0 + ..; x: word rows (hoisted) or node-order rows
-                  const int row0 = src >= 0 ? src * n + i0 : (hoist ? i0 : i0 - xlo);
-                  tma_tile2d_mc(smem_u32(sStage + (size_t)st * kStageBytes + cr * RPC * 128),
-                                src >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x,
-                                &bar_full[st], ka * 64, row0 + cr * RPC, mask);
-                }
-              } else if (lane < RPC / 4) {
-                const int rb = cr * RPC + 4 * lane;
-                const int4 rv = *reinterpret_cast<const int4 *>((src < 0 ? m.xr : m.ch[src]) + rb);
-                tma_gather4_mc(smem_u32(sStage + (size_t)st * kStageBytes + rb * 128),
-                               src < 0 ? (const void *)&ta.tm_x : (const void *)&ta.tm_h,
-                               &bar_full[st], ka * 64, rv.x, rv.y, rv.z, rv.w, mask);
+              mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);
+              tc_mark(a, sslot + 0, kFeed0 * 32);
+              if (lane == 0) {
+                mbar_arrive_expect_tx(&bar_full[st], kStageBytes);
+                // child slot k: rows k*n + i0 + ..; x: word rows (hoisted) or node-order rows
+                const int row0 = src >= 0 ? src * n + i0 : (hoist ? i0 : i0 - xlo);
+                tma_tile2d_mc(smem_u32(sStage + (size_t)st * kStageBytes),
+                              src >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x,
+                              &bar_full[st], ka * 64, row0, (uint16_t)1);
               }
               __syncwarp();
-              tc_mark(a, sslot + 1, kTmaWarp * 32);
+              tc_mark(a, sslot + 1, kFeed0 * 32);
               Sg++;
             }
           }
         }
-        tc_mark(a, 3 + 4 * l, kTmaWarp * 32);
+        tc_mark(a, 3 + 4 * l, kFeed0 * 32);
+      } else if (!C::LSTM && warp >= kFeed0 && warp < kMeta0) {
+        // ========================= cp.async gathers ==============================
+        // per stage: one K-atom of one slot for the tile's 128 rows, 16-byte
+        // cp.async into the swizzled layout (zero-fill: absent child, unused
+        // row); each thread's cp.async.mbarrier.arrive fires when its copies land
+        constexpr int FT = 32 * C::FEEDW, kChunks = kTM * 8 / FT;
+        const int p = tid - kFeed0 * 32;
+        uint32_t Sg = Sg0;
+        for (int t = 0; t < ntiles; t++) {
+          const uint32_t TT = T0 + t;
+          const int ms = TT % kMetaRing;
+          mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
+          const TcMeta<J> &m = meta[ms];
+          for (int ka = 0; ka < KA; ka++) {
+            for (int s = 0; s < nsl; s++) {
+              int src, bm, acc;
+              C::slot(leaf, s, src, bm, acc);
+              const int st = Sg % S;
+              mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);
+              const uint32_t dst0 = smem_u32(sStage + (size_t)st * kStageBytes);
+              const int *rows = src < 0 ? m.xr : m.ch[src];
+              const unsigned short *base = src < 0 ? xb : hb;
+#pragma unroll
+              for (int e = 0; e < kChunks; e++) {
+                const int q = p + FT * e, r = q >> 3, c = q & 7;
+                const int row = rows[r];
+                const bool valid = row >= 0;
+                cp16_zfill(dst0 + sw128_off(r, c), base + (size_t)(valid ? row : 0) * H + ka * 64 + c * 8,
+                           valid);
+              }
+              mbar_arrive_cpasync(&bar_full[st]);
+              Sg++;
+            }
+          }
+        }
       } else if (warp == kMmaWarp) {
         // =========================== MMA issuer ==================================
         if (lane == 0) {
@@ -710,6 +737,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_kernel(const __grid_constant
                 const int sslot = (l == 1 && kst < 16) ? 64 + 4 * kst : 1 << 30;
                 mbar_wait(&bar_full[st], (Sg / S) & 1);
                 tc_mark(a, sslot + 2, kMmaWarp * 32);
+                if (!C::LSTM) fence_proxy_async();  // landed cp.async data (generic proxy) -> tensor core
                 fence_after();
                 const uint32_t a0 = smem_u32(sStage + (size_t)st * kStageBytes);
                 const uint32_t b0 = smem_u32((bm ? sB1 : sB0) + (size_t)ka * (bm ? C::B1 : C::B0) * 128);
@@ -903,7 +931,7 @@ bool tc_plan_one(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   if (max_clusters < 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C::CL * 64);
-    cfg.blockDim = dim3(kTcThreads);
+    cfg.blockDim = dim3(C::THREADS);
     cfg.dynamicSmemBytes = C::dyn_bytes;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -923,7 +951,7 @@ bool tc_plan_one(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   *Gn = min(num_sms / C::GU, max_clusters * C::CL / C::GU);
   if (*Gn < 1) return false;
   p->ctas = *Gn * *Gu;
-  p->threads = kTcThreads;
+  p->threads = C::THREADS;
   p->smem = C::dyn_bytes;
   p->kernel = (const void *)k;
   p->cluster = C::CL;
@@ -1006,16 +1034,9 @@ cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &f, cudaStream_t stream
   std::memset(&ta, 0, sizeof ta);
   ta.f = f;
   const long long xrows = f.xmode ? f.n : f.V;
-  const long long hrows = (long long)f.n + (f.hoist ? f.V : 0);
-  if (!encode_rows(&ta.tm_h, f.hb, f.H, hrows)) return cudaErrorInvalidValue;
-  if (f.pb) {  // TreeLSTM: contiguous operands, multicast tile loads of 128/CL rows
-    const int brows = kTM / plan.cluster;
-    if (!encode_rows(&ta.tm_p, f.pb, f.H, 2LL * f.n, brows)) return cudaErrorInvalidValue;
-    if (!encode_rows(&ta.tm_x, f.xb, f.H, xrows, brows)) return cudaErrorInvalidValue;
-  } else {
-    if (f.cell_has_x ? !encode_rows(&ta.tm_x, f.xb, f.H, xrows) : false) return cudaErrorInvalidValue;
-    if (!f.cell_has_x) ta.tm_x = ta.tm_h;
-    ta.tm_p = ta.tm_h;
+  if (f.pb) {  // TreeLSTM: contiguous operands, 128-row tile loads
+    if (!encode_rows(&ta.tm_p, f.pb, f.H, 2LL * f.n, kTM)) return cudaErrorInvalidValue;
+    if (!encode_rows(&ta.tm_x, f.xb, f.H, xrows, kTM)) return cudaErrorInvalidValue;
   }
   void *params[] = {&ta};
   cudaLaunchConfig_t cfg = {};
