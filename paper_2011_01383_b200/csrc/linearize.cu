@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
   }
   if (tid == 0) {
     a.hdr->err_key = kNoError;
-    a.misc[0] = a.misc[1] = a.misc[2] = a.misc[3] = a.misc[4] = a.misc[5] = 0;
+    a.misc[0] = a.misc[1] = a.misc[2] = a.misc[3] = a.misc[4] = a.misc[5] = a.misc[6] = 0;
   }
   if (threadIdx.x == 0) s_tmp[32] = 0;
   grid_sync(a.bar, G, epoch);
@@ -240,8 +240,62 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
           if (v < n && __ldcg(&hgt[v]) < 0) todo |= 1u << j;
         }
       }
+      // Asynchronous pass (register-cached path): every thread finalises its
+      // nodes as soon as all their children are final (height = 1 + max) --
+      // no barrier per level; the critical path is the longest path's chain
+      // of hand-offs. A thread that sees no progress for ~2^20 polls flags a
+      // stall; the exact rounds below then redo the heights (and report a
+      // cycle if there is one), so correctness never depends on timing.
+      bool async_ok = false;
+      if (cached) {
+        int hmax = 0;
+        bool stalled = false;
+        unsigned spins = 0, todo_a = todo;
+        while (todo_a) {
+          bool prog = false;
+#pragma unroll
+          for (int j = 0; j < kJacNodes; j++) {
+            if (!(todo_a & (1u << j))) continue;
+            int hm = -1;
+            bool ok = true;
+#pragma unroll
+            for (int k = 0; k < kJacMaxC; k++) {
+              if (cc[j][k] < 0) break;
+              const int hc = __ldcg(&hgt[cc[j][k]]);
+              ok = ok && hc >= 0;
+              hm = max(hm, hc);
+            }
+            if (ok) {
+              __stcg(&hgt[cv[j]], hm + 1);
+              hmax = max(hmax, hm + 1);
+              todo_a &= ~(1u << j);
+              prog = true;
+            }
+          }
+          if (prog) {
+            spins = 0;
+          } else {
+            if (++spins > (1u << 20)) {
+              stalled = true;
+              break;
+            }
+            __nanosleep(32);
+          }
+        }
+        for (int o = 16; o; o >>= 1) hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+        if (lane == 0) atomicMax(&a.misc[4], hmax);
+        if (__syncthreads_or(stalled) && threadIdx.x == 0) atomicAdd(&a.misc[6], 1);
+        grid_sync(a.bar, G, epoch);
+        async_ok = __ldcg(&a.misc[6]) == 0;
+        if (!async_ok) {  // redo exactly: internal heights unknown again
+          for (int v = tid; v < n; v += nthr)
+            if (ch[v] != -1) hgt[v] = -1;
+          grid_sync(a.bar, G, epoch);
+        }
+      }
       int r = 0;
-      while (fin_prev < n) {
+      if (async_ok) r = __ldcg(&a.misc[4]);
+      while (!async_ok && fin_prev < n) {
         r++;
         int *round_ptr = &a.misc[r % 3];
         int local = 0;
