@@ -126,6 +126,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
     cp_async_commit();
   }
 
+  // DAG-RNN computation hoisting: the input projection
+  // W_x x + b depends only on the word, so with fewer vocabulary words than
+  // nodes it is computed once per word (st rows [0, V)) and every level --
+  // leaves included, as a level without children -- reads its node's word row
+  const bool dag_hoist = CELL == CX_DAGRNN && a.V < n;
   // ---- words of this CTA's leaf-phase nodes, in the new numbering -----------
   const int lo0 = CELL == CX_DAGRNN ? 0 : first_leaf;
   int plo, phi;
@@ -152,10 +157,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
                             bool leaf) {
     if (tid < cnt) {
       const int i = i0 + tid;
+      if (leaf && dag_hoist) {  // projection rows are word rows
+        r_own = -1;
+        r_word = i;
+        return;
+      }
       r_own = __ldg(a.perm + i);
       if (leaf) {
         r_word = __ldcg(wn + i);
       } else {
+        if (dag_hoist) r_word = __ldcg(wn + i);
 #pragma unroll
         for (int k = 0; k < kMaxC; k++) r_ch[k] = k < a.maxc ? __ldg(a.chn + (size_t)k * n + i) : -1;
       }
@@ -170,6 +181,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
       if (leaf) {
         M.word[tid] = r_word;
       } else {
+        if (dag_hoist) M.word[tid] = r_word;
         bool absent = false;
 #pragma unroll
         for (int k = 0; k < kMaxC; k++) {
@@ -210,7 +222,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
           src_row = M.ch[t][k];
           valid = src_row >= 0;
         } else {
-          src_row = M.node[t];
+          src_row = dag_hoist ? M.word[t] : M.node[t];  // the node's projection row
           valid = true;
         }
         cp_async16_zfill(A + (size_t)r * 32 + 4 * c, st + (size_t)(valid ? src_row : 0) * H + unit0 + 4 * c,
@@ -296,7 +308,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
             const int i = M.node[t];
             const float p = s1[0] + s_bias[u];
             st[(size_t)i * H + unit] = p;
-            if (i >= first_leaf) {
+            if (!dag_hoist && i >= first_leaf) {
               const float hh = tanhf_(p);
               hs[(size_t)i * H + unit] = hh;
               a.h_out[(size_t)M.own[t] * H + unit] = hh;
@@ -323,7 +335,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
   // ---- leaf phase (TreeLSTM leaves / DAG-RNN projections of all nodes) -------
   cp_async_wait_all();
   __syncthreads();
-  pass(plo, phi, true, false);
+  if (dag_hoist) {
+    int wlo, whi;
+    chunk_of(a.V, a.Gn, gn, wlo, whi);
+    pass(wlo, whi, true, false);
+  } else {
+    pass(plo, phi, true, false);
+  }
   __syncthreads();
   // recurrent gates (TreeLSTM: U_iou, U_f; DAG-RNN: U): land during the barrier
   {
@@ -340,7 +358,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
   }
 
   // ---- levels -----------------------------------------------------------------
-  for (int l = 1; l < L; l++) {
+  const int lstart = dag_hoist ? 0 : 1;  // hoisted DAG-RNN: leaves are a level
+  for (int l = lstart; l < L; l++) {
     const int base = __ldg(a.lbeg + l), M = __ldg(a.lsize + l);
     int lo, hi;
     chunk_of(M, a.Gn, gn, lo, hi);
@@ -360,7 +379,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
       store_meta(meta[1], lo + kBT, c1, r_own, r_ch, r_word, false);
     }
     grid_wait(a.bar, gridDim.x, epoch);
-    if (l == 1) {
+    if (l == lstart) {
       cp_async_wait_all();
       __syncthreads();
     }
