@@ -124,7 +124,7 @@ size_t cx_forward_workspace_bytes(const cx_model *m, int32_t n) {
   if (!m) return 0;
   if (m->dtype == CX_BF16)
     return sizeof(cx::GridBar) + cx::tc_workspace_bytes(m->cell, m->hidden, m->vocab, n) + 512;
-  return cx::fwd_workspace_bytes(m->cell, m->hidden, n) + 256;
+  return cx::fwd_workspace_bytes(m->cell, m->hidden, n, m->vocab) + 256;
 }
 
 cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,

@@ -718,7 +718,7 @@ bool mvrnn_plan(int H, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
 bool rw_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
 bool cluster_plan(int cell, int H, int maxc, int n, int roots, FwdPlan *plan, int *Gn, int *Gu);
 bool big_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
-size_t big_workspace_bytes(int H, int n);
+size_t big_workspace_bytes(int cell, int H, int n, int V);
 
 template <int CELL, int MAXC, class C>
 static bool plan_for(int H, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
@@ -787,11 +787,11 @@ bool fwd_plan(int cell, int H, int maxc, int n, int path, int num_sms, FwdPlan *
   return false;
 }
 
-size_t fwd_workspace_bytes(int cell, int H, int n) {
+size_t fwd_workspace_bytes(int cell, int H, int n, int V) {
   size_t N = (size_t)(n > 0 ? n : 1), h = (size_t)H;
   size_t b = sizeof(GridBar);
   if (cell == CX_TREELSTM || cell == CX_DAGRNN) {  // large-batch path: hs, st + words
-    size_t big = big_workspace_bytes(H, (int)N);
+    size_t big = big_workspace_bytes(cell, H, (int)N, V);
     size_t other = 4 * N * h;
     return b + (big > other ? big : other) + 1024;
   }

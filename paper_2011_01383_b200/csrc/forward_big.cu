@@ -98,9 +98,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
   float *const Abase = red + Lay::red;
   auto Xb = [&](int b) { return Xbase + (size_t)b * Lay::x; };
   auto Ab = [&](int b) { return Abase + (size_t)b * Lay::aux; };
-  float *hs = a.pbuf;                       // [n][H] h, new numbering (workspace)
-  float *st = a.pbuf + (size_t)n * H;       // [n][H] c (LSTM) or projections (DAG)
-  int *wn = reinterpret_cast<int *>(a.pbuf + 2 * (size_t)n * H);  // [n] word of new id
+  // TreeLSTM computation hoisting: with fewer
+  // vocabulary words than nodes the leaf cell is evaluated once per word (state
+  // rows [0, V)), internal node i lives at row V + i, parents read leaf
+  // children from their word's row, and the leaves' outputs are copied at the end
+  const bool lstm_hoist = CELL == CX_TREELSTM && a.V < n;
+  const int sbase = lstm_hoist ? a.V : 0;
+  const size_t R = (size_t)n + sbase;       // state rows
+  float *hs = a.pbuf;                       // [R][H] h (workspace)
+  float *st = a.pbuf + R * H;               // [R][H] c (LSTM) or projections (DAG)
+  int *wn = reinterpret_cast<int *>(a.pbuf + 2 * R * H);  // [n] word of new id
   unsigned epoch = 0;
 
   // biases of the owned units
@@ -131,6 +138,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
   // nodes it is computed once per word (st rows [0, V)) and every level --
   // leaves included, as a level without children -- reads its node's word row
   const bool dag_hoist = CELL == CX_DAGRNN && a.V < n;
+  const bool hoist_rows = dag_hoist || lstm_hoist;  // leaf/projection pass over word rows
   // ---- words of this CTA's leaf-phase nodes, in the new numbering -----------
   const int lo0 = CELL == CX_DAGRNN ? 0 : first_leaf;
   int plo, phi;
@@ -149,6 +157,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
     }
   }
   __syncthreads();
+  // hoisted TreeLSTM: level bookkeeping (prefetched before a level barrier
+  // completes) maps leaf children through other CTAs' wn entries
+  if (lstm_hoist) grid_sync(a.bar, gridDim.x, epoch);
 
   // ---------------------------------------------------------------------------
   // One pipelined pass over [lo, hi). `leaf` selects the leaf/projection phase.
@@ -157,7 +168,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
                             bool leaf) {
     if (tid < cnt) {
       const int i = i0 + tid;
-      if (leaf && dag_hoist) {  // projection rows are word rows
+      if (leaf && hoist_rows) {  // leaf / projection pass over word rows
         r_own = -1;
         r_word = i;
         return;
@@ -169,6 +180,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
         if (dag_hoist) r_word = __ldcg(wn + i);
 #pragma unroll
         for (int k = 0; k < kMaxC; k++) r_ch[k] = k < a.maxc ? __ldg(a.chn + (size_t)k * n + i) : -1;
+        if (lstm_hoist) {  // state rows: a leaf child's word row, else V + child
+#pragma unroll
+          for (int k = 0; k < kMaxC; k++)
+            if (r_ch[k] >= 0) r_ch[k] = r_ch[k] >= first_leaf ? __ldcg(wn + r_ch[k]) : sbase + r_ch[k];
+        }
       }
     }
   };
@@ -274,11 +290,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
             const int i = M.node[t];
             float cc = sigmoidf_(s3[0] + s_bias[u]) * tanhf_(s3[2] + s_bias[64 + u]);
             float hh = sigmoidf_(s3[1] + s_bias[32 + u]) * tanhf_(cc);
-            hs[(size_t)i * H + unit] = hh;
+            hs[(size_t)i * H + unit] = hh;  // hoisted: i is the word row
             st[(size_t)i * H + unit] = cc;
-            const size_t o = (size_t)M.own[t] * H + unit;
-            a.h_out[o] = hh;
-            if (a.aux_out) a.aux_out[o] = cc;
+            if (!lstm_hoist) {
+              const size_t o = (size_t)M.own[t] * H + unit;
+              a.h_out[o] = hh;
+              if (a.aux_out) a.aux_out[o] = cc;
+            }
           }
         } else {
           float acc[3 + MAXC][kBT], s5[3 + MAXC];
@@ -292,8 +310,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
             for (int k = 0; k < MAXC; k++)
               if (M.ch[t][k] >= 0) cc += sigmoidf_(s5[3 + k] + bf) * A[(t * NAUX + k) * 32 + u];
             float hh = sigmoidf_(s5[1] + s_bias[32 + u]) * tanhf_(cc);
-            hs[(size_t)i * H + unit] = hh;
-            st[(size_t)i * H + unit] = cc;
+            hs[(size_t)(sbase + i) * H + unit] = hh;
+            st[(size_t)(sbase + i) * H + unit] = cc;
             const size_t o = (size_t)M.own[t] * H + unit;
             a.h_out[o] = hh;
             if (a.aux_out) a.aux_out[o] = cc;
@@ -335,7 +353,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
   // ---- leaf phase (TreeLSTM leaves / DAG-RNN projections of all nodes) -------
   cp_async_wait_all();
   __syncthreads();
-  if (dag_hoist) {
+  if (hoist_rows) {
     int wlo, whi;
     chunk_of(a.V, a.Gn, gn, wlo, whi);
     pass(wlo, whi, true, false);
@@ -387,6 +405,25 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
   }
   cp_async_wait_all();
 
+  // state row of new id i
+  auto srow = [&](int i) -> size_t {
+    return lstm_hoist ? (size_t)(i >= first_leaf ? __ldcg(wn + i) : sbase + i) : (size_t)i;
+  };
+  // ---- hoisted TreeLSTM leaves: caller outputs from their word's row --------
+  if (lstm_hoist) {
+    if (L == 1) grid_sync(a.bar, gridDim.x, epoch);  // else a level barrier ordered it
+    const int q = H / 4;
+    const int gw = (blockIdx.x * blockDim.x + tid) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int j = first_leaf + gw; j < n; j += nw) {  // a warp per leaf row
+      const int own = __ldg(a.perm + j);
+      const size_t w = (size_t)__ldcg(wn + j) * H;
+      for (int c = lane; c < q; c += 32) {
+        __stcs(reinterpret_cast<float4 *>(a.h_out + (size_t)own * H) + c, ldcg4(hs + w + 4 * c));
+        if (a.aux_out)
+          __stcs(reinterpret_cast<float4 *>(a.aux_out + (size_t)own * H) + c, ldcg4(st + w + 4 * c));
+      }
+    }
+  }
   // ---- packed root states (after a final barrier every row of hs is final) ---
   if (a.root_out) {
     grid_sync(a.bar, gridDim.x, epoch);
@@ -394,8 +431,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1) big_kernel(FwdArgs a) {
     const int q = H / 4;
     for (int idx = blockIdx.x * blockDim.x + tid; idx < R * q; idx += gridDim.x * blockDim.x) {
       const int r = idx / q, c = idx - r * q;
-      const int i = __ldg(a.roots + r);
-      *reinterpret_cast<float4 *>(a.root_out + (size_t)r * H + 4 * c) = ldcg4(hs + (size_t)i * H + 4 * c);
+      const size_t i = srow(__ldg(a.roots + r));
+      *reinterpret_cast<float4 *>(a.root_out + (size_t)r * H + 4 * c) = ldcg4(hs + i * H + 4 * c);
     }
   }
   publish_and_exit(a);
@@ -453,8 +490,9 @@ bool big_plan(int cell, int H, int maxc, int num_sms, FwdPlan *p, int *Gn, int *
 }
 
 // workspace floats of the large-batch path: hs, st ([n][H] each) + words [n]
-size_t big_workspace_bytes(int H, int n) {
-  return sizeof(float) * (2 * (size_t)n * H) + sizeof(int) * (size_t)n + 256;
+size_t big_workspace_bytes(int cell, int H, int n, int V) {
+  const size_t R = (size_t)n + (cell == CX_TREELSTM && V < n ? (size_t)V : 0);  // hoisted word rows
+  return sizeof(float) * (2 * R * H) + sizeof(int) * (size_t)n + 256;
 }
 
 }  // namespace cx

@@ -70,7 +70,7 @@ struct FwdPlan {
 constexpr int kRwMaxNodes = 32768;
 bool fwd_plan(int cell, int H, int maxc, int n, int path, int num_sms, FwdPlan *plan, int *Gn,
               int *Gu);
-size_t fwd_workspace_bytes(int cell, int H, int n);
+size_t fwd_workspace_bytes(int cell, int H, int n, int V);
 // bf16 tensor-core path (forward_tc.cu)
 bool tc_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
 int tc_xmode(int n, int V);
