@@ -51,6 +51,8 @@ for l in range(nl):
     print(f"level {l:2d} M={sizes[l]:6d}: start {g(st)}..{f(st)}  prod done max {f(pr)}  "
           f"mma done max {f(mm)}  epi done min {g(ep)} max {f(ep)}")
 
+if (tr[:, 63] > 0).any():
+    print(f"leaf output copy: start max {rel(tr[:,62].max()):8.2f} end max {rel(tr[:,63].max()):8.2f}")
 print("per-tile role timestamps, CTA 0 (us rel. to level start): prod [start,end] mma [start,end] epi [start,end]")
 for l in range(2):
     ls = tr[0, 2 + 4 * l]
