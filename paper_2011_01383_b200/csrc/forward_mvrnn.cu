@@ -93,38 +93,53 @@ __global__ void __launch_bounds__(kT, 1) mvrnn_kernel(FwdArgs a) {
   constexpr int RT = H / 16;    // rows per thread in the A_n product
   constexpr int TPO = kT / H;   // threads per output of W p (k interleaved)
   const int ti = tid >> 4, tj = tid & 15;
+  // node bookkeeping (depends on the linearization only): children, their
+  // input ids, leaf flags and words; the first node of each level is loaded
+  // (and its leaf children's Mw matrices prefetched into L2) while the CTA
+  // waits at the level barrier
+  auto load_node = [&](int i) {
+    int own = __ldg(a.perm + i);
+    s_own = own;
+    int nc = 0;
+    int c[2] = {-1, -1};
+    for (int k = 0; k < a.maxc; k++) {
+      int ck = __ldg(a.chn + (size_t)k * n + i);
+      if (ck < 0) break;
+      if (k < 2) c[k] = ck;
+      nc++;
+    }
+    if (nc != 2) {
+      latch_error(a.hdr, CX_E_ARITY, own);
+      if (c[1] < 0) c[1] = c[0];
+    }
+    for (int k = 0; k < 2; k++) {
+      s_cin[k] = __ldg(a.perm + c[k]);
+      s_isleaf[k] = c[k] >= first_leaf;
+      int w = 0;
+      if (s_isleaf[k]) {
+        w = __ldg(a.words + s_cin[k]);
+        if (w < 0 || w >= a.V) w = 0;  // latched by the leaf phase
+      }
+      s_leafw[k] = w;
+    }
+  };
   for (int l = 1; l < L; l++) {
-    grid_sync(a.bar, G, epoch);
+    grid_arrive(a.bar, epoch);
     const int base = __ldg(a.lbeg + l), M = __ldg(a.lsize + l);
     int lo, hi;
     chunk_of_m(M, G, g, lo, hi);
+    if (tid == 0 && lo < hi) {
+      load_node(base + lo);
+      for (int k = 0; k < 2; k++)
+        if (s_isleaf[k]) {
+          const char *src = reinterpret_cast<const char *>(Mw + s_leafw[k] * HH);
+          for (size_t off = 0; off < HH * sizeof(float); off += 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(src + off));
+        }
+    }
+    grid_wait(a.bar, G, epoch);
     for (int i = base + lo; i < base + hi; i++) {
-      if (tid == 0) {
-        int own = __ldg(a.perm + i);
-        s_own = own;
-        int nc = 0;
-        int c[2] = {-1, -1};
-        for (int k = 0; k < a.maxc; k++) {
-          int ck = __ldg(a.chn + (size_t)k * n + i);
-          if (ck < 0) break;
-          if (k < 2) c[k] = ck;
-          nc++;
-        }
-        if (nc != 2) {
-          latch_error(a.hdr, CX_E_ARITY, own);
-          if (c[1] < 0) c[1] = c[0];
-        }
-        for (int k = 0; k < 2; k++) {
-          s_cin[k] = __ldg(a.perm + c[k]);
-          s_isleaf[k] = c[k] >= first_leaf;
-          int w = 0;
-          if (s_isleaf[k]) {
-            w = __ldg(a.words + s_cin[k]);
-            if (w < 0 || w >= a.V) w = 0;  // latched by the leaf phase
-          }
-          s_leafw[k] = w;
-        }
-      }
+      if (tid == 0 && i != base + lo) load_node(i);
       __syncthreads();
       // gather a, b and [A; B]
       for (int u = tid; u < 2 * H; u += kT) {
