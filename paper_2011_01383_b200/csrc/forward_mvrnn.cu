@@ -42,6 +42,40 @@ struct MvLayout {
   static constexpr size_t bytes = sizeof(float) * (w + wmt + ab + vec);
 };
 
+// CTAs per node at a level of M nodes (G CTAs): 4 or 2 when the level is that
+// small and the per-thread row count RT divides
+template <int RT>
+__device__ __forceinline__ int split_factor(int M, int G) {
+  return (RT >= 4 && 4 * M <= G) ? 4 : (RT >= 2 && 2 * M <= G) ? 2 : 1;
+}
+
+// rows [r0 + ti*RR, +RR) x cols [tj*4H/64 ..) of W_M [A; B] (thread (ti, tj) of 16 x 16)
+template <int RR, int H, int AP>
+__device__ __forceinline__ void mv_rows(const float *WMt, const float *AB, float *dst, int r0, int ti,
+                                        int tj) {
+  constexpr int RC = H / 16;  // columns per thread
+  float acc[RR][RC];
+#pragma unroll
+  for (int r = 0; r < RR; r++)
+#pragma unroll
+    for (int c = 0; c < RC; c++) acc[r][c] = 0.f;
+  for (int k = 0; k < 2 * H; k++) {
+    float w[RR], x[RC];
+#pragma unroll
+    for (int r = 0; r < RR; r++) w[r] = WMt[(size_t)k * H + r0 + ti * RR + r];
+#pragma unroll
+    for (int c = 0; c < RC; c++) x[c] = AB[(size_t)k * AP + tj * RC + c];
+#pragma unroll
+    for (int r = 0; r < RR; r++)
+#pragma unroll
+      for (int c = 0; c < RC; c++) acc[r][c] = fmaf(w[r], x[c], acc[r][c]);
+  }
+#pragma unroll
+  for (int r = 0; r < RR; r++)
+#pragma unroll
+    for (int c = 0; c < RC; c++) dst[(size_t)(r0 + ti * RR + r) * H + tj * RC + c] = acc[r][c];
+}
+
 template <int H>
 __global__ void __launch_bounds__(kT, 1) mvrnn_kernel(FwdArgs a) {
   using Lay = MvLayout<H>;
@@ -91,6 +125,7 @@ __global__ void __launch_bounds__(kT, 1) mvrnn_kernel(FwdArgs a) {
 
   // ---- internal levels ------------------------------------------------------
   constexpr int RT = H / 16;    // rows per thread in the A_n product
+
   constexpr int TPO = kT / H;   // threads per output of W p (k interleaved)
   const int ti = tid >> 4, tj = tid & 15;
   // node bookkeeping (depends on the linearization only): children, their
@@ -126,8 +161,17 @@ __global__ void __launch_bounds__(kT, 1) mvrnn_kernel(FwdArgs a) {
   for (int l = 1; l < L; l++) {
     grid_arrive(a.bar, epoch);
     const int base = __ldg(a.lbeg + l), M = __ldg(a.lsize + l);
+    // a level with at most G/F nodes: F (4 or 2) CTAs per node, each computing
+    // 1/F of the W_M [A; B] rows (the matrix product dominates the node)
+    const int F = split_factor<RT>(M, G);
+    const int half = g % F;  // this CTA's part of the node
     int lo, hi;
-    chunk_of_m(M, G, g, lo, hi);
+    if (F > 1) {
+      lo = min(g / F, M);
+      hi = min(lo + 1, M);
+    } else {
+      chunk_of_m(M, G, g, lo, hi);
+    }
     if (tid == 0 && lo < hi) {
       load_node(base + lo);
       for (int k = 0; k < 2; k++)
@@ -175,32 +219,18 @@ __global__ void __launch_bounds__(kT, 1) mvrnn_kernel(FwdArgs a) {
         for (int k = q; k < 2 * H; k += TPO) s = fmaf(Ws[o * Lay::WP + k], pv[k], s);
 #pragma unroll
         for (int d = TPO / 2; d >= 1; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
-        if (q == 0) a.h_out[(size_t)s_own * H + o] = tanhf_(s + __ldg(beta + o));
+        if (q == 0 && half == 0) a.h_out[(size_t)s_own * H + o] = tanhf_(s + __ldg(beta + o));
       }
       // A_n = W_M [A; B]: thread (ti, tj) computes rows ti*RT.., cols tj*RT..
-      {
-        float acc[RT][RT];
-#pragma unroll
-        for (int r = 0; r < RT; r++)
-#pragma unroll
-          for (int c = 0; c < RT; c++) acc[r][c] = 0.f;
-        for (int k = 0; k < 2 * H; k++) {
-          float w[RT], x[RT];
-#pragma unroll
-          for (int r = 0; r < RT; r++) w[r] = WMt[(size_t)k * H + ti * RT + r];
-#pragma unroll
-          for (int c = 0; c < RT; c++) x[c] = AB[(size_t)k * Lay::AP + tj * RT + c];
-#pragma unroll
-          for (int r = 0; r < RT; r++)
-#pragma unroll
-            for (int c = 0; c < RT; c++) acc[r][c] = fmaf(w[r], x[c], acc[r][c]);
-        }
-        float *dst = a.Abuf + (size_t)s_own * HH;
-#pragma unroll
-        for (int r = 0; r < RT; r++)
-#pragma unroll
-          for (int c = 0; c < RT; c++) dst[(size_t)(ti * RT + r) * H + tj * RT + c] = acc[r][c];
+      // (split: this CTA's half of the rows, RT/2 per thread)
+      float *An = a.Abuf + (size_t)s_own * HH;
+      if constexpr (RT >= 4) {
+        if (F == 4) mv_rows<RT / 4, H, Lay::AP>(WMt, AB, An, half * (H / 4), ti, tj);
       }
+      if constexpr (RT >= 2) {
+        if (F == 2) mv_rows<RT / 2, H, Lay::AP>(WMt, AB, An, half * (H / 2), ti, tj);
+      }
+      if (F == 1) mv_rows<RT, H, Lay::AP>(WMt, AB, An, 0, ti, tj);
       __syncthreads();
     }
   }
@@ -211,8 +241,14 @@ __global__ void __launch_bounds__(kT, 1) mvrnn_kernel(FwdArgs a) {
     for (int r = 0; r < R; r++) {
       int i = __ldg(a.roots + r);
       int lvl = __ldg(a.hnew + i);
-      int own = lvl == 0 ? owner_of_m(i - first_leaf, n - first_leaf, G)
-                         : owner_of_m(i - __ldg(a.lbeg + lvl), __ldg(a.lsize + lvl), G);
+      int own;
+      if (lvl == 0) {
+        own = owner_of_m(i - first_leaf, n - first_leaf, G);
+      } else {
+        const int Ml = __ldg(a.lsize + lvl), pos = i - __ldg(a.lbeg + lvl);
+        const int F = split_factor<H / 16>(Ml, G);
+        own = F > 1 ? F * pos : owner_of_m(pos, Ml, G);  // split levels: part 0 wrote h
+      }
       if (own != g) continue;
       int src = __ldg(a.perm + i);
       for (int u = tid; u < H; u += kT)
