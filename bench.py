@@ -1,8 +1,10 @@
 #!/usr/bin/env python
 """Benchmark of the Cortex hot path on B200.
 
-One step = cx_linearize + cx_forward over one batch of synthetic structures
-(the whole hot path, reading Q17 of DESIGN.md). Default workload =
+One step = cx_linearize_forward over one batch of synthetic structures (the
+whole hot path, reading Q17 of DESIGN.md): the linearizer fused into the
+forward kernel, one launch, where the batch allows it, else
+cx_linearize + cx_forward. Default workload =
 BASELINE.json configs[1]: TreeLSTM (child-sum, binary SST-shaped trees),
 batch 10 per GPU, H = 256, fp32. Multi-GPU: one process per GPU (torchrun),
 each rank evaluates its own independent batch (weak scaling, no data-path
@@ -14,6 +16,7 @@ collective); timing is the max over ranks.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -318,9 +321,23 @@ def run_gpu(args, rank, world, local_rank):
     def fwd_call():
         cx.forward(cell, H, weights, emb, words, lin, dtype=dtype, h_out=h, root_out=roots)
 
+    # one step = cx_linearize_forward: ONE launch (linearizer fused into the
+    # forward kernel) where it applies, else the two kernels
+    fused = cx.fused_applies(cell, H, n, ch_np.shape[0], V, dtype)
+    ws_lf = torch.zeros(cx.lib().cx_linearize_forward_workspace_bytes(
+        ctypes.byref(cx._cx._model(cell, H, V, dtype)), n, ch_np.shape[0]), dtype=torch.uint8,
+        device=dev)
+
     def step():
+        cx.linearize_forward(children, inp["kind"], cell, H, weights, emb, words, dtype=dtype,
+                             out=lin, h_out=h, root_out=roots, workspace=ws_lf)
+
+    def step2():
         lin_call()
         fwd_call()
+
+    step()
+    cx.check(lin)
 
     def capture(fn):
         g = torch.cuda.CUDAGraph()
@@ -330,6 +347,7 @@ def run_gpu(args, rank, world, local_rank):
 
     # one step = one CUDA graph (2 kernel nodes); breakdown graphs for each call
     g_step, g_lin, g_fwd = capture(step), capture(lin_call), capture(fwd_call)
+    g_step2 = capture(step2)
     stream = torch.cuda.current_stream()
 
     # L2 flush buffer (> 126 MB L2): written between timed steps, outside the events
@@ -378,6 +396,15 @@ def run_gpu(args, rank, world, local_rank):
     torch.cuda.synchronize()
     lin_ms = [evb[k][0].elapsed_time(evb[k][1]) for k in range(nb)]
     fwd_ms = [evb[k][1].elapsed_time(evb[k][2]) for k in range(nb)]
+    # the two-launch step (cx_linearize + cx_forward graph), for comparison
+    ev2 = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nb)]
+    for k in range(nb):
+        ev2[k][0].record(stream)
+        g_step2.replay()
+        ev2[k][1].record(stream)
+        flush.fill_(1.0)
+    torch.cuda.synchronize()
+    two_ms = [ev2[k][0].elapsed_time(ev2[k][1]) for k in range(nb)]
 
     # eager (no graph) latency through the Python API, for reference
     eager_ms = []
@@ -420,8 +447,8 @@ def run_gpu(args, rank, world, local_rank):
     for _ in range(3):
         ch_dev.copy_(ch_host, non_blocking=True)
         w_dev.copy_(w_host, non_blocking=True)
-        cx.linearize(ch_dev, inp["kind"], out=lin)
-        cx.forward(cell, H, weights, emb, w_dev, lin, dtype=dtype, h_out=h, root_out=roots)
+        cx.linearize_forward(ch_dev, inp["kind"], cell, H, weights, emb, w_dev, dtype=dtype,
+                             out=lin, h_out=h, root_out=roots, workspace=ws_lf)
         roots_host.copy_(roots, non_blocking=True)
     torch.cuda.synchronize()
     if world > 1:
@@ -433,8 +460,8 @@ def run_gpu(args, rank, world, local_rank):
         s0.record(stream)
         ch_dev.copy_(ch_host, non_blocking=True)
         w_dev.copy_(w_host, non_blocking=True)
-        cx.linearize(ch_dev, inp["kind"], out=lin)
-        cx.forward(cell, H, weights, emb, w_dev, lin, dtype=dtype, h_out=h, root_out=roots)
+        cx.linearize_forward(ch_dev, inp["kind"], cell, H, weights, emb, w_dev, dtype=dtype,
+                             out=lin, h_out=h, root_out=roots, workspace=ws_lf)
         roots_host.copy_(roots, non_blocking=True)
         s1.record(stream)
         s1.synchronize()  # the host reads the step's result
@@ -456,7 +483,8 @@ def run_gpu(args, rank, world, local_rank):
 
     if rank != 0:
         return
-    fwd_mean = sum(fwd_ms) / len(fwd_ms)
+    # the dominant kernel: the fused kernel (= the whole step) or cx_forward's
+    fwd_mean = sum(step_ms) / len(step_ms) if fused else sum(fwd_ms) / len(fwd_ms)
     flops, alg_bytes = algorithmic_work(cell, H, n, n_leaves, n - n_leaves, R, ch_np.shape[0])
     achieved = flops / (fwd_mean / 1e3) / 1e12
     info = cx.launch_info(cell, H, V, dtype)
@@ -482,7 +510,8 @@ def run_gpu(args, rank, world, local_rank):
     else:
         roofline = {"bound": "alu", "achieved": achieved, "peak": FMA_PEAK_TFLOPS,
                     "unit": "TFLOP/s", "frac": achieved / FMA_PEAK_TFLOPS, "traffic": traffic,
-                    "kernel": "fwd_kernel (cx_forward)", "flops_per_launch": flops,
+                    "kernel": "ck_kernel<fused> (cx_linearize_forward, one launch per step)"
+                              if fused else "fwd_kernel (cx_forward)", "flops_per_launch": flops,
                     "alg_bytes_per_launch": alg_bytes,
                     "note": "fp32 FMA peak = 148 SM x 128 lanes x 2 x 1.965 GHz; the step is "
                             "critical-path (levels x barrier) bound, see DESIGN.md"}
@@ -501,8 +530,12 @@ def run_gpu(args, rank, world, local_rank):
         "linearize_us": statistics.median(lin_ms) * 1e3,
         "forward_us": statistics.median(fwd_ms) * 1e3,
         "eager_latency_us": statistics.median(eager_ms) * 1e3,
-        "timing": "CUDA graph replay of linearize+forward per step, events on the launch stream",
-        "gpu_launches": 2 * args.steps,
+        "two_launch_latency_us": statistics.median(two_ms) * 1e3,
+        "fused": fused,
+        "timing": "CUDA graph replay of cx_linearize_forward per step (one fused launch where "
+                  "it applies), events on the launch stream; linearize_us / forward_us / "
+                  "two_launch_latency_us time the separate cx_linearize and cx_forward launches",
+        "gpu_launches": (1 if fused else 2) * args.steps,
         "allgather_roots_us": allgather_us,
         "launch": info,
         "roofline": roofline,

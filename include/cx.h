@@ -155,6 +155,36 @@ cx_status cx_forward(const cx_model *model, const cx_weights *weights, const flo
                      float *aux_out, float *root_out, void *workspace, size_t workspace_bytes,
                      void *stream);
 
+/* Bytes of device workspace cx_linearize_forward needs (same zero-fill
+ * contract as the other workspaces). */
+size_t cx_linearize_forward_workspace_bytes(const cx_model *model, int32_t n, int32_t max_children);
+
+/* cx_linearize followed by cx_forward in ONE launch where the batch allows it
+ * (the paper's single fused kernel, T6 "#Kernel calls 1"
+ * P:1441, with the linearizer of §4.2 P:1060-1085 moved from the host into the
+ * kernel's prologue). Results are exactly those of the two calls in sequence
+ * on `stream`: every output of cx_linearize in `out` (header included) and
+ * every output of cx_forward.
+ *   children, n, max_children, kind   as cx_linearize.
+ *   model, weights, emb, word_ids, h_out, aux_out, root_out   as cx_forward.
+ *   workspace  >= cx_linearize_forward_workspace_bytes(model, n, max_children),
+ *              zero-filled before first use, reusable.
+ * One launch: fp32 TreeLSTM / DAG-RNN with H in {64, 128, 256}, max_children
+ * <= 4 and a batch small enough for the latency (cluster) kernel (n <= ~600 at
+ * H = 256): every CTA linearizes the batch in its shared memory (CTA 0 also
+ * writes `out`) while it loads its register weights and prefetches the
+ * batch's embedding rows into L2. Otherwise the two kernels are launched back
+ * to back (no host synchronisation either way). Argument errors return
+ * synchronously; data errors are latched in out->header exactly as by the
+ * two calls (CX_E_CHILD_* / KIND / CYCLE from the linearization take
+ * precedence: the forward part does not run). CX_FUSED=0 in the environment
+ * forces the two-launch path (for measurement). */
+cx_status cx_linearize_forward(const int32_t *children, int32_t n, int32_t max_children,
+                               cx_kind kind, const cx_model *model, const cx_weights *weights,
+                               const float *emb, const int32_t *word_ids, cx_linearization *out,
+                               float *h_out, float *aux_out, float *root_out, void *workspace,
+                               size_t workspace_bytes, void *stream);
+
 /* Synchronise `stream` and return the latched status of lin->header;
  * *bad_node (host, may be NULL) receives the offending input id or -1. */
 cx_status cx_status_sync(const cx_linearization *lin, int32_t *bad_node, void *stream);

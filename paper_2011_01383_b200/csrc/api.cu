@@ -59,30 +59,14 @@ bool weights_ok(int cell, const cx_weights *w) {
 
 }  // namespace
 
-extern "C" {
-
-size_t cx_linearize_workspace_bytes(int32_t n, int32_t max_children) {
-  (void)max_children;
-  return cx::lin_workspace_bytes(n < 0 ? 0 : n);
-}
-
-cx_status cx_linearize(const int32_t *children, int32_t n, int32_t max_children, cx_kind kind,
-                       void *workspace, size_t workspace_bytes, cx_linearization *out,
-                       void *stream) {
-  if (!out || n < 0 || max_children < 1 || (n > 0 && !children)) return CX_E_ARG;
-  if (kind != CX_SEQUENCE && kind != CX_TREE && kind != CX_DAG) return CX_E_ARG;
-  if (kind == CX_SEQUENCE && max_children != 1) return CX_E_ARG;
-  if (!out->header || (n > 0 && (!out->perm || !out->inv || !out->children || !out->height ||
-                                 !out->level_begin || !out->level_size || !out->roots ||
-                                 !out->structure)))
-    return CX_E_ARG;
-  if (!workspace || workspace_bytes < cx::lin_workspace_bytes(n)) return CX_E_WORKSPACE;
+namespace {
+void lin_args(const int32_t *children, int32_t n, int32_t max_children, cx_kind kind,
+              void *workspace, cx_linearization *out, cx::LinArgs *ap) {
+  cx::LinArgs &a = *ap;
   out->n = n;
   out->max_children = max_children;
   out->kind = kind;
-
   char *p = align_up(static_cast<char *>(workspace), 128);
-  cx::LinArgs a;
   a.bar = reinterpret_cast<cx::GridBar *>(p);
   p += sizeof(cx::GridBar);
   a.misc = reinterpret_cast<int32_t *>(p);
@@ -110,36 +94,17 @@ cx_status cx_linearize(const int32_t *children, int32_t n, int32_t max_children,
     std::lock_guard<std::mutex> lk(g_mu);
     a.trace = g_lin_trace;
   }
-  int sms;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    sms = num_sms_current();
-  }
-  if (sms <= 0) return CX_E_CUDA;
-  cudaError_t e = cx::launch_linearize(a, sms, static_cast<cudaStream_t>(stream));
-  return e == cudaSuccess ? CX_OK : CX_E_CUDA;
 }
+}  // namespace
 
-size_t cx_forward_workspace_bytes(const cx_model *m, int32_t n) {
-  if (!m) return 0;
-  if (m->dtype == CX_BF16)
-    return sizeof(cx::GridBar) + cx::tc_workspace_bytes(m->cell, m->hidden, m->vocab, n) + 512;
-  return cx::fwd_workspace_bytes(m->cell, m->hidden, n, m->vocab) + 256;
-}
-
-cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
-                     const int32_t *word_ids, const cx_linearization *lin, float *h_out,
-                     float *aux_out, float *root_out, void *workspace, size_t workspace_bytes,
-                     void *stream) {
-  if (!m || !w || !lin || !lin->header) return CX_E_ARG;
-  if (m->cell < CX_TREERNN || m->cell > CX_DAGRNN) return CX_E_ARG;
-  if (m->dtype != CX_F32 && m->dtype != CX_BF16) return CX_E_ARG;
-  if (m->hidden <= 0 || m->vocab <= 0) return CX_E_ARG;
+namespace {
+// cx_forward after argument checks; `fused` (non-NULL) = linearizer arguments
+// for the fused launch (its plan is required to exist).
+cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
+                       const int32_t *word_ids, const cx_linearization *lin, float *h_out,
+                       float *aux_out, float *root_out, void *workspace, const cx::LinArgs *fused,
+                       void *stream) {
   const int n = lin->n;
-  if (n < 0) return CX_E_ARG;
-  if (n > 0 && (!emb || !word_ids || !h_out || !weights_ok(m->cell, w))) return CX_E_ARG;
-  if (!workspace || workspace_bytes < cx_forward_workspace_bytes(m, n)) return CX_E_WORKSPACE;
-  if (n == 0) return CX_OK;
 
   cx::FwdPlan plan;
   int Gn = 0, Gu = 0;
@@ -147,7 +112,8 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
     std::lock_guard<std::mutex> lk(g_mu);
     int sms = num_sms_current();
     if (sms <= 0) return CX_E_CUDA;
-    const bool ok = m->dtype == CX_BF16
+    const bool ok = fused ? cx::fused_plan(m->cell, m->hidden, lin->max_children, n, &plan, &Gn, &Gu)
+                    : m->dtype == CX_BF16
                         ? cx::tc_plan(m->cell, m->hidden, lin->max_children, sms, &plan, &Gn, &Gu)
                         : cx::fwd_plan(m->cell, m->hidden, lin->max_children, n, forward_path(),
                                        sms, &plan, &Gn, &Gu);
@@ -219,9 +185,120 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
     a.trace = g_trace;
     a.trace_slots = g_trace_slots;
   }
+  if (fused) a.lin = *fused;
   cudaError_t e = plan.tc ? cx::tc_launch(plan, a, static_cast<cudaStream_t>(stream))
                           : cx::fwd_launch(plan, a, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? CX_OK : CX_E_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t cx_linearize_workspace_bytes(int32_t n, int32_t max_children) {
+  (void)max_children;
+  return cx::lin_workspace_bytes(n < 0 ? 0 : n);
+}
+
+cx_status cx_linearize(const int32_t *children, int32_t n, int32_t max_children, cx_kind kind,
+                       void *workspace, size_t workspace_bytes, cx_linearization *out,
+                       void *stream) {
+  if (!out || n < 0 || max_children < 1 || (n > 0 && !children)) return CX_E_ARG;
+  if (kind != CX_SEQUENCE && kind != CX_TREE && kind != CX_DAG) return CX_E_ARG;
+  if (kind == CX_SEQUENCE && max_children != 1) return CX_E_ARG;
+  if (!out->header || (n > 0 && (!out->perm || !out->inv || !out->children || !out->height ||
+                                 !out->level_begin || !out->level_size || !out->roots ||
+                                 !out->structure)))
+    return CX_E_ARG;
+  if (!workspace || workspace_bytes < cx::lin_workspace_bytes(n)) return CX_E_WORKSPACE;
+  cx::LinArgs a;
+  lin_args(children, n, max_children, kind, workspace, out, &a);
+  int sms;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    sms = num_sms_current();
+  }
+  if (sms <= 0) return CX_E_CUDA;
+  cudaError_t e = cx::launch_linearize(a, sms, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? CX_OK : CX_E_CUDA;
+}
+
+
+size_t cx_forward_workspace_bytes(const cx_model *m, int32_t n) {
+  if (!m) return 0;
+  if (m->dtype == CX_BF16)
+    return sizeof(cx::GridBar) + cx::tc_workspace_bytes(m->cell, m->hidden, m->vocab, n) + 512;
+  return cx::fwd_workspace_bytes(m->cell, m->hidden, n, m->vocab) + 256;
+}
+
+cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
+                     const int32_t *word_ids, const cx_linearization *lin, float *h_out,
+                     float *aux_out, float *root_out, void *workspace, size_t workspace_bytes,
+                     void *stream) {
+  if (!m || !w || !lin || !lin->header) return CX_E_ARG;
+  if (m->cell < CX_TREERNN || m->cell > CX_DAGRNN) return CX_E_ARG;
+  if (m->dtype != CX_F32 && m->dtype != CX_BF16) return CX_E_ARG;
+  if (m->hidden <= 0 || m->vocab <= 0) return CX_E_ARG;
+  const int n = lin->n;
+  if (n < 0) return CX_E_ARG;
+  if (n > 0 && (!emb || !word_ids || !h_out || !weights_ok(m->cell, w))) return CX_E_ARG;
+  if (!workspace || workspace_bytes < cx_forward_workspace_bytes(m, n)) return CX_E_WORKSPACE;
+  if (n == 0) return CX_OK;
+  return forward_impl(m, w, emb, word_ids, lin, h_out, aux_out, root_out, workspace, nullptr, stream);
+}
+
+
+static size_t lin_part_bytes(int32_t n) { return (cx::lin_workspace_bytes(n < 0 ? 0 : n) + 255) / 256 * 256; }
+
+size_t cx_linearize_forward_workspace_bytes(const cx_model *m, int32_t n, int32_t max_children) {
+  if (!m) return 0;
+  (void)max_children;
+  return lin_part_bytes(n) + cx_forward_workspace_bytes(m, n) + 256;
+}
+
+cx_status cx_linearize_forward(const int32_t *children, int32_t n, int32_t max_children,
+                               cx_kind kind, const cx_model *m, const cx_weights *w,
+                               const float *emb, const int32_t *word_ids, cx_linearization *out,
+                               float *h_out, float *aux_out, float *root_out, void *workspace,
+                               size_t workspace_bytes, void *stream) {
+  if (!m || !w || !out) return CX_E_ARG;
+  if (!workspace || workspace_bytes < cx_linearize_forward_workspace_bytes(m, n, max_children))
+    return CX_E_WORKSPACE;
+  char *lws = align_up(static_cast<char *>(workspace), 256);
+  char *fws = lws + lin_part_bytes(n);
+  const size_t fbytes = cx_forward_workspace_bytes(m, n);
+  // the fused kernel: fp32 cluster path, one launch
+  const char *env = std::getenv("CX_FUSED");
+  const bool try_fused = !(env && env[0] == '0') && m->dtype == CX_F32 && n > 0 &&
+                         (forward_path() == 0 || forward_path() == 3);
+  if (try_fused) {
+    // the same argument checks as the two calls
+    if (n < 0 || max_children < 1 || !children) return CX_E_ARG;
+    if (kind != CX_SEQUENCE && kind != CX_TREE && kind != CX_DAG) return CX_E_ARG;
+    if (kind == CX_SEQUENCE && max_children != 1) return CX_E_ARG;
+    if (!out->header || !out->perm || !out->inv || !out->children || !out->height ||
+        !out->level_begin || !out->level_size || !out->roots || !out->structure)
+      return CX_E_ARG;
+    if (m->cell < CX_TREERNN || m->cell > CX_DAGRNN || m->hidden <= 0 || m->vocab <= 0)
+      return CX_E_ARG;
+    if (!emb || !word_ids || !h_out || !weights_ok(m->cell, w)) return CX_E_ARG;
+    cx::FwdPlan plan;
+    int Gn = 0, Gu = 0;
+    bool ok;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      ok = cx::fused_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu);
+    }
+    if (ok) {
+      cx::LinArgs la;
+      lin_args(children, n, max_children, kind, lws, out, &la);
+      la.trace = nullptr;
+      return forward_impl(m, w, emb, word_ids, out, h_out, aux_out, root_out, fws, &la, stream);
+    }
+  }
+  cx_status st = cx_linearize(children, n, max_children, kind, lws, lin_part_bytes(n), out, stream);
+  if (st != CX_OK) return st;
+  return cx_forward(m, w, emb, word_ids, out, h_out, aux_out, root_out, fws, fbytes, stream);
 }
 
 cx_status cx_status_sync(const cx_linearization *lin, int32_t *bad_node, void *stream) {
@@ -249,6 +326,18 @@ cx_status cx_debug_set_lin_trace(unsigned long long *buf) {
   std::lock_guard<std::mutex> lk(g_mu);
   g_lin_trace = buf;
   return CX_OK;
+}
+
+// Debug only (reporting): 1 if cx_linearize_forward would use the fused
+// single launch for this model and batch shape, else 0.
+int32_t cx_debug_fused_applies(const cx_model *m, int32_t n, int32_t max_children) {
+  if (!m || m->dtype != CX_F32 || n <= 0) return 0;
+  const char *env = std::getenv("CX_FUSED");
+  if ((env && env[0] == '0') || !(forward_path() == 0 || forward_path() == 3)) return 0;
+  cx::FwdPlan plan;
+  int Gn, Gu;
+  std::lock_guard<std::mutex> lk(g_mu);
+  return cx::fused_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu) ? 1 : 0;
 }
 
 // Debug only: an empty kernel launch (measures launch overhead).

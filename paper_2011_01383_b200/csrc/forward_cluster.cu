@@ -24,6 +24,7 @@
 #include <climits>
 #include <type_traits>
 
+#include "lin_single.cuh"
 #include "rw_engine.cuh"
 
 namespace cg = cooperative_groups;
@@ -70,6 +71,14 @@ struct CLayout {
 
 // Max nodes the cluster path takes (per-node slices live in shared memory).
 constexpr int kClusterMaxN = 768;
+// Fused linearize + forward: count-table entries of the
+// in-kernel single-CTA linearizer, and its extra shared memory (ints): the
+// linearizer's arrays stand in for the prologue's perm/label/level arrays,
+// plus the remapped children, the cluster's level lists and their offsets.
+constexpr int kFusedCnt = 2048;
+inline size_t fused_extra_ints(int n, int maxc) {
+  return lin_sm_ints(n, maxc, kFusedCnt) + (size_t)maxc * n + 3 * (size_t)n + 64;
+}
 
 struct CS {  // shared-memory carve of one CTA
   float *X, *red, *red2, *cv, *hsl, *aux;
@@ -106,7 +115,14 @@ __device__ __forceinline__ void pull_rows(cg::cluster_group &cl, const CS &s, in
 }
 
 // ---------------------------------------------------------------------------
-template <int CELL, int H, int MAXC>
+// FUSED: the kernel linearizes the batch itself (every CTA redundantly runs
+// the single-CTA linearizer of lin_single.cuh on its own shared memory, so no
+// grid-wide synchronisation is needed; CTA 0 also writes the cx_linearization
+// outputs), overlapping it with the register weight loads and an L2 prefetch
+// of every node's embedding row. Forward data errors are latched into a
+// workspace word and merged into the header by the last CTA out, after CTA 0
+// has written it.
+template <int CELL, int H, int MAXC, bool FUSED>
 __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   using Cfg = CCfg<CELL, MAXC>;
   using Lay = CLayout<CELL, H, MAXC>;
@@ -152,9 +168,33 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   } else {
     if (tid < kCUnits) s_bias[tid] = __ldg(a.w[2] + unit0 + tid);
   }
-  griddep_wait();
-  if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
-  const int L = a.hdr->num_levels, first_leaf = a.hdr->first_leaf, n = a.n, R = a.hdr->num_roots;
+  unsigned long long *ferr = reinterpret_cast<unsigned long long *>(&a.bar->pad[0]);
+  int L, first_leaf, R;
+  const int n = a.n;
+  LinSm ls;
+  int *fint = nullptr;
+  if constexpr (FUSED) {
+    fint = reinterpret_cast<int *>(smem + Lay::x_floats + Lay::red_floats + Lay::red2_floats +
+                                   Lay::cv_floats + 2 * (size_t)kCUnits * n);
+    LinPrefetch pf{a.words, a.emb, H, a.V};
+    const LinOut lo = lin_single_body(a.lin, fint, kFusedCnt, blockIdx.x == 0,
+                                      fint + lin_sm_ints(n, maxc, kFusedCnt), pf);
+    trace_mark(a, 20);
+    if (!lo.ok) {
+      fused_exit(a, ferr);
+      return;
+    }
+    ls = lin_carve(fint, n, maxc);
+    L = lo.L;
+    first_leaf = lo.first_leaf;
+    R = lo.num_roots;
+  } else {
+    griddep_wait();
+    if (*reinterpret_cast<volatile int *>(&a.hdr->status) != CX_OK) return;
+    L = a.hdr->num_levels;
+    first_leaf = a.hdr->first_leaf;
+    R = a.hdr->num_roots;
+  }
 
   CS s;
   s.X = smem;
@@ -163,14 +203,25 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   s.cv = s.red2 + Lay::red2_floats;
   s.hsl = s.cv + Lay::cv_floats;
   s.aux = s.hsl + (size_t)kCUnits * n;
-  s.perm = reinterpret_cast<int *>(s.aux + (size_t)kCUnits * n);
-  s.lab = s.perm + n;
-  s.list = s.lab + n;
-  s.chn = s.list + n;
-  s.lbeg = s.chn + (size_t)maxc * n;
-  s.lsize = s.lbeg + L;
-  s.coff = s.lsize + L;      // [L + 1] start of level l in this cluster's list
-  s.ccur = s.coff + L + 1;   // [L] fill cursors
+  if constexpr (FUSED) {  // the linearizer's shared-memory results
+    s.perm = ls.perm;
+    s.lab = ls.sid;
+    s.lbeg = ls.lb;
+    s.lsize = ls.ls;
+    s.chn = fint + lin_sm_ints(n, maxc, kFusedCnt);
+    s.list = s.chn + (size_t)maxc * n;
+    s.coff = s.list + n;
+    s.ccur = s.coff + n + 1;
+  } else {
+    s.perm = reinterpret_cast<int *>(s.aux + (size_t)kCUnits * n);
+    s.lab = s.perm + n;
+    s.list = s.lab + n;
+    s.chn = s.list + n;
+    s.lbeg = s.chn + (size_t)maxc * n;
+    s.lsize = s.lbeg + L;
+    s.coff = s.lsize + L;      // [L + 1] start of level l in this cluster's list
+    s.ccur = s.coff + L + 1;   // [L] fill cursors
+  }
 
   RCtx ctx;
   ctx.a = &a;
@@ -187,16 +238,19 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
 
 
   // ---- prologue: structure labels (root index, propagated top-down) --------
-  for (int l = tid; l < L; l += blockDim.x) {
-    s.lbeg[l] = __ldg(a.lbeg + l);
-    s.lsize[l] = __ldg(a.lsize + l);
+  if constexpr (!FUSED) {
+    for (int l = tid; l < L; l += blockDim.x) {
+      s.lbeg[l] = __ldg(a.lbeg + l);
+      s.lsize[l] = __ldg(a.lsize + l);
+    }
+    for (int v = tid; v < n; v += blockDim.x) {
+      s.perm[v] = __ldg(a.perm + v);
+      s.lab[v] = __ldg(a.sid + v);  // structure index (cx_linearize)
+    }
+    for (int e = tid; e < maxc * n; e += blockDim.x) s.chn[e] = __ldg(a.chn + e);
+    __syncthreads();
   }
-  for (int v = tid; v < n; v += blockDim.x) {
-    s.perm[v] = __ldg(a.perm + v);
-    s.lab[v] = __ldg(a.sid + v);  // structure index (cx_linearize)
-  }
-  for (int e = tid; e < maxc * n; e += blockDim.x) s.chn[e] = __ldg(a.chn + e);
-  __syncthreads();
+  bool one_cluster = false;
   if (a.kind == CX_DAG) {  // structures sharing a node: one cluster does everything
     bool bad = false;
     for (int i = tid; i < first_leaf; i += blockDim.x)
@@ -205,15 +259,15 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
         if (c < 0) break;
         if (s.lab[c] != s.lab[i]) bad = true;
       }
-    if (__syncthreads_or(bad))
-      for (int v = tid; v < n; v += blockDim.x) s.lab[v] = 0;
-    __syncthreads();
+    one_cluster = __syncthreads_or(bad);
   }
 
   // ---- this cluster's nodes, bucketed by level once (order inside a level is
   // irrelevant: every slice is addressed by new id) ---------------------------
   for (int l = tid; l < L; l += blockDim.x) s.ccur[l] = 0;
   __syncthreads();
+  // this cluster evaluates node i (new id)
+  auto mine = [&](int i) { return (one_cluster ? 0 : s.lab[i] % ncl) == cid; };
   // level of new id i: ids are level-contiguous, root-most level first
   auto level_of = [&](int i) {
     int lo = 0, hi = L - 1;  // find l with lbeg[l] <= i < lbeg[l] + lsize[l]
@@ -224,7 +278,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     return lo;
   };
   for (int i = tid; i < n; i += blockDim.x)
-    if ((s.lab[i] % ncl) == cid) atomicAdd(&s.ccur[level_of(i)], 1);
+    if (mine(i)) atomicAdd(&s.ccur[level_of(i)], 1);
   __syncthreads();
   if (warp == 0) {  // exclusive scan of the per-level counts (level 0 first)
     int acc = 0;
@@ -244,7 +298,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   for (int l = tid; l < L; l += blockDim.x) s.ccur[l] = 0;
   __syncthreads();
   for (int i = tid; i < n; i += blockDim.x)
-    if ((s.lab[i] % ncl) == cid) {
+    if (mine(i)) {
       const int l = level_of(i);
       s.list[s.coff[l] + atomicAdd(&s.ccur[l], 1)] = i;
     }
@@ -264,7 +318,10 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
         int own = s.perm[v];
         int wd = __ldg(a.words + own);
         if (wd < 0 || wd >= a.V) {
-          if (latch) latch_error(a.hdr, CX_E_WORD_RANGE, own);
+          if (latch) {
+            if constexpr (FUSED) atomicMax(ferr, ~(((unsigned long long)CX_E_WORD_RANGE << 32) | (unsigned)own));
+            else latch_error(a.hdr, CX_E_WORD_RANGE, own);
+          }
           wd = 0;
         }
         s_nodes[tid] = v;
@@ -396,21 +453,33 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
 
   // ---- packed root states (this CTA's units of this cluster's roots) --------
   if (a.root_out) {
-    for (int r = warp; r < R; r += kRNW) {
-      const int v = __ldg(a.roots + r);
-      if ((s.lab[v] % ncl) != cid) continue;
-      if (lane < kCUnits) a.root_out[(size_t)r * H + unit0 + lane] = s.hsl[(size_t)v * kCUnits + lane];
+    if constexpr (FUSED) {  // roots: in-degree 0; their structure index is their slot
+      for (int v = warp; v < n; v += kRNW) {
+        if (ls.indeg[s.perm[v]] != 0 || !mine(v)) continue;
+        if (lane < kCUnits)
+          a.root_out[(size_t)s.lab[v] * H + unit0 + lane] = s.hsl[(size_t)v * kCUnits + lane];
+      }
+    } else {
+      for (int r = warp; r < R; r += kRNW) {
+        const int v = __ldg(a.roots + r);
+        if (!mine(v)) continue;
+        if (lane < kCUnits) a.root_out[(size_t)r * H + unit0 + lane] = s.hsl[(size_t)v * kCUnits + lane];
+      }
     }
   }
   trace_mark(a, a.trace_slots - 1);
-  publish_and_exit(a);
+  if constexpr (FUSED) fused_exit(a, ferr);
+  else publish_and_exit(a);
 }
 
-template <int CELL, int H, int MAXC>
+template <int CELL, int H, int MAXC, bool FUSED>
 bool cplan_one(int n, int maxc, int L_bound, int num_roots_hint, FwdPlan *p, int *Gn, int *Gu) {
   constexpr int CSZ = H / kCUnits;
-  auto k = ck_kernel<CELL, H, MAXC>;
-  const size_t smem = CLayout<CELL, H, MAXC>::bytes(n, maxc, L_bound);
+  auto k = ck_kernel<CELL, H, MAXC, FUSED>;
+  size_t smem = CLayout<CELL, H, MAXC>::bytes(n, maxc, L_bound);
+  if (FUSED)  // the linearizer's arrays replace the prologue's int arrays
+    smem = smem - sizeof(int) * ((size_t)(3 + maxc) * n + 4 * (size_t)L_bound + 64) +
+           sizeof(int) * fused_extra_ints(n, maxc);
   if (smem > 227 * 1024) return false;
   static int cached_max = -1;
   static size_t smem_set = 0;
@@ -451,14 +520,34 @@ bool cplan_one(int n, int maxc, int L_bound, int num_roots_hint, FwdPlan *p, int
   p->smem = smem;
   p->kernel = (const void *)k;
   p->cluster = CSZ;
+  p->fused = FUSED;
   return true;
 }
 
-template <int CELL, int H>
+template <int CELL, int H, bool FUSED>
 bool cplan_cell(int n, int maxc, int L_bound, int roots, FwdPlan *p, int *Gn, int *Gu) {
-  if (maxc <= 1) return cplan_one<CELL, H, 1>(n, maxc, L_bound, roots, p, Gn, Gu);
-  if (maxc <= 2) return cplan_one<CELL, H, 2>(n, maxc, L_bound, roots, p, Gn, Gu);
-  if (maxc <= 4) return cplan_one<CELL, H, 4>(n, maxc, L_bound, roots, p, Gn, Gu);
+  if (maxc <= 1) return cplan_one<CELL, H, 1, FUSED>(n, maxc, L_bound, roots, p, Gn, Gu);
+  if (maxc <= 2) return cplan_one<CELL, H, 2, FUSED>(n, maxc, L_bound, roots, p, Gn, Gu);
+  if (maxc <= 4) return cplan_one<CELL, H, 4, FUSED>(n, maxc, L_bound, roots, p, Gn, Gu);
+  return false;
+}
+
+template <bool FUSED>
+bool cplan(int cell, int H, int maxc, int n, int roots, FwdPlan *p, int *Gn, int *Gu) {
+  if (n > kClusterMaxN || n < 1) return false;
+  const int L_bound = n;  // level arrays sized for the worst case
+  switch (cell) {
+    case CX_TREELSTM:
+      if (H == 256) return cplan_cell<CX_TREELSTM, 256, FUSED>(n, maxc, L_bound, roots, p, Gn, Gu);
+      if (H == 128) return cplan_cell<CX_TREELSTM, 128, FUSED>(n, maxc, L_bound, roots, p, Gn, Gu);
+      if (H == 64) return cplan_cell<CX_TREELSTM, 64, FUSED>(n, maxc, L_bound, roots, p, Gn, Gu);
+      return false;
+    case CX_DAGRNN:
+      if (H == 256) return cplan_cell<CX_DAGRNN, 256, FUSED>(n, maxc, L_bound, roots, p, Gn, Gu);
+      if (H == 128) return cplan_cell<CX_DAGRNN, 128, FUSED>(n, maxc, L_bound, roots, p, Gn, Gu);
+      if (H == 64) return cplan_cell<CX_DAGRNN, 64, FUSED>(n, maxc, L_bound, roots, p, Gn, Gu);
+      return false;
+  }
   return false;
 }
 
@@ -467,21 +556,13 @@ bool cplan_cell(int n, int maxc, int L_bound, int roots, FwdPlan *p, int *Gn, in
 // Cluster path for small batches: TreeLSTM and DAG-RNN, H in {64, 128, 256},
 // n <= kClusterMaxN. `roots` (<= 0: unknown) caps the number of clusters.
 bool cluster_plan(int cell, int H, int maxc, int n, int roots, FwdPlan *p, int *Gn, int *Gu) {
-  if (n > kClusterMaxN || n < 1) return false;
-  const int L_bound = n;  // level arrays sized for the worst case
-  switch (cell) {
-    case CX_TREELSTM:
-      if (H == 256) return cplan_cell<CX_TREELSTM, 256>(n, maxc, L_bound, roots, p, Gn, Gu);
-      if (H == 128) return cplan_cell<CX_TREELSTM, 128>(n, maxc, L_bound, roots, p, Gn, Gu);
-      if (H == 64) return cplan_cell<CX_TREELSTM, 64>(n, maxc, L_bound, roots, p, Gn, Gu);
-      return false;
-    case CX_DAGRNN:
-      if (H == 256) return cplan_cell<CX_DAGRNN, 256>(n, maxc, L_bound, roots, p, Gn, Gu);
-      if (H == 128) return cplan_cell<CX_DAGRNN, 128>(n, maxc, L_bound, roots, p, Gn, Gu);
-      if (H == 64) return cplan_cell<CX_DAGRNN, 64>(n, maxc, L_bound, roots, p, Gn, Gu);
-      return false;
-  }
-  return false;
+  return cplan<false>(cell, H, maxc, n, roots, p, Gn, Gu);
+}
+
+// The same kernel with the single-CTA linearizer fused into its prologue
+// (cx_linearize_forward); false when the shared memory does not fit.
+bool fused_plan(int cell, int H, int maxc, int n, FwdPlan *p, int *Gn, int *Gu) {
+  return cplan<true>(cell, H, maxc, n, 0, p, Gn, Gu);
 }
 
 }  // namespace cx

@@ -160,5 +160,33 @@ __device__ __forceinline__ void publish_and_exit(const FwdArgs &a) {
   }
 }
 
+// Fused linearize + forward: data errors of the forward phase are latched into
+// `ferr` (a workspace word, inverted key: 0 = none, atomicMax keeps the lowest
+// key) because CTA 0 writes the header with plain stores while the other CTAs
+// already run. The last CTA out -- after CTA 0's header stores, ordered by the
+// exit counter -- merges it into the header and resets the words.
+__device__ __forceinline__ void fused_exit(const FwdArgs &a, unsigned long long *ferr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned prev = atomicAdd(&a.bar->exit, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence();
+      const unsigned long long f = atomicExch(ferr, 0ull);
+      unsigned long long *hk = reinterpret_cast<unsigned long long *>(&a.hdr->err_key);
+      if (f) atomicMin(hk, ~f);
+      const unsigned long long key = atomicAdd(hk, 0ull);
+      if (key != kNoError) {
+        a.hdr->status = (int)(key >> 32);
+        a.hdr->bad_node = (int)(key & 0xffffffffu);
+        a.hdr->num_levels = 0;
+      }
+      a.bar->count = 0;
+      a.bar->exit = 0;
+      __threadfence();
+    }
+  }
+}
+
 }  // namespace fwd
 }  // namespace cx

@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "lin_kernels.cuh"
 
 namespace cx {
 
@@ -42,6 +43,7 @@ struct FwdArgs {
   int Gn, Gu;   // node groups x unit groups = CTAs
   unsigned long long *trace;  // debug: %globaltimer per CTA and phase (cx_debug_set_trace)
   int trace_slots;
+  LinArgs lin;  // fused linearize + forward (cx_linearize_forward): the linearizer's arguments
 };
 
 // thread 0 of each CTA records %globaltimer into slot `s` (debug builds of a run only)
@@ -60,6 +62,7 @@ struct FwdPlan {
   int cluster = 1;  // > 1: thread-block clusters of this size (no cooperative launch)
   bool big = false; // large-batch pipelined kernel: workspace holds hs, st [n][H] + words [n]
   bool tc = false;  // bf16 tensor-core kernel (forward_tc.cu): launched by tc_launch
+  bool fused = false;  // the kernel also linearizes (FwdArgs::lin), cx_linearize_forward
 };
 
 // Returns false (CX_E_UNSUPPORTED) when no instantiation covers the model.
@@ -80,5 +83,8 @@ bool tc_hoist(int cell, int n, int V);
 size_t tc_state_rows(int cell, int n, int V);
 cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream);
 bool pdl_enabled();
+// Fused linearize + forward (forward_cluster.cu): fp32 cluster
+// path of TreeLSTM / DAG-RNN for small batches. False when not applicable.
+bool fused_plan(int cell, int H, int maxc, int n, FwdPlan *plan, int *Gn, int *Gu);
 
 }  // namespace cx

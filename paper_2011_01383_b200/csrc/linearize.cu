@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "lin_kernels.cuh"
+#include "lin_single.cuh"
 
 namespace cx {
 
@@ -642,344 +643,13 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
   grid_exit(a.bar, G);
 }
 
-__device__ __noinline__ void lin_latch(unsigned long long *err, int code, int v) {
-  atomicMin(err, ((unsigned long long)(unsigned)code << 32) | (unsigned)v);
-}
-
 // ---------------------------------------------------------------------------
-// Single-CTA linearizer: every working array lives in shared memory; the only
-// global traffic is one coalesced read of `children` and fire-and-forget
-// stores of the outputs (no dependent global round trips on the latency path).
-// smem (ints): ch[maxc*n] | hgt[n] | indeg[n] | perm[n] | inv[n] | lb[n] | cnt[kLinSmemCnt]
+// Single-CTA linearizer (lin_single.cuh): every working array in shared memory.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kLinSingleThreads, 1) lin_single_kernel(LinArgs a) {
   griddep_launch_dependents();  // the forward may stage its weights meanwhile
   extern __shared__ int sm[];
-  __shared__ unsigned long long s_err;
-  __shared__ int s_tmp[33];
-  __shared__ int s_count, s_round;
-  const int n = a.n, maxc = a.maxc, tid = threadIdx.x, nthr = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  int *ch = sm, *hgt = ch + maxc * n, *indeg = hgt + n, *perm = indeg + n, *inv = perm + n,
-      *lb = inv + n, *ls_s = lb + n, *sid = ls_s + n, *par = sid + n, *cnt_s = par + n;
-
-  lin_mark(a, 0);
-  for (int i = tid; i < maxc * n; i += nthr) ch[i] = __ldg(a.ch + i);
-  for (int v = tid; v < n; v += nthr) {
-    indeg[v] = 0;
-    hgt[v] = -1;
-    par[v] = -1;  // parent pointer (trees/sequences)
-    sid[v] = INT_MAX;
-  }
-  if (tid == 0) {
-    s_err = kNoError;
-    s_count = 0;
-    s_round = 0;
-    s_tmp[32] = 0;
-  }
-  __syncthreads();
-
-  // a1: validation + in-degree; errors latched in shared memory (lowest key).
-  // For trees and sequences the same pass records parent pointers (perm[] is
-  // free until a4) and the number of children (inv[]) for the walk-up below.
-  const bool tree_like = a.kind != CX_DAG;
-  int *parent = par, *pending = inv;
-  for (int v = tid; v < n; v += nthr) {
-    bool absent = false;
-    int nc = 0;
-    for (int k = 0; k < maxc; k++) {
-      int c = ch[k * n + v];
-      if (c == -1) {
-        absent = true;
-        continue;
-      }
-      nc++;
-      if (absent) lin_latch(&s_err, CX_E_CHILD_LAYOUT, v);
-      if (c < 0 || c >= n) {
-        lin_latch(&s_err, CX_E_CHILD_RANGE, v);
-        continue;
-      }
-      atomicAdd(&indeg[c], 1);
-      if (tree_like) parent[c] = v;
-      for (int k2 = 0; k2 < k; k2++)
-        if (ch[k2 * n + v] == c) lin_latch(&s_err, CX_E_KIND, v);
-    }
-    if (nc == 0) hgt[v] = 0;
-    pending[v] = nc;
-  }
-  __syncthreads();
-  if (tree_like)
-    for (int v = tid; v < n; v += nthr)
-      if (indeg[v] > 1) lin_latch(&s_err, CX_E_KIND, v);
-  __syncthreads();
-  lin_mark(a, 1);
-  bool failed = s_err != kNoError;
-
-  // a2: heights. Trees/sequences: every leaf walks up its parent chain; at
-  // each parent it raises the height (atomicMax) and decrements the pending
-  // count -- only the last arriving child continues, so every node is
-  // finalised exactly once with h = 1 + max over its children, and no block
-  // barrier is needed per level. DAGs: Jacobi rounds, one __syncthreads_or
-  // each (round r finalises exactly the nodes of height r).
-  int L = 0;
-  if (!failed && n > 0) {
-    int hmax = 0;
-    if (tree_like) {
-      for (int v = tid; v < n; v += nthr) {
-        // start at leaves only: an immutable test (a node's pending count can
-        // reach 0 while this loop runs, when the walk of its last child passes
-        // through it; re-walking it would decrement its parent twice)
-        if (ch[v] != -1) continue;
-        int cur = v, hc = 0;
-        while (true) {
-          int p = parent[cur];
-          if (p < 0) break;
-          atomicMax(&hgt[p], hc + 1);
-          __threadfence_block();
-          if (atomicSub(&pending[p], 1) != 1) break;
-          __threadfence_block();
-          cur = p;
-          hc = atomicAdd(&hgt[p], 0);  // every child's atomicMax precedes its decrement
-        }
-        hmax = max(hmax, hc);
-      }
-      __syncthreads();
-      bool unfinished = false;
-      for (int v = tid; v < n; v += nthr)
-        if (pending[v] > 0) {  // on or above a cycle
-          lin_latch(&s_err, CX_E_CYCLE, v);
-          unfinished = true;
-        }
-      if (__syncthreads_or(unfinished)) failed = true;
-      for (int o = 16; o; o >>= 1) hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
-      if (lane == 0) atomicMax(&s_round, hmax);
-      __syncthreads();
-      L = s_round + 1;
-    } else {
-      int r = 0;
-      bool progress = true;
-      while (progress) {
-        r++;
-        bool any = false;
-        for (int v = tid; v < n; v += nthr) {
-          if (hgt[v] >= 0) continue;
-          bool ok = true;
-          for (int k = 0; k < maxc; k++) {
-            int c = ch[k * n + v];
-            if (c == -1) break;
-            int hc = hgt[c];
-            if (hc < 0 || hc >= r) {
-              ok = false;
-              break;
-            }
-          }
-          if (ok) {
-            hgt[v] = r;
-            any = true;
-          }
-        }
-        progress = __syncthreads_or(any);
-      }
-      bool unfinished = false;
-      for (int v = tid; v < n; v += nthr)
-        if (hgt[v] < 0) {
-          lin_latch(&s_err, CX_E_CYCLE, v);
-          unfinished = true;
-        }
-      if (__syncthreads_or(unfinished)) failed = true;
-      L = r;
-    }
-  }
-  lin_mark(a, 2);
-
-  if (!failed && n > 0) {
-    // a3: per-(level, id segment) counts + roots row, always in shared memory:
-    // S segments of `seg` ids (one warp each), S shrinks when L is large.
-    const int nw = nthr >> 5;
-    int S = min(nw, max(1, kLinSmemCnt / (L + 1)));
-    S = min(S, (n + 31) / 32);
-    const int seg = 32 * ((((n + 31) / 32) + S - 1) / S);
-    S = (n + seg - 1) / seg;
-    int *cnt = cnt_s;
-    for (int e = tid; e < (L + 1) * S; e += nthr) cnt[e] = 0;
-    __syncthreads();
-    const unsigned lt = (1u << lane) - 1u;
-    if (warp < S) {
-      const int s = warp, end = min(n, (s + 1) * seg);
-      for (int base = s * seg; base < end; base += 32) {
-        int v = base + lane;
-        bool valid = v < end;
-        int hv = valid ? hgt[v] : -1;
-        unsigned m = __match_any_sync(0xffffffffu, hv);
-        if (valid && (m & lt) == 0) cnt[hv * S + s] += __popc(m);
-        unsigned rb = __ballot_sync(0xffffffffu, valid && indeg[v] == 0);
-        if (lane == 0 && rb) cnt[L * S + s] += __popc(rb);
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    lin_mark(a, 3);
-    // exclusive scan in the order (level L-1 .. 0) x (segment 0 .. S-1): warp w
-    // takes levels w, w + nw, ...; level totals, then a warp-0 scan over them
-    for (int l = warp; l < L; l += nw) {
-      int x = lane < S ? cnt[l * S + lane] : 0;  // S <= 32 when L < kLinSmemCnt/32
-      int incl = x;
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (S <= 32) {
-        if (lane < S) cnt[l * S + lane] = incl - x;  // within-level offset
-        if (lane == 31) ls_s[l] = incl;               // level size
-      } else {
-        // wide tables (tiny L): serial per level
-        if (lane == 0) {
-          int acc = 0;
-          for (int s2 = 0; s2 < S; s2++) {
-            int c = cnt[l * S + s2];
-            cnt[l * S + s2] = acc;
-            acc += c;
-          }
-          ls_s[l] = acc;
-        }
-      }
-    }
-    if (warp == nw - 1) {  // roots row
-      int acc = 0;
-      for (int b = 0; b < S; b += 32) {
-        int x = b + lane < S ? cnt[L * S + b + lane] : 0;
-        int incl = x;
-        for (int o = 1; o < 32; o <<= 1) {
-          int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        if (b + lane < S) cnt[L * S + b + lane] = acc + incl - x;
-        acc += __shfl_sync(0xffffffffu, incl, 31);
-      }
-      if (lane == 0) s_count = acc;
-    }
-    __syncthreads();
-    // level begins: exclusive scan of level sizes from level L-1 down (warp 0)
-    if (warp == 0) {
-      int acc = 0, mx = 0;
-      for (int b = 0; b < L; b += 32) {
-        int l = L - 1 - (b + lane);
-        int x = l >= 0 ? ls_s[l] : 0;
-        int incl = x;
-        for (int o = 1; o < 32; o <<= 1) {
-          int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        if (l >= 0) {
-          lb[l] = acc + incl - x;
-          a.lbeg[l] = acc + incl - x;
-          a.lsize[l] = x;
-          mx = max(mx, x);
-        }
-        acc += __shfl_sync(0xffffffffu, incl, 31);
-      }
-      for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0) s_tmp[32] = mx;
-    }
-    __syncthreads();
-    lin_mark(a, 4);
-    // a4: stable scatter (each warp walks its segment in id order)
-    if (warp < S) {
-      const int s = warp, end = min(n, (s + 1) * seg);
-      int rbase = cnt[L * S + s];
-      for (int base = s * seg; base < end; base += 32) {
-        int v = base + lane;
-        bool valid = v < end;
-        int hv = valid ? hgt[v] : -1;
-        unsigned m = __match_any_sync(0xffffffffu, hv);
-        int leader = __ffs(m) - 1;
-        int b = (valid && lane == leader) ? lb[hv] + cnt[hv * S + s] : 0;
-        b = __shfl_sync(0xffffffffu, b, leader);
-        int nid = b + __popc(m & lt);
-        bool isroot = valid && indeg[v] == 0;
-        unsigned rb = __ballot_sync(0xffffffffu, isroot);
-        __syncwarp();
-        if (valid && lane == leader) cnt[hv * S + s] += __popc(m);
-        if (valid) {
-          perm[nid] = v;
-          inv[v] = nid;
-          a.perm[nid] = v;
-          a.inv[v] = nid;
-          a.hnew[nid] = hv;
-          if (isroot) {
-            a.roots[rbase + __popc(rb & lt)] = nid;
-            sid[nid] = rbase + __popc(rb & lt);
-          }
-        }
-        rbase += __popc(rb);
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    lin_mark(a, 5);
-    // a5: remap children to new ids
-    for (int i = tid; i < n; i += nthr) {
-      int v = perm[i];
-      for (int k = 0; k < maxc; k++) {
-        int c = ch[k * n + v];
-        a.chn[(long long)k * n + i] = c == -1 ? -1 : inv[c];
-      }
-    }
-    // a6: structure of every node. Trees/sequences: walk up to the root (roots
-    // already hold their index); DAGs: the smallest root index reaching the
-    // node, propagated top-down one level per round.
-    if (tree_like) {
-      __syncthreads();
-      for (int i = tid; i < n; i += nthr) {
-        int v = perm[i], p = parent[v];
-        if (p < 0) continue;
-        while (p >= 0) {
-          v = p;
-          p = parent[v];
-        }
-        sid[i] = sid[inv[v]];
-      }
-      __syncthreads();
-    } else {
-      for (int l = L - 1; l >= 1; l--) {
-        const int b = lb[l], e = b + ls_s[l];
-        for (int i = b + tid; i < e; i += nthr) {
-          const int si = sid[i], v = perm[i];
-          for (int k = 0; k < maxc; k++) {
-            int c = ch[k * n + v];
-            if (c == -1) break;
-            atomicMin(&sid[inv[c]], si);
-          }
-        }
-        __syncthreads();
-      }
-    }
-    for (int i = tid; i < n; i += nthr) a.sid[i] = sid[i];
-  }
-
-  // header (one thread; plain stores)
-  __syncthreads();
-  lin_mark(a, 6);
-  if (tid == 0) {
-    cx_lin_header *h = a.hdr;
-    unsigned long long key = s_err;
-    h->err_key = key;
-    h->num_nodes = n;
-    if (key != kNoError) {
-      h->status = (int)(key >> 32);
-      h->bad_node = (int)(key & 0xffffffffu);
-      h->num_levels = 0;
-    } else {
-      h->status = CX_OK;
-      h->bad_node = -1;
-      h->num_levels = n > 0 ? L : 0;
-      h->num_roots = n > 0 ? s_count : 0;
-      int nl = n > 0 ? n - lb[0] : 0;
-      h->num_leaves = nl;
-      h->first_leaf = n - nl;
-      h->max_level_size = n > 0 ? s_tmp[32] : 0;
-    }
-  }
+  lin_single_body(a, sm, kLinSmemCnt, true, nullptr, LinPrefetch{});
 }
 
 __global__ void empty_kernel(unsigned long long *t) {
@@ -1008,7 +678,7 @@ cudaError_t launch_empty(int ctas, int threads, int coop, unsigned long long *t,
 }
 
 size_t lin_single_smem_bytes(int n, int maxc) {
-  return sizeof(int) * ((size_t)(maxc + 8) * n + kLinSmemCnt);
+  return sizeof(int) * lin_sm_ints(n, maxc, kLinSmemCnt);
 }
 
 bool lin_use_single(int n, int maxc) {

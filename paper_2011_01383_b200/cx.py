@@ -75,6 +75,12 @@ def lib():
             L.cx_forward.argtypes = [ctypes.POINTER(_Model), ctypes.POINTER(_Weights), P, P,
                                      ctypes.POINTER(_Lin), P, P, P, P, S, P]
             L.cx_forward.restype = ctypes.c_int
+            L.cx_linearize_forward_workspace_bytes.argtypes = [ctypes.POINTER(_Model), I, I]
+            L.cx_linearize_forward_workspace_bytes.restype = S
+            L.cx_linearize_forward.argtypes = [P, I, I, I, ctypes.POINTER(_Model),
+                                               ctypes.POINTER(_Weights), P, P, ctypes.POINTER(_Lin),
+                                               P, P, P, P, S, P]
+            L.cx_linearize_forward.restype = ctypes.c_int
             L.cx_status_sync.argtypes = [ctypes.POINTER(_Lin), ctypes.POINTER(I), P]
             L.cx_status_sync.restype = ctypes.c_int
             L.cx_status_str.argtypes = [ctypes.c_int]
@@ -214,19 +220,7 @@ def launch_info(cell, hidden, vocab=1, dtype=F32):
     return dict(ctas=a.value, threads=b.value, smem=c.value)
 
 
-def forward(cell: int, hidden: int, weights, emb: torch.Tensor, word_ids: torch.Tensor,
-            lin: Linearization, dtype: int = F32, want_aux: bool = False, num_roots=None,
-            h_out=None, aux_out=None, root_out=None, stream=None, workspace=None):
-    """cx_forward. Returns (h_out [n, H], aux or None, roots or None)."""
-    dev = emb.device
-    n = lin.n
-    vocab = emb.shape[0]
-    ws_list = list(weights)
-    if len(ws_list) != N_WEIGHTS[cell]:
-        raise ValueError(f"cell {cell} takes {N_WEIGHTS[cell]} weight tensors")
-    for w in ws_list:
-        if w.dtype != torch.float32 or not w.is_cuda or not w.is_contiguous():
-            raise ValueError("weights must be contiguous fp32 CUDA tensors")
+def _outputs(cell, hidden, n, dev, want_aux, num_roots, h_out, aux_out, root_out):
     if h_out is None:
         h_out = torch.empty(max(n, 1), hidden, dtype=torch.float32, device=dev)[:n]
     if want_aux and aux_out is None:
@@ -236,10 +230,75 @@ def forward(cell: int, hidden: int, weights, emb: torch.Tensor, word_ids: torch.
             aux_out = torch.empty(n, hidden, hidden, dtype=torch.float32, device=dev)
     if num_roots is not None and root_out is None:
         root_out = torch.empty(num_roots, hidden, dtype=torch.float32, device=dev)
-    m = _model(cell, hidden, vocab, dtype)
+    return h_out, aux_out, root_out
+
+
+def _weights(cell, weights):
+    ws_list = list(weights)
+    if len(ws_list) != N_WEIGHTS[cell]:
+        raise ValueError(f"cell {cell} takes {N_WEIGHTS[cell]} weight tensors")
+    for t in ws_list:
+        if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("weights must be contiguous fp32 CUDA tensors")
     w = _Weights()
     for i, t in enumerate(ws_list):
         w.p[i] = t.data_ptr()
+    return w
+
+
+def fused_applies(cell, hidden, n, max_children, vocab=1, dtype=F32) -> bool:
+    """Whether cx_linearize_forward runs as ONE launch for this shape (reporting)."""
+    L = lib()
+    L.cx_debug_fused_applies.argtypes = [ctypes.POINTER(_Model), ctypes.c_int32, ctypes.c_int32]
+    L.cx_debug_fused_applies.restype = ctypes.c_int32
+    m = _model(cell, hidden, vocab, dtype)
+    return bool(L.cx_debug_fused_applies(ctypes.byref(m), n, max_children))
+
+
+def linearize_forward(children: torch.Tensor, kind: int, cell: int, hidden: int, weights,
+                      emb: torch.Tensor, word_ids: torch.Tensor, dtype: int = F32,
+                      out: Linearization = None, want_aux: bool = False, num_roots=None,
+                      h_out=None, aux_out=None, root_out=None, stream=None, workspace=None):
+    """cx_linearize_forward: linearize + forward, one launch where the batch
+    allows it. Returns (lin, h_out, aux or None, roots or None)."""
+    if children.dim() != 2 or children.dtype != torch.int32 or not children.is_cuda:
+        raise ValueError("children must be an int32 CUDA tensor [max_children, n]")
+    if not children.is_contiguous():
+        children = children.contiguous()
+    maxc, n = children.shape
+    dev = emb.device
+    if out is None:
+        out = alloc_linearization(n, maxc, kind, children.device)
+    elif (out.n, out.max_children) != (n, maxc):
+        raise ValueError("out was allocated for a different (n, max_children)")
+    out.kind = kind
+    w = _weights(cell, weights)
+    h_out, aux_out, root_out = _outputs(cell, hidden, n, dev, want_aux, num_roots, h_out,
+                                        aux_out, root_out)
+    m = _model(cell, hidden, emb.shape[0], dtype)
+    L = lib()
+    need = L.cx_linearize_forward_workspace_bytes(ctypes.byref(m), n, maxc)
+    ws = workspace if workspace is not None else _ws.get(dev, "linfwd", need)
+    st = L.cx_linearize_forward(_ptr(children), n, maxc, kind, ctypes.byref(m), ctypes.byref(w),
+                                _ptr(emb), _ptr(word_ids), ctypes.byref(out.c), _ptr(h_out),
+                                _ptr(aux_out), _ptr(root_out), _ptr(ws), ws.numel(),
+                                _stream(stream))
+    if st != OK:
+        raise CxError(st, "cx_linearize_forward")
+    return out, h_out, aux_out, root_out
+
+
+def forward(cell: int, hidden: int, weights, emb: torch.Tensor, word_ids: torch.Tensor,
+            lin: Linearization, dtype: int = F32, want_aux: bool = False, num_roots=None,
+            h_out=None, aux_out=None, root_out=None, stream=None, workspace=None):
+    """cx_forward. Returns (h_out [n, H], aux or None, roots or None)."""
+    dev = emb.device
+    n = lin.n
+    vocab = emb.shape[0]
+    w = _weights(cell, weights)
+    h_out, aux_out, root_out = _outputs(cell, hidden, n, dev, want_aux, num_roots, h_out,
+                                        aux_out, root_out)
+    m = _model(cell, hidden, vocab, dtype)
     L = lib()
     need = L.cx_forward_workspace_bytes(ctypes.byref(m), n)
     ws = workspace if workspace is not None else _ws.get(dev, "fwd", need)

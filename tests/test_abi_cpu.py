@@ -25,7 +25,7 @@ def declared_functions():
 
 def test_exports_every_declared_symbol(cxmod):
     names = declared_functions()
-    assert len(names) == 7
+    assert len(names) == 9
     L = cxmod.lib()
     for name in names:
         assert hasattr(L, name), name

@@ -12,6 +12,7 @@ import bench  # noqa: E402
 import paper_2011_01383_b200 as cx  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2_treelstm_b10"
+fused = len(sys.argv) > 2 and sys.argv[2] == "fused"  # cx_linearize_forward (slot 20 = lin done)
 inp = bench.make_inputs(name, 0, 1)
 dev = torch.device("cuda", 0)
 t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a, dtype=dt)).to(dev)
@@ -29,9 +30,12 @@ cx.forward(cell, H, weights, emb, words, lin)
 torch.cuda.synchronize()
 for rep in range(3):
     flush.fill_(1.0)
-    lin = cx.linearize(children, inp["kind"])
     L.cx_debug_set_trace(ctypes.c_void_p(buf.data_ptr()), S)
-    cx.forward(cell, H, weights, emb, words, lin)
+    if fused:
+        lin = cx.linearize_forward(children, inp["kind"], cell, H, weights, emb, words)[0]
+    else:
+        lin = cx.linearize(children, inp["kind"])
+        cx.forward(cell, H, weights, emb, words, lin)
     L.cx_debug_set_trace(None, 0)
     torch.cuda.synchronize()
 tr = buf.view(info["ctas"], S).cpu().numpy().astype(np.int64)
@@ -39,7 +43,7 @@ nl = lin.header_dict()["num_levels"]
 t0 = tr[:, 0].min()
 rel = lambda x: (x - t0) / 1000.0
 print(f"{name}: ctas={info['ctas']} levels={nl}")
-for sl, nm in [(0, "entry"), (1, "labels"), (12, "leaf words"), (13, "leaf gather"), (2, "leaf phase")] + [(3 + l, f"level {l}") for l in range(1, nl)] + [(S - 1, "exit")]:
+for sl, nm in [(0, "entry"), (20, "lin (fused)"), (1, "labels"), (12, "leaf words"), (13, "leaf gather"), (2, "leaf phase")] + [(3 + l, f"level {l}") for l in range(1, nl)] + [(S - 1, "exit")]:
     col = tr[:, sl]
     ok = col > 0
     print(f"{nm:12s} min {rel(col[ok].min()):7.2f} max {rel(col[ok].max()):7.2f}")
