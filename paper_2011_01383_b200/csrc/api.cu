@@ -94,6 +94,8 @@ void lin_args(const int32_t *children, int32_t n, int32_t max_children, cx_kind 
     std::lock_guard<std::mutex> lk(g_mu);
     a.trace = g_lin_trace;
   }
+  const char *hj = std::getenv("CX_LIN_JACOBI");
+  a.hjacobi = hj && hj[0] == '1';  // measurement only: Jacobi rounds for trees too
 }
 }  // namespace
 

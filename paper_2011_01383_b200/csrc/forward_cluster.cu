@@ -158,15 +158,28 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     gs[0] = {a.w[0], 0, H, 0}; gs[1] = {a.w[1], 0, H, 0};
     ng = 2;
   }
-  load_wregs<4, KC>(w, gs, ng, unit0 + u, k0);
-  if constexpr (CELL == CX_TREELSTM) {
-    if (tid < 4 * kCUnits) {
-      int g = tid / kCUnits, uu = tid % kCUnits;
-      const float *b = g < 3 ? a.w[2] + g * H : a.w[4];
-      s_bias[tid] = __ldg(b + unit0 + uu);
+  auto load_leaf_weights = [&]() {
+    load_wregs<4, KC>(w, gs, ng, unit0 + u, k0);
+    if constexpr (CELL == CX_TREELSTM) {
+      if (tid < 4 * kCUnits) {
+        int g = tid / kCUnits, uu = tid % kCUnits;
+        const float *b = g < 3 ? a.w[2] + g * H : a.w[4];
+        s_bias[tid] = __ldg(b + unit0 + uu);
+      }
+    } else {
+      if (tid < kCUnits) s_bias[tid] = __ldg(a.w[2] + unit0 + tid);
+    }
+  };
+  if constexpr (FUSED) {
+    // fire-and-forget L2 prefetch of this thread's weight rows; the register
+    // loads follow the in-kernel linearization (loads in flight would queue
+    // ahead of the linearizer's own children loads)
+    for (int g = 0; g < ng; g++) {
+      const float *src = gs[g].base + (size_t)(gs[g].r0 + unit0 + u) * gs[g].ld + gs[g].c0 + k0;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
     }
   } else {
-    if (tid < kCUnits) s_bias[tid] = __ldg(a.w[2] + unit0 + tid);
+    load_leaf_weights();
   }
   unsigned long long *ferr = reinterpret_cast<unsigned long long *>(&a.bar->pad[0]);
   int L, first_leaf, R;
@@ -184,6 +197,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       fused_exit(a, ferr);
       return;
     }
+    load_leaf_weights();
     ls = lin_carve(fint, n, maxc);
     L = lo.L;
     first_leaf = lo.first_leaf;

@@ -26,6 +26,7 @@ struct LinArgs {
   int32_t *cnt;    // budget
   int budget;
   unsigned long long *trace;  // debug: %globaltimer per phase (CTA 0), NULL = off
+  int hjacobi;  // single-CTA path: Jacobi rounds for trees too (CX_LIN_JACOBI=1, measurement)
 };
 
 __device__ __forceinline__ void lin_mark(const LinArgs &a, int s) {

@@ -22,30 +22,52 @@ cell, H = inp["cell"], inp["H"]
 S = 128
 info = cx.launch_info(cell, H)
 buf = torch.zeros(info["ctas"] * S, dtype=torch.int64, device=dev)
+lbuf = torch.zeros(32, dtype=torch.int64, device=dev)
 L = cx.lib()
 L.cx_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 lin = cx.linearize(children, inp["kind"])
 cx.forward(cell, H, weights, emb, words, lin)
 torch.cuda.synchronize()
-for rep in range(3):
-    flush.fill_(1.0)
+def run_once():
+    global lin
     L.cx_debug_set_trace(ctypes.c_void_p(buf.data_ptr()), S)
     if fused:
-        lin = cx.linearize_forward(children, inp["kind"], cell, H, weights, emb, words)[0]
+        lin = cx.linearize_forward(children, inp["kind"], cell, H, weights, emb, words, out=lin,
+                                   h_out=h)[0]
     else:
-        lin = cx.linearize(children, inp["kind"])
-        cx.forward(cell, H, weights, emb, words, lin)
+        L.cx_debug_set_lin_trace.argtypes = [ctypes.c_void_p]
+        L.cx_debug_set_lin_trace(ctypes.c_void_p(lbuf.data_ptr()))
+        cx.linearize(children, inp["kind"], out=lin)
+        L.cx_debug_set_lin_trace(None)
+        cx.forward(cell, H, weights, emb, words, lin, h_out=h)
     L.cx_debug_set_trace(None, 0)
+
+
+h = torch.empty(children.shape[1], H, device=dev)
+run_once()
+torch.cuda.synchronize()
+# graph-replayed like bench.py (trace buffers are baked into the captured launches)
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):
+    run_once()
+for rep in range(3):
+    flush.fill_(1.0)
+    g.replay()
     torch.cuda.synchronize()
 tr = buf.view(info["ctas"], S).cpu().numpy().astype(np.int64)
 nl = lin.header_dict()["num_levels"]
 t0 = tr[:, 0].min()
 rel = lambda x: (x - t0) / 1000.0
 print(f"{name}: ctas={info['ctas']} levels={nl}")
+if not fused:
+    lt = lbuf.cpu().numpy().astype(np.int64)
+    print(f"cx_linearize (CTA 0): entry {rel(lt[0]):7.2f}  end {rel(lt[6]):7.2f} us (relative to the forward's entry)")
 for sl, nm in [(0, "entry"), (20, "lin (fused)"), (1, "labels"), (12, "leaf words"), (13, "leaf gather"), (2, "leaf phase")] + [(3 + l, f"level {l}") for l in range(1, nl)] + [(S - 1, "exit")]:
     col = tr[:, sl]
     ok = col > 0
+    if not ok.any():
+        continue
     print(f"{nm:12s} min {rel(col[ok].min()):7.2f} max {rel(col[ok].max()):7.2f}")
 print("first tile of each level, mean over CTAs with a tile (us): list->meta, meta->pulled, pulled->contracted, ->epilogue")
 for l in range(1, nl):
