@@ -492,7 +492,8 @@ def run_gpu(args, rank, world, local_rank):
     prof = os.path.join(ROOT, "profiles", "forward_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(name if args.dtype == "f32" else f"{name}:bf16")
+            traffic = json.load(open(prof)).get(
+                f"{name}:fused" if fused else name if args.dtype == "f32" else f"{name}:bf16")
         except Exception:
             traffic = None
     if args.dtype == "bf16":

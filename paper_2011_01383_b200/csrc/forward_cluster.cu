@@ -319,6 +319,26 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   __syncthreads();
   trace_mark(a, 1);
 
+  // The level barrier is split: arrive (release: this CTA's state slices are
+  // published to the cluster), then the caller's outputs of the level just
+  // finished go to global memory, then wait (acquire). Issued before the
+  // arrive, those global stores would stall the release fence (ncu: the
+  // barrier's MEMBAR was the top stall); after it they drain while the
+  // cluster meets and the next level starts.
+  auto cl_arrive = [] { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); };
+  auto cl_wait = [] { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); };
+  // h_out (and TreeLSTM c into aux_out) of this cluster's nodes at list
+  // positions [pb, pe), this CTA's 16 units: 64-byte row pieces
+  auto put_outputs = [&](int pb, int pe) {
+    const bool wa = CELL == CX_TREELSTM && a.aux_out;
+    for (int idx = tid; idx < (pe - pb) * kCUnits; idx += blockDim.x) {
+      const int v = s.list[pb + idx / kCUnits], uu = idx % kCUnits;
+      const size_t o = (size_t)s.perm[v] * H + unit0 + uu;
+      a.h_out[o] = s.hsl[(size_t)v * kCUnits + uu];
+      if (wa) a.aux_out[o] = s.aux[(size_t)v * kCUnits + uu];
+    }
+  };
+
   // ---- leaf / projection phase ----------------------------------------------
   {
     // TreeLSTM: leaves. DAG-RNN: every node (input projection P = W_x x + b;
@@ -360,9 +380,6 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
               float hh = sigmoidf_(sacc[1] + s_bias[16 + u]) * tanhf_(cc);
               s.hsl[(size_t)v * kCUnits + u] = hh;
               s.aux[(size_t)v * kCUnits + u] = cc;
-              const size_t o = (size_t)s.perm[v] * H + unit0 + u;
-              a.h_out[o] = hh;
-              if (a.aux_out) a.aux_out[o] = cc;
             }
           } else {
             float sacc[1];
@@ -374,7 +391,6 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
               if (v >= first_leaf) {
                 const float hh = tanhf_(p);
                 s.hsl[(size_t)v * kCUnits + u] = hh;
-                a.h_out[(size_t)s.perm[v] * H + unit0 + u] = hh;
               }
             }
           }
@@ -395,7 +411,9 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     load_wregs<4, KC>(w, gs, 4, unit0 + u, k0);
   }
   trace_mark(a, 2);
-  cl.sync();
+  cl_arrive();
+  put_outputs(s.coff[0], s.coff[1]);  // the leaves (level 0)
+  cl_wait();
 
   // ---- internal levels: one cluster barrier per level -----------------------
   for (int l = 1; l < L; l++) {
@@ -438,9 +456,6 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
             float hh = sigmoidf_(sacc[1] + s_bias[16 + u]) * tanhf_(cc);
             s.hsl[(size_t)v * kCUnits + u] = hh;
             s.aux[(size_t)v * kCUnits + u] = cc;
-            const size_t o = (size_t)s.perm[v] * H + unit0 + u;
-            a.h_out[o] = hh;
-            if (a.aux_out) a.aux_out[o] = cc;
           }
         } else {
           float sacc[1];
@@ -449,7 +464,6 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
             const int v = s_nodes[t];
             const float hh = tanhf_(sacc[0] + s.aux[(size_t)v * kCUnits + u]);
             s.hsl[(size_t)v * kCUnits + u] = hh;
-            a.h_out[(size_t)s.perm[v] * H + unit0 + u] = hh;
           }
         }
         __syncthreads();
@@ -461,15 +475,18 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       else tile(std::integral_constant<int, 1>{});
       if (t0 == 0 && l < 20) trace_mark(a, tb + 4);
     }
-    cl.sync();
+    cl_arrive();
+    put_outputs(lbase, lbase + cnt);
+    cl_wait();
     trace_mark(a, 3 + l);
   }
 
   // ---- packed root states (this CTA's units of this cluster's roots) --------
   if (a.root_out) {
     if constexpr (FUSED) {  // roots: in-degree 0; their structure index is their slot
-      for (int v = warp; v < n; v += kRNW) {
-        if (ls.indeg[s.perm[v]] != 0 || !mine(v)) continue;
+      for (int p = warp; p < s.coff[L]; p += kRNW) {  // this cluster's nodes
+        const int v = s.list[p];
+        if (ls.indeg[s.perm[v]] != 0) continue;
         if (lane < kCUnits)
           a.root_out[(size_t)s.lab[v] * H + unit0 + lane] = s.hsl[(size_t)v * kCUnits + lane];
       }
