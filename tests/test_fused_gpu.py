@@ -204,3 +204,34 @@ def test_graph_capture(cx):
     torch.cuda.synchronize()
     assert torch.equal(h, h0) and torch.equal(r, r0)
     assert cx.status(lin) == (0, -1)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fused_fuzz(cx, seed):
+    """Random shuffled forests / DAGs / chains up to the fused size limit:
+    linearization bit-exact vs the oracle, forward bit-exact vs the two calls."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(1, 700))
+    maxc = int(rng.integers(1, 5))
+    shape = seed % 3
+    if shape == 0:
+        ch = synth.random_forest(n, maxc, seed)
+        kind, cell = T.TREE, T.TREELSTM
+    elif shape == 1:
+        ch = synth.random_dag(min(n, 300), maxc, seed)
+        kind, cell = T.DAG, T.DAGRNN
+    else:
+        ch, _ = synth.chains(1 + seed % 4, 1 + n // (1 + seed % 4))
+        kind, cell = T.SEQUENCE, T.TREELSTM
+    ch, _, _ = synth.shuffle_ids(ch, None, seed)
+    H = (64, 128, 256)[seed % 3]
+    words, emb, ws_np, ws_dev = _case(cell, H, 37, ch, kind, seed)
+    chd, wdd, embd = dev_i32(ch), dev_i32(words), dev_f32(emb)
+    ref = oracle.linearize(ch, kind)
+    R = ref["num_roots"]
+    lin_f, h_f, _, r_f = cx.linearize_forward(chd, kind, cell, H, ws_dev, embd, wdd, num_roots=R)
+    assert cx.status(lin_f) == (0, -1)
+    assert_lin_equal(lin_to_numpy(lin_f), ref)
+    lin_s = cx.linearize(chd, kind)
+    h_s, _, r_s = cx.forward(cell, H, ws_dev, embd, wdd, lin_s, num_roots=R)
+    assert torch.equal(h_f, h_s) and torch.equal(r_f, r_s)
