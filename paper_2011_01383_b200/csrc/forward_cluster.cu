@@ -36,41 +36,49 @@ using namespace rw;
 
 constexpr int kCUnits = kRUG;  // units per CTA (16)
 
+// DAG-RNN level: U h~ + W_x x in one accumulator. Rows per node in X: the
+// MAXC children, x (vector MAXC), then h~ (vector MAXC + 1, the HTS row).
 template <int MAXC>
-struct CDagLevel : PhBase<2, MAXC, MAXC, 1, 1> {  // U h~ (gate 1 of {W_x, U})
-  __device__ static constexpr int g(int p) { return 1; }
-  __device__ static constexpr int v(int p) { return MAXC; }
+struct CDagLevel : PhBase<2, MAXC + 1, MAXC, 1, 2> {
+  __device__ static constexpr int g(int p) { return p == 0 ? 1 : 0; }
+  __device__ static constexpr int v(int p) { return p == 0 ? MAXC + 1 : MAXC; }
   __device__ static constexpr int a(int p) { return 0; }
 };
 
 template <int CELL, int MAXC>
 struct CCfg;
+// RPN: X rows per node at a level; AUX: a per-node aux slice in shared memory
+// (TreeLSTM's memory cell; DAG-RNN recomputes W_x x at the node's level instead
+// of keeping its projection, which halves the per-node footprint)
 template <int MAXC>
 struct CCfg<CX_TREELSTM, MAXC> {
-  static constexpr int TMAX = 8, NVMAX = MAXC, NAMAX = 3 + MAXC, LEAFB = 48;
+  static constexpr int TMAX = 8, NVMAX = MAXC, NAMAX = 3 + MAXC, LEAFB = 48, RPN = MAXC + 1;
+  static constexpr bool AUX = true;
 };
 template <int MAXC>
 struct CCfg<CX_DAGRNN, MAXC> {
-  static constexpr int TMAX = 16, NVMAX = MAXC, NAMAX = 1, LEAFB = 32;
+  static constexpr int TMAX = 16, NVMAX = MAXC, NAMAX = 1, LEAFB = 32, RPN = MAXC + 2;
+  static constexpr bool AUX = false;
 };
 
 template <int CELL, int H, int MAXC>
 struct CLayout {
   using C = CCfg<CELL, MAXC>;
-  static constexpr size_t xl = (size_t)C::TMAX * (C::NVMAX + 1) * H, xb = (size_t)C::LEAFB * H;
+  static constexpr size_t xl = (size_t)C::TMAX * C::RPN * H, xb = (size_t)C::LEAFB * H;
+  static constexpr int SL = C::AUX ? 2 : 1;  // per-node slices (h [, aux])
   static constexpr size_t x_floats = xl > xb ? xl : xb;
   static constexpr size_t red_floats = (size_t)kRNW * C::NAMAX * C::TMAX * kRUG;
   static constexpr size_t red2_floats = (size_t)C::NAMAX * C::TMAX * kRUG;
   static constexpr size_t cv_floats = (size_t)C::TMAX * kMaxC * kRUG;
   // per node: h slice + aux slice (floats) and perm, label, maxc children, list (ints)
   static size_t bytes(int n, int maxc, int L) {
-    return sizeof(float) * (x_floats + red_floats + red2_floats + cv_floats + 2 * (size_t)kCUnits * n) +
+    return sizeof(float) * (x_floats + red_floats + red2_floats + cv_floats + SL * (size_t)kCUnits * n) +
            sizeof(int) * ((size_t)(3 + maxc) * n + 4 * (size_t)L + 64);
   }
 };
 
 // Max nodes the cluster path takes (per-node slices live in shared memory).
-constexpr int kClusterMaxN = 768;
+constexpr int kClusterMaxN = 1536;  // and the shared-memory check of the plan
 // Fused linearize + forward: count-table entries of the
 // in-kernel single-CTA linearizer, and its extra shared memory (ints): the
 // linearizer's arrays stand in for the prologue's perm/label/level arrays,
@@ -86,8 +94,8 @@ struct CS {  // shared-memory carve of one CTA
 };
 
 // Pull the full H-rows of `rows` (new ids, -1 = zeros) from the CS slices into
-// X (NV + 1 rows per node: the NV children, then their sum h~).
-template <int H, int NV>
+// X (RPN rows per node: the NV children, ..., their sum h~ in the last row).
+template <int H, int NV, int RPN = NV + 1>
 __device__ __forceinline__ void pull_rows(cg::cluster_group &cl, const CS &s, int cnt,
                                           const int (*rows)[kMaxC]) {
   constexpr int CSZ = H / kCUnits;
@@ -107,10 +115,10 @@ __device__ __forceinline__ void pull_rows(cg::cluster_group &cl, const CS &s, in
     float4 sum = v[0];
 #pragma unroll
     for (int j = 0; j < NV; j++) {
-      *reinterpret_cast<float4 *>(s.X + (size_t)(t * (NV + 1) + j) * H + peer * kCUnits + 4 * q) = v[j];
+      *reinterpret_cast<float4 *>(s.X + (size_t)(t * RPN + j) * H + peer * kCUnits + 4 * q) = v[j];
       if (j) { sum.x += v[j].x; sum.y += v[j].y; sum.z += v[j].z; sum.w += v[j].w; }
     }
-    *reinterpret_cast<float4 *>(s.X + (size_t)(t * (NV + 1) + NV) * H + peer * kCUnits + 4 * q) = sum;
+    *reinterpret_cast<float4 *>(s.X + (size_t)(t * RPN + RPN - 1) * H + peer * kCUnits + 4 * q) = sum;
   }
 }
 
@@ -188,7 +196,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   int *fint = nullptr;
   if constexpr (FUSED) {
     fint = reinterpret_cast<int *>(smem + Lay::x_floats + Lay::red_floats + Lay::red2_floats +
-                                   Lay::cv_floats + 2 * (size_t)kCUnits * n);
+                                   Lay::cv_floats + Lay::SL * (size_t)kCUnits * n);
     LinPrefetch pf{a.words, a.emb, H, a.V};
     const LinOut lo = lin_single_body(a.lin, fint, kFusedCnt, blockIdx.x == 0,
                                       fint + lin_sm_ints(n, maxc, kFusedCnt), pf);
@@ -216,7 +224,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   s.red2 = s.red + Lay::red_floats;
   s.cv = s.red2 + Lay::red2_floats;
   s.hsl = s.cv + Lay::cv_floats;
-  s.aux = s.hsl + (size_t)kCUnits * n;
+  s.aux = s.hsl + (size_t)kCUnits * n;  // TreeLSTM only (Lay::SL == 2)
   if constexpr (FUSED) {  // the linearizer's shared-memory results
     s.perm = ls.perm;
     s.lab = ls.sid;
@@ -227,7 +235,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     s.coff = s.list + n;
     s.ccur = s.coff + n + 1;
   } else {
-    s.perm = reinterpret_cast<int *>(s.aux + (size_t)kCUnits * n);
+    s.perm = reinterpret_cast<int *>(s.hsl + (size_t)Lay::SL * kCUnits * n);
     s.lab = s.perm + n;
     s.list = s.lab + n;
     s.chn = s.list + n;
@@ -341,10 +349,9 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
 
   // ---- leaf / projection phase ----------------------------------------------
   {
-    // TreeLSTM: leaves. DAG-RNN: every node (input projection P = W_x x + b;
-    // leaves finish with h = tanh(P)).
-    // TreeLSTM: this cluster's leaves (level 0); DAG-RNN: all its nodes
-    const int lb0 = 0, cnt = CELL == CX_DAGRNN ? s.coff[L] : s.coff[1 <= L - 1 ? 1 : L];
+    // this cluster's leaves (level 0). TreeLSTM: [i; o; u] = W_iou x + b;
+    // DAG-RNN: h = tanh(W_x x + b) (internal nodes add W_x x at their level)
+    const int lb0 = 0, cnt = s.coff[1];
     for (int b0 = lb0; b0 < cnt; b0 += LEAFB) {
       const int cntb = min(LEAFB, cnt - b0);
       if (tid < cntb) {
@@ -386,12 +393,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
             contract<RDagLeaf, H, T>(ctx, s.X + (size_t)t0 * H, w, sacc);
             if (t < cntt) {
               const int v = s_nodes[t0 + t];
-              const float p = sacc[0] + s_bias[u];
-              s.aux[(size_t)v * kCUnits + u] = p;
-              if (v >= first_leaf) {
-                const float hh = tanhf_(p);
-                s.hsl[(size_t)v * kCUnits + u] = hh;
-              }
+              s.hsl[(size_t)v * kCUnits + u] = tanhf_(sacc[0] + s_bias[u]);
             }
           }
           __syncthreads();
@@ -426,10 +428,30 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
         int v = s.list[lbase + t0 + tid];
         s_nodes[tid] = v;
         for (int k = 0; k < kMaxC; k++) s_rows[tid][k] = k < maxc ? s.chn[k * n + v] : -1;
+        if constexpr (CELL == CX_DAGRNN) {  // the node's input row (W_x x at this level)
+          const int own = s.perm[v];
+          int wd = __ldg(a.words + own);
+          if (wd < 0 || wd >= a.V) {
+            if (latch) {
+              if constexpr (FUSED) atomicMax(ferr, ~(((unsigned long long)CX_E_WORD_RANGE << 32) | (unsigned)own));
+              else latch_error(a.hdr, CX_E_WORD_RANGE, own);
+            }
+            wd = 0;
+          }
+          s_word[tid] = wd;
+        }
       }
       __syncthreads();
       if (t0 == 0 && l < 20) trace_mark(a, tb + 1);
-      pull_rows<H, Cfg::NVMAX>(cl, s, cntt, s_rows);
+      if constexpr (CELL == CX_DAGRNN) {  // x rows (L2; prefetched in the fused kernel)
+        constexpr int q4 = H / 4, RPN = Cfg::RPN;
+        for (int idx = tid; idx < cntt * q4; idx += blockDim.x) {
+          const int t = idx / q4, c = idx - t * q4;
+          *reinterpret_cast<float4 *>(s.X + (size_t)(t * RPN + MAXC) * H + 4 * c) =
+              ldcg4(a.emb + (size_t)s_word[t] * H + 4 * c);
+        }
+      }
+      pull_rows<H, Cfg::NVMAX, Cfg::RPN>(cl, s, cntt, s_rows);
       if constexpr (CELL == CX_TREELSTM) {
         for (int idx = tid; idx < cntt * MAXC * kCUnits; idx += blockDim.x) {
           int t = idx / (MAXC * kCUnits), r = idx - t * MAXC * kCUnits, k = r >> 4, uu = r & 15;
@@ -462,8 +484,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
           contract<CDagLevel<MAXC>, H, T, true>(ctx, s.X, w, sacc);
           if (t < cntt) {
             const int v = s_nodes[t];
-            const float hh = tanhf_(sacc[0] + s.aux[(size_t)v * kCUnits + u]);
-            s.hsl[(size_t)v * kCUnits + u] = hh;
+            s.hsl[(size_t)v * kCUnits + u] = tanhf_(sacc[0] + s_bias[u]);
           }
         }
         __syncthreads();
