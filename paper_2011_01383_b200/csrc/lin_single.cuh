@@ -191,28 +191,64 @@ __device__ __forceinline__ LinOut lin_single_body(const LinArgs &a, int *sm, int
       __syncthreads();
       L = s_round + 1;
     } else {
+      // each thread walks only its unfinished nodes (ids tid + j * nthr, a
+      // bitmask): a round costs one pass over the open frontier, not over n
+      const int J = (n + nthr - 1) / nthr;
+      unsigned todo = 0;
+      if (J <= 32) {
+#pragma unroll 1
+        for (int j = 0; j < J; j++) {
+          const int v = tid + j * nthr;
+          if (v < n && hgt[v] < 0) todo |= 1u << j;
+        }
+      }
       int r = 0;
       bool progress = true;
       while (progress) {
         r++;
         bool any = false;
+        if (J <= 32) {
+          unsigned t = todo;
+          while (t) {
+            const int j = __ffs(t) - 1;
+            t &= t - 1;
+            const int v = tid + j * nthr;
+            bool ok = true;
 #pragma unroll 1
-        for (int v = tid; v < n; v += nthr) {
-          if (hgt[v] >= 0) continue;
-          bool ok = true;
-#pragma unroll 1
-          for (int k = 0; k < maxc; k++) {
-            int c = ch[k * n + v];
-            if (c == -1) break;
-            int hc = hgt[c];
-            if (hc < 0 || hc >= r) {
-              ok = false;
-              break;
+            for (int k = 0; k < maxc; k++) {
+              const int c = ch[k * n + v];
+              if (c == -1) break;
+              const int hc = hgt[c];
+              if (hc < 0 || hc >= r) {
+                ok = false;
+                break;
+              }
+            }
+            if (ok) {
+              hgt[v] = r;
+              todo &= ~(1u << j);
+              any = true;
             }
           }
-          if (ok) {
-            hgt[v] = r;
-            any = true;
+        } else {
+#pragma unroll 1
+          for (int v = tid; v < n; v += nthr) {
+            if (hgt[v] >= 0) continue;
+            bool ok = true;
+#pragma unroll 1
+            for (int k = 0; k < maxc; k++) {
+              int c = ch[k * n + v];
+              if (c == -1) break;
+              int hc = hgt[c];
+              if (hc < 0 || hc >= r) {
+                ok = false;
+                break;
+              }
+            }
+            if (ok) {
+              hgt[v] = r;
+              any = true;
+            }
           }
         }
         progress = __syncthreads_or(any);
