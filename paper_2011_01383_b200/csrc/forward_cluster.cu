@@ -95,9 +95,8 @@ struct CS {  // shared-memory carve of one CTA
 
 // Pull the full H-rows of `rows` (new ids, -1 = zeros) from the CS slices into
 // X (RPN rows per node: the NV children, ..., their sum h~ in the last row).
-template <int H, int NV, int RPN = NV + 1>
-__device__ __forceinline__ void pull_rows(cg::cluster_group &cl, const CS &s, int cnt,
-                                          const int (*rows)[kMaxC]) {
+template <int H, int NV, int RPN = NV + 1, class ROW>
+__device__ __forceinline__ void pull_rows(cg::cluster_group &cl, const CS &s, int cnt, ROW row) {
   constexpr int CSZ = H / kCUnits;
   constexpr int Q = kCUnits / 4;  // float4 per slice
   const int total = cnt * CSZ * Q;
@@ -108,7 +107,7 @@ __device__ __forceinline__ void pull_rows(cg::cluster_group &cl, const CS &s, in
     float4 v[NV];
 #pragma unroll
     for (int j = 0; j < NV; j++) {
-      const int c = rows[t][j];
+      const int c = row(t, j);
       v[j] = c >= 0 ? *reinterpret_cast<const float4 *>(remote + (size_t)c * kCUnits + 4 * q)
                     : make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -138,7 +137,6 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   constexpr int TMAX = Cfg::TMAX;
   extern __shared__ __align__(16) float smem[];
   constexpr int LEAFB = Cfg::LEAFB;
-  __shared__ int s_rows[TMAX][kMaxC];
   __shared__ int s_nodes[LEAFB];
   __shared__ int s_word[LEAFB];
   __shared__ int s_cnt;
@@ -424,38 +422,33 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     if (l < 20) trace_mark(a, tb);
     for (int t0 = 0; t0 < cnt; t0 += TMAX) {
       const int cntt = min(TMAX, cnt - t0);
-      if (tid < cntt) {
-        int v = s.list[lbase + t0 + tid];
-        s_nodes[tid] = v;
-        for (int k = 0; k < kMaxC; k++) s_rows[tid][k] = k < maxc ? s.chn[k * n + v] : -1;
-        if constexpr (CELL == CX_DAGRNN) {  // the node's input row (W_x x at this level)
-          const int own = s.perm[v];
-          int wd = __ldg(a.words + own);
-          if (wd < 0 || wd >= a.V) {
-            if (latch) {
-              if constexpr (FUSED) atomicMax(ferr, ~(((unsigned long long)CX_E_WORD_RANGE << 32) | (unsigned)own));
-              else latch_error(a.hdr, CX_E_WORD_RANGE, own);
-            }
-            wd = 0;
-          }
-          s_word[tid] = wd;
-        }
-      }
-      __syncthreads();
+      // tile node t and its children come straight from the shared-memory
+      // level list and child table (no per-tile staging barrier)
+      const int *tl = s.list + lbase + t0;
+      auto child = [&](int t, int k) { return k < maxc ? s.chn[k * n + tl[t]] : -1; };
       if (t0 == 0 && l < 20) trace_mark(a, tb + 1);
       if constexpr (CELL == CX_DAGRNN) {  // x rows (L2; prefetched in the fused kernel)
         constexpr int q4 = H / 4, RPN = Cfg::RPN;
         for (int idx = tid; idx < cntt * q4; idx += blockDim.x) {
           const int t = idx / q4, c = idx - t * q4;
+          const int own = s.perm[tl[t]];
+          int wd = __ldg(a.words + own);
+          if (wd < 0 || wd >= a.V) {
+            if (latch && c == 0) {
+              if constexpr (FUSED) atomicMax(ferr, ~(((unsigned long long)CX_E_WORD_RANGE << 32) | (unsigned)own));
+              else latch_error(a.hdr, CX_E_WORD_RANGE, own);
+            }
+            wd = 0;
+          }
           *reinterpret_cast<float4 *>(s.X + (size_t)(t * RPN + MAXC) * H + 4 * c) =
-              ldcg4(a.emb + (size_t)s_word[t] * H + 4 * c);
+              ldcg4(a.emb + (size_t)wd * H + 4 * c);
         }
       }
-      pull_rows<H, Cfg::NVMAX, Cfg::RPN>(cl, s, cntt, s_rows);
+      pull_rows<H, Cfg::NVMAX, Cfg::RPN>(cl, s, cntt, child);
       if constexpr (CELL == CX_TREELSTM) {
         for (int idx = tid; idx < cntt * MAXC * kCUnits; idx += blockDim.x) {
           int t = idx / (MAXC * kCUnits), r = idx - t * MAXC * kCUnits, k = r >> 4, uu = r & 15;
-          int c = s_rows[t][k];
+          const int c = child(t, k);
           s.cv[(t * kMaxC + k) * kCUnits + uu] = c >= 0 ? s.aux[(size_t)c * kCUnits + uu] : 0.f;
         }
       }
@@ -469,12 +462,12 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
           contract<RLstmLevel<MAXC>, H, T, true>(ctx, s.X, w, sacc);
           if (t0 == 0 && l < 20) trace_mark(a, tb + 3);
           if (t < cntt) {
-            const int v = s_nodes[t];
+            const int v = tl[t];
             float cc = sigmoidf_(sacc[0] + s_bias[u]) * tanhf_(sacc[2] + s_bias[32 + u]);
             const float bf = s_bias[48 + u];
 #pragma unroll
             for (int k = 0; k < MAXC; k++)
-              if (s_rows[t][k] >= 0) cc += sigmoidf_(sacc[3 + k] + bf) * s.cv[(t * kMaxC + k) * kCUnits + u];
+              if (child(t, k) >= 0) cc += sigmoidf_(sacc[3 + k] + bf) * s.cv[(t * kMaxC + k) * kCUnits + u];
             float hh = sigmoidf_(sacc[1] + s_bias[16 + u]) * tanhf_(cc);
             s.hsl[(size_t)v * kCUnits + u] = hh;
             s.aux[(size_t)v * kCUnits + u] = cc;
@@ -483,7 +476,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
           float sacc[1];
           contract<CDagLevel<MAXC>, H, T, true>(ctx, s.X, w, sacc);
           if (t < cntt) {
-            const int v = s_nodes[t];
+            const int v = tl[t];
             s.hsl[(size_t)v * kCUnits + u] = tanhf_(sacc[0] + s_bias[u]);
           }
         }
