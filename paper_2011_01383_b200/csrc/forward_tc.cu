@@ -109,9 +109,12 @@ struct TcCfg {
   // CTAs that own different unit slices of the same node tiles form a cluster
   // of CL; each fetches 1/CL of every stage and multicasts it to all
   static constexpr int GU = H / U;
-  // one CTA per cluster: measured, cluster-multicast gathers were gated by the
-  // slowest CTA and TMA gather4 is issue-bound; TreeLSTM loads contiguous
-  // tiles, the others gather with per-CTA cp.async
+  // One CTA per cluster. Measured: cluster-multicast gathers were gated by the
+  // slowest CTA and TMA gather4 is issue-bound; multicasting TreeLSTM's
+  // contiguous tiles over the GU unit-group CTAs (CL = GU, stage k issued by
+  // rank k mod CL, every CTA expecting the stage's bytes) was correct but
+  // slower: only 15 clusters of 8 are co-resident (120 CTAs instead of 144;
+  // b4096 forward 293 -> 340 us).
   static constexpr int CL = 1;
   static constexpr int FEEDW = LSTM ? 1 : 4;             // feeding warps
   static constexpr int META0 = kFeed0 + FEEDW;           // first bookkeeping warp

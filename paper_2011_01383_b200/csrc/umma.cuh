@@ -147,8 +147,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, unsigned parity) {
       : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   return ok != 0;
 }
+// Watchdog: a phase that never completes (a lost arrival / transaction) traps
+// (sticky launch error, reported as CX_E_CUDA) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  unsigned spins = 0;
   while (!mbar_try_wait(bar, parity)) {
+    if (++spins > (1u << 26)) __trap();
   }
 }
 
