@@ -34,7 +34,7 @@ using namespace rw;
 template <int H, int MAXC>
 struct RTreeLstm {
   static constexpr int kPhases = 1;
-  using M = TileMetaT<2 * RCfg<CX_TREELSTM, H, MAXC>::TMAX>;
+  using M = TileMetaT<kLeafBlock>;
   __device__ static int leaf_gates(const FwdArgs &a, Gate *g) {
     g[0] = {a.w[0], 0, H, 0}; g[1] = {a.w[0], H, H, 0}; g[2] = {a.w[0], 2 * H, H, 0};
     return 3;
@@ -123,7 +123,7 @@ struct RTreeLstm {
 template <int H, int MAXC>
 struct RTreeGru {
   static constexpr int kPhases = 2;
-  using M = TileMetaT<2 * RCfg<CX_TREEGRU, H, MAXC>::TMAX>;
+  using M = TileMetaT<kLeafBlock>;
   __device__ static int leaf_gates(const FwdArgs &a, Gate *g) {
     g[0] = {a.w[0], 0, H, 0}; g[1] = {a.w[0], H, H, 0};
     return 2;
@@ -218,7 +218,7 @@ struct RTreeGru {
 template <int H, int MAXC>
 struct RTreeFc {
   static constexpr int kPhases = 1;
-  using M = TileMetaT<2 * RCfg<CX_TREEFC, H, MAXC>::TMAX>;
+  using M = TileMetaT<kLeafBlock>;
   __device__ static int leaf_gates(const FwdArgs &, Gate *) { return 0; }
   __device__ static int level_gates(const FwdArgs &a, Gate *g) {
     g[0] = {a.w[0], 0, 2 * H, 0}; g[1] = {a.w[0], 0, 2 * H, H};
@@ -263,7 +263,7 @@ struct RTreeFc {
 template <int H, int MAXC>
 struct RDagRnn {
   static constexpr int kPhases = 1;
-  using M = TileMetaT<2 * RCfg<CX_DAGRNN, H, MAXC>::TMAX>;
+  using M = TileMetaT<kLeafBlock>;
   // gates {W_x, U} resident through leaves and levels (input projections are
   // fused into each level instead of a separate all-node GEMM)
   __device__ static int leaf_gates(const FwdArgs &a, Gate *g) {
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kRThreads, 1) rw_kernel(FwdArgs a) {
   float w[4][KC];
   Gate gs[4];
   // ---- leaf phase (specialised leaf loop nest) ------------------
-  // Leaves are processed in blocks of up to 2 TMAX: one bookkeeping pass and one
+  // Leaves are processed in blocks of up to kLeafBlock: one bookkeeping pass and one
   // Emb gather per block (the first block's overlap the weight loads).
   {
     int ng = C::leaf_gates(a, gs);
@@ -377,8 +377,8 @@ __global__ void __launch_bounds__(kRThreads, 1) rw_kernel(FwdArgs a) {
     chunk_of(n - lo0, a.Gn, gn, lo, hi);
     typename C::Leaf f{ctx, &meta, w, 0};
     f.c.tslot = a.trace ? 59 : -1;
-    for (int b0 = lo0 + lo; b0 < lo0 + hi; b0 += 2 * Cfg::TMAX) {
-      const int cntb = min(2 * Cfg::TMAX, lo0 + hi - b0);
+    for (int b0 = lo0 + lo; b0 < lo0 + hi; b0 += kLeafBlock) {
+      const int cntb = min(kLeafBlock, lo0 + hi - b0);
       __syncthreads();  // previous block's readers of meta / X are done
       f.meta(b0, cntb);
       __syncthreads();

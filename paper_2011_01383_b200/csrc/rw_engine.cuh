@@ -19,6 +19,7 @@ using namespace fwd;
 constexpr int kRUG = 16;            // hidden units per CTA
 constexpr int kRNW = 16;            // warps per CTA
 constexpr int kRThreads = 32 * kRNW;
+constexpr int kLeafBlock = 32;      // leaves per bookkeeping + gather block (rw kernel)
 
 // ---------------------------------------------------------------------------
 // Product tables. Vectors 0..NV-1 are gathered rows; vector NV is h~, the sum
@@ -99,7 +100,11 @@ struct RCfg<CX_DAGRNN, H, MAXC> {
 template <int CELL, int H, int MAXC>
 struct RLayout {
   using C = RCfg<CELL, H, MAXC>;
-  static constexpr size_t x_floats = (size_t)C::TMAX * (C::NVMAX > 2 ? C::NVMAX : 2) * H;
+  // X holds a level tile's gathered rows, or a leaf block of kLeafBlock rows
+  // (one bookkeeping pass + one Emb gather per block; fewer, larger blocks
+  // put fewer dependent global round trips on the leaf phase's path)
+  static constexpr size_t tile_rows = (size_t)C::TMAX * (C::NVMAX > 2 ? C::NVMAX : 2);
+  static constexpr size_t x_floats = (tile_rows > kLeafBlock ? tile_rows : kLeafBlock) * H;
   static constexpr size_t red_floats = (size_t)kRNW * C::NAMAX * C::TMAX * kRUG;
   static constexpr size_t red2_floats = (size_t)C::NAMAX * C::TMAX * kRUG;
   static constexpr size_t cv_floats = (size_t)C::TMAX * kMaxC * kRUG;
