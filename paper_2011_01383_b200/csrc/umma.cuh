@@ -147,13 +147,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, unsigned parity) {
       : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   return ok != 0;
 }
-// Watchdog: a phase that never completes (a lost arrival / transaction) traps
-// (sticky launch error, reported as CX_E_CUDA) instead of hanging the GPU.
+// Watchdog (build with -DCX_MBAR_WATCHDOG while developing): a phase that
+// never completes (a lost arrival / transaction) traps instead of hanging.
+// Off by default: the counter measurably slowed the bf16 kernels' waits.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+#ifdef CX_MBAR_WATCHDOG
   unsigned spins = 0;
   while (!mbar_try_wait(bar, parity)) {
     if (++spins > (1u << 26)) __trap();
   }
+#else
+  while (!mbar_try_wait(bar, parity)) {
+  }
+#endif
 }
 
 // Arrive once on an mbarrier and add `bytes` to its expected transaction count.
