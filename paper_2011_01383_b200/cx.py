@@ -288,6 +288,45 @@ def linearize_forward(children: torch.Tensor, kind: int, cell: int, hidden: int,
     return out, h_out, aux_out, root_out
 
 
+class LinearizeForwardPlan:
+    """A prepared cx_linearize_forward call for repeated batches of one shape
+    (serving): outputs, workspace and the marshalled C arguments are built
+    once; each call() is a single C call on the same device buffers. The
+    caller refreshes `children` / `word_ids` in place (e.g. an async H2D copy
+    on `stream`) before calling. Same results as linearize_forward()."""
+
+    def __init__(self, children: torch.Tensor, kind: int, cell: int, hidden: int, weights,
+                 emb: torch.Tensor, word_ids: torch.Tensor, dtype: int = F32,
+                 want_aux: bool = False, num_roots=None, stream=None):
+        if children.dim() != 2 or children.dtype != torch.int32 or not children.is_cuda \
+                or not children.is_contiguous():
+            raise ValueError("children must be a contiguous int32 CUDA tensor [max_children, n]")
+        maxc, n = children.shape
+        dev = emb.device
+        self.children, self.word_ids, self.emb = children, word_ids, emb
+        self.weights = list(weights)  # keep the tensors alive
+        self.lin = alloc_linearization(n, maxc, kind, children.device)
+        self.lin.kind = kind
+        self.h_out, self.aux_out, self.root_out = _outputs(cell, hidden, n, dev, want_aux,
+                                                           num_roots, None, None, None)
+        self._w = _weights(cell, self.weights)
+        self._m = _model(cell, hidden, emb.shape[0], dtype)
+        L = lib()
+        need = L.cx_linearize_forward_workspace_bytes(ctypes.byref(self._m), n, maxc)
+        self.workspace = torch.zeros(max(need, 1), dtype=torch.uint8, device=dev)
+        self._fn = L.cx_linearize_forward
+        self._args = (_ptr(children), n, maxc, kind, ctypes.byref(self._m), ctypes.byref(self._w),
+                      _ptr(emb), _ptr(word_ids), ctypes.byref(self.lin.c), _ptr(self.h_out),
+                      _ptr(self.aux_out), _ptr(self.root_out), _ptr(self.workspace),
+                      self.workspace.numel(), _stream(stream))
+
+    def __call__(self):
+        st = self._fn(*self._args)
+        if st != OK:
+            raise CxError(st, "cx_linearize_forward")
+        return self.h_out, self.aux_out, self.root_out
+
+
 def forward(cell: int, hidden: int, weights, emb: torch.Tensor, word_ids: torch.Tensor,
             lin: Linearization, dtype: int = F32, want_aux: bool = False, num_roots=None,
             h_out=None, aux_out=None, root_out=None, stream=None, workspace=None):

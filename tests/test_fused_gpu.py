@@ -235,3 +235,24 @@ def test_fused_fuzz(cx, seed):
     lin_s = cx.linearize(chd, kind)
     h_s, _, r_s = cx.forward(cell, H, ws_dev, embd, wdd, lin_s, num_roots=R)
     assert torch.equal(h_f, h_s) and torch.equal(r_f, r_s)
+
+
+def test_plan_matches_call(cx):
+    """LinearizeForwardPlan (prepared call) == linearize_forward, also after the
+    input buffers are refreshed in place."""
+    w = synth.workload("cfg2_treelstm_b10")
+    cell, H, V = w["cell"], w["hidden"], w["vocab"]
+    words, emb, ws_np, ws_dev = _case(cell, H, V, w["children"], w["kind"], w["seed"])
+    chd, wdd, embd = dev_i32(w["children"]), dev_i32(words), dev_f32(emb)
+    plan = cx.LinearizeForwardPlan(chd, w["kind"], cell, H, ws_dev, embd, wdd,
+                                   num_roots=w["batch"])
+    h, _, r = plan()
+    lin2, h2, _, r2 = cx.linearize_forward(chd, w["kind"], cell, H, ws_dev, embd, wdd,
+                                           num_roots=w["batch"])
+    assert cx.status(plan.lin) == (0, -1)
+    assert torch.equal(h, h2) and torch.equal(r, r2)
+    words2 = synth.word_ids(w["children"], V, 99)
+    wdd.copy_(dev_i32(words2))
+    h, _, _ = plan()
+    h3 = cx.linearize_forward(chd, w["kind"], cell, H, ws_dev, embd, dev_i32(words2))[1]
+    assert torch.equal(h, h3) and not torch.equal(h3, h2)
