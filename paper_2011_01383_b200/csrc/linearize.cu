@@ -598,15 +598,38 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
         a.sid[i] = __ldcg(&a.sid[__ldcg(&a.inv[v])]);
       }
     } else {  // smallest root index reaching the node, propagated top-down
+      // level ranges cached in shared memory (free after the sort): a round is
+      // then one barrier plus one round trip (sid and all children loaded
+      // together) instead of three dependent ones
+      const bool cache = L <= kLinTabLevels;
+      if (cache) {
+        for (int l = threadIdx.x; l < L; l += blockDim.x) {
+          lsm[l] = __ldcg(&a.lbeg[l]);
+          lsm[kLinTabLevels + l] = __ldcg(&a.lsize[l]);
+        }
+        __syncthreads();
+      }
       for (int l = L - 1; l >= 1; l--) {
         grid_sync(a.bar, G, epoch);
-        const int b = __ldcg(&a.lbeg[l]), e = b + __ldcg(&a.lsize[l]);
+        const int b = cache ? lsm[l] : __ldcg(&a.lbeg[l]);
+        const int e = b + (cache ? lsm[kLinTabLevels + l] : __ldcg(&a.lsize[l]));
         for (int i = b + tid; i < e; i += nthr) {
           const int si = __ldcg(&a.sid[i]);
-          for (int k = 0; k < maxc; k++) {
-            int c = __ldcg(&a.chn[(long long)k * n + i]);
-            if (c == -1) break;
-            atomicMin(&a.sid[c], si);
+          if (maxc <= 4) {
+            int cc[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) cc[k] = k < maxc ? __ldcg(&a.chn[(long long)k * n + i]) : -1;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              if (cc[k] == -1) break;
+              atomicMin(&a.sid[cc[k]], si);
+            }
+          } else {
+            for (int k = 0; k < maxc; k++) {
+              int c = __ldcg(&a.chn[(long long)k * n + i]);
+              if (c == -1) break;
+              atomicMin(&a.sid[c], si);
+            }
           }
         }
       }
