@@ -36,6 +36,9 @@ constexpr int kLinThreads = 1024;   // multi-CTA path
 constexpr int kLinSingleThreads = 512;
 constexpr int kSegMin = 256;
 constexpr int kLinTabLevels = 256;  // levels handled by the block-chunked sort (lin_kernel)
+#ifndef CX_JAC_SLEEP
+#define CX_JAC_SLEEP 0  // ns between polls of the async DAG height pass (measured: 0 < 32 < 200)
+#endif
 constexpr int kJacNodes = 4, kJacMaxC = 4;  // DAG Jacobi rounds: per-thread register cache
 constexpr size_t kLinMultiSmem = sizeof(int) * (2 + 32) * kLinTabLevels;
 
@@ -252,23 +255,35 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
         int hmax = 0;
         bool stalled = false;
         unsigned spins = 0, todo_a = todo;
+        // children already seen final are not polled again (their height is
+        // kept in hk): fewer L2 requests per poll, so the hand-offs on the
+        // critical path are served faster
+        unsigned known = 0;  // bit j * kJacMaxC + k
+        int hk[kJacNodes];
+#pragma unroll
+        for (int j = 0; j < kJacNodes; j++) hk[j] = -1;
         while (todo_a) {
           bool prog = false;
 #pragma unroll
           for (int j = 0; j < kJacNodes; j++) {
             if (!(todo_a & (1u << j))) continue;
-            int hm = -1;
             bool ok = true;
 #pragma unroll
             for (int k = 0; k < kJacMaxC; k++) {
               if (cc[j][k] < 0) break;
+              const unsigned bit = 1u << (j * kJacMaxC + k);
+              if (known & bit) continue;
               const int hc = __ldcg(&hgt[cc[j][k]]);
-              ok = ok && hc >= 0;
-              hm = max(hm, hc);
+              if (hc >= 0) {
+                known |= bit;
+                hk[j] = max(hk[j], hc);
+              } else {
+                ok = false;
+              }
             }
             if (ok) {
-              __stcg(&hgt[cv[j]], hm + 1);
-              hmax = max(hmax, hm + 1);
+              __stcg(&hgt[cv[j]], hk[j] + 1);
+              hmax = max(hmax, hk[j] + 1);
               todo_a &= ~(1u << j);
               prog = true;
             }
@@ -280,7 +295,7 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
               stalled = true;
               break;
             }
-            __nanosleep(32);
+            __nanosleep(CX_JAC_SLEEP);
           }
         }
         for (int o = 16; o; o >>= 1) hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
