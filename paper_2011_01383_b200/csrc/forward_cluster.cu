@@ -52,7 +52,11 @@ struct CCfg;
 // of keeping its projection, which halves the per-node footprint)
 template <int MAXC>
 struct CCfg<CX_TREELSTM, MAXC> {
-  static constexpr int TMAX = 8, NVMAX = MAXC, NAMAX = 3 + MAXC, LEAFB = 48, RPN = MAXC + 1;
+  // LEAFB: leaves per bookkeeping + gather block; sequences (MAXC = 1) have
+  // one leaf per chain, and the smaller X buffer lets 1000-node chain batches
+  // keep their per-node slices on chip
+  static constexpr int TMAX = 8, NVMAX = MAXC, NAMAX = 3 + MAXC, LEAFB = MAXC == 1 ? 16 : 48,
+                       RPN = MAXC + 1;
   static constexpr bool AUX = true;
 };
 template <int MAXC>
