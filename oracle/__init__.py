@@ -7,16 +7,23 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline and
 The arithmetic lives in oracle.c (plain C99, fp64); this module only marshals
 numpy arrays through ctypes. See oracle.h for the citations.
 
-Parity status per function (DESIGN.md §Oracle pins):
-  linearize        pinned (worked examples S:228/S:247, closed forms, brute force, invariants)
-  forward TreeRNN  pinned (S:471 worked example, tanh(2t) closed form)
-  forward TreeFC   pinned (identity reduction to TreeRNN)
-  forward TreeLSTM pinned (torch.nn.LSTMCell on chains, zero-weight closed form)
-  forward TreeGRU  pinned (torch.nn.GRUCell on chains with r == 1)
-  forward DAG-RNN  pinned (torch.nn.RNNCell on 1xn grids)
-  forward MV-RNN   pinned (identity reduction to TreeFC) -- the per-node
-                   matrix path (A != I) is pinned only by a brute-force H=1
-                   hand evaluation.
+Parity status per function (every pin is a -m "not gpu" test):
+  linearize        pinned: worked examples S:228/S:247 (tests/golden/worked_examples.json),
+                   closed forms (perfect trees, grids, chains), brute force over all
+                   labellings (N <= 6), invariants on fuzz cases
+  forward, all 7 cells (TreeRNN, TreeFC, TreeLSTM, TreeGRU, SimpleTreeGRU, MV-RNN,
+  DAG-RNN)         pinned by brute force: tests/golden/brute_force.json, written by
+                   tools/gen_goldens.py in 50-digit mpmath from hand-typed inputs at
+                   H = 1-2 on <= 7-node structures (asymmetric, non-identity matrices,
+                   so the MV-RNN pairing [B a; A b] and the TreeGRU per-child reset gate
+                   are distinguished from their alternatives)
+  plus             S:471 worked example and the tanh(2t) closed form (TreeRNN); identity
+                   reduction TreeFC == TreeRNN and MV-RNN == TreeFC; torch LSTMCell /
+                   GRUCell / RNNCell on chains; W = U = 0 TreeLSTM closed form
+The mutation check (tests/test_oracle_mutations.py) rebuilds oracle.c with each of 14
+plausible bugs (-DCX_ORACLE_MUTATION=k) and asserts that some pin fails for every k.
+Absolute agreement with Cortex's own trained models is unpinnable (the paper prints no
+hidden-state values).
 """
 from __future__ import annotations
 
@@ -28,7 +35,9 @@ import threading
 import numpy as np
 
 _DIR = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_DIR, "liboracle.so")
+# CX_ORACLE_MUTATION=k (mutation check only) builds a separate, deliberately broken library
+_MUTATION = int(os.environ.get("CX_ORACLE_MUTATION", "0") or 0)
+_LIB_PATH = os.path.join(_DIR, "liboracle.so" if not _MUTATION else f"liboracle_mut{_MUTATION}.so")
 _SRC = [os.path.join(_DIR, "oracle.c"), os.path.join(_DIR, "oracle.h")]
 _lock = threading.Lock()
 _lib = None
@@ -43,7 +52,7 @@ def build(force: bool = False) -> str:
     if stale:
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-std=c99", "-O2", "-fPIC", "-shared", "-Wall",
-                               "-o", tmp, _SRC[0], "-lm"])
+                               f"-DCX_ORACLE_MUTATION={_MUTATION}", "-o", tmp, _SRC[0], "-lm"])
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
 

@@ -9,6 +9,11 @@
  * reorders independent work. So the forward oracle is the recursive
  * definition itself, and the linearization oracle is the definition of the
  * numbering written out with naive loops.
+ *
+ * MUT(k): the mutation check (tests/test_oracle_mutations.py) rebuilds this
+ * file with -DCX_ORACLE_MUTATION=k, each k one plausible bug (a dropped term,
+ * a swapped operand, a wrong index), and asserts that some pin fails. The
+ * default build has CX_ORACLE_MUTATION = 0: every MUT(k) is false.
  */
 #include "oracle.h"
 
@@ -16,6 +21,11 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+
+#ifndef CX_ORACLE_MUTATION
+#define CX_ORACLE_MUTATION 0
+#endif
+#define MUT(k) (CX_ORACLE_MUTATION == (k))
 
 /* ------------------------------------------------------------------------ */
 /* error latch: lowest (code, node) wins (SURVEY §8(c) "Error reporting")    */
@@ -152,14 +162,17 @@ int oracle_linearize(const int32_t *children, int32_t n, int32_t maxc, int32_t k
   for (int32_t v = 0; v < n; v++) level_size[h[v]]++;
   int32_t acc = 0, maxsz = 0;
   for (int32_t l = L - 1; l >= 0; l--) {
+    if (MUT(10)) { level_begin[L - 1 - l] = acc; acc += level_size[L - 1 - l]; continue; }
     level_begin[l] = acc;
     acc += level_size[l];
     if (level_size[l] > maxsz) maxsz = level_size[l];
   }
   int32_t next = 0;
   for (int32_t l = L - 1; l >= 0; l--)
-    for (int32_t v = 0; v < n; v++)
-      if (h[v] == l) perm[next++] = v;
+    for (int32_t v = 0; v < n; v++) {
+      const int32_t u = MUT(9) ? n - 1 - v : v;
+      if (h[u] == l) perm[next++] = u;
+    }
   for (int32_t i = 0; i < n; i++) inv[perm[i]] = i;
   for (int k = 0; k < maxc; k++)
     for (int32_t i = 0; i < n; i++) {
@@ -285,8 +298,9 @@ static void eval_node(fwd_ctx *F, int32_t v) {
       const double *hr = F->h + (int64_t)F->ch[(int64_t)F->n + v] * H;
       for (int r = 0; r < H; r++) {
         double s = 0.0;
-        for (int k = 0; k < H; k++) s += (double)W[0][(int64_t)r * 2 * H + k] * hl[k];
-        for (int k = 0; k < H; k++) s += (double)W[0][(int64_t)r * 2 * H + H + k] * hr[k];
+        const double *h0 = MUT(6) ? hr : hl, *h1 = MUT(6) ? hl : hr;
+        for (int k = 0; k < H; k++) s += (double)W[0][(int64_t)r * 2 * H + k] * h0[k];
+        for (int k = 0; k < H; k++) s += (double)W[0][(int64_t)r * 2 * H + H + k] * h1[k];
         hv[r] = tanh(s + (double)W[1][r]);
       }
     }
@@ -301,11 +315,13 @@ static void eval_node(fwd_ctx *F, int32_t v) {
       matvec(W[1], H, 0, 0, 3 * H, H, ht, g);
     }
     for (int r = 0; r < 3 * H; r++) g[r] += (double)W[2][r];
-    for (int i = 0; i < H; i++) cv[i] = sigm(g[i]) * tanh(g[2 * H + i]);
+    for (int i = 0; i < H; i++)
+      cv[i] = sigm(g[i]) * (MUT(8) && nc == 0 ? sigm(g[2 * H + i]) : tanh(g[2 * H + i]));
     for (int k = 0; k < nc; k++) { /* f_k = sigma(U_f h_k + b_f); c += f_k * c_k */
       int32_t ck = F->ch[(int64_t)k * F->n + v];
       double *f = g + 3 * H; /* reuse the tail of the 4H scratch */
-      matvec(W[3], H, 0, 0, H, H, F->h + (int64_t)ck * H, f);
+      matvec(W[3], H, 0, 0, H, H, MUT(1) ? ht : F->h + (int64_t)ck * H, f);
+      if (MUT(13)) ck = F->ch[(int64_t)((k + 1) % nc) * F->n + v];
       for (int i = 0; i < H; i++)
         cv[i] += sigm(f[i] + (double)W[4][i]) * F->c[(int64_t)ck * H + i];
     }
@@ -313,7 +329,8 @@ static void eval_node(fwd_ctx *F, int32_t v) {
     break;
   }
 
-  case OR_TREEGRU: { /* Q3: child-sum TreeGRU, reset gate per child before U_h */
+  case OR_TREEGRU:         /* Q3: child-sum TreeGRU, reset gate per child before U_h */
+  case OR_SIMPLETREEGRU: { /* Q24 (footnote P:1638-1640): h = (1 - z) h' at internal nodes */
     double *z = g, *s = g + H, *t = g + 2 * H, *r = g + 3 * H;
     if (nc == 0) { /* z = sigma(W_z x + b_z); g = tanh(W_h x + b_h); h = (1-z) g */
       if (!load_x(F, v, x)) { for (int i = 0; i < H; i++) hv[i] = 0.0; return; }
@@ -322,21 +339,25 @@ static void eval_node(fwd_ctx *F, int32_t v) {
       for (int i = 0; i < H; i++) {
         double zz = sigm(z[i] + (double)W[4][i]);
         double gg = tanh(t[i] + (double)W[6][i]);
-        hv[i] = (1.0 - zz) * gg;
+        hv[i] = MUT(14) ? zz * gg : (1.0 - zz) * gg;
       }
     } else {
       matvec(W[1], H, 0, 0, H, H, ht, z);               /* U_z h~ */
       for (int i = 0; i < H; i++) s[i] = 0.0;
       for (int k = 0; k < nc; k++) {                    /* s = sum_k r_k * h_k */
         const double *hk = F->h + (int64_t)F->ch[(int64_t)k * F->n + v] * H;
-        matvec(W[2], H, 0, 0, H, H, hk, r);             /* U_r h_k */
-        for (int i = 0; i < H; i++) s[i] += sigm(r[i] + (double)W[5][i]) * hk[i];
+        const double *rk = MUT(5) ? ht : hk;             /* (mutation: reset on h~) */
+        matvec(W[2], H, 0, 0, H, H, rk, r);             /* U_r h_k */
+        for (int i = 0; i < H; i++) s[i] += sigm(r[i] + (double)W[5][i]) * rk[i];
+        if (MUT(5)) break;
       }
       matvec(W[3], H, 0, 0, H, H, s, t);                /* U_h s */
       for (int i = 0; i < H; i++) {
         double zz = sigm(z[i] + (double)W[4][i]);
         double gg = tanh(t[i] + (double)W[6][i]);
-        hv[i] = zz * ht[i] + (1.0 - zz) * gg;
+        if (F->cell == OR_SIMPLETREEGRU && !MUT(11)) hv[i] = (1.0 - zz) * gg;
+        else if (MUT(3)) hv[i] = (1.0 - zz) * ht[i] + zz * gg;
+        else hv[i] = zz * ht[i] + (1.0 - zz) * gg;
       }
     }
     break;
@@ -360,8 +381,10 @@ static void eval_node(fwd_ctx *F, int32_t v) {
       double *p = g; /* [B a; A b], 2H */
       for (int i = 0; i < H; i++) {
         double s1 = 0.0, s2 = 0.0;
-        for (int k = 0; k < H; k++) s1 += Br[(int64_t)i * H + k] * a[k];
-        for (int k = 0; k < H; k++) s2 += Al[(int64_t)i * H + k] * b[k];
+        const double *m1 = MUT(2) ? Al : Br, *m2 = MUT(2) ? Br : Al;
+        for (int k = 0; k < H; k++)
+          s1 += (MUT(12) ? m1[(int64_t)k * H + i] : m1[(int64_t)i * H + k]) * a[k];
+        for (int k = 0; k < H; k++) s2 += m2[(int64_t)i * H + k] * b[k];
         p[i] = s1; p[H + i] = s2;
       }
       for (int i = 0; i < H; i++) {
@@ -372,8 +395,10 @@ static void eval_node(fwd_ctx *F, int32_t v) {
       for (int i = 0; i < H; i++)
         for (int j = 0; j < H; j++) {
           double s = 0.0;
-          for (int k = 0; k < H; k++) s += (double)W[3][(int64_t)i * 2 * H + k] * Al[(int64_t)k * H + j];
-          for (int k = 0; k < H; k++) s += (double)W[3][(int64_t)i * 2 * H + H + k] * Br[(int64_t)k * H + j];
+          for (int k = 0; k < H; k++)
+            s += (double)W[3][(int64_t)i * 2 * H + k] * (MUT(4) ? Al[(int64_t)j * H + k] : Al[(int64_t)k * H + j]);
+          for (int k = 0; k < H; k++)
+            s += (double)W[3][(int64_t)i * 2 * H + H + k] * (MUT(4) ? Br[(int64_t)j * H + k] : Br[(int64_t)k * H + j]);
           Av[(int64_t)i * H + j] = s;
         }
     }
@@ -383,6 +408,7 @@ static void eval_node(fwd_ctx *F, int32_t v) {
   case OR_DAGRNN: { /* Q8: h = tanh(W_x x + U h~ + b), every node has an input */
     if (!load_x(F, v, x)) { for (int i = 0; i < H; i++) hv[i] = 0.0; return; }
     matvec(W[0], H, 0, 0, H, H, x, g);
+    if (MUT(7) && nc > 0) for (int i = 0; i < H; i++) g[i] = 0.0;
     matvec(W[1], H, 0, 0, H, H, ht, g + H);
     for (int i = 0; i < H; i++) hv[i] = tanh(g[i] + g[H + i] + (double)W[2][i]);
     break;

@@ -22,7 +22,7 @@ enum {
 };
 enum { OR_SEQUENCE = 0, OR_TREE = 1, OR_DAG = 2 };
 enum { OR_TREERNN = 0, OR_TREEFC = 1, OR_TREELSTM = 2, OR_TREEGRU = 3,
-       OR_MVRNN = 4, OR_DAGRNN = 5 };
+       OR_MVRNN = 4, OR_DAGRNN = 5, OR_SIMPLETREEGRU = 6 };
 
 typedef struct {
   int32_t status, bad_node;

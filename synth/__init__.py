@@ -31,9 +31,10 @@ MASK64 = (1 << 64) - 1
 P_STRUCT, P_WORDS, P_EMB, P_WEIGHTS, P_MW = 1, 2, 3, 4, 5
 
 # cell ids, identical to cx_cell in include/cx.h
-TREERNN, TREEFC, TREELSTM, TREEGRU, MVRNN, DAGRNN = range(6)
+TREERNN, TREEFC, TREELSTM, TREEGRU, MVRNN, DAGRNN, SIMPLETREEGRU = range(7)
 CELL_NAMES = {TREERNN: "treernn", TREEFC: "treefc", TREELSTM: "treelstm",
-              TREEGRU: "treegru", MVRNN: "mvrnn", DAGRNN: "dagrnn"}
+              TREEGRU: "treegru", MVRNN: "mvrnn", DAGRNN: "dagrnn",
+              SIMPLETREEGRU: "simpletreegru"}
 # structure kinds, identical to cx_kind
 SEQUENCE, TREE, DAG = 0, 1, 2
 
@@ -254,7 +255,7 @@ def weight_shapes(cell: int, hidden: int, vocab: int):
     if cell == TREELSTM:
         return [("W_iou", (3 * H, H), H), ("U_iou", (3 * H, H), H), ("b_iou", (3 * H,), None),
                 ("U_f", (H, H), H), ("b_f", (H,), None)]
-    if cell == TREEGRU:
+    if cell in (TREEGRU, SIMPLETREEGRU):  # SimpleTreeGRU: same parameters
         return [("W_zh", (2 * H, H), H), ("U_z", (H, H), H), ("U_r", (H, H), H), ("U_h", (H, H), H),
                 ("b_z", (H,), None), ("b_r", (H,), None), ("b_h", (H,), None)]
     if cell == MVRNN:
