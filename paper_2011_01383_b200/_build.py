@@ -13,11 +13,15 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "build")
-LIB = os.path.join(PKG, "libcx.so")
+# CX_TRACE=1 selects the debug timeline build (-DCX_TRACE, libcx_trace.so, used by
+# tools/trace_*.py); the default product library has no trace code on the hot path.
+TRACE = os.environ.get("CX_TRACE", "0") not in ("", "0")
+OBJ = os.path.join(PKG, "build_trace" if TRACE else "build")
+LIB = os.path.join(PKG, "libcx_trace.so" if TRACE else "libcx.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "177"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "177"] + \
+    (["-DCX_TRACE"] if TRACE else [])
 
 
 def sources():

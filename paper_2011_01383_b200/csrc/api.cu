@@ -184,6 +184,8 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
   a.Gu = Gu;
   {
     std::lock_guard<std::mutex> lk(g_mu);
+    const char *pe = std::getenv("CX_PUSH");
+    a.push_off = pe && pe[0] == '0';
     a.trace = g_trace;
     a.trace_slots = g_trace_slots;
   }

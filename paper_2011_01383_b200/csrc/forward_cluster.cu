@@ -55,7 +55,7 @@ struct CCfg<CX_TREELSTM, MAXC> {
   // LEAFB: leaves per bookkeeping + gather block; sequences (MAXC = 1) have
   // one leaf per chain, and the smaller X buffer lets 1000-node chain batches
   // keep their per-node slices on chip
-  static constexpr int TMAX = 8, NVMAX = MAXC, NAMAX = 3 + MAXC, LEAFB = MAXC == 1 ? 16 : 48,
+  static constexpr int TMAX = 8, NVMAX = MAXC, NAMAX = 3 + MAXC, LEAFB = MAXC == 1 ? 16 : 24,
                        RPN = MAXC + 1;
   static constexpr bool AUX = true;
 };
@@ -69,15 +69,20 @@ template <int CELL, int H, int MAXC>
 struct CLayout {
   using C = CCfg<CELL, MAXC>;
   static constexpr size_t xl = (size_t)C::TMAX * C::RPN * H, xb = (size_t)C::LEAFB * H;
-  static constexpr int SL = C::AUX ? 2 : 1;  // per-node slices (h [, aux])
   static constexpr size_t x_floats = xl > xb ? xl : xb;
   static constexpr size_t red_floats = (size_t)kRNW * C::NAMAX * C::TMAX * kRUG;
   static constexpr size_t red2_floats = (size_t)C::NAMAX * C::TMAX * kRUG;
   static constexpr size_t cv_floats = (size_t)C::TMAX * kMaxC * kRUG;
-  // per node: h slice + aux slice (floats) and perm, label, maxc children, list (ints)
+  // fixed floats: tile buffer, reduction buffers, child memory cells, and the
+  // per-node aux slice (TreeLSTM memory cell) -- then the ints, then region R:
+  // the per-node h slices (barrier + pull mode) or the push-mode arrays
+  __host__ __device__ static size_t fixed_floats(int n) {
+    return x_floats + red_floats + red2_floats + cv_floats + (C::AUX ? (size_t)kCUnits * n : 0);
+  }
+  static size_t r_min_bytes(int n) { return sizeof(float) * (size_t)kCUnits * n + 16; }
+  static size_t ints(int n, int maxc, int L) { return (size_t)(3 + maxc) * n + 4 * (size_t)L + 64; }
   static size_t bytes(int n, int maxc, int L) {
-    return sizeof(float) * (x_floats + red_floats + red2_floats + cv_floats + SL * (size_t)kCUnits * n) +
-           sizeof(int) * ((size_t)(3 + maxc) * n + 4 * (size_t)L + 64);
+    return sizeof(float) * fixed_floats(n) + sizeof(int) * ints(n, maxc, L) + r_min_bytes(n);
   }
 };
 
@@ -88,7 +93,7 @@ constexpr int kClusterMaxN = 1536;  // and the shared-memory check of the plan
 // linearizer's arrays stand in for the prologue's perm/label/level arrays,
 // plus the remapped children, the cluster's level lists and their offsets.
 constexpr int kFusedCnt = 2048;
-inline size_t fused_extra_ints(int n, int maxc) {
+__host__ __device__ inline size_t fused_extra_ints(int n, int maxc) {
   return lin_sm_ints(n, maxc, kFusedCnt) + (size_t)maxc * n + 3 * (size_t)n + 64;
 }
 
@@ -143,8 +148,8 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   constexpr int LEAFB = Cfg::LEAFB;
   __shared__ int s_nodes[LEAFB];
   __shared__ int s_word[LEAFB];
-  __shared__ int s_cnt;
   __shared__ float s_bias[4 * kCUnits];
+  __shared__ __align__(16) float s_stage[16 * kCUnits];  // a tile's new h slices (push mode)
 
   cg::cluster_group cl = cg::this_cluster();
   const int maxc = a.maxc;
@@ -181,9 +186,10 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     }
   };
   if constexpr (FUSED) {
-    // fire-and-forget L2 prefetch of this thread's weight rows; the register
-    // loads follow the in-kernel linearization (loads in flight would queue
-    // ahead of the linearizer's own children loads)
+    // fire-and-forget L2 prefetch of this thread's weight rows (leaf gates and,
+    // for TreeLSTM, the recurrent gates loaded after the leaf phase); the
+    // register loads follow the in-kernel linearization (loads in flight would
+    // queue ahead of the linearizer's own children loads)
     for (int g = 0; g < ng; g++) {
       const float *src = gs[g].base + (size_t)(gs[g].r0 + unit0 + u) * gs[g].ld + gs[g].c0 + k0;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
@@ -191,14 +197,21 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   } else {
     load_leaf_weights();
   }
+  if constexpr (CELL == CX_TREELSTM) {
+    for (int g = 0; g < 4; g++) {
+      const float *src = (g < 3 ? a.w[1] + (size_t)(g * H + unit0 + u) * H
+                                : a.w[3] + (size_t)(unit0 + u) * H) + k0;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
+    }
+  }
   unsigned long long *ferr = reinterpret_cast<unsigned long long *>(&a.bar->pad[0]);
   int L, first_leaf, R;
   const int n = a.n;
   LinSm ls;
   int *fint = nullptr;
+  const size_t fixed = Lay::fixed_floats(n);
   if constexpr (FUSED) {
-    fint = reinterpret_cast<int *>(smem + Lay::x_floats + Lay::red_floats + Lay::red2_floats +
-                                   Lay::cv_floats + Lay::SL * (size_t)kCUnits * n);
+    fint = reinterpret_cast<int *>(smem + fixed);
     LinPrefetch pf{a.words, a.emb, H, a.V};
     const LinOut lo = lin_single_body(a.lin, fint, kFusedCnt, blockIdx.x == 0,
                                       fint + lin_sm_ints(n, maxc, kFusedCnt), pf);
@@ -219,14 +232,15 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     first_leaf = a.hdr->first_leaf;
     R = a.hdr->num_roots;
   }
+  (void)first_leaf;
 
   CS s;
   s.X = smem;
   s.red = s.X + Lay::x_floats;
   s.red2 = s.red + Lay::red_floats;
   s.cv = s.red2 + Lay::red2_floats;
-  s.hsl = s.cv + Lay::cv_floats;
-  s.aux = s.hsl + (size_t)kCUnits * n;  // TreeLSTM only (Lay::SL == 2)
+  s.aux = s.cv + Lay::cv_floats;  // TreeLSTM only
+  int *int_end;
   if constexpr (FUSED) {  // the linearizer's shared-memory results
     s.perm = ls.perm;
     s.lab = ls.sid;
@@ -236,8 +250,9 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     s.list = s.chn + (size_t)maxc * n;
     s.coff = s.list + n;
     s.ccur = s.coff + n + 1;
+    int_end = fint + fused_extra_ints(n, maxc);
   } else {
-    s.perm = reinterpret_cast<int *>(s.hsl + (size_t)Lay::SL * kCUnits * n);
+    s.perm = reinterpret_cast<int *>(smem + fixed);
     s.lab = s.perm + n;
     s.list = s.lab + n;
     s.chn = s.list + n;
@@ -245,7 +260,12 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     s.lsize = s.lbeg + L;
     s.coff = s.lsize + L;      // [L + 1] start of level l in this cluster's list
     s.ccur = s.coff + L + 1;   // [L] fill cursors
+    int_end = s.ccur + L;
   }
+  // region R: everything after the ints, up to the end of the dynamic smem
+  char *Rb = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(int_end) + 15) & ~uintptr_t(15));
+  const size_t r_bytes = (size_t)dynamic_smem_bytes() - (size_t)(Rb - reinterpret_cast<char *>(smem));
+  s.hsl = reinterpret_cast<float *>(Rb);  // barrier + pull mode
 
   RCtx ctx;
   ctx.a = &a;
@@ -259,7 +279,6 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   ctx.unit0 = unit0;
   ctx.latch = latch;
   ctx.tslot = -1;
-
 
   // ---- prologue: structure labels (root index, propagated top-down) --------
   if constexpr (!FUSED) {
@@ -277,7 +296,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   bool one_cluster = false;
   if (a.kind == CX_DAG) {  // structures sharing a node: one cluster does everything
     bool bad = false;
-    for (int i = tid; i < first_leaf; i += blockDim.x)
+    for (int i = tid; i < n; i += blockDim.x)
       for (int k = 0; k < maxc; k++) {
         int c = s.chn[k * n + i];
         if (c < 0) break;
@@ -319,15 +338,93 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     if (lane == 0) s.coff[L] = acc;
   }
   __syncthreads();
-  for (int l = tid; l < L; l += blockDim.x) s.ccur[l] = 0;
-  __syncthreads();
-  for (int i = tid; i < n; i += blockDim.x)
-    if (mine(i)) {
-      const int l = level_of(i);
-      s.list[s.coff[l] + atomicAdd(&s.ccur[l], 1)] = i;
+  // fill in ascending new id inside each level, so every CTA of the cluster
+  // builds the SAME list (push mode addresses a node's rows by its position):
+  // g = #mine before i by a block-wide scan; levels are contiguous id ranges,
+  // root-most first, so #mine before level l's first id = coff[L] - coff[l + 1]
+  {
+    __shared__ int s_wsum[kRNW];
+    int G = 0;
+    for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+      const int i = c0 + tid;
+      const bool f = i < n && mine(i);
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) s_wsum[warp] = __popc(bal);
+      __syncthreads();
+      int before = G;
+      for (int ww = 0; ww < warp; ww++) before += s_wsum[ww];
+      int tot = 0;
+      for (int ww = 0; ww < kRNW; ww++) tot += s_wsum[ww];
+      if (f) {
+        const int l = level_of(i);
+        const int g = before + __popc(bal & ((1u << lane) - 1u));
+        s.list[s.coff[l] + g - (s.coff[L] - s.coff[l + 1])] = i;
+      }
+      G += tot;
+      __syncthreads();
     }
-  __syncthreads();
+  }
   trace_mark(a, 1);
+
+  // ---- push mode (trees: one parent per node) --------------------------------
+  // Every internal node of this cluster owns MAXC rows of H floats in region R
+  // (level-major, in list order: row (p - coff[1]) * MAXC + k for the k-th
+  // child of the node at list position p). The epilogue that finishes a node
+  // writes its 16-unit slice of h straight into its parent's row in all CS
+  // CTAs of the cluster (st.async, DSMEM), each store signalling the
+  // receiving CTA's mbarrier of the parent's level. A level starts when its
+  // mbarrier has received all its rows: no cluster barrier, no pull and no
+  // release fence on the level-to-level path. Falls back to the barrier + pull
+  // mode (per cluster, uniformly) when the rows do not fit in region R.
+  bool push = false;
+  unsigned long long *mb = nullptr;
+  int *prow = nullptr, *plev = nullptr;
+  float *XA = nullptr;
+  if constexpr (CELL == CX_TREELSTM) {
+    if (a.kind != CX_DAG && L > 1 && !a.push_off) {
+      char *q = Rb;
+      mb = reinterpret_cast<unsigned long long *>(q);
+      q += ((size_t)8 * L + 15) & ~size_t(15);
+      prow = reinterpret_cast<int *>(q);
+      plev = prow + n;
+      q += ((size_t)8 * n + 15) & ~size_t(15);
+      XA = reinterpret_cast<float *>(q);
+      // + slack: a partial last tile reads (discarded) rows past the level end
+      const size_t rows = (size_t)(s.coff[L] - s.coff[1] + TMAX) * MAXC;
+      push = (size_t)(q - Rb) + rows * H * sizeof(float) <= r_bytes;
+    }
+  }
+  if (push) {
+    for (int v = tid; v < n; v += blockDim.x) prow[v] = -1;
+    for (int l = tid; l < L; l += blockDim.x) s.ccur[l] = 0;
+    __syncthreads();
+    for (int p = s.coff[1] + tid; p < s.coff[L]; p += blockDim.x) {
+      const int i = s.list[p], lv = level_of(i);
+      int nc = 0;
+#pragma unroll
+      for (int k = 0; k < MAXC; k++) {
+        const int c = k < maxc ? s.chn[k * n + i] : -1;
+        const int row = (p - s.coff[1]) * MAXC + k;
+        if (c >= 0) {
+          prow[c] = row;
+          plev[c] = lv;
+          nc++;
+        } else {  // absent child: a zero row nobody pushes into
+          float4 *z = reinterpret_cast<float4 *>(XA + (size_t)row * H);
+          for (int q4 = 0; q4 < H / 4; q4++) z[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      atomicAdd(&s.ccur[lv], nc);
+    }
+    for (int l = 1 + tid; l < L; l += blockDim.x) mbar_init(&mb[l], 1);
+    fence_mbar_init_cluster();
+    __syncthreads();
+    for (int l = 1 + tid; l < L; l += blockDim.x)
+      if (s.coff[l + 1] > s.coff[l]) mbar_expect_tx(&mb[l], (unsigned)s.ccur[l] * H * 4u);
+    // every CTA of the cluster has initialised its mbarriers before any push
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
 
   // The level barrier is split: arrive (release: this CTA's state slices are
   // published to the cluster), then the caller's outputs of the level just
@@ -347,6 +444,27 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       a.h_out[o] = s.hsl[(size_t)v * kCUnits + uu];
       if (wa) a.aux_out[o] = s.aux[(size_t)v * kCUnits + uu];
     }
+  };
+  // push mode, node v (tile slot t) finished with h = hh, c = cc at unit u:
+  // caller outputs straight from the epilogue, the slice into the stage buffer
+  auto emit = [&](int v, int t, float hh, float cc) {
+    const size_t o = (size_t)s.perm[v] * H + unit0 + u;
+    a.h_out[o] = hh;
+    if (CELL == CX_TREELSTM && a.aux_out) a.aux_out[o] = cc;
+    if (a.root_out && prow[v] < 0) a.root_out[(size_t)s.lab[v] * H + unit0 + u] = hh;
+    s_stage[t * kCUnits + u] = hh;
+  };
+  // ... then (after __syncwarp) lane u of node t's half-warp sends the 64-byte
+  // slice to CTA u's row of the parent
+  auto push_slice = [&](int v, int t) {
+    constexpr int CSZ = H / kCUnits;  // CTAs of the cluster: lane u < CSZ serves CTA u
+    const int pr = prow[v];
+    if (pr < 0 || u >= CSZ) return;
+    const unsigned dst = mapa_rank(smem_addr(XA + (size_t)pr * H + unit0), (unsigned)u);
+    const unsigned bar = mapa_rank(smem_addr(&mb[plev[v]]), (unsigned)u);
+    const float4 *src = reinterpret_cast<const float4 *>(s_stage + t * kCUnits);
+#pragma unroll
+    for (int q4 = 0; q4 < kCUnits / 4; q4++) st_async_v4(dst + 16u * q4, src[q4], bar);
   };
 
   // ---- leaf / projection phase ----------------------------------------------
@@ -387,8 +505,14 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
               const int v = s_nodes[t0 + t];
               float cc = sigmoidf_(sacc[0] + s_bias[u]) * tanhf_(sacc[2] + s_bias[32 + u]);
               float hh = sigmoidf_(sacc[1] + s_bias[16 + u]) * tanhf_(cc);
-              s.hsl[(size_t)v * kCUnits + u] = hh;
               s.aux[(size_t)v * kCUnits + u] = cc;
+              if (push) emit(v, t, hh, cc);
+              else s.hsl[(size_t)v * kCUnits + u] = hh;
+            }
+            if (push) {
+              __syncwarp();
+              if (t < cntt) push_slice(s_nodes[t0 + t], t);
+              __syncwarp();
             }
           } else {
             float sacc[1];
@@ -415,15 +539,25 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     load_wregs<4, KC>(w, gs, 4, unit0 + u, k0);
   }
   trace_mark(a, 2);
-  cl_arrive();
-  put_outputs(s.coff[0], s.coff[1]);  // the leaves (level 0)
-  cl_wait();
+  if (!push) {
+    cl_arrive();
+    put_outputs(s.coff[0], s.coff[1]);  // the leaves (level 0)
+    cl_wait();
+  }
 
-  // ---- internal levels: one cluster barrier per level -----------------------
+  // ---- internal levels: one cluster barrier per level (pull mode) or one
+  // mbarrier wait per level (push mode) ---------------------------------------
   for (int l = 1; l < L; l++) {
     const int tb = 24 + 5 * l;  // debug trace slots of this level's first tile
     const int lbase = s.coff[l], cnt = s.coff[l + 1] - lbase;
     if (l < 20) trace_mark(a, tb);
+    if (push && cnt > 0) {  // this level's child rows have arrived
+      // watchdog: a lost row would otherwise spin forever; trap (sticky launch
+      // error, reported as CX_E_CUDA) instead of hanging the device
+      unsigned long long spins = 0;
+      while (!mbar_try_wait_cluster(&mb[l], 0))
+        if (++spins > (1ull << 24)) __trap();
+    }
     for (int t0 = 0; t0 < cnt; t0 += TMAX) {
       const int cntt = min(TMAX, cnt - t0);
       // tile node t and its children come straight from the shared-memory
@@ -431,50 +565,66 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       const int *tl = s.list + lbase + t0;
       auto child = [&](int t, int k) { return k < maxc ? s.chn[k * n + tl[t]] : -1; };
       if (t0 == 0 && l < 20) trace_mark(a, tb + 1);
-      if constexpr (CELL == CX_DAGRNN) {  // x rows (L2; prefetched in the fused kernel)
-        constexpr int q4 = H / 4, RPN = Cfg::RPN;
-        for (int idx = tid; idx < cntt * q4; idx += blockDim.x) {
-          const int t = idx / q4, c = idx - t * q4;
-          const int own = s.perm[tl[t]];
-          int wd = __ldg(a.words + own);
-          if (wd < 0 || wd >= a.V) {
-            if (latch && c == 0) {
-              if constexpr (FUSED) atomicMax(ferr, ~(((unsigned long long)CX_E_WORD_RANGE << 32) | (unsigned)own));
-              else latch_error(a.hdr, CX_E_WORD_RANGE, own);
+      if (!push) {
+        if constexpr (CELL == CX_DAGRNN) {  // x rows (L2; prefetched in the fused kernel)
+          constexpr int q4 = H / 4, RPN = Cfg::RPN;
+          for (int idx = tid; idx < cntt * q4; idx += blockDim.x) {
+            const int t = idx / q4, c = idx - t * q4;
+            const int own = s.perm[tl[t]];
+            int wd = __ldg(a.words + own);
+            if (wd < 0 || wd >= a.V) {
+              if (latch && c == 0) {
+                if constexpr (FUSED) atomicMax(ferr, ~(((unsigned long long)CX_E_WORD_RANGE << 32) | (unsigned)own));
+                else latch_error(a.hdr, CX_E_WORD_RANGE, own);
+              }
+              wd = 0;
             }
-            wd = 0;
+            *reinterpret_cast<float4 *>(s.X + (size_t)(t * RPN + MAXC) * H + 4 * c) =
+                ldcg4(a.emb + (size_t)wd * H + 4 * c);
           }
-          *reinterpret_cast<float4 *>(s.X + (size_t)(t * RPN + MAXC) * H + 4 * c) =
-              ldcg4(a.emb + (size_t)wd * H + 4 * c);
         }
-      }
-      pull_rows<H, Cfg::NVMAX, Cfg::RPN>(cl, s, cntt, child);
-      if constexpr (CELL == CX_TREELSTM) {
-        for (int idx = tid; idx < cntt * MAXC * kCUnits; idx += blockDim.x) {
-          int t = idx / (MAXC * kCUnits), r = idx - t * MAXC * kCUnits, k = r >> 4, uu = r & 15;
-          const int c = child(t, k);
-          s.cv[(t * kMaxC + k) * kCUnits + uu] = c >= 0 ? s.aux[(size_t)c * kCUnits + uu] : 0.f;
+        pull_rows<H, Cfg::NVMAX, Cfg::RPN>(cl, s, cntt, child);
+        if constexpr (CELL == CX_TREELSTM) {
+          for (int idx = tid; idx < cntt * MAXC * kCUnits; idx += blockDim.x) {
+            int t = idx / (MAXC * kCUnits), r = idx - t * MAXC * kCUnits, k = r >> 4, uu = r & 15;
+            const int c = child(t, k);
+            s.cv[(t * kMaxC + k) * kCUnits + uu] = c >= 0 ? s.aux[(size_t)c * kCUnits + uu] : 0.f;
+          }
         }
+        __syncthreads();
       }
-      __syncthreads();
       if (t0 == 0 && l < 20) trace_mark(a, tb + 2);
       auto tile = [&](auto tt) {
         constexpr int T = decltype(tt)::value;
         const int t = tid >> 4;
         if constexpr (CELL == CX_TREELSTM) {
           float sacc[3 + MAXC];
-          contract<RLstmLevel<MAXC>, H, T, true>(ctx, s.X, w, sacc);
+          if (push)  // the MAXC child rows of each node, h~ summed in registers
+            contract<RLstmLevel<MAXC>, H, T, false>(
+                ctx, XA + (size_t)(lbase + t0 - s.coff[1]) * MAXC * H, w, sacc);
+          else
+            contract<RLstmLevel<MAXC>, H, T, true>(ctx, s.X, w, sacc);
           if (t0 == 0 && l < 20) trace_mark(a, tb + 3);
           if (t < cntt) {
             const int v = tl[t];
             float cc = sigmoidf_(sacc[0] + s_bias[u]) * tanhf_(sacc[2] + s_bias[32 + u]);
             const float bf = s_bias[48 + u];
 #pragma unroll
-            for (int k = 0; k < MAXC; k++)
-              if (child(t, k) >= 0) cc += sigmoidf_(sacc[3 + k] + bf) * s.cv[(t * kMaxC + k) * kCUnits + u];
+            for (int k = 0; k < MAXC; k++) {
+              const int c = child(t, k);
+              if (c >= 0)
+                cc += sigmoidf_(sacc[3 + k] + bf) *
+                      (push ? s.aux[(size_t)c * kCUnits + u] : s.cv[(t * kMaxC + k) * kCUnits + u]);
+            }
             float hh = sigmoidf_(sacc[1] + s_bias[16 + u]) * tanhf_(cc);
-            s.hsl[(size_t)v * kCUnits + u] = hh;
             s.aux[(size_t)v * kCUnits + u] = cc;
+            if (push) emit(v, t, hh, cc);
+            else s.hsl[(size_t)v * kCUnits + u] = hh;
+          }
+          if (push) {
+            __syncwarp();
+            if (t < cntt) push_slice(tl[t], t);
+            __syncwarp();
           }
         } else {
           float sacc[1];
@@ -484,7 +634,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
             s.hsl[(size_t)v * kCUnits + u] = tanhf_(sacc[0] + s_bias[u]);
           }
         }
-        __syncthreads();
+        if (!push) __syncthreads();
       };
       if (cntt > 8) tile(std::integral_constant<int, (TMAX >= 16 ? 16 : TMAX)>{});
       else if (cntt > 4) tile(std::integral_constant<int, 8>{});
@@ -493,14 +643,17 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       else tile(std::integral_constant<int, 1>{});
       if (t0 == 0 && l < 20) trace_mark(a, tb + 4);
     }
-    cl_arrive();
-    put_outputs(lbase, lbase + cnt);
-    cl_wait();
+    if (!push) {
+      cl_arrive();
+      put_outputs(lbase, lbase + cnt);
+      cl_wait();
+    }
     trace_mark(a, 3 + l);
   }
 
   // ---- packed root states (this CTA's units of this cluster's roots) --------
-  if (a.root_out) {
+  // (push mode: written by the epilogue)
+  if (a.root_out && !push) {
     if constexpr (FUSED) {  // roots: in-degree 0; their structure index is their slot
       for (int p = warp; p < s.coff[L]; p += kRNW) {  // this cluster's nodes
         const int v = s.list[p];
@@ -524,29 +677,40 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
 template <int CELL, int H, int MAXC, bool FUSED>
 bool cplan_one(int n, int maxc, int L_bound, int num_roots_hint, FwdPlan *p, int *Gn, int *Gu) {
   constexpr int CSZ = H / kCUnits;
+  using Lay = CLayout<CELL, H, MAXC>;
   auto k = ck_kernel<CELL, H, MAXC, FUSED>;
-  size_t smem = CLayout<CELL, H, MAXC>::bytes(n, maxc, L_bound);
+  size_t need = Lay::bytes(n, maxc, L_bound);
   if (FUSED)  // the linearizer's arrays replace the prologue's int arrays
-    smem = smem - sizeof(int) * ((size_t)(3 + maxc) * n + 4 * (size_t)L_bound + 64) +
-           sizeof(int) * fused_extra_ints(n, maxc);
-  if (smem > 227 * 1024) return false;
-  static int cached_max = -1;
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    need = need - sizeof(int) * Lay::ints(n, maxc, L_bound) + sizeof(int) * fused_extra_ints(n, maxc);
+  // per-device cache (caller holds the api mutex): the largest dynamic shared
+  // memory a CTA can have, the attribute setup and the co-resident clusters.
+  // The kernel always gets all of it: region R beyond `need` holds the push
+  // mode's rows (forward_cluster.cu header).
+  constexpr int kMaxDev = 64;
+  static int max_dyn[kMaxDev], cached_max[kMaxDev];
+  static bool done[kMaxDev];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return false;
+  if (!done[dev]) {
+    int optin = 0;
+    cudaFuncAttributes fa;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+        cudaFuncGetAttributes(&fa, (const void *)k) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    const int dyn = (optin - (int)fa.sharedSizeBytes) & ~127;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) != cudaSuccess) {
       cudaGetLastError();
       return false;
     }
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (CSZ > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaGetLastError();
-    smem_set = smem;
-  }
-  if (cached_max < 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CSZ * 8);
     cfg.blockDim = dim3(kRThreads);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = dyn;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CSZ;
@@ -557,16 +721,18 @@ bool cplan_one(int n, int maxc, int L_bound, int num_roots_hint, FwdPlan *p, int
     int m = 0;
     if (cudaOccupancyMaxActiveClusters(&m, (const void *)k, &cfg) != cudaSuccess) m = 0;
     cudaGetLastError();
-    cached_max = m;
+    max_dyn[dev] = dyn;
+    cached_max[dev] = m;
+    done[dev] = true;
   }
-  if (cached_max < 1) return false;
-  int ncl = cached_max;
+  if (need > (size_t)max_dyn[dev] || cached_max[dev] < 1) return false;
+  int ncl = cached_max[dev];
   if (num_roots_hint > 0 && num_roots_hint < ncl) ncl = num_roots_hint;
   *Gn = ncl;
   *Gu = CSZ;
   p->ctas = ncl * CSZ;
   p->threads = kRThreads;
-  p->smem = smem;
+  p->smem = (size_t)max_dyn[dev];
   p->kernel = (const void *)k;
   p->cluster = CSZ;
   p->fused = FUSED;

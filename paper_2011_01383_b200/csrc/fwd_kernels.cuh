@@ -43,16 +43,25 @@ struct FwdArgs {
   int Gn, Gu;   // node groups x unit groups = CTAs
   unsigned long long *trace;  // debug: %globaltimer per CTA and phase (cx_debug_set_trace)
   int trace_slots;
+  int push_off;  // measurement/test: CX_PUSH=0 forces the cluster kernel's barrier + pull mode
   LinArgs lin;  // fused linearize + forward (cx_linearize_forward): the linearizer's arguments
 };
 
-// thread 0 of each CTA records %globaltimer into slot `s` (debug builds of a run only)
+// thread 0 of each CTA records %globaltimer into slot `s`. Compiled in only in
+// the separate trace build (libcx_trace.so, -DCX_TRACE: SURVEY §8(d)
+// "per-level breakdown from a separate CX_TRACE_LEVELS build"); the product
+// library carries no trace checks on the hot path.
 __device__ __forceinline__ void trace_mark(const FwdArgs &a, int s) {
+#ifdef CX_TRACE
   if (a.trace && threadIdx.x == 0 && s < a.trace_slots) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[(size_t)blockIdx.x * a.trace_slots + s] = t;
   }
+#else
+  (void)a;
+  (void)s;
+#endif
 }
 
 struct FwdPlan {

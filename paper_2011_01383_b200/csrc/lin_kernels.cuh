@@ -29,13 +29,19 @@ struct LinArgs {
   int hjacobi;  // single-CTA path: Jacobi rounds for trees too (CX_LIN_JACOBI=1, measurement)
 };
 
+// debug timeline (trace build only, see trace_mark in fwd_kernels.cuh)
 __device__ __forceinline__ void lin_mark(const LinArgs &a, int s) {
+#ifdef CX_TRACE
   if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[s] = t;
     a.trace[16 + s] = clock64();
   }
+#else
+  (void)a;
+  (void)s;
+#endif
 }
 
 // multi-CTA path: parent pointers [n] + per-block level-count table

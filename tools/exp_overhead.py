@@ -1,5 +1,7 @@
 """Fixed-overhead experiment: graph-replayed linearize / forward on tiny and
 headline inputs, with and without an L2 flush between replays."""
+import os as _os
+_os.environ.setdefault("CX_TRACE", "1")  # debug timeline build (libcx_trace.so)
 import os
 import sys
 

@@ -1,5 +1,7 @@
 """Timeline of the cluster forward kernel (slots: 0 entry, 1 labels done,
 2 leaf phase done, 3+l after level l's cluster barrier, S-1 exit)."""
+import os as _os
+_os.environ.setdefault("CX_TRACE", "1")  # debug timeline build (libcx_trace.so)
 import ctypes
 import os
 import sys

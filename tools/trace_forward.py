@@ -5,6 +5,8 @@ Slots: 0 entry, 1 leaf weights staged, 2 leaf phase done, 3+2j / 4+2j arrive / e
 barrier j, 64+5j.. first-tile breakdown of level j (meta, gather, fma, reduce, end),
 S-2 loop end, S-1 exit.
 """
+import os as _os
+_os.environ.setdefault("CX_TRACE", "1")  # debug timeline build (libcx_trace.so)
 import ctypes
 import os
 import sys

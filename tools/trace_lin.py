@@ -3,6 +3,8 @@ phase of CTA 0; slots 0..7 = lin_mark calls in linearize.cu).
 
     python tools/trace_lin.py [workload]
 """
+import os as _os
+_os.environ.setdefault("CX_TRACE", "1")  # debug timeline build (libcx_trace.so)
 import ctypes
 import os
 import sys

@@ -3,6 +3,8 @@
 
     python tools/trace_tc.py [workload]
 """
+import os as _os
+_os.environ.setdefault("CX_TRACE", "1")  # debug timeline build (libcx_trace.so)
 import ctypes
 import os
 import sys
