@@ -26,6 +26,7 @@
 
 #include "lin_single.cuh"
 #include "rw_engine.cuh"
+#include "warp_engine.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -33,6 +34,7 @@ namespace cx {
 namespace {
 using namespace fwd;
 using namespace rw;
+using namespace wq;
 
 constexpr int kCUnits = kRUG;  // units per CTA (16)
 
@@ -55,13 +57,15 @@ struct CCfg<CX_TREELSTM, MAXC> {
   // LEAFB: leaves per bookkeeping + gather block; sequences (MAXC = 1) have
   // one leaf per chain, and the smaller X buffer lets 1000-node chain batches
   // keep their per-node slices on chip
-  static constexpr int TMAX = 8, NVMAX = MAXC, NAMAX = 3 + MAXC, LEAFB = MAXC == 1 ? 16 : 24,
-                       RPN = MAXC + 1;
+  // TMAX: nodes per level tile (3 + MAXC packed accumulators per node must
+  // stay in registers); TLEAF: leaves per leaf tile (3 accumulators)
+  static constexpr int TMAX = 4, TLEAF = 8, NVMAX = MAXC, NAMAX = 3 + MAXC,
+                       LEAFB = MAXC == 1 ? 16 : 24, RPN = MAXC + 1;
   static constexpr bool AUX = true;
 };
 template <int MAXC>
 struct CCfg<CX_DAGRNN, MAXC> {
-  static constexpr int TMAX = 16, NVMAX = MAXC, NAMAX = 1, LEAFB = 32, RPN = MAXC + 2;
+  static constexpr int TMAX = 16, TLEAF = 16, NVMAX = MAXC, NAMAX = 1, LEAFB = 32, RPN = MAXC + 2;
   static constexpr bool AUX = false;
 };
 
@@ -70,14 +74,12 @@ struct CLayout {
   using C = CCfg<CELL, MAXC>;
   static constexpr size_t xl = (size_t)C::TMAX * C::RPN * H, xb = (size_t)C::LEAFB * H;
   static constexpr size_t x_floats = xl > xb ? xl : xb;
-  static constexpr size_t red_floats = (size_t)kRNW * C::NAMAX * C::TMAX * kRUG;
-  static constexpr size_t red2_floats = (size_t)C::NAMAX * C::TMAX * kRUG;
-  static constexpr size_t cv_floats = (size_t)C::TMAX * kMaxC * kRUG;
-  // fixed floats: tile buffer, reduction buffers, child memory cells, and the
-  // per-node aux slice (TreeLSTM memory cell) -- then the ints, then region R:
-  // the per-node h slices (barrier + pull mode) or the push-mode arrays
+  // fixed floats: tile buffer and the per-node aux slice (TreeLSTM memory
+  // cell) -- then the ints, then region R: the per-node h slices (barrier +
+  // pull mode) or the push-mode arrays. (The warp engine needs no reduction
+  // buffers.)
   __host__ __device__ static size_t fixed_floats(int n) {
-    return x_floats + red_floats + red2_floats + cv_floats + (C::AUX ? (size_t)kCUnits * n : 0);
+    return x_floats + (C::AUX ? (size_t)kCUnits * n : 0);
   }
   static size_t r_min_bytes(int n) { return sizeof(float) * (size_t)kCUnits * n + 16; }
   static size_t ints(int n, int maxc, int L) { return (size_t)(3 + maxc) * n + 4 * (size_t)L + 64; }
@@ -97,8 +99,22 @@ __host__ __device__ inline size_t fused_extra_ints(int n, int maxc) {
   return lin_sm_ints(n, maxc, kFusedCnt) + (size_t)maxc * n + 3 * (size_t)n + 64;
 }
 
+// run tile<T>() for the smallest power of two T >= cnt (T <= TM; warp-uniform)
+template <int TM, class F>
+__device__ __forceinline__ void dispatch_tile(int cnt, F &&f) {
+  if constexpr (TM >= 16) {
+    if (cnt > 8) { f(std::integral_constant<int, 16>{}); return; }
+  }
+  if constexpr (TM >= 8) {
+    if (cnt > 4) { f(std::integral_constant<int, 8>{}); return; }
+  }
+  if (cnt > 2) f(std::integral_constant<int, 4>{});
+  else if (cnt == 2) f(std::integral_constant<int, 2>{});
+  else f(std::integral_constant<int, 1>{});
+}
+
 struct CS {  // shared-memory carve of one CTA
-  float *X, *red, *red2, *cv, *hsl, *aux;
+  float *X, *hsl, *aux;
   int *perm, *lab, *chn, *list, *lbeg, *lsize, *coff, *ccur;  // coff/ccur: this cluster's level lists
 };
 
@@ -131,33 +147,39 @@ __device__ __forceinline__ void pull_rows(cg::cluster_group &cl, const CS &s, in
 }
 
 // ---------------------------------------------------------------------------
+// The kernel. Thread (warp w, lane c) holds the k-chunk c of every gate row of
+// hidden unit unit0 + w (warp_engine.cuh): tiles are contracted and their
+// gates evaluated without any block-wide reduction; one __syncthreads per
+// tile stages the finished h slices for the push (or ends a pull-mode tile).
+//
 // FUSED: the kernel linearizes the batch itself (every CTA redundantly runs
 // the single-CTA linearizer of lin_single.cuh on its own shared memory, so no
 // grid-wide synchronisation is needed; CTA 0 also writes the cx_linearization
-// outputs), overlapping it with the register weight loads and an L2 prefetch
-// of every node's embedding row. Forward data errors are latched into a
-// workspace word and merged into the header by the last CTA out, after CTA 0
-// has written it.
+// outputs). Forward data errors are latched into a workspace word and merged
+// into the header by the last CTA out, after CTA 0 has written it.
+// EARLY (fused TreeLSTM): the leaves are evaluated before the linearizer (see
+// the phase below).
 template <int CELL, int H, int MAXC, bool FUSED>
 __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   using Cfg = CCfg<CELL, MAXC>;
   using Lay = CLayout<CELL, H, MAXC>;
-  constexpr int KC = RShape<H>::KC;
+  constexpr int KC = WShape<H>::KC;
   constexpr int TMAX = Cfg::TMAX;
   extern __shared__ __align__(16) float smem[];
   constexpr int LEAFB = Cfg::LEAFB;
   __shared__ int s_nodes[LEAFB];
   __shared__ int s_word[LEAFB];
   __shared__ float s_bias[4 * kCUnits];
-  __shared__ __align__(16) float s_stage[16 * kCUnits];  // a tile's new h slices (push mode)
+  __shared__ __align__(16) float s_stage[2][(TMAX > Cfg::TLEAF ? TMAX : Cfg::TLEAF) * kCUnits];  // a tile's new h slices (push mode)
 
   cg::cluster_group cl = cg::this_cluster();
   const int maxc = a.maxc;
   const int crank = (int)cl.block_rank();
   const int cid = blockIdx.x / (int)cl.num_blocks(), ncl = gridDim.x / (int)cl.num_blocks();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int u = lane & 15, k0 = (warp * 2 + (lane >> 4)) * KC;
+  const int hu = lane & 15;  // half-warp lane: row-piece and push mapping
   const int unit0 = crank * kCUnits;
+  const int myu = unit0 + warp;  // this warp's hidden unit
   const bool latch = crank == 0;
   trace_mark(a, 0);
 
@@ -174,7 +196,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     ng = 2;
   }
   auto load_leaf_weights = [&]() {
-    load_wregs<4, KC>(w, gs, ng, unit0 + u, k0);
+    load_wregs_w<4, KC>(w, gs, ng, myu, lane);
     if constexpr (CELL == CX_TREELSTM) {
       if (tid < 4 * kCUnits) {
         int g = tid / kCUnits, uu = tid % kCUnits;
@@ -185,34 +207,130 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       if (tid < kCUnits) s_bias[tid] = __ldg(a.w[2] + unit0 + tid);
     }
   };
-  if constexpr (FUSED) {
-    // fire-and-forget L2 prefetch of this thread's weight rows (leaf gates and,
-    // for TreeLSTM, the recurrent gates loaded after the leaf phase); the
-    // register loads follow the in-kernel linearization (loads in flight would
-    // queue ahead of the linearizer's own children loads)
+  auto load_rec_weights = [&]() {  // TreeLSTM recurrent gates U_iou, U_f
+    gs[0] = {a.w[1], 0, H, 0}; gs[1] = {a.w[1], H, H, 0}; gs[2] = {a.w[1], 2 * H, H, 0};
+    gs[3] = {a.w[3], 0, H, 0};
+    load_wregs_w<4, KC>(w, gs, 4, myu, lane);
+  };
+  constexpr bool EARLY = FUSED && CELL == CX_TREELSTM;
+  if constexpr (FUSED && !EARLY) {
+    // fire-and-forget L2 prefetch of this thread's weight rows; the register
+    // loads follow the in-kernel linearization (loads in flight would queue
+    // ahead of the linearizer's own children loads)
     for (int g = 0; g < ng; g++) {
-      const float *src = gs[g].base + (size_t)(gs[g].r0 + unit0 + u) * gs[g].ld + gs[g].c0 + k0;
+      const float *src = gs[g].base + (size_t)(gs[g].r0 + myu) * gs[g].ld + gs[g].c0 + 4 * lane;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
     }
-  } else {
+  } else if constexpr (!FUSED) {
     load_leaf_weights();
   }
   if constexpr (CELL == CX_TREELSTM) {
     for (int g = 0; g < 4; g++) {
-      const float *src = (g < 3 ? a.w[1] + (size_t)(g * H + unit0 + u) * H
-                                : a.w[3] + (size_t)(unit0 + u) * H) + k0;
+      const float *src = (g < 3 ? a.w[1] + (size_t)(g * H + myu) * H
+                                : a.w[3] + (size_t)myu * H) + 4 * lane;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
     }
   }
   unsigned long long *ferr = reinterpret_cast<unsigned long long *>(&a.bar->pad[0]);
+  auto latch_word = [&](int own) {
+    if constexpr (FUSED) atomicMax(ferr, ~(((unsigned long long)CX_E_WORD_RANGE << 32) | (unsigned)own));
+    else latch_error(a.hdr, CX_E_WORD_RANGE, own);
+  };
   int L, first_leaf, R;
   const int n = a.n;
   LinSm ls;
   int *fint = nullptr;
   const size_t fixed = Lay::fixed_floats(n);
+  float *const X = smem;
+
+  // ---- EARLY leaf phase (fused TreeLSTM): a leaf's cell needs no linearization
+  // -- only its word -- so the leaves are evaluated at kernel entry, spread over
+  // ALL clusters by input id (cluster c takes ids [c n / ncl, (c+1) n / ncl)),
+  // h into h_out and c into cbuf (aux_out or workspace), both in input
+  // numbering; one release increment of a grid-wide counter per CTA publishes
+  // them. The linearizer then runs while those stores drain, and each cluster
+  // imports its internal nodes' leaf children from L2 after one acquire of the
+  // counter (complete long before). A leaf is a node whose first child slot is
+  // absent; malformed inputs are caught by the linearizer (its codes rank
+  // below CX_E_WORD_RANGE) and outputs are then unspecified.
+  if constexpr (EARLY) {
+    load_leaf_weights();
+    // the chunk's leaves and their word ids (one round trip for both), then
+    // every leaf row gathered at once into E (all of the shared memory is free
+    // before the linearizer runs; blocks of EB rows if the chunk is larger)
+    int lo, hi;
+    chunk_of(n, ncl, cid, lo, hi);
+    const int span = hi - lo;
+    // (+ TLEAF slack rows: a partial tile reads, and discards, rows past its end)
+    const int EB = min(span, (int)(((size_t)dynamic_smem_bytes() - 8 * (size_t)span - 64) /
+                                   (sizeof(float) * H)) - Cfg::TLEAF);
+    float *E = smem;
+    int *elist = reinterpret_cast<int *>(smem + (size_t)(EB + Cfg::TLEAF) * H), *ewd = elist + span;
+    __shared__ int s_wc[kRNW];
+    int ecnt = 0;
+    for (int base = lo; base < hi; base += blockDim.x) {  // compact the chunk's leaves
+      const int v = base + tid;
+      bool f = false;
+      int wd = 0;
+      if (v < hi) {
+        const int c0 = __ldg(a.lin.ch + v);
+        wd = __ldg(a.words + v);
+        f = c0 == -1;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) s_wc[warp] = __popc(bal);
+      __syncthreads();
+      int before = ecnt, tot = 0;
+      for (int ww = 0; ww < kRNW; ww++) {
+        if (ww < warp) before += s_wc[ww];
+        tot += s_wc[ww];
+      }
+      if (f) {
+        if (wd < 0 || wd >= a.V) {
+          if (latch) latch_word(v);
+          wd = 0;
+        }
+        const int pos = before + __popc(bal & ((1u << lane) - 1u));
+        elist[pos] = v;
+        ewd[pos] = wd;
+      }
+      ecnt += tot;
+      __syncthreads();
+    }
+    for (int b0 = 0; b0 < ecnt; b0 += EB) {
+      const int cntb = min(EB, ecnt - b0);
+      if (b0) __syncthreads();  // E is overwritten
+      gather_rows_c<1, H>(E, cntb, [&](int t, int) { return a.emb + (size_t)ewd[b0 + t] * H; });
+      __syncthreads();
+      for (int t0 = 0; t0 < cntb; t0 += Cfg::TLEAF) {
+        const int cntt = min(Cfg::TLEAF, cntb - t0);
+        auto tile = [&](auto tt) {
+          constexpr int T = decltype(tt)::value;
+          float r[3];
+          contract_w<RLstmLeaf, H, T>(E + (size_t)t0 * H, w, r);
+          const int tn = node_of_lane<T>(lane);
+          if (lead_lane<T>(lane) && tn < cntt) {
+            const size_t o = (size_t)elist[b0 + t0 + tn] * H + myu;
+            const float cc = sigmoidf_(r[0] + s_bias[warp]) * tanhf_(r[2] + s_bias[32 + warp]);
+            a.h_out[o] = sigmoidf_(r[1] + s_bias[16 + warp]) * tanhf_(cc);
+            a.cbuf[o] = cc;
+          }
+        };
+        dispatch_tile<Cfg::TLEAF>(cntt, tile);
+      }
+    }
+    __syncthreads();  // the linearizer reuses the shared memory
+    if (tid == 0) {
+      __threadfence();
+      red_release_add_u32(&a.bar->count, 1u);
+    }
+    load_rec_weights();  // the recurrent gates -> registers, overlapping the linearizer
+    trace_mark(a, 21);
+  }
   if constexpr (FUSED) {
     fint = reinterpret_cast<int *>(smem + fixed);
     LinPrefetch pf{a.words, a.emb, H, a.V};
+    if (EARLY) pf.words = nullptr;  // no leaf rows left to fetch
     const LinOut lo = lin_single_body(a.lin, fint, kFusedCnt, blockIdx.x == 0,
                                       fint + lin_sm_ints(n, maxc, kFusedCnt), pf);
     trace_mark(a, 20);
@@ -220,7 +338,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       fused_exit(a, ferr);
       return;
     }
-    load_leaf_weights();
+    if (!EARLY) load_leaf_weights();
     ls = lin_carve(fint, n, maxc);
     L = lo.L;
     first_leaf = lo.first_leaf;
@@ -235,11 +353,8 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   (void)first_leaf;
 
   CS s;
-  s.X = smem;
-  s.red = s.X + Lay::x_floats;
-  s.red2 = s.red + Lay::red_floats;
-  s.cv = s.red2 + Lay::red2_floats;
-  s.aux = s.cv + Lay::cv_floats;  // TreeLSTM only
+  s.X = X;
+  s.aux = smem + Lay::x_floats;  // TreeLSTM only
   int *int_end;
   if constexpr (FUSED) {  // the linearizer's shared-memory results
     s.perm = ls.perm;
@@ -267,19 +382,6 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   const size_t r_bytes = (size_t)dynamic_smem_bytes() - (size_t)(Rb - reinterpret_cast<char *>(smem));
   s.hsl = reinterpret_cast<float *>(Rb);  // barrier + pull mode
 
-  RCtx ctx;
-  ctx.a = &a;
-  ctx.X = s.X;
-  ctx.red = s.red;
-  ctx.red2 = s.red2;
-  ctx.cv = s.cv;
-  ctx.bias = s_bias;
-  ctx.gn = cid;
-  ctx.gu = crank;
-  ctx.unit0 = unit0;
-  ctx.latch = latch;
-  ctx.tslot = -1;
-
   // ---- prologue: structure labels (root index, propagated top-down) --------
   if constexpr (!FUSED) {
     for (int l = tid; l < L; l += blockDim.x) {
@@ -305,8 +407,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     one_cluster = __syncthreads_or(bad);
   }
 
-  // ---- this cluster's nodes, bucketed by level once (order inside a level is
-  // irrelevant: every slice is addressed by new id) ---------------------------
+  // ---- this cluster's nodes, bucketed by level once ---------------------------
   for (int l = tid; l < L; l += blockDim.x) s.ccur[l] = 0;
   __syncthreads();
   // this cluster evaluates node i (new id)
@@ -408,7 +509,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
         if (c >= 0) {
           prow[c] = row;
           plev[c] = lv;
-          nc++;
+          if (!EARLY || c < first_leaf) nc++;  // EARLY: leaf rows are imported, not pushed
         } else {  // absent child: a zero row nobody pushes into
           float4 *z = reinterpret_cast<float4 *>(XA + (size_t)row * H);
           for (int q4 = 0; q4 < H / 4; q4++) z[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -420,18 +521,53 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     fence_mbar_init_cluster();
     __syncthreads();
     for (int l = 1 + tid; l < L; l += blockDim.x)
-      if (s.coff[l + 1] > s.coff[l]) mbar_expect_tx(&mb[l], (unsigned)s.ccur[l] * H * 4u);
+      if (s.coff[l + 1] > s.coff[l] && s.ccur[l] > 0)
+        mbar_expect_tx(&mb[l], (unsigned)s.ccur[l] * H * 4u);
+  }
+  // EARLY: import this cluster's leaves (list positions [0, coff[1])) from L2
+  // once every CTA has published its share: push mode -- the full h row into
+  // the parent's slot row; both modes -- this CTA's 16-unit slice of c (the
+  // parents' forget-gate term), and of h in pull mode
+  if constexpr (EARLY) {
+    if (tid == 0) {
+      unsigned long long spins = 0;
+      while (ld_relaxed_u32(&a.bar->count) < gridDim.x)
+        if (++spins > (1ull << 26)) __trap();
+      (void)ld_acquire_u32(&a.bar->count);
+    }
+    __syncthreads();
+    const int nl0 = s.coff[1];
+    constexpr int Q4 = H / 4;
+    // cp.async (L2 -> shared, all pieces in flight at once, one wait)
+    if (push)
+      for (int idx = tid; idx < nl0 * Q4; idx += blockDim.x) {
+        const int v = s.list[idx / Q4], q = idx % Q4, pr = prow[v];
+        if (pr >= 0) cp_async16(XA + (size_t)pr * H + 4 * q, a.h_out + (size_t)s.perm[v] * H + 4 * q);
+      }
+    constexpr int Q16 = kCUnits / 4;  // 16-byte pieces of a 16-unit slice
+    for (int idx = tid; idx < nl0 * Q16; idx += blockDim.x) {
+      const int v = s.list[idx / Q16], qq = idx % Q16;
+      const size_t o = (size_t)s.perm[v] * H + unit0 + 4 * qq;
+      cp_async16(s.aux + (size_t)v * kCUnits + 4 * qq, a.cbuf + o);
+      if (!push) cp_async16(s.hsl + (size_t)v * kCUnits + 4 * qq, a.h_out + o);
+      else if (a.root_out && prow[v] < 0)  // a single-node tree: its leaf is its root
+        *reinterpret_cast<float4 *>(a.root_out + (size_t)s.lab[v] * H + unit0 + 4 * qq) =
+            ldcg4(a.h_out + o);
+    }
+    cp_async_wait_all();
+    trace_mark(a, 22);
+  }
+  if (push) {
     // every CTA of the cluster has initialised its mbarriers before any push
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
 
-  // The level barrier is split: arrive (release: this CTA's state slices are
-  // published to the cluster), then the caller's outputs of the level just
-  // finished go to global memory, then wait (acquire). Issued before the
-  // arrive, those global stores would stall the release fence (ncu: the
-  // barrier's MEMBAR was the top stall); after it they drain while the
-  // cluster meets and the next level starts.
+  // The level barrier of pull mode is split: arrive (release: this CTA's state
+  // slices are published to the cluster), then the caller's outputs of the
+  // level just finished go to global memory, then wait (acquire). Issued before
+  // the arrive, those global stores would stall the release fence (ncu: the
+  // barrier's MEMBAR was the top stall).
   auto cl_arrive = [] { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); };
   auto cl_wait = [] { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); };
   // h_out (and TreeLSTM c into aux_out) of this cluster's nodes at list
@@ -445,103 +581,90 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       if (wa) a.aux_out[o] = s.aux[(size_t)v * kCUnits + uu];
     }
   };
-  // push mode, node v (tile slot t) finished with h = hh, c = cc at unit u:
-  // caller outputs straight from the epilogue, the slice into the stage buffer
+  // push mode, node v (tile slot t) finished with h = hh, c = cc at this warp's
+  // unit: caller outputs straight from the epilogue, the h value into the stage
+  int sb = 0;  // stage buffer of the current tile (double-buffered)
   auto emit = [&](int v, int t, float hh, float cc) {
-    const size_t o = (size_t)s.perm[v] * H + unit0 + u;
+    const size_t o = (size_t)s.perm[v] * H + myu;
     a.h_out[o] = hh;
     if (CELL == CX_TREELSTM && a.aux_out) a.aux_out[o] = cc;
-    if (a.root_out && prow[v] < 0) a.root_out[(size_t)s.lab[v] * H + unit0 + u] = hh;
-    s_stage[t * kCUnits + u] = hh;
+    if (a.root_out && prow[v] < 0) a.root_out[(size_t)s.lab[v] * H + myu] = hh;
+    s_stage[sb][t * kCUnits + warp] = hh;
   };
-  // ... then (after __syncwarp) lane u of node t's half-warp sends the 64-byte
-  // slice to CTA u's row of the parent
+  // ... then (after __syncthreads) lane hu of node t's half-warp sends the
+  // 64-byte slice to CTA hu's row of the parent
   auto push_slice = [&](int v, int t) {
-    constexpr int CSZ = H / kCUnits;  // CTAs of the cluster: lane u < CSZ serves CTA u
+    constexpr int CSZ = H / kCUnits;  // CTAs of the cluster: lane hu < CSZ serves CTA hu
     const int pr = prow[v];
-    if (pr < 0 || u >= CSZ) return;
-    const unsigned dst = mapa_rank(smem_addr(XA + (size_t)pr * H + unit0), (unsigned)u);
-    const unsigned bar = mapa_rank(smem_addr(&mb[plev[v]]), (unsigned)u);
-    const float4 *src = reinterpret_cast<const float4 *>(s_stage + t * kCUnits);
+    if (pr < 0 || hu >= CSZ) return;
+    const unsigned dst = mapa_rank(smem_addr(XA + (size_t)pr * H + unit0), (unsigned)hu);
+    const unsigned bar = mapa_rank(smem_addr(&mb[plev[v]]), (unsigned)hu);
+    const float4 *src = reinterpret_cast<const float4 *>(&s_stage[sb][t * kCUnits]);
 #pragma unroll
     for (int q4 = 0; q4 < kCUnits / 4; q4++) st_async_v4(dst + 16u * q4, src[q4], bar);
   };
+  // after a tile's epilogue: stage complete, push, flip the stage buffer
+  auto push_tile = [&](const int *tl, int cntt) {
+    __syncthreads();
+    if (tid < cntt * kCUnits) push_slice(tl[tid >> 4], tid >> 4);
+    sb ^= 1;
+  };
 
-  // ---- leaf / projection phase ----------------------------------------------
-  {
+  // ---- leaf / projection phase (done at entry when EARLY) --------------------
+  if (!EARLY) {
     // this cluster's leaves (level 0). TreeLSTM: [i; o; u] = W_iou x + b;
     // DAG-RNN: h = tanh(W_x x + b) (internal nodes add W_x x at their level)
-    const int lb0 = 0, cnt = s.coff[1];
-    for (int b0 = lb0; b0 < cnt; b0 += LEAFB) {
+    const int cnt = s.coff[1];
+    for (int b0 = 0; b0 < cnt; b0 += LEAFB) {
       const int cntb = min(LEAFB, cnt - b0);
       if (tid < cntb) {
         int v = s.list[b0 + tid];
         int own = s.perm[v];
         int wd = __ldg(a.words + own);
         if (wd < 0 || wd >= a.V) {
-          if (latch) {
-            if constexpr (FUSED) atomicMax(ferr, ~(((unsigned long long)CX_E_WORD_RANGE << 32) | (unsigned)own));
-            else latch_error(a.hdr, CX_E_WORD_RANGE, own);
-          }
+          if (latch) latch_word(own);
           wd = 0;
         }
         s_nodes[tid] = v;
         s_word[tid] = wd;
       }
       __syncthreads();
-      if (b0 == 0) trace_mark(a, 12);
-      gather_rows_c<1, H>(s.X, cntb, [&](int t, int) { return a.emb + (size_t)s_word[t] * H; });
+      gather_rows_c<1, H>(X, cntb, [&](int t, int) { return a.emb + (size_t)s_word[t] * H; });
       __syncthreads();
-      if (b0 == 0) trace_mark(a, 13);
-      for (int t0 = 0; t0 < cntb; t0 += TMAX) {
-        const int cntt = min(TMAX, cntb - t0);
+      for (int t0 = 0; t0 < cntb; t0 += Cfg::TLEAF) {
+        const int cntt = min(Cfg::TLEAF, cntb - t0);
         auto tile = [&](auto tt) {
           constexpr int T = decltype(tt)::value;
-          const int t = tid >> 4;
+          const int tn = node_of_lane<T>(lane);
+          const bool lead = lead_lane<T>(lane) && tn < cntt;
           if constexpr (CELL == CX_TREELSTM) {
-            float sacc[3];
-            contract<RLstmLeaf, H, T>(ctx, s.X + (size_t)t0 * H, w, sacc);
-            if (t < cntt) {
-              const int v = s_nodes[t0 + t];
-              float cc = sigmoidf_(sacc[0] + s_bias[u]) * tanhf_(sacc[2] + s_bias[32 + u]);
-              float hh = sigmoidf_(sacc[1] + s_bias[16 + u]) * tanhf_(cc);
-              s.aux[(size_t)v * kCUnits + u] = cc;
-              if (push) emit(v, t, hh, cc);
-              else s.hsl[(size_t)v * kCUnits + u] = hh;
+            float r[3];
+            contract_w<RLstmLeaf, H, T>(X + (size_t)t0 * H, w, r);
+            if (lead) {
+              const int v = s_nodes[t0 + tn];
+              const float cc = sigmoidf_(r[0] + s_bias[warp]) * tanhf_(r[2] + s_bias[32 + warp]);
+              const float hh = sigmoidf_(r[1] + s_bias[16 + warp]) * tanhf_(cc);
+              s.aux[(size_t)v * kCUnits + warp] = cc;
+              if (push) emit(v, tn, hh, cc);
+              else s.hsl[(size_t)v * kCUnits + warp] = hh;
             }
-            if (push) {
-              __syncwarp();
-              if (t < cntt) push_slice(s_nodes[t0 + t], t);
-              __syncwarp();
-            }
+            if (push) push_tile(s_nodes + t0, cntt);
           } else {
-            float sacc[1];
-            contract<RDagLeaf, H, T>(ctx, s.X + (size_t)t0 * H, w, sacc);
-            if (t < cntt) {
-              const int v = s_nodes[t0 + t];
-              s.hsl[(size_t)v * kCUnits + u] = tanhf_(sacc[0] + s_bias[u]);
-            }
+            float r[1];
+            contract_w<RDagLeaf, H, T>(X + (size_t)t0 * H, w, r);
+            if (lead) s.hsl[(size_t)s_nodes[t0 + tn] * kCUnits + warp] = tanhf_(r[0] + s_bias[warp]);
           }
-          __syncthreads();
         };
-        if (cntt > 8) tile(std::integral_constant<int, (TMAX >= 16 ? 16 : TMAX)>{});
-        else if (cntt > 4) tile(std::integral_constant<int, 8>{});
-        else if (cntt > 2) tile(std::integral_constant<int, 4>{});
-        else if (cntt == 2) tile(std::integral_constant<int, 2>{});
-        else tile(std::integral_constant<int, 1>{});
+        dispatch_tile<Cfg::TLEAF>(cntt, tile);
       }
+      __syncthreads();  // X and s_nodes are overwritten by the next block
     }
-  }
-  // recurrent gates -> registers
-  if constexpr (CELL == CX_TREELSTM) {
-    gs[0] = {a.w[1], 0, H, 0}; gs[1] = {a.w[1], H, H, 0}; gs[2] = {a.w[1], 2 * H, H, 0};
-    gs[3] = {a.w[3], 0, H, 0};
-    load_wregs<4, KC>(w, gs, 4, unit0 + u, k0);
+    if constexpr (CELL == CX_TREELSTM) load_rec_weights();
   }
   trace_mark(a, 2);
   if (!push) {
     cl_arrive();
-    put_outputs(s.coff[0], s.coff[1]);  // the leaves (level 0)
+    if (!EARLY) put_outputs(s.coff[0], s.coff[1]);  // the leaves (level 0)
     cl_wait();
   }
 
@@ -551,7 +674,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     const int tb = 24 + 5 * l;  // debug trace slots of this level's first tile
     const int lbase = s.coff[l], cnt = s.coff[l + 1] - lbase;
     if (l < 20) trace_mark(a, tb);
-    if (push && cnt > 0) {  // this level's child rows have arrived
+    if (push && cnt > 0 && s.ccur[l] > 0) {  // this level's pushed child rows have arrived
       // watchdog: a lost row would otherwise spin forever; trap (sticky launch
       // error, reported as CX_E_CUDA) instead of hanging the device
       unsigned long long spins = 0;
@@ -573,10 +696,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
             const int own = s.perm[tl[t]];
             int wd = __ldg(a.words + own);
             if (wd < 0 || wd >= a.V) {
-              if (latch && c == 0) {
-                if constexpr (FUSED) atomicMax(ferr, ~(((unsigned long long)CX_E_WORD_RANGE << 32) | (unsigned)own));
-                else latch_error(a.hdr, CX_E_WORD_RANGE, own);
-              }
+              if (latch && c == 0) latch_word(own);
               wd = 0;
             }
             *reinterpret_cast<float4 *>(s.X + (size_t)(t * RPN + MAXC) * H + 4 * c) =
@@ -584,63 +704,44 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
           }
         }
         pull_rows<H, Cfg::NVMAX, Cfg::RPN>(cl, s, cntt, child);
-        if constexpr (CELL == CX_TREELSTM) {
-          for (int idx = tid; idx < cntt * MAXC * kCUnits; idx += blockDim.x) {
-            int t = idx / (MAXC * kCUnits), r = idx - t * MAXC * kCUnits, k = r >> 4, uu = r & 15;
-            const int c = child(t, k);
-            s.cv[(t * kMaxC + k) * kCUnits + uu] = c >= 0 ? s.aux[(size_t)c * kCUnits + uu] : 0.f;
-          }
-        }
         __syncthreads();
       }
-      if (t0 == 0 && l < 20) trace_mark(a, tb + 2);
       auto tile = [&](auto tt) {
         constexpr int T = decltype(tt)::value;
-        const int t = tid >> 4;
+        const int tn = node_of_lane<T>(lane);
+        const bool lead = lead_lane<T>(lane) && tn < cntt;
         if constexpr (CELL == CX_TREELSTM) {
-          float sacc[3 + MAXC];
+          float r[3 + MAXC];
           if (push)  // the MAXC child rows of each node, h~ summed in registers
-            contract<RLstmLevel<MAXC>, H, T, false>(
-                ctx, XA + (size_t)(lbase + t0 - s.coff[1]) * MAXC * H, w, sacc);
+            contract_w<RLstmLevel<MAXC>, H, T, false>(
+                XA + (size_t)(lbase + t0 - s.coff[1]) * MAXC * H, w, r);
           else
-            contract<RLstmLevel<MAXC>, H, T, true>(ctx, s.X, w, sacc);
+            contract_w<RLstmLevel<MAXC>, H, T, true>(s.X, w, r);
           if (t0 == 0 && l < 20) trace_mark(a, tb + 3);
-          if (t < cntt) {
-            const int v = tl[t];
-            float cc = sigmoidf_(sacc[0] + s_bias[u]) * tanhf_(sacc[2] + s_bias[32 + u]);
-            const float bf = s_bias[48 + u];
+          if (lead) {
+            const int v = tl[tn];
+            float cc = sigmoidf_(r[0] + s_bias[warp]) * tanhf_(r[2] + s_bias[32 + warp]);
+            const float bf = s_bias[48 + warp];
 #pragma unroll
             for (int k = 0; k < MAXC; k++) {
-              const int c = child(t, k);
-              if (c >= 0)
-                cc += sigmoidf_(sacc[3 + k] + bf) *
-                      (push ? s.aux[(size_t)c * kCUnits + u] : s.cv[(t * kMaxC + k) * kCUnits + u]);
+              const int c = child(tn, k);
+              if (c >= 0) cc += sigmoidf_(r[3 + k] + bf) * s.aux[(size_t)c * kCUnits + warp];
             }
-            float hh = sigmoidf_(sacc[1] + s_bias[16 + u]) * tanhf_(cc);
-            s.aux[(size_t)v * kCUnits + u] = cc;
-            if (push) emit(v, t, hh, cc);
-            else s.hsl[(size_t)v * kCUnits + u] = hh;
+            const float hh = sigmoidf_(r[1] + s_bias[16 + warp]) * tanhf_(cc);
+            s.aux[(size_t)v * kCUnits + warp] = cc;
+            if (push) emit(v, tn, hh, cc);
+            else s.hsl[(size_t)v * kCUnits + warp] = hh;
           }
-          if (push) {
-            __syncwarp();
-            if (t < cntt) push_slice(tl[t], t);
-            __syncwarp();
-          }
+          if (t0 == 0 && l < 20) trace_mark(a, tb + 2);
+          if (push) push_tile(tl, cntt);
         } else {
-          float sacc[1];
-          contract<CDagLevel<MAXC>, H, T, true>(ctx, s.X, w, sacc);
-          if (t < cntt) {
-            const int v = tl[t];
-            s.hsl[(size_t)v * kCUnits + u] = tanhf_(sacc[0] + s_bias[u]);
-          }
+          float r[1];
+          contract_w<CDagLevel<MAXC>, H, T, true>(s.X, w, r);
+          if (lead) s.hsl[(size_t)tl[tn] * kCUnits + warp] = tanhf_(r[0] + s_bias[warp]);
         }
         if (!push) __syncthreads();
       };
-      if (cntt > 8) tile(std::integral_constant<int, (TMAX >= 16 ? 16 : TMAX)>{});
-      else if (cntt > 4) tile(std::integral_constant<int, 8>{});
-      else if (cntt > 2) tile(std::integral_constant<int, 4>{});
-      else if (cntt == 2) tile(std::integral_constant<int, 2>{});
-      else tile(std::integral_constant<int, 1>{});
+      dispatch_tile<TMAX>(cntt, tile);
       if (t0 == 0 && l < 20) trace_mark(a, tb + 4);
     }
     if (!push) {

@@ -103,7 +103,11 @@ __device__ void load_meta(const FwdArgs &a, M &m, int i0, int cnt, bool want_chi
   }
 }
 
-// X[t][j][:] = row src(t, j) (H floats) or zeros, for t < cnt (L2 loads).
+// X[t][j][:] = row src(t, j) (H floats) or zeros, for t < cnt. The pieces are
+// cp.async.cg copies (L2, no register round trip): every iteration's copy is
+// in flight at once and the thread waits once at the end -- a loaded-value
+// loop would pay one dependent L2/HBM round trip per iteration. The caller's
+// __syncthreads publishes the rows to the CTA.
 template <int NV, int H, class SRC>
 __device__ __forceinline__ void gather_rows_c(float *X, int cnt, SRC src) {
   constexpr int q = H / 4;
@@ -112,9 +116,11 @@ __device__ __forceinline__ void gather_rows_c(float *X, int cnt, SRC src) {
     int row = idx / q, c = idx - row * q;
     int t = row / NV, j = row - t * NV;
     const float *p = src(t, j);
-    float4 v = p ? ldcg4(p + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4 *>(X + (size_t)row * H + 4 * c) = v;
+    float *d = X + (size_t)row * H + 4 * c;
+    if (p) cp_async16(d, p + 4 * c);
+    else *reinterpret_cast<float4 *>(d) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  cp_async_wait_all();
 }
 
 // Walk [lo, hi) in tiles of at most TMAX nodes; a tile of cnt nodes runs the

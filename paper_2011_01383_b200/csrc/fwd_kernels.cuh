@@ -51,12 +51,19 @@ struct FwdArgs {
 // the separate trace build (libcx_trace.so, -DCX_TRACE: SURVEY §8(d)
 // "per-level breakdown from a separate CX_TRACE_LEVELS build"); the product
 // library carries no trace checks on the hot path.
+// Marks record clock64() (a few cycles; %globaltimer reads cost ~0.2 us each
+// and distorted per-level timings); slot 0 (entry) and the last slot (exit)
+// also record %globaltimer into trace[gridDim.x * slots + 2 * cta + {0, 1}]
+// so the host can align CTAs on different SMs.
 __device__ __forceinline__ void trace_mark(const FwdArgs &a, int s) {
 #ifdef CX_TRACE
   if (a.trace && threadIdx.x == 0 && s < a.trace_slots) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[(size_t)blockIdx.x * a.trace_slots + s] = t;
+    a.trace[(size_t)blockIdx.x * a.trace_slots + s] = clock64();
+    if (s == 0 || s == a.trace_slots - 1) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[(size_t)gridDim.x * a.trace_slots + 2 * blockIdx.x + (s ? 1 : 0)] = t;
+    }
   }
 #else
   (void)a;

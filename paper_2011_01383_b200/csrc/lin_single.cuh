@@ -82,8 +82,14 @@ __device__ __forceinline__ LinOut lin_single_body(const LinArgs &a, int *sm, int
     const long long pv = blockIdx.x + (long long)gridDim.x * tid;
     if (pv < n) pf_w = __ldg(pf.words + pv);
   }
+  // the children, as 4-byte cp.async copies: every piece in flight at once
+  // (one HBM round trip, not one per loop iteration); waited before the
+  // barrier below
 #pragma unroll 1
-  for (int i = tid; i < maxc * n; i += nthr) ch[i] = __ldg(a.ch + i);
+  for (int i = tid; i < maxc * n; i += nthr) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(ch + i);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(a.ch + i) : "memory");
+  }
   if (pf_w >= 0 && pf_w < pf.V) {
     const float *row = pf.emb + (size_t)pf_w * pf.H;
 #pragma unroll 1
@@ -102,6 +108,7 @@ __device__ __forceinline__ LinOut lin_single_body(const LinArgs &a, int *sm, int
     s_round = 0;
     s_max = 0;
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
 
   // a1: validation + in-degree; errors latched in shared memory (lowest key).

@@ -23,7 +23,7 @@ weights = [t(w, np.float32) for w in inp["weights"]]
 cell, H = inp["cell"], inp["H"]
 S = 128
 info = cx.launch_info(cell, H)
-buf = torch.zeros(info["ctas"] * S, dtype=torch.int64, device=dev)
+buf = torch.zeros(info["ctas"] * (S + 2), dtype=torch.int64, device=dev)
 lbuf = torch.zeros(32, dtype=torch.int64, device=dev)
 L = cx.lib()
 L.cx_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
@@ -57,26 +57,35 @@ for rep in range(3):
     flush.fill_(1.0)
     g.replay()
     torch.cuda.synchronize()
-tr = buf.view(info["ctas"], S).cpu().numpy().astype(np.int64)
+C = info["ctas"]
+raw = buf.cpu().numpy().astype(np.int64)
+clk = raw[:C * S].reshape(C, S)
+gt = raw[C * S:C * S + 2 * C].reshape(C, 2)
+MHZ = float(os.environ.get("CX_SM_MHZ", "1965"))
+# per CTA: clock64 deltas from its entry mark (slot 0), placed on the common
+# time axis by the CTA's entry %globaltimer
+t0 = gt[:, 0].min()
+tr = np.full((C, S), np.nan)
+for c in range(C):
+    ok = clk[c] != 0
+    tr[c, ok] = (gt[c, 0] - t0) / 1000.0 + (clk[c, ok] - clk[c, 0]) / MHZ
 nl = lin.header_dict()["num_levels"]
-t0 = tr[:, 0].min()
-rel = lambda x: (x - t0) / 1000.0
-print(f"{name}: ctas={info['ctas']} levels={nl}")
-if not fused:
-    lt = lbuf.cpu().numpy().astype(np.int64)
-    print(f"cx_linearize (CTA 0): entry {rel(lt[0]):7.2f}  end {rel(lt[6]):7.2f} us (relative to the forward's entry)")
-for sl, nm in [(0, "entry"), (20, "lin (fused)"), (1, "labels"), (12, "leaf words"), (13, "leaf gather"), (2, "leaf phase")] + [(3 + l, f"level {l}") for l in range(1, nl)] + [(S - 1, "exit")]:
+print(f"{name}: ctas={C} levels={nl} (clock64 marks at {MHZ:.0f} MHz, CTAs aligned by %globaltimer at entry)")
+print(f"exit by %globaltimer: min {(gt[:, 1].min() - t0) / 1000:7.2f} max {(gt[:, 1].max() - t0) / 1000:7.2f} us")
+for sl, nm in [(0, "entry"), (21, "early leaves"), (20, "lin (fused)"), (1, "level lists"), (22, "leaf import"),
+               (2, "leaf phase")] + [(3 + l, f"level {l}") for l in range(1, nl)] + [(S - 1, "exit")]:
     col = tr[:, sl]
-    ok = col > 0
+    ok = ~np.isnan(col)
     if not ok.any():
         continue
-    print(f"{nm:12s} min {rel(col[ok].min()):7.2f} max {rel(col[ok].max()):7.2f}")
-print("first tile of each level, mean over CTAs with a tile (us): list->meta, meta->pulled, pulled->contracted, ->epilogue")
+    print(f"{nm:13s} min {col[ok].min():7.2f} max {col[ok].max():7.2f}")
+print("first tile of each level, mean over CTAs with a tile (us): start->waited, waited->contracted, "
+      "contracted->epilogue math (warp 0), ->pushed")
 for l in range(1, nl):
     b = 24 + 5 * l
-    blk = tr[:, b:b + 5]
-    ok = (blk > 0).all(axis=1)
+    blk = tr[:, [b, b + 1, b + 3, b + 2, b + 4]]
+    ok = ~np.isnan(blk).any(axis=1)
     if ok.any():
-        d = np.diff(blk[ok], axis=1).mean(axis=0) / 1000
-        pre = (blk[ok][:, 0] - tr[ok, 2 + l]).mean() / 1000 if l > 1 else (blk[ok][:, 0] - tr[ok, 2]).mean() / 1000
-        print(f"level {l}: barrier->list {pre:5.2f}  " + "  ".join(f"{x:5.2f}" for x in d))
+        d = np.diff(blk[ok], axis=1).mean(axis=0)
+        mx = np.diff(blk[ok], axis=1).max(axis=0)
+        print(f"level {l:2d}: " + "  ".join(f"{x:5.2f}" for x in d) + "   max " + "  ".join(f"{x:5.2f}" for x in mx))

@@ -27,7 +27,7 @@ weights = [t(w, np.float32) for w in inp["weights"]]
 cell, H = inp["cell"], inp["H"]
 S = 256
 info = cx.launch_info(cell, H)
-buf = torch.zeros(info["ctas"] * S, dtype=torch.int64, device=dev)
+buf = torch.zeros(info["ctas"] * (S + 2), dtype=torch.int64, device=dev)
 L = cx.lib()
 L.cx_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
