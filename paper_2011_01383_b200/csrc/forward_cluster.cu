@@ -170,7 +170,11 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   __shared__ int s_nodes[LEAFB];
   __shared__ int s_word[LEAFB];
   __shared__ float s_bias[4 * kCUnits];
-  __shared__ __align__(16) float s_stage[2][(TMAX > Cfg::TLEAF ? TMAX : Cfg::TLEAF) * kCUnits];  // a tile's new h slices (push mode)
+  // push mode: the new h slices of up to SG nodes (several tiles of a level)
+  // are staged, then pushed after ONE __syncthreads (double-buffered)
+  constexpr int SG = 32;
+  static_assert(SG % TMAX == 0 && SG % Cfg::TLEAF == 0 && SG >= LEAFB, "stage groups align with tiles");
+  __shared__ __align__(16) float s_stage[2][SG * kCUnits];
 
   cg::cluster_group cl = cg::this_cluster();
   const int maxc = a.maxc;
@@ -179,13 +183,14 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int hu = lane & 15;  // half-warp lane: row-piece and push mapping
   const int unit0 = crank * kCUnits;
+  const Roles<1> ro(warp, lane);  // one unit per warp (UW = 1, warp_engine.cuh)
   const int myu = unit0 + warp;  // this warp's hidden unit
   const bool latch = crank == 0;
   trace_mark(a, 0);
 
   // ---- weights -> registers (first the leaf / projection gates): inputs only,
   // so this overlaps cx_linearize under programmatic dependent launch --------
-  float w[4][KC];
+  WRegs<H> w;
   Gate gs[4];
   int ng;
   if constexpr (CELL == CX_TREELSTM) {
@@ -196,7 +201,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     ng = 2;
   }
   auto load_leaf_weights = [&]() {
-    load_wregs_w<4, KC>(w, gs, ng, myu, lane);
+    load_wregs_w<4, H, 1>(w, gs, ng, myu, ro);
     if constexpr (CELL == CX_TREELSTM) {
       if (tid < 4 * kCUnits) {
         int g = tid / kCUnits, uu = tid % kCUnits;
@@ -210,7 +215,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   auto load_rec_weights = [&]() {  // TreeLSTM recurrent gates U_iou, U_f
     gs[0] = {a.w[1], 0, H, 0}; gs[1] = {a.w[1], H, H, 0}; gs[2] = {a.w[1], 2 * H, H, 0};
     gs[3] = {a.w[3], 0, H, 0};
-    load_wregs_w<4, KC>(w, gs, 4, myu, lane);
+    load_wregs_w<4, H, 1>(w, gs, 4, myu, ro);
   };
   constexpr bool EARLY = FUSED && CELL == CX_TREELSTM;
   if constexpr (FUSED && !EARLY) {
@@ -297,19 +302,21 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       ecnt += tot;
       __syncthreads();
     }
+    trace_mark(a, 13);
     for (int b0 = 0; b0 < ecnt; b0 += EB) {
       const int cntb = min(EB, ecnt - b0);
       if (b0) __syncthreads();  // E is overwritten
       gather_rows_c<1, H>(E, cntb, [&](int t, int) { return a.emb + (size_t)ewd[b0 + t] * H; });
       __syncthreads();
+      trace_mark(a, 14);
       for (int t0 = 0; t0 < cntb; t0 += Cfg::TLEAF) {
         const int cntt = min(Cfg::TLEAF, cntb - t0);
         auto tile = [&](auto tt) {
           constexpr int T = decltype(tt)::value;
           float r[3];
-          contract_w<RLstmLeaf, H, T>(E + (size_t)t0 * H, w, r);
-          const int tn = node_of_lane<T>(lane);
-          if (lead_lane<T>(lane) && tn < cntt) {
+          const bool act = contract_w<RLstmLeaf, H, T, 1>(E + (size_t)t0 * H, w, r, ro, nullptr);
+          const int tn = node_of_lane<T, 1>(lane);
+          if (act && tn < cntt) {
             const size_t o = (size_t)elist[b0 + t0 + tn] * H + myu;
             const float cc = sigmoidf_(r[0] + s_bias[warp]) * tanhf_(r[2] + s_bias[32 + warp]);
             a.h_out[o] = sigmoidf_(r[1] + s_bias[16 + warp]) * tanhf_(cc);
@@ -319,6 +326,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
         dispatch_tile<Cfg::TLEAF>(cntt, tile);
       }
     }
+    trace_mark(a, 15);
     __syncthreads();  // the linearizer reuses the shared memory
     if (tid == 0) {
       __threadfence();
@@ -529,6 +537,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   // the parent's slot row; both modes -- this CTA's 16-unit slice of c (the
   // parents' forget-gate term), and of h in pull mode
   if constexpr (EARLY) {
+    trace_mark(a, 17);
     if (tid == 0) {
       unsigned long long spins = 0;
       while (ld_relaxed_u32(&a.bar->count) < gridDim.x)
@@ -536,6 +545,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       (void)ld_acquire_u32(&a.bar->count);
     }
     __syncthreads();
+    trace_mark(a, 18);
     const int nl0 = s.coff[1];
     constexpr int Q4 = H / 4;
     // cp.async (L2 -> shared, all pieces in flight at once, one wait)
@@ -583,8 +593,8 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   };
   // push mode, node v (tile slot t) finished with h = hh, c = cc at this warp's
   // unit: caller outputs straight from the epilogue, the h value into the stage
-  int sb = 0;  // stage buffer of the current tile (double-buffered)
-  auto emit = [&](int v, int t, float hh, float cc) {
+  int sb = 0;  // stage buffer of the current group (double-buffered)
+  auto emit = [&](int v, int t, float hh, float cc) {  // t: position in the stage group
     const size_t o = (size_t)s.perm[v] * H + myu;
     a.h_out[o] = hh;
     if (CELL == CX_TREELSTM && a.aux_out) a.aux_out[o] = cc;
@@ -603,10 +613,11 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
 #pragma unroll
     for (int q4 = 0; q4 < kCUnits / 4; q4++) st_async_v4(dst + 16u * q4, src[q4], bar);
   };
-  // after a tile's epilogue: stage complete, push, flip the stage buffer
-  auto push_tile = [&](const int *tl, int cntt) {
+  // after the last tile of a stage group (nodes gl[0 .. cntg)): stage
+  // complete, push, flip the stage buffer
+  auto flush = [&](const int *gl, int cntg) {
     __syncthreads();
-    if (tid < cntt * kCUnits) push_slice(tl[tid >> 4], tid >> 4);
+    if (tid < cntg * kCUnits) push_slice(gl[tid >> 4], tid >> 4);
     sb ^= 1;
   };
 
@@ -635,23 +646,23 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
         const int cntt = min(Cfg::TLEAF, cntb - t0);
         auto tile = [&](auto tt) {
           constexpr int T = decltype(tt)::value;
-          const int tn = node_of_lane<T>(lane);
-          const bool lead = lead_lane<T>(lane) && tn < cntt;
+          const int tn = node_of_lane<T, 1>(lane);
+          bool lead;
           if constexpr (CELL == CX_TREELSTM) {
             float r[3];
-            contract_w<RLstmLeaf, H, T>(X + (size_t)t0 * H, w, r);
+            lead = contract_w<RLstmLeaf, H, T, 1>(X + (size_t)t0 * H, w, r, ro, nullptr) && tn < cntt;
             if (lead) {
               const int v = s_nodes[t0 + tn];
               const float cc = sigmoidf_(r[0] + s_bias[warp]) * tanhf_(r[2] + s_bias[32 + warp]);
               const float hh = sigmoidf_(r[1] + s_bias[16 + warp]) * tanhf_(cc);
               s.aux[(size_t)v * kCUnits + warp] = cc;
-              if (push) emit(v, tn, hh, cc);
+              if (push) emit(v, t0 + tn, hh, cc);
               else s.hsl[(size_t)v * kCUnits + warp] = hh;
             }
-            if (push) push_tile(s_nodes + t0, cntt);
+            if (push && t0 + Cfg::TLEAF >= cntb) flush(s_nodes, cntb);
           } else {
             float r[1];
-            contract_w<RDagLeaf, H, T>(X + (size_t)t0 * H, w, r);
+            lead = contract_w<RDagLeaf, H, T, 1>(X + (size_t)t0 * H, w, r, ro, nullptr) && tn < cntt;
             if (lead) s.hsl[(size_t)s_nodes[t0 + tn] * kCUnits + warp] = tanhf_(r[0] + s_bias[warp]);
           }
         };
@@ -708,15 +719,16 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       }
       auto tile = [&](auto tt) {
         constexpr int T = decltype(tt)::value;
-        const int tn = node_of_lane<T>(lane);
-        const bool lead = lead_lane<T>(lane) && tn < cntt;
+        const int tn = node_of_lane<T, 1>(lane);
+        bool lead;
         if constexpr (CELL == CX_TREELSTM) {
           float r[3 + MAXC];
           if (push)  // the MAXC child rows of each node, h~ summed in registers
-            contract_w<RLstmLevel<MAXC>, H, T, false>(
-                XA + (size_t)(lbase + t0 - s.coff[1]) * MAXC * H, w, r);
+            lead = contract_w<RLstmLevel<MAXC>, H, T, 1, false>(
+                XA + (size_t)(lbase + t0 - s.coff[1]) * MAXC * H, w, r, ro, nullptr);
           else
-            contract_w<RLstmLevel<MAXC>, H, T, true>(s.X, w, r);
+            lead = contract_w<RLstmLevel<MAXC>, H, T, 1, true>(s.X, w, r, ro, nullptr);
+          lead = lead && tn < cntt;
           if (t0 == 0 && l < 20) trace_mark(a, tb + 3);
           if (lead) {
             const int v = tl[tn];
@@ -729,14 +741,17 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
             }
             const float hh = sigmoidf_(r[1] + s_bias[16 + warp]) * tanhf_(cc);
             s.aux[(size_t)v * kCUnits + warp] = cc;
-            if (push) emit(v, tn, hh, cc);
+            if (push) emit(v, (t0 % SG) + tn, hh, cc);
             else s.hsl[(size_t)v * kCUnits + warp] = hh;
           }
           if (t0 == 0 && l < 20) trace_mark(a, tb + 2);
-          if (push) push_tile(tl, cntt);
+          if (push && ((t0 + TMAX) % SG == 0 || t0 + TMAX >= cnt)) {
+            const int g0 = t0 - t0 % SG;
+            flush(s.list + lbase + g0, t0 + cntt - g0);
+          }
         } else {
           float r[1];
-          contract_w<CDagLevel<MAXC>, H, T, true>(s.X, w, r);
+          lead = contract_w<CDagLevel<MAXC>, H, T, 1, true>(s.X, w, r, ro, nullptr) && tn < cntt;
           if (lead) s.hsl[(size_t)tl[tn] * kCUnits + warp] = tanhf_(r[0] + s_bias[warp]);
         }
         if (!push) __syncthreads();

@@ -72,7 +72,7 @@ for c in range(C):
 nl = lin.header_dict()["num_levels"]
 print(f"{name}: ctas={C} levels={nl} (clock64 marks at {MHZ:.0f} MHz, CTAs aligned by %globaltimer at entry)")
 print(f"exit by %globaltimer: min {(gt[:, 1].min() - t0) / 1000:7.2f} max {(gt[:, 1].max() - t0) / 1000:7.2f} us")
-for sl, nm in [(0, "entry"), (21, "early leaves"), (20, "lin (fused)"), (1, "level lists"), (22, "leaf import"),
+for sl, nm in [(0, "entry"), (13, "e: compacted"), (14, "e: gathered"), (15, "e: tiles"), (21, "early leaves"), (20, "lin (fused)"), (1, "level lists"), (17, "push setup"), (18, "leaves ready"), (22, "leaf import"),
                (2, "leaf phase")] + [(3 + l, f"level {l}") for l in range(1, nl)] + [(S - 1, "exit")]:
     col = tr[:, sl]
     ok = ~np.isnan(col)
