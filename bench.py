@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes
+import faulthandler
 import json
 import os
 import statistics
@@ -86,8 +87,23 @@ def make_inputs(name, rank, world, seed=0):
                 g0=g0, g1=g1)
 
 
-def algorithmic_work(cell, H, n, n_leaves, n_internal, batch, maxc=2):
-    """Algorithmic flops and bytes per step."""
+WEIGHT_FLOATS = {  # per cell, cx_weights order (include/cx.h): matrices + biases
+    synth.TREERNN: lambda H: 0,
+    synth.TREEFC: lambda H: 2 * H * H + H,
+    synth.TREELSTM: lambda H: 7 * H * H + 4 * H,
+    synth.TREEGRU: lambda H: 5 * H * H + 3 * H,
+    synth.MVRNN: lambda H: 4 * H * H + H,
+    synth.DAGRNN: lambda H: 2 * H * H + H,
+}
+
+
+def algorithmic_work(cell, H, n, n_leaves, n_internal, batch, maxc=2, vocab=None, hoisted=False):
+    """Algorithmic flops and bytes per step: flops of
+    the cell over every node; bytes = children + word ids + the Emb rows read +
+    h_out written + the weights once. Returns (flops, bytes, flops_performed):
+    with computation hoisting (the leaf cell / input projection evaluated once
+    per vocabulary word) the kernel performs the leaf work for
+    `vocab` words instead of every leaf (DAG-RNN: every node's projection)."""
     leaf_f = {synth.TREELSTM: 6 * H * H, synth.TREEGRU: 4 * H * H, synth.DAGRNN: 2 * H * H}.get(cell, 0)
     int_f = {synth.TREERNN: H, synth.TREEFC: 4 * H * H, synth.TREELSTM: 10 * H * H,
              synth.TREEGRU: 8 * H * H, synth.MVRNN: 4 * H ** 3 + 8 * H * H,
@@ -95,11 +111,117 @@ def algorithmic_work(cell, H, n, n_leaves, n_internal, batch, maxc=2):
     flops = leaf_f * n_leaves + int_f * n_internal
     if cell == synth.DAGRNN:
         flops += 2 * H * H * n_internal  # every node has an input projection
+    performed = flops
+    if hoisted and vocab:
+        if cell == synth.DAGRNN:  # projection once per word
+            performed = int_f * n_internal + 2 * H * H * vocab
+        else:
+            performed = leaf_f * min(vocab, n_leaves) + int_f * n_internal
     emb_rows = n if cell == synth.DAGRNN else n_leaves
     bytes_ = 4 * maxc * n + 4 * n + 4 * H * emb_rows + 4 * H * n  # children, words, Emb, h_out
+    bytes_ += 4 * WEIGHT_FLOATS[cell](H)
     if cell == synth.MVRNN:
         bytes_ += 4 * H * H * n_leaves
-    return flops, bytes_
+    return flops, bytes_, performed
+
+
+def hoisting_applies(cell, n, n_leaves, vocab, dtype_name, fused):
+    """Whether the forward evaluates the leaf cell / projection per word
+    (forward_tc.cu tc_hoist, forward_big.cu): batches with more leaves
+    (DAG-RNN: nodes) than V / 2 on the large-batch paths."""
+    if fused:
+        return False
+    if cell == synth.TREELSTM:
+        return n_leaves > vocab // 2 and (dtype_name == "bf16" or n > 32768)
+    if cell == synth.DAGRNN:
+        return n > vocab and (dtype_name == "f32" and n > 32768)
+    return False
+
+
+def cpu_info():
+    """CPU model and core counts of the host (for the oracle baselines)."""
+    model, phys = None, set()
+    try:
+        cur = {}
+        for ln in open("/proc/cpuinfo"):
+            if ":" in ln:
+                k, v = [x.strip() for x in ln.split(":", 1)]
+                if k == "model name" and model is None:
+                    model = v
+                if k in ("physical id", "core id"):
+                    cur[k] = v
+            elif cur:
+                phys.add((cur.get("physical id"), cur.get("core id")))
+                cur = {}
+    except OSError:
+        pass
+    logical = os.cpu_count()
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = logical
+    return {"cpu_model": model, "physical_cores": len(phys) or None, "logical_cores": logical,
+            "usable_cores": usable}
+
+
+# ---------------------------------------------------------------------------
+# critical-path bound (SURVEY §8(d)): T_cp = t_launch + (L - 1) t_sync + L t_chain
+# ---------------------------------------------------------------------------
+def launch_floor_us(n_launches, dev, reps=50):
+    """Mean event time of a CUDA graph of `n_launches` empty kernels, replayed
+    with the same L2 flush between replays as the timed steps."""
+    import torch
+    import paper_2011_01383_b200 as cx
+    L = cx.lib()
+    L.cx_debug_empty.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
+                                 ctypes.c_void_p]
+
+    def fn():  # the current stream at call time (the capture stream inside the graph)
+        st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        for _ in range(n_launches):
+            L.cx_debug_empty(1, 32, 0, None, st)
+
+    fn()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    ev = []
+    for i in range(reps + 5):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        g.replay()
+        a1.record(stream)
+        flush.fill_(1.0)
+        if i >= 5:
+            ev.append((a0, a1))
+    torch.cuda.synchronize()
+    return statistics.median(x.elapsed_time(y) for x, y in ev) * 1e3
+
+
+SYNC_KINDS = {0: "push hand-off (st.async + mbarrier, 16-CTA cluster)",
+              1: "barrier.cluster (16-CTA cluster)",
+              2: "grid barrier (release/acquire counter, 1 CTA per SM)"}
+
+
+def critical_path(levels, n_launches, sync_kind, sm_mhz, dev):
+    """Measured components of the critical-path bound, in this process."""
+    import paper_2011_01383_b200 as cx
+    cyc = {k: cx.diag_sync_cycles(k, 4000 if k != 2 else 1000, dev) for k in (0, 1, 2, 3)}
+    us = {k: v / sm_mhz for k, v in cyc.items()}
+    t_launch = launch_floor_us(n_launches, dev)
+    t_cp = t_launch + (levels - 1) * us[sync_kind] + levels * us[3]
+    return {"t_launch_us": t_launch, "launches": n_launches, "levels": levels,
+            "t_sync_us": us[sync_kind], "sync": SYNC_KINDS[sync_kind], "t_chain_us": us[3],
+            "T_cp_us": t_cp,
+            "sync_us_all": {"push": us[0], "cluster_barrier": us[1], "grid_barrier": us[2]},
+            "cycles": {"push": cyc[0], "cluster_barrier": cyc[1], "grid_barrier": cyc[2],
+                       "chain": cyc[3]},
+            "sm_mhz": sm_mhz,
+            "formula": "T_cp = t_launch + (L-1) t_sync + L t_chain (SURVEY 8(d)); t_sync, t_chain "
+                       "from cx_diag_sync_cycles on this device, t_launch = empty-kernel graph "
+                       "replay with the step's L2 flush"}
 
 
 def measured_peaks():
@@ -194,30 +316,73 @@ def run_reference(args, rank, world):
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": name, "batch_per_step": cap, "hidden": H},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": sample},
+            "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                  "sample": sample}, **cpu_info()),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(name, seconds=12.0):
-    """The oracle as it stands, timed on one host core, on a bounded sample."""
+def _oracle_rate(inp, cell, H, V, cap, seconds):
+    """Structures per second of the oracle (linearize + forward) on the first
+    `cap` structures of `inp`, repeated for about `seconds`."""
     import oracle
-    inp = make_inputs(name, 0, 1)
-    gen, cell, H, V, batch, _ = WORKLOADS[name]
-    cap = min(batch, 16)
     b = int(inp["offsets"][cap])
     sub, words = inp["children"][:, :b], inp["words"][:b]
     done, t0 = 0, time.perf_counter()
     while True:
-        lin = oracle.linearize(sub, inp["kind"])
+        oracle.linearize(sub, inp["kind"])
         oracle.forward(cell, H, V, inp["weights"], inp["emb"], words, sub)
         done += 1
         el = time.perf_counter() - t0
         if el >= seconds or (done >= 3 and el * (done + 1) / done > seconds * 1.5):
             break
-    return {"value": done * cap / el, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{done} x {cap} structures of {name} in {el:.1f}s (fp64 naive recursion, 1 thread)"}
+    return done, el
+
+
+def cpu_baseline(name, seconds=12.0):
+    """The oracle as it stands (fp64 naive recursion), timed on the host cores
+    on bounded samples: the workload itself on 1 thread, and (default
+    workload) the batch-4096 TreeLSTM config split over T =
+    hardware-concurrency threads and on 1 thread (SURVEY 8(d) timing
+    protocol). ctypes releases the GIL during the C calls."""
+    inp = make_inputs(name, 0, 1)
+    gen, cell, H, V, batch, _ = WORKLOADS[name]
+    cap = min(batch, 16)
+    done, el = _oracle_rate(inp, cell, H, V, cap, seconds)
+    out = {"value": done * cap / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+           "sample": f"{done} x {cap} structures of {name} in {el:.1f}s (fp64 naive recursion, 1 thread)"}
+    out.update(cpu_info())
+    if name == "cfg2_treelstm_b10":
+        big = make_inputs("cfg5_treelstm_b4096", 0, 1)
+        _, bcell, bH, bV, _, _ = WORKLOADS["cfg5_treelstm_b4096"]
+        T = max(1, out["usable_cores"] or 1)
+        per = 16  # trees per call per thread
+        res = [None] * T
+
+        def work(i):
+            off = big["offsets"]
+            g0 = (i * per) % (len(off) - 1 - per)
+            blk = big["children"][:, off[g0]:off[g0 + per]]
+            sub = dict(big, children=np.where(blk >= 0, blk - off[g0], -1).astype(np.int32),
+                       words=big["words"][off[g0]:off[g0 + per]],
+                       offsets=off[g0:g0 + per + 1] - off[g0])
+            res[i] = _oracle_rate(sub, bcell, bH, bV, per, seconds * 0.6)
+
+        th = [threading.Thread(target=work, args=(i,)) for i in range(T)]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        wall = time.perf_counter() - t0
+        trees = sum(d * per for d, _ in res)
+        d1, e1 = _oracle_rate(big, bcell, bH, bV, per, seconds * 0.3)
+        out["b4096"] = {"threads": T, "value": trees / wall, "unit": UNIT,
+                        "sample": f"{trees} trees of cfg5_treelstm_b4096 ({per} per call) on {T} "
+                                  f"threads in {wall:.1f}s",
+                        "one_thread": {"value": d1 * per / e1,
+                                       "sample": f"{d1} x {per} trees in {e1:.1f}s"}}
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -445,6 +610,7 @@ def run_gpu(args, rank, world, local_rank):
         [np.asarray(ch_np, np.int32).ravel(), np.asarray(inp["words"], np.int32)]))).pin_memory()
     in_dev = torch.empty_like(in_host, device=dev)
     roots_host = torch.empty((R, H), dtype=torch.float32).pin_memory()
+    h_host = torch.empty((n, H), dtype=torch.float32).pin_memory()
     ch_dev = in_dev[:maxc_ * n].view(maxc_, n)
     w_dev = in_dev[maxc_ * n:]
     e2e_steps = max(5, min(args.steps, 200))
@@ -452,34 +618,42 @@ def run_gpu(args, rank, world, local_rank):
     # on fixed device buffers (one C call per step)
     plan = cx.LinearizeForwardPlan(ch_dev, inp["kind"], cell, H, weights, emb, w_dev,
                                    dtype=dtype, num_roots=R)
-    for _ in range(3):
-        in_dev.copy_(in_host, non_blocking=True)
-        plan()
-        roots_host.copy_(plan.root_out, non_blocking=True)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e2e_ms = []
-    for _ in range(e2e_steps):
-        s0 = torch.cuda.Event(enable_timing=True)
-        s1 = torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        in_dev.copy_(in_host, non_blocking=True)
-        plan()
-        roots_host.copy_(plan.root_out, non_blocking=True)
-        s1.record(stream)
-        s1.synchronize()  # the host reads the step's result
-        e2e_ms.append(s0.elapsed_time(s1))
-        flush.fill_(1.0)
-    torch.cuda.synchronize()
-    e2e_total = sum(e2e_ms)
-    if world > 1:
-        tt = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_total = float(tt.item())
-    e2e_value = trees_total / (e2e_total / e2e_steps / 1e3)
+    def e2e_run(full):
+        """Per step: inputs H2D from pinned memory, the C call, the result D2H
+        (every node's h -- cx_forward's output -- or only the packed roots)."""
+        for _ in range(3):
+            in_dev.copy_(in_host, non_blocking=True)
+            plan()
+            (h_host.copy_(plan.h_out, non_blocking=True) if full
+             else roots_host.copy_(plan.root_out, non_blocking=True))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = []
+        for _ in range(e2e_steps):
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            in_dev.copy_(in_host, non_blocking=True)
+            plan()
+            (h_host.copy_(plan.h_out, non_blocking=True) if full
+             else roots_host.copy_(plan.root_out, non_blocking=True))
+            s1.record(stream)
+            s1.synchronize()  # the host reads the step's result
+            ms.append(s0.elapsed_time(s1))
+            flush.fill_(1.0)
+        torch.cuda.synchronize()
+        tot = sum(ms)
+        if world > 1:
+            tt = torch.tensor([tot], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tot = float(tt.item())
+        return trees_total / (tot / e2e_steps / 1e3)
+
+    e2e_value = e2e_run(full=True)
+    e2e_roots_value = e2e_run(full=False)
     h2d = in_host.numel() * 4
-    d2h = roots_host.numel() * 4
+    d2h = h_host.numel() * 4
 
     secondary = None
     if args.secondary and name == "cfg2_treelstm_b10":
@@ -488,10 +662,13 @@ def run_gpu(args, rank, world, local_rank):
     if rank != 0:
         return
     # the dominant kernel: the fused kernel (= the whole step) or cx_forward's
-    fwd_mean = sum(step_ms) / len(step_ms) if fused else sum(fwd_ms) / len(fwd_ms)
-    flops, alg_bytes = algorithmic_work(cell, H, n, n_leaves, n - n_leaves, R, ch_np.shape[0])
+    step_mean = sum(step_ms) / len(step_ms)
+    fwd_mean = step_mean if fused else sum(fwd_ms) / len(fwd_ms)
+    hoisted = hoisting_applies(cell, n, n_leaves, V, args.dtype, fused)
+    flops, alg_bytes, performed = algorithmic_work(cell, H, n, n_leaves, n - n_leaves, R,
+                                                   ch_np.shape[0], vocab=V, hoisted=hoisted)
     achieved = flops / (fwd_mean / 1e3) / 1e12
-    info = cx.launch_info(cell, H, V, dtype)
+    info = cx.linearize_forward_launch_info(cell, H, n, ch_np.shape[0], V, dtype)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "forward_traffic.json")
     if os.path.exists(prof):
@@ -500,27 +677,47 @@ def run_gpu(args, rank, world, local_rank):
                 f"{name}:fused" if fused else name if args.dtype == "f32" else f"{name}:bf16")
         except Exception:
             traffic = None
+    peaks = measured_peaks()
+    hbm_peak = peaks["hbm_gbs"] if peaks else 7700.0
+    clocks = sampler.summary()
+    sm_mhz = clocks.get("sm_mhz") or 1965.0
+    # level-to-level synchronisation of the kernel that runs: the fused cluster
+    # kernel's push hand-off (TreeLSTM trees) or cluster barrier (DAG-RNN),
+    # else a grid barrier (register / shared-memory / tensor-core kernels)
+    if fused:
+        sync_kind = 0 if (cell == synth.TREELSTM and inp["kind"] != synth.DAG) else 1
+    else:
+        sync_kind = 2
+    cp = critical_path(L, 1 if fused else 2, sync_kind, sm_mhz, dev)
+    step_us = step_mean * 1e3
     if args.dtype == "bf16":
-        peaks = measured_peaks()
         peak, src = (peaks["bf16_tflops"], "MEASURED_PEAKS.json bf16_tflops (burst)") if peaks \
             else (2250.0, "B200 nominal dense bf16 (MEASURED_PEAKS.json absent)")
+        compute_floor = performed / (peak * 1e12) * 1e6
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": traffic,
-                    "kernel": "tc_kernel (cx_forward, dtype bf16)", "flops_per_launch": flops,
-                    "alg_bytes_per_launch": alg_bytes,
-                    "hbm_frac": alg_bytes / (fwd_mean / 1e3) / 1e9 /
-                                (peaks["hbm_gbs"] if peaks else 7700.0),
+                    "kernel": "tc_kernel (cx_forward, dtype bf16)",
                     "note": f"peak = {src}; algorithmic flops (SURVEY 8(d)), not the MMA's "
                             "(child-sum by linearity issues 16H^2 per TreeLSTM node)"}
     else:
+        compute_floor = performed / (FMA_PEAK_TFLOPS * 1e12) * 1e6
         roofline = {"bound": "alu", "achieved": achieved, "peak": FMA_PEAK_TFLOPS,
                     "unit": "TFLOP/s", "frac": achieved / FMA_PEAK_TFLOPS, "traffic": traffic,
                     "kernel": "ck_kernel<fused> (cx_linearize_forward, one launch per step)"
-                              if fused else "fwd_kernel (cx_forward)", "flops_per_launch": flops,
-                    "alg_bytes_per_launch": alg_bytes,
-                    "note": "fp32 FMA peak = 148 SM x 128 lanes x 2 x 1.965 GHz; the step is "
-                            "critical-path (levels x barrier) bound, see DESIGN.md"}
-    clocks = sampler.summary()
+                              if fused else "forward kernel (cx_forward)",
+                    "note": "fp32 FMA peak = 148 SM x 128 lanes x 2 x 1.965 GHz (DESIGN.md 7)"}
+    floors = {"compute": compute_floor, "hbm": alg_bytes / (hbm_peak * 1e9) * 1e6,
+              "critical_path": cp["T_cp_us"]}
+    binding = max(floors, key=floors.get)
+    roofline.update({
+        "flops_per_launch": flops, "flops_performed": performed, "hoisted_leaf_work": hoisted,
+        "alg_bytes_per_launch": alg_bytes,
+        "alg_bytes_note": "children + word ids + Emb rows read + h_out written + weights once",
+        "hbm_achieved_gbs": alg_bytes / (fwd_mean / 1e3) / 1e9, "hbm_peak_gbs": hbm_peak,
+        "floors_us": floors, "binding": binding,
+        "binding_frac": floors[binding] / step_us,
+        "critical_path": dict(cp, frac=cp["T_cp_us"] / step_us),
+    })
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -545,7 +742,10 @@ def run_gpu(args, rank, world, local_rank):
         "launch": info,
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h,
+                "what": "LinearizeForwardPlan (one cx_linearize_forward C call) per step; "
+                        "children + word ids H2D from pinned memory, every node's h_out D2H",
+                "roots_only": {"value": e2e_roots_value, "d2h_bytes_per_step": R * H * 4}},
         "clocks": clocks,
     }
     if secondary:
@@ -556,6 +756,7 @@ def run_gpu(args, rank, world, local_rank):
 
 
 def main():
+    faulthandler.enable()  # a native crash prints the Python stack
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=500)

@@ -198,6 +198,37 @@ const char *cx_status_str(cx_status s);
 cx_status cx_forward_launch_info(const cx_model *model, int32_t *ctas, int32_t *threads,
                                  int32_t *smem_bytes);
 
+/* The launch cx_linearize_forward would make for a batch of n nodes (host,
+ * for reporting): *fused = 1 for the single fused launch, then the shape of
+ * that kernel (CTAs, threads per CTA, dynamic shared memory per CTA, cluster
+ * size); *fused = 0 for the two-launch path, then the shape of cx_forward's
+ * kernel. Any output pointer may be NULL. */
+cx_status cx_linearize_forward_launch_info(const cx_model *model, int32_t n, int32_t max_children,
+                                           int32_t *fused, int32_t *ctas, int32_t *threads,
+                                           int32_t *smem_bytes, int32_t *cluster);
+
+/* ---- Diagnostics (measurement; not part of the hot path) -------------------
+ * cx_diag_sync_cycles: SM cycles per level of one synchronisation or
+ * dependent-arithmetic step of the critical-path bound of SURVEY.md §8(d),
+ * T_cp = t_launch + (L - 1) t_sync + L t_chain, measured on the current
+ * device (see csrc/diag.cu): kind 0 = the cluster kernel's push hand-off
+ * (st.async + mbarrier, 16-CTA cluster), 1 = barrier.cluster, 2 = grid
+ * barrier (release/acquire counter, one CTA per SM; `workspace` = 128 zeroed
+ * bytes, left zeroed), 3 = the dependent arithmetic of one level (H = 256,
+ * one warp). out (device, >= 2 entries): out[0] = cycles per level, out[1] =
+ * levels. Asynchronous on `stream`. */
+cx_status cx_diag_sync_cycles(int32_t kind, int32_t levels, unsigned long long *out,
+                              void *workspace, void *stream);
+
+/* Debug hooks (tools/trace_*.py, tests): %globaltimer / clock64 timelines of
+ * the trace build (libcx_trace.so) and reporting helpers. buf = NULL turns a
+ * trace off. */
+cx_status cx_debug_set_trace(unsigned long long *buf, int32_t slots);
+cx_status cx_debug_set_lin_trace(unsigned long long *buf);
+int32_t cx_debug_fused_applies(const cx_model *model, int32_t n, int32_t max_children);
+cx_status cx_debug_empty(int32_t ctas, int32_t threads, int32_t coop, unsigned long long *t,
+                         void *stream);
+
 #ifdef __cplusplus
 }
 #endif

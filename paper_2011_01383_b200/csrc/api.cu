@@ -368,6 +368,34 @@ const char *cx_status_str(cx_status s) {
   return "unknown status";
 }
 
+cx_status cx_linearize_forward_launch_info(const cx_model *m, int32_t n, int32_t max_children,
+                                           int32_t *fused, int32_t *ctas, int32_t *threads,
+                                           int32_t *smem_bytes, int32_t *cluster) {
+  if (!m || n < 0 || max_children < 1) return CX_E_ARG;
+  cx::FwdPlan plan;
+  int Gn = 0, Gu = 0;
+  std::lock_guard<std::mutex> lk(g_mu);
+  const char *env = std::getenv("CX_FUSED");
+  bool f = !(env && env[0] == '0') && m->dtype == CX_F32 && n > 0 &&
+           (forward_path() == 0 || forward_path() == 3) &&
+           cx::fused_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu);
+  if (!f) {
+    const int sms = num_sms_current();
+    if (sms <= 0) return CX_E_CUDA;
+    const bool ok = m->dtype == CX_BF16
+                        ? cx::tc_plan(m->cell, m->hidden, max_children, sms, &plan, &Gn, &Gu)
+                        : cx::fwd_plan(m->cell, m->hidden, max_children, n > 0 ? n : 1, forward_path(),
+                                       sms, &plan, &Gn, &Gu);
+    if (!ok) return CX_E_UNSUPPORTED;
+  }
+  if (fused) *fused = f ? 1 : 0;
+  if (ctas) *ctas = plan.ctas;
+  if (threads) *threads = plan.threads;
+  if (smem_bytes) *smem_bytes = (int32_t)plan.smem;
+  if (cluster) *cluster = plan.cluster;
+  return CX_OK;
+}
+
 cx_status cx_forward_launch_info(const cx_model *m, int32_t *ctas, int32_t *threads,
                                  int32_t *smem_bytes) {
   if (!m) return CX_E_ARG;

@@ -246,6 +246,43 @@ def _weights(cell, weights):
     return w
 
 
+def linearize_forward_launch_info(cell, hidden, n, max_children, vocab=1, dtype=F32):
+    """The launch cx_linearize_forward makes for n nodes: fused flag and kernel shape."""
+    L = lib()
+    P = ctypes.POINTER(ctypes.c_int32)
+    L.cx_linearize_forward_launch_info.argtypes = [ctypes.POINTER(_Model), ctypes.c_int32,
+                                                   ctypes.c_int32, P, P, P, P, P]
+    L.cx_linearize_forward_launch_info.restype = ctypes.c_int
+    m = _model(cell, hidden, vocab, dtype)
+    v = [ctypes.c_int32() for _ in range(5)]
+    st = L.cx_linearize_forward_launch_info(ctypes.byref(m), n, max_children,
+                                            *[ctypes.byref(x) for x in v])
+    if st != OK:
+        raise CxError(st, "cx_linearize_forward_launch_info")
+    return dict(fused=bool(v[0].value), ctas=v[1].value, threads=v[2].value, smem=v[3].value,
+                cluster=v[4].value)
+
+
+def diag_sync_cycles(kind: int, levels: int, device=None) -> int:
+    """SM cycles per level of a synchronisation / dependent-arithmetic step
+    (cx_diag_sync_cycles: 0 push hand-off, 1 cluster barrier, 2 grid barrier,
+    3 one level's dependent arithmetic). Synchronises the device."""
+    L = lib()
+    L.cx_diag_sync_cycles.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p]
+    L.cx_diag_sync_cycles.restype = ctypes.c_int
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    out = torch.zeros(2, dtype=torch.int64, device=dev)
+    ws = torch.zeros(32, dtype=torch.int32, device=dev)
+    st = L.cx_diag_sync_cycles(kind, levels, ctypes.c_void_p(out.data_ptr()),
+                               ctypes.c_void_p(ws.data_ptr()),
+                               ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    if st != OK:
+        raise CxError(st, "cx_diag_sync_cycles")
+    torch.cuda.synchronize(dev)
+    return int(out[0].item())
+
+
 def fused_applies(cell, hidden, n, max_children, vocab=1, dtype=F32) -> bool:
     """Whether cx_linearize_forward runs as ONE launch for this shape (reporting)."""
     L = lib()

@@ -25,10 +25,20 @@ def declared_functions():
 
 def test_exports_every_declared_symbol(cxmod):
     names = declared_functions()
-    assert len(names) == 9
+    assert len(names) == 15
     L = cxmod.lib()
     for name in names:
         assert hasattr(L, name), name
+
+
+def test_every_exported_symbol_is_declared(cxmod):
+    import subprocess
+    from paper_2011_01383_b200 import _build
+    out = subprocess.run(["nm", "-D", "--defined-only", _build.LIB], capture_output=True,
+                         text=True).stdout
+    exported = sorted({ln.split()[-1] for ln in out.splitlines()
+                       if ln.split() and ln.split()[-1].startswith("cx_")})
+    assert exported == declared_functions()
 
 
 def test_built_for_sm100a(cxmod):
