@@ -48,6 +48,9 @@ WORKLOADS = {
     "cfg5_dagrnn_b10": ("grid", synth.DAGRNN, 256, 20000, 10, "weak"),
     "cfg5_dagrnn_b1": ("grid", synth.DAGRNN, 256, 20000, 1, "weak"),
     "cfg1_treernn": ("perfect3", synth.TREERNN, 8, 100, 1, "weak"),
+    # SimpleTreeGRU (footnote P:1638-1640) at the TreeGRU config
+    "f3_simpletreegru_b10": ("sst", synth.SIMPLETREEGRU, 512, 20000, 10, "weak"),
+    "f3_simpletreegru_b1": ("sst", synth.SIMPLETREEGRU, 512, 20000, 1, "weak"),
     # GRNN-comparison sequences (length 100, H = 256)
     "f4_lstm_seq100_b10": ("chain100", synth.TREELSTM, 256, 20000, 10, "weak"),
     "f4_lstm_seq100_b1": ("chain100", synth.TREELSTM, 256, 20000, 1, "weak"),
@@ -92,6 +95,7 @@ WEIGHT_FLOATS = {  # per cell, cx_weights order (include/cx.h): matrices + biase
     synth.TREEFC: lambda H: 2 * H * H + H,
     synth.TREELSTM: lambda H: 7 * H * H + 4 * H,
     synth.TREEGRU: lambda H: 5 * H * H + 3 * H,
+    synth.SIMPLETREEGRU: lambda H: 5 * H * H + 3 * H,
     synth.MVRNN: lambda H: 4 * H * H + H,
     synth.DAGRNN: lambda H: 2 * H * H + H,
 }
@@ -104,10 +108,11 @@ def algorithmic_work(cell, H, n, n_leaves, n_internal, batch, maxc=2, vocab=None
     with computation hoisting (the leaf cell / input projection evaluated once
     per vocabulary word) the kernel performs the leaf work for
     `vocab` words instead of every leaf (DAG-RNN: every node's projection)."""
-    leaf_f = {synth.TREELSTM: 6 * H * H, synth.TREEGRU: 4 * H * H, synth.DAGRNN: 2 * H * H}.get(cell, 0)
+    leaf_f = {synth.TREELSTM: 6 * H * H, synth.TREEGRU: 4 * H * H, synth.SIMPLETREEGRU: 4 * H * H,
+              synth.DAGRNN: 2 * H * H}.get(cell, 0)
     int_f = {synth.TREERNN: H, synth.TREEFC: 4 * H * H, synth.TREELSTM: 10 * H * H,
-             synth.TREEGRU: 8 * H * H, synth.MVRNN: 4 * H ** 3 + 8 * H * H,
-             synth.DAGRNN: 2 * H * H}[cell]
+             synth.TREEGRU: 8 * H * H, synth.SIMPLETREEGRU: 8 * H * H,
+             synth.MVRNN: 4 * H ** 3 + 8 * H * H, synth.DAGRNN: 2 * H * H}[cell]
     flops = leaf_f * n_leaves + int_f * n_internal
     if cell == synth.DAGRNN:
         flops += 2 * H * H * n_internal  # every node has an input projection

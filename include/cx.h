@@ -44,7 +44,8 @@ extern "C" {
 
 typedef enum { CX_SEQUENCE = 0, CX_TREE = 1, CX_DAG = 2 } cx_kind;
 typedef enum {
-  CX_TREERNN = 0, CX_TREEFC = 1, CX_TREELSTM = 2, CX_TREEGRU = 3, CX_MVRNN = 4, CX_DAGRNN = 5
+  CX_TREERNN = 0, CX_TREEFC = 1, CX_TREELSTM = 2, CX_TREEGRU = 3, CX_MVRNN = 4, CX_DAGRNN = 5,
+  CX_SIMPLETREEGRU = 6  /* footnote P:1638-1640: h = (1 - z) h' at internal nodes; TreeGRU's weights */
 } cx_cell;
 /* compute precision; inputs, weights and outputs are always fp32 */
 typedef enum { CX_F32 = 0, CX_BF16 = 1 } cx_dtype;

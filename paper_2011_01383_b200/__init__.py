@@ -9,7 +9,7 @@ include/cx.h. See DESIGN.md.
     lin, h, aux, roots = cx.linearize_forward(children, cx.TREE, cx.TREELSTM, 256, weights, emb, words)
 """
 from .cx import (BF16, DAG, DAGRNN, F32, MVRNN, SEQUENCE, TREE, TREEFC, TREEGRU, TREELSTM,
-                 TREERNN, CELL_IDS, CxError, Linearization, alloc_linearization, check, forward, launch_info, lib,
+                 TREERNN, SIMPLETREEGRU, CELL_IDS, CxError, Linearization, alloc_linearization, check, forward, launch_info, lib,
                  fused_applies, linearize, linearize_forward, LinearizeForwardPlan, status, status_str,
                  linearize_forward_launch_info, diag_sync_cycles)
 from . import cx as _cx
@@ -19,4 +19,4 @@ OK = _cx.OK
 __all__ = ["linearize", "linearize_forward", "LinearizeForwardPlan", "fused_applies", "alloc_linearization", "forward", "check", "status", "status_str", "launch_info", "lib",
            "linearize_forward_launch_info", "diag_sync_cycles",
            "Linearization", "CxError", "SEQUENCE", "TREE", "DAG", "TREERNN", "TREEFC",
-           "TREELSTM", "TREEGRU", "MVRNN", "DAGRNN", "F32", "BF16", "CELL_IDS", "OK"]
+           "TREELSTM", "TREEGRU", "MVRNN", "DAGRNN", "SIMPLETREEGRU", "F32", "BF16", "CELL_IDS", "OK"]

@@ -51,7 +51,7 @@ inline char *align_up(char *p, size_t a) {
 }
 
 bool weights_ok(int cell, const cx_weights *w) {
-  static const int need[6] = {0, 2, 5, 7, 4, 3};
+  static const int need[7] = {0, 2, 5, 7, 4, 3, 7};
   for (int i = 0; i < need[cell]; i++)
     if (!w->p[i]) return false;
   return true;
@@ -175,7 +175,8 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
   } else if (plan.big) a.pbuf = buf;  // hs, st [n][H] + words [n] (forward_big.cu)
   else switch (m->cell) {
     case CX_TREELSTM: a.cbuf = aux_out ? aux_out : buf; break;
-    case CX_TREEGRU: a.zbuf = buf; a.sbuf = buf + N * H; break;
+    case CX_TREEGRU:
+    case CX_SIMPLETREEGRU: a.zbuf = buf; a.sbuf = buf + N * H; break;
     case CX_DAGRNN: a.pbuf = buf; break;
     case CX_MVRNN: a.Abuf = aux_out ? aux_out : buf; break;
     default: break;
@@ -240,7 +241,7 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
                      float *aux_out, float *root_out, void *workspace, size_t workspace_bytes,
                      void *stream) {
   if (!m || !w || !lin || !lin->header) return CX_E_ARG;
-  if (m->cell < CX_TREERNN || m->cell > CX_DAGRNN) return CX_E_ARG;
+  if (m->cell < CX_TREERNN || m->cell > CX_SIMPLETREEGRU) return CX_E_ARG;
   if (m->dtype != CX_F32 && m->dtype != CX_BF16) return CX_E_ARG;
   if (m->hidden <= 0 || m->vocab <= 0) return CX_E_ARG;
   const int n = lin->n;
@@ -283,7 +284,7 @@ cx_status cx_linearize_forward(const int32_t *children, int32_t n, int32_t max_c
     if (!out->header || !out->perm || !out->inv || !out->children || !out->height ||
         !out->level_begin || !out->level_size || !out->roots || !out->structure)
       return CX_E_ARG;
-    if (m->cell < CX_TREERNN || m->cell > CX_DAGRNN || m->hidden <= 0 || m->vocab <= 0)
+    if (m->cell < CX_TREERNN || m->cell > CX_SIMPLETREEGRU || m->hidden <= 0 || m->vocab <= 0)
       return CX_E_ARG;
     if (!emb || !word_ids || !h_out || !weights_ok(m->cell, w)) return CX_E_ARG;
     cx::FwdPlan plan;

@@ -753,7 +753,7 @@ bool fwd_plan(int cell, int H, int maxc, int n, int path, int num_sms, FwdPlan *
   // the shared-memory-weight kernel below for large batches, where 32 units
   // per CTA minimise the re-gathering of child rows across unit groups.
   const bool rw_ok = (cell == CX_TREELSTM || cell == CX_TREEGRU || cell == CX_TREEFC ||
-                      cell == CX_DAGRNN) && (H == 64 || H == 128 || H == 256 || H == 512);
+                      cell == CX_DAGRNN || cell == CX_SIMPLETREEGRU) && (H == 64 || H == 128 || H == 256 || H == 512);
   if ((path == 0 || path == 3) && cluster_plan(cell, H, maxc, n, 0, plan, Gn, Gu)) return true;
   if ((path == 4 || (path == 0 && n > kRwMaxNodes)) && big_plan(cell, H, maxc, num_sms, plan, Gn, Gu))
     return true;
@@ -797,7 +797,8 @@ size_t fwd_workspace_bytes(int cell, int H, int n, int V) {
   }
   switch (cell) {
     case CX_TREELSTM: b += 4 * N * h; break;            // c (when aux_out == NULL)
-    case CX_TREEGRU: b += 2 * 4 * N * h; break;         // z, s
+    case CX_TREEGRU:
+    case CX_SIMPLETREEGRU: b += 2 * 4 * N * h; break;   // z, s (refactored: m)
     case CX_DAGRNN: b += 4 * N * h; break;              // projections
     case CX_MVRNN: b += 4 * N * h * h; break;           // A (when aux_out == NULL)
     default: break;

@@ -19,6 +19,7 @@
 // sweep that dominated small levels.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "rw_engine.cuh"
@@ -28,12 +29,15 @@ namespace {
 using namespace fwd;
 using namespace rw;
 
+constexpr bool kGruRefactorDefault = false;  // set from the measurement
+
 // ---------------------------------------------------------------------------
 // Cells
 // ---------------------------------------------------------------------------
 template <int H, int MAXC>
 struct RTreeLstm {
   static constexpr int kPhases = 1;
+  static constexpr bool kLeafPost = false;
   using M = TileMetaT<kLeafBlock>;
   __device__ static int leaf_gates(const FwdArgs &a, Gate *g) {
     g[0] = {a.w[0], 0, H, 0}; g[1] = {a.w[0], H, H, 0}; g[2] = {a.w[0], 2 * H, H, 0};
@@ -120,9 +124,15 @@ struct RTreeLstm {
   };
 };
 
-template <int H, int MAXC>
+// TreeGRU (reading Q3) and SimpleTreeGRU (SIMPLE, Q24: h = (1 - z) g at
+// internal nodes, footnote P:1638-1640), ORIGINAL schedule: phase A gathers the
+// children's h and forms z = sigma(U_z h~ + b_z) and s = sum_k sigma(U_r h_k +
+// b_r) * h_k (3 matvecs); a grid barrier; phase B g = tanh(U_h s + b_h) (1
+// matvec) and h; a grid barrier.
+template <int H, int MAXC, bool SIMPLE = false>
 struct RTreeGru {
   static constexpr int kPhases = 2;
+  static constexpr bool kLeafPost = false;
   using M = TileMetaT<kLeafBlock>;
   __device__ static int leaf_gates(const FwdArgs &a, Gate *g) {
     g[0] = {a.w[0], 0, H, 0}; g[1] = {a.w[0], H, H, 0};
@@ -207,7 +217,7 @@ struct RTreeGru {
           size_t o = (size_t)m->own[t] * H + c.unit0 + u;
           float g = tanhf_(s[0] + c.bias[32 + u]);
           float z = __ldcg(a.zbuf + o), ht = __ldcg(a.h_out + o);
-          put_h(a, *m, t, c.unit0 + u, z * ht + (1.f - z) * g);
+          put_h(a, *m, t, c.unit0 + u, SIMPLE ? (1.f - z) * g : z * ht + (1.f - z) * g);
         }
         __syncthreads();
       }
@@ -215,9 +225,127 @@ struct RTreeGru {
   };
 };
 
+// Recursive refactoring (§3.1, evaluated P:1632-1644) of the
+// two GRU cells: the reset-gated contribution m_k = sigma(U_r h_k + b_r) * h_k
+// depends on the child only, so it moves across the recursion backedge into
+// the CHILD's step (A1 of Fig. rec_refactoring), right after its h is
+// complete. A level then runs
+//   phase 0: gather h~ = sum_k h_k and m~ = sum_k m_k (sums formed in the
+//            gather), z = sigma(U_z h~ + b_z), g = tanh(U_h m~ + b_h), h (2 matvecs
+//            on the critical path instead of 3); grid barrier;
+//   phase 1: m = sigma(U_r h + b_r) * h of the level's own nodes (1 matvec);
+//            grid barrier
+// plus one extra phase for the leaves' m after the leaf phase. The barrier
+// count per level is the same as the original schedule (each phase needs a
+// complete vector of the one before); the work on the per-level critical path
+// drops from 4 to 3 matvecs per node. Both schedules are measured.
+template <int H, int MAXC, bool SIMPLE>
+struct RTreeGruR {
+  static constexpr int kPhases = 2;
+  static constexpr bool kLeafPost = true;
+  using M = TileMetaT<kLeafBlock>;
+  // products: phase 0 U_z . h~ (vector 0) and U_h . m~ (vector 1); phase 1 U_r . h
+  struct P0 : PhBase<3, 2, 0, 2, 2> {
+    __device__ static constexpr int g(int p) { return p; }
+    __device__ static constexpr int v(int p) { return p; }
+    __device__ static constexpr int a(int p) { return p; }
+  };
+  struct P1 : PhBase<3, 1, 0, 1, 1> {
+    __device__ static constexpr int g(int p) { return 2; }
+    __device__ static constexpr int v(int p) { return 0; }
+    __device__ static constexpr int a(int p) { return 0; }
+  };
+  __device__ static int leaf_gates(const FwdArgs &a, Gate *g) {
+    g[0] = {a.w[0], 0, H, 0}; g[1] = {a.w[0], H, H, 0};
+    return 2;
+  }
+  __device__ static int level_gates(const FwdArgs &a, Gate *g) {  // U_z, U_h, U_r
+    g[0] = {a.w[1], 0, H, 0}; g[1] = {a.w[3], 0, H, 0}; g[2] = {a.w[2], 0, H, 0};
+    return 3;
+  }
+  __device__ static int biases(const FwdArgs &a, const float **b, int *off) {
+    b[0] = a.w[4]; b[1] = a.w[5]; b[2] = a.w[6]; off[0] = off[1] = off[2] = 0;
+    return 3;
+  }
+  __device__ static int leaf_lo(int first_leaf) { return first_leaf; }
+  using Leaf = typename RTreeGru<H, MAXC, SIMPLE>::Leaf;
+  // m = sigma(U_r h + b_r) * h of the nodes [i0, i0 + cnt) (their h complete)
+  __device__ static void m_phase(const RCtx &c, M *m, const float (*w)[RShape<H>::KC], int i0,
+                                 int cnt, auto tt) {
+    constexpr int T = decltype(tt)::value;
+    const FwdArgs &a = *c.a;
+    gather_rows_c<1, H>(c.X, cnt, [&](int t, int) { return a.h_out + (size_t)m->own[t] * H; });
+    __syncthreads();
+    float s[1];
+    contract<P1, H, T>(c, c.X, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+    const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
+    if (t < cnt) {
+      const int unit = c.unit0 + u;
+      const float h = c.X[(size_t)t * H + unit];
+      a.sbuf[(size_t)m->own[t] * H + unit] = sigmoidf_(s[0] + c.bias[16 + u]) * h;
+    }
+    __syncthreads();
+  }
+  struct LeafPost {
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int pre;
+    __device__ void meta(int i0, int cnt) { load_meta(*c.a, *m, i0, cnt, false, false, false, false); }
+    template <int T>
+    __device__ __forceinline__ void run(int i0, int cnt) {
+      meta(i0, cnt);
+      __syncthreads();
+      m_phase(c, m, w, i0, cnt, std::integral_constant<int, T>{});
+    }
+  };
+  struct Level {
+    RCtx c; M *m; const float (*w)[RShape<H>::KC]; int phase, pre;
+    __device__ void meta(int i0, int cnt) {
+      if (phase == 0) load_meta(*c.a, *m, i0, cnt, true, false, false, c.latch);
+      else load_meta(*c.a, *m, i0, cnt, false, false, false, false);
+    }
+    template <int T>
+    __device__ __forceinline__ void run(int i0, int cnt) {
+      const FwdArgs &a = *c.a;
+      if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
+      if (phase == 1) {
+        m_phase(c, m, w, i0, cnt, std::integral_constant<int, T>{});
+        return;
+      }
+      // X rows per node: h~ then m~, summed over the present children
+      constexpr int q = H / 4;
+      for (int idx = threadIdx.x; idx < cnt * q; idx += blockDim.x) {
+        const int t = idx / q, cq = idx - t * q;
+        float4 hs = make_float4(0.f, 0.f, 0.f, 0.f), ms = hs;
+#pragma unroll
+        for (int k = 0; k < MAXC; k++) {
+          const int ci = m->cin[t][k];
+          if (ci >= 0) {
+            hs = add4(hs, ldcg4(a.h_out + (size_t)ci * H + 4 * cq));
+            ms = add4(ms, ldcg4(a.sbuf + (size_t)ci * H + 4 * cq));
+          }
+        }
+        *reinterpret_cast<float4 *>(c.X + (size_t)(2 * t) * H + 4 * cq) = hs;
+        *reinterpret_cast<float4 *>(c.X + (size_t)(2 * t + 1) * H + 4 * cq) = ms;
+      }
+      __syncthreads();
+      float s[2];
+      contract<P0, H, T>(c, c.X, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
+      const int t = threadIdx.x >> 4, u = threadIdx.x & 15;
+      if (t < cnt) {
+        const int unit = c.unit0 + u;
+        const float z = sigmoidf_(s[0] + c.bias[u]);
+        const float g = tanhf_(s[1] + c.bias[32 + u]);
+        const float ht = c.X[(size_t)(2 * t) * H + unit];
+        put_h(a, *m, t, unit, SIMPLE ? (1.f - z) * g : z * ht + (1.f - z) * g);
+      }
+      __syncthreads();
+    }
+  };
+};
+
 template <int H, int MAXC>
 struct RTreeFc {
   static constexpr int kPhases = 1;
+  static constexpr bool kLeafPost = false;
   using M = TileMetaT<kLeafBlock>;
   __device__ static int leaf_gates(const FwdArgs &, Gate *) { return 0; }
   __device__ static int level_gates(const FwdArgs &a, Gate *g) {
@@ -263,6 +391,7 @@ struct RTreeFc {
 template <int H, int MAXC>
 struct RDagRnn {
   static constexpr int kPhases = 1;
+  static constexpr bool kLeafPost = false;
   using M = TileMetaT<kLeafBlock>;
   // gates {W_x, U} resident through leaves and levels (input projections are
   // fused into each level instead of a separate all-node GEMM)
@@ -395,12 +524,21 @@ __global__ void __launch_bounds__(kRThreads, 1) rw_kernel(FwdArgs a) {
     int ng = C::level_gates(a, gs);
     load_wregs<Cfg::NG, KC>(w, gs, ng, ctx.unit0 + u, k0);
   }
+  if constexpr (C::kLeafPost) {  // refactored GRU: the leaves' m once their h is complete
+    grid_sync(a.bar, gridDim.x, epoch);
+    const int lo0 = C::leaf_lo(first_leaf);
+    int lo, hi;
+    chunk_of(n - lo0, a.Gn, gn, lo, hi);
+    typename C::LeafPost f{ctx, &meta, w, -1};
+    for_tiles<Cfg::TMAX>(lo0 + lo, lo0 + hi, f);
+  }
   // ---- internal batches: one grid barrier per level (and phase) -------------
   for (int l = 1; l < L; l++) {
     const int base = __ldg(a.lbeg + l), M = __ldg(a.lsize + l);
     int lo, hi;
     chunk_of(M, a.Gn, gn, lo, hi);
     for (int ph = 0; ph < C::kPhases; ph++) {
+      if (C::kLeafPost && ph == 1 && l == L - 1) break;  // the top level's m feeds nobody
       const int slot = 3 + 2 * ((l - 1) * C::kPhases + ph);
       trace_mark(a, slot);
       grid_arrive(a.bar, epoch);
@@ -444,14 +582,20 @@ bool rplan(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
 }
 
 template <int CELL, int H>
-bool rplan_maxc(int maxc, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
+bool rplan_maxc(int maxc, int num_sms, FwdPlan *p, int *Gn, int *Gu, int variant = 0) {
   if constexpr (CELL == CX_TREEFC) {
     return rplan<CELL, H, 2, RTreeFc<H, 2>>(num_sms, p, Gn, Gu);
   } else {
     auto pick = [&](auto mc) {
       constexpr int MC = decltype(mc)::value;
       if constexpr (CELL == CX_TREELSTM) return rplan<CELL, H, MC, RTreeLstm<H, MC>>(num_sms, p, Gn, Gu);
-      if constexpr (CELL == CX_TREEGRU) return rplan<CELL, H, MC, RTreeGru<H, MC>>(num_sms, p, Gn, Gu);
+      if constexpr (CELL == CX_TREEGRU) {
+        // GRU cells share one configuration; the variant picks the schedule
+        if (variant == 0) return rplan<CELL, H, MC, RTreeGru<H, MC, false>>(num_sms, p, Gn, Gu);
+        if (variant == 1) return rplan<CELL, H, MC, RTreeGru<H, MC, true>>(num_sms, p, Gn, Gu);
+        if (variant == 2) return rplan<CELL, H, MC, RTreeGruR<H, MC, false>>(num_sms, p, Gn, Gu);
+        return rplan<CELL, H, MC, RTreeGruR<H, MC, true>>(num_sms, p, Gn, Gu);
+      }
       if constexpr (CELL == CX_DAGRNN) return rplan<CELL, H, MC, RDagRnn<H, MC>>(num_sms, p, Gn, Gu);
       return false;
     };
@@ -462,11 +606,22 @@ bool rplan_maxc(int maxc, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   }
 }
 
+// GRU schedule: original (2 phases: 3 + 1 matvecs) or recursive refactoring
+// (2 phases: 2 + 1 matvecs, plus the leaves' m) -- CX_GRU_REFACTOR=0/1
+// overrides the default for measurement.
+inline int gru_variant(bool simple) {
+  const char *e = std::getenv("CX_GRU_REFACTOR");
+  const bool refac = e ? e[0] == '1' : kGruRefactorDefault;
+  return (simple ? 1 : 0) + (refac ? 2 : 0);
+}
+
 template <int H>
 bool rplan_cell(int cell, int maxc, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   switch (cell) {
     case CX_TREELSTM: return rplan_maxc<CX_TREELSTM, H>(maxc, num_sms, p, Gn, Gu);
-    case CX_TREEGRU: return rplan_maxc<CX_TREEGRU, H>(maxc, num_sms, p, Gn, Gu);
+    // TreeGRU / SimpleTreeGRU x original / refactored schedule (gru_variant)
+    case CX_TREEGRU: return rplan_maxc<CX_TREEGRU, H>(maxc, num_sms, p, Gn, Gu, gru_variant(false));
+    case CX_SIMPLETREEGRU: return rplan_maxc<CX_TREEGRU, H>(maxc, num_sms, p, Gn, Gu, gru_variant(true));
     case CX_TREEFC: return rplan_maxc<CX_TREEFC, H>(maxc, num_sms, p, Gn, Gu);
     case CX_DAGRNN: return rplan_maxc<CX_DAGRNN, H>(maxc, num_sms, p, Gn, Gu);
   }

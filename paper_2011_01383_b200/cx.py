@@ -18,14 +18,16 @@ from . import _build
 
 # --- enums mirrored from include/cx.h --------------------------------------
 SEQUENCE, TREE, DAG = 0, 1, 2
-TREERNN, TREEFC, TREELSTM, TREEGRU, MVRNN, DAGRNN = range(6)
+TREERNN, TREEFC, TREELSTM, TREEGRU, MVRNN, DAGRNN, SIMPLETREEGRU = range(7)
 F32, BF16 = 0, 1
 OK, E_ARG, E_CHILD_RANGE, E_CHILD_LAYOUT, E_KIND, E_CYCLE, E_ARITY, E_WORD_RANGE, \
     E_UNSUPPORTED, E_WORKSPACE, E_CUDA = range(11)
 
 CELL_IDS = {"treernn": TREERNN, "treefc": TREEFC, "treelstm": TREELSTM,
-            "treegru": TREEGRU, "mvrnn": MVRNN, "dagrnn": DAGRNN}
-N_WEIGHTS = {TREERNN: 0, TREEFC: 2, TREELSTM: 5, TREEGRU: 7, MVRNN: 4, DAGRNN: 3}
+            "treegru": TREEGRU, "mvrnn": MVRNN, "dagrnn": DAGRNN,
+            "simpletreegru": SIMPLETREEGRU}
+N_WEIGHTS = {TREERNN: 0, TREEFC: 2, TREELSTM: 5, TREEGRU: 7, MVRNN: 4, DAGRNN: 3,
+             SIMPLETREEGRU: 7}
 HEADER_FIELDS = ("status", "bad_node", "num_nodes", "num_levels", "num_leaves", "first_leaf",
                  "max_level_size", "num_roots")
 
