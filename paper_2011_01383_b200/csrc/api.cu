@@ -114,7 +114,8 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
     std::lock_guard<std::mutex> lk(g_mu);
     int sms = num_sms_current();
     if (sms <= 0) return CX_E_CUDA;
-    const bool ok = fused ? cx::fused_plan(m->cell, m->hidden, lin->max_children, n, &plan, &Gn, &Gu)
+    const bool ok = fused ? (cx::fused_plan(m->cell, m->hidden, lin->max_children, n, &plan, &Gn, &Gu) ||
+                             cx::single_plan(m->cell, m->hidden, lin->max_children, n, &plan, &Gn, &Gu))
                     : m->dtype == CX_BF16
                         ? cx::tc_plan(m->cell, m->hidden, lin->max_children, sms, &plan, &Gn, &Gu)
                         : cx::fwd_plan(m->cell, m->hidden, lin->max_children, n, forward_path(),
@@ -292,7 +293,8 @@ cx_status cx_linearize_forward(const int32_t *children, int32_t n, int32_t max_c
     bool ok;
     {
       std::lock_guard<std::mutex> lk(g_mu);
-      ok = cx::fused_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu);
+      ok = cx::fused_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu) ||
+           cx::single_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu);
     }
     if (ok) {
       cx::LinArgs la;
@@ -342,7 +344,9 @@ int32_t cx_debug_fused_applies(const cx_model *m, int32_t n, int32_t max_childre
   cx::FwdPlan plan;
   int Gn, Gu;
   std::lock_guard<std::mutex> lk(g_mu);
-  return cx::fused_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu) ? 1 : 0;
+  return cx::fused_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu) ||
+                 cx::single_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu)
+             ? 1 : 0;
 }
 
 // Debug only: an empty kernel launch (measures launch overhead).
@@ -379,7 +383,8 @@ cx_status cx_linearize_forward_launch_info(const cx_model *m, int32_t n, int32_t
   const char *env = std::getenv("CX_FUSED");
   bool f = !(env && env[0] == '0') && m->dtype == CX_F32 && n > 0 &&
            (forward_path() == 0 || forward_path() == 3) &&
-           cx::fused_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu);
+           (cx::fused_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu) ||
+            cx::single_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu));
   if (!f) {
     const int sms = num_sms_current();
     if (sms <= 0) return CX_E_CUDA;

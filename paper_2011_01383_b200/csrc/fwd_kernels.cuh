@@ -102,5 +102,8 @@ bool pdl_enabled();
 // Fused linearize + forward (forward_cluster.cu): fp32 cluster
 // path of TreeLSTM / DAG-RNN for small batches. False when not applicable.
 bool fused_plan(int cell, int H, int maxc, int n, FwdPlan *plan, int *Gn, int *Gu);
+// Fused single-CTA-per-structure-group path (forward_single.cu, SURVEY §8(f)
+// f2): TreeRNN (recursion unrolled, CX_UNROLL) and tiny TreeFC batches.
+bool single_plan(int cell, int H, int maxc, int n, FwdPlan *plan, int *Gn, int *Gu);
 
 }  // namespace cx
