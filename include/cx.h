@@ -227,6 +227,7 @@ cx_status cx_diag_sync_cycles(int32_t kind, int32_t levels, unsigned long long *
 cx_status cx_debug_set_trace(unsigned long long *buf, int32_t slots);
 cx_status cx_debug_set_lin_trace(unsigned long long *buf);
 int32_t cx_debug_fused_applies(const cx_model *model, int32_t n, int32_t max_children);
+int32_t cx_debug_forward_family(const cx_model *model, int32_t n, int32_t max_children);
 cx_status cx_debug_empty(int32_t ctas, int32_t threads, int32_t coop, unsigned long long *t,
                          void *stream);
 

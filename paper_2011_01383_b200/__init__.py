@@ -11,12 +11,12 @@ include/cx.h. See DESIGN.md.
 from .cx import (BF16, DAG, DAGRNN, F32, MVRNN, SEQUENCE, TREE, TREEFC, TREEGRU, TREELSTM,
                  TREERNN, SIMPLETREEGRU, CELL_IDS, CxError, Linearization, alloc_linearization, check, forward, launch_info, lib,
                  fused_applies, linearize, linearize_forward, LinearizeForwardPlan, status, status_str,
-                 linearize_forward_launch_info, diag_sync_cycles)
+                 linearize_forward_launch_info, diag_sync_cycles, forward_family)
 from . import cx as _cx
 
 OK = _cx.OK
 
 __all__ = ["linearize", "linearize_forward", "LinearizeForwardPlan", "fused_applies", "alloc_linearization", "forward", "check", "status", "status_str", "launch_info", "lib",
-           "linearize_forward_launch_info", "diag_sync_cycles",
+           "linearize_forward_launch_info", "diag_sync_cycles", "forward_family",
            "Linearization", "CxError", "SEQUENCE", "TREE", "DAG", "TREERNN", "TREEFC",
            "TREELSTM", "TREEGRU", "MVRNN", "DAGRNN", "SIMPLETREEGRU", "F32", "BF16", "CELL_IDS", "OK"]

@@ -249,6 +249,9 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
   if (n < 0) return CX_E_ARG;
   if (n > 0 && (!emb || !word_ids || !h_out || !weights_ok(m->cell, w))) return CX_E_ARG;
   if (!workspace || workspace_bytes < cx_forward_workspace_bytes(m, n)) return CX_E_WORKSPACE;
+  // the bf16 TreeLSTM kernel stores each node's h in its ONE parent's child
+  // slot (forward_tc.cu): a DAG linearization (shared children) is refused
+  if (m->dtype == CX_BF16 && m->cell == CX_TREELSTM && lin->kind == CX_DAG) return CX_E_UNSUPPORTED;
   if (n == 0) return CX_OK;
   return forward_impl(m, w, emb, word_ids, lin, h_out, aux_out, root_out, workspace, nullptr, stream);
 }
@@ -347,6 +350,23 @@ int32_t cx_debug_fused_applies(const cx_model *m, int32_t n, int32_t max_childre
   return cx::fused_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu) ||
                  cx::single_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu)
              ? 1 : 0;
+}
+
+// Debug / tests: the kernel family cx_forward runs for this model and batch
+// shape (FwdPlan::family: 1 smem, 2 register weights, 3 cluster, 4 large
+// batch, 5 MV-RNN, 6 bf16 tensor cores), honouring CX_FORWARD_PATH; 0 if none.
+int32_t cx_debug_forward_family(const cx_model *m, int32_t n, int32_t max_children) {
+  if (!m || n < 1 || max_children < 1) return 0;
+  cx::FwdPlan plan;
+  int Gn, Gu;
+  std::lock_guard<std::mutex> lk(g_mu);
+  const int sms = num_sms_current();
+  if (sms <= 0) return 0;
+  const bool ok = m->dtype == CX_BF16
+                      ? cx::tc_plan(m->cell, m->hidden, max_children, sms, &plan, &Gn, &Gu)
+                      : cx::fwd_plan(m->cell, m->hidden, max_children, n, forward_path(), sms,
+                                     &plan, &Gn, &Gu);
+  return ok ? plan.family : 0;
 }
 
 // Debug only: an empty kernel launch (measures launch overhead).

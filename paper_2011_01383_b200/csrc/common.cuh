@@ -13,6 +13,15 @@ namespace cx {
 
 constexpr uint64_t kNoError = ~0ull;
 
+// Host: per-device slot for the lazily filled kernel-attribute caches
+// (cudaFuncSetAttribute applies per device context). -1 when unavailable.
+constexpr int kMaxDevices = 64;
+inline int device_slot() {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return -1;
+  return dev;
+}
+
 // 128-byte aligned synchronisation words kept in the caller's workspace.
 struct GridBar {
   unsigned int count;   // arrivals, monotonic within one launch

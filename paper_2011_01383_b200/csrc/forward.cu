@@ -729,11 +729,13 @@ static bool plan_for(int H, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   size_t smem = Lay::bytes(H);
   if (smem > 227 * 1024) return false;
   auto k = fwd_kernel<CELL, MAXC, C>;
-  static size_t smem_set = 0;  // callers serialise plans (api.cu mutex)
-  if (smem > smem_set) {
+  static size_t smem_set[kMaxDevices];  // per device; callers serialise plans (api.cu mutex)
+  const int dev = device_slot();
+  if (dev < 0) return false;
+  if (smem > smem_set[dev]) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return false;
-    smem_set = smem;
+    smem_set[dev] = smem;
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaGetLastError();
   }
@@ -743,6 +745,7 @@ static bool plan_for(int H, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   p->threads = kFwdThreads;
   p->smem = smem;
   p->kernel = (const void *)k;
+  p->family = 1;
   return true;
 }
 

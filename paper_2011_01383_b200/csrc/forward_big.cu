@@ -443,15 +443,17 @@ bool bplan_one(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   constexpr size_t smem = BLayout<CELL, H, MAXC>::bytes;
   if (smem > 227 * 1024) return false;
   auto k = big_kernel<CELL, H, MAXC>;
-  static bool set = false;
-  if (!set) {
+  static bool set_dev[kMaxDevices];  // per device (attributes are per context)
+  const int dev = device_slot();
+  if (dev < 0) return false;
+  if (!set_dev[dev]) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
       cudaGetLastError();
       return false;
     }
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaGetLastError();
-    set = true;
+    set_dev[dev] = true;
   }
   *Gu = H / kUG;
   *Gn = num_sms / *Gu;
@@ -459,6 +461,7 @@ bool bplan_one(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   p->threads = kFwdThreads;
   p->smem = smem;
   p->kernel = (const void *)k;
+  p->family = 4;
   p->cluster = 1;
   p->big = true;
   return true;

@@ -852,6 +852,7 @@ bool cplan_one(int n, int maxc, int L_bound, int num_roots_hint, FwdPlan *p, int
   p->kernel = (const void *)k;
   p->cluster = CSZ;
   p->fused = FUSED;
+  p->family = 3;
   return true;
 }
 

@@ -277,11 +277,13 @@ template <int H>
 bool plan_h(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   auto k = mvrnn_kernel<H>;
   size_t smem = MvLayout<H>::bytes;
-  static bool set = false;
-  if (!set) {
+  static bool set_dev[kMaxDevices];  // per device (attributes are per context)
+  const int dev = device_slot();
+  if (dev < 0) return false;
+  if (!set_dev[dev]) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return false;
-    set = true;
+    set_dev[dev] = true;
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaGetLastError();
   }
@@ -291,6 +293,7 @@ bool plan_h(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   p->threads = kT;
   p->smem = smem;
   p->kernel = (const void *)k;
+  p->family = 5;
   return true;
 }
 

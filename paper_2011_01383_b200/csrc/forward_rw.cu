@@ -563,11 +563,13 @@ bool rplan(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   constexpr size_t smem = RLayout<CELL, H, MAXC>::bytes;
   if (smem > 227 * 1024) return false;
   auto k = rw_kernel<CELL, H, MAXC, C>;
-  static bool set = false;
-  if (!set) {
+  static bool set_dev[kMaxDevices];  // per device (attributes are per context)
+  const int dev = device_slot();
+  if (dev < 0) return false;
+  if (!set_dev[dev]) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return false;
-    set = true;
+    set_dev[dev] = true;
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaGetLastError();
   }
@@ -578,6 +580,7 @@ bool rplan(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   p->threads = kRThreads;
   p->smem = smem;
   p->kernel = (const void *)k;
+  p->family = 2;
   return true;
 }
 

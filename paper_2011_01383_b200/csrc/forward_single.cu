@@ -219,6 +219,7 @@ bool sc_plan_one(int n, int maxc, FwdPlan *p, int *Gn, int *Gu) {
   p->kernel = (const void *)k;
   p->cluster = 1;
   p->fused = true;
+  p->family = 7;
   return true;
 }
 

@@ -921,16 +921,21 @@ bool tc_plan_one(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   using C = TcCfg<CELL, H, MAXC>;
   static_assert(C::S >= 2, "at least two pipeline stages");
   auto k = tc_kernel<CELL, H, MAXC>;
-  static bool set = false;
-  if (!set) {
+  // per-device caches (attributes and occupancy are per device context)
+  static bool set[kMaxDevices];
+  static int max_clusters_dev[kMaxDevices];
+  const int dev = device_slot();
+  if (dev < 0) return false;
+  if (!set[dev]) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::dyn_bytes) !=
         cudaSuccess) {
       cudaGetLastError();
       return false;
     }
-    set = true;
+    set[dev] = true;
+    max_clusters_dev[dev] = -1;
   }
-  static int max_clusters = -1;  // co-resident clusters (the grid barrier needs all)
+  int &max_clusters = max_clusters_dev[dev];  // co-resident clusters (the grid barrier needs all)
   if (max_clusters < 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C::CL * 64);
@@ -958,6 +963,7 @@ bool tc_plan_one(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   p->smem = C::dyn_bytes;
   p->kernel = (const void *)k;
   p->cluster = C::CL;
+  p->family = 6;
   p->big = false;
   p->tc = true;
   return true;

@@ -185,7 +185,8 @@ __device__ __forceinline__ void fused_exit(const FwdArgs &a, unsigned long long 
       if (key != kNoError) {
         a.hdr->status = (int)(key >> 32);
         a.hdr->bad_node = (int)(key & 0xffffffffu);
-        a.hdr->num_levels = 0;
+        // (num_levels stays as the linearization wrote it: the header equals
+        // the two separate calls', cx.h)
       }
       a.bar->count = 0;
       a.bar->exit = 0;

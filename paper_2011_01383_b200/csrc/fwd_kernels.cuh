@@ -79,6 +79,11 @@ struct FwdPlan {
   bool big = false; // large-batch pipelined kernel: workspace holds hs, st [n][H] + words [n]
   bool tc = false;  // bf16 tensor-core kernel (forward_tc.cu): launched by tc_launch
   bool fused = false;  // the kernel also linearizes (FwdArgs::lin), cx_linearize_forward
+  // kernel family (reporting / tests): 1 smem weights (forward.cu), 2 register
+  // weights (forward_rw.cu), 3 cluster (forward_cluster.cu), 4 large-batch
+  // (forward_big.cu), 5 MV-RNN, 6 bf16 tensor cores (forward_tc.cu), 7 fused
+  // single-CTA (forward_single.cu)
+  int family = 0;
 };
 
 // Returns false (CX_E_UNSUPPORTED) when no instantiation covers the model.

@@ -36,6 +36,7 @@ constexpr int kLinThreads = 1024;   // multi-CTA path
 constexpr int kLinSingleThreads = 512;
 constexpr int kSegMin = 256;
 constexpr int kLinTabLevels = 256;  // levels handled by the block-chunked sort (lin_kernel)
+constexpr int kLinWalkLevels = 64;  // P8: trees up to this deep walk to their root, deeper ones pointer-jump
 #ifndef CX_JAC_SLEEP
 #define CX_JAC_SLEEP 0  // ns between polls of the async DAG height pass (measured: 0 < 32 < 200)
 #endif
@@ -77,8 +78,8 @@ __device__ int block_exclusive_scan(int v, int &total, int *s_tmp) {
 //       child counts
 //   P3  heights. Trees/sequences: every leaf walks up its parent chain with
 //       global atomics (atomicMax of the height, atomicSub of the pending
-//       child count; only the last arriving child continues): O(n) work and no
-//       barrier per level. DAGs: Jacobi rounds (round r finalises exactly the
+//       child count; only the last arriving child continues): O(n) work for
+//       any shape and no barrier per level. DAGs: Jacobi rounds (round r finalises exactly the
 //       nodes of height r), one barrier each.
 //   P4-P6 stable counting sort by height, block-chunked: CTA b owns the ids
 //       [b C, (b+1) C); it counts its ids per level in shared memory (warp
@@ -88,8 +89,9 @@ __device__ int block_exclusive_scan(int v, int &total, int *s_tmp) {
 //       Very deep structures (L + 1 > kLinTabLevels) use the per-segment
 //       variant below instead.
 //   P7  remap children to new ids
-//   P8  structures: trees walk up to their root; DAGs propagate the smallest
-//       root index top-down, one level per round.
+//   P8  structures: trees walk up to their root (pointer jumping when deeper
+//       than kLinWalkLevels); DAGs propagate the smallest root index top-down,
+//       one level per round.
 __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
   griddep_launch_dependents();
   lin_mark(a, 7);
@@ -119,6 +121,7 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
   if (tid == 0) {
     a.hdr->err_key = kNoError;
     a.misc[0] = a.misc[1] = a.misc[2] = a.misc[3] = a.misc[4] = a.misc[5] = a.misc[6] = 0;
+    a.misc[7] = a.misc[8] = 0;
   }
   if (threadIdx.x == 0) s_tmp[32] = 0;
   grid_sync(a.bar, G, epoch);
@@ -162,62 +165,40 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
   int L = 0;
   if (!failed && n > 0) {
     if (tree_like) {
-      // every leaf walks to its root with dependent parent loads only and posts
-      // height[ancestor] = max(., distance) fire-and-forget: height = longest
-      // distance to a leaf below. Brent's check stops a walk that entered a
-      // cycle (invalid input; handled below).
+      // every leaf walks up its parent chain: at each parent it raises the
+      // height (atomicMax) and decrements the pending-child count; only the
+      // last arriving child continues, with the parent's final height (every
+      // child's atomicMax precedes its decrement) -- O(n) work for any shape.
+      // A node on or above a cycle never reaches pending 0, so no walk loops;
+      // those nodes are the CX_E_CYCLE candidates (lowest id reported).
       int hmax = 0;
-      bool looped = false;
       for (int v = tid; v < n; v += nthr) {
         if (ch[v] != -1) continue;  // walks start at leaves
-        int cur = v, d = 0, tort = v, power = 1, lam = 0;
+        int cur = v, d = 0;
         while (true) {
           const int p = __ldcg(&parent[cur]);
           if (p < 0) break;
-          d++;
-          atomicMax(&hgt[p], d);  // result unused: a RED.MAX
+          atomicMax(&hgt[p], d + 1);
+          __threadfence();
+          if (atomicSub(&pending[p], 1) != 1) break;
+          __threadfence();
+          d = atomicAdd(&hgt[p], 0);
           cur = p;
-          if (cur == tort) {
-            looped = true;
-            break;
-          }
-          if (++lam == power) {
-            tort = cur;
-            power <<= 1;
-            lam = 0;
-          }
         }
         hmax = max(hmax, d);
       }
       for (int o = 16; o; o >>= 1) hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
       if (lane == 0) atomicMax(&a.misc[4], hmax);
-      if (__syncthreads_or(looped) && threadIdx.x == 0) atomicAdd(&a.misc[3], 1);
       grid_sync(a.bar, G, epoch);
-      // a node no walk reached (a cycle without leaves below) also means a cycle
-      bool unreached = false;
-      for (int v = tid; v < n; v += nthr) unreached = unreached || __ldcg(&hgt[v]) < 0;
-      if (__syncthreads_or(unreached) && threadIdx.x == 0) atomicAdd(&a.misc[3], 1);
-      grid_sync(a.bar, G, epoch);
-      if (__ldcg(&a.misc[3]) != 0) {
-        // error path: peel the acyclic part from the leaves with pending child
-        // counts (the last arriving child continues); what is left are the
-        // cycle nodes, the lowest of which is reported
-        for (int v = tid; v < n; v += nthr) {
-          if (ch[v] != -1) continue;
-          int cur = v;
-          while (true) {
-            const int p = __ldcg(&parent[cur]);
-            if (p < 0) break;
-            __threadfence();
-            if (atomicSub(&pending[p], 1) != 1) break;
-            cur = p;
-          }
+      bool cyc = false;
+      for (int v = tid; v < n; v += nthr)
+        if (__ldcg(&pending[v]) > 0) {
+          latch_error(a.hdr, CX_E_CYCLE, v);
+          cyc = true;
         }
-        grid_sync(a.bar, G, epoch);
-        for (int v = tid; v < n; v += nthr)
-          if (__ldcg(&pending[v]) > 0) latch_error(a.hdr, CX_E_CYCLE, v);
-        failed = true;
-      }
+      if (__syncthreads_or(cyc) && threadIdx.x == 0) atomicAdd(&a.misc[3], 1);
+      grid_sync(a.bar, G, epoch);
+      if (__ldcg(&a.misc[3]) != 0) failed = true;
       L = __ldcg(&a.misc[4]) + 1;
     } else {
       // finished-node counts: misc[3] = leaves; round r adds into misc[r % 3],
@@ -601,7 +582,7 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
     }
     lin_mark(a, 14);
     // ---- P8 (a6): structures ------------------------------------------------------
-    if (tree_like) {  // walk up to the root; roots already hold their index
+    if (tree_like && L <= kLinWalkLevels) {  // walk up to the root (<= L - 1 steps)
       for (int i = tid; i < n; i += nthr) {
         int v = __ldcg(&a.perm[i]);
         int p = __ldcg(&parent[v]);
@@ -611,6 +592,37 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
           p = __ldcg(&parent[v]);
         }
         a.sid[i] = __ldcg(&a.sid[__ldcg(&a.inv[v])]);
+      }
+    } else if (tree_like) {
+      // deep structures: pointer jumping on anc[] (the input-id height array,
+      // free after the sort): anc[v] <- anc[anc[v]] until no node changes,
+      // O(n log depth) work and log depth barriers instead of O(n depth)
+      int *anc = hgt;
+      for (int v = tid; v < n; v += nthr) {
+        const int p = __ldcg(&parent[v]);
+        anc[v] = p < 0 ? v : p;
+      }
+      for (int round = 0;; round++) {
+        grid_sync(a.bar, G, epoch);
+        bool changed = false;
+        for (int v = tid; v < n; v += nthr) {
+          const int x = __ldcg(&anc[v]), y = __ldcg(&anc[x]);
+          if (y != x) {
+            anc[v] = y;
+            changed = true;
+          }
+        }
+        if (__syncthreads_or(changed) && threadIdx.x == 0) atomicAdd(&a.misc[7 + (round & 1)], 1);
+        grid_sync(a.bar, G, epoch);
+        const bool any = __ldcg(&a.misc[7 + (round & 1)]) != 0;
+        grid_sync(a.bar, G, epoch);  // everyone has read the flag before it is cleared
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.misc[7 + (round & 1)] = 0;
+        if (!any) break;
+      }
+      for (int i = tid; i < n; i += nthr) {
+        const int v = __ldcg(&a.perm[i]);
+        if (__ldcg(&parent[v]) < 0) continue;
+        a.sid[i] = __ldcg(&a.sid[__ldcg(&a.inv[__ldcg(&anc[v])])]);
       }
     } else {  // smallest root index reaching the node, propagated top-down
       // level ranges cached in shared memory (free after the sort): a round is
@@ -724,14 +736,16 @@ bool lin_use_single(int n, int maxc) {
 }
 
 cudaError_t launch_linearize(const LinArgs &a, int num_sms, cudaStream_t stream) {
-  static bool attr_done = false;  // idempotent attribute set (benign race)
-  if (!attr_done) {
+  static bool attr_done[kMaxDevices];  // per device; idempotent (benign race)
+  const int dev = device_slot();
+  if (dev < 0) return cudaErrorInvalidDevice;
+  if (!attr_done[dev]) {
     cudaFuncSetAttribute(lin_single_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kLinSmemMax);
     cudaFuncSetAttribute(lin_single_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(lin_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLinMultiSmem);
-    attr_done = true;
+    attr_done[dev] = true;
   }
   if (lin_use_single(a.n, a.maxc)) {
     size_t smem = lin_single_smem_bytes(a.n, a.maxc);

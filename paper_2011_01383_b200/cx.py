@@ -108,19 +108,28 @@ def _stream(stream):
 
 
 class _WorkspaceCache:
-    """Zero-filled workspaces, grown on demand, one per (device, role). The
-    kernels leave their synchronisation words zero, so reuse needs no memset."""
+    """Zero-filled workspaces, grown on demand, one per (device, stream, role).
+    The kernels leave their synchronisation words zero, so reuse needs no
+    memset. Keyed by stream too: two streams never share grid-barrier words.
+    A grown buffer never frees its predecessor: CUDA graphs captured earlier
+    may still point at it (they stay valid for the life of the process).
+    Pass an explicit `workspace=` to control the memory instead."""
 
     def __init__(self):
         self._bufs = {}
+        self._retired = []
         self._lock = threading.Lock()
 
-    def get(self, device, role, nbytes):
-        key = (str(device), role)
+    def get(self, device, role, nbytes, stream=None):
+        dev = torch.device(device)
+        st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+        key = (str(dev), int(st or 0), role)
         with self._lock:
             buf = self._bufs.get(key)
             if buf is None or buf.numel() < nbytes:
-                buf = torch.zeros(max(nbytes, 1 << 12), dtype=torch.uint8, device=device)
+                if buf is not None:
+                    self._retired.append(buf)
+                buf = torch.zeros(max(nbytes, 1 << 12), dtype=torch.uint8, device=dev)
                 self._bufs[key] = buf
             return buf
 
@@ -186,7 +195,7 @@ def linearize(children: torch.Tensor, kind: int, stream=None, workspace=None,
     out.kind = kind
     L = lib()
     need = L.cx_linearize_workspace_bytes(n, maxc)
-    ws = workspace if workspace is not None else _ws.get(children.device, "lin", need)
+    ws = workspace if workspace is not None else _ws.get(children.device, "lin", need, None if stream is None else stream.cuda_stream)
     st = L.cx_linearize(_ptr(children), n, maxc, kind, _ptr(ws), ws.numel(), ctypes.byref(out.c),
                         _stream(stream))
     if st != OK:
@@ -285,6 +294,19 @@ def diag_sync_cycles(kind: int, levels: int, device=None) -> int:
     return int(out[0].item())
 
 
+FAMILIES = {1: "smem", 2: "rw", 3: "cluster", 4: "big", 5: "mvrnn", 6: "tc"}
+
+
+def forward_family(cell, hidden, n, max_children, vocab=1, dtype=F32):
+    """Name of the kernel family cx_forward runs for this shape (honours
+    CX_FORWARD_PATH), or None."""
+    L = lib()
+    L.cx_debug_forward_family.argtypes = [ctypes.POINTER(_Model), ctypes.c_int32, ctypes.c_int32]
+    L.cx_debug_forward_family.restype = ctypes.c_int32
+    m = _model(cell, hidden, vocab, dtype)
+    return FAMILIES.get(L.cx_debug_forward_family(ctypes.byref(m), n, max_children))
+
+
 def fused_applies(cell, hidden, n, max_children, vocab=1, dtype=F32) -> bool:
     """Whether cx_linearize_forward runs as ONE launch for this shape (reporting)."""
     L = lib()
@@ -317,7 +339,7 @@ def linearize_forward(children: torch.Tensor, kind: int, cell: int, hidden: int,
     m = _model(cell, hidden, emb.shape[0], dtype)
     L = lib()
     need = L.cx_linearize_forward_workspace_bytes(ctypes.byref(m), n, maxc)
-    ws = workspace if workspace is not None else _ws.get(dev, "linfwd", need)
+    ws = workspace if workspace is not None else _ws.get(dev, "linfwd", need, None if stream is None else stream.cuda_stream)
     st = L.cx_linearize_forward(_ptr(children), n, maxc, kind, ctypes.byref(m), ctypes.byref(w),
                                 _ptr(emb), _ptr(word_ids), ctypes.byref(out.c), _ptr(h_out),
                                 _ptr(aux_out), _ptr(root_out), _ptr(ws), ws.numel(),
@@ -379,7 +401,7 @@ def forward(cell: int, hidden: int, weights, emb: torch.Tensor, word_ids: torch.
     m = _model(cell, hidden, vocab, dtype)
     L = lib()
     need = L.cx_forward_workspace_bytes(ctypes.byref(m), n)
-    ws = workspace if workspace is not None else _ws.get(dev, "fwd", need)
+    ws = workspace if workspace is not None else _ws.get(dev, "fwd", need, None if stream is None else stream.cuda_stream)
     st = L.cx_forward(ctypes.byref(m), ctypes.byref(w), _ptr(emb), _ptr(word_ids),
                       ctypes.byref(lin.c), _ptr(h_out), _ptr(aux_out), _ptr(root_out), _ptr(ws),
                       ws.numel(), _stream(stream))

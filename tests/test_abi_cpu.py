@@ -25,7 +25,7 @@ def declared_functions():
 
 def test_exports_every_declared_symbol(cxmod):
     names = declared_functions()
-    assert len(names) == 15
+    assert len(names) == 16
     L = cxmod.lib()
     for name in names:
         assert hasattr(L, name), name

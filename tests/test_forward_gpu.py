@@ -33,13 +33,15 @@ def _parity(cell, hidden, vocab, children, kind, seed=0, want_aux=False, all_wor
             check_roots=True):
     import os
     import paper_2011_01383_b200 as cx
-    if os.environ.get("CX_FORWARD_PATH"):
-        # a forced kernel family may not instantiate this (cell, H): skip, the
+    forced = os.environ.get("CX_FORWARD_PATH")
+    if forced:
+        # the forced family must be the one that runs (fwd_plan falls back to
+        # another family for shapes the forced one does not instantiate): skip
+        # such cases instead of testing a different kernel under this ID; the
         # automatic path is covered by the "auto" parameter
-        try:
-            cx.launch_info(cell, hidden)
-        except cx.CxError:
-            pytest.skip("no instantiation in the forced kernel family")
+        fam = cx.forward_family(cell, hidden, children.shape[1], children.shape[0], vocab)
+        if fam != forced:
+            pytest.skip(f"forced {forced} does not instantiate this shape (runs {fam})")
     words = synth.word_ids(children, vocab, seed, all_nodes=(cell == T.DAGRNN))
     emb = synth.embedding(vocab, hidden, seed)
     ws_np, ws_dev = weights_dev(cell, hidden, vocab)
@@ -120,6 +122,8 @@ def test_batch4096_sampled(cx, name, fpath, monkeypatch):
         monkeypatch.setenv("CX_FORWARD_PATH", fpath)
     w = synth.workload(name)
     ch, cell, H, V = w["children"], w["cell"], w["hidden"], w["vocab"]
+    assert cx.forward_family(cell, H, ch.shape[1], ch.shape[0], V) == ("big" if fpath == "auto"
+                                                                       else fpath)
     words, emb = w["words"], synth.embedding(V, H, w["seed"])
     ws_np, ws_dev = weights_dev(cell, H, V)
     lin = cx.linearize(dev_i32(ch), w["kind"])
@@ -199,3 +203,16 @@ def test_all_leaves_and_single_node(cx):
         Hc = 64
         ch = np.full((2, 5), -1, np.int32)  # five single-node trees
         _parity(cell, Hc, V, ch, T.TREE if cell != T.DAGRNN else T.DAG, seed=1, want_aux=True)
+
+
+@pytest.mark.parametrize("name,family", [("cfg1_treernn", "smem"), ("cfg2_treelstm_b10", "cluster"),
+                                         ("cfg3_treegru_b10", "rw"), ("cfg3_treefc_b10", "rw"),
+                                         ("cfg4_mvrnn_b10", "mvrnn"), ("cfg5_dagrnn_b10", "cluster"),
+                                         ("cfg5_treelstm_b4096", "big")])
+def test_automatic_family(cx, name, family, monkeypatch):
+    """The automatic plan (cx_forward, fp32) runs the documented kernel family
+    for every BASELINE configuration."""
+    monkeypatch.delenv("CX_FORWARD_PATH", raising=False)
+    w = synth.workload(name)
+    ch = w["children"]
+    assert cx.forward_family(w["cell"], w["hidden"], ch.shape[1], ch.shape[0], w["vocab"]) == family

@@ -134,3 +134,21 @@ def test_tree_cycles_multi_cta(cx):
     c2[:, :n] = ch
     c2[0, n], c2[0, n + 1], c2[0, n + 2] = n + 1, n + 2, n  # ring without leaves
     _check(cx, c2, synth.TREE)
+
+
+@pytest.mark.parametrize("spine,shuffle", [(6000, False), (6000, True), (40000, False)])
+def test_deep_caterpillar_multi_cta(cx, spine, shuffle):
+    """Caterpillar trees (every spine node has one leaf child and the next
+    spine node as children) far deeper than the walk limit, above the
+    single-CTA size: the multi-CTA heights pass must be O(n) (pending-count
+    peeling) and the structure pass pointer-jumps. Bit-exact
+    vs the oracle, plus a short caterpillar forest next to it."""
+    n = 2 * spine + 1
+    ch = np.full((2, n), -1, np.int32)
+    for i in range(spine):  # spine node 2i: children (2i + 1 = leaf, 2i + 2 = next spine)
+        ch[0, 2 * i], ch[1, 2 * i] = 2 * i + 1, 2 * i + 2
+    extra, _ = synth.sst_shaped_forest(20, 9)
+    full = np.concatenate([ch, np.where(extra >= 0, extra + n, -1).astype(np.int32)], axis=1)
+    if shuffle:
+        full, _, _ = synth.shuffle_ids(full, None, 5)
+    _check(cx, full, synth.TREE)
