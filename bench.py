@@ -6,9 +6,11 @@ whole hot path, reading Q17 of DESIGN.md): the linearizer fused into the
 forward kernel, one launch, where the batch allows it, else
 cx_linearize + cx_forward. Default workload =
 BASELINE.json configs[1]: TreeLSTM (child-sum, binary SST-shaped trees),
-batch 10 per GPU, H = 256, fp32. Multi-GPU: one process per GPU (torchrun),
-each rank evaluates its own independent batch (weak scaling, no data-path
-collective); timing is the max over ranks.
+batch 10, H = 256, fp32. Multi-GPU: one process per GPU (torchrun); the batch's
+structures are split into contiguous blocks across the ranks (strong scaling,
+no data-path collective), timing is the max over ranks, and the packed root
+states are all-gathered over NCCL (timed separately); the batch-4096 lines
+(trees/s at 1/2/4/8 GPUs) are split the same way.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
     python bench.py --impl reference ...   # the CPU oracle on the host cores
@@ -37,7 +39,10 @@ UNIT = "trees/s"
 FMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4: SMs x FP32 lanes x 2 x max clock
 
 WORKLOADS = {
-    # name: (generator, cell, hidden, vocab, per-GPU batch or total batch, scaling)
+    # name: (generator, cell, hidden, vocab, batch, scaling). Every workload is
+    # one fixed batch of independent structures split across the N ranks
+    # (strong scaling): at N > 1 the b10 line is "batch-10
+    # latency sharded 5/3/2 per rank", the b4096 lines the trees/s headline.
     "cfg2_treelstm_b10": ("sst", synth.TREELSTM, 256, 20000, 10, "weak"),
     "cfg2_treelstm_b1": ("sst", synth.TREELSTM, 256, 20000, 1, "weak"),
     "cfg3_treegru_b10": ("sst", synth.TREEGRU, 512, 20000, 10, "weak"),
@@ -591,7 +596,7 @@ def run_gpu(args, rank, world, local_rank):
 
     # optional NCCL all-gather of the packed root states (the only collective)
     allgather_us = None
-    if world > 1 and args.allgather:
+    if world > 1 and not args.no_allgather:
         from paper_2011_01383_b200 import shard
         for _ in range(3):
             shard.all_gather_roots(roots, inp["total"])
@@ -606,6 +611,9 @@ def run_gpu(args, rank, world, local_rank):
             ag.append((a0, a1))
         torch.cuda.synchronize()
         allgather_us = statistics.median(x.elapsed_time(y) for x, y in ag) * 1e3
+        tt = torch.tensor([allgather_us], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)  # max over ranks
+        allgather_us = float(tt.item())
 
     # ---- end to end through the public API with host buffers --------------
     # the step's inputs packed in one pinned buffer (children [maxc, n] then words [n]):
@@ -661,7 +669,7 @@ def run_gpu(args, rank, world, local_rank):
     d2h = h_host.numel() * 4
 
     secondary = None
-    if args.secondary and name == "cfg2_treelstm_b10":
+    if args.secondary and name == "cfg2_treelstm_b10":  # at every N (strong scaling)
         secondary = [throughput_b4096(dt, rank, world, local_rank) for dt in ("bf16", "f32")]
 
     if rank != 0:
@@ -773,8 +781,8 @@ def main():
                    help="skip the batch-4096 throughput lines (bf16, f32) of the default run")
     p.add_argument("--dtype", default="f32", choices=["f32", "bf16"],
                    help="compute precision of cx_forward (bf16 = tcgen05 tensor-core path)")
-    p.add_argument("--allgather", action="store_true",
-                   help="N>1: also time the NCCL all-gather of root states")
+    p.add_argument("--no-allgather", action="store_true",
+                   help="N>1: skip timing the NCCL all-gather of the root states")
     args = p.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -790,6 +798,8 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
+        # NCCL's INFO lines (ranks, transports, NVLS) stay in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_gpu(args, rank, world, local_rank)

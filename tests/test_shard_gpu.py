@@ -1,0 +1,85 @@
+"""Sharded CUDA runs: G = 2/4/8 ranks (gloo
+process group, world_size G, every rank on cuda:0 -- one GPU here) each run
+cx_linearize_forward on their contiguous block of structures, the packed root
+states are all-gathered over gloo, and the result equals the unsharded CUDA
+run BIT FOR BIT (per-node arithmetic does not depend on the batch
+composition: shard invariance)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import synth
+from paper_2011_01383_b200 import shard
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run_cuda(w, children, words, dtype_name):
+    import paper_2011_01383_b200 as cx
+    dev = torch.device("cuda", 0)
+    d = lambda a, t: torch.as_tensor(np.ascontiguousarray(a, dtype=t)).to(dev)
+    H, V, cell = w["hidden"], w["vocab"], w["cell"]
+    ws = [d(a, np.float32) for _, a in synth.weights(cell, H, V)]
+    emb = d(synth.embedding(V, H, w["seed"]), np.float32)
+    import oracle  # host linearization only to count roots (test infrastructure)
+    R = oracle.linearize(children, w["kind"])["num_roots"]
+    dtype = cx.BF16 if dtype_name == "bf16" else cx.F32
+    lin, h, _, roots = cx.linearize_forward(d(children, np.int32), w["kind"], cell, H, ws, emb,
+                                            d(words, np.int32), dtype=dtype, num_roots=R)
+    assert cx.status(lin) == (0, -1)
+    return h.cpu(), roots.cpu()
+
+
+def _worker(rank, world, port, name, dtype_name, result_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        w = synth.workload(name)
+        sub, wl, (g0, g1), base = shard.shard(w["children"], w["offsets"], rank, world, w["words"])
+        # ranks take turns on the one GPU (a multi-GPU run has one each)
+        for r in range(world):
+            if r == rank:
+                h, roots_local = _run_cuda(w, sub, wl, dtype_name)
+            dist.barrier()
+        assert roots_local.shape[0] == g1 - g0
+        roots = shard.all_gather_roots(roots_local, len(w["offsets"]) - 1)
+        np.save(os.path.join(result_dir, f"h{rank}.npy"), h.numpy())
+        if rank == 0:
+            np.save(os.path.join(result_dir, "roots.npy"), roots.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("name,dtype", [("cfg2_treelstm_b10", "f32"), ("cfg5_dagrnn_b10", "f32"),
+                                        ("cfg3_treegru_b10", "f32"), ("cfg5_treelstm_b4096", "bf16")])
+def test_sharded_cuda_equals_unsharded(tmp_path, world, name, dtype):
+    w = synth.workload(name)
+    if name == "cfg5_treelstm_b4096" and world != 8:
+        pytest.skip("one b4096 split is enough (G = 8: 512 trees per rank)")
+    mp.spawn(_worker, args=(world, _free_port(), name, dtype, str(tmp_path)), nprocs=world,
+             join=True)
+    h_all, roots_all = _run_cuda(w, w["children"], w["words"], dtype)
+    got = np.load(tmp_path / "roots.npy")
+    assert got.shape == tuple(roots_all.shape)
+    assert np.array_equal(got, roots_all.numpy()), "gathered roots differ from the unsharded run"
+    off = w["offsets"]
+    for r in range(world):
+        g0, g1 = shard.block_range(len(off) - 1, r, world)
+        hr = np.load(tmp_path / f"h{r}.npy")
+        assert np.array_equal(hr, h_all.numpy()[off[g0]:off[g1]]), f"rank {r} h rows differ"
