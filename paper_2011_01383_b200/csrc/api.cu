@@ -42,6 +42,7 @@ int forward_path() {
   if (!std::strcmp(e, "smem")) return 2;
   if (!std::strcmp(e, "cluster")) return 3;
   if (!std::strcmp(e, "big")) return 4;
+  if (!std::strcmp(e, "tc")) return 5;  // bf16: always the tensor-core kernel
   return 0;
 }
 
@@ -100,6 +101,32 @@ void lin_args(const int32_t *children, int32_t n, int32_t max_children, cx_kind 
 }  // namespace
 
 namespace {
+// The one forward plan of a call (caller holds g_mu). fp32: the fused cluster /
+// single-CTA kernels (cx_linearize_forward) or fwd_plan. bf16 ("per-batch
+// precision dispatch", north_star: tensor cores only where the levels are
+// dense GEMMs): batches small enough for the cluster kernel run it on FMA with
+// bf16-rounded operands (its levels are a few nodes: 128-row UMMA tiles would
+// be mostly padding), larger batches the tcgen05 kernel. CX_FORWARD_PATH (tests)
+// disables the bf16 cluster route unless it asks for the cluster kernel.
+bool plan_forward(const cx_model *m, int maxc, int n, bool fused, int sms, cx::FwdPlan *plan,
+                  int *Gn, int *Gu) {
+  const int path = forward_path();
+  if (m->dtype == CX_BF16) {
+    const bool small_ok = (path == 0 || path == 3) && m->cell != CX_TREEFC;
+    if (small_ok && (fused ? cx::fused_plan(m->cell, m->hidden, maxc, n, plan, Gn, Gu)
+                           : cx::cluster_plan(m->cell, m->hidden, maxc, n, 0, plan, Gn, Gu))) {
+      plan->bf16ops = true;
+      return true;
+    }
+    if (fused) return false;
+    return cx::tc_plan(m->cell, m->hidden, maxc, sms, plan, Gn, Gu);
+  }
+  if (fused)
+    return cx::fused_plan(m->cell, m->hidden, maxc, n, plan, Gn, Gu) ||
+           cx::single_plan(m->cell, m->hidden, maxc, n, plan, Gn, Gu);
+  return cx::fwd_plan(m->cell, m->hidden, maxc, n, path == 5 ? 0 : path, sms, plan, Gn, Gu);
+}
+
 // cx_forward after argument checks; `fused` (non-NULL) = linearizer arguments
 // for the fused launch (its plan is required to exist).
 cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
@@ -114,13 +141,11 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
     std::lock_guard<std::mutex> lk(g_mu);
     int sms = num_sms_current();
     if (sms <= 0) return CX_E_CUDA;
-    const bool ok = fused ? (cx::fused_plan(m->cell, m->hidden, lin->max_children, n, &plan, &Gn, &Gu) ||
-                             cx::single_plan(m->cell, m->hidden, lin->max_children, n, &plan, &Gn, &Gu))
-                    : m->dtype == CX_BF16
-                        ? cx::tc_plan(m->cell, m->hidden, lin->max_children, sms, &plan, &Gn, &Gu)
-                        : cx::fwd_plan(m->cell, m->hidden, lin->max_children, n, forward_path(),
-                                       sms, &plan, &Gn, &Gu);
+    const bool ok = plan_forward(m, lin->max_children, n, fused != nullptr, sms, &plan, &Gn, &Gu);
     if (!ok) return CX_E_UNSUPPORTED;
+    // the bf16 tensor-core TreeLSTM stores each node's h in its ONE parent's
+    // child slot (forward_tc.cu): a DAG linearization (shared children) is refused
+    if (plan.tc && m->cell == CX_TREELSTM && lin->kind == CX_DAG) return CX_E_UNSUPPORTED;
   }
   const size_t N = (size_t)n, H = (size_t)m->hidden;
   char *p = align_up(static_cast<char *>(workspace), 128);
@@ -148,7 +173,8 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
   a.h_out = h_out;
   a.aux_out = aux_out;
   a.root_out = root_out;
-  if (m->dtype == CX_BF16) {  // hb, cs, xb [, hf, crow] (forward_tc.cu)
+  a.bf16ops = plan.bf16ops ? 1 : 0;
+  if (plan.tc) {  // hb, cs, xb [, hf, crow] (forward_tc.cu)
     const size_t R = cx::tc_state_rows(m->cell, n, m->vocab);
     char *q = reinterpret_cast<char *>(buf);
     a.hb = reinterpret_cast<unsigned short *>(q);
@@ -232,9 +258,12 @@ cx_status cx_linearize(const int32_t *children, int32_t n, int32_t max_children,
 
 size_t cx_forward_workspace_bytes(const cx_model *m, int32_t n) {
   if (!m) return 0;
-  if (m->dtype == CX_BF16)
-    return sizeof(cx::GridBar) + cx::tc_workspace_bytes(m->cell, m->hidden, m->vocab, n) + 512;
-  return cx::fwd_workspace_bytes(m->cell, m->hidden, n, m->vocab) + 256;
+  const size_t f32 = cx::fwd_workspace_bytes(m->cell, m->hidden, n, m->vocab) + 256;
+  if (m->dtype == CX_BF16) {  // tensor-core kernel, or the FMA cluster kernel for small batches
+    const size_t tc = sizeof(cx::GridBar) + cx::tc_workspace_bytes(m->cell, m->hidden, m->vocab, n) + 512;
+    return tc > f32 ? tc : f32;
+  }
+  return f32;
 }
 
 cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
@@ -249,9 +278,6 @@ cx_status cx_forward(const cx_model *m, const cx_weights *w, const float *emb,
   if (n < 0) return CX_E_ARG;
   if (n > 0 && (!emb || !word_ids || !h_out || !weights_ok(m->cell, w))) return CX_E_ARG;
   if (!workspace || workspace_bytes < cx_forward_workspace_bytes(m, n)) return CX_E_WORKSPACE;
-  // the bf16 TreeLSTM kernel stores each node's h in its ONE parent's child
-  // slot (forward_tc.cu): a DAG linearization (shared children) is refused
-  if (m->dtype == CX_BF16 && m->cell == CX_TREELSTM && lin->kind == CX_DAG) return CX_E_UNSUPPORTED;
   if (n == 0) return CX_OK;
   return forward_impl(m, w, emb, word_ids, lin, h_out, aux_out, root_out, workspace, nullptr, stream);
 }
@@ -278,7 +304,7 @@ cx_status cx_linearize_forward(const int32_t *children, int32_t n, int32_t max_c
   const size_t fbytes = cx_forward_workspace_bytes(m, n);
   // the fused kernel: fp32 cluster path, one launch
   const char *env = std::getenv("CX_FUSED");
-  const bool try_fused = !(env && env[0] == '0') && m->dtype == CX_F32 && n > 0 &&
+  const bool try_fused = !(env && env[0] == '0') && n > 0 &&
                          (forward_path() == 0 || forward_path() == 3);
   if (try_fused) {
     // the same argument checks as the two calls
@@ -296,8 +322,7 @@ cx_status cx_linearize_forward(const int32_t *children, int32_t n, int32_t max_c
     bool ok;
     {
       std::lock_guard<std::mutex> lk(g_mu);
-      ok = cx::fused_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu) ||
-           cx::single_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu);
+      ok = plan_forward(m, max_children, n, true, 0, &plan, &Gn, &Gu);
     }
     if (ok) {
       cx::LinArgs la;
@@ -341,15 +366,13 @@ cx_status cx_debug_set_lin_trace(unsigned long long *buf) {
 // Debug only (reporting): 1 if cx_linearize_forward would use the fused
 // single launch for this model and batch shape, else 0.
 int32_t cx_debug_fused_applies(const cx_model *m, int32_t n, int32_t max_children) {
-  if (!m || m->dtype != CX_F32 || n <= 0) return 0;
+  if (!m || n <= 0) return 0;
   const char *env = std::getenv("CX_FUSED");
   if ((env && env[0] == '0') || !(forward_path() == 0 || forward_path() == 3)) return 0;
   cx::FwdPlan plan;
   int Gn, Gu;
   std::lock_guard<std::mutex> lk(g_mu);
-  return cx::fused_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu) ||
-                 cx::single_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu)
-             ? 1 : 0;
+  return plan_forward(m, max_children, n, true, 0, &plan, &Gn, &Gu) ? 1 : 0;
 }
 
 // Debug / tests: the kernel family cx_forward runs for this model and batch
@@ -362,11 +385,7 @@ int32_t cx_debug_forward_family(const cx_model *m, int32_t n, int32_t max_childr
   std::lock_guard<std::mutex> lk(g_mu);
   const int sms = num_sms_current();
   if (sms <= 0) return 0;
-  const bool ok = m->dtype == CX_BF16
-                      ? cx::tc_plan(m->cell, m->hidden, max_children, sms, &plan, &Gn, &Gu)
-                      : cx::fwd_plan(m->cell, m->hidden, max_children, n, forward_path(), sms,
-                                     &plan, &Gn, &Gu);
-  return ok ? plan.family : 0;
+  return plan_forward(m, max_children, n, false, sms, &plan, &Gn, &Gu) ? plan.family : 0;
 }
 
 // Debug only: an empty kernel launch (measures launch overhead).
@@ -401,18 +420,13 @@ cx_status cx_linearize_forward_launch_info(const cx_model *m, int32_t n, int32_t
   int Gn = 0, Gu = 0;
   std::lock_guard<std::mutex> lk(g_mu);
   const char *env = std::getenv("CX_FUSED");
-  bool f = !(env && env[0] == '0') && m->dtype == CX_F32 && n > 0 &&
-           (forward_path() == 0 || forward_path() == 3) &&
-           (cx::fused_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu) ||
-            cx::single_plan(m->cell, m->hidden, max_children, n, &plan, &Gn, &Gu));
+  bool f = !(env && env[0] == '0') && n > 0 && (forward_path() == 0 || forward_path() == 3) &&
+           plan_forward(m, max_children, n, true, 0, &plan, &Gn, &Gu);
   if (!f) {
     const int sms = num_sms_current();
     if (sms <= 0) return CX_E_CUDA;
-    const bool ok = m->dtype == CX_BF16
-                        ? cx::tc_plan(m->cell, m->hidden, max_children, sms, &plan, &Gn, &Gu)
-                        : cx::fwd_plan(m->cell, m->hidden, max_children, n > 0 ? n : 1, forward_path(),
-                                       sms, &plan, &Gn, &Gu);
-    if (!ok) return CX_E_UNSUPPORTED;
+    if (!plan_forward(m, max_children, n > 0 ? n : 1, false, sms, &plan, &Gn, &Gu))
+      return CX_E_UNSUPPORTED;
   }
   if (fused) *fused = f ? 1 : 0;
   if (ctas) *ctas = plan.ctas;

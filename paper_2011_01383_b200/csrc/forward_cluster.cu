@@ -19,6 +19,7 @@
 // DAG whose structures share nodes, every node falls back to cluster 0
 // (still correct, just serial over one cluster).
 #include <cooperative_groups.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -37,6 +38,34 @@ using namespace rw;
 using namespace wq;
 
 constexpr int kCUnits = kRUG;  // units per CTA (16)
+
+// dtype = CX_BF16 on this (FMA) path: the contraction operands -- weights,
+// input rows x, gathered child states -- are rounded to bf16 where they are
+// produced (weight registers, gathered / imported / pushed rows); products
+// and sums stay fp32, as on the tensor cores (reading Q18). Outputs stay fp32.
+__device__ __forceinline__ float rbf(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+__device__ __forceinline__ float4 rbf4(float4 v) {
+  return make_float4(rbf(v.x), rbf(v.y), rbf(v.z), rbf(v.w));
+}
+// round rows [0, cnt) of H floats at X in place (block-wide; caller syncs)
+template <int H>
+__device__ __forceinline__ void round_rows(float *X, int cnt) {
+  for (int idx = threadIdx.x; idx < cnt * H / 4; idx += blockDim.x) {
+    float4 *p = reinterpret_cast<float4 *>(X) + idx;
+    *p = rbf4(*p);
+  }
+}
+template <int H>
+__device__ __forceinline__ void round_wregs(WRegs<H> &w) {
+#pragma unroll
+  for (int g = 0; g < 4; g++)
+#pragma unroll
+    for (int j = 0; j < WShape<H>::KC / 2; j++) {
+      float lo, hi;
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(w[g][j]));
+      w[g][j] = f2pack(rbf(lo), rbf(hi));
+    }
+}
 
 // DAG-RNN level: U h~ + W_x x in one accumulator. Rows per node in X: the
 // MAXC children, x (vector MAXC), then h~ (vector MAXC + 1, the HTS row).
@@ -121,7 +150,8 @@ struct CS {  // shared-memory carve of one CTA
 // Pull the full H-rows of `rows` (new ids, -1 = zeros) from the CS slices into
 // X (RPN rows per node: the NV children, ..., their sum h~ in the last row).
 template <int H, int NV, int RPN = NV + 1, class ROW>
-__device__ __forceinline__ void pull_rows(cg::cluster_group &cl, const CS &s, int cnt, ROW row) {
+__device__ __forceinline__ void pull_rows(cg::cluster_group &cl, const CS &s, int cnt, ROW row,
+                                          bool bf16ops) {
   constexpr int CSZ = H / kCUnits;
   constexpr int Q = kCUnits / 4;  // float4 per slice
   const int total = cnt * CSZ * Q;
@@ -135,6 +165,7 @@ __device__ __forceinline__ void pull_rows(cg::cluster_group &cl, const CS &s, in
       const int c = row(t, j);
       v[j] = c >= 0 ? *reinterpret_cast<const float4 *>(remote + (size_t)c * kCUnits + 4 * q)
                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (bf16ops) v[j] = rbf4(v[j]);
     }
     float4 sum = v[0];
 #pragma unroll
@@ -202,6 +233,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
   }
   auto load_leaf_weights = [&]() {
     load_wregs_w<4, H, 1>(w, gs, ng, myu, ro);
+    if (a.bf16ops) round_wregs<H>(w);
     if constexpr (CELL == CX_TREELSTM) {
       if (tid < 4 * kCUnits) {
         int g = tid / kCUnits, uu = tid % kCUnits;
@@ -216,6 +248,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     gs[0] = {a.w[1], 0, H, 0}; gs[1] = {a.w[1], H, H, 0}; gs[2] = {a.w[1], 2 * H, H, 0};
     gs[3] = {a.w[3], 0, H, 0};
     load_wregs_w<4, H, 1>(w, gs, 4, myu, ro);
+    if (a.bf16ops) round_wregs<H>(w);
   };
   constexpr bool EARLY = FUSED && CELL == CX_TREELSTM;
   if constexpr (FUSED && !EARLY) {
@@ -308,6 +341,10 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       if (b0) __syncthreads();  // E is overwritten
       gather_rows_c<1, H>(E, cntb, [&](int t, int) { return a.emb + (size_t)ewd[b0 + t] * H; });
       __syncthreads();
+      if (a.bf16ops) {
+        round_rows<H>(E, cntb);
+        __syncthreads();
+      }
       trace_mark(a, 14);
       for (int t0 = 0; t0 < cntb; t0 += Cfg::TLEAF) {
         const int cntt = min(Cfg::TLEAF, cntb - t0);
@@ -565,6 +602,14 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
             ldcg4(a.h_out + o);
     }
     cp_async_wait_all();
+    if (push && a.bf16ops)  // each thread rounds the pieces it copied itself
+      for (int idx = tid; idx < nl0 * Q4; idx += blockDim.x) {
+        const int v = s.list[idx / Q4], q = idx % Q4, pr = prow[v];
+        if (pr >= 0) {
+          float4 *d = reinterpret_cast<float4 *>(XA + (size_t)pr * H + 4 * q);
+          *d = rbf4(*d);
+        }
+      }
     trace_mark(a, 22);
   }
   if (push) {
@@ -599,7 +644,7 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
     a.h_out[o] = hh;
     if (CELL == CX_TREELSTM && a.aux_out) a.aux_out[o] = cc;
     if (a.root_out && prow[v] < 0) a.root_out[(size_t)s.lab[v] * H + myu] = hh;
-    s_stage[sb][t * kCUnits + warp] = hh;
+    s_stage[sb][t * kCUnits + warp] = a.bf16ops ? rbf(hh) : hh;  // the parent's operand
   };
   // ... then (after __syncthreads) lane hu of node t's half-warp sends the
   // 64-byte slice to CTA hu's row of the parent
@@ -642,6 +687,10 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
       __syncthreads();
       gather_rows_c<1, H>(X, cntb, [&](int t, int) { return a.emb + (size_t)s_word[t] * H; });
       __syncthreads();
+      if (a.bf16ops) {
+        round_rows<H>(X, cntb);
+        __syncthreads();
+      }
       for (int t0 = 0; t0 < cntb; t0 += Cfg::TLEAF) {
         const int cntt = min(Cfg::TLEAF, cntb - t0);
         auto tile = [&](auto tt) {
@@ -711,10 +760,10 @@ __global__ void __launch_bounds__(kRThreads, 1) ck_kernel(FwdArgs a) {
               wd = 0;
             }
             *reinterpret_cast<float4 *>(s.X + (size_t)(t * RPN + MAXC) * H + 4 * c) =
-                ldcg4(a.emb + (size_t)wd * H + 4 * c);
+                a.bf16ops ? rbf4(ldcg4(a.emb + (size_t)wd * H + 4 * c)) : ldcg4(a.emb + (size_t)wd * H + 4 * c);
           }
         }
-        pull_rows<H, Cfg::NVMAX, Cfg::RPN>(cl, s, cntt, child);
+        pull_rows<H, Cfg::NVMAX, Cfg::RPN>(cl, s, cntt, child, a.bf16ops);
         __syncthreads();
       }
       auto tile = [&](auto tt) {

@@ -44,6 +44,7 @@ struct FwdArgs {
   unsigned long long *trace;  // debug: %globaltimer per CTA and phase (cx_debug_set_trace)
   int trace_slots;
   int push_off;  // measurement/test: CX_PUSH=0 forces the cluster kernel's barrier + pull mode
+  int bf16ops;   // dtype CX_BF16 on the FMA cluster path: operands rounded to bf16 (reading Q18)
   LinArgs lin;  // fused linearize + forward (cx_linearize_forward): the linearizer's arguments
 };
 
@@ -84,6 +85,7 @@ struct FwdPlan {
   // (forward_big.cu), 5 MV-RNN, 6 bf16 tensor cores (forward_tc.cu), 7 fused
   // single-CTA (forward_single.cu)
   int family = 0;
+  bool bf16ops = false;  // dtype CX_BF16 served by an FMA kernel with bf16-rounded operands
 };
 
 // Returns false (CX_E_UNSUPPORTED) when no instantiation covers the model.
@@ -107,6 +109,9 @@ bool pdl_enabled();
 // Fused linearize + forward (forward_cluster.cu): fp32 cluster
 // path of TreeLSTM / DAG-RNN for small batches. False when not applicable.
 bool fused_plan(int cell, int H, int maxc, int n, FwdPlan *plan, int *Gn, int *Gu);
+// The cluster kernel without the linearizer (forward_cluster.cu); `roots` <= 0:
+// unknown. False when the batch does not fit its shared memory.
+bool cluster_plan(int cell, int H, int maxc, int n, int roots, FwdPlan *plan, int *Gn, int *Gu);
 // Fused single-CTA-per-structure-group path (forward_single.cu, SURVEY §8(f)
 // f2): TreeRNN (recursion unrolled, CX_UNROLL) and tiny TreeFC batches.
 bool single_plan(int cell, int H, int maxc, int n, FwdPlan *plan, int *Gn, int *Gu);

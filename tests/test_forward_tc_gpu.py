@@ -23,6 +23,14 @@ def cx():
     return m
 
 
+@pytest.fixture(autouse=True)
+def _force_tensor_cores(monkeypatch):
+    """Small bf16 batches run the FMA cluster kernel by default (per-batch
+    dispatch, test_bf16_dispatch_gpu.py); this file tests the tensor-core
+    kernel at every size."""
+    monkeypatch.setenv("CX_FORWARD_PATH", "tc")
+
+
 def _run(cx, cell, H, V, ch, kind, words, emb, want_aux=False, num_roots=None):
     _, wd = weights_dev(cell, H, V)
     lin = cx.linearize(dev_i32(ch), kind)
