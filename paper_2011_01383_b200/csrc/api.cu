@@ -214,6 +214,8 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
     std::lock_guard<std::mutex> lk(g_mu);
     const char *pe = std::getenv("CX_PUSH");
     a.push_off = pe && pe[0] == '0';
+    const char *de = std::getenv("CX_DISCARD");
+    a.discard_off = de && de[0] == '0';
     a.trace = g_trace;
     a.trace_slots = g_trace_slots;
   }

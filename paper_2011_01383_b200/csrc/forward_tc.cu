@@ -146,6 +146,12 @@ __device__ __forceinline__ void cp16_zfill(uint32_t dst, const void *src, bool v
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                "r"(valid ? 16 : 0) : "memory");
 }
+// Drop a dead 128-byte workspace line from L2 without writing it back (its
+// only reader has consumed it): the TreeLSTM memory cells and parent-slot rows
+// would otherwise be evicted to HBM although nobody reads them again.
+__device__ __forceinline__ void discard_l2(const void *p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -337,6 +343,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
   const int L = status0 == CX_OK ? a.hdr->num_levels : 0, first_leaf = a.hdr->first_leaf;
   const int xlo = C::DAG ? 0 : first_leaf;  // node-order x rows start here
   const bool hoist = C::LSTM && a.hoist;
+  const bool discard_ok = !a.discard_off;  // CX_DISCARD=0: keep dead lines (measurement)
   const int sbase = hoist ? a.V : 0;  // state row of internal node i = sbase + i
   // ---- phase 0: bf16 input rows ------------------------------------------------
   if (C::XSLOT && status0 == CX_OK) {
@@ -544,6 +551,19 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
         const int tslot = (l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
         tc_mark(a, tslot + 0, warp * 32);
         TcMeta<J> &m = meta[ms];
+        if constexpr (C::LSTM) {
+          // the slot's previous tile (TT - kMetaRing, filled by this warp) is
+          // done: its children's memory-cell lines of this CTA's units were
+          // read once, by that epilogue, and are dead (a tree node has one
+          // parent; hoisted word rows [0, V) are shared and stay)
+          if (TT >= (uint32_t)kMetaRing && discard_ok)
+            for (int r = lane; r < kTM; r += 32)
+#pragma unroll
+              for (int k = 0; k < J; k++) {
+                const int row = m.ch[k][r];
+                if (row >= (hoist ? a.V : 0)) discard_l2(cs + (size_t)row * H + unit0);
+              }
+        }
         constexpr int RQ = kTM / 32;
         int own[RQ], sv[RQ], psv[RQ], ch[RQ][J];
 #pragma unroll
@@ -616,6 +636,18 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
     for (int l = 0; l < L; l++) {
       const bool leaf = l == 0;
       if (l > 0) level_sync();
+      if (C::LSTM && discard_ok && l >= 2) {
+        // level l - 1 is complete: its tiles' parent-slot operand rows (rows
+        // k n + [lbeg, lbeg + lsize) of pb, loaded by every unit-group CTA) are
+        // dead; every CTA drops a share of their 128-byte lines
+        const int lb = __ldg(a.lbeg + l - 1), ls = __ldg(a.lsize + l - 1);
+        constexpr int LPR = H * 2 / 128;  // lines per bf16 row
+        const long long total = (long long)J * ls * LPR;
+        for (long long e = (long long)blockIdx.x * kWork + tid; e < total; e += (long long)gridDim.x * kWork) {
+          const int k = (int)(e / ((long long)ls * LPR)), rem = (int)(e % ((long long)ls * LPR));
+          discard_l2(a.pb + ((size_t)k * n + lb + rem / LPR) * H + (rem % LPR) * 64);
+        }
+      }
       if (l == 1 && hoist) {  // the word table is complete: fill the leaves' parent slots
         leaf_pass(true);
         level_sync();

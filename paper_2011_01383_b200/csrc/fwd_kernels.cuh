@@ -45,6 +45,7 @@ struct FwdArgs {
   int trace_slots;
   int push_off;  // measurement/test: CX_PUSH=0 forces the cluster kernel's barrier + pull mode
   int bf16ops;   // dtype CX_BF16 on the FMA cluster path: operands rounded to bf16 (reading Q18)
+  int discard_off;  // measurement: CX_DISCARD=0 keeps the tc kernel's dead workspace lines in L2
   LinArgs lin;  // fused linearize + forward (cx_linearize_forward): the linearizer's arguments
 };
 
