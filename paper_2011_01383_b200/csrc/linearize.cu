@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
   if (tid == 0) {
     a.hdr->err_key = kNoError;
     a.misc[0] = a.misc[1] = a.misc[2] = a.misc[3] = a.misc[4] = a.misc[5] = a.misc[6] = 0;
-    a.misc[7] = a.misc[8] = 0;
+    a.misc[7] = a.misc[8] = a.misc[9] = 0;
   }
   if (threadIdx.x == 0) s_tmp[32] = 0;
   grid_sync(a.bar, G, epoch);
@@ -165,40 +165,85 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
   int L = 0;
   if (!failed && n > 0) {
     if (tree_like) {
-      // every leaf walks up its parent chain: at each parent it raises the
-      // height (atomicMax) and decrements the pending-child count; only the
-      // last arriving child continues, with the parent's final height (every
-      // child's atomicMax precedes its decrement) -- O(n) work for any shape.
-      // A node on or above a cycle never reaches pending 0, so no walk loops;
-      // those nodes are the CX_E_CYCLE candidates (lowest id reported).
+      // Pass 1: every leaf walks up its parent chain (at most kLinWalkLevels
+      // steps) with dependent parent loads only, posting height[ancestor] =
+      // max(., distance) fire-and-forget: O(sum of leaf depths) = O(n depth),
+      // cheap for the shallow forests of the configs. Brent's check stops a
+      // walk that entered a cycle.
+      // Pass 2 (only if a walk hit the cap, looped, or left a node unreached):
+      // pending-count peeling -- at each parent raise the height, decrement
+      // its pending-child count, and only the last arriving child continues
+      // with the parent's final height: O(n) for any shape (deep caterpillars,
+      // ADVICE round 1). Nodes left with pending > 0 are on or above a cycle.
       int hmax = 0;
+      bool looped = false, deep = false;
       for (int v = tid; v < n; v += nthr) {
         if (ch[v] != -1) continue;  // walks start at leaves
-        int cur = v, d = 0;
+        int cur = v, d = 0, tort = v, power = 1, lam = 0;
         while (true) {
           const int p = __ldcg(&parent[cur]);
           if (p < 0) break;
-          atomicMax(&hgt[p], d + 1);
-          __threadfence();
-          if (atomicSub(&pending[p], 1) != 1) break;
-          __threadfence();
-          d = atomicAdd(&hgt[p], 0);
+          if (d == kLinWalkLevels) {
+            deep = true;
+            break;
+          }
+          d++;
+          atomicMax(&hgt[p], d);  // result unused: a RED.MAX
           cur = p;
+          if (cur == tort) {
+            looped = true;
+            break;
+          }
+          if (++lam == power) {
+            tort = cur;
+            power <<= 1;
+            lam = 0;
+          }
         }
         hmax = max(hmax, d);
       }
       for (int o = 16; o; o >>= 1) hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
       if (lane == 0) atomicMax(&a.misc[4], hmax);
+      if (__syncthreads_or(looped || deep) && threadIdx.x == 0) atomicAdd(&a.misc[3], 1);
       grid_sync(a.bar, G, epoch);
-      bool cyc = false;
-      for (int v = tid; v < n; v += nthr)
-        if (__ldcg(&pending[v]) > 0) {
-          latch_error(a.hdr, CX_E_CYCLE, v);
-          cyc = true;
+      // misc[3] changes only before that barrier: every CTA takes the same path
+      bool need2 = __ldcg(&a.misc[3]) != 0;
+      if (!need2) {
+        // a node no walk reached (a cycle without leaves below) also needs pass 2
+        bool unreached = false;
+        for (int v = tid; v < n; v += nthr) unreached = unreached || __ldcg(&hgt[v]) < 0;
+        if (__syncthreads_or(unreached) && threadIdx.x == 0) atomicAdd(&a.misc[9], 1);
+        grid_sync(a.bar, G, epoch);
+        need2 = __ldcg(&a.misc[9]) != 0;
+      }
+      if (need2) {
+        hmax = 0;
+        for (int v = tid; v < n; v += nthr) {
+          if (ch[v] != -1) continue;
+          int cur = v, d = 0;
+          while (true) {
+            const int p = __ldcg(&parent[cur]);
+            if (p < 0) break;
+            atomicMax(&hgt[p], d + 1);  // pass-1 values are lower bounds: max is unaffected
+            __threadfence();
+            if (atomicSub(&pending[p], 1) != 1) break;
+            __threadfence();
+            d = atomicAdd(&hgt[p], 0);
+            cur = p;
+          }
+          hmax = max(hmax, d);
         }
-      if (__syncthreads_or(cyc) && threadIdx.x == 0) atomicAdd(&a.misc[3], 1);
-      grid_sync(a.bar, G, epoch);
-      if (__ldcg(&a.misc[3]) != 0) failed = true;
+        for (int o = 16; o; o >>= 1) hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+        if (lane == 0) atomicMax(&a.misc[4], hmax);
+        grid_sync(a.bar, G, epoch);
+        for (int v = tid; v < n; v += nthr)
+          if (__ldcg(&pending[v]) > 0) {
+            latch_error(a.hdr, CX_E_CYCLE, v);
+            failed = true;  // (read back below for every CTA)
+          }
+        grid_sync(a.bar, G, epoch);
+        failed = __ldcg(reinterpret_cast<const unsigned long long *>(&a.hdr->err_key)) != kNoError;
+      }
       L = __ldcg(&a.misc[4]) + 1;
     } else {
       // finished-node counts: misc[3] = leaves; round r adds into misc[r % 3],
