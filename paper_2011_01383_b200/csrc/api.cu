@@ -101,6 +101,10 @@ void lin_args(const int32_t *children, int32_t n, int32_t max_children, cx_kind 
 }  // namespace
 
 namespace {
+// bf16 TreeFC batches up to this many nodes run the register-weight FMA kernel
+// (b1: 255 nodes, 47 us vs 80 us on the tensor cores; b10: 2,550 nodes, tensor
+// cores 96 us vs 160 us)
+constexpr int kBf16FcFmaMaxN = 1024;
 // The one forward plan of a call (caller holds g_mu). fp32: the fused cluster /
 // single-CTA kernels (cx_linearize_forward) or fwd_plan. bf16 ("per-batch
 // precision dispatch", north_star: tensor cores only where the levels are
@@ -115,6 +119,12 @@ bool plan_forward(const cx_model *m, int maxc, int n, bool fused, int sms, cx::F
     const bool small_ok = (path == 0 || path == 3) && m->cell != CX_TREEFC;
     if (small_ok && (fused ? cx::fused_plan(m->cell, m->hidden, maxc, n, plan, Gn, Gu)
                            : cx::cluster_plan(m->cell, m->hidden, maxc, n, 0, plan, Gn, Gu))) {
+      plan->bf16ops = true;
+      return true;
+    }
+    // TreeFC: small batches on the register-weight kernel (FMA, rounded operands)
+    if (!fused && path == 0 && m->cell == CX_TREEFC && n <= kBf16FcFmaMaxN &&
+        cx::fwd_plan(m->cell, m->hidden, maxc, n, 1, sms, plan, Gn, Gu)) {
       plan->bf16ops = true;
       return true;
     }

@@ -19,6 +19,8 @@
 // sweep that dominated small levels.
 #include <cuda_runtime.h>
 
+#include <cuda_bf16.h>
+
 #include <cstdlib>
 #include <type_traits>
 
@@ -378,6 +380,11 @@ struct RTreeFc {
       const FwdArgs &a = *c.a;
       if (i0 != pre) { meta(i0, cnt); __syncthreads(); }
       gather_rows_c<2, H>(c.X, cnt, [&](int t, int j) { return a.h_out + (size_t)m->cin[t][j] * H; });
+      if (a.bf16ops) {  // dtype bf16 on FMA: the gathered operand rows rounded (reading Q18)
+        __syncthreads();  // (the rows were copied by other threads' cp.async)
+        for (int idx = threadIdx.x; idx < cnt * 2 * H; idx += blockDim.x)
+          c.X[idx] = __bfloat162float(__float2bfloat16_rn(c.X[idx]));
+      }
       __syncthreads();
       float s[1];
       contract<RFcLevel, H, T>(c, c.X, *reinterpret_cast<const float(*)[4][RShape<H>::KC]>(w), s);
@@ -523,6 +530,11 @@ __global__ void __launch_bounds__(kRThreads, 1) rw_kernel(FwdArgs a) {
   {
     int ng = C::level_gates(a, gs);
     load_wregs<Cfg::NG, KC>(w, gs, ng, ctx.unit0 + u, k0);
+    if (a.bf16ops)  // dtype bf16 on FMA (TreeFC small batches): weights rounded
+#pragma unroll
+      for (int g = 0; g < 4; g++)
+#pragma unroll
+        for (int j = 0; j < KC; j++) w[g][j] = __bfloat162float(__float2bfloat16_rn(w[g][j]));
   }
   if constexpr (C::kLeafPost) {  // refactored GRU: the leaves' m once their h is complete
     grid_sync(a.bar, gridDim.x, epoch);

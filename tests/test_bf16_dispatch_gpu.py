@@ -84,3 +84,22 @@ def test_bf16_treelstm_dag(cx, monkeypatch):
     with pytest.raises(cx.CxError) as ei:
         cx.forward(T.TREELSTM, H, wd, dev_f32(emb), dev_i32(words), lin, dtype=cx.BF16)
     assert ei.value.code == 8
+
+
+@pytest.mark.parametrize("name,family", [("cfg3_treefc_b1", "rw"), ("cfg3_treefc_b10", "tc")])
+def test_bf16_treefc_dispatch(cx, name, family, monkeypatch):
+    """bf16 TreeFC: small batches on the register-weight FMA kernel with rounded
+    operands, larger ones on the tensor cores; both within the bf16 tolerance."""
+    monkeypatch.delenv("CX_FORWARD_PATH", raising=False)
+    w = synth.workload(name)
+    cell, H, V, ch, kind = w["cell"], w["hidden"], w["vocab"], w["children"], w["kind"]
+    assert cx.forward_family(cell, H, ch.shape[1], ch.shape[0], V, cx.BF16) == family
+    words = synth.word_ids(ch, V, w["seed"])
+    emb = synth.embedding(V, H, w["seed"])
+    ws_np, wd = weights_dev(cell, H, V)
+    lin = cx.linearize(dev_i32(ch), kind)
+    h, _, _ = cx.forward(cell, H, wd, dev_f32(emb), dev_i32(words), lin, dtype=cx.BF16)
+    h32, _, _ = cx.forward(cell, H, wd, dev_f32(emb), dev_i32(words), lin)
+    st, _, rh, _ = oracle.forward(cell, H, V, ws_np, emb, words, ch)
+    e, e32 = normwise_rel_err(h.cpu().numpy(), rh), normwise_rel_err(h32.cpu().numpy(), rh)
+    assert e <= TOL_BF16 and e32 <= 1e-4 and e > 10 * e32, (e, e32)
