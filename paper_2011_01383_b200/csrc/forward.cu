@@ -847,6 +847,10 @@ cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream) 
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  if (plan.family == 7) {  // fused single-CTA kernel: no grid-wide dependency, plain launch
+    cfg.attrs = attr + 1;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  }
   return cudaLaunchKernelExC(&cfg, plan.kernel, params);
 }
 

@@ -29,6 +29,7 @@
 
 #include "fwd_common.cuh"
 #include "lin_single.cuh"
+#include "lin_warp.cuh"
 
 namespace cx {
 namespace {
@@ -50,7 +51,18 @@ __global__ void __launch_bounds__(kScThreads) sc_kernel(FwdArgs a) {
   trace_mark(a, 0);
   LinPrefetch pf{a.words, a.emb, H, a.V};
   int *chn = sm + lin_sm_ints(n, maxc, kScCnt);
-  const LinOut lo = lin_single_body(a.lin, sm, kScCnt, blockIdx.x == 0, chn, pf);
+  const bool tiny = lin_warp_applies(n, maxc);
+  if (tiny && tid >= 32) {
+    // warp 0 linearizes; the others fetch the word ids and pull the nodes'
+    // embedding rows into L2 meanwhile (fire-and-forget prefetches)
+    for (int v = tid - 32; v < n; v += blockDim.x - 32) {
+      const int wd = __ldg(a.words + v);
+      if (wd >= 0 && wd < a.V)
+        for (int q = 0; q < H; q += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.emb + (size_t)wd * H + q));
+    }
+  }
+  const LinOut lo = tiny ? lin_warp_body(a.lin, sm, blockIdx.x == 0, chn)
+                         : lin_single_body(a.lin, sm, kScCnt, blockIdx.x == 0, chn, pf);
   trace_mark(a, 20);
   if (!lo.ok) {
     fused_exit(a, ferr);
@@ -79,7 +91,7 @@ __global__ void __launch_bounds__(kScThreads) sc_kernel(FwdArgs a) {
   // state rows: shared memory when they fit (after the ints), else h_out
   float *hs = reinterpret_cast<float *>(lev + n + 4);
   const bool on_chip = (size_t)(reinterpret_cast<char *>(hs + (size_t)n * H) -
-                                reinterpret_cast<char *>(sm)) <= kScSmem;
+                                reinterpret_cast<char *>(sm)) <= dynamic_smem_bytes();
   auto hrow = [&](int i) { return on_chip ? hs + (size_t)i * H : a.h_out + (size_t)ls.perm[i] * H; };
   auto hput = [&](int i, int u, float v) {  // state + caller output
     if (on_chip) {
@@ -192,8 +204,11 @@ __global__ void __launch_bounds__(kScThreads) sc_kernel(FwdArgs a) {
 constexpr int kScMaxWork = 1 << 22;  // TreeFC: n H^2 multiply-adds per launch
 
 template <int CELL, int U>
-bool sc_plan_one(int n, int maxc, FwdPlan *p, int *Gn, int *Gu) {
+bool sc_plan_one(int n, int maxc, int H, FwdPlan *p, int *Gn, int *Gu) {
   const size_t smem = sizeof(int) * sc_smem_ints(n, maxc);
+  // + the state rows when they fit (the kernel checks %dynamic_smem_size); the
+  // launch asks for no more shared memory than it uses
+  const size_t with_rows = smem + sizeof(float) * ((size_t)n * H + 16);
   auto k = sc_kernel<CELL, U>;
   constexpr int kMaxDev = 64;
   static int set[kMaxDev];
@@ -215,7 +230,7 @@ bool sc_plan_one(int n, int maxc, FwdPlan *p, int *Gn, int *Gu) {
   *Gu = 1;
   p->ctas = G;
   p->threads = kScThreads;
-  p->smem = kScSmem;  // the state rows use the rest when they fit
+  p->smem = with_rows <= kScSmem ? with_rows : smem;
   p->kernel = (const void *)k;
   p->cluster = 1;
   p->fused = true;
@@ -233,11 +248,11 @@ bool single_plan(int cell, int H, int maxc, int n, FwdPlan *p, int *Gn, int *Gu)
   if (cell == CX_TREERNN) {
     const char *e = std::getenv("CX_UNROLL");
     const int U = e ? std::atoi(e) : 2;
-    if (U == 1) return sc_plan_one<CX_TREERNN, 1>(n, maxc, p, Gn, Gu);
-    return sc_plan_one<CX_TREERNN, 2>(n, maxc, p, Gn, Gu);
+    if (U == 1) return sc_plan_one<CX_TREERNN, 1>(n, maxc, H, p, Gn, Gu);
+    return sc_plan_one<CX_TREERNN, 2>(n, maxc, H, p, Gn, Gu);
   }
   if (cell == CX_TREEFC && (size_t)n * H * H <= (size_t)kScMaxWork)
-    return sc_plan_one<CX_TREEFC, 1>(n, maxc, p, Gn, Gu);
+    return sc_plan_one<CX_TREEFC, 1>(n, maxc, H, p, Gn, Gu);
   return false;
 }
 

@@ -27,6 +27,7 @@
 #include "common.cuh"
 #include "lin_kernels.cuh"
 #include "lin_single.cuh"
+#include "lin_warp.cuh"
 
 namespace cx {
 
@@ -744,7 +745,8 @@ __global__ void __launch_bounds__(kLinThreads, 1) lin_kernel(LinArgs a) {
 __global__ void __launch_bounds__(kLinSingleThreads, 1) lin_single_kernel(LinArgs a) {
   griddep_launch_dependents();  // the forward may stage its weights meanwhile
   extern __shared__ int sm[];
-  lin_single_body(a, sm, kLinSmemCnt, true, nullptr, LinPrefetch{});
+  if (lin_warp_applies(a.n, a.maxc)) lin_warp_body(a, sm, true, nullptr);  // tiny forests
+  else lin_single_body(a, sm, kLinSmemCnt, true, nullptr, LinPrefetch{});
 }
 
 __global__ void empty_kernel(unsigned long long *t) {

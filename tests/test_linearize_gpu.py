@@ -152,3 +152,38 @@ def test_deep_caterpillar_multi_cta(cx, spine, shuffle):
     if shuffle:
         full, _, _ = synth.shuffle_ids(full, None, 5)
     _check(cx, full, synth.TREE)
+
+
+def test_tiny_fuzz_warp_path(cx):
+    """n <= 32 (the one-warp linearizer, lin_warp.cuh): 1,500 random trees,
+    forests, DAGs, chains with shuffled ids, plus corrupted inputs of every
+    error kind -- bit-exact vs the oracle, errors included."""
+    rng = np.random.default_rng(7)
+    for seed in range(1500):
+        n = 1 + seed % 32
+        r = seed % 5
+        maxc = 1 + seed % 4
+        if r == 0:
+            ch, kind = synth.random_dag(n, maxc, seed, p_edge=0.4), synth.DAG
+        elif r == 1:
+            ch, kind = synth.chains(1 + seed % 3, 1 + (n - 1) // 3)[0], synth.SEQUENCE
+        else:
+            ch, kind = synth.random_forest(n, maxc, seed), synth.TREE
+        if seed % 2:
+            ch, _, _ = synth.shuffle_ids(ch, None, seed)
+        ch = np.ascontiguousarray(ch, dtype=np.int32)
+        if seed % 7 == 3 and ch.size:  # corrupt: out of range, layout, duplicate, cycle
+            ch = ch.copy()
+            m, n2 = ch.shape
+            v = int(rng.integers(n2))
+            kk = int(rng.integers(m))
+            op = (seed // 7) % 4
+            if op == 0:
+                ch[kk, v] = n2 + 3
+            elif op == 1 and m > 1:
+                ch[0, v], ch[m - 1, v] = -1, int(rng.integers(n2))
+            elif op == 2 and m > 1:
+                ch[0, v] = ch[1, v] = int(rng.integers(n2))
+            else:
+                ch[kk, v] = v  # self edge: a cycle
+        _check(cx, ch, kind)
