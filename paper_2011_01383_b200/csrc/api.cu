@@ -105,6 +105,14 @@ namespace {
 // (b1: 255 nodes, 47 us vs 80 us on the tensor cores; b10: 2,550 nodes, tensor
 // cores 96 us vs 160 us)
 constexpr int kBf16FcFmaMaxN = 1024;
+// fp32 batches of TreeLSTM / DAG-RNN / TreeFC with at least this many nodes run
+// the split-fp32 tensor-core kernel (forward_tc.cu, SP = 2): their levels are
+// dense GEMMs. CX_TC_F32_MIN_N overrides (measurement).
+constexpr int kTcF32MinN = 2048;
+int tc_f32_min_n() {
+  const char *e = std::getenv("CX_TC_F32_MIN_N");
+  return e ? std::atoi(e) : kTcF32MinN;
+}
 // The one forward plan of a call (caller holds g_mu). fp32: the fused cluster /
 // single-CTA kernels (cx_linearize_forward) or fwd_plan. bf16 ("per-batch
 // precision dispatch", north_star: tensor cores only where the levels are
@@ -112,8 +120,9 @@ constexpr int kBf16FcFmaMaxN = 1024;
 // bf16-rounded operands (its levels are a few nodes: 128-row UMMA tiles would
 // be mostly padding), larger batches the tcgen05 kernel. CX_FORWARD_PATH (tests)
 // disables the bf16 cluster route unless it asks for the cluster kernel.
-bool plan_forward(const cx_model *m, int maxc, int n, bool fused, int sms, cx::FwdPlan *plan,
-                  int *Gn, int *Gu) {
+// kind: the linearization's (-1 unknown: a workspace or launch-shape query)
+bool plan_forward(const cx_model *m, int maxc, int n, int kind, bool fused, int sms,
+                  cx::FwdPlan *plan, int *Gn, int *Gu) {
   const int path = forward_path();
   if (m->dtype == CX_BF16) {
     const bool small_ok = (path == 0 || path == 3) && m->cell != CX_TREEFC;
@@ -129,11 +138,18 @@ bool plan_forward(const cx_model *m, int maxc, int n, bool fused, int sms, cx::F
       return true;
     }
     if (fused) return false;
-    return cx::tc_plan(m->cell, m->hidden, maxc, sms, plan, Gn, Gu);
+    return cx::tc_plan(m->cell, m->hidden, maxc, 1, sms, plan, Gn, Gu);
   }
   if (fused)
     return cx::fused_plan(m->cell, m->hidden, maxc, n, plan, Gn, Gu) ||
            cx::single_plan(m->cell, m->hidden, maxc, n, plan, Gn, Gu);
+  // dense levels: the split-fp32 tensor-core kernel (a TreeLSTM DAG
+  // linearization stays on FMA: that kernel hands each h to ONE parent slot)
+  const bool tc_cell = m->cell == CX_TREELSTM || m->cell == CX_DAGRNN || m->cell == CX_TREEFC;
+  if (tc_cell && !(m->cell == CX_TREELSTM && kind == CX_DAG) &&
+      (path == 5 || (path == 0 && n >= tc_f32_min_n())) &&
+      cx::tc_plan(m->cell, m->hidden, maxc, 2, sms, plan, Gn, Gu))
+    return true;
   return cx::fwd_plan(m->cell, m->hidden, maxc, n, path == 5 ? 0 : path, sms, plan, Gn, Gu);
 }
 
@@ -151,7 +167,8 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
     std::lock_guard<std::mutex> lk(g_mu);
     int sms = num_sms_current();
     if (sms <= 0) return CX_E_CUDA;
-    const bool ok = plan_forward(m, lin->max_children, n, fused != nullptr, sms, &plan, &Gn, &Gu);
+    const bool ok = plan_forward(m, lin->max_children, n, lin->kind, fused != nullptr, sms, &plan,
+                                 &Gn, &Gu);
     if (!ok) return CX_E_UNSUPPORTED;
     // the bf16 tensor-core TreeLSTM stores each node's h in its ONE parent's
     // child slot (forward_tc.cu): a DAG linearization (shared children) is refused
@@ -184,18 +201,19 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
   a.aux_out = aux_out;
   a.root_out = root_out;
   a.bf16ops = plan.bf16ops ? 1 : 0;
-  if (plan.tc) {  // hb, cs, xb [, hf, crow] (forward_tc.cu)
+  if (plan.tc) {  // hb, cs, xb [, hf, crow] [, pb, pslot] (forward_tc.cu)
     const size_t R = cx::tc_state_rows(m->cell, n, m->vocab);
+    const size_t RW = H * (size_t)plan.tc_sp;  // bf16 per operand row
     char *q = reinterpret_cast<char *>(buf);
     a.hb = reinterpret_cast<unsigned short *>(q);
-    q = align_up(q + 2 * R * H, 256);
+    q = align_up(q + 2 * R * RW, 256);
     if (m->cell == CX_TREELSTM) {
       a.cs = reinterpret_cast<float *>(q);
       q = align_up(q + 4 * R * H, 256);
     }
     a.xb = reinterpret_cast<unsigned short *>(q);
     a.xmode = cx::tc_xmode(n, m->vocab);
-    q = align_up(q + 2 * (a.xmode ? N : (size_t)m->vocab) * H, 256);
+    q = align_up(q + 2 * (a.xmode ? N : (size_t)m->vocab) * RW, 256);
     a.cell_has_x = m->cell == CX_TREELSTM || m->cell == CX_DAGRNN;
     a.hoist = cx::tc_hoist(m->cell, n, m->vocab) ? 1 : 0;
     if (a.hoist) {
@@ -206,7 +224,7 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
     }
     if (m->cell == CX_TREELSTM) {
       a.pb = reinterpret_cast<unsigned short *>(q);
-      q = align_up(q + 2 * (2 * N) * H, 256);
+      q = align_up(q + 2 * (2 * N) * RW, 256);
       a.pslot = reinterpret_cast<int *>(q);
     }
   } else if (plan.big) a.pbuf = buf;  // hs, st [n][H] + words [n] (forward_big.cu)
@@ -272,7 +290,11 @@ size_t cx_forward_workspace_bytes(const cx_model *m, int32_t n) {
   if (!m) return 0;
   const size_t f32 = cx::fwd_workspace_bytes(m->cell, m->hidden, n, m->vocab) + 256;
   if (m->dtype == CX_BF16) {  // tensor-core kernel, or the FMA cluster kernel for small batches
-    const size_t tc = sizeof(cx::GridBar) + cx::tc_workspace_bytes(m->cell, m->hidden, m->vocab, n) + 512;
+    const size_t tc = sizeof(cx::GridBar) + cx::tc_workspace_bytes(m->cell, m->hidden, m->vocab, n, 1) + 512;
+    return tc > f32 ? tc : f32;
+  }
+  if (m->cell == CX_TREELSTM || m->cell == CX_DAGRNN || m->cell == CX_TREEFC) {  // split-fp32 tensor cores
+    const size_t tc = sizeof(cx::GridBar) + cx::tc_workspace_bytes(m->cell, m->hidden, m->vocab, n, 2) + 512;
     return tc > f32 ? tc : f32;
   }
   return f32;
@@ -334,7 +356,7 @@ cx_status cx_linearize_forward(const int32_t *children, int32_t n, int32_t max_c
     bool ok;
     {
       std::lock_guard<std::mutex> lk(g_mu);
-      ok = plan_forward(m, max_children, n, true, 0, &plan, &Gn, &Gu);
+      ok = plan_forward(m, max_children, n, kind, true, 0, &plan, &Gn, &Gu);
     }
     if (ok) {
       cx::LinArgs la;
@@ -384,12 +406,13 @@ int32_t cx_debug_fused_applies(const cx_model *m, int32_t n, int32_t max_childre
   cx::FwdPlan plan;
   int Gn, Gu;
   std::lock_guard<std::mutex> lk(g_mu);
-  return plan_forward(m, max_children, n, true, 0, &plan, &Gn, &Gu) ? 1 : 0;
+  return plan_forward(m, max_children, n, -1, true, 0, &plan, &Gn, &Gu) ? 1 : 0;
 }
 
 // Debug / tests: the kernel family cx_forward runs for this model and batch
 // shape (FwdPlan::family: 1 smem, 2 register weights, 3 cluster, 4 large
-// batch, 5 MV-RNN, 6 bf16 tensor cores), honouring CX_FORWARD_PATH; 0 if none.
+// batch, 5 MV-RNN, 6 bf16 tensor cores, 7 fused single-CTA, 8 split-fp32 tensor
+// cores), honouring CX_FORWARD_PATH; 0 if none.
 int32_t cx_debug_forward_family(const cx_model *m, int32_t n, int32_t max_children) {
   if (!m || n < 1 || max_children < 1) return 0;
   cx::FwdPlan plan;
@@ -397,7 +420,7 @@ int32_t cx_debug_forward_family(const cx_model *m, int32_t n, int32_t max_childr
   std::lock_guard<std::mutex> lk(g_mu);
   const int sms = num_sms_current();
   if (sms <= 0) return 0;
-  return plan_forward(m, max_children, n, false, sms, &plan, &Gn, &Gu) ? plan.family : 0;
+  return plan_forward(m, max_children, n, -1, false, sms, &plan, &Gn, &Gu) ? plan.family : 0;
 }
 
 // Debug only: an empty kernel launch (measures launch overhead).
@@ -433,11 +456,11 @@ cx_status cx_linearize_forward_launch_info(const cx_model *m, int32_t n, int32_t
   std::lock_guard<std::mutex> lk(g_mu);
   const char *env = std::getenv("CX_FUSED");
   bool f = !(env && env[0] == '0') && n > 0 && (forward_path() == 0 || forward_path() == 3) &&
-           plan_forward(m, max_children, n, true, 0, &plan, &Gn, &Gu);
+           plan_forward(m, max_children, n, -1, true, 0, &plan, &Gn, &Gu);
   if (!f) {
     const int sms = num_sms_current();
     if (sms <= 0) return CX_E_CUDA;
-    if (!plan_forward(m, max_children, n > 0 ? n : 1, false, sms, &plan, &Gn, &Gu))
+    if (!plan_forward(m, max_children, n > 0 ? n : 1, -1, false, sms, &plan, &Gn, &Gu))
       return CX_E_UNSUPPORTED;
   }
   if (fused) *fused = f ? 1 : 0;
@@ -456,7 +479,7 @@ cx_status cx_forward_launch_info(const cx_model *m, int32_t *ctas, int32_t *thre
   std::lock_guard<std::mutex> lk(g_mu);
   int sms = num_sms_current();
   if (sms <= 0) return CX_E_CUDA;
-  const bool ok = m->dtype == CX_BF16 ? cx::tc_plan(m->cell, m->hidden, 2, sms, &plan, &Gn, &Gu)
+  const bool ok = m->dtype == CX_BF16 ? cx::tc_plan(m->cell, m->hidden, 2, 1, sms, &plan, &Gn, &Gu)
                                       : cx::fwd_plan(m->cell, m->hidden, 2, 1, forward_path(), sms,
                                                      &plan, &Gn, &Gu);
   if (!ok) return CX_E_UNSUPPORTED;

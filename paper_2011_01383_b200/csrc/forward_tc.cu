@@ -42,6 +42,7 @@
 // used when the batch has more x rows than half the vocabulary) or the batch's
 // own x rows in node order. h_out / aux_out / root_out are written by the
 // epilogue in the caller's numbering.
+#include <cuda_bf16.h>
 #include <cuda.h>  // CUtensorMap types (the encoder is fetched from the driver at run time)
 #include <cuda_runtime.h>
 
@@ -92,12 +93,24 @@ struct TcMeta {
 
 constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 
-template <int CELL, int H, int MAXC>
+// SP = 1: bf16 operands (dtype CX_BF16). SP = 2: the fp32 path on the tensor
+// cores (dtype CX_F32, large batches): every fp32 operand x is split into
+// x_hi = bf16(x) and x_lo = bf16(x - x_hi) (|x - x_hi - x_lo| <= 2^-17 |x|),
+// stored as one bf16 row [hi | lo] of 2H, and each product is formed as
+// A_hi B_hi + A_hi B_lo + A_lo B_hi (three bf16 MMAs, fp32 accumulation in
+// TMEM; the dropped A_lo B_lo term is <= 2^-16 |A B|): fp32-class accuracy on
+// the bf16 tensor pipe, at 3x its MMA work.
+template <int CELL, int H, int MAXC, int SP = 1>
 struct TcCfg {
   static constexpr bool LSTM = CELL == CX_TREELSTM, DAG = CELL == CX_DAGRNN, FC = CELL == CX_TREEFC;
   static constexpr int J = MAXC;
-  static constexpr int U = DAG ? (H >= 128 ? 128 : H) : 32;
-  static constexpr int KA = H / 64;
+  static constexpr int U = DAG ? (SP == 2 ? 64 : (H >= 128 ? 128 : H)) : 32;
+  static constexpr int KA = H / 64;        // K-atoms (64 bf16) of one hi or lo half
+  static constexpr int KAA = SP * KA;      // K-atoms of a gathered operand row (hi [| lo])
+  static constexpr int RW = SP * H;        // bf16 elements per operand row
+  // split TreeLSTM: W_iou (leaf phase) and [U_iou; U_f] (levels) take turns in
+  // one shared-memory region (both at once would not fit with the stages)
+  static constexpr bool BSHARE = LSTM && SP == 2;
   static constexpr int B0 = LSTM ? 3 * U : U;  // rows: LSTM W_iou | DAG W_x | FC W_left
   static constexpr int B1 = LSTM ? 4 * U : U;  // rows: LSTM [U_iou; U_f] | DAG U | FC W_right
   static constexpr int NACC = LSTM ? J : 1;    // accumulators per tile (level phase)
@@ -120,12 +133,13 @@ struct TcCfg {
   static constexpr int META0 = kFeed0 + FEEDW;           // first bookkeeping warp
   static constexpr int THREADS = 32 * (META0 + kMetaWarps);
   static constexpr int WORK = 32 * META0;                // threads of the working warps
-  static constexpr size_t bbytes0 = (size_t)B0 * KA * 128, bbytes1 = (size_t)B1 * KA * 128;
+  static constexpr size_t bbytes0 = (size_t)B0 * KAA * 128, bbytes1 = (size_t)B1 * KAA * 128;
+  static constexpr size_t bregion = BSHARE ? (bbytes0 > bbytes1 ? bbytes0 : bbytes1) : bbytes0 + bbytes1;
   static constexpr size_t static_bytes = sizeof(TcMeta<J>) * kMetaRing + 4 * U * 4 + 64 * 8 + 64;
   static constexpr int S_fit =
-      (int)((kSmemLimit - 1024 - static_bytes - bbytes0 - bbytes1) / kStageBytes);
+      (int)((kSmemLimit - 1024 - static_bytes - bregion) / kStageBytes);
   static constexpr int S = S_fit > 8 ? 8 : S_fit;
-  static constexpr size_t dyn_bytes = 1024 + bbytes0 + bbytes1 + (size_t)S * kStageBytes;
+  static constexpr size_t dyn_bytes = 1024 + bregion + (size_t)S * kStageBytes;
   static_assert(H % 64 == 0 && H % U == 0, "H must be a multiple of 64 and of U");
   static_assert(BUFC * 2 <= 512, "TMEM: two accumulator buffers must fit 512 columns");
   static_assert(NLVL <= 256 && NLEAF <= 256 && NLVL % 16 == 0, "UMMA N");
@@ -218,6 +232,35 @@ __device__ __forceinline__ void st_row_bf16(unsigned short *p, const float (&v)[
   for (int q = 0; q < N / 16; q++) st256_bf16(p + 16 * q, v + 16 * q);
 }
 
+__device__ __forceinline__ float bf16_round(float x) {
+  return __bfloat162float(__float2bfloat16_rn(x));
+}
+// An operand row piece: SP = 1 -> bf16(v) at row[col..]; SP = 2 (split fp32,
+// see TcCfg) -> hi = bf16(v) at row[col..] and lo = bf16(v - hi) at row[H + col..]
+template <int SP, int H, int N>
+__device__ __forceinline__ void st_op(unsigned short *row, int col, const float (&v)[N]) {
+  if constexpr (SP == 1) {
+    st_row_bf16<N>(row + col, v);
+  } else {
+    float hi[N], lo[N];
+#pragma unroll
+    for (int j = 0; j < N; j++) {
+      hi[j] = bf16_round(v[j]);
+      lo[j] = v[j] - hi[j];  // exact in fp32
+    }
+    st_row_bf16<N>(row + col, hi);
+    st_row_bf16<N>(row + H + col, lo);
+  }
+}
+// 8 consecutive fp32 values -> their bf16 hi (and lo) pieces
+__device__ __forceinline__ void split8(float4 a, float4 b, uint4 &hi, uint4 &lo) {
+  hi = f32x8_to_bf16(a, b);
+  const float4 ah = make_float4(bf16_round(a.x), bf16_round(a.y), bf16_round(a.z), bf16_round(a.w));
+  const float4 bh = make_float4(bf16_round(b.x), bf16_round(b.y), bf16_round(b.z), bf16_round(b.w));
+  lo = f32x8_to_bf16(make_float4(a.x - ah.x, a.y - ah.y, a.z - ah.z, a.w - ah.w),
+                     make_float4(b.x - bh.x, b.y - bh.y, b.z - bh.z, b.w - bh.w));
+}
+
 // Gate nonlinearities of the bf16 path: one MUFU op each (tanh.approx.f32,
 // relative error ~2^-11, far inside the bf16 path's 2e-2 budget; the fp32
 // path keeps the ex2/rcp forms of common.cuh).
@@ -227,6 +270,16 @@ __device__ __forceinline__ float tanh_mufu(float x) {
   return y;
 }
 __device__ __forceinline__ float sigm_mufu(float x) { return fmaf(0.5f, tanh_mufu(0.5f * x), 0.5f); }
+// per path: the bf16 path's MUFU forms, the split fp32 path's those of the fp32
+// kernels (common.cuh, within ~5e-6 relative)
+template <int SP>
+__device__ __forceinline__ float act_sig(float x) {
+  if constexpr (SP == 1) return sigm_mufu(x); else return sigmoidf_(x);
+}
+template <int SP>
+__device__ __forceinline__ float act_tanh(float x) {
+  if constexpr (SP == 1) return tanh_mufu(x); else return tanhf_(x);
+}
 
 
 // debug timeline (cx_debug_set_trace): thread `who` of each CTA records
@@ -240,13 +293,13 @@ __device__ __forceinline__ void tc_mark(const FwdArgs &a, int s, int who) {
   }
 }
 
-template <int CELL, int H, int MAXC>
-__global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
+template <int CELL, int H, int MAXC, int SP>
+__global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
     tc_kernel(const __grid_constant__ TcArgs ta) {
   const FwdArgs &a = ta.f;
-  using C = TcCfg<CELL, H, MAXC>;
+  using C = TcCfg<CELL, H, MAXC, SP>;
   constexpr int kMeta0 = C::META0, kWork = C::WORK;
-  constexpr int J = C::J, U = C::U, KA = C::KA, S = C::S;
+  constexpr int J = C::J, U = C::U, KA = C::KA, KAA = C::KAA, RW = C::RW, S = C::S;
   extern __shared__ unsigned char smem_raw[];
   __shared__ TcMeta<J> meta[kMetaRing];
   __shared__ float s_bias[4 * U];
@@ -262,7 +315,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
   const bool latch = gu == 0;
   unsigned char *sm = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  unsigned char *sB0 = sm, *sB1 = sm + C::bbytes0, *sStage = sB1 + C::bbytes1;
+  unsigned char *sB0 = sm, *sB1 = C::BSHARE ? sm : sm + C::bbytes0, *sStage = sm + C::bregion;
   unsigned short *hb = a.hb;
   float *cs = a.cs;
   const unsigned short *xb = a.xb;
@@ -285,15 +338,18 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
   } else {
     for (int q = tid; q < U; q += blockDim.x) s_bias[q] = __ldg(a.w[C::DAG ? 2 : 1] + unit0 + q);
   }
-  // weights: B0 / B1 rows -> bf16, K-major SW128; 8 chunks' loads in flight
-  // per thread before their conversions and stores
-  {
-    constexpr int NCH = (C::B0 + C::B1) * KA * 8;
+  // weights: B0 / B1 rows -> bf16 (SP = 2: hi atoms [0, KA), lo atoms
+  // [KA, 2 KA)), K-major SW128; 8 chunks' loads in flight per thread before
+  // their conversions and stores. sel: 0 both, 1 B0 only, 2 B1 only (BSHARE)
+  auto load_b = [&](int sel, int nthr) {
+    const int r0 = sel == 2 ? C::B0 : 0, r1 = sel == 1 ? C::B0 : C::B0 + C::B1;
+    const int NCH = (r1 - r0) * KA * 8;
     auto wsrc = [&](int idx, unsigned char *&Bm, int &rows, int &q, int &ka, int &c) -> const float * {
       q = idx / (KA * 8);
       const int rem = idx - q * (KA * 8);
       ka = rem >> 3;
       c = rem & 7;
+      q += r0;
       const bool second = q >= C::B0;
       if (second) q -= C::B0;
       Bm = second ? sB1 : sB0;
@@ -309,11 +365,11 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
         return a.w[0] + (size_t)(unit0 + q) * 2 * H + (second ? H : 0);              // W [H][2H]
       }
     };
-    for (int base = 0; base < NCH; base += 8 * (int)blockDim.x) {
+    for (int base = 0; base < NCH; base += 8 * nthr) {
       float4 lo[8], hi[8];
 #pragma unroll
       for (int e = 0; e < 8; e++) {
-        const int idx = base + e * blockDim.x + tid;
+        const int idx = base + e * nthr + tid;
         if (idx < NCH) {
           unsigned char *Bm;
           int rows, q, ka, c;
@@ -325,16 +381,24 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
       }
 #pragma unroll
       for (int e = 0; e < 8; e++) {
-        const int idx = base + e * blockDim.x + tid;
+        const int idx = base + e * nthr + tid;
         if (idx < NCH) {
           unsigned char *Bm;
           int rows, q, ka, c;
           (void)wsrc(idx, Bm, rows, q, ka, c);
-          *reinterpret_cast<uint4 *>(Bm + (size_t)ka * rows * 128 + sw128_off(q, c)) = f32x8_to_bf16(lo[e], hi[e]);
+          if constexpr (SP == 1) {
+            *reinterpret_cast<uint4 *>(Bm + (size_t)ka * rows * 128 + sw128_off(q, c)) = f32x8_to_bf16(lo[e], hi[e]);
+          } else {
+            uint4 ph, pl;
+            split8(lo[e], hi[e], ph, pl);
+            *reinterpret_cast<uint4 *>(Bm + (size_t)ka * rows * 128 + sw128_off(q, c)) = ph;
+            *reinterpret_cast<uint4 *>(Bm + (size_t)(ka + KA) * rows * 128 + sw128_off(q, c)) = pl;
+          }
         }
       }
     }
-  }
+  };
+  load_b(C::BSHARE ? 1 : 0, (int)blockDim.x);
 
   tc_mark(a, 60, 0);
   // the linearization is read from here on (PDL: the above overlapped it)
@@ -367,7 +431,17 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 4; e++) {
           const size_t idx = b0 + e * total_threads;
-          if (idx < total) *reinterpret_cast<uint4 *>(xw + idx * 8) = f32x8_to_bf16(lo[e], hi[e]);
+          if (idx < total) {
+            if constexpr (SP == 1) {
+              *reinterpret_cast<uint4 *>(xw + idx * 8) = f32x8_to_bf16(lo[e], hi[e]);
+            } else {  // row idx / q8, columns 8 (idx % q8): hi, then lo at + H
+              const size_t o = (idx / q8) * RW + (idx % q8) * 8;
+              uint4 ph, pl;
+              split8(lo[e], hi[e], ph, pl);
+              *reinterpret_cast<uint4 *>(xw + o) = ph;
+              *reinterpret_cast<uint4 *>(xw + o + H) = pl;
+            }
+          }
         }
       }
       if (hoist) {  // state row of every node: leaves -> their word's row
@@ -396,7 +470,14 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
           w = 0;
         }
         const float4 *s = reinterpret_cast<const float4 *>(a.emb + (size_t)w * H + c * 8);
-        *reinterpret_cast<uint4 *>(xw + (size_t)r * H + c * 8) = f32x8_to_bf16(__ldg(s), __ldg(s + 1));
+        if constexpr (SP == 1) {
+          *reinterpret_cast<uint4 *>(xw + (size_t)r * H + c * 8) = f32x8_to_bf16(__ldg(s), __ldg(s + 1));
+        } else {
+          uint4 ph, pl;
+          split8(__ldg(s), __ldg(s + 1), ph, pl);
+          *reinterpret_cast<uint4 *>(xw + (size_t)r * RW + c * 8) = ph;
+          *reinterpret_cast<uint4 *>(xw + (size_t)r * RW + H + c * 8) = pl;
+        }
       }
     }
   }
@@ -447,8 +528,9 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
         }
       }
       const int cnt = min(32, nleaf - j0);
-      if (slot_fill) {  // bf16 rows: H/16 lanes x 32 B per row, 32/(H/16) rows per pass
-        constexpr int LPR = H / 16, RPP = 32 / LPR;
+      if (slot_fill) {  // bf16 rows: RW/16 lanes x 32 B per row, 32/(RW/16) rows per pass
+        constexpr int LPR = RW / 16 > 32 ? 32 : RW / 16, RPP = 32 / LPR;  // (hoisting: TreeLSTM only)
+        static_assert(!C::LSTM || RW / 16 <= 32, "one warp per operand row");
         for (int k0 = 0; k0 < cnt; k0 += 8 * RPP) {
           float v[8][8];
           int dk[8];
@@ -459,11 +541,11 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
             dk[u] = __shfl_sync(0xffffffffu, dst, kk);
             const int wk = __shfl_sync(0xffffffffu, w, kk);
             if (k >= cnt) dk[u] = -1;
-            ld256(reinterpret_cast<const float *>(hb + (size_t)wk * H) + 8 * (lane % LPR), v[u]);
+            ld256(reinterpret_cast<const float *>(hb + (size_t)wk * RW) + 8 * (lane % LPR), v[u]);
           }
 #pragma unroll
           for (int u = 0; u < 8; u++)
-            if (dk[u] >= 0) st256(reinterpret_cast<float *>(a.pb + (size_t)dk[u] * H) + 8 * (lane % LPR), v[u]);
+            if (dk[u] >= 0) st256(reinterpret_cast<float *>(a.pb + (size_t)dk[u] * RW) + 8 * (lane % LPR), v[u]);
         }
       } else {  // fp32 rows: H/8 lanes x 32 B per row
         constexpr int LPR = H / 8 > 32 ? 32 : H / 8, CPL = H / 8 / LPR, RPP = 32 / LPR;
@@ -636,16 +718,21 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
     for (int l = 0; l < L; l++) {
       const bool leaf = l == 0;
       if (l > 0) level_sync();
+      if (C::BSHARE && l == 1) {  // the leaf phase's MMAs are complete: B1 replaces B0
+        load_b(2, kWork);
+        fence_proxy_async();
+        named_bar(3, kWork);
+      }
       if (C::LSTM && discard_ok && l >= 2) {
         // level l - 1 is complete: its tiles' parent-slot operand rows (rows
         // k n + [lbeg, lbeg + lsize) of pb, loaded by every unit-group CTA) are
         // dead; every CTA drops a share of their 128-byte lines
         const int lb = __ldg(a.lbeg + l - 1), ls = __ldg(a.lsize + l - 1);
-        constexpr int LPR = H * 2 / 128;  // lines per bf16 row
+        constexpr int LPR = RW * 2 / 128;  // lines per operand row
         const long long total = (long long)J * ls * LPR;
         for (long long e = (long long)blockIdx.x * kWork + tid; e < total; e += (long long)gridDim.x * kWork) {
           const int k = (int)(e / ((long long)ls * LPR)), rem = (int)(e % ((long long)ls * LPR));
-          discard_l2(a.pb + ((size_t)k * n + lb + rem / LPR) * H + (rem % LPR) * 64);
+          discard_l2(a.pb + ((size_t)k * n + lb + rem / LPR) * RW + (rem % LPR) * 64);
         }
       }
       if (l == 1 && hoist) {  // the word table is complete: fill the leaves' parent slots
@@ -668,8 +755,14 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
             }
             const float4 v = __ldg(reinterpret_cast<const float4 *>(a.emb + (size_t)w * H + unit0) + c);
             *reinterpret_cast<float4 *>(a.h_out + (size_t)own * H + unit0 + 4 * c) = v;
-            *reinterpret_cast<uint2 *>(hb + (size_t)i * H + unit0 + 4 * c) =
+            *reinterpret_cast<uint2 *>(hb + (size_t)i * RW + unit0 + 4 * c) =
                 make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+            if constexpr (SP == 2) {
+              const float4 l4 = make_float4(v.x - bf16_round(v.x), v.y - bf16_round(v.y),
+                                            v.z - bf16_round(v.z), v.w - bf16_round(v.w));
+              *reinterpret_cast<uint2 *>(hb + (size_t)i * RW + H + unit0 + 4 * c) =
+                  make_uint2(pack_bf16(l4.x, l4.y), pack_bf16(l4.z, l4.w));
+            }
             if (a.root_out) {
               const int r = __ldg(a.sid + i);
               if (__ldg(a.roots + r) == i)
@@ -691,7 +784,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
         uint32_t Sg = Sg0;
         for (int t = 0; t < ntiles; t++) {
           const int i0 = lo + t * kTM;
-          for (int ka = 0; ka < KA; ka++) {
+          for (int ka = 0; ka < KAA; ka++) {
             for (int s = 0; s < nsl; s++) {
               int src, bm, acc;
               C::slot(leaf, s, src, bm, acc);
@@ -728,7 +821,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
           const int ms = TT % kMetaRing;
           mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
           const TcMeta<J> &m = meta[ms];
-          for (int ka = 0; ka < KA; ka++) {
+          for (int ka = 0; ka < KAA; ka++) {
             for (int s = 0; s < nsl; s++) {
               int src, bm, acc;
               C::slot(leaf, s, src, bm, acc);
@@ -742,7 +835,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
                 const int q = p + FT * e, r = q >> 3, c = q & 7;
                 const int row = rows[r];
                 const bool valid = row >= 0;
-                cp16_zfill(dst0 + sw128_off(r, c), base + (size_t)(valid ? row : 0) * H + ka * 64 + c * 8,
+                cp16_zfill(dst0 + sw128_off(r, c), base + (size_t)(valid ? row : 0) * RW + ka * 64 + c * 8,
                            valid);
               }
               mbar_arrive_cpasync(&bar_full[st]);
@@ -763,7 +856,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
             const int tslot = (l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
             tc_mark(a, tslot + 2, kMmaWarp * 32);
             uint32_t started = 0;
-            for (int ka = 0; ka < KA; ka++) {
+            for (int ka = 0; ka < KAA; ka++) {
               for (int s = 0; s < nsl; s++) {
                 int src, bm, acc;
                 C::slot(leaf, s, src, bm, acc);
@@ -775,12 +868,22 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
                 if (!C::LSTM) fence_proxy_async();  // landed cp.async data (generic proxy) -> tensor core
                 fence_after();
                 const uint32_t a0 = smem_u32(sStage + (size_t)st * kStageBytes);
-                const uint32_t b0 = smem_u32((bm ? sB1 : sB0) + (size_t)ka * (bm ? C::B1 : C::B0) * 128);
+                const size_t brows = bm ? C::B1 : C::B0;
+                unsigned char *bbase = bm ? sB1 : sB0;
+                // SP = 2: a hi atom (ka < KA) meets B_hi and B_lo, a lo atom B_hi
+                const int kb = ka < KA ? ka : ka - KA;
+                const uint32_t b0 = smem_u32(bbase + (size_t)kb * brows * 128);
                 const uint32_t d = tmem + buf * C::BUFC + acc * ncol;
   #pragma unroll
                 for (int kk = 0; kk < 4; kk++) {
                   const uint32_t accum = ((started >> acc) & 1u) | (kk > 0 ? 1u : 0u);
                   mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, accum);
+                }
+                if (SP == 2 && ka < KA) {
+                  const uint32_t b1 = smem_u32(bbase + (size_t)(kb + KA) * brows * 128);
+  #pragma unroll
+                  for (int kk = 0; kk < 4; kk++)
+                    mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b1 + kk * 32), idesc, 1u);
                 }
                 started |= 1u << acc;
                 mma_commit_mc(&bar_empty[st], (uint16_t)((1u << C::CL) - 1));  // frees the slot cluster-wide
@@ -836,10 +939,10 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
               tmem_ld<16>(tb + 0, v);        // i
               tmem_ld<16>(tb + 2 * U, w);    // u
   #pragma unroll
-              for (int j = 0; j < 16; j++) c[j] = sigm_mufu(v[j] + bi[j]) * tanh_mufu(w[j] + bu[j]);
+              for (int j = 0; j < 16; j++) c[j] = act_sig<SP>(v[j] + bi[j]) * act_tanh<SP>(w[j] + bu[j]);
               tmem_ld<16>(tb + U, v);        // o
   #pragma unroll
-              for (int j = 0; j < 16; j++) h[j] = sigm_mufu(v[j] + bo[j]) * tanh_mufu(c[j]);
+              for (int j = 0; j < 16; j++) h[j] = act_sig<SP>(v[j] + bo[j]) * act_tanh<SP>(c[j]);
             } else {
   #pragma unroll
               for (int j = 0; j < 16; j++) c[j] = 0.f;
@@ -848,7 +951,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
                 tmem_ld<16>(tb + k * NL + 3 * U, v);
                 if (ck[k] >= 0) {
   #pragma unroll
-                  for (int j = 0; j < 16; j++) c[j] = fmaf(sigm_mufu(v[j] + bf[j]), cp[k][j], c[j]);
+                  for (int j = 0; j < 16; j++) c[j] = fmaf(act_sig<SP>(v[j] + bf[j]), cp[k][j], c[j]);
                 }
               }
               tmem_ld<16>(tb + 0, v);        // i = sum_k acc_k[i], u = sum_k acc_k[u]
@@ -867,7 +970,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
                 }
               }
   #pragma unroll
-              for (int j = 0; j < 16; j++) c[j] = fmaf(sigm_mufu(v[j] + bi[j]), tanh_mufu(w[j] + bu[j]), c[j]);
+              for (int j = 0; j < 16; j++) c[j] = fmaf(act_sig<SP>(v[j] + bi[j]), act_tanh<SP>(w[j] + bu[j]), c[j]);
               tmem_ld<16>(tb + U, v);        // o
   #pragma unroll
               for (int k = 1; k < J; k++) {
@@ -878,13 +981,14 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
                 }
               }
   #pragma unroll
-              for (int j = 0; j < 16; j++) h[j] = sigm_mufu(v[j] + bo[j]) * tanh_mufu(c[j]);
+              for (int j = 0; j < 16; j++) h[j] = act_sig<SP>(v[j] + bo[j]) * act_tanh<SP>(c[j]);
             }
             if (valid) {
               const bool wordrow = leaf && hoist;  // hoisted leaf cell: row i = word i
-              const size_t ui = (size_t)(wordrow ? i : sbase + i) * H + unit0 + u0;
-              if (wordrow) st_row_bf16<16>(hb + ui, h);  // the word table (copied to slots below)
-              else if (m.ps[r] >= 0) st_row_bf16<16>(a.pb + (size_t)m.ps[r] * H + unit0 + u0, h);
+              const size_t rowi = (size_t)(wordrow ? i : sbase + i);
+              const size_t ui = rowi * H + unit0 + u0;
+              if (wordrow) st_op<SP, H, 16>(hb + rowi * RW, unit0 + u0, h);  // the word table (copied to slots below)
+              else if (m.ps[r] >= 0) st_op<SP, H, 16>(a.pb + (size_t)m.ps[r] * RW, unit0 + u0, h);
               st_row<16>(cs + ui, c);
               if (wordrow) {
                 st_row<16>(a.hf + (size_t)i * H + unit0 + u0, h);
@@ -905,11 +1009,11 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
               float v[CW];
               tmem_ld<CW>(tb + q * CW, v);
   #pragma unroll
-              for (int j = 0; j < CW; j++) v[j] = tanh_mufu(v[j] + s_bias[u0 + q * CW + j]);
+              for (int j = 0; j < CW; j++) v[j] = act_tanh<SP>(v[j] + s_bias[u0 + q * CW + j]);
               if (valid) {
                 const int uu = unit0 + u0 + q * CW;
                 st_row_cs<CW>(a.h_out + (size_t)own * H + uu, v);
-                st_row_bf16<CW>(hb + (size_t)i * H + uu, v);
+                st_op<SP, H, CW>(hb + (size_t)i * RW, uu, v);
                 if (root >= 0) st_row_cs<CW>(a.root_out + (size_t)root * H + uu, v);
               }
             }
@@ -922,7 +1026,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
         tc_mark(a, 5 + 4 * l, 0);
       }
       T0 += ntiles;
-      Sg0 += (uint32_t)ntiles * KA * nsl;
+      Sg0 += (uint32_t)ntiles * KAA * nsl;
     }
 
     if (hoist && L > 0) {  // leaves' caller outputs (the table is complete since level 1)
@@ -948,11 +1052,11 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC>::THREADS, 1)
   publish_and_exit(a);
 }
 
-template <int CELL, int H, int MAXC>
+template <int CELL, int H, int MAXC, int SP>
 bool tc_plan_one(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
-  using C = TcCfg<CELL, H, MAXC>;
+  using C = TcCfg<CELL, H, MAXC, SP>;
   static_assert(C::S >= 2, "at least two pipeline stages");
-  auto k = tc_kernel<CELL, H, MAXC>;
+  auto k = tc_kernel<CELL, H, MAXC, SP>;
   // per-device caches (attributes and occupancy are per device context)
   static bool set[kMaxDevices];
   static int max_clusters_dev[kMaxDevices];
@@ -995,43 +1099,50 @@ bool tc_plan_one(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   p->smem = C::dyn_bytes;
   p->kernel = (const void *)k;
   p->cluster = C::CL;
-  p->family = 6;
+  p->family = SP == 2 ? 8 : 6;
   p->big = false;
   p->tc = true;
+  p->tc_sp = SP;
   return true;
 }
 
-template <int CELL, int H>
+template <int CELL, int H, int SP>
 bool tc_plan_c(int maxc, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   if constexpr (CELL == CX_TREEFC) {
-    return maxc == 2 && tc_plan_one<CELL, H, 2>(num_sms, p, Gn, Gu);
+    return maxc == 2 && tc_plan_one<CELL, H, 2, SP>(num_sms, p, Gn, Gu);
   } else {
-    if (maxc == 1) return tc_plan_one<CELL, H, 1>(num_sms, p, Gn, Gu);
-    if (maxc == 2) return tc_plan_one<CELL, H, 2>(num_sms, p, Gn, Gu);
+    if (maxc == 1) return tc_plan_one<CELL, H, 1, SP>(num_sms, p, Gn, Gu);
+    if (maxc == 2) return tc_plan_one<CELL, H, 2, SP>(num_sms, p, Gn, Gu);
     return false;
   }
+}
+template <int SP>
+bool tc_plan_sp(int cell, int H, int maxc, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
+  switch (cell) {
+    case CX_TREELSTM:
+      if (H == 256) return tc_plan_c<CX_TREELSTM, 256, SP>(maxc, num_sms, p, Gn, Gu);
+      if (H == 128) return tc_plan_c<CX_TREELSTM, 128, SP>(maxc, num_sms, p, Gn, Gu);
+      return false;
+    case CX_DAGRNN:
+      if (H == 256) return tc_plan_c<CX_DAGRNN, 256, SP>(maxc, num_sms, p, Gn, Gu);
+      if (H == 128) return tc_plan_c<CX_DAGRNN, 128, SP>(maxc, num_sms, p, Gn, Gu);
+      return false;
+    case CX_TREEFC:
+      if (H == 512) return tc_plan_c<CX_TREEFC, 512, SP>(maxc, num_sms, p, Gn, Gu);
+      if (H == 256) return tc_plan_c<CX_TREEFC, 256, SP>(maxc, num_sms, p, Gn, Gu);
+      return false;
+  }
+  return false;
 }
 
 }  // namespace
 
-// bf16 tensor-core path: TreeLSTM / DAG-RNN H in {128, 256}, TreeFC H in {256, 512};
-// max_children <= 2 (TMEM holds two accumulator buffers of max_children x 4U columns).
-bool tc_plan(int cell, int H, int maxc, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
-  switch (cell) {
-    case CX_TREELSTM:
-      if (H == 256) return tc_plan_c<CX_TREELSTM, 256>(maxc, num_sms, p, Gn, Gu);
-      if (H == 128) return tc_plan_c<CX_TREELSTM, 128>(maxc, num_sms, p, Gn, Gu);
-      return false;
-    case CX_DAGRNN:
-      if (H == 256) return tc_plan_c<CX_DAGRNN, 256>(maxc, num_sms, p, Gn, Gu);
-      if (H == 128) return tc_plan_c<CX_DAGRNN, 128>(maxc, num_sms, p, Gn, Gu);
-      return false;
-    case CX_TREEFC:
-      if (H == 512) return tc_plan_c<CX_TREEFC, 512>(maxc, num_sms, p, Gn, Gu);
-      if (H == 256) return tc_plan_c<CX_TREEFC, 256>(maxc, num_sms, p, Gn, Gu);
-      return false;
-  }
-  return false;
+// Tensor-core path: TreeLSTM / DAG-RNN H in {128, 256}, TreeFC H in {256, 512};
+// max_children <= 2 (TMEM holds two accumulator buffers of max_children x 4U
+// columns). sp = 1: bf16 operands; sp = 2: split fp32 operands (TcCfg).
+bool tc_plan(int cell, int H, int maxc, int sp, int num_sms, FwdPlan *p, int *Gn, int *Gu) {
+  return sp == 2 ? tc_plan_sp<2>(cell, H, maxc, num_sms, p, Gn, Gu)
+                 : tc_plan_sp<1>(cell, H, maxc, num_sms, p, Gn, Gu);
 }
 
 // ---- launch: tensor maps of the gathered operands + cooperative launch --------
@@ -1075,9 +1186,10 @@ cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &f, cudaStream_t stream
   std::memset(&ta, 0, sizeof ta);
   ta.f = f;
   const long long xrows = f.xmode ? f.n : f.V;
-  if (f.pb) {  // TreeLSTM: contiguous operands, 128-row tile loads
-    if (!encode_rows(&ta.tm_p, f.pb, f.H, 2LL * f.n, kTM)) return cudaErrorInvalidValue;
-    if (!encode_rows(&ta.tm_x, f.xb, f.H, xrows, kTM)) return cudaErrorInvalidValue;
+  if (f.pb) {  // TreeLSTM: contiguous operands, 128-row tile loads of rows of sp x H bf16
+    const int rw = plan.tc_sp * f.H;
+    if (!encode_rows(&ta.tm_p, f.pb, rw, 2LL * f.n, kTM)) return cudaErrorInvalidValue;
+    if (!encode_rows(&ta.tm_x, f.xb, rw, xrows, kTM)) return cudaErrorInvalidValue;
   }
   void *params[] = {&ta};
   cudaLaunchConfig_t cfg = {};
@@ -1115,16 +1227,18 @@ size_t tc_state_rows(int cell, int n, int V) {
   return (size_t)(n > 0 ? n : 1) + (tc_hoist(cell, n, V) ? (size_t)V : 0);
 }
 
-// workspace bytes of the tensor-core path (after the GridBar); tc_carve() in
-// api.cu lays the buffers out in this order
-size_t tc_workspace_bytes(int cell, int H, int V, int n) {
+// workspace bytes of the tensor-core path (after the GridBar); forward_impl in
+// api.cu lays the buffers out in this order. Operand rows (hb, xb, pb) hold
+// sp x H bf16 (sp = 2: the split fp32 path).
+size_t tc_workspace_bytes(int cell, int H, int V, int n, int sp) {
   const size_t N = (size_t)(n > 0 ? n : 1), h = (size_t)H, R = tc_state_rows(cell, n, V);
-  size_t b = 2 * R * h + 256;                                   // hb
+  const size_t rw = h * (sp == 2 ? 2 : 1);                     // bf16 per operand row
+  size_t b = 2 * R * rw + 256;                                  // hb
   if (cell == CX_TREELSTM) b += 4 * R * h + 256;                // cs
   if (cell == CX_TREELSTM || cell == CX_DAGRNN)                 // xb
-    b += 2 * (tc_xmode(n, V) ? N : (size_t)V) * h + 256;
+    b += 2 * (tc_xmode(n, V) ? N : (size_t)V) * rw + 256;
   if (tc_hoist(cell, n, V)) b += 4 * (size_t)V * h + 4 * N + 512;  // hf, crow
-  if (cell == CX_TREELSTM) b += 2 * (2 * N) * h + 4 * N + 512;     // pb (J <= 2), pslot
+  if (cell == CX_TREELSTM) b += 2 * (2 * N) * rw + 4 * N + 512;    // pb (J <= 2), pslot
   return b;
 }
 

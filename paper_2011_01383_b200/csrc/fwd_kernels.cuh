@@ -84,9 +84,10 @@ struct FwdPlan {
   // kernel family (reporting / tests): 1 smem weights (forward.cu), 2 register
   // weights (forward_rw.cu), 3 cluster (forward_cluster.cu), 4 large-batch
   // (forward_big.cu), 5 MV-RNN, 6 bf16 tensor cores (forward_tc.cu), 7 fused
-  // single-CTA (forward_single.cu)
+  // single-CTA (forward_single.cu), 8 split-fp32 tensor cores (forward_tc.cu)
   int family = 0;
   bool bf16ops = false;  // dtype CX_BF16 served by an FMA kernel with bf16-rounded operands
+  int tc_sp = 1;         // tensor-core kernel operands: 1 bf16, 2 split fp32 (hi + lo bf16)
 };
 
 // Returns false (CX_E_UNSUPPORTED) when no instantiation covers the model.
@@ -99,9 +100,10 @@ bool fwd_plan(int cell, int H, int maxc, int n, int path, int num_sms, FwdPlan *
               int *Gu);
 size_t fwd_workspace_bytes(int cell, int H, int n, int V);
 // bf16 tensor-core path (forward_tc.cu)
-bool tc_plan(int cell, int H, int maxc, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
+// sp = 1 bf16 operands (dtype CX_BF16); sp = 2 split fp32 operands (dtype CX_F32)
+bool tc_plan(int cell, int H, int maxc, int sp, int num_sms, FwdPlan *plan, int *Gn, int *Gu);
 int tc_xmode(int n, int V);
-size_t tc_workspace_bytes(int cell, int H, int V, int n);
+size_t tc_workspace_bytes(int cell, int H, int V, int n, int sp);
 cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &args, cudaStream_t stream);
 bool tc_hoist(int cell, int n, int V);
 size_t tc_state_rows(int cell, int n, int V);

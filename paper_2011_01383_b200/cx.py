@@ -294,7 +294,8 @@ def diag_sync_cycles(kind: int, levels: int, device=None) -> int:
     return int(out[0].item())
 
 
-FAMILIES = {1: "smem", 2: "rw", 3: "cluster", 4: "big", 5: "mvrnn", 6: "tc"}
+FAMILIES = {1: "smem", 2: "rw", 3: "cluster", 4: "big", 5: "mvrnn", 6: "tc", 7: "single",
+            8: "tc32"}
 
 
 def forward_family(cell, hidden, n, max_children, vocab=1, dtype=F32):

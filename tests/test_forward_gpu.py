@@ -112,7 +112,7 @@ def test_baseline_configs(cx, name, path):
 
 
 @pytest.mark.parametrize("name", ["cfg5_treelstm_b4096", "cfg5_dagrnn_b4096"])
-@pytest.mark.parametrize("fpath", ["auto", "smem"])
+@pytest.mark.parametrize("fpath", ["auto", "smem", "big"])
 def test_batch4096_sampled(cx, name, fpath, monkeypatch):
     """Full-size launch (the bench configuration); oracle on 64 sampled
     structures (their roots and everything below them)."""
@@ -122,7 +122,8 @@ def test_batch4096_sampled(cx, name, fpath, monkeypatch):
         monkeypatch.setenv("CX_FORWARD_PATH", fpath)
     w = synth.workload(name)
     ch, cell, H, V = w["children"], w["cell"], w["hidden"], w["vocab"]
-    assert cx.forward_family(cell, H, ch.shape[1], ch.shape[0], V) == ("big" if fpath == "auto"
+    # automatic: the split-fp32 tensor-core kernel (test_forward_tc32_gpu.py)
+    assert cx.forward_family(cell, H, ch.shape[1], ch.shape[0], V) == ("tc32" if fpath == "auto"
                                                                        else fpath)
     words, emb = w["words"], synth.embedding(V, H, w["seed"])
     ws_np, ws_dev = weights_dev(cell, H, V)
