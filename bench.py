@@ -135,16 +135,20 @@ def algorithmic_work(cell, H, n, n_leaves, n_internal, batch, maxc=2, vocab=None
     return flops, bytes_, performed
 
 
-def hoisting_applies(cell, n, n_leaves, vocab, dtype_name, fused):
-    """Whether the forward evaluates the leaf cell / projection per word
-    (forward_tc.cu tc_hoist, forward_big.cu): batches with more leaves
-    (DAG-RNN: nodes) than V / 2 on the large-batch paths."""
+def hoisting_applies(cell, n, n_leaves, vocab, family, fused):
+    """Whether the forward evaluates the leaf cell / projection per word:
+    the tensor-core kernels (forward_tc.cu tc_hoist: TreeLSTM with 2n > V) and
+    the fp32 large-batch kernel (forward_big.cu: more leaves, DAG-RNN nodes,
+    than V / 2)."""
     if fused:
         return False
-    if cell == synth.TREELSTM:
-        return n_leaves > vocab // 2 and (dtype_name == "bf16" or n > 32768)
-    if cell == synth.DAGRNN:
-        return n > vocab and (dtype_name == "f32" and n > 32768)
+    if family in ("tc", "tc32"):
+        return cell == synth.TREELSTM and 2 * n > vocab
+    if family == "big":
+        if cell == synth.TREELSTM:
+            return n_leaves > vocab // 2
+        if cell == synth.DAGRNN:
+            return n > vocab
     return False
 
 
@@ -677,7 +681,8 @@ def run_gpu(args, rank, world, local_rank):
     # the dominant kernel: the fused kernel (= the whole step) or cx_forward's
     step_mean = sum(step_ms) / len(step_ms)
     fwd_mean = step_mean if fused else sum(fwd_ms) / len(fwd_ms)
-    hoisted = hoisting_applies(cell, n, n_leaves, V, args.dtype, fused)
+    family = "fused" if fused else cx.forward_family(cell, H, n, ch_np.shape[0], V, dtype)
+    hoisted = hoisting_applies(cell, n, n_leaves, V, family, fused)
     flops, alg_bytes, performed = algorithmic_work(cell, H, n, n_leaves, n - n_leaves, R,
                                                    ch_np.shape[0], vocab=V, hoisted=hoisted)
     achieved = flops / (fwd_mean / 1e3) / 1e12
@@ -703,15 +708,21 @@ def run_gpu(args, rank, world, local_rank):
         sync_kind = 2
     cp = critical_path(L, 1 if fused else 2, sync_kind, sm_mhz, dev)
     step_us = step_mean * 1e3
-    if args.dtype == "bf16":
+    if family in ("tc", "tc32"):
         peak, src = (peaks["bf16_tflops"], "MEASURED_PEAKS.json bf16_tflops (burst)") if peaks \
             else (2250.0, "B200 nominal dense bf16 (MEASURED_PEAKS.json absent)")
-        compute_floor = performed / (peak * 1e12) * 1e6
+        # tc32 (fp32 on the tensor cores): three bf16 MMAs per fp32 product
+        # (hi.hi + hi.lo + lo.hi), so its floor is 3x the algorithmic work
+        mma_per_product = 3 if family == "tc32" else 1
+        compute_floor = mma_per_product * performed / (peak * 1e12) * 1e6
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": traffic,
-                    "kernel": "tc_kernel (cx_forward, dtype bf16)",
-                    "note": f"peak = {src}; algorithmic flops (SURVEY 8(d)), not the MMA's "
-                            "(child-sum by linearity issues 16H^2 per TreeLSTM node)"}
+                    "kernel": f"tc_kernel (cx_forward, {'split fp32' if family == 'tc32' else 'bf16'}"
+                              " operands)",
+                    "bf16_mma_per_product": mma_per_product,
+                    "note": f"peak = {src} (the bf16 pipe the MMAs run on); algorithmic flops "
+                            "(SURVEY 8(d)), not the MMA's (child-sum by linearity issues 16H^2 "
+                            "per TreeLSTM node)"}
     else:
         compute_floor = performed / (FMA_PEAK_TFLOPS * 1e12) * 1e6
         roofline = {"bound": "alu", "achieved": achieved, "peak": FMA_PEAK_TFLOPS,
@@ -752,7 +763,7 @@ def run_gpu(args, rank, world, local_rank):
                   "two_launch_latency_us time the separate cx_linearize and cx_forward launches",
         "gpu_launches": (1 if fused else 2) * args.steps,
         "allgather_roots_us": allgather_us,
-        "launch": info,
+        "launch": dict(info, family=family),
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,

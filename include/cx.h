@@ -102,7 +102,10 @@ typedef struct {
 
 /* Bytes of device workspace cx_linearize needs for (n, max_children). The
  * workspace must be zero-filled before its first use; every call leaves its
- * synchronisation words zero again, so it can be reused without clearing. */
+ * synchronisation words zero again, so it can be reused without clearing by
+ * calls with the same shape arguments (n, max_children and, for the forward
+ * calls, the model). The words' offsets depend on those arguments: a workspace
+ * reused for another shape must be zero-filled again first. */
 size_t cx_linearize_workspace_bytes(int32_t n, int32_t max_children);
 
 /* Linearize a batch (forest) of structures.

@@ -57,6 +57,17 @@ namespace {
 using namespace fwd;
 using namespace umma;
 
+// measurement knobs (tools/build_variant.sh): W_iou / [U_iou; U_f] sharing one
+// region on the bf16 path too (more stages), and the stage-count cap
+#ifndef CX_TC_BSHARE_ALL
+#define CX_TC_BSHARE_ALL 0
+#endif
+#ifndef CX_TC_SKIP_LO  // timing experiment only: drop the A_hi B_lo MMAs (wrong numerics)
+#define CX_TC_SKIP_LO 0
+#endif
+#ifndef CX_TC_SMAX
+#define CX_TC_SMAX 8
+#endif
 constexpr int kTM = 128;                    // tile rows = UMMA M
 // warps 0-7: epilogue (warp w reads TMEM lane quadrant w % 4 = tile rows
 // 32(w%4)..+31, column half w / 4); warp 8: MMA issuer; warps 9..: operand
@@ -110,7 +121,7 @@ struct TcCfg {
   static constexpr int RW = SP * H;        // bf16 elements per operand row
   // split TreeLSTM: W_iou (leaf phase) and [U_iou; U_f] (levels) take turns in
   // one shared-memory region (both at once would not fit with the stages)
-  static constexpr bool BSHARE = LSTM && SP == 2;
+  static constexpr bool BSHARE = LSTM && (SP == 2 || CX_TC_BSHARE_ALL);
   static constexpr int B0 = LSTM ? 3 * U : U;  // rows: LSTM W_iou | DAG W_x | FC W_left
   static constexpr int B1 = LSTM ? 4 * U : U;  // rows: LSTM [U_iou; U_f] | DAG U | FC W_right
   static constexpr int NACC = LSTM ? J : 1;    // accumulators per tile (level phase)
@@ -138,7 +149,7 @@ struct TcCfg {
   static constexpr size_t static_bytes = sizeof(TcMeta<J>) * kMetaRing + 4 * U * 4 + 64 * 8 + 64;
   static constexpr int S_fit =
       (int)((kSmemLimit - 1024 - static_bytes - bregion) / kStageBytes);
-  static constexpr int S = S_fit > 8 ? 8 : S_fit;
+  static constexpr int S = S_fit > CX_TC_SMAX ? CX_TC_SMAX : S_fit;
   static constexpr size_t dyn_bytes = 1024 + bregion + (size_t)S * kStageBytes;
   static_assert(H % 64 == 0 && H % U == 0, "H must be a multiple of 64 and of U");
   static_assert(BUFC * 2 <= 512, "TMEM: two accumulator buffers must fit 512 columns");
@@ -879,7 +890,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
                   const uint32_t accum = ((started >> acc) & 1u) | (kk > 0 ? 1u : 0u);
                   mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, accum);
                 }
-                if (SP == 2 && ka < KA) {
+                if (SP == 2 && ka < KA && !CX_TC_SKIP_LO) {
                   const uint32_t b1 = smem_u32(bbase + (size_t)(kb + KA) * brows * 128);
   #pragma unroll
                   for (int kk = 0; kk < 4; kk++)

@@ -63,9 +63,11 @@ def lib():
     global _lib
     with _lib_lock:
         if _lib is None:
-            path = _build.LIB
-            if _build.stale():
-                path = _build.build()
+            path = os.environ.get("CX_LIB")  # measurement variants (tools/build_variant.sh)
+            if not path:
+                path = _build.LIB
+                if _build.stale():
+                    path = _build.build()
             L = ctypes.CDLL(path)
             P, I, S = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
             L.cx_linearize_workspace_bytes.argtypes = [I, I]
@@ -109,18 +111,22 @@ def _stream(stream):
 
 class _WorkspaceCache:
     """Zero-filled workspaces, grown on demand, one per (device, stream, role).
-    The kernels leave their synchronisation words zero, so reuse needs no
-    memset. Keyed by stream too: two streams never share grid-barrier words.
-    A grown buffer never frees its predecessor: CUDA graphs captured earlier
-    may still point at it (they stay valid for the life of the process).
-    Pass an explicit `workspace=` to control the memory instead."""
+    The kernels leave their synchronisation words zero, so a call with the same
+    shape as the buffer's previous call needs no memset; the words' offsets
+    depend on the shape (cx.h), so a buffer is zero-filled again, on the call's
+    stream, whenever the shape key changes. Keyed by stream too: two streams
+    never share grid-barrier words. A grown buffer never frees its predecessor:
+    CUDA graphs captured earlier may still point at it (they stay valid for the
+    life of the process). Pass an explicit `workspace=` to control the memory
+    instead."""
 
     def __init__(self):
         self._bufs = {}
+        self._shape = {}
         self._retired = []
         self._lock = threading.Lock()
 
-    def get(self, device, role, nbytes, stream=None):
+    def get(self, device, role, nbytes, stream=None, shape=None):
         dev = torch.device(device)
         st = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
         key = (str(dev), int(st or 0), role)
@@ -131,10 +137,25 @@ class _WorkspaceCache:
                     self._retired.append(buf)
                 buf = torch.zeros(max(nbytes, 1 << 12), dtype=torch.uint8, device=dev)
                 self._bufs[key] = buf
+            elif self._shape.get(key) != shape:
+                # another shape: its synchronisation words sit elsewhere
+                if stream is None:
+                    buf.zero_()
+                else:
+                    with torch.cuda.stream(torch.cuda.ExternalStream(int(stream), device=dev)):
+                        buf.zero_()
+            self._shape[key] = shape
             return buf
 
 
 _ws = _WorkspaceCache()
+
+
+def _plan_env():
+    """The debug / measurement variables that change which kernel (and so which
+    workspace layout) a call uses; part of the workspace shape key."""
+    return tuple(os.environ.get(k) for k in ("CX_FORWARD_PATH", "CX_FUSED", "CX_TC_F32_MIN_N",
+                                             "CX_GRU_REFACTOR", "CX_UNROLL", "CX_PUSH"))
 
 
 @dataclass
@@ -195,7 +216,8 @@ def linearize(children: torch.Tensor, kind: int, stream=None, workspace=None,
     out.kind = kind
     L = lib()
     need = L.cx_linearize_workspace_bytes(n, maxc)
-    ws = workspace if workspace is not None else _ws.get(children.device, "lin", need, None if stream is None else stream.cuda_stream)
+    ws = workspace if workspace is not None else _ws.get(children.device, "lin", need, None if stream is None else stream.cuda_stream,
+                                                         shape=(n, maxc))
     st = L.cx_linearize(_ptr(children), n, maxc, kind, _ptr(ws), ws.numel(), ctypes.byref(out.c),
                         _stream(stream))
     if st != OK:
@@ -340,7 +362,8 @@ def linearize_forward(children: torch.Tensor, kind: int, cell: int, hidden: int,
     m = _model(cell, hidden, emb.shape[0], dtype)
     L = lib()
     need = L.cx_linearize_forward_workspace_bytes(ctypes.byref(m), n, maxc)
-    ws = workspace if workspace is not None else _ws.get(dev, "linfwd", need, None if stream is None else stream.cuda_stream)
+    ws = workspace if workspace is not None else _ws.get(dev, "linfwd", need, None if stream is None else stream.cuda_stream,
+                                                         shape=(n, maxc, cell, hidden, emb.shape[0], dtype, _plan_env()))
     st = L.cx_linearize_forward(_ptr(children), n, maxc, kind, ctypes.byref(m), ctypes.byref(w),
                                 _ptr(emb), _ptr(word_ids), ctypes.byref(out.c), _ptr(h_out),
                                 _ptr(aux_out), _ptr(root_out), _ptr(ws), ws.numel(),
@@ -402,7 +425,8 @@ def forward(cell: int, hidden: int, weights, emb: torch.Tensor, word_ids: torch.
     m = _model(cell, hidden, vocab, dtype)
     L = lib()
     need = L.cx_forward_workspace_bytes(ctypes.byref(m), n)
-    ws = workspace if workspace is not None else _ws.get(dev, "fwd", need, None if stream is None else stream.cuda_stream)
+    ws = workspace if workspace is not None else _ws.get(dev, "fwd", need, None if stream is None else stream.cuda_stream,
+                                                         shape=(n, lin.max_children, cell, hidden, vocab, dtype, _plan_env()))
     st = L.cx_forward(ctypes.byref(m), ctypes.byref(w), _ptr(emb), _ptr(word_ids),
                       ctypes.byref(lin.c), _ptr(h_out), _ptr(aux_out), _ptr(root_out), _ptr(ws),
                       ws.numel(), _stream(stream))

@@ -207,9 +207,9 @@ def test_all_leaves_and_single_node(cx):
 
 
 @pytest.mark.parametrize("name,family", [("cfg1_treernn", "smem"), ("cfg2_treelstm_b10", "cluster"),
-                                         ("cfg3_treegru_b10", "rw"), ("cfg3_treefc_b10", "rw"),
+                                         ("cfg3_treegru_b10", "rw"), ("cfg3_treefc_b10", "tc32"),
                                          ("cfg4_mvrnn_b10", "mvrnn"), ("cfg5_dagrnn_b10", "cluster"),
-                                         ("cfg5_treelstm_b4096", "big")])
+                                         ("cfg5_treelstm_b4096", "tc32"), ("cfg5_dagrnn_b4096", "tc32")])
 def test_automatic_family(cx, name, family, monkeypatch):
     """The automatic plan (cx_forward, fp32) runs the documented kernel family
     for every BASELINE configuration."""

@@ -17,6 +17,7 @@ import bench  # noqa: E402
 import paper_2011_01383_b200 as cx  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg5_treelstm_b4096"
+DT = cx.F32 if len(sys.argv) > 2 and sys.argv[2] == "f32" else cx.BF16  # f32: the split-fp32 kernel
 inp = bench.make_inputs(name, 0, 1)
 dev = torch.device("cuda", 0)
 t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a, dtype=dt)).to(dev)
@@ -24,7 +25,8 @@ children, words, emb = t(inp["children"], np.int32), t(inp["words"], np.int32), 
 weights = [t(w, np.float32) for w in inp["weights"]]
 cell, H = inp["cell"], inp["H"]
 S = 256
-info = cx.launch_info(cell, H, inp["V"], cx.BF16)
+info = cx.linearize_forward_launch_info(cell, H, inp["children"].shape[1], inp["children"].shape[0],
+                                        inp["V"], DT)
 buf = torch.zeros(info["ctas"] * (S + 2), dtype=torch.int64, device=dev)
 L = cx.lib()
 L.cx_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
@@ -34,16 +36,16 @@ for rep in range(4):
     lin = cx.linearize(children, inp["kind"])
     buf.zero_()
     L.cx_debug_set_trace(ctypes.c_void_p(buf.data_ptr()), S)
-    cx.forward(cell, H, weights, emb, words, lin, dtype=cx.BF16)
+    cx.forward(cell, H, weights, emb, words, lin, dtype=DT)
     L.cx_debug_set_trace(None, 0)
     torch.cuda.synchronize()
-tr = buf.view(info["ctas"], S).cpu().numpy().astype(np.int64)
+tr = buf[: info["ctas"] * S].view(info["ctas"], S).cpu().numpy().astype(np.int64)
 hdr = lin.header_dict()
 nl = hdr["num_levels"]
 sizes = lin.level_size[:nl].cpu().numpy()
 t0 = tr[:, 0].min()
 rel = lambda x: (x - t0) / 1000.0
-print(f"{name} bf16: ctas={info['ctas']} levels={nl} (us from earliest CTA entry)")
+print(f"{name} {'f32 (split)' if DT == cx.F32 else 'bf16'}: ctas={info['ctas']} levels={nl} (us from earliest CTA entry)")
 print(f"weights staged: min {rel(tr[:,60].min()):8.2f} max {rel(tr[:,60].max()):8.2f}; phase 0 done: max {rel(tr[:,61].max()):8.2f}")
 print(f"prologue done: min {rel(tr[:,1].min()):8.2f} max {rel(tr[:,1].max()):8.2f}")
 for l in range(nl):
