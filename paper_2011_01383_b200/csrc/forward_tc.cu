@@ -122,12 +122,19 @@ struct TcCfg {
   // split TreeLSTM: W_iou (leaf phase) and [U_iou; U_f] (levels) take turns in
   // one shared-memory region (both at once would not fit with the stages)
   static constexpr bool BSHARE = LSTM && (SP == 2 || CX_TC_BSHARE_ALL);
+  // split DAG-RNN / TreeFC: the B_hi and B_lo rows of a K-atom are adjacent
+  // (one 2R-row operand), so a hi A atom meets both in ONE MMA of N = 2R (its
+  // A tile is read from shared memory once, not twice) into accumulator
+  // columns [0, R) (A B_hi) and [R, 2R) (A_hi B_lo), summed by the epilogue
+  // (TreeLSTM's 4U = 128-column accumulators per child would not fit TMEM twice)
+  static constexpr bool MERGE = SP == 2 && !LSTM && !CX_TC_SKIP_LO;
+  static constexpr int MW = MERGE ? 2 : 1;  // accumulator width factor
   static constexpr int B0 = LSTM ? 3 * U : U;  // rows: LSTM W_iou | DAG W_x | FC W_left
   static constexpr int B1 = LSTM ? 4 * U : U;  // rows: LSTM [U_iou; U_f] | DAG U | FC W_right
   static constexpr int NACC = LSTM ? J : 1;    // accumulators per tile (level phase)
   static constexpr int NLVL = LSTM ? 4 * U : U;  // N of a level-phase MMA
   static constexpr int NLEAF = LSTM ? 3 * U : U;
-  static constexpr int BUFC = NACC * NLVL;      // TMEM columns per accumulator buffer
+  static constexpr int BUFC = NACC * NLVL * MW;  // TMEM columns per accumulator buffer
   static constexpr int TCOLS = pow2_cols(2 * BUFC);
   static constexpr bool XSLOT = LSTM || DAG;
   // CTAs that own different unit slices of the same node tiles form a cluster
@@ -153,7 +160,7 @@ struct TcCfg {
   static constexpr size_t dyn_bytes = 1024 + bregion + (size_t)S * kStageBytes;
   static_assert(H % 64 == 0 && H % U == 0, "H must be a multiple of 64 and of U");
   static_assert(BUFC * 2 <= 512, "TMEM: two accumulator buffers must fit 512 columns");
-  static_assert(NLVL <= 256 && NLEAF <= 256 && NLVL % 16 == 0, "UMMA N");
+  static_assert(NLVL * MW <= 256 && NLEAF * MW <= 256 && NLVL % 16 == 0, "UMMA N");
 
   __host__ __device__ static constexpr int nslots(bool leaf) {
     return leaf ? 1 : (LSTM ? J : DAG ? J + 1 : 2);
@@ -399,6 +406,11 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
           (void)wsrc(idx, Bm, rows, q, ka, c);
           if constexpr (SP == 1) {
             *reinterpret_cast<uint4 *>(Bm + (size_t)ka * rows * 128 + sw128_off(q, c)) = f32x8_to_bf16(lo[e], hi[e]);
+          } else if constexpr (C::MERGE) {  // atom ka = [hi rows; lo rows]
+            uint4 ph, pl;
+            split8(lo[e], hi[e], ph, pl);
+            *reinterpret_cast<uint4 *>(Bm + (size_t)ka * 2 * rows * 128 + sw128_off(q, c)) = ph;
+            *reinterpret_cast<uint4 *>(Bm + (size_t)ka * 2 * rows * 128 + sw128_off(rows + q, c)) = pl;
           } else {
             uint4 ph, pl;
             split8(lo[e], hi[e], ph, pl);
@@ -858,7 +870,8 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         // =========================== MMA issuer ==================================
         if (lane == 0) {
           const uint32_t idesc = idesc_bf16(kTM, leaf ? C::NLEAF : C::NLVL);
-          const int ncol = leaf ? C::NLEAF : C::NLVL;
+          const uint32_t idesc2 = idesc_bf16(kTM, (leaf ? C::NLEAF : C::NLVL) * C::MW);  // MERGE hi atoms
+          const int ncol = (leaf ? C::NLEAF : C::NLVL) * C::MW;
           uint32_t Sg = Sg0;
           for (int t = 0; t < ntiles; t++) {
             const uint32_t TT = T0 + t, buf = TT & 1;
@@ -883,14 +896,15 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
                 unsigned char *bbase = bm ? sB1 : sB0;
                 // SP = 2: a hi atom (ka < KA) meets B_hi and B_lo, a lo atom B_hi
                 const int kb = ka < KA ? ka : ka - KA;
-                const uint32_t b0 = smem_u32(bbase + (size_t)kb * brows * 128);
+                const uint32_t b0 = smem_u32(bbase + (size_t)kb * brows * C::MW * 128);
                 const uint32_t d = tmem + buf * C::BUFC + acc * ncol;
+                const uint32_t idk = (C::MERGE && ka < KA) ? idesc2 : idesc;  // N = 2R: B_hi and B_lo at once
   #pragma unroll
                 for (int kk = 0; kk < 4; kk++) {
                   const uint32_t accum = ((started >> acc) & 1u) | (kk > 0 ? 1u : 0u);
-                  mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idesc, accum);
+                  mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idk, accum);
                 }
-                if (SP == 2 && ka < KA && !CX_TC_SKIP_LO) {
+                if (SP == 2 && !C::MERGE && ka < KA && !CX_TC_SKIP_LO) {
                   const uint32_t b1 = smem_u32(bbase + (size_t)(kb + KA) * brows * 128);
   #pragma unroll
                   for (int kk = 0; kk < 4; kk++)
@@ -1019,6 +1033,12 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
             for (int q = 0; q < UC / CW; q++) {
               float v[CW];
               tmem_ld<CW>(tb + q * CW, v);
+              if constexpr (C::MERGE) {  // + the A_hi B_lo columns
+                float v2[CW];
+                tmem_ld<CW>(tb + U + q * CW, v2);
+  #pragma unroll
+                for (int j = 0; j < CW; j++) v[j] += v2[j];
+              }
   #pragma unroll
               for (int j = 0; j < CW; j++) v[j] = act_tanh<SP>(v[j] + s_bias[u0 + q * CW + j]);
               if (valid) {
