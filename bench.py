@@ -34,6 +34,9 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 
+# L2 flush between timed steps: a 256 MiB write (> the 126 MB L2). CX_BENCH_NOFLUSH=1
+# (diagnostic only, the line says so) keeps L2 warm to expose cold-miss costs.
+FLUSH_FLOATS = 4 if os.environ.get("CX_BENCH_NOFLUSH") == "1" else 256 * 1024 * 1024 // 4
 METRIC = "TreeLSTM fwd latency µs (batch 10, H=256) and trees/s at 1/2/4/8 B200"
 UNIT = "trees/s"
 FMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4: SMs x FP32 lanes x 2 x max clock
@@ -199,7 +202,7 @@ def launch_floor_us(n_launches, dev, reps=50):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         fn()
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush = torch.empty(FLUSH_FLOATS, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
     ev = []
     for i in range(reps + 5):
@@ -432,7 +435,7 @@ def throughput_b4096(dtype_name, rank, world, local_rank, steps=30, warmup=5):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         step()
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush = torch.empty(FLUSH_FLOATS, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
     for _ in range(warmup):
         g.replay()
@@ -530,7 +533,7 @@ def run_gpu(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
 
     # L2 flush buffer (> 126 MB L2): written between timed steps, outside the events
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush = torch.empty(FLUSH_FLOATS, dtype=torch.float32, device=dev)
 
     for _ in range(args.warmup):
         g_step.replay()
@@ -749,7 +752,8 @@ def run_gpu(args, rank, world, local_rank):
         "config": {"workload": name, "cell": synth.CELL_NAMES[cell], "hidden": H, "vocab": V,
                    "structures_per_gpu": R, "nodes_per_gpu": n, "levels": L,
                    "parallelism": f"dp{world} (independent structures per rank)",
-                   "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+                   "l2": "flushed between timed steps (256 MiB write, outside the events)"
+                         if FLUSH_FLOATS > 1 else "NOT flushed (CX_BENCH_NOFLUSH diagnostic: not a valid bench line)"},
         "latency_us": statistics.median(step_ms) * 1e3,
         "latency_p10_us": float(np.percentile(step_ms, 10)) * 1e3,
         "latency_p90_us": float(np.percentile(step_ms, 90)) * 1e3,
