@@ -215,7 +215,7 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
     a.xmode = cx::tc_xmode(n, m->vocab);
     q = align_up(q + 2 * (a.xmode ? N : (size_t)m->vocab) * RW, 256);
     a.cell_has_x = m->cell == CX_TREELSTM || m->cell == CX_DAGRNN;
-    a.hoist = cx::tc_hoist(m->cell, n, m->vocab) ? 1 : 0;
+    a.hoist = cx::tc_hoist(m->cell, n, m->vocab, plan.tc_sp) ? 1 : 0;
     if (a.hoist) {
       a.hf = reinterpret_cast<float *>(q);
       q = align_up(q + 4 * (size_t)m->vocab * H, 256);

@@ -46,6 +46,7 @@
 #include <cuda.h>  // CUtensorMap types (the encoder is fetched from the driver at run time)
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -304,7 +305,7 @@ __device__ __forceinline__ float act_tanh(float x) {
 // %globaltimer into slot s. Slots: 0 entry, 1 prologue done, 2+4l level l
 // start, 3+4l producers done, 4+4l MMA issue done, 5+4l epilogue done.
 __device__ __forceinline__ void tc_mark(const FwdArgs &a, int s, int who) {
-  if (a.trace && threadIdx.x == who && s < a.trace_slots) {
+  if (a.trace && threadIdx.x == who && s >= 0 && s < a.trace_slots) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[(size_t)blockIdx.x * a.trace_slots + s] = t;
@@ -430,6 +431,24 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
   const int L = status0 == CX_OK ? a.hdr->num_levels : 0, first_leaf = a.hdr->first_leaf;
   const int xlo = C::DAG ? 0 : first_leaf;  // node-order x rows start here
   const bool hoist = C::LSTM && a.hoist;
+  // DAG-RNN computation hoisting (PAPER §4.3; the input matvecs as
+  // one GEMM up front): in table mode the input projection
+  // W_x x + b is computed once per vocabulary word (phase l = -1, into the fp32
+  // table a.hf [V][H]); the leaves (level 0) are h = tanh(P[word]) without an
+  // MMA, and a level's tiles contract only the children (U h~) and add their
+  // word's P row in the epilogue.
+  const bool hx = C::DAG && SP == 2 && a.hoist;
+  const int l0 = hx ? -1 : 0;
+  auto nsl_of = [&](int l) -> int { return hx ? (l < 0 ? 1 : l == 0 ? 0 : J) : C::nslots(l == 0); };
+  auto slot_of = [&](int l, int s_, int &src, int &bm, int &acc) {
+    if (hx) {
+      src = l < 0 ? -1 : s_;
+      bm = l < 0 ? 0 : 1;
+      acc = 0;
+      return;
+    }
+    C::slot(l == 0, s_, src, bm, acc);
+  };
   const bool discard_ok = !a.discard_off;  // CX_DISCARD=0: keep dead lines (measurement)
   const int sbase = hoist ? a.V : 0;  // state row of internal node i = sbase + i
   // ---- phase 0: bf16 input rows ------------------------------------------------
@@ -608,7 +627,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
 
   // level ranges: identical in every role
   auto level_range = [&](int l, int &lo, int &hi) {
-    if (l == 0 && hoist) {  // the leaf cell once per vocabulary word (rows [0, V))
+    if (l < 0 || (l == 0 && hoist)) {  // once per vocabulary word (rows [0, V))
       chunk_of(a.V, a.Gn, gn, lo, hi);
     } else {
       chunk_of(__ldg(a.lsize + l), a.Gn, gn, lo, hi);
@@ -639,8 +658,8 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
     // It depends on the linearization only, so these warps run ahead of the
     // level barriers (bounded by the 4-slot ring the epilogue releases).
     uint32_t T0m = 0;
-    for (int l = 0; l < L; l++) {
-      const bool leaf = l == 0;
+    for (int l = l0; l < L; l++) {
+      const bool leaf = l == 0, proj = l < 0;
       if (C::FC && leaf) continue;  // TreeFC leaves: a copy, no tiles
       int lo, hi;
       level_range(l, lo, hi);
@@ -653,7 +672,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         const int ms = TT % kMetaRing;
         const int i0 = lo + t * kTM, cnt = min(kTM, hi - i0);
         mbar_wait(&bar_mempty[ms], ((TT / kMetaRing) & 1) ^ 1);
-        const int tslot = (l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
+        const int tslot = (l >= 0 && l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
         tc_mark(a, tslot + 0, warp * 32);
         TcMeta<J> &m = meta[ms];
         if constexpr (C::LSTM) {
@@ -679,7 +698,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
           psv[q] = -1;
 #pragma unroll
           for (int k = 0; k < J; k++) ch[q][k] = -1;
-          if (r < cnt && !(leaf && hoist)) {
+          if (r < cnt && !(leaf && hoist) && !proj) {
             own[q] = __ldg(a.perm + i);
             if (C::LSTM) psv[q] = __ldcg(a.pslot + i);
             if (a.root_out) sv[q] = __ldg(a.sid + i);
@@ -695,7 +714,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
           int root = -1, xr = -1;
           if (r < cnt) {
             if (sv[q] >= 0) root = __ldg(a.roots + sv[q]) == i ? sv[q] : -1;
-            if (leaf && hoist) {
+            if ((leaf && hoist) || proj) {
               xr = i;  // word row
             } else if (C::XSLOT && (leaf || C::DAG)) {
               if (a.xmode == 0) {
@@ -737,10 +756,12 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
       T0m += ntiles;
     }
   } else {
-    uint32_t T0 = 0, Sg0 = 0;  // tiles / stages before this level (identical in every role)
-    for (int l = 0; l < L; l++) {
-      const bool leaf = l == 0;
-      if (l > 0) level_sync();
+    // tiles / stages / accumulator tiles (tiles with MMAs) before this level,
+    // identical in every role
+    uint32_t T0 = 0, Sg0 = 0, A0 = 0;
+    for (int l = l0; l < L; l++) {
+      const bool leaf = l == 0, proj = l < 0;
+      if (l > l0) level_sync();
       if (C::BSHARE && l == 1) {  // the leaf phase's MMAs are complete: B1 replaces B0
         load_b(2, kWork);
         fence_proxy_async();
@@ -762,7 +783,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         leaf_pass(true);
         level_sync();
       }
-      tc_mark(a, 2 + 4 * l, 0);
+      tc_mark(a, l >= 0 ? 2 + 4 * l : -1, 0);
       int lo, hi;
       level_range(l, lo, hi);
       if constexpr (C::FC) {
@@ -796,7 +817,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         }
       }
       const int ntiles = (hi - lo + kTM - 1) / kTM;
-      const int nsl = C::nslots(leaf);
+      const int nsl = nsl_of(l);
 
       if (C::LSTM && warp == kFeed0) {
         // ========================= TMA tile loads ================================
@@ -810,7 +831,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
           for (int ka = 0; ka < KAA; ka++) {
             for (int s = 0; s < nsl; s++) {
               int src, bm, acc;
-              C::slot(leaf, s, src, bm, acc);
+              slot_of(l, s, src, bm, acc);
               const int st = Sg % S;
               const int kst = (int)(Sg - Sg0);
               const int sslot = (l == 1 && kst < 16) ? 64 + 4 * kst : 1 << 30;
@@ -830,7 +851,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
             }
           }
         }
-        tc_mark(a, 3 + 4 * l, kFeed0 * 32);
+        tc_mark(a, l >= 0 ? 3 + 4 * l : -1, kFeed0 * 32);
       } else if (!C::LSTM && warp >= kFeed0 && warp < kMeta0) {
         // ========================= cp.async gathers ==============================
         // per stage: one K-atom of one slot for the tile's 128 rows, 16-byte
@@ -847,7 +868,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
           for (int ka = 0; ka < KAA; ka++) {
             for (int s = 0; s < nsl; s++) {
               int src, bm, acc;
-              C::slot(leaf, s, src, bm, acc);
+              slot_of(l, s, src, bm, acc);
               const int st = Sg % S;
               mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);
               const uint32_t dst0 = smem_u32(sStage + (size_t)st * kStageBytes);
@@ -868,22 +889,22 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         }
       } else if (warp == kMmaWarp) {
         // =========================== MMA issuer ==================================
-        if (lane == 0) {
+        if (lane == 0 && nsl > 0) {  // (no MMAs in a hoisted DAG-RNN leaf level)
           const uint32_t idesc = idesc_bf16(kTM, leaf ? C::NLEAF : C::NLVL);
           const uint32_t idesc2 = idesc_bf16(kTM, (leaf ? C::NLEAF : C::NLVL) * C::MW);  // MERGE hi atoms
           const int ncol = (leaf ? C::NLEAF : C::NLVL) * C::MW;
           uint32_t Sg = Sg0;
           for (int t = 0; t < ntiles; t++) {
-            const uint32_t TT = T0 + t, buf = TT & 1;
-            mbar_wait(&bar_tempty[buf], ((TT >> 1) & 1) ^ 1);
+            const uint32_t TA = A0 + t, buf = TA & 1;
+            mbar_wait(&bar_tempty[buf], ((TA >> 1) & 1) ^ 1);
             fence_after();
-            const int tslot = (l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
+            const int tslot = (l >= 0 && l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
             tc_mark(a, tslot + 2, kMmaWarp * 32);
             uint32_t started = 0;
             for (int ka = 0; ka < KAA; ka++) {
               for (int s = 0; s < nsl; s++) {
                 int src, bm, acc;
-                C::slot(leaf, s, src, bm, acc);
+                slot_of(l, s, src, bm, acc);
                 const int st = Sg % S;
                 const int kst = (int)(Sg - Sg0);
                 const int sslot = (l == 1 && kst < 16) ? 64 + 4 * kst : 1 << 30;
@@ -919,7 +940,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
             mma_commit(&bar_tfull[buf]);
             tc_mark(a, tslot + 3, kMmaWarp * 32);
           }
-          tc_mark(a, 4 + 4 * l, kMmaWarp * 32);
+          tc_mark(a, l >= 0 ? 4 + 4 * l : -1, kMmaWarp * 32);
         }
         __syncwarp();
       } else {
@@ -929,13 +950,13 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         const int q4 = warp & 3, hh = warp >> 2;
         const int r = q4 * 32 + lane, u0 = hh * UC;
         for (int t = 0; t < ntiles; t++) {
-          const uint32_t TT = T0 + t, buf = TT & 1;
+          const uint32_t TT = T0 + t, TA = A0 + t, buf = TA & 1;
           const int ms = TT % kMetaRing;
           mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
           const TcMeta<J> &m = meta[ms];
           const bool valid = r < m.cnt;
           const int i = m.i0 + r, own = m.own[r], root = m.root[r];
-          const int tslot = (l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
+          const int tslot = (l >= 0 && l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
           const uint32_t tb = tmem + ((uint32_t)(q4 * 32) << 16) + buf * C::BUFC + u0;
           if constexpr (C::LSTM) {
             static_assert(UC == 16, "TreeLSTM epilogue: 16 units per thread");
@@ -956,7 +977,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
                 ld256(src + 8, cp[k] + 8);
               }
             }
-            mbar_wait(&bar_tfull[buf], (TT >> 1) & 1);
+            mbar_wait(&bar_tfull[buf], (TA >> 1) & 1);
             fence_after();
             tc_mark(a, tslot + 4, 0);
             const float *bi = s_bias + u0, *bo = bi + U, *bu = bi + 2 * U, *bf = bi + 3 * U;
@@ -1026,21 +1047,54 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
             }
           } else {  // DAG-RNN / TreeFC: h = tanh(acc + b)
             constexpr int CW = UC < 32 ? UC : 32;
-            mbar_wait(&bar_tfull[buf], (TT >> 1) & 1);
-            fence_after();
+            // hoisted DAG-RNN: this row's word projection (bias included),
+            // first chunk loaded before the accumulator wait
+            const int xrow = (hx && !proj && valid) ? m.xr[r] : -1;
+            float pv[CW];
+            if (xrow >= 0) {
+              const float *pr = a.hf + (size_t)xrow * H + unit0 + u0;
+  #pragma unroll
+              for (int j = 0; j < CW; j += 8) ld256(pr + j, pv + j);
+            }
+            if (nsl > 0) {
+              mbar_wait(&bar_tfull[buf], (TA >> 1) & 1);
+              fence_after();
+            }
             tc_mark(a, tslot + 4, 0);
   #pragma unroll 1
             for (int q = 0; q < UC / CW; q++) {
               float v[CW];
-              tmem_ld<CW>(tb + q * CW, v);
-              if constexpr (C::MERGE) {  // + the A_hi B_lo columns
-                float v2[CW];
-                tmem_ld<CW>(tb + U + q * CW, v2);
+              if (nsl > 0) {
+                tmem_ld<CW>(tb + q * CW, v);
+                if constexpr (C::MERGE) {  // + the A_hi B_lo columns
+                  float v2[CW];
+                  tmem_ld<CW>(tb + U + q * CW, v2);
   #pragma unroll
-                for (int j = 0; j < CW; j++) v[j] += v2[j];
+                  for (int j = 0; j < CW; j++) v[j] += v2[j];
+                }
+              } else {
+  #pragma unroll
+                for (int j = 0; j < CW; j++) v[j] = 0.f;
               }
+              if (proj) {  // W_x x + b of word i -> the table (no outputs)
+                if (valid) {
   #pragma unroll
-              for (int j = 0; j < CW; j++) v[j] = act_tanh<SP>(v[j] + s_bias[u0 + q * CW + j]);
+                  for (int j = 0; j < CW; j++) v[j] += s_bias[u0 + q * CW + j];
+                  st_row<CW>(a.hf + (size_t)i * H + unit0 + u0 + q * CW, v);
+                }
+                continue;
+              }
+              if (hx) {
+                if (q > 0 && xrow >= 0) {
+  #pragma unroll
+                  for (int j = 0; j < CW; j += 8) ld256(a.hf + (size_t)xrow * H + unit0 + u0 + q * CW + j, pv + j);
+                }
+  #pragma unroll
+                for (int j = 0; j < CW; j++) v[j] = act_tanh<SP>(v[j] + pv[j]);
+              } else {
+  #pragma unroll
+                for (int j = 0; j < CW; j++) v[j] = act_tanh<SP>(v[j] + s_bias[u0 + q * CW + j]);
+              }
               if (valid) {
                 const int uu = unit0 + u0 + q * CW;
                 st_row_cs<CW>(a.h_out + (size_t)own * H + uu, v);
@@ -1050,14 +1104,15 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
             }
           }
           fence_before();
-          mbar_arrive(&bar_tempty[buf]);
+          if (nsl > 0) mbar_arrive(&bar_tempty[buf]);
           mbar_arrive(&bar_mempty[ms]);
           tc_mark(a, tslot + 5, 0);
         }
-        tc_mark(a, 5 + 4 * l, 0);
+        tc_mark(a, l >= 0 ? 5 + 4 * l : -1, 0);
       }
       T0 += ntiles;
       Sg0 += (uint32_t)ntiles * KAA * nsl;
+      if (nsl > 0) A0 += ntiles;
     }
 
     if (hoist && L > 0) {  // leaves' caller outputs (the table is complete since level 1)
@@ -1251,11 +1306,19 @@ int tc_xmode(int n, int V) { return (size_t)n * 2 <= (size_t)V ? 1 : 0; }
 // has more leaves' worth of x rows than V/2 (table mode) the leaf level is
 // evaluated once per vocabulary word and parents read leaf children from that
 // table.
-bool tc_hoist(int cell, int n, int V) { return cell == CX_TREELSTM && tc_xmode(n, V) == 0; }
+// DAG-RNN (split fp32 operands only: on bf16 operands the extra phase and the
+// epilogue's table loads cost more than the removed x slot, measured): the
+// input projection W_x x + b once per word (a [V][H] fp32 table) in the same
+// condition. CX_TC_HOIST=0 disables both (measurement).
+bool tc_hoist(int cell, int n, int V, int sp) {
+  const char *e = std::getenv("CX_TC_HOIST");
+  if (e && e[0] == '0') return false;
+  return (cell == CX_TREELSTM || (cell == CX_DAGRNN && sp == 2)) && tc_xmode(n, V) == 0;
+}
 
 // State rows: hoisted TreeLSTM keeps the V word rows first, node i at row V + i.
 size_t tc_state_rows(int cell, int n, int V) {
-  return (size_t)(n > 0 ? n : 1) + (tc_hoist(cell, n, V) ? (size_t)V : 0);
+  return (size_t)(n > 0 ? n : 1) + (cell == CX_TREELSTM && tc_hoist(cell, n, V, 1) ? (size_t)V : 0);
 }
 
 // workspace bytes of the tensor-core path (after the GridBar); forward_impl in
@@ -1268,7 +1331,7 @@ size_t tc_workspace_bytes(int cell, int H, int V, int n, int sp) {
   if (cell == CX_TREELSTM) b += 4 * R * h + 256;                // cs
   if (cell == CX_TREELSTM || cell == CX_DAGRNN)                 // xb
     b += 2 * (tc_xmode(n, V) ? N : (size_t)V) * rw + 256;
-  if (tc_hoist(cell, n, V)) b += 4 * (size_t)V * h + 4 * N + 512;  // hf, crow
+  if (tc_hoist(cell, n, V, sp)) b += 4 * (size_t)V * h + 4 * N + 512;  // hf, crow
   if (cell == CX_TREELSTM) b += 2 * (2 * N) * rw + 4 * N + 512;    // pb (J <= 2), pslot
   return b;
 }

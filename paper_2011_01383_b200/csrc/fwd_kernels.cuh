@@ -105,7 +105,7 @@ bool tc_plan(int cell, int H, int maxc, int sp, int num_sms, FwdPlan *plan, int 
 int tc_xmode(int n, int V);
 size_t tc_workspace_bytes(int cell, int H, int V, int n, int sp);
 cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &args, cudaStream_t stream);
-bool tc_hoist(int cell, int n, int V);
+bool tc_hoist(int cell, int n, int V, int sp);
 size_t tc_state_rows(int cell, int n, int V);
 cudaError_t fwd_launch(const FwdPlan &plan, FwdArgs &args, cudaStream_t stream);
 bool pdl_enabled();

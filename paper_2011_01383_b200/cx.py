@@ -154,7 +154,7 @@ _ws = _WorkspaceCache()
 def _plan_env():
     """The debug / measurement variables that change which kernel (and so which
     workspace layout) a call uses; part of the workspace shape key."""
-    return tuple(os.environ.get(k) for k in ("CX_FORWARD_PATH", "CX_FUSED", "CX_TC_F32_MIN_N",
+    return tuple(os.environ.get(k) for k in ("CX_FORWARD_PATH", "CX_FUSED", "CX_TC_F32_MIN_N", "CX_TC_HOIST",
                                              "CX_GRU_REFACTOR", "CX_UNROLL", "CX_PUSH"))
 
 
