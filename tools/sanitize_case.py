@@ -59,9 +59,17 @@ elif case == "big_lstm":
 elif case == "mvrnn":
     run(synth.MVRNN, 16, 50, forest(3), synth.TREE)
 elif case == "tc_lstm":
-    run(synth.TREELSTM, 128, 50, forest(3), synth.TREE, dtype=cx.BF16)
+    run(synth.TREELSTM, 128, 50, forest(3), synth.TREE, dtype=cx.BF16, path="tc")
 elif case == "tc_dag":
-    run(synth.DAGRNN, 128, 50, synth.grid_dags(2, 4, 4)[0], synth.DAG, dtype=cx.BF16)
+    run(synth.DAGRNN, 128, 50, synth.grid_dags(2, 4, 4)[0], synth.DAG, dtype=cx.BF16, path="tc")
+elif case == "tc32_lstm":  # split-fp32 tensor-core kernel, hoisted leaves (2n > V)
+    run(synth.TREELSTM, 128, 50, forest(3), synth.TREE, path="tc")
+elif case == "tc32_dag":  # split-fp32, hoisted input projection (2n > V)
+    run(synth.DAGRNN, 128, 50, synth.grid_dags(2, 4, 4)[0], synth.DAG, path="tc")
+elif case == "tc32_dag_nohoist":  # split-fp32, per-node projection (node-order x rows)
+    run(synth.DAGRNN, 128, 5000, synth.grid_dags(2, 4, 4)[0], synth.DAG, path="tc")
+elif case == "tc32_fc":
+    run(synth.TREEFC, 256, 50, synth.perfect_forest(2, 3)[0], synth.TREE, path="tc")
 elif case == "single_rnn":
     run(synth.TREERNN, 8, 50, forest(2), synth.TREE, fused=True)
 else:
