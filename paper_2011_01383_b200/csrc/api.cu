@@ -244,6 +244,8 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
     a.push_off = pe && pe[0] == '0';
     const char *de = std::getenv("CX_DISCARD");
     a.discard_off = de && de[0] == '0';
+    const char *fe = std::getenv("CX_TC_FMA");
+    a.tc_fma_off = fe && fe[0] == '0';
     a.trace = g_trace;
     a.trace_slots = g_trace_slots;
   }

@@ -69,6 +69,9 @@ using namespace umma;
 #ifndef CX_TC_SMAX
 #define CX_TC_SMAX 8
 #endif
+#ifndef CX_TC_FML_FC  // split TreeFC: nodes per node group up to which a level runs on FMA
+#define CX_TC_FML_FC 10
+#endif
 constexpr int kTM = 128;                    // tile rows = UMMA M
 // warps 0-7: epilogue (warp w reads TMEM lane quadrant w % 4 = tile rows
 // 32(w%4)..+31, column half w / 4); warp 8: MMA issuer; warps 9..: operand
@@ -450,6 +453,19 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
     C::slot(l == 0, s_, src, bm, acc);
   };
   const bool discard_ok = !a.discard_off;  // CX_DISCARD=0: keep dead lines (measurement)
+  // Per-level precision/unit dispatch (north_star: tensor cores only where the
+  // level really is a dense GEMM): a level whose node chunk has at most FMX
+  // nodes per node group runs on the epilogue warps' FMA pipes (resident B from
+  // shared memory, operands staged in the idle stage ring) instead of a
+  // 128-row UMMA tile (whose K pipeline, MMA and epilogue latency chain would
+  // cost several microseconds for a handful of rows). Same operand precision:
+  // bf16 (SP = 1) or hi + lo (SP = 2), fp32 products and sums.
+  // FMX: nodes per batch (staged at once); FML: nodes per node group up to
+  // which a level runs on FMA, in batches (TreeFC's 2H-deep contraction of
+  // split operands costs the tile path ~17 us per level: more levels qualify)
+  constexpr int FMX = C::LSTM ? 4 : C::FC ? 10 : 6;
+  constexpr int FML = C::FC ? (SP == 2 ? CX_TC_FML_FC : 10) : FMX;
+  auto is_fma = [&](int l) { return l >= 1 && !a.tc_fma_off && __ldg(a.lsize + l) <= FML * a.Gn; };
   const int sbase = hoist ? a.V : 0;  // state row of internal node i = sbase + i
   // ---- phase 0: bf16 input rows ------------------------------------------------
   if (C::XSLOT && status0 == CX_OK) {
@@ -653,6 +669,210 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
     named_bar(3, kWork);
   };
 
+  // ---- a small level on FMA (is_fma): the 8 epilogue warps ------------------
+  // 1. node info; 2. operand rows -> fp32 in the stage ring; 3. partial dot
+  // products thread = (accumulator column, K part); 4. sums + the cell's gate
+  // epilogue per (node, unit), outputs as the tile epilogue writes them.
+  auto fma_batch = [&](int l, int lo, int hi) {
+    constexpr int NA = C::NACC, NC = C::NLVL, COLS = NA * NC;
+    constexpr int KS = kEpiThreads / COLS >= 1 ? kEpiThreads / COLS : 1;
+    constexpr int NSLM = C::LSTM ? J : C::DAG ? J + 1 : 2;
+    static_assert(COLS <= kEpiThreads && kEpiThreads % COLS == 0 && (H / KS) % 8 == 0, "FMA split");
+    constexpr size_t kAf = (size_t)NSLM * FMX * H, kDp = (size_t)KS * FMX * COLS;
+    static_assert(4 * (kAf + kDp) + 4 * FMX * (8 + 2 * J) <= (size_t)S * kStageBytes, "FMA level fits the stage ring");
+    const int cnt = hi - lo, ntid = tid;  // tid < kEpiThreads
+    const int nsl = nsl_of(l);
+    float *Af = reinterpret_cast<float *>(sStage), *Dp = Af + kAf;
+    int *n_own = reinterpret_cast<int *>(Dp + kDp), *n_root = n_own + FMX, *n_ps = n_root + FMX,
+        *n_xr = n_ps + FMX, *n_ch = n_xr + FMX /* [J][FMX] operand rows */, *n_ck = n_ch + J * FMX;
+    if (ntid < cnt) {  // 1. node info (as the bookkeeping warps compute it)
+      const int i = lo + ntid, own = __ldg(a.perm + i);
+      n_own[ntid] = own;
+      int root = -1;
+      if (a.root_out) {
+        const int sv = __ldg(a.sid + i);
+        root = __ldg(a.roots + sv) == i ? sv : -1;
+      }
+      n_root[ntid] = root;
+      n_ps[ntid] = C::LSTM ? __ldcg(a.pslot + i) : -1;
+      int xr = -1;
+      if (C::DAG) {
+        if (a.xmode == 0) {
+          int w = __ldg(a.words + own);
+          if (w < 0 || w >= a.V) {
+            if (latch) latch_error(a.hdr, CX_E_WORD_RANGE, own);
+            w = 0;
+          }
+          xr = w;
+        } else {
+          xr = i - xlo;
+        }
+      }
+      n_xr[ntid] = xr;
+      bool absent = false;
+      int nc = 0;
+#pragma unroll
+      for (int k = 0; k < J; k++) {
+        int c = __ldg(a.chn + (size_t)k * n + i);
+        absent = absent || c < 0;
+        if (absent) c = -1;
+        nc += c >= 0;
+        const int srow = c >= 0 ? (hoist ? __ldcg(a.crow + c) : c) : -1;  // the child's state row
+        n_ck[k * FMX + ntid] = srow;
+        // operand row of slot k: TreeLSTM the parent-slot row, else the state row
+        n_ch[k * FMX + ntid] = C::LSTM ? (c >= 0 ? k * n + i : -1) : srow;
+      }
+      if (C::FC && nc != 2 && latch) latch_error(a.hdr, CX_E_ARITY, own);
+    }
+    named_bar(5, kEpiThreads);
+    // 2. operands -> fp32 (hi [+ lo]); absent rows -> zeros
+    constexpr int Q8 = H / 8;
+    for (int idx = ntid; idx < nsl * cnt * Q8; idx += kEpiThreads) {
+      const int q = idx % Q8, st = idx / Q8, t = st % cnt, sl = st / cnt;
+      int src, bm, acc;
+      slot_of(l, sl, src, bm, acc);
+      const int row = src < 0 ? n_xr[t] : n_ch[src * FMX + t];
+      const unsigned short *base = src < 0 ? xb : (C::LSTM ? a.pb : hb);
+      float f[8];
+      if (row >= 0) {
+        const uint4 hv = __ldcg(reinterpret_cast<const uint4 *>(base + (size_t)row * RW + 8 * q));
+        const unsigned hw[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          f[2 * e] = __uint_as_float(hw[e] << 16);
+          f[2 * e + 1] = __uint_as_float(hw[e] & 0xffff0000u);
+        }
+        if constexpr (SP == 2) {
+          const uint4 lv = __ldcg(reinterpret_cast<const uint4 *>(base + (size_t)row * RW + H + 8 * q));
+          const unsigned lw[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            f[2 * e] += __uint_as_float(lw[e] << 16);
+            f[2 * e + 1] += __uint_as_float(lw[e] & 0xffff0000u);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; e++) f[e] = 0.f;
+      }
+      float4 *d = reinterpret_cast<float4 *>(Af + ((size_t)sl * FMX + t) * H + 8 * q);
+      d[0] = make_float4(f[0], f[1], f[2], f[3]);
+      d[1] = make_float4(f[4], f[5], f[6], f[7]);
+    }
+    named_bar(5, kEpiThreads);
+    // 3. partial sums: column col of accumulator ac, K part p, every node
+    {
+      const int col = ntid % COLS, p = ntid / COLS;
+      const int ac = col / NC, cc = col % NC;
+      float part[FMX];
+#pragma unroll
+      for (int t = 0; t < FMX; t++) part[t] = 0.f;
+      for (int sl = 0; sl < nsl; sl++) {
+        int src, bm, acc;
+        slot_of(l, sl, src, bm, acc);
+        if (acc != ac) continue;
+        const unsigned char *Bm = bm ? sB1 : sB0;
+        const int rows = bm ? C::B1 : C::B0;
+        for (int k = p * (H / KS); k < (p + 1) * (H / KS); k += 8) {
+          const int ka = k >> 6, c8 = (k >> 3) & 7;
+          float w[8];
+          const unsigned char *hp, *lp = nullptr;
+          if constexpr (C::MERGE) {
+            hp = Bm + (size_t)ka * 2 * rows * 128 + sw128_off(cc, c8);
+            lp = Bm + (size_t)ka * 2 * rows * 128 + sw128_off(rows + cc, c8);
+          } else {
+            hp = Bm + (size_t)ka * rows * 128 + sw128_off(cc, c8);
+            if (SP == 2) lp = Bm + (size_t)(ka + KA) * rows * 128 + sw128_off(cc, c8);
+          }
+          const uint4 hv = *reinterpret_cast<const uint4 *>(hp);
+          const unsigned hw[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            w[2 * e] = __uint_as_float(hw[e] << 16);
+            w[2 * e + 1] = __uint_as_float(hw[e] & 0xffff0000u);
+          }
+          if (SP == 2) {
+            const uint4 lv = *reinterpret_cast<const uint4 *>(lp);
+            const unsigned lw[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+              w[2 * e] += __uint_as_float(lw[e] << 16);
+              w[2 * e + 1] += __uint_as_float(lw[e] & 0xffff0000u);
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < FMX; t++) {
+            if (t < cnt) {
+              const float4 *ap = reinterpret_cast<const float4 *>(Af + ((size_t)sl * FMX + t) * H + k);
+              const float4 x0 = ap[0], x1 = ap[1];
+              float sacc = part[t];
+              sacc = fmaf(x0.x, w[0], sacc); sacc = fmaf(x0.y, w[1], sacc);
+              sacc = fmaf(x0.z, w[2], sacc); sacc = fmaf(x0.w, w[3], sacc);
+              sacc = fmaf(x1.x, w[4], sacc); sacc = fmaf(x1.y, w[5], sacc);
+              sacc = fmaf(x1.z, w[6], sacc); sacc = fmaf(x1.w, w[7], sacc);
+              part[t] = sacc;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < FMX; t++)
+        if (t < cnt) Dp[((size_t)p * FMX + t) * COLS + col] = part[t];
+    }
+    named_bar(5, kEpiThreads);
+    auto D = [&](int t, int col) {
+      float v = 0.f;
+#pragma unroll
+      for (int p = 0; p < KS; p++) v += Dp[((size_t)p * FMX + t) * COLS + col];
+      return v;
+    };
+    // 4. the cell epilogue per (node, unit)
+    for (int idx = ntid; idx < cnt * U; idx += kEpiThreads) {
+      const int t = idx / U, u = idx % U, i = lo + t, own = n_own[t], root = n_root[t];
+      const int uu = unit0 + u;
+      float h;
+      if constexpr (C::LSTM) {
+        float c = 0.f, vi = 0.f, vo = 0.f, vu = 0.f;
+#pragma unroll
+        for (int k = 0; k < J; k++) {
+          const int ck = n_ck[k * FMX + t];
+          if (ck < 0) continue;
+          c = fmaf(act_sig<SP>(D(t, k * NC + 3 * U + u) + s_bias[3 * U + u]), __ldcg(cs + (size_t)ck * H + uu), c);
+          vi += D(t, k * NC + u);
+          vo += D(t, k * NC + U + u);
+          vu += D(t, k * NC + 2 * U + u);
+        }
+        c = fmaf(act_sig<SP>(vi + s_bias[u]), act_tanh<SP>(vu + s_bias[2 * U + u]), c);
+        h = act_sig<SP>(vo + s_bias[U + u]) * act_tanh<SP>(c);
+        cs[(size_t)(sbase + i) * H + uu] = c;
+        if (a.aux_out) a.aux_out[(size_t)own * H + uu] = c;
+        const int ps = n_ps[t];
+        if (ps >= 0) {
+          unsigned short *prow = a.pb + (size_t)ps * RW;
+          const float hi_ = bf16_round(h);
+          prow[uu] = (unsigned short)(__float_as_uint(hi_) >> 16);
+          if (SP == 2) prow[H + uu] = (unsigned short)(__float_as_uint(bf16_round(h - hi_)) >> 16);
+        }
+      } else {
+        float v = D(t, u);
+        if (hx) v += __ldcg(a.hf + (size_t)n_xr[t] * H + uu);
+        else v += s_bias[u];
+        h = act_tanh<SP>(v);
+        unsigned short *hrow = hb + (size_t)i * RW;
+        const float hi_ = bf16_round(h);
+        hrow[uu] = (unsigned short)(__float_as_uint(hi_) >> 16);
+        if (SP == 2) hrow[H + uu] = (unsigned short)(__float_as_uint(bf16_round(h - hi_)) >> 16);
+      }
+      a.h_out[(size_t)own * H + uu] = h;
+      if (root >= 0) a.root_out[(size_t)root * H + uu] = h;
+    }
+    fence_proxy_async();  // the stage ring (generic writes) is TMA's again next level
+    named_bar(5, kEpiThreads);
+  };
+  auto fma_level = [&](int l, int lo, int hi) {
+    for (int b0 = lo; b0 < hi; b0 += FMX) fma_batch(l, b0, min(hi, b0 + FMX));
+  };
+
   if (warp >= kMeta0) {
     // ======================== tile bookkeeping ===============================
     // It depends on the linearization only, so these warps run ahead of the
@@ -663,7 +883,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
       if (C::FC && leaf) continue;  // TreeFC leaves: a copy, no tiles
       int lo, hi;
       level_range(l, lo, hi);
-      const int ntiles = (hi - lo + kTM - 1) / kTM;
+      const int ntiles = is_fma(l) ? 0 : (hi - lo + kTM - 1) / kTM;
       const uint32_t T0 = T0m;
       // lane handles rows lane + 32 q; two dependent rounds of index loads
       const int mw = warp - kMeta0;
@@ -816,8 +1036,10 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
           continue;
         }
       }
-      const int ntiles = (hi - lo + kTM - 1) / kTM;
+      const bool fma_l = is_fma(l);
+      const int ntiles = fma_l ? 0 : (hi - lo + kTM - 1) / kTM;
       const int nsl = nsl_of(l);
+      if (fma_l && warp < kEpiWarps) fma_level(l, lo, hi);
 
       if (C::LSTM && warp == kFeed0) {
         // ========================= TMA tile loads ================================

@@ -44,6 +44,7 @@ struct FwdArgs {
   unsigned long long *trace;  // debug: %globaltimer per CTA and phase (cx_debug_set_trace)
   int trace_slots;
   int push_off;  // measurement/test: CX_PUSH=0 forces the cluster kernel's barrier + pull mode
+  int tc_fma_off;  // measurement/test: CX_TC_FMA=0 -- tensor-core kernel runs every level on UMMA tiles
   int bf16ops;   // dtype CX_BF16 on the FMA cluster path: operands rounded to bf16 (reading Q18)
   int discard_off;  // measurement: CX_DISCARD=0 keeps the tc kernel's dead workspace lines in L2
   LinArgs lin;  // fused linearize + forward (cx_linearize_forward): the linearizer's arguments

@@ -3,7 +3,9 @@ process group, world_size G, every rank on cuda:0 -- one GPU here) each run
 cx_linearize_forward on their contiguous block of structures, the packed root
 states are all-gathered over gloo, and the result equals the unsharded CUDA
 run BIT FOR BIT (per-node arithmetic does not depend on the batch
-composition: shard invariance)."""
+composition: shard invariance) on the FMA kernels; the
+tensor-core kernel's per-level FMA/UMMA dispatch depends on level sizes, so
+its shards agree within the bf16 tolerance."""
 import os
 import socket
 
@@ -77,8 +79,20 @@ def test_sharded_cuda_equals_unsharded(tmp_path, world, name, dtype):
     h_all, roots_all = _run_cuda(w, w["children"], w["words"], dtype)
     got = np.load(tmp_path / "roots.npy")
     assert got.shape == tuple(roots_all.shape)
-    assert np.array_equal(got, roots_all.numpy()), "gathered roots differ from the unsharded run"
     off = w["offsets"]
+    if dtype == "bf16":
+        # the tensor-core kernel dispatches per level by level size (small
+        # levels on FMA): a shard's smaller levels may take
+        # the other unit, which changes only the fp32 summation order
+        def close(x, y):
+            return (np.abs(x - y).max(axis=1) / np.maximum(np.abs(y).max(axis=1), 1e-6)).max()
+        assert close(got, roots_all.numpy()) <= 2e-2
+        for r in range(world):
+            g0, g1 = shard.block_range(len(off) - 1, r, world)
+            hr = np.load(tmp_path / f"h{r}.npy")
+            assert close(hr, h_all.numpy()[off[g0]:off[g1]]) <= 2e-2, f"rank {r} h rows differ"
+        return
+    assert np.array_equal(got, roots_all.numpy()), "gathered roots differ from the unsharded run"
     for r in range(world):
         g0, g1 = shard.block_range(len(off) - 1, r, world)
         hr = np.load(tmp_path / f"h{r}.npy")
