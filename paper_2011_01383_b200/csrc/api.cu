@@ -107,11 +107,14 @@ namespace {
 constexpr int kBf16FcFmaMaxN = 1024;
 // fp32 batches of TreeLSTM / DAG-RNN / TreeFC with at least this many nodes run
 // the split-fp32 tensor-core kernel (forward_tc.cu, SP = 2): their levels are
-// dense GEMMs. CX_TC_F32_MIN_N overrides (measurement).
-constexpr int kTcF32MinN = 2048;
-int tc_f32_min_n() {
+// dense GEMMs. Per cell, from the measured crossover against the FMA kernels
+// (tools/tc32_crossover.py): TreeLSTM between 1,950 and 3,900
+// nodes, DAG-RNN between 5,000 and 10,000, TreeFC (H = 512) near 600.
+// CX_TC_F32_MIN_N overrides (measurement).
+int tc_f32_min_n(int cell) {
   const char *e = std::getenv("CX_TC_F32_MIN_N");
-  return e ? std::atoi(e) : kTcF32MinN;
+  if (e) return std::atoi(e);
+  return cell == CX_TREELSTM ? 3000 : cell == CX_DAGRNN ? 7000 : 1000;
 }
 // The one forward plan of a call (caller holds g_mu). fp32: the fused cluster /
 // single-CTA kernels (cx_linearize_forward) or fwd_plan. bf16 ("per-batch
@@ -147,7 +150,7 @@ bool plan_forward(const cx_model *m, int maxc, int n, int kind, bool fused, int 
   // linearization stays on FMA: that kernel hands each h to ONE parent slot)
   const bool tc_cell = m->cell == CX_TREELSTM || m->cell == CX_DAGRNN || m->cell == CX_TREEFC;
   if (tc_cell && !(m->cell == CX_TREELSTM && kind == CX_DAG) &&
-      (path == 5 || (path == 0 && n >= tc_f32_min_n())) &&
+      (path == 5 || (path == 0 && n >= tc_f32_min_n(m->cell))) &&
       cx::tc_plan(m->cell, m->hidden, maxc, 2, sms, plan, Gn, Gu))
     return true;
   return cx::fwd_plan(m->cell, m->hidden, maxc, n, path == 5 ? 0 : path, sms, plan, Gn, Gu);

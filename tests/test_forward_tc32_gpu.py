@@ -5,7 +5,7 @@ oracle at the fp32 tolerance: max per-node normwise relative error <= 1e-4
 (BASELINE.json north_star). Forced with CX_FORWARD_PATH=tc at every size
 (inputs spanning several 128-node tiles per CTA with ragged tails, both
 input-row modes, sequences, child-sum arity 1..2, the BASELINE.json configs
-the kernel covers); the automatic dispatch (batches >= 2,048 nodes) at the
+the kernel covers); the automatic dispatch (large batches, per-cell thresholds) at the
 full batch-4096 configs, sampled; a TreeLSTM DAG linearization stays on FMA."""
 import numpy as np
 import pytest
