@@ -66,6 +66,9 @@ using namespace umma;
 #ifndef CX_TC_SKIP_LO  // timing experiment only: drop the A_hi B_lo MMAs (wrong numerics)
 #define CX_TC_SKIP_LO 0
 #endif
+#ifndef CX_TC_TMA_MC  // measurement: the multicast TMA form even for single-CTA clusters
+#define CX_TC_TMA_MC 0
+#endif
 #ifndef CX_TC_SMAX
 #define CX_TC_SMAX 8
 #endif
@@ -1063,9 +1066,14 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
                 mbar_arrive_expect_tx(&bar_full[st], kStageBytes);
                 // child slot k: rows k*n + i0 + ..; x: word rows (hoisted) or node-order rows
                 const int row0 = src >= 0 ? src * n + i0 : (hoist ? i0 : i0 - xlo);
-                tma_tile2d_mc(smem_u32(sStage + (size_t)st * kStageBytes),
-                              src >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x,
-                              &bar_full[st], ka * 64, row0, (uint16_t)1);
+                if (C::CL == 1 && !CX_TC_TMA_MC)
+                  tma_tile2d(smem_u32(sStage + (size_t)st * kStageBytes),
+                             src >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x,
+                             &bar_full[st], ka * 64, row0);
+                else
+                  tma_tile2d_mc(smem_u32(sStage + (size_t)st * kStageBytes),
+                                src >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x,
+                                &bar_full[st], ka * 64, row0, (uint16_t)1);
               }
               __syncwarp();
               tc_mark(a, sslot + 1, kFeed0 * 32);
@@ -1154,7 +1162,8 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
                     mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b1 + kk * 32), idesc, 1u);
                 }
                 started |= 1u << acc;
-                mma_commit_mc(&bar_empty[st], (uint16_t)((1u << C::CL) - 1));  // frees the slot cluster-wide
+                if (C::CL == 1 && !CX_TC_TMA_MC) mma_commit(&bar_empty[st]);  // frees the slot
+                else mma_commit_mc(&bar_empty[st], (uint16_t)((1u << C::CL) - 1));  // ... cluster-wide
                 tc_mark(a, sslot + 3, kMmaWarp * 32);
                 Sg++;
               }

@@ -194,6 +194,14 @@ __device__ __forceinline__ void tma_gather4_mc(uint32_t dst, const void *tmap, u
 }
 // 2D tile load (box of the tensor map at {c0, c1}) delivered to every CTA in
 // `mask` (same smem offset / mbarrier offset in each), complete_tx on `bar`.
+// 2D tensor tile load into this CTA's shared memory (no multicast)
+__device__ __forceinline__ void tma_tile2d(uint32_t dst, const void *tmap, uint64_t *bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma_tile2d_mc(uint32_t dst, const void *tmap, uint64_t *bar, int c0,
                                               int c1, uint16_t mask) {
   asm volatile(
