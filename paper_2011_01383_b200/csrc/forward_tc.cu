@@ -72,6 +72,9 @@ using namespace umma;
 #ifndef CX_TC_SMAX
 #define CX_TC_SMAX 8
 #endif
+#ifndef CX_TC_NAB  // K-atoms per TreeLSTM TMA stage (one 3D box)
+#define CX_TC_NAB 2
+#endif
 #ifndef CX_TC_FML_FC  // split TreeFC: nodes per node group up to which a level runs on FMA
 #define CX_TC_FML_FC 10
 #endif
@@ -161,10 +164,16 @@ struct TcCfg {
   static constexpr size_t bbytes0 = (size_t)B0 * KAA * 128, bbytes1 = (size_t)B1 * KAA * 128;
   static constexpr size_t bregion = BSHARE ? (bbytes0 > bbytes1 ? bbytes0 : bbytes1) : bbytes0 + bbytes1;
   static constexpr size_t static_bytes = sizeof(TcMeta<J>) * kMetaRing + 4 * U * 4 + 64 * 8 + 64;
+  // TreeLSTM stages hold NAB K-atoms, loaded by ONE 3D TMA instruction:
+  // tools/micro/tma_rate.cu measures ~0.36 us per TMA instruction per issuing
+  // thread whatever its size (16 KB: 45 GB/s/SM, 32 KB: 87, 64 KB: 137), so
+  // the one-lane producer feeds twice as fast with 2-atom boxes
+  static constexpr int NAB = LSTM && KAA % CX_TC_NAB == 0 ? CX_TC_NAB : 1;
+  static constexpr int STB = kStageBytes * NAB;  // bytes per stage
   static constexpr int S_fit =
-      (int)((kSmemLimit - 1024 - static_bytes - bregion) / kStageBytes);
+      (int)((kSmemLimit - 1024 - static_bytes - bregion) / STB);
   static constexpr int S = S_fit > CX_TC_SMAX ? CX_TC_SMAX : S_fit;
-  static constexpr size_t dyn_bytes = 1024 + bregion + (size_t)S * kStageBytes;
+  static constexpr size_t dyn_bytes = 1024 + bregion + (size_t)S * STB;
   static_assert(H % 64 == 0 && H % U == 0, "H must be a multiple of 64 and of U");
   static_assert(BUFC * 2 <= 512, "TMEM: two accumulator buffers must fit 512 columns");
   static_assert(NLVL * MW <= 256 && NLEAF * MW <= 256 && NLVL % 16 == 0, "UMMA N");
@@ -682,7 +691,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
     constexpr int NSLM = C::LSTM ? J : C::DAG ? J + 1 : 2;
     static_assert(COLS <= kEpiThreads && kEpiThreads % COLS == 0 && (H / KS) % 8 == 0, "FMA split");
     constexpr size_t kAf = (size_t)NSLM * FMX * H, kDp = (size_t)KS * FMX * COLS;
-    static_assert(4 * (kAf + kDp) + 4 * FMX * (8 + 2 * J) <= (size_t)S * kStageBytes, "FMA level fits the stage ring");
+    static_assert(4 * (kAf + kDp) + 4 * FMX * (8 + 2 * J) <= (size_t)S * C::STB, "FMA level fits the stage ring");
     const int cnt = hi - lo, ntid = tid;  // tid < kEpiThreads
     const int nsl = nsl_of(l);
     float *Af = reinterpret_cast<float *>(sStage), *Dp = Af + kAf;
@@ -1053,7 +1062,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         uint32_t Sg = Sg0;
         for (int t = 0; t < ntiles; t++) {
           const int i0 = lo + t * kTM;
-          for (int ka = 0; ka < KAA; ka++) {
+          for (int ka = 0; ka < KAA; ka += C::NAB) {
             for (int s = 0; s < nsl; s++) {
               int src, bm, acc;
               slot_of(l, s, src, bm, acc);
@@ -1063,17 +1072,17 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
               mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);
               tc_mark(a, sslot + 0, kFeed0 * 32);
               if (lane == 0) {
-                mbar_arrive_expect_tx(&bar_full[st], kStageBytes);
+                mbar_arrive_expect_tx(&bar_full[st], C::STB);
                 // child slot k: rows k*n + i0 + ..; x: word rows (hoisted) or node-order rows
                 const int row0 = src >= 0 ? src * n + i0 : (hoist ? i0 : i0 - xlo);
-                if (C::CL == 1 && !CX_TC_TMA_MC)
-                  tma_tile2d(smem_u32(sStage + (size_t)st * kStageBytes),
-                             src >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x,
-                             &bar_full[st], ka * 64, row0);
+                const void *tm = src >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x;
+                const uint32_t dst = smem_u32(sStage + (size_t)st * C::STB);
+                if (C::NAB > 1)  // atoms ka .. ka + NAB - 1 of the 128 rows, atom after atom
+                  tma_tile3d(dst, tm, &bar_full[st], 0, row0, ka);
+                else if (C::CL == 1 && !CX_TC_TMA_MC)
+                  tma_tile2d(dst, tm, &bar_full[st], ka * 64, row0);
                 else
-                  tma_tile2d_mc(smem_u32(sStage + (size_t)st * kStageBytes),
-                                src >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x,
-                                &bar_full[st], ka * 64, row0, (uint16_t)1);
+                  tma_tile2d_mc(dst, tm, &bar_full[st], ka * 64, row0, (uint16_t)1);
               }
               __syncwarp();
               tc_mark(a, sslot + 1, kFeed0 * 32);
@@ -1101,7 +1110,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
               slot_of(l, s, src, bm, acc);
               const int st = Sg % S;
               mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);
-              const uint32_t dst0 = smem_u32(sStage + (size_t)st * kStageBytes);
+              const uint32_t dst0 = smem_u32(sStage + (size_t)st * C::STB);
               const int *rows = src < 0 ? m.xr : m.ch[src];
               const unsigned short *base = src < 0 ? xb : hb;
 #pragma unroll
@@ -1131,7 +1140,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
             const int tslot = (l >= 0 && l < 2 && t < 5) ? 128 + 12 * (t + 5 * l) : 1 << 30;
             tc_mark(a, tslot + 2, kMmaWarp * 32);
             uint32_t started = 0;
-            for (int ka = 0; ka < KAA; ka++) {
+            for (int ka0 = 0; ka0 < KAA; ka0 += C::NAB) {
               for (int s = 0; s < nsl; s++) {
                 int src, bm, acc;
                 slot_of(l, s, src, bm, acc);
@@ -1142,26 +1151,29 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
                 tc_mark(a, sslot + 2, kMmaWarp * 32);
                 if (!C::LSTM) fence_proxy_async();  // landed cp.async data (generic proxy) -> tensor core
                 fence_after();
-                const uint32_t a0 = smem_u32(sStage + (size_t)st * kStageBytes);
-                const size_t brows = bm ? C::B1 : C::B0;
-                unsigned char *bbase = bm ? sB1 : sB0;
-                // SP = 2: a hi atom (ka < KA) meets B_hi and B_lo, a lo atom B_hi
-                const int kb = ka < KA ? ka : ka - KA;
-                const uint32_t b0 = smem_u32(bbase + (size_t)kb * brows * C::MW * 128);
-                const uint32_t d = tmem + buf * C::BUFC + acc * ncol;
-                const uint32_t idk = (C::MERGE && ka < KA) ? idesc2 : idesc;  // N = 2R: B_hi and B_lo at once
-  #pragma unroll
-                for (int kk = 0; kk < 4; kk++) {
-                  const uint32_t accum = ((started >> acc) & 1u) | (kk > 0 ? 1u : 0u);
-                  mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idk, accum);
+                for (int aj = 0; aj < C::NAB; aj++) {  // the stage's K-atoms
+                  const int ka = ka0 + aj;
+                  const uint32_t a0 = smem_u32(sStage + (size_t)st * C::STB + (size_t)aj * kStageBytes);
+                  const size_t brows = bm ? C::B1 : C::B0;
+                  unsigned char *bbase = bm ? sB1 : sB0;
+                  // SP = 2: a hi atom (ka < KA) meets B_hi and B_lo, a lo atom B_hi
+                  const int kb = ka < KA ? ka : ka - KA;
+                  const uint32_t b0 = smem_u32(bbase + (size_t)kb * brows * C::MW * 128);
+                  const uint32_t d = tmem + buf * C::BUFC + acc * ncol;
+                  const uint32_t idk = (C::MERGE && ka < KA) ? idesc2 : idesc;  // N = 2R: B_hi and B_lo at once
+    #pragma unroll
+                  for (int kk = 0; kk < 4; kk++) {
+                    const uint32_t accum = ((started >> acc) & 1u) | (kk > 0 ? 1u : 0u);
+                    mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b0 + kk * 32), idk, accum);
+                  }
+                  if (SP == 2 && !C::MERGE && ka < KA && !CX_TC_SKIP_LO) {
+                    const uint32_t b1 = smem_u32(bbase + (size_t)(kb + KA) * brows * 128);
+    #pragma unroll
+                    for (int kk = 0; kk < 4; kk++)
+                      mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b1 + kk * 32), idesc, 1u);
+                  }
+                  started |= 1u << acc;
                 }
-                if (SP == 2 && !C::MERGE && ka < KA && !CX_TC_SKIP_LO) {
-                  const uint32_t b1 = smem_u32(bbase + (size_t)(kb + KA) * brows * 128);
-  #pragma unroll
-                  for (int kk = 0; kk < 4; kk++)
-                    mma_bf16(d, sdesc_sw128(a0 + kk * 32), sdesc_sw128(b1 + kk * 32), idesc, 1u);
-                }
-                started |= 1u << acc;
                 if (C::CL == 1 && !CX_TC_TMA_MC) mma_commit(&bar_empty[st]);  // frees the slot
                 else mma_commit_mc(&bar_empty[st], (uint16_t)((1u << C::CL) - 1));  // ... cluster-wide
                 tc_mark(a, sslot + 3, kMmaWarp * 32);
@@ -1342,7 +1354,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         tc_mark(a, l >= 0 ? 5 + 4 * l : -1, 0);
       }
       T0 += ntiles;
-      Sg0 += (uint32_t)ntiles * KAA * nsl;
+      Sg0 += (uint32_t)ntiles * (KAA / C::NAB) * nsl;
       if (nsl > 0) A0 += ntiles;
     }
 
@@ -1420,6 +1432,7 @@ bool tc_plan_one(int num_sms, FwdPlan *p, int *Gn, int *Gu) {
   p->big = false;
   p->tc = true;
   p->tc_sp = SP;
+  p->tc_nab = C::NAB;
   return true;
 }
 
@@ -1495,6 +1508,20 @@ bool encode_rows(TmaDesc *d, const void *base, int H, long long rows, int box_ro
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// the same rows as a 3D tensor {64 columns, rows, K-atoms} (strides: row =
+// H * 2 bytes, atom = 128 bytes), box {64, box_rows, nab}: nab K-atoms of
+// box_rows rows per load, landing atom after atom (each a K-major SW128 block)
+bool encode_rows3(TmaDesc *d, const void *base, int H, long long rows, int box_rows, int nab) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || rows < 1 || H % 64) return false;
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(H / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)H * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)nab}, es[3] = {1, 1, 1};
+  return fn(reinterpret_cast<CUtensorMap *>(d), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+            const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 }  // namespace
 
 cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &f, cudaStream_t stream) {
@@ -1505,8 +1532,13 @@ cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &f, cudaStream_t stream
   const long long xrows = f.xmode ? f.n : f.V;
   if (f.pb) {  // TreeLSTM: contiguous operands, 128-row tile loads of rows of sp x H bf16
     const int rw = plan.tc_sp * f.H;
-    if (!encode_rows(&ta.tm_p, f.pb, rw, 2LL * f.n, kTM)) return cudaErrorInvalidValue;
-    if (!encode_rows(&ta.tm_x, f.xb, rw, xrows, kTM)) return cudaErrorInvalidValue;
+    if (plan.tc_nab > 1) {  // NAB K-atoms per load (3D box)
+      if (!encode_rows3(&ta.tm_p, f.pb, rw, 2LL * f.n, kTM, plan.tc_nab)) return cudaErrorInvalidValue;
+      if (!encode_rows3(&ta.tm_x, f.xb, rw, xrows, kTM, plan.tc_nab)) return cudaErrorInvalidValue;
+    } else {
+      if (!encode_rows(&ta.tm_p, f.pb, rw, 2LL * f.n, kTM)) return cudaErrorInvalidValue;
+      if (!encode_rows(&ta.tm_x, f.xb, rw, xrows, kTM)) return cudaErrorInvalidValue;
+    }
   }
   void *params[] = {&ta};
   cudaLaunchConfig_t cfg = {};

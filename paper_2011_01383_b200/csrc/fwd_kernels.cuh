@@ -89,6 +89,7 @@ struct FwdPlan {
   int family = 0;
   bool bf16ops = false;  // dtype CX_BF16 served by an FMA kernel with bf16-rounded operands
   int tc_sp = 1;         // tensor-core kernel operands: 1 bf16, 2 split fp32 (hi + lo bf16)
+  int tc_nab = 1;        // tensor-core kernel: K-atoms per TMA stage (3D tensor maps when > 1)
 };
 
 // Returns false (CX_E_UNSUPPORTED) when no instantiation covers the model.

@@ -202,6 +202,15 @@ __device__ __forceinline__ void tma_tile2d(uint32_t dst, const void *tmap, uint6
       ::"r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// 3D tensor tile load (coordinates innermost first) into this CTA's shared memory
+__device__ __forceinline__ void tma_tile3d(uint32_t dst, const void *tmap, uint64_t *bar, int c0, int c1,
+                                           int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma_tile2d_mc(uint32_t dst, const void *tmap, uint64_t *bar, int c0,
                                               int c1, uint16_t mask) {
   asm volatile(
