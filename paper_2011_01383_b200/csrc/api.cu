@@ -149,7 +149,7 @@ bool plan_forward(const cx_model *m, int maxc, int n, int kind, bool fused, int 
   // dense levels: the split-fp32 tensor-core kernel (a TreeLSTM DAG
   // linearization stays on FMA: that kernel hands each h to ONE parent slot)
   const bool tc_cell = m->cell == CX_TREELSTM || m->cell == CX_DAGRNN || m->cell == CX_TREEFC;
-  if (tc_cell && !(m->cell == CX_TREELSTM && kind == CX_DAG) &&
+  if (tc_cell && !((m->cell == CX_TREELSTM || m->cell == CX_TREEFC) && kind == CX_DAG) &&
       (path == 5 || (path == 0 && n >= tc_f32_min_n(m->cell))) &&
       cx::tc_plan(m->cell, m->hidden, maxc, 2, sms, plan, Gn, Gu))
     return true;
@@ -173,9 +173,19 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
     const bool ok = plan_forward(m, lin->max_children, n, lin->kind, fused != nullptr, sms, &plan,
                                  &Gn, &Gu);
     if (!ok) return CX_E_UNSUPPORTED;
-    // the bf16 tensor-core TreeLSTM stores each node's h in its ONE parent's
-    // child slot (forward_tc.cu): a DAG linearization (shared children) is refused
-    if (plan.tc && m->cell == CX_TREELSTM && lin->kind == CX_DAG) return CX_E_UNSUPPORTED;
+    // the tensor-core TreeLSTM / TreeFC store each node's h in its ONE parent's
+    // child slot (forward_tc.cu): a DAG linearization (shared children) is not
+    // run there (fp32 never plans it; bf16 TreeFC falls back, TreeLSTM is refused)
+    if (plan.tc && (m->cell == CX_TREELSTM || m->cell == CX_TREEFC) && lin->kind == CX_DAG) {
+      // a bf16 TreeFC over a DAG: the register-weight FMA kernel with rounded operands
+      plan = cx::FwdPlan();
+      if (m->cell == CX_TREEFC && m->dtype == CX_BF16 &&
+          cx::fwd_plan(m->cell, m->hidden, lin->max_children, n, 1, sms, &plan, &Gn, &Gu)) {
+        plan.bf16ops = true;
+      } else {
+        return CX_E_UNSUPPORTED;
+      }
+    }
   }
   const size_t N = (size_t)n, H = (size_t)m->hidden;
   char *p = align_up(static_cast<char *>(workspace), 128);
@@ -214,10 +224,12 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
       a.cs = reinterpret_cast<float *>(q);
       q = align_up(q + 4 * R * H, 256);
     }
-    a.xb = reinterpret_cast<unsigned short *>(q);
     a.xmode = cx::tc_xmode(n, m->vocab);
-    q = align_up(q + 2 * (a.xmode ? N : (size_t)m->vocab) * RW, 256);
     a.cell_has_x = m->cell == CX_TREELSTM || m->cell == CX_DAGRNN;
+    if (a.cell_has_x) {  // x rows (tc_workspace_bytes counts them for these cells only)
+      a.xb = reinterpret_cast<unsigned short *>(q);
+      q = align_up(q + 2 * (a.xmode ? N : (size_t)m->vocab) * RW, 256);
+    }
     a.hoist = cx::tc_hoist(m->cell, n, m->vocab, plan.tc_sp) ? 1 : 0;
     if (a.hoist) {
       a.hf = reinterpret_cast<float *>(q);
@@ -225,7 +237,7 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
       a.crow = reinterpret_cast<int *>(q);
       q = align_up(q + 4 * N, 256);
     }
-    if (m->cell == CX_TREELSTM) {
+    if (m->cell == CX_TREELSTM || m->cell == CX_TREEFC) {  // parent-slot operand rows
       a.pb = reinterpret_cast<unsigned short *>(q);
       q = align_up(q + 2 * (2 * N) * RW, 256);
       a.pslot = reinterpret_cast<int *>(q);

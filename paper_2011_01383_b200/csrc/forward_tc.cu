@@ -157,7 +157,11 @@ struct TcCfg {
   // slower: only 15 clusters of 8 are co-resident (120 CTAs instead of 144;
   // b4096 forward 293 -> 340 us).
   static constexpr int CL = 1;
-  static constexpr int FEEDW = LSTM ? 1 : 4;             // feeding warps
+  // TreeLSTM and TreeFC (trees: one parent per node) keep each node's operand
+  // row in its parent's child slot (pb), so a level tile's operands are
+  // contiguous rows loaded by TMA; DAG-RNN gathers rows with cp.async
+  static constexpr bool SLOTS = LSTM || FC;
+  static constexpr int FEEDW = SLOTS ? 1 : 4;            // feeding warps
   static constexpr int META0 = kFeed0 + FEEDW;           // first bookkeeping warp
   static constexpr int THREADS = 32 * (META0 + kMetaWarps);
   static constexpr int WORK = 32 * META0;                // threads of the working warps
@@ -168,7 +172,7 @@ struct TcCfg {
   // tools/micro/tma_rate.cu measures ~0.36 us per TMA instruction per issuing
   // thread whatever its size (16 KB: 45 GB/s/SM, 32 KB: 87, 64 KB: 137), so
   // the one-lane producer feeds twice as fast with 2-atom boxes
-  static constexpr int NAB = LSTM && KAA % CX_TC_NAB == 0 ? CX_TC_NAB : 1;
+  static constexpr int NAB = SLOTS && KAA % CX_TC_NAB == 0 ? CX_TC_NAB : 1;
   static constexpr int STB = kStageBytes * NAB;  // bytes per stage
   static constexpr int S_fit =
       (int)((kSmemLimit - 1024 - static_bytes - bregion) / STB);
@@ -358,7 +362,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
   // ---- prologue: barriers, TMEM, biases, resident bf16 weights ---------------
   if (tid == 0) {
     // full: TreeLSTM 1 arrive + TMA bytes; cp.async feeding: one noinc arrival per thread
-    for (int s = 0; s < S; s++) { mbar_init(&bar_full[s], C::LSTM ? 1 : 32 * C::FEEDW); mbar_init(&bar_empty[s], C::CL); }
+    for (int s = 0; s < S; s++) { mbar_init(&bar_full[s], C::SLOTS ? 1 : 32 * C::FEEDW); mbar_init(&bar_empty[s], C::CL); }
     for (int b = 0; b < 2; b++) { mbar_init(&bar_tfull[b], 1); mbar_init(&bar_tempty[b], kEpiThreads); }
     for (int m = 0; m < kMetaRing; m++) { mbar_init(&bar_mfull[m], 1); mbar_init(&bar_mempty[m], kEpiThreads); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -551,7 +555,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
       }
     }
   }
-  if (C::LSTM && status0 == CX_OK) {  // parent-slot row of every non-root node
+  if (C::SLOTS && status0 == CX_OK) {  // parent-slot row of every non-root node
     const size_t total_threads = (size_t)gridDim.x * blockDim.x;
     const size_t gt = (size_t)blockIdx.x * blockDim.x + tid;
     for (size_t pn = gt; pn < (size_t)first_leaf; pn += total_threads) {
@@ -706,7 +710,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         root = __ldg(a.roots + sv) == i ? sv : -1;
       }
       n_root[ntid] = root;
-      n_ps[ntid] = C::LSTM ? __ldcg(a.pslot + i) : -1;
+      n_ps[ntid] = C::SLOTS ? __ldcg(a.pslot + i) : -1;
       int xr = -1;
       if (C::DAG) {
         if (a.xmode == 0) {
@@ -732,7 +736,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         const int srow = c >= 0 ? (hoist ? __ldcg(a.crow + c) : c) : -1;  // the child's state row
         n_ck[k * FMX + ntid] = srow;
         // operand row of slot k: TreeLSTM the parent-slot row, else the state row
-        n_ch[k * FMX + ntid] = C::LSTM ? (c >= 0 ? k * n + i : -1) : srow;
+        n_ch[k * FMX + ntid] = C::SLOTS ? (c >= 0 ? k * n + i : -1) : srow;
       }
       if (C::FC && nc != 2 && latch) latch_error(a.hdr, CX_E_ARITY, own);
     }
@@ -744,7 +748,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
       int src, bm, acc;
       slot_of(l, sl, src, bm, acc);
       const int row = src < 0 ? n_xr[t] : n_ch[src * FMX + t];
-      const unsigned short *base = src < 0 ? xb : (C::LSTM ? a.pb : hb);
+      const unsigned short *base = src < 0 ? xb : (C::SLOTS ? a.pb : hb);
       float f[8];
       if (row >= 0) {
         const uint4 hv = __ldcg(reinterpret_cast<const uint4 *>(base + (size_t)row * RW + 8 * q));
@@ -870,10 +874,14 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         if (hx) v += __ldcg(a.hf + (size_t)n_xr[t] * H + uu);
         else v += s_bias[u];
         h = act_tanh<SP>(v);
-        unsigned short *hrow = hb + (size_t)i * RW;
-        const float hi_ = bf16_round(h);
-        hrow[uu] = (unsigned short)(__float_as_uint(hi_) >> 16);
-        if (SP == 2) hrow[H + uu] = (unsigned short)(__float_as_uint(bf16_round(h - hi_)) >> 16);
+        // the operand row: TreeFC the parent's child slot (none for a root), DAG-RNN the state row
+        unsigned short *hrow = C::SLOTS ? (n_ps[t] >= 0 ? a.pb + (size_t)n_ps[t] * RW : nullptr)
+                                        : hb + (size_t)i * RW;
+        if (hrow) {
+          const float hi_ = bf16_round(h);
+          hrow[uu] = (unsigned short)(__float_as_uint(hi_) >> 16);
+          if (SP == 2) hrow[H + uu] = (unsigned short)(__float_as_uint(bf16_round(h - hi_)) >> 16);
+        }
       }
       a.h_out[(size_t)own * H + uu] = h;
       if (root >= 0) a.root_out[(size_t)root * H + uu] = h;
@@ -932,7 +940,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
           for (int k = 0; k < J; k++) ch[q][k] = -1;
           if (r < cnt && !(leaf && hoist) && !proj) {
             own[q] = __ldg(a.perm + i);
-            if (C::LSTM) psv[q] = __ldcg(a.pslot + i);
+            if (C::SLOTS) psv[q] = __ldcg(a.pslot + i);
             if (a.root_out) sv[q] = __ldg(a.sid + i);
             if (!leaf) {
 #pragma unroll
@@ -999,7 +1007,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         fence_proxy_async();
         named_bar(3, kWork);
       }
-      if (C::LSTM && discard_ok && l >= 2) {
+      if (C::SLOTS && discard_ok && l >= 2) {
         // level l - 1 is complete: its tiles' parent-slot operand rows (rows
         // k n + [lbeg, lbeg + lsize) of pb, loaded by every unit-group CTA) are
         // dead; every CTA drops a share of their 128-byte lines
@@ -1031,13 +1039,16 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
             }
             const float4 v = __ldg(reinterpret_cast<const float4 *>(a.emb + (size_t)w * H + unit0) + c);
             *reinterpret_cast<float4 *>(a.h_out + (size_t)own * H + unit0 + 4 * c) = v;
-            *reinterpret_cast<uint2 *>(hb + (size_t)i * RW + unit0 + 4 * c) =
-                make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
-            if constexpr (SP == 2) {
-              const float4 l4 = make_float4(v.x - bf16_round(v.x), v.y - bf16_round(v.y),
-                                            v.z - bf16_round(v.z), v.w - bf16_round(v.w));
-              *reinterpret_cast<uint2 *>(hb + (size_t)i * RW + H + unit0 + 4 * c) =
-                  make_uint2(pack_bf16(l4.x, l4.y), pack_bf16(l4.z, l4.w));
+            const int ps = __ldcg(a.pslot + i);  // the parent's child-slot row (-1: a root)
+            if (ps >= 0) {
+              unsigned short *prow = a.pb + (size_t)ps * RW;
+              *reinterpret_cast<uint2 *>(prow + unit0 + 4 * c) = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+              if constexpr (SP == 2) {
+                const float4 l4 = make_float4(v.x - bf16_round(v.x), v.y - bf16_round(v.y),
+                                              v.z - bf16_round(v.z), v.w - bf16_round(v.w));
+                *reinterpret_cast<uint2 *>(prow + H + unit0 + 4 * c) =
+                    make_uint2(pack_bf16(l4.x, l4.y), pack_bf16(l4.z, l4.w));
+              }
             }
             if (a.root_out) {
               const int r = __ldg(a.sid + i);
@@ -1053,7 +1064,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
       const int nsl = nsl_of(l);
       if (fma_l && warp < kEpiWarps) fma_level(l, lo, hi);
 
-      if (C::LSTM && warp == kFeed0) {
+      if (C::SLOTS && warp == kFeed0) {
         // ========================= TMA tile loads ================================
         // per stage: one K-atom (64 bf16) of one slot for the tile's 128 rows
         // with one 2D tile load: TreeLSTM operands are contiguous (h stored in
@@ -1091,7 +1102,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
           }
         }
         tc_mark(a, l >= 0 ? 3 + 4 * l : -1, kFeed0 * 32);
-      } else if (!C::LSTM && warp >= kFeed0 && warp < kMeta0) {
+      } else if (!C::SLOTS && warp >= kFeed0 && warp < kMeta0) {
         // ========================= cp.async gathers ==============================
         // per stage: one K-atom of one slot for the tile's 128 rows, 16-byte
         // cp.async into the swizzled layout (zero-fill: absent child, unused
@@ -1149,7 +1160,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
                 const int sslot = (l == 1 && kst < 16) ? 64 + 4 * kst : 1 << 30;
                 mbar_wait(&bar_full[st], (Sg / S) & 1);
                 tc_mark(a, sslot + 2, kMmaWarp * 32);
-                if (!C::LSTM) fence_proxy_async();  // landed cp.async data (generic proxy) -> tensor core
+                if (!C::SLOTS) fence_proxy_async();  // landed cp.async data (generic proxy) -> tensor core
                 fence_after();
                 for (int aj = 0; aj < C::NAB; aj++) {  // the stage's K-atoms
                   const int ka = ka0 + aj;
@@ -1341,7 +1352,11 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
               if (valid) {
                 const int uu = unit0 + u0 + q * CW;
                 st_row_cs<CW>(a.h_out + (size_t)own * H + uu, v);
-                st_op<SP, H, CW>(hb + (size_t)i * RW, uu, v);
+                if constexpr (C::SLOTS) {  // TreeFC: the parent's child-slot row
+                  if (m.ps[r] >= 0) st_op<SP, H, CW>(a.pb + (size_t)m.ps[r] * RW, uu, v);
+                } else {
+                  st_op<SP, H, CW>(hb + (size_t)i * RW, uu, v);
+                }
                 if (root >= 0) st_row_cs<CW>(a.root_out + (size_t)root * H + uu, v);
               }
             }
@@ -1534,10 +1549,10 @@ cudaError_t tc_launch(const FwdPlan &plan, const FwdArgs &f, cudaStream_t stream
     const int rw = plan.tc_sp * f.H;
     if (plan.tc_nab > 1) {  // NAB K-atoms per load (3D box)
       if (!encode_rows3(&ta.tm_p, f.pb, rw, 2LL * f.n, kTM, plan.tc_nab)) return cudaErrorInvalidValue;
-      if (!encode_rows3(&ta.tm_x, f.xb, rw, xrows, kTM, plan.tc_nab)) return cudaErrorInvalidValue;
+      if (f.xb && !encode_rows3(&ta.tm_x, f.xb, rw, xrows, kTM, plan.tc_nab)) return cudaErrorInvalidValue;
     } else {
       if (!encode_rows(&ta.tm_p, f.pb, rw, 2LL * f.n, kTM)) return cudaErrorInvalidValue;
-      if (!encode_rows(&ta.tm_x, f.xb, rw, xrows, kTM)) return cudaErrorInvalidValue;
+      if (f.xb && !encode_rows(&ta.tm_x, f.xb, rw, xrows, kTM)) return cudaErrorInvalidValue;
     }
   }
   void *params[] = {&ta};
@@ -1595,7 +1610,7 @@ size_t tc_workspace_bytes(int cell, int H, int V, int n, int sp) {
   if (cell == CX_TREELSTM || cell == CX_DAGRNN)                 // xb
     b += 2 * (tc_xmode(n, V) ? N : (size_t)V) * rw + 256;
   if (tc_hoist(cell, n, V, sp)) b += 4 * (size_t)V * h + 4 * N + 512;  // hf, crow
-  if (cell == CX_TREELSTM) b += 2 * (2 * N) * rw + 4 * N + 512;    // pb (J <= 2), pslot
+  if (cell == CX_TREELSTM || cell == CX_TREEFC) b += 2 * (2 * N) * rw + 4 * N + 512;  // pb (J <= 2), pslot
   return b;
 }
 

@@ -172,3 +172,12 @@ def test_single_nodes(cx):
     _parity(cx, T.TREELSTM, 128, 50, ch, T.TREE, seed=1)
     _parity(cx, T.DAGRNN, 128, 50, ch, T.DAG, seed=1)
     _parity(cx, T.TREEFC, 256, 50, ch, T.TREE, seed=1)
+
+
+def test_treefc_dag_linearization_not_on_slots(cx):
+    """TreeFC over a DAG linearization (a child shared by two parents): the
+    tensor-core kernel hands each h to ONE parent slot, so the bf16 call runs
+    the register-weight FMA kernel instead -- and still matches the oracle."""
+    # leaves 3, 4, 5; 1 = (3, 4), 2 = (4, 5), 0 = (1, 2): node 4 has two parents
+    ch = np.array([[1, 3, 4, -1, -1, -1], [2, 4, 5, -1, -1, -1]], np.int32)
+    _parity(cx, T.TREEFC, 256, 40, ch, T.DAG, seed=9)
