@@ -72,6 +72,9 @@ using namespace umma;
 #ifndef CX_TC_SMAX
 #define CX_TC_SMAX 8
 #endif
+#ifndef CX_TC_TMA_LANES  // lanes of the TMA warp issuing stages side by side (measured: 2 or 3
+#define CX_TC_TMA_LANES 1    // lanes slowed the split-fp32 TreeLSTM / TreeFC by 3-7 %, bf16 +-0)
+#endif
 #ifndef CX_TC_NAB  // K-atoms per TreeLSTM TMA stage (one 3D box)
 #define CX_TC_NAB 2
 #endif
@@ -1066,40 +1069,42 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
 
       if (C::SLOTS && warp == kFeed0) {
         // ========================= TMA tile loads ================================
-        // per stage: one K-atom (64 bf16) of one slot for the tile's 128 rows
-        // with one 2D tile load: TreeLSTM operands are contiguous (h stored in
-        // the parent's child-slot row, x rows word- or node-ordered); rows of
-        // absent children / padding rows are not read by the epilogue
-        uint32_t Sg = Sg0;
-        for (int t = 0; t < ntiles; t++) {
-          const int i0 = lo + t * kTM;
-          for (int ka = 0; ka < KAA; ka += C::NAB) {
-            for (int s = 0; s < nsl; s++) {
-              int src, bm, acc;
-              slot_of(l, s, src, bm, acc);
-              const int st = Sg % S;
-              const int kst = (int)(Sg - Sg0);
-              const int sslot = (l == 1 && kst < 16) ? 64 + 4 * kst : 1 << 30;
-              mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);
-              tc_mark(a, sslot + 0, kFeed0 * 32);
-              if (lane == 0) {
-                mbar_arrive_expect_tx(&bar_full[st], C::STB);
-                // child slot k: rows k*n + i0 + ..; x: word rows (hoisted) or node-order rows
-                const int row0 = src >= 0 ? src * n + i0 : (hoist ? i0 : i0 - xlo);
-                const void *tm = src >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x;
-                const uint32_t dst = smem_u32(sStage + (size_t)st * C::STB);
-                if (C::NAB > 1)  // atoms ka .. ka + NAB - 1 of the 128 rows, atom after atom
-                  tma_tile3d(dst, tm, &bar_full[st], 0, row0, ka);
-                else if (C::CL == 1 && !CX_TC_TMA_MC)
-                  tma_tile2d(dst, tm, &bar_full[st], ka * 64, row0);
-                else
-                  tma_tile2d_mc(dst, tm, &bar_full[st], ka * 64, row0, (uint16_t)1);
-              }
-              __syncwarp();
-              tc_mark(a, sslot + 1, kFeed0 * 32);
-              Sg++;
-            }
+        // per stage: NAB K-atoms (64 bf16 each) of one slot for the tile's 128
+        // rows with one tile load: TreeLSTM / TreeFC operands are contiguous
+        // (h stored in the parent's child-slot row, x rows word- or
+        // node-ordered); rows of absent children / padding rows are not read
+        // by the epilogue
+        // TPL lanes issue consecutive stages side by side (a thread completes
+        // about one TMA load per 0.36 us, tools/micro/tma_rate.cu): stage
+        // q = (t * nka + ka / NAB) * nsl + s of this level goes to lane q % TPL
+        constexpr int TPL = CX_TC_TMA_LANES < S ? CX_TC_TMA_LANES : S;  // <= S stages at once
+        const int nka = KAA / C::NAB, total = ntiles * nka * nsl;
+        for (int q0 = 0; q0 < total; q0 += TPL) {
+          const int q = q0 + lane;
+          if (lane < TPL && q < total) {
+            const int s = q % nsl, kq = (q / nsl) % nka, t = q / (nsl * nka);
+            const int ka = kq * C::NAB, i0 = lo + t * kTM;
+            const uint32_t Sg = Sg0 + (uint32_t)q;
+            int src, bm, acc;
+            slot_of(l, s, src, bm, acc);
+            const int st = Sg % S;
+            const int sslot = (l == 1 && q < 16) ? 64 + 4 * q : 1 << 30;
+            mbar_wait(&bar_empty[st], ((Sg / S) & 1) ^ 1);
+            tc_mark(a, sslot + 0, kFeed0 * 32);
+            mbar_arrive_expect_tx(&bar_full[st], C::STB);
+            // child slot k: rows k*n + i0 + ..; x: word rows (hoisted) or node-order rows
+            const int row0 = src >= 0 ? src * n + i0 : (hoist ? i0 : i0 - xlo);
+            const void *tm = src >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x;
+            const uint32_t dst = smem_u32(sStage + (size_t)st * C::STB);
+            if (C::NAB > 1)  // atoms ka .. ka + NAB - 1 of the 128 rows, atom after atom
+              tma_tile3d(dst, tm, &bar_full[st], 0, row0, ka);
+            else if (C::CL == 1 && !CX_TC_TMA_MC)
+              tma_tile2d(dst, tm, &bar_full[st], ka * 64, row0);
+            else
+              tma_tile2d_mc(dst, tm, &bar_full[st], ka * 64, row0, (uint16_t)1);
+            tc_mark(a, sslot + 1, kFeed0 * 32);
           }
+          __syncwarp();
         }
         tc_mark(a, l >= 0 ? 3 + 4 * l : -1, kFeed0 * 32);
       } else if (!C::SLOTS && warp >= kFeed0 && warp < kMeta0) {
