@@ -42,27 +42,28 @@ UNIT = "trees/s"
 FMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4: SMs x FP32 lanes x 2 x max clock
 
 WORKLOADS = {
-    # name: (generator, cell, hidden, vocab, batch, scaling). Every workload is
-    # one fixed batch of independent structures split across the N ranks
-    # (strong scaling): at N > 1 the b10 line is "batch-10
-    # latency sharded 5/3/2 per rank", the b4096 lines the trees/s headline.
-    "cfg2_treelstm_b10": ("sst", synth.TREELSTM, 256, 20000, 10, "weak"),
+    # name: (generator, cell, hidden, vocab, batch, scaling). Batches of
+    # several structures are one fixed batch split across the N ranks (strong
+    # scaling): at N > 1 the b10 line is "batch-10 latency
+    # sharded 5/3/2 per rank", the b4096 lines the trees/s headline. A single
+    # structure is not split: b1 / cfg1 run as replicas (weak).
+    "cfg2_treelstm_b10": ("sst", synth.TREELSTM, 256, 20000, 10, "strong"),
     "cfg2_treelstm_b1": ("sst", synth.TREELSTM, 256, 20000, 1, "weak"),
-    "cfg3_treegru_b10": ("sst", synth.TREEGRU, 512, 20000, 10, "weak"),
+    "cfg3_treegru_b10": ("sst", synth.TREEGRU, 512, 20000, 10, "strong"),
     "cfg3_treegru_b1": ("sst", synth.TREEGRU, 512, 20000, 1, "weak"),
-    "cfg3_treefc_b10": ("perfect7", synth.TREEFC, 512, 20000, 10, "weak"),
+    "cfg3_treefc_b10": ("perfect7", synth.TREEFC, 512, 20000, 10, "strong"),
     "cfg3_treefc_b1": ("perfect7", synth.TREEFC, 512, 20000, 1, "weak"),
-    "cfg4_mvrnn_b10": ("sst", synth.MVRNN, 64, 20000, 10, "weak"),
-    "cfg5_dagrnn_b10": ("grid", synth.DAGRNN, 256, 20000, 10, "weak"),
+    "cfg4_mvrnn_b10": ("sst", synth.MVRNN, 64, 20000, 10, "strong"),
+    "cfg5_dagrnn_b10": ("grid", synth.DAGRNN, 256, 20000, 10, "strong"),
     "cfg5_dagrnn_b1": ("grid", synth.DAGRNN, 256, 20000, 1, "weak"),
     "cfg1_treernn": ("perfect3", synth.TREERNN, 8, 100, 1, "weak"),
     # SimpleTreeGRU (footnote P:1638-1640) at the TreeGRU config
-    "f3_simpletreegru_b10": ("sst", synth.SIMPLETREEGRU, 512, 20000, 10, "weak"),
+    "f3_simpletreegru_b10": ("sst", synth.SIMPLETREEGRU, 512, 20000, 10, "strong"),
     "f3_simpletreegru_b1": ("sst", synth.SIMPLETREEGRU, 512, 20000, 1, "weak"),
     # GRNN-comparison sequences (length 100, H = 256)
-    "f4_lstm_seq100_b10": ("chain100", synth.TREELSTM, 256, 20000, 10, "weak"),
+    "f4_lstm_seq100_b10": ("chain100", synth.TREELSTM, 256, 20000, 10, "strong"),
     "f4_lstm_seq100_b1": ("chain100", synth.TREELSTM, 256, 20000, 1, "weak"),
-    "f4_gru_seq100_b10": ("chain100", synth.TREEGRU, 256, 20000, 10, "weak"),
+    "f4_gru_seq100_b10": ("chain100", synth.TREEGRU, 256, 20000, 10, "strong"),
     "f4_gru_seq100_b1": ("chain100", synth.TREEGRU, 256, 20000, 1, "weak"),
     # strong scaling: the batch is split across ranks
     "cfg5_treelstm_b4096": ("sst", synth.TREELSTM, 256, 20000, 4096, "strong"),
