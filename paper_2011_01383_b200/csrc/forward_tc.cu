@@ -1,47 +1,51 @@
-// forward_tc.cu -- the bf16 tensor-core forward (cx_model.dtype == CX_BF16):
-// one persistent cooperative kernel per batch that walks the levels of the
-// linearization (Listing 2; one barrier per batch, App. A.4
-// P:2010-2040) and runs every level's contraction as a dense GEMM on the
-// 5th-generation tensor cores (tcgen05.mma, bf16 operands, fp32 accumulators
-// in tensor memory), with the gates fused into the epilogue and
-// the recurrent weights resident in shared memory for the whole batch (model
-// persistence).
+// forward_tc.cu -- the tensor-core forward: one persistent kernel per batch
+// that walks the levels of the linearization (Listing 2; one
+// barrier per batch, App. A.4) and runs each level's contraction as
+// a dense GEMM on the 5th-generation tensor cores (tcgen05.mma, fp32
+// accumulators in tensor memory), with the gates fused into the epilogue
+// and the recurrent weights resident in shared memory for the
+// whole batch (model persistence). Two operand precisions (TcCfg
+// SP): bf16 (dtype CX_BF16) and split fp32 (dtype CX_F32, large batches: every
+// operand as bf16 hi + lo, three bf16 MMAs per product).
 //
 // Work split. CTA (gn, gu) owns hidden units [gu*U, gu*U + U) of every gate
 // and the contiguous chunk gn of each level's nodes, walked in tiles of 128
 // nodes (the UMMA M dimension; rows are nodes, so a partial tile's unused rows
 // never influence the valid ones). A tile's GEMM is
-//     D[128 x N] (+)= A_slot[128 x H] * B_slot[N x H]^T      for each slot,
-// where a slot is one gathered operand: the bf16 state rows of the tile's k-th
-// children (zero rows for absent children) or the bf16 input rows x = Emb[word].
-// The child sums of child-sum cells use linearity (U h~ = sum_k U h_k), so no
-// operand is summed before the MMA.
+//     D[128 x N] (+)= A_slot[128 x K] * B_slot[N x K]^T      for each slot,
+// where a slot is one operand row set: the tile's k-th children's state rows
+// (zero rows for absent children) or the input rows x = Emb[word]. The child
+// sums of child-sum cells use linearity (U h~ = sum_k U h_k).
 //   TreeLSTM  leaf:  slot x, B = W_iou slice (i,o,u rows)      -> [i o u]
 //             level: slot child k, B = [U_iou; U_f] slice     -> acc k = [i o u f]_k;
 //                    epilogue: iou = sum_k acc_k, f_k from acc_k (Q1)
-//   DAG-RNN   every level: slot x (B = W_x slice) + child slots (B = U slice), all
-//                    into one accumulator; h = tanh(acc + b)             (Q8)
+//   DAG-RNN   level: slot x (B = W_x slice) + child slots (B = U slice) into one
+//                    accumulator, h = tanh(acc + b) (Q8); split fp32 in table
+//                    mode: W_x x + b once per word (phase l = -1), levels
+//                    contract the children only and add the word's row
 //   TreeFC    leaf:  h = Emb[word] (copy, no GEMM)
 //             level: slot left (B = W[:, :H] slice) + slot right (B = W[:, H:]) (Q2)
+// Small levels (a few nodes per node group) skip the tiles and run on the
+// epilogue warps' FMA pipes against the same resident B (fma_level, §6.2j).
 //
-// Warp roles (416 threads): warps 0-3 epilogue (warp w owns TMEM lanes
-// 32w..32w+31 = tile rows), warp 4 MMA issuer (one lane; also allocates TMEM),
-// warps 5-12 producers. Producers gather one K-atom (64 bf16 = 128 bytes of
-// each of the tile's 128 rows) of one slot per pipeline stage with 16-byte
-// cp.async into the K-major 128B-swizzled layout (umma.cuh), fence the
-// generic->async proxy and arrive on the stage's "full" mbarrier; the MMA
-// lane waits, issues 4 MMAs (K = 16 each) and frees the stage with
-// tcgen05.commit. Accumulators are double-buffered in TMEM so the epilogue of
-// tile t overlaps the MMAs of tile t+1. A 4-deep ring of tile bookkeeping
-// (node ids, children, rows of x, roots) in shared memory is filled by the
-// producers and released by the epilogue.
+// Warp roles: warps 0-7 epilogue (warp w reads TMEM lane quadrant w % 4 = tile
+// rows, column half w / 4), warp 8 MMA issuer (one lane; also allocates TMEM),
+// then the operand feed, then 2 bookkeeping warps that fill a 4-deep ring of
+// tile metadata (node ids, children, x rows, roots, parent slots) and run ahead
+// of the level barriers. Feed: TreeLSTM / TreeFC (trees) store each node's h
+// in its parent's child-slot row, so a tile's operands are contiguous rows
+// loaded by one lane with 3D TMA boxes of NAB K-atoms; DAG-RNN gathers rows
+// with 16-byte cp.async by 4 warps. The MMA lane waits a stage's "full"
+// mbarrier, issues the stage's MMAs (K = 16 each) and frees it with
+// tcgen05.commit; accumulators are double-buffered in TMEM so the epilogue of
+// tile t overlaps the MMAs of tile t+1.
 //
-// State (workspace, linearized numbering): hb [n][H] bf16 (the MMA operand
-// for parents), cs [n][H] fp32 (TreeLSTM memory cells), xb bf16 input rows:
-// either the whole embedding table converted once per call (indexed by word;
-// used when the batch has more x rows than half the vocabulary) or the batch's
-// own x rows in node order. h_out / aux_out / root_out are written by the
-// epilogue in the caller's numbering.
+// State (workspace, linearized numbering): hb state rows (DAG-RNN; hoisted
+// TreeLSTM word rows), pb parent-slot rows (TreeLSTM, TreeFC), cs fp32 TreeLSTM
+// memory cells, xb input rows (the embedding table converted once per call,
+// or the batch's rows in node order), hf fp32 word table (hoisting); operand
+// rows hold SP x H bf16 ([hi | lo] when split). h_out / aux_out / root_out are
+// written by the epilogue in the caller's numbering.
 #include <cuda_bf16.h>
 #include <cuda.h>  // CUtensorMap types (the encoder is fetched from the driver at run time)
 #include <cuda_runtime.h>
