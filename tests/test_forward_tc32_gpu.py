@@ -152,3 +152,30 @@ def test_batch4096_sampled(cx, name, monkeypatch):
     e = normwise_rel_err(h.cpu().numpy(), rh, rows=rows)
     assert e <= TOL_F32, e
     assert np.array_equal(roots.cpu().numpy()[picks], h.cpu().numpy()[targets])
+
+
+def test_errors(cx, forced):
+    """Latched data errors on the split-fp32 kernel: the lowest (code, node)
+    wins, as on every other path (word range in table mode -- hoisted leaves /
+    hoisted DAG projection -- and in node-order mode; TreeFC arity)."""
+    H, V = 128, 5
+    emb = np.ones((50, H), np.float32)
+    ch = np.array([[1, -1, -1], [2, -1, -1]], np.int32)
+    for Vx in (V, 50):
+        lin, _, _, _ = _run(cx, T.TREELSTM, H, Vx, ch, T.TREE, np.array([-1, 70, 0]), emb[:Vx])
+        assert cx.status(lin) == (7, 1)
+        lin, _, _, _ = _run(cx, T.DAGRNN, H, Vx, ch, T.DAG, np.array([90, 0, 0]), emb[:Vx])
+        assert cx.status(lin) == (7, 0)
+    ch = np.array([[1, 2, -1], [-1, -1, -1]], np.int32)
+    lin, _, _, _ = _run(cx, T.TREEFC, 256, V, ch, T.TREE, np.array([-1, -1, 0]),
+                        np.ones((V, 256), np.float32))
+    assert cx.status(lin) == (6, 0)
+
+
+def test_single_nodes(cx, forced):
+    """One-node structures only: every node is a leaf and a root (no level
+    beyond 0; hoisted tables in table mode)."""
+    ch = np.full((2, 300), -1, np.int32)
+    _parity(cx, T.TREELSTM, 128, 50, ch, T.TREE, seed=1)
+    _parity(cx, T.DAGRNN, 128, 50, ch, T.DAG, seed=1)
+    _parity(cx, T.TREEFC, 256, 50, ch, T.TREE, seed=1)
