@@ -15,6 +15,7 @@ import paper_2011_01383_b200 as cx  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2_treelstm_b10"
 fused = len(sys.argv) > 2 and sys.argv[2] == "fused"  # cx_linearize_forward (slot 20 = lin done)
+DT = cx.BF16 if len(sys.argv) > 3 and sys.argv[3] == "bf16" else cx.F32  # bf16: rounded-operand FMA
 inp = bench.make_inputs(name, 0, 1)
 dev = torch.device("cuda", 0)
 t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a, dtype=dt)).to(dev)
@@ -36,13 +37,13 @@ def run_once():
     L.cx_debug_set_trace(ctypes.c_void_p(buf.data_ptr()), S)
     if fused:
         lin = cx.linearize_forward(children, inp["kind"], cell, H, weights, emb, words, out=lin,
-                                   h_out=h)[0]
+                                   h_out=h, dtype=DT)[0]
     else:
         L.cx_debug_set_lin_trace.argtypes = [ctypes.c_void_p]
         L.cx_debug_set_lin_trace(ctypes.c_void_p(lbuf.data_ptr()))
         cx.linearize(children, inp["kind"], out=lin)
         L.cx_debug_set_lin_trace(None)
-        cx.forward(cell, H, weights, emb, words, lin, h_out=h)
+        cx.forward(cell, H, weights, emb, words, lin, h_out=h, dtype=DT)
     L.cx_debug_set_trace(None, 0)
 
 
