@@ -79,6 +79,9 @@ using namespace umma;
 #ifndef CX_TC_TMA_LANES  // lanes of the TMA warp issuing stages side by side (measured: 2 or 3
 #define CX_TC_TMA_LANES 1    // lanes slowed the split-fp32 TreeLSTM / TreeFC by 3-7 %, bf16 +-0)
 #endif
+#ifndef CX_TC_L2PF  // stages ahead whose operand tile the TMA lane prefetches into L2
+#define CX_TC_L2PF 0  // (0: none; 4 or 8 measured within +-0.5 %: the operands are L2-resident)
+#endif
 #ifndef CX_TC_NAB  // K-atoms per TreeLSTM TMA stage (one 3D box)
 #define CX_TC_NAB 2
 #endif
@@ -1106,6 +1109,17 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
               tma_tile2d(dst, tm, &bar_full[st], ka * 64, row0);
             else
               tma_tile2d_mc(dst, tm, &bar_full[st], ka * 64, row0, (uint16_t)1);
+            if (CX_TC_L2PF > 0 && q + CX_TC_L2PF < total) {  // warm L2 for a later stage
+              const int qp = q + CX_TC_L2PF;
+              const int sp = qp % nsl, kp = ((qp / nsl) % nka) * C::NAB, tp = qp / (nsl * nka);
+              int srcp, bmp, accp;
+              slot_of(l, sp, srcp, bmp, accp);
+              const int i0p = lo + tp * kTM;
+              const int rowp = srcp >= 0 ? srcp * n + i0p : (hoist ? i0p : i0p - xlo);
+              const void *tmp = srcp >= 0 ? (const void *)&ta.tm_p : (const void *)&ta.tm_x;
+              if (C::NAB > 1) tma_prefetch3d(tmp, 0, rowp, kp);
+              else tma_prefetch2d(tmp, kp * 64, rowp);
+            }
             tc_mark(a, sslot + 1, kFeed0 * 32);
           }
           __syncwarp();

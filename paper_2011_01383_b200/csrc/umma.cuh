@@ -202,6 +202,15 @@ __device__ __forceinline__ void tma_tile2d(uint32_t dst, const void *tmap, uint6
       ::"r"(dst), "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// L2 prefetch of a 3D / 2D tensor tile (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch3d(const void *tmap, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+               ::"l"(tmap), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch2d(const void *tmap, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
+               ::"l"(tmap), "r"(c0), "r"(c1) : "memory");
+}
 // 3D tensor tile load (coordinates innermost first) into this CTA's shared memory
 __device__ __forceinline__ void tma_tile3d(uint32_t dst, const void *tmap, uint64_t *bar, int c0, int c1,
                                            int c2) {
