@@ -320,13 +320,16 @@ __device__ __forceinline__ float tanh_mufu(float x) {
 __device__ __forceinline__ float sigm_mufu(float x) { return fmaf(0.5f, tanh_mufu(0.5f * x), 0.5f); }
 // per path: the bf16 path's MUFU forms, the split fp32 path's those of the fp32
 // kernels (common.cuh, within ~5e-6 relative)
+#ifndef CX_TC_FASTACT  // timing experiment only: the bf16 MUFU forms on the split path too
+#define CX_TC_FASTACT 0
+#endif
 template <int SP>
 __device__ __forceinline__ float act_sig(float x) {
-  if constexpr (SP == 1) return sigm_mufu(x); else return sigmoidf_(x);
+  if constexpr (SP == 1 || CX_TC_FASTACT) return sigm_mufu(x); else return sigmoidf_(x);
 }
 template <int SP>
 __device__ __forceinline__ float act_tanh(float x) {
-  if constexpr (SP == 1) return tanh_mufu(x); else return tanhf_(x);
+  if constexpr (SP == 1 || CX_TC_FASTACT) return tanh_mufu(x); else return tanhf_(x);
 }
 
 
