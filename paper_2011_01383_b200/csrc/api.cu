@@ -237,10 +237,17 @@ cx_status forward_impl(const cx_model *m, const cx_weights *w, const float *emb,
       a.crow = reinterpret_cast<int *>(q);
       q = align_up(q + 4 * N, 256);
     }
-    if (m->cell == CX_TREELSTM || m->cell == CX_TREEFC) {  // parent-slot operand rows
+    const bool dag2 = m->cell == CX_DAGRNN && plan.tc_sp == 2;
+    if (m->cell == CX_TREELSTM || m->cell == CX_TREEFC || dag2) {  // parent-slot operand rows
       a.pb = reinterpret_cast<unsigned short *>(q);
       q = align_up(q + 2 * (2 * N) * RW, 256);
       a.pslot = reinterpret_cast<int *>(q);
+      q = align_up(q + 4 * N, 256);
+    }
+    if (dag2) {  // split-fp32 DAG-RNN: a second parent's slot row, parent counts
+      a.pslot1 = reinterpret_cast<int *>(q);
+      q = align_up(q + 4 * N, 256);
+      a.pcnt = reinterpret_cast<int *>(q);
     }
   } else if (plan.big) a.pbuf = buf;  // hs, st [n][H] + words [n] (forward_big.cu)
   else switch (m->cell) {

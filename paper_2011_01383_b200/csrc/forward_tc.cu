@@ -82,6 +82,9 @@ using namespace umma;
 #ifndef CX_TC_L2PF  // stages ahead whose operand tile the TMA lane prefetches into L2
 #define CX_TC_L2PF 0  // (0: none; 4 or 8 measured within +-0.5 %: the operands are L2-resident)
 #endif
+#ifndef CX_TC_DSLOT  // split-fp32 DAG-RNN parent-slot operands (in-degree <= 2)
+#define CX_TC_DSLOT 1
+#endif
 #ifndef CX_TC_NAB  // K-atoms per TreeLSTM TMA stage (one 3D box)
 #define CX_TC_NAB 2
 #endif
@@ -118,7 +121,8 @@ struct TcMeta {
   alignas(16) int xr[kTM];     // row of xb (word or node-order row), -1 = none (zeros)
   alignas(16) int root[kTM];   // index in roots[] or -1
   alignas(16) int ch[J][kTM];  // children state rows, -1 absent (zeros)
-  alignas(16) int ps[kTM];     // TreeLSTM: parent-slot row of the node's h, -1 = root
+  alignas(16) int ps[kTM];     // TreeLSTM / TreeFC / DAG slots: parent-slot row of the node's h, -1 = none
+  alignas(16) int ps1[kTM];    // DAG slots: a second parent's slot row, -1 = none
   int i0, cnt;
 };
 
@@ -171,6 +175,10 @@ struct TcCfg {
   // row in its parent's child slot (pb), so a level tile's operands are
   // contiguous rows loaded by TMA; DAG-RNN gathers rows with cp.async
   static constexpr bool SLOTS = LSTM || FC;
+  // split-fp32 DAG-RNN: when no node has more than two parents (decided on the
+  // device, the prologue counts them) each h goes into both parents' slot rows
+  // and the operands load by TMA as for trees; else the cp.async gathers
+  static constexpr bool DSLOT = DAG && SP == 2 && CX_TC_DSLOT;
   static constexpr int FEEDW = SLOTS ? 1 : 4;            // feeding warps
   static constexpr int META0 = kFeed0 + FEEDW;           // first bookkeeping warp
   static constexpr int THREADS = 32 * (META0 + kMetaWarps);
@@ -182,7 +190,7 @@ struct TcCfg {
   // tools/micro/tma_rate.cu measures ~0.36 us per TMA instruction per issuing
   // thread whatever its size (16 KB: 45 GB/s/SM, 32 KB: 87, 64 KB: 137), so
   // the one-lane producer feeds twice as fast with 2-atom boxes
-  static constexpr int NAB = SLOTS && KAA % CX_TC_NAB == 0 ? CX_TC_NAB : 1;
+  static constexpr int NAB = (SLOTS || DSLOT) && KAA % CX_TC_NAB == 0 ? CX_TC_NAB : 1;
   static constexpr int STB = kStageBytes * NAB;  // bytes per stage
   static constexpr int S_fit =
       (int)((kSmemLimit - 1024 - static_bytes - bregion) / STB);
@@ -496,6 +504,15 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
   constexpr int FML = C::FC ? (SP == 2 ? CX_TC_FML_FC : 10) : FMX;
   auto is_fma = [&](int l) { return l >= 1 && !a.tc_fma_off && __ldg(a.lsize + l) <= FML * a.Gn; };
   const int sbase = hoist ? a.V : 0;  // state row of internal node i = sbase + i
+  if (C::DSLOT && status0 == CX_OK) {  // parent counts / slots start empty everywhere
+    const size_t total_threads = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + tid; i < (size_t)n; i += total_threads) {
+      a.pcnt[i] = 0;
+      a.pslot[i] = -1;
+      a.pslot1[i] = -1;
+    }
+    grid_sync(a.bar, gridDim.x, epoch);
+  }
   // ---- phase 0: bf16 input rows ------------------------------------------------
   if (C::XSLOT && status0 == CX_OK) {
     const size_t total_threads = (size_t)gridDim.x * blockDim.x;
@@ -581,6 +598,26 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
     const int R = a.hdr->num_roots;  // roots are nobody's child: no conflict
     for (size_t r = gt; r < (size_t)R; r += total_threads) a.pslot[__ldg(a.roots + r)] = -1;
   }
+  if (C::DSLOT && status0 == CX_OK) {  // up to two parents' slot rows per node
+    const size_t total_threads = (size_t)gridDim.x * blockDim.x;
+    const size_t gt = (size_t)blockIdx.x * blockDim.x + tid;
+    for (size_t pn = gt; pn < (size_t)n; pn += total_threads) {
+#pragma unroll
+      for (int k = 0; k < J; k++) {
+        const int c = __ldg(a.chn + (size_t)k * n + pn);
+        if (c < 0) {  // an absent child's slot row is summed by the MMA: zeros (a
+          // previous call of this shape may have left a child's h in it)
+          uint4 *z = reinterpret_cast<uint4 *>(a.pb + ((size_t)k * n + pn) * RW);
+          for (int q = 0; q < RW / 8; q++) z[q] = make_uint4(0u, 0u, 0u, 0u);
+          continue;
+        }
+        const int idx = atomicAdd(a.pcnt + c, 1);  // which parent gets which slot: either
+        if (idx == 0) a.pslot[c] = k * n + (int)pn;
+        else if (idx == 1) a.pslot1[c] = k * n + (int)pn;
+        else atomicOr(&a.bar->pad[2], 1u);  // a third parent: gather mode
+      }
+    }
+  }
   tc_mark(a, 61, 0);
   fence_proxy_async();  // resident weights (generic stores) -> tensor-core reads
   fence_before();
@@ -588,6 +625,17 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
   grid_sync(a.bar, gridDim.x, epoch);
   fence_after();
   const uint32_t tmem = s_tmem;
+  // DAG parent slots usable: no node has a third parent, and every operand row
+  // set is contiguous (x rows hoisted away or in node order)
+  const bool dslots = C::DSLOT && status0 == CX_OK && (hx || a.xmode == 1) &&
+                      *reinterpret_cast<volatile unsigned *>(&a.bar->pad[2]) == 0u;
+  if (dslots) {  // stages are filled by ONE TMA arrival (+ bytes), not per-thread cp.async arrivals
+    if (tid == 0) {
+      for (int s_ = 0; s_ < S; s_++) mbar_init(&bar_full[s_], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   tc_mark(a, 1, 0);
 
   // Hoisted leaves. slot_fill: each leaf's bf16 h copied from the word table
@@ -708,12 +756,13 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
     constexpr int NSLM = C::LSTM ? J : C::DAG ? J + 1 : 2;
     static_assert(COLS <= kEpiThreads && kEpiThreads % COLS == 0 && (H / KS) % 8 == 0, "FMA split");
     constexpr size_t kAf = (size_t)NSLM * FMX * H, kDp = (size_t)KS * FMX * COLS;
-    static_assert(4 * (kAf + kDp) + 4 * FMX * (8 + 2 * J) <= (size_t)S * C::STB, "FMA level fits the stage ring");
+    static_assert(4 * (kAf + kDp) + 4 * FMX * (9 + 2 * J) <= (size_t)S * C::STB, "FMA level fits the stage ring");
     const int cnt = hi - lo, ntid = tid;  // tid < kEpiThreads
     const int nsl = nsl_of(l);
     float *Af = reinterpret_cast<float *>(sStage), *Dp = Af + kAf;
     int *n_own = reinterpret_cast<int *>(Dp + kDp), *n_root = n_own + FMX, *n_ps = n_root + FMX,
-        *n_xr = n_ps + FMX, *n_ch = n_xr + FMX /* [J][FMX] operand rows */, *n_ck = n_ch + J * FMX;
+        *n_ps1 = n_ps + FMX, *n_xr = n_ps1 + FMX, *n_ch = n_xr + FMX /* [J][FMX] operand rows */,
+        *n_ck = n_ch + J * FMX;
     if (ntid < cnt) {  // 1. node info (as the bookkeeping warps compute it)
       const int i = lo + ntid, own = __ldg(a.perm + i);
       n_own[ntid] = own;
@@ -723,7 +772,8 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         root = __ldg(a.roots + sv) == i ? sv : -1;
       }
       n_root[ntid] = root;
-      n_ps[ntid] = C::SLOTS ? __ldcg(a.pslot + i) : -1;
+      n_ps[ntid] = (C::SLOTS || dslots) ? __ldcg(a.pslot + i) : -1;
+      n_ps1[ntid] = dslots ? __ldcg(a.pslot1 + i) : -1;
       int xr = -1;
       if (C::DAG) {
         if (a.xmode == 0) {
@@ -749,7 +799,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         const int srow = c >= 0 ? (hoist ? __ldcg(a.crow + c) : c) : -1;  // the child's state row
         n_ck[k * FMX + ntid] = srow;
         // operand row of slot k: TreeLSTM the parent-slot row, else the state row
-        n_ch[k * FMX + ntid] = C::SLOTS ? (c >= 0 ? k * n + i : -1) : srow;
+        n_ch[k * FMX + ntid] = (C::SLOTS || dslots) ? (c >= 0 ? k * n + i : -1) : srow;
       }
       if (C::FC && nc != 2 && latch) latch_error(a.hdr, CX_E_ARITY, own);
     }
@@ -761,7 +811,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
       int src, bm, acc;
       slot_of(l, sl, src, bm, acc);
       const int row = src < 0 ? n_xr[t] : n_ch[src * FMX + t];
-      const unsigned short *base = src < 0 ? xb : (C::SLOTS ? a.pb : hb);
+      const unsigned short *base = src < 0 ? xb : ((C::SLOTS || dslots) ? a.pb : hb);
       float f[8];
       if (row >= 0) {
         const uint4 hv = __ldcg(reinterpret_cast<const uint4 *>(base + (size_t)row * RW + 8 * q));
@@ -887,13 +937,19 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
         if (hx) v += __ldcg(a.hf + (size_t)n_xr[t] * H + uu);
         else v += s_bias[u];
         h = act_tanh<SP>(v);
-        // the operand row: TreeFC the parent's child slot (none for a root), DAG-RNN the state row
-        unsigned short *hrow = C::SLOTS ? (n_ps[t] >= 0 ? a.pb + (size_t)n_ps[t] * RW : nullptr)
-                                        : hb + (size_t)i * RW;
-        if (hrow) {
-          const float hi_ = bf16_round(h);
-          hrow[uu] = (unsigned short)(__float_as_uint(hi_) >> 16);
-          if (SP == 2) hrow[H + uu] = (unsigned short)(__float_as_uint(bf16_round(h - hi_)) >> 16);
+        // the operand rows: TreeFC / DAG slots the parents' child slots (none for a
+        // root), else the DAG-RNN state row
+        const float hi_ = bf16_round(h);
+        const unsigned short hb16 = (unsigned short)(__float_as_uint(hi_) >> 16);
+        const unsigned short lb16 = (unsigned short)(__float_as_uint(bf16_round(h - hi_)) >> 16);
+        for (int pp = 0; pp < 2; pp++) {
+          const int prow = pp == 0 ? n_ps[t] : n_ps1[t];
+          unsigned short *hrow = (C::SLOTS || dslots) ? (prow >= 0 ? a.pb + (size_t)prow * RW : nullptr)
+                                                      : (pp == 0 ? hb + (size_t)i * RW : nullptr);
+          if (hrow) {
+            hrow[uu] = hb16;
+            if (SP == 2) hrow[H + uu] = lb16;
+          }
         }
       }
       a.h_out[(size_t)own * H + uu] = h;
@@ -942,18 +998,20 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
               }
         }
         constexpr int RQ = kTM / 32;
-        int own[RQ], sv[RQ], psv[RQ], ch[RQ][J];
+        int own[RQ], sv[RQ], psv[RQ], ps1v[RQ], ch[RQ][J];
 #pragma unroll
         for (int q = 0; q < RQ; q++) {  // round 1: perm, structure, children
           const int r = lane + 32 * q, i = i0 + r;
           own[q] = -1;
           sv[q] = -1;
           psv[q] = -1;
+          ps1v[q] = -1;
 #pragma unroll
           for (int k = 0; k < J; k++) ch[q][k] = -1;
           if (r < cnt && !(leaf && hoist) && !proj) {
             own[q] = __ldg(a.perm + i);
-            if (C::SLOTS) psv[q] = __ldcg(a.pslot + i);
+            if (C::SLOTS || dslots) psv[q] = __ldcg(a.pslot + i);
+            if (dslots) ps1v[q] = __ldcg(a.pslot1 + i);
             if (a.root_out) sv[q] = __ldg(a.sid + i);
             if (!leaf) {
 #pragma unroll
@@ -998,6 +1056,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
           m.xr[r] = xr;
           m.root[r] = root;
           m.ps[r] = psv[q];
+          m.ps1[r] = ps1v[q];
 #pragma unroll
           for (int k = 0; k < J; k++) m.ch[k][r] = ch[q][k];
         }
@@ -1077,7 +1136,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
       const int nsl = nsl_of(l);
       if (fma_l && warp < kEpiWarps) fma_level(l, lo, hi);
 
-      if (C::SLOTS && warp == kFeed0) {
+      if ((C::SLOTS || dslots) && warp == kFeed0) {
         // ========================= TMA tile loads ================================
         // per stage: NAB K-atoms (64 bf16 each) of one slot for the tile's 128
         // rows with one tile load: TreeLSTM / TreeFC operands are contiguous
@@ -1128,7 +1187,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
           __syncwarp();
         }
         tc_mark(a, l >= 0 ? 3 + 4 * l : -1, kFeed0 * 32);
-      } else if (!C::SLOTS && warp >= kFeed0 && warp < kMeta0) {
+      } else if (!C::SLOTS && !dslots && warp >= kFeed0 && warp < kMeta0) {
         // ========================= cp.async gathers ==============================
         // per stage: one K-atom of one slot for the tile's 128 rows, 16-byte
         // cp.async into the swizzled layout (zero-fill: absent child, unused
@@ -1141,7 +1200,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
           const int ms = TT % kMetaRing;
           mbar_wait(&bar_mfull[ms], (TT / kMetaRing) & 1);
           const TcMeta<J> &m = meta[ms];
-          for (int ka = 0; ka < KAA; ka++) {
+          for (int ka = 0; ka < KAA; ka += C::NAB) {
             for (int s = 0; s < nsl; s++) {
               int src, bm, acc;
               slot_of(l, s, src, bm, acc);
@@ -1151,13 +1210,15 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
               const int *rows = src < 0 ? m.xr : m.ch[src];
               const unsigned short *base = src < 0 ? xb : hb;
 #pragma unroll
-              for (int e = 0; e < kChunks; e++) {
-                const int q = p + FT * e, r = q >> 3, c = q & 7;
-                const int row = rows[r];
-                const bool valid = row >= 0;
-                cp16_zfill(dst0 + sw128_off(r, c), base + (size_t)(valid ? row : 0) * RW + ka * 64 + c * 8,
-                           valid);
-              }
+              for (int aj = 0; aj < C::NAB; aj++)  // the stage's K-atoms, atom after atom
+#pragma unroll
+                for (int e = 0; e < kChunks; e++) {
+                  const int q = p + FT * e, r = q >> 3, c = q & 7;
+                  const int row = rows[r];
+                  const bool valid = row >= 0;
+                  cp16_zfill(dst0 + aj * kStageBytes + sw128_off(r, c),
+                             base + (size_t)(valid ? row : 0) * RW + (ka + aj) * 64 + c * 8, valid);
+                }
               mbar_arrive_cpasync(&bar_full[st]);
               Sg++;
             }
@@ -1223,7 +1284,7 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
           tc_mark(a, l >= 0 ? 4 + 4 * l : -1, kMmaWarp * 32);
         }
         __syncwarp();
-      } else {
+      } else if (warp < kEpiWarps) {  // (idle feed warps of a DAG slot run skip all roles)
         // =========================== epilogue ====================================
         // thread = tile row r (TMEM lane) x column half hh: units [u0, u0 + U/2)
         constexpr int UC = U / 2;
@@ -1378,8 +1439,9 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
               if (valid) {
                 const int uu = unit0 + u0 + q * CW;
                 st_row_cs<CW>(a.h_out + (size_t)own * H + uu, v);
-                if constexpr (C::SLOTS) {  // TreeFC: the parent's child-slot row
+                if (C::SLOTS || dslots) {  // TreeFC / DAG slots: the parents' child-slot rows
                   if (m.ps[r] >= 0) st_op<SP, H, CW>(a.pb + (size_t)m.ps[r] * RW, uu, v);
+                  if (dslots && m.ps1[r] >= 0) st_op<SP, H, CW>(a.pb + (size_t)m.ps1[r] * RW, uu, v);
                 } else {
                   st_op<SP, H, CW>(hb + (size_t)i * RW, uu, v);
                 }
@@ -1636,7 +1698,9 @@ size_t tc_workspace_bytes(int cell, int H, int V, int n, int sp) {
   if (cell == CX_TREELSTM || cell == CX_DAGRNN)                 // xb
     b += 2 * (tc_xmode(n, V) ? N : (size_t)V) * rw + 256;
   if (tc_hoist(cell, n, V, sp)) b += 4 * (size_t)V * h + 4 * N + 512;  // hf, crow
-  if (cell == CX_TREELSTM || cell == CX_TREEFC) b += 2 * (2 * N) * rw + 4 * N + 512;  // pb (J <= 2), pslot
+  if (cell == CX_TREELSTM || cell == CX_TREEFC || (cell == CX_DAGRNN && sp == 2))
+    b += 2 * (2 * N) * rw + 4 * N + 512;                                     // pb (J <= 2), pslot
+  if (cell == CX_DAGRNN && sp == 2) b += 8 * N + 512;                           // pslot1, pcnt
   return b;
 }
 

@@ -161,6 +161,7 @@ __device__ __forceinline__ void publish_and_exit(const FwdArgs &a) {
       }
       a.bar->count = 0;
       a.bar->exit = 0;
+      a.bar->pad[2] = 0;  // the tensor-core kernel's DAG in-degree overflow flag
       __threadfence();
     }
   }
@@ -190,6 +191,7 @@ __device__ __forceinline__ void fused_exit(const FwdArgs &a, unsigned long long 
       }
       a.bar->count = 0;
       a.bar->exit = 0;
+      a.bar->pad[2] = 0;  // the tensor-core kernel's DAG in-degree overflow flag
       __threadfence();
     }
   }

@@ -39,6 +39,8 @@ struct FwdArgs {
   unsigned short *pb;  // TreeLSTM: [J*n][H] bf16 h of node i stored in its parent's child
                        // slot row k*n + parent (a level tile's k-th children are contiguous)
   int *pslot;          // [n] that row for every non-root node
+  int *pslot1;         // [n] split-fp32 DAG-RNN: a second parent's slot row (-1: none)
+  int *pcnt;           // [n] split-fp32 DAG-RNN: parents counted in the prologue
   GridBar *bar;
   int Gn, Gu;   // node groups x unit groups = CTAs
   unsigned long long *trace;  // debug: %globaltimer per CTA and phase (cx_debug_set_trace)

@@ -179,3 +179,21 @@ def test_single_nodes(cx, forced):
     _parity(cx, T.TREELSTM, 128, 50, ch, T.TREE, seed=1)
     _parity(cx, T.DAGRNN, 128, 50, ch, T.DAG, seed=1)
     _parity(cx, T.TREEFC, 256, 50, ch, T.TREE, seed=1)
+
+
+def test_dag_slots_reused_workspace(cx, forced):
+    """DAG-RNN on parent-slot operands: a second call of the same shape whose
+    DAG has fewer edges reuses the workspace (no re-zeroing for an unchanged
+    shape); the slot rows of now-absent children must read as zeros. Also a
+    DAG with a third parent for some node (the cp.async gather fallback)."""
+    ch, _ = synth.grid_dags(40, 9, 11)
+    _parity(cx, T.DAGRNN, 128, 97, ch, T.DAG, seed=4)
+    ch2 = ch.copy()
+    rng = np.random.default_rng(5)
+    two = np.where(ch2[1] >= 0)[0]
+    ch2[1, rng.choice(two, len(two) // 3, replace=False)] = -1  # drop some second children
+    _parity(cx, T.DAGRNN, 128, 97, ch2, T.DAG, seed=4)
+    ch3 = ch.copy()
+    ch3[1, 50] = ch3[0, 1]  # ... gives node ch[0, 1] extra parents (in-degree 3)
+    if ch3[1, 50] != ch3[0, 50] and ch3[1, 50] >= 0 and ch[0, 50] >= 0:
+        _parity(cx, T.DAGRNN, 128, 97, ch3, T.DAG, seed=4)
