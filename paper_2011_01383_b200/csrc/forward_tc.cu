@@ -501,7 +501,8 @@ __global__ void __launch_bounds__(TcCfg<CELL, H, MAXC, SP>::THREADS, 1)
   // which a level runs on FMA, in batches (TreeFC's 2H-deep contraction of
   // split operands costs the tile path ~17 us per level: more levels qualify)
   constexpr int FMX = C::LSTM ? 4 : C::FC ? 10 : 6;
-  constexpr int FML = C::FC ? (SP == 2 ? CX_TC_FML_FC : 10) : FMX;
+  // (bf16 TreeLSTM: its 8-stage tiles beat the FMA path, measured ~1 %: tiles only)
+  constexpr int FML = C::FC ? (SP == 2 ? CX_TC_FML_FC : 10) : (C::LSTM && SP == 1) ? 0 : FMX;
   auto is_fma = [&](int l) { return l >= 1 && !a.tc_fma_off && __ldg(a.lsize + l) <= FML * a.Gn; };
   const int sbase = hoist ? a.V : 0;  // state row of internal node i = sbase + i
   if (C::DSLOT && status0 == CX_OK) {  // parent counts / slots start empty everywhere
